@@ -1,0 +1,805 @@
+// api.cu — host side of libtac: the C ABI of include/tac.h.
+//
+// tac_create: validation, fp64 precompute of the rest shape (Dm^-1 rows, volumes,
+// lumped masses), gel surface extraction, indenter BVHs (body frame,
+// static, shared by all envs), fp64 marker location, device allocation in the
+// env-fastest layout of internal.h.  tac_step: the launch sequence of SURVEY §3.3
+// (rows a1-a9) on the caller's stream, no host synchronisation in fixed-iteration mode.
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../include/tac.h"
+#include "internal.h"
+
+using namespace tac;
+
+struct tac_sim {
+  Dev d;
+  int device;
+  std::vector<void*> allocs;
+  std::string err;
+  bool sticky = false;
+  long long launches = 0;
+  int max_iters, fixed_iters, check_every;
+  // host copies for debug hooks
+  std::vector<int> sv, st_flat, se_flat, ie_flat;
+  std::vector<int> mk_tet, mk_idx;
+  std::vector<double> mk_w;
+  int* d_flag = nullptr;
+  int* h_flag = nullptr;
+  unsigned long long* d_dbg_cand = nullptr;
+  int* d_dbg_cnt = nullptr;
+  float* d_scratch = nullptr;  // [nv][3] host<->device staging
+  tac::Profiler* prof = nullptr;
+};
+
+static thread_local std::string g_create_err;
+
+namespace tac {
+// per-kernel CUDA-event timing of the launches issued by tac_step / tac_markers
+struct Profiler {
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[KID_COUNT];
+  cudaEvent_t cur[KID_COUNT] = {};
+  double ms[KID_COUNT] = {};
+  long long cnt[KID_COUNT] = {};
+  cudaEvent_t get() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  void drain() {
+    for (int k = 0; k < KID_COUNT; ++k) {
+      for (auto& pr : pending[k]) {
+        float t = 0.f;
+        cudaEventSynchronize(pr.second);
+        cudaEventElapsedTime(&t, pr.first, pr.second);
+        ms[k] += t;
+        cnt[k] += 1;
+        pool.push_back(pr.first);
+        pool.push_back(pr.second);
+      }
+      pending[k].clear();
+    }
+  }
+  ~Profiler() {
+    drain();
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+void prof_begin(int kid, cudaStream_t s) {
+  cudaEvent_t e = g_prof->get();
+  cudaEventRecord(e, s);
+  g_prof->cur[kid] = e;
+}
+void prof_end(int kid, cudaStream_t s) {
+  cudaEvent_t e = g_prof->get();
+  cudaEventRecord(e, s);
+  g_prof->pending[kid].push_back({g_prof->cur[kid], e});
+}
+}  // namespace tac
+
+namespace {
+
+#define CK(x)                                                                   \
+  do {                                                                          \
+    cudaError_t e_ = (x);                                                       \
+    if (e_ != cudaSuccess) {                                                    \
+      sim->err = std::string(#x) + ": " + cudaGetErrorString(e_);               \
+      sim->sticky = true;                                                       \
+      return TAC_ECUDA;                                                         \
+    }                                                                           \
+  } while (0)
+
+template <typename T>
+tac_status upload(tac_sim* sim, const std::vector<T>& h, T** out) {
+  size_t n = std::max<size_t>(1, h.size()) * sizeof(T);
+  void* p = nullptr;
+  if (cudaMalloc(&p, n) != cudaSuccess) { sim->err = "cudaMalloc failed"; return TAC_ENOMEM; }
+  sim->allocs.push_back(p);
+  if (!h.empty()) CK(cudaMemcpy(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+  *out = (T*)p;
+  return TAC_OK;
+}
+template <typename T>
+tac_status zalloc(tac_sim* sim, size_t n, T** out) {
+  void* p = nullptr;
+  if (cudaMalloc(&p, std::max<size_t>(1, n) * sizeof(T)) != cudaSuccess) {
+    sim->err = "cudaMalloc failed (" + std::to_string(n * sizeof(T)) + " bytes)";
+    return TAC_ENOMEM;
+  }
+  sim->allocs.push_back(p);
+  CK(cudaMemset(p, 0, std::max<size_t>(1, n) * sizeof(T)));
+  *out = (T*)p;
+  return TAC_OK;
+}
+
+typedef std::array<double, 3> V;
+V sub(const V& a, const V& b) { return {a[0] - b[0], a[1] - b[1], a[2] - b[2]}; }
+double det(const V& a, const V& b, const V& c) {  // det [a b c] (columns)
+  return a[0] * (b[1] * c[2] - b[2] * c[1]) - b[0] * (a[1] * c[2] - a[2] * c[1]) + c[0] * (a[1] * b[2] - a[2] * b[1]);
+}
+
+// ---- BVH over indenter primitives (body frame), median split on the longest centroid axis ----
+struct Build {
+  std::vector<BNode>* nodes;
+  std::vector<int>* prims;
+  const std::vector<std::array<float, 6>>* box;  // prim boxes (lo, hi)
+};
+int build_node(Build& B, std::vector<int>& ids, int lo, int hi) {
+  BNode n;
+  for (int a = 0; a < 3; ++a) { n.lo[a] = INFINITY; n.hi[a] = -INFINITY; }
+  float clo[3] = {INFINITY, INFINITY, INFINITY}, chi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int i = lo; i < hi; ++i) {
+    const auto& b = (*B.box)[ids[i]];
+    for (int a = 0; a < 3; ++a) {
+      n.lo[a] = std::min(n.lo[a], b[a]);
+      n.hi[a] = std::max(n.hi[a], b[3 + a]);
+      float c = 0.5f * (b[a] + b[3 + a]);
+      clo[a] = std::min(clo[a], c);
+      chi[a] = std::max(chi[a], c);
+    }
+  }
+  int idx = (int)B.nodes->size();
+  B.nodes->push_back(n);
+  if (hi - lo <= kNodeLeaf) {
+    (*B.nodes)[idx].left = -(int)B.prims->size() - 1;
+    (*B.nodes)[idx].right = hi - lo;
+    for (int i = lo; i < hi; ++i) B.prims->push_back(ids[i]);
+    return idx;
+  }
+  int ax = 0;
+  for (int a = 1; a < 3; ++a)
+    if (chi[a] - clo[a] > chi[ax] - clo[ax]) ax = a;
+  int mid = (lo + hi) / 2;
+  std::nth_element(ids.begin() + lo, ids.begin() + mid, ids.begin() + hi, [&](int x, int y) {
+    const auto& bx = (*B.box)[x];
+    const auto& by = (*B.box)[y];
+    float cx = bx[ax] + bx[3 + ax], cy = by[ax] + by[3 + ax];
+    return cx < cy || (cx == cy && x < y);
+  });
+  int l = build_node(B, ids, lo, mid);
+  int r = build_node(B, ids, mid, hi);
+  (*B.nodes)[idx].left = l;
+  (*B.nodes)[idx].right = r;
+  return idx;
+}
+int build_bvh(std::vector<BNode>& nodes, std::vector<int>& prims, const std::vector<std::array<float, 6>>& box) {
+  std::vector<int> ids(box.size());
+  std::iota(ids.begin(), ids.end(), 0);
+  Build B{&nodes, &prims, &box};
+  if (ids.empty()) {  // empty tree: a node that never hits
+    BNode n;
+    for (int a = 0; a < 3; ++a) { n.lo[a] = INFINITY; n.hi[a] = -INFINITY; }
+    n.left = -(int)prims.size() - 1;
+    n.right = 0;
+    nodes.push_back(n);
+    return (int)nodes.size() - 1;
+  }
+  return build_node(B, ids, 0, (int)ids.size());
+}
+
+float down(double x) { float f = (float)x; return (double)f > x ? std::nextafter(f, -INFINITY) : f; }
+float up(double x) { float f = (float)x; return (double)f < x ? std::nextafter(f, INFINITY) : f; }
+
+}  // namespace
+
+extern "C" {
+
+const char* tac_last_error(const tac_sim* sim) { return sim ? sim->err.c_str() : g_create_err.c_str(); }
+
+tac_status tac_create(const tac_create_info* info, tac_sim** out) {
+  if (!out) return TAC_EINVAL;
+  *out = nullptr;
+  g_create_err.clear();
+  auto fail = [&](tac_status st, const std::string& m) { g_create_err = m; return st; };
+  if (!info || !info->gel || !info->mat || !info->markers || !info->indenter || !info->params || !info->init_poses)
+    return fail(TAC_EINVAL, "null pointer in tac_create_info");
+  const tac_tet_mesh& G = *info->gel;
+  const tac_tri_mesh& I = *info->indenter;
+  const tac_marker_set& MS = *info->markers;
+  const tac_solver_params& P = *info->params;
+  const tac_material& MT = *info->mat;
+  if (G.n_verts < 4 || G.n_tets < 1 || !G.rest_xyz || !G.tets || G.n_fixed < 0 || (G.n_fixed > 0 && !G.fixed))
+    return fail(TAC_EINVAL, "invalid gel mesh");
+  if (I.n_verts < 3 || I.n_tris < 1 || !I.rest_xyz || !I.tris) return fail(TAC_EINVAL, "invalid indenter mesh");
+  if (info->n_envs < 1) return fail(TAC_EINVAL, "n_envs must be >= 1");
+  if (!(MT.E > 0) || !(MT.nu >= 0 && MT.nu < 0.5) || !(MT.rho > 0) || !(MT.mu_f >= 0))
+    return fail(TAC_EINVAL, "invalid material");
+  if (!(P.dhat > 0) || !(P.bp_margin >= 0.5 * P.dhat) || !(P.ccd_s > 0 && P.ccd_s < 1) || !(P.k_t > 0) ||
+      !(P.k_r > 0) || !(P.f_max > 0) || !(P.t_max > 0) || !(P.eps_v > 0) || P.max_iters < 1 || P.fixed_iters < 0)
+    return fail(TAC_EINVAL, "invalid solver parameters");
+  if (MS.rows * MS.cols < 1 || !MS.rest_xyz || (MS.mode != 0 && MS.mode != 1))
+    return fail(TAC_EINVAL, "invalid marker set");
+  int nv = G.n_verts, nt = G.n_tets, niv = I.n_verts, nit = I.n_tris, nm = MS.rows * MS.cols;
+  std::vector<V> X(nv), Y(niv);
+  for (int i = 0; i < nv; ++i) X[i] = {G.rest_xyz[3 * i], G.rest_xyz[3 * i + 1], G.rest_xyz[3 * i + 2]};
+  for (int i = 0; i < niv; ++i) Y[i] = {I.rest_xyz[3 * i], I.rest_xyz[3 * i + 1], I.rest_xyz[3 * i + 2]};
+  for (int i = 0; i < 4 * nt; ++i)
+    if (G.tets[i] < 0 || G.tets[i] >= nv) return fail(TAC_EINVAL, "tet index out of range");
+  for (int i = 0; i < 3 * nit; ++i)
+    if (I.tris[i] < 0 || I.tris[i] >= niv) return fail(TAC_EINVAL, "indenter triangle index out of range");
+  std::vector<unsigned char> vflag(nv, 0);
+  for (int i = 0; i < G.n_fixed; ++i) {
+    if (G.fixed[i] < 0 || G.fixed[i] >= nv) return fail(TAC_EINVAL, "fixed index out of range");
+    vflag[G.fixed[i]] |= 1;
+  }
+  // rest shape: b_k = rows of Dm^-1 (k = 1..3), V_e = det(Dm)/6, lumped mass rho V_e / 4 per vertex
+  std::vector<float4> tetb(3 * (size_t)nt);
+  std::vector<int4> tets(nt);
+  std::vector<double> massd(nv, 0.0);
+  for (int e = 0; e < nt; ++e) {
+    const int* t = G.tets + 4 * e;
+    tets[e] = make_int4(t[0], t[1], t[2], t[3]);
+    V a = sub(X[t[1]], X[t[0]]), b = sub(X[t[2]], X[t[0]]), c = sub(X[t[3]], X[t[0]]);
+    double D = det(a, b, c);
+    if (!(D > 0)) return fail(TAC_EINVAL, "non-positive tet volume at tet " + std::to_string(e));
+    // inverse of [a b c] (columns) by cofactors: row k of the inverse = (cross of the other two)/D
+    V r0 = {(b[1] * c[2] - b[2] * c[1]) / D, (b[2] * c[0] - b[0] * c[2]) / D, (b[0] * c[1] - b[1] * c[0]) / D};
+    V r1 = {(c[1] * a[2] - c[2] * a[1]) / D, (c[2] * a[0] - c[0] * a[2]) / D, (c[0] * a[1] - c[1] * a[0]) / D};
+    V r2 = {(a[1] * b[2] - a[2] * b[1]) / D, (a[2] * b[0] - a[0] * b[2]) / D, (a[0] * b[1] - a[1] * b[0]) / D};
+    double vol = D / 6.0;
+    tetb[3 * e] = make_float4((float)r0[0], (float)r0[1], (float)r0[2], (float)vol);
+    tetb[3 * e + 1] = make_float4((float)r1[0], (float)r1[1], (float)r1[2], 0.f);
+    tetb[3 * e + 2] = make_float4((float)r2[0], (float)r2[1], (float)r2[2], 0.f);
+    for (int k = 0; k < 4; ++k) massd[t[k]] += MT.rho * vol / 4.0;
+  }
+  // gel surface: faces of exactly one tet, minus faces whose 3 vertices are all fixed
+  std::map<std::array<int, 3>, int> fc;
+  for (int e = 0; e < nt; ++e) {
+    const int* t = G.tets + 4 * e;
+    for (int skip = 0; skip < 4; ++skip) {
+      std::array<int, 3> f;
+      int n = 0;
+      for (int k = 0; k < 4; ++k)
+        if (k != skip) f[n++] = t[k];
+      std::sort(f.begin(), f.end());
+      fc[f] += 1;
+    }
+  }
+  std::vector<std::array<int, 3>> st;
+  std::set<int> svs;
+  std::set<std::pair<int, int>> ses;
+  for (auto& kv : fc) {
+    if (kv.second != 1) continue;
+    const auto& f = kv.first;
+    if ((vflag[f[0]] & 1) && (vflag[f[1]] & 1) && (vflag[f[2]] & 1)) continue;
+    st.push_back(f);
+    for (int i = 0; i < 3; ++i) {
+      svs.insert(f[i]);
+      int a = f[i], b = f[(i + 1) % 3];
+      ses.insert({std::min(a, b), std::max(a, b)});
+    }
+  }
+  std::set<std::pair<int, int>> ies;
+  for (int i = 0; i < nit; ++i)
+    for (int k = 0; k < 3; ++k) {
+      int a = I.tris[3 * i + k], b = I.tris[3 * i + (k + 1) % 3];
+      ies.insert({std::min(a, b), std::max(a, b)});
+    }
+  tac_sim* sim = new tac_sim;
+  sim->device = info->device;
+  if (cudaSetDevice(info->device) != cudaSuccess) {
+    delete sim;
+    return fail(TAC_ECUDA, "cudaSetDevice failed");
+  }
+  sim->sv.assign(svs.begin(), svs.end());
+  for (auto& f : st) for (int k = 0; k < 3; ++k) sim->st_flat.push_back(f[k]);
+  for (auto& e : ses) { sim->se_flat.push_back(e.first); sim->se_flat.push_back(e.second); }
+  for (auto& e : ies) { sim->ie_flat.push_back(e.first); sim->ie_flat.push_back(e.second); }
+  for (int v : sim->sv) vflag[v] |= 2;
+  // markers: barycentric in the lowest-index rest tet with all coordinates >= -1e-12 (R22)
+  sim->mk_tet.assign(nm, -1);
+  sim->mk_idx.assign(4 * nm, 0);
+  sim->mk_w.assign(4 * nm, 0.0);
+  for (int m = 0; m < nm; ++m) {
+    V p = {MS.rest_xyz[3 * m], MS.rest_xyz[3 * m + 1], MS.rest_xyz[3 * m + 2]};
+    if (MS.mode == 0) {
+      for (int e = 0; e < nt; ++e) {
+        const int* t = G.tets + 4 * e;
+        V a = sub(X[t[1]], X[t[0]]), b = sub(X[t[2]], X[t[0]]), c = sub(X[t[3]], X[t[0]]), q = sub(p, X[t[0]]);
+        double D = det(a, b, c);
+        double l1 = det(q, b, c) / D, l2 = det(a, q, c) / D, l3 = det(a, b, q) / D;  // Cramer
+        double l[4] = {1.0 - l1 - l2 - l3, l1, l2, l3};
+        if (l[0] >= -1e-12 && l[1] >= -1e-12 && l[2] >= -1e-12 && l[3] >= -1e-12) {
+          double s = 0;
+          for (double& x : l) { x = std::max(0.0, x); s += x; }
+          for (int k = 0; k < 4; ++k) { sim->mk_idx[4 * m + k] = t[k]; sim->mk_w[4 * m + k] = l[k] / s; }
+          sim->mk_tet[m] = e;
+          break;
+        }
+      }
+      if (sim->mk_tet[m] < 0) {
+        delete sim;
+        return fail(TAC_EINVAL, "marker " + std::to_string(m) + " outside the gel mesh");
+      }
+    } else {
+      int k = MS.k;
+      if (k < 1 || k > 4 || (int)sim->sv.size() < k) { delete sim; return fail(TAC_EINVAL, "invalid kNN k"); }
+      std::vector<std::pair<double, int>> dv;
+      for (int v : sim->sv) {
+        V q = sub(X[v], p);
+        dv.push_back({std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2]), v});
+      }
+      std::partial_sort(dv.begin(), dv.begin() + k, dv.end());
+      for (int j = 0; j < 4; ++j) sim->mk_idx[4 * m + j] = dv[0].second;
+      if (dv[0].first == 0.0) sim->mk_w[4 * m] = 1.0;
+      else {
+        double s = 0;
+        for (int j = 0; j < k; ++j) s += 1.0 / dv[j].first;
+        for (int j = 0; j < k; ++j) { sim->mk_idx[4 * m + j] = dv[j].second; sim->mk_w[4 * m + j] = (1.0 / dv[j].first) / s; }
+      }
+    }
+  }
+  // indenter BVHs (body frame): triangles, edges, vertices
+  std::vector<std::array<float, 6>> btri(nit), bedge(ies.size()), bvert(niv);
+  auto primbox = [&](const int* ids, int n) {
+    std::array<float, 6> b;
+    for (int a = 0; a < 3; ++a) {
+      double lo = Y[ids[0]][a], hi = lo;
+      for (int j = 1; j < n; ++j) { lo = std::min(lo, Y[ids[j]][a]); hi = std::max(hi, Y[ids[j]][a]); }
+      b[a] = down(lo);
+      b[3 + a] = up(hi);
+    }
+    return b;
+  };
+  for (int i = 0; i < nit; ++i) btri[i] = primbox(I.tris + 3 * i, 3);
+  for (size_t i = 0; i < bedge.size(); ++i) bedge[i] = primbox(&sim->ie_flat[2 * i], 2);
+  for (int i = 0; i < niv; ++i) { int id = i; bvert[i] = primbox(&id, 1); }
+  std::vector<BNode> nodes;
+  std::vector<int> prims;
+  Dev& d = sim->d;
+  d.root_tri = build_bvh(nodes, prims, btri);
+  d.root_edge = build_bvh(nodes, prims, bedge);
+  d.root_vert = build_bvh(nodes, prims, bvert);
+  // sizes and parameters
+  d.nv = nv; d.nt = nt; d.nsv = (int)sim->sv.size(); d.nse = (int)ses.size(); d.nst = (int)st.size();
+  d.niv = niv; d.nie = (int)ies.size(); d.nit = nit; d.nm = nm;
+  d.E = info->n_envs;
+  d.Es = (d.E + 31) / 32 * 32;
+  d.kmax = P.max_candidates > 0 ? P.max_candidates : 16384;
+  d.amax = P.max_anchors > 0 ? P.max_anchors : 4096;
+  d.mu = (float)(MT.E / (2 * (1 + MT.nu)));
+  double lam = MT.E * MT.nu / ((1 + MT.nu) * (1 - 2 * MT.nu));
+  d.lam2 = (float)(lam + MT.E / (2 * (1 + MT.nu)));
+  d.mu_f = MT.mu_f;
+  d.rho_max = 0;
+  for (auto& y : Y) d.rho_max = std::max(d.rho_max, std::sqrt(y[0] * y[0] + y[1] * y[1] + y[2] * y[2]));
+  d.dhat = P.dhat; d.eps_v = P.eps_v; d.tol_x = P.tol_x; d.k_t = P.k_t; d.k_r = P.k_r; d.f_max = P.f_max;
+  d.t_max = P.t_max; d.ccd_s = P.ccd_s; d.bp_margin = P.bp_margin; d.c1 = P.c1; d.eps_E = P.eps_E;
+  d.kappa_phys = P.kappa_phys;
+  if (!(d.kappa_phys > 0)) {  // R4 default: 0.2 E lbar^2 / (12.25 dhat), lbar = mean gel surface edge length
+    double sl = 0;
+    for (auto& e : ses) { V q = sub(X[e.first], X[e.second]); sl += std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2]); }
+    double lbar = ses.empty() ? 1e-3 : sl / ses.size();
+    d.kappa_phys = 0.2 * MT.E * lbar * lbar / (12.25 * P.dhat);
+  }
+  d.beta_rule = P.beta_rule; d.precond = P.precond; d.max_halv = P.max_halvings; d.stagnation = P.stagnation;
+  d.fixed_iters = P.fixed_iters;
+  for (int a = 0; a < 3; ++a) { d.t1[a] = MS.t1[a]; d.t2[a] = MS.t2[a]; d.nrm[a] = MS.n[a]; }
+  sim->max_iters = P.max_iters;
+  sim->fixed_iters = P.fixed_iters;
+  sim->check_every = P.check_every > 0 ? P.check_every : 25;
+  // device upload
+  std::vector<float4> Xf(nv), Yf(niv);
+  for (int i = 0; i < nv; ++i) Xf[i] = make_float4((float)X[i][0], (float)X[i][1], (float)X[i][2], 0.f);
+  for (int i = 0; i < niv; ++i)
+    Yf[i] = make_float4((float)Y[i][0], (float)Y[i][1], (float)Y[i][2],
+                        (float)std::sqrt(Y[i][0] * Y[i][0] + Y[i][1] * Y[i][1] + Y[i][2] * Y[i][2]));
+  std::vector<float> massf(nv);
+  for (int i = 0; i < nv; ++i) massf[i] = (float)massd[i];
+  std::vector<int2> se2, ie2;
+  for (auto& e : ses) se2.push_back(make_int2(e.first, e.second));
+  for (auto& e : ies) ie2.push_back(make_int2(e.first, e.second));
+  std::vector<int4> st4, it4;
+  for (auto& f : st) st4.push_back(make_int4(f[0], f[1], f[2], 0));
+  for (int i = 0; i < nit; ++i) it4.push_back(make_int4(I.tris[3 * i], I.tris[3 * i + 1], I.tris[3 * i + 2], 0));
+  std::vector<int4> mki(nm);
+  std::vector<float4> mkw(nm);
+  for (int m = 0; m < nm; ++m) {
+    mki[m] = make_int4(sim->mk_idx[4 * m], sim->mk_idx[4 * m + 1], sim->mk_idx[4 * m + 2], sim->mk_idx[4 * m + 3]);
+    mkw[m] = make_float4((float)sim->mk_w[4 * m], (float)sim->mk_w[4 * m + 1], (float)sim->mk_w[4 * m + 2],
+                         (float)sim->mk_w[4 * m + 3]);
+  }
+  tac_status rc = TAC_OK;
+#define UP(vec, dst)                                  \
+  do {                                                \
+    auto* tmp_ = (std::remove_const<std::remove_pointer<decltype(dst)>::type>::type*)nullptr; \
+    rc = upload(sim, vec, &tmp_);                      \
+    if (rc) goto fail;                                \
+    dst = tmp_;                                       \
+  } while (0)
+  {
+    UP(tets, d.tets);
+    UP(tetb, d.tetb);
+    UP(Xf, d.X);
+    UP(massf, d.mass);
+    UP(vflag, d.vflag);
+    UP(sim->sv, d.sv);
+    UP(se2, d.se);
+    UP(st4, d.st);
+    UP(Yf, d.Y);
+    UP(ie2, d.ie);
+    UP(it4, d.it);
+    UP(nodes, d.bvh);
+    UP(prims, d.bvh_prims);
+    UP(mki, d.mk_idx);
+    UP(mkw, d.mk_w);
+    size_t nvec = 3 * (size_t)nv * d.Es;
+    if ((rc = zalloc(sim, nvec, &d.u)) || (rc = zalloc(sim, nvec, &d.ut)) || (rc = zalloc(sim, nvec, &d.vt)) ||
+        (rc = zalloc(sim, nvec, &d.uh)) || (rc = zalloc(sim, nvec, &d.g)) || (rc = zalloc(sim, nvec, &d.gp)) ||
+        (rc = zalloc(sim, nvec, &d.p)) || (rc = zalloc(sim, 2 * nvec, &d.D)) || (rc = zalloc(sim, (size_t)d.E, &d.es)) ||
+        (rc = zalloc(sim, (size_t)kNAcc * d.Es, &d.acc)) || (rc = zalloc(sim, (size_t)kNAccU * d.Es, &d.accu)) ||
+        (rc = zalloc(sim, (size_t)d.Es, &d.dalpha)) || (rc = zalloc(sim, (size_t)d.Es, &d.beta)) ||
+        (rc = zalloc(sim, (size_t)d.Es, &d.run)) || (rc = zalloc(sim, (size_t)d.Es, &d.pcf)) ||
+        (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.cand)) || (rc = zalloc(sim, (size_t)d.E, &d.ncand)) ||
+        (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc)) || (rc = zalloc(sim, (size_t)d.E, &d.nanc)) ||
+        (rc = zalloc(sim, 1, &sim->d_flag)) || (rc = zalloc(sim, (size_t)d.kmax, &sim->d_dbg_cand)) ||
+        (rc = zalloc(sim, 1, &sim->d_dbg_cnt)) || (rc = zalloc(sim, 3 * (size_t)nv, &sim->d_scratch)))
+      goto fail;
+    if (cudaMallocHost(&sim->h_flag, sizeof(int)) != cudaSuccess) { rc = TAC_ENOMEM; goto fail; }
+    // initial poses: per-env fp64 state on the host, then upload
+    std::vector<EnvS> es(d.E);
+    for (int e = 0; e < d.E; ++e) {
+      memset(&es[e], 0, sizeof(EnvS));
+      const float* q = info->init_poses + 7 * e;
+      double w = q[3], x = q[4], y = q[5], z = q[6];
+      double n = std::sqrt(w * w + x * x + y * y + z * z);
+      if (!(n > 0)) { rc = TAC_EINVAL; sim->err = "zero quaternion in init_poses"; goto fail; }
+      w /= n; x /= n; y /= n; z /= n;
+      double R[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                     2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                     2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
+      for (int i = 0; i < 3; ++i) es[e].c[i] = es[e].ct[i] = es[e].cs[i] = q[i];
+      for (int i = 0; i < 9; ++i) es[e].R[i] = es[e].Rt[i] = es[e].Rs[i] = R[i];
+      es[e].mode = kActive;
+    }
+    if (cudaMemcpy(d.es, es.data(), sizeof(EnvS) * d.E, cudaMemcpyHostToDevice) != cudaSuccess) {
+      rc = TAC_ECUDA; sim->err = "upload env state"; goto fail;
+    }
+    // feasibility of the initial poses: no candidate within dhat may have d <= 0
+    launch_broadphase(d, false, 0);
+    std::vector<int> run(d.Es, 1);
+    if (cudaMemcpy(d.run, run.data(), sizeof(int) * d.Es, cudaMemcpyHostToDevice) != cudaSuccess) { rc = TAC_ECUDA; goto fail; }
+    launch_eval(d, 1e-3, 0);  // energies at rest: infinite barrier energy <=> touching / intersecting
+    if (cudaDeviceSynchronize() != cudaSuccess) { rc = TAC_ECUDA; sim->err = "initial feasibility check failed"; goto fail; }
+    std::vector<EnvS> chk(d.E);
+    cudaMemcpy(chk.data(), d.es, sizeof(EnvS) * d.E, cudaMemcpyDeviceToHost);
+    for (int e = 0; e < d.E; ++e)
+      if (chk[e].flags & 8) { rc = TAC_EINVAL; sim->err = "indenter touches the gel at its initial pose (env " + std::to_string(e) + ")"; goto fail; }
+    // restore the clean initial state
+    if (cudaMemcpy(d.es, es.data(), sizeof(EnvS) * d.E, cudaMemcpyHostToDevice) != cudaSuccess) { rc = TAC_ECUDA; goto fail; }
+    cudaMemset(d.acc, 0, sizeof(double) * kNAcc * d.Es);
+    cudaMemset(d.run, 0, sizeof(int) * d.Es);
+    cudaMemset(d.ncand, 0, sizeof(int) * d.E);
+    cudaMemset(d.u, 0, sizeof(float) * nvec);
+    cudaMemset(d.g, 0, sizeof(float) * nvec);
+    cudaMemset(d.D, 0, sizeof(float) * 2 * nvec);
+    if (cudaDeviceSynchronize() != cudaSuccess) { rc = TAC_ECUDA; goto fail; }
+  }
+  *out = sim;
+  return TAC_OK;
+fail:
+  g_create_err = sim->err.empty() ? "tac_create failed" : sim->err;
+  tac_destroy(sim);
+  return rc ? rc : TAC_ECUDA;
+}
+
+tac_status tac_destroy(tac_sim* sim) {
+  if (!sim) return TAC_OK;
+  cudaSetDevice(sim->device);
+  for (void* p : sim->allocs) cudaFree(p);
+  if (sim->h_flag) cudaFreeHost(sim->h_flag);
+  delete sim->prof;
+  delete sim;
+  return TAC_OK;
+}
+
+static tac_status check_sim(tac_sim* sim) {
+  if (!sim) return TAC_EINVAL;
+  if (sim->sticky) return TAC_ECUDA;
+  return TAC_OK;
+}
+static tac_status post_launch(tac_sim* sim) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    sim->err = std::string("kernel launch: ") + cudaGetErrorString(e);
+    sim->sticky = true;
+    return TAC_ECUDA;
+  }
+  return TAC_OK;
+}
+
+tac_status tac_step(tac_sim* sim, const float* target_poses, float dt, void* stream) {
+  tac_status st = check_sim(sim);
+  if (st) return st;
+  if (!target_poses || !(dt > 0)) { sim->err = "tac_step: null poses or dt <= 0"; return TAC_EINVAL; }
+  cudaSetDevice(sim->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const Dev& d = sim->d;
+  double h = dt;
+  g_launches = 0;
+  g_prof = sim->prof;
+  launch_step_setup(d, target_poses, h, s);  // a1
+  launch_broadphase(d, false, s);            // a2
+  launch_anchors(d, h, s);                   // a3
+  int K = sim->fixed_iters > 0 ? sim->fixed_iters : sim->max_iters;
+  for (int it = 0; it < K; ++it) {
+    launch_eval(d, h, s);       // a4 + a5 + Armijo (a8)
+    launch_direction(d, s);     // a6
+    launch_curvature(d, h, s);  // a7
+    launch_alpha(d, h, s);      // a7/a8 (+ a2 rebuild)
+    if (sim->fixed_iters == 0 && (it + 1) % sim->check_every == 0) {
+      cudaMemsetAsync(sim->d_flag, 0, sizeof(int), s);
+      launch_any_active(d, sim->d_flag, s);
+      cudaMemcpyAsync(sim->h_flag, sim->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s);
+      if (cudaStreamSynchronize(s) != cudaSuccess) { g_prof = nullptr; return post_launch(sim); }
+      if (*sim->h_flag == 0) break;
+    }
+  }
+  launch_finalize(d, h, s);  // a9
+  sim->launches = g_launches;
+  g_prof = nullptr;
+  return post_launch(sim);
+}
+
+tac_status tac_markers(tac_sim* sim, float* out, int32_t ncomp, void* stream) {
+  tac_status st = check_sim(sim);
+  if (st) return st;
+  if (!out || (ncomp != 2 && ncomp != 3)) { sim->err = "tac_markers: bad output or ncomp"; return TAC_EINVAL; }
+  cudaSetDevice(sim->device);
+  g_launches = 0;
+  g_prof = sim->prof;
+  launch_markers(sim->d, out, ncomp, (cudaStream_t)stream);
+  g_prof = nullptr;
+  sim->launches = g_launches;
+  return post_launch(sim);
+}
+
+tac_status tac_reset(tac_sim* sim, const uint8_t* env_mask, const float* poses, void* stream) {
+  tac_status st = check_sim(sim);
+  if (st) return st;
+  if (!env_mask || !poses) { sim->err = "tac_reset: null pointer"; return TAC_EINVAL; }
+  cudaSetDevice(sim->device);
+  launch_reset(sim->d, env_mask, poses, (cudaStream_t)stream);
+  return post_launch(sim);
+}
+
+tac_status tac_env_status(tac_sim* sim, int32_t* iters, float* pg_norm, uint32_t* flags, void* stream) {
+  tac_status st = check_sim(sim);
+  if (st) return st;
+  cudaSetDevice(sim->device);
+  launch_status(sim->d, iters, pg_norm, flags, (cudaStream_t)stream);
+  return post_launch(sim);
+}
+
+tac_status tac_info(const tac_sim* sim, int32_t* out) {
+  if (!sim || !out) return TAC_EINVAL;
+  const Dev& d = sim->d;
+  int v[8] = {d.nv, d.nt, d.E, d.Es, d.nm, d.nsv, d.nse, d.nst};
+  memcpy(out, v, sizeof(v));
+  return TAC_OK;
+}
+
+int64_t tac_last_launch_count(const tac_sim* sim) { return sim ? sim->launches : 0; }
+
+tac_status tac_profile_enable(tac_sim* sim, int32_t on) {
+  if (!sim) return TAC_EINVAL;
+  cudaSetDevice(sim->device);
+  if (on && !sim->prof) sim->prof = new tac::Profiler;
+  if (!on && sim->prof) { delete sim->prof; sim->prof = nullptr; }
+  return TAC_OK;
+}
+
+tac_status tac_profile_read(tac_sim* sim, double* ms, int64_t* counts, int32_t n) {
+  if (!sim || !sim->prof) return TAC_ESTATE;
+  cudaSetDevice(sim->device);
+  sim->prof->drain();
+  for (int k = 0; k < n && k < KID_COUNT; ++k) {
+    if (ms) ms[k] = sim->prof->ms[k];
+    if (counts) counts[k] = sim->prof->cnt[k];
+    sim->prof->ms[k] = 0;
+    sim->prof->cnt[k] = 0;
+  }
+  return TAC_OK;
+}
+
+const char* tac_profile_kernel_name(int32_t id) { return tac::kernel_name(id); }
+
+// ---------------------------------------------------------------- debug hooks
+static tac_status gather_vec(tac_sim* sim, const float* dsrc, int env, double* out) {
+  const Dev& d = sim->d;
+  std::vector<float> tmp(3 * (size_t)d.nv);
+  for (int c = 0; c < 3; ++c)
+    CK(cudaMemcpy2D(tmp.data() + (size_t)c * d.nv, sizeof(float), dsrc + (size_t)c * d.nv * d.Es + env,
+                    sizeof(float) * d.Es, sizeof(float), d.nv, cudaMemcpyDeviceToHost));
+  for (int v = 0; v < d.nv; ++v)
+    for (int c = 0; c < 3; ++c) out[3 * v + c] = tmp[(size_t)c * d.nv + v];
+  return TAC_OK;
+}
+static tac_status scatter_vec(tac_sim* sim, float* ddst, int env, const double* in) {
+  const Dev& d = sim->d;
+  std::vector<float> tmp(3 * (size_t)d.nv);
+  for (int v = 0; v < d.nv; ++v)
+    for (int c = 0; c < 3; ++c) tmp[(size_t)c * d.nv + v] = (float)in[3 * v + c];
+  for (int c = 0; c < 3; ++c)
+    CK(cudaMemcpy2D(ddst + (size_t)c * d.nv * d.Es + env, sizeof(float) * d.Es, tmp.data() + (size_t)c * d.nv,
+                    sizeof(float), sizeof(float), d.nv, cudaMemcpyHostToDevice));
+  return TAC_OK;
+}
+
+tac_status tac_get_state(tac_sim* sim, int32_t env, double* u, double* v, double* c, double* R) {
+  tac_status st = check_sim(sim);
+  if (st) return st;
+  if (env < 0 || env >= sim->d.E) return TAC_EINVAL;
+  cudaSetDevice(sim->device);
+  CK(cudaDeviceSynchronize());
+  if (u && (st = gather_vec(sim, sim->d.ut, env, u))) return st;
+  if (v && (st = gather_vec(sim, sim->d.vt, env, v))) return st;
+  EnvS es;
+  CK(cudaMemcpy(&es, sim->d.es + env, sizeof(EnvS), cudaMemcpyDeviceToHost));
+  if (c) for (int i = 0; i < 3; ++i) c[i] = es.ct[i];
+  if (R) for (int i = 0; i < 9; ++i) R[i] = es.Rt[i];
+  return TAC_OK;
+}
+
+tac_status tac_set_state(tac_sim* sim, int32_t env, const double* u, const double* v, const double* c,
+                         const double* R) {
+  tac_status st = check_sim(sim);
+  if (st) return st;
+  if (env < 0 || env >= sim->d.E || !u || !v || !c || !R) return TAC_EINVAL;
+  cudaSetDevice(sim->device);
+  CK(cudaDeviceSynchronize());
+  if ((st = scatter_vec(sim, sim->d.ut, env, u)) || (st = scatter_vec(sim, sim->d.u, env, u)) ||
+      (st = scatter_vec(sim, sim->d.vt, env, v)))
+    return st;
+  EnvS es;
+  CK(cudaMemcpy(&es, sim->d.es + env, sizeof(EnvS), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < 3; ++i) es.c[i] = es.ct[i] = c[i];
+  for (int i = 0; i < 9; ++i) es.R[i] = es.Rt[i] = R[i];
+  CK(cudaMemcpy(sim->d.es + env, &es, sizeof(EnvS), cudaMemcpyHostToDevice));
+  return TAC_OK;
+}
+
+tac_status tac_debug_surface(const tac_sim* sim, int32_t* sv, int32_t* se, int32_t* st, int32_t* ie, int32_t* counts) {
+  if (!sim) return TAC_EINVAL;
+  if (sv) memcpy(sv, sim->sv.data(), sizeof(int) * sim->sv.size());
+  if (se) memcpy(se, sim->se_flat.data(), sizeof(int) * sim->se_flat.size());
+  if (st) memcpy(st, sim->st_flat.data(), sizeof(int) * sim->st_flat.size());
+  if (ie) memcpy(ie, sim->ie_flat.data(), sizeof(int) * sim->ie_flat.size());
+  if (counts) counts[0] = (int)sim->ie_flat.size() / 2;
+  return TAC_OK;
+}
+
+tac_status tac_debug_marker_map(const tac_sim* sim, int32_t* tet, int32_t* idx, double* w) {
+  if (!sim) return TAC_EINVAL;
+  int nm = sim->d.nm;
+  if (tet) memcpy(tet, sim->mk_tet.data(), sizeof(int) * nm);
+  if (idx) memcpy(idx, sim->mk_idx.data(), sizeof(int) * 4 * nm);
+  if (w) memcpy(w, sim->mk_w.data(), sizeof(double) * 4 * nm);
+  return TAC_OK;
+}
+
+static tac_status set_pose_current(tac_sim* sim, int env, const double* c, const double* R) {
+  EnvS es;
+  CK(cudaMemcpy(&es, sim->d.es + env, sizeof(EnvS), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < 3; ++i) es.c[i] = c[i];
+  for (int i = 0; i < 9; ++i) es.R[i] = R[i];
+  es.mode = kActive;
+  CK(cudaMemcpy(sim->d.es + env, &es, sizeof(EnvS), cudaMemcpyHostToDevice));
+  return TAC_OK;
+}
+
+tac_status tac_debug_broadphase(tac_sim* sim, int32_t env, const float* u, const double* c, const double* R,
+                                double r, int32_t* out, int32_t cap, int32_t* n) {
+  tac_status st = check_sim(sim);
+  if (st) return st;
+  if (env < 0 || env >= sim->d.E || !u || !c || !R || !n) return TAC_EINVAL;
+  cudaSetDevice(sim->device);
+  Dev d = sim->d;
+  std::vector<double> ud(3 * (size_t)d.nv);
+  for (size_t i = 0; i < ud.size(); ++i) ud[i] = u[i];
+  if ((st = scatter_vec(sim, d.u, env, ud.data())) || (st = set_pose_current(sim, env, c, R))) return st;
+  // run the production kernel restricted to this env (E = env + 1, blocks of env only)
+  CK(cudaMemset(sim->d_dbg_cnt, 0, sizeof(int)));
+  Dev dd = d;
+  dd.E = env + 1;
+  std::vector<EnvS> all(env + 1);
+  CK(cudaMemcpy(all.data(), d.es, sizeof(EnvS) * (env + 1), cudaMemcpyDeviceToHost));
+  std::vector<EnvS> masked = all;
+  for (int e = 0; e < env; ++e) masked[e].mode = kDone;
+  CK(cudaMemcpy(d.es, masked.data(), sizeof(EnvS) * (env + 1), cudaMemcpyHostToDevice));
+  launch_debug_broadphase(dd, r, sim->d_dbg_cand, sim->d_dbg_cnt, d.kmax, 0);
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(d.es, all.data(), sizeof(EnvS) * (env + 1), cudaMemcpyHostToDevice));
+  int cnt = 0;
+  CK(cudaMemcpy(&cnt, sim->d_dbg_cnt, sizeof(int), cudaMemcpyDeviceToHost));
+  *n = cnt;
+  int m = std::min(std::min(cnt, cap), d.kmax);
+  std::vector<unsigned long long> rec(m);
+  if (m) CK(cudaMemcpy(rec.data(), sim->d_dbg_cand, sizeof(unsigned long long) * m, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < m; ++i) {
+    out[3 * i] = (int)(rec[i] >> 62);
+    out[3 * i + 1] = (int)((rec[i] >> 31) & 0x7fffffffu);
+    out[3 * i + 2] = (int)(rec[i] & 0x7fffffffu);
+  }
+  return post_launch(sim);
+}
+
+tac_status tac_debug_eval(tac_sim* sim, int32_t env, const double* u_t, const double* v_t, const double* c_t,
+                          const double* R_t, const double* u, const double* c, const double* R,
+                          const double* target7, double dt, double* parts, double* g, double* D, double* grig,
+                          double* Drig) {
+  tac_status st = check_sim(sim);
+  if (st) return st;
+  if (env < 0 || env >= sim->d.E || !(dt > 0)) return TAC_EINVAL;
+  cudaSetDevice(sim->device);
+  Dev d = sim->d;
+  if ((st = tac_set_state(sim, env, u_t, v_t, c_t, R_t))) return st;
+  // step setup for all envs with the target, then mask every other env
+  std::vector<float> poses(7 * (size_t)d.E, 0.f);
+  std::vector<EnvS> all(d.E);
+  CK(cudaMemcpy(all.data(), d.es, sizeof(EnvS) * d.E, cudaMemcpyDeviceToHost));
+  for (int e = 0; e < d.E; ++e) {
+    for (int i = 0; i < 3; ++i) poses[7 * e + i] = (float)all[e].ct[i];
+    poses[7 * e + 3] = 1.f;
+  }
+  for (int i = 0; i < 7; ++i) poses[7 * env + i] = (float)target7[i];
+  float* dp = nullptr;
+  CK(cudaMalloc(&dp, sizeof(float) * poses.size()));
+  CK(cudaMemcpy(dp, poses.data(), sizeof(float) * poses.size(), cudaMemcpyHostToDevice));
+  launch_step_setup(d, dp, dt, 0);
+  CK(cudaDeviceSynchronize());
+  cudaFree(dp);
+  std::vector<EnvS> es(d.E);
+  CK(cudaMemcpy(es.data(), d.es, sizeof(EnvS) * d.E, cudaMemcpyDeviceToHost));
+  for (int e = 0; e < d.E; ++e)
+    if (e != env) es[e].mode = kDone;
+  CK(cudaMemcpy(d.es, es.data(), sizeof(EnvS) * d.E, cudaMemcpyHostToDevice));
+  std::vector<int> run(d.Es, 0);
+  run[env] = 1;
+  CK(cudaMemcpy(d.run, run.data(), sizeof(int) * d.Es, cudaMemcpyHostToDevice));
+  launch_broadphase(d, false, 0);
+  launch_anchors(d, dt, 0);
+  // move to the evaluation state (u, c, R) and rebuild the candidates there
+  if ((st = scatter_vec(sim, d.u, env, u)) || (st = set_pose_current(sim, env, c, R))) return st;
+  CK(cudaMemset(d.ncand + env, 0, sizeof(int)));
+  launch_broadphase(d, false, 0);
+  launch_eval(d, dt, 0);
+  CK(cudaDeviceSynchronize());
+  // results: accept kernel stored the energy and rigid terms in EnvS; g / D in the vectors
+  EnvS r;
+  CK(cudaMemcpy(&r, d.es + env, sizeof(EnvS), cudaMemcpyDeviceToHost));
+  if (g && (st = gather_vec(sim, d.g, env, g))) return st;
+  if (D) {
+    std::vector<float> tmp(6 * (size_t)d.nv);
+    for (int c6 = 0; c6 < 6; ++c6)
+      CK(cudaMemcpy2D(tmp.data() + (size_t)c6 * d.nv, sizeof(float), d.D + (size_t)c6 * d.nv * d.Es + env,
+                      sizeof(float) * d.Es, sizeof(float), d.nv, cudaMemcpyDeviceToHost));
+    for (int v = 0; v < d.nv; ++v) {
+      float xx = tmp[v], yy = tmp[d.nv + v], zz = tmp[2 * d.nv + v], xy = tmp[3 * d.nv + v], xz = tmp[4 * d.nv + v],
+            yz = tmp[5 * d.nv + v];
+      double M[9] = {xx, xy, xz, xy, yy, yz, xz, yz, zz};
+      for (int k = 0; k < 9; ++k) D[9 * v + k] = M[k];
+    }
+  }
+  if (grig) for (int k = 0; k < 6; ++k) grig[k] = r.gr[k];
+  if (Drig) for (int k = 0; k < 9; ++k) { Drig[k] = r.Dc[k]; Drig[9 + k] = r.Dth[k]; }
+  if (parts) for (int k = 0; k < 5; ++k) parts[k] = r.Ep[k];
+  return post_launch(sim);
+}
+
+}  // extern "C"

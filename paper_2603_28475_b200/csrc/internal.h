@@ -1,0 +1,132 @@
+// internal.h — device data layout and launchers of libtac (not part of the ABI).
+//
+// Layout (DESIGN.md §"Data layout in HBM"): per-env vectors are SoA with the env
+// index fastest, A[c][v][Es] (Es = n_envs rounded up to 32), so a warp = 32 envs
+// of one vertex / tet and every vertex row is one 128-byte coalesced transaction;
+// the static mesh (tets, b-vectors, volumes, masses) is shared by all envs and
+// read with warp-uniform broadcast loads.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tac {
+
+constexpr int kNodeLeaf = 4;
+
+struct BNode {  // indenter BVH node, body frame; leaf if left < 0: prims [-left-1, -left-1+right)
+  float lo[3];
+  int left;
+  float hi[3];
+  int right;
+};
+
+// friction anchor: frozen at the step start
+struct Anchor {
+  int kind, a, b, pad;
+  float w[4];
+  float t1[3], lam;
+  float t2[3], pad2;
+};
+
+// per-env solver state (fp64 control, one thread per env in the scalar kernels)
+struct EnvS {
+  double c[3], R[9];          // current pose (trial point)
+  double cp[3], Rp[9];        // pose at the last accepted iterate x_k
+  double ct[3], Rt[9];        // pose at the step start
+  double cs[3], Rs[9];        // target pose
+  double gr[6], grp[6], pr[6];  // rigid gradient, previous gradient, direction (c, theta)
+  double Dc[9], Dth[9];       // rigid diagonal blocks of the last accepted evaluation
+  double E, Eprev, alpha, gp_prev, gPg_prev, S, beta, best_pg, pg, pose_res;
+  double Lrel_last;
+  double Ep[5];                // energy parts of the last evaluation (diagnostics)
+  int iter, halv, restart, reeval, mode, flags, best_it, accepted, rebuild, ncand_over;
+};
+
+// modes
+constexpr int kActive = 0, kDone = 1;
+
+// double accumulators [kNAcc][Es]
+enum AccIdx {
+  A_EIN = 0, A_EEL, A_EB, A_EF,
+  A_GR = 4,        // 6
+  A_DR = 10,       // 18 (Dc 9, Dth 9)
+  A_DOT = 28,      // 7: gPy, yp, yPy, pg, gPg, gg, pp
+  A_PHP = 35,
+  kNAcc = 36
+};
+// uint accumulators [kNAccU][Es] (non-negative floats compared as uint)
+enum AccUIdx { U_PGMAX = 0, U_M, U_LREL, U_ACCD, kNAccU };
+
+struct Dev {
+  // sizes
+  int nv, nt, nsv, nse, nst, niv, nie, nit, nm, E, Es;
+  int kmax, amax;
+  // static mesh
+  const int4* tets;      // [nt]
+  const float4* tetb;    // [nt][3]: (b1, vol), (b2, 0), (b3, 0)
+  const float4* X;       // [nv] rest position (fp32 exact), w = 0
+  const float* mass;     // [nv]
+  const unsigned char* vflag;  // [nv] bit0 fixed, bit1 on the gel surface
+  const int* sv;         // [nsv]
+  const int2* se;        // [nse]
+  const int4* st;        // [nst]
+  const float4* Y;       // [niv] body frame, w = |Y|
+  const int2* ie;        // [nie]
+  const int4* it;        // [nit]
+  const BNode* bvh;      // nodes of the 3 BVHs
+  const int* bvh_prims;  // prim lists
+  int root_tri, root_edge, root_vert;
+  const int4* mk_idx;    // [nm]
+  const float4* mk_w;    // [nm]
+  // per-env vectors [c][nv][Es]
+  float *u, *ut, *vt, *uh, *g, *gp, *p, *D;
+  EnvS* es;              // [E]
+  double* acc;           // [kNAcc][Es]
+  unsigned* accu;        // [kNAccU][Es]
+  float* dalpha;         // [Es] pending update u += dalpha p
+  float* beta;           // [Es]
+  int* run;              // [Es] bit0 evaluate, bit1 direction, bit2 rebuild
+  float4* pcf;           // [Es] rigid p_c (float) for L_rel
+  unsigned long long* cand;  // [E][kmax] (kind<<62 | a<<31 | b)
+  int* ncand;            // [E]
+  Anchor* anc;           // [E][amax]
+  int* nanc;             // [E]
+  // material / params
+  float mu, lam2;        // mu, lambda' = lambda + mu
+  double rho_max, dhat, kappa_phys, eps_v, tol_x, k_t, k_r, f_max, t_max, ccd_s, bp_margin, c1, eps_E, mu_f;
+  int beta_rule, precond, max_halv, stagnation, fixed_iters;
+  double t1[3], t2[3], nrm[3];
+};
+
+// ---- launchers (kernels.cu) ----
+void launch_step_setup(const Dev& d, const float* poses, double h, cudaStream_t s);
+void launch_vert_setup(const Dev& d, double h, cudaStream_t s);
+void launch_broadphase(const Dev& d, bool masked, cudaStream_t s);
+void launch_anchors(const Dev& d, double h, cudaStream_t s);
+void launch_eval(const Dev& d, double h, cudaStream_t s);  // vertex pre + element + contact + accept
+void launch_direction(const Dev& d, cudaStream_t s);
+void launch_curvature(const Dev& d, double h, cudaStream_t s);
+void launch_alpha(const Dev& d, double h, cudaStream_t s);
+void launch_finalize(const Dev& d, double h, cudaStream_t s);
+void launch_markers(const Dev& d, float* out, int ncomp, cudaStream_t s);
+void launch_reset(const Dev& d, const unsigned char* mask, const float* poses, cudaStream_t s);
+void launch_status(const Dev& d, int* iters, float* pg, unsigned* flags, cudaStream_t s);
+void launch_any_active(const Dev& d, int* out, cudaStream_t s);
+// debug
+void launch_debug_broadphase(const Dev& d, double r, unsigned long long* out, int* cnt, int cap, cudaStream_t s);
+int launches_per_iteration();
+extern thread_local long long g_launches;
+
+// ---- optional per-kernel CUDA-event profiling (bench.py roofline; off by default) ----
+enum KernelId {
+  KID_STEP_SETUP = 0, KID_VERT_SETUP, KID_BROADPHASE, KID_ANCHORS, KID_VERT_PRE, KID_ELEM_GRAD, KID_CONTACT_GRAD,
+  KID_ACCEPT, KID_DIR_REDUCE, KID_DIR_SCALAR, KID_DIR_APPLY, KID_ELEM_CURV, KID_CONTACT_CURV, KID_ALPHA,
+  KID_CCD, KID_FIN_VERT, KID_FIN_ENV, KID_MARKERS, KID_OTHER, KID_COUNT
+};
+struct Profiler;
+extern thread_local Profiler* g_prof;
+void prof_begin(int kid, cudaStream_t s);
+void prof_end(int kid, cudaStream_t s);
+const char* kernel_name(int kid);
+
+}  // namespace tac

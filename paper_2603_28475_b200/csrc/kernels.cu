@@ -1,0 +1,1407 @@
+// kernels.cu — sm_100a kernels of the batched PNCG-IPC step.
+//
+// Citations: P:L = PAPER.md line L (Supp. §A: P:419-466), R# = DESIGN.md reading.
+// Thread mapping:
+//   vertex / element kernels: block (32, 8); lane = env (env-fastest SoA), warp = one
+//     vertex or tet, so static mesh data is a warp-uniform broadcast load and per-env
+//     vertex rows are 128-byte coalesced;
+//   contact kernels: blockIdx.y = env, threads stride over that env's candidate pairs;
+//   scalar kernels: one thread per env (fp64 control flow of the NCG).
+#include <cfloat>
+#include <cmath>
+
+#include "internal.h"
+
+namespace tac {
+
+thread_local long long g_launches = 0;
+thread_local Profiler* g_prof = nullptr;
+
+static const char* kNames[KID_COUNT] = {
+    "step_setup", "vert_setup", "broadphase", "anchors", "vert_pre", "elem_grad", "contact_grad", "accept",
+    "dir_reduce", "dir_scalar", "dir_apply", "elem_curv", "contact_curv", "alpha", "ccd", "finalize_vert",
+    "finalize_env", "markers", "other"};
+const char* kernel_name(int kid) { return (kid >= 0 && kid < KID_COUNT) ? kNames[kid] : "?"; }
+
+// ------------------------------------------------------------------ small helpers
+__device__ __forceinline__ size_t vidx(const Dev& d, int c, int v, int e) {
+  return ((size_t)c * d.nv + v) * d.Es + e;
+}
+struct d3 {
+  double x, y, z;
+};
+__device__ __forceinline__ d3 mk(double x, double y, double z) { return d3{x, y, z}; }
+__device__ __forceinline__ d3 operator+(d3 a, d3 b) { return mk(a.x + b.x, a.y + b.y, a.z + b.z); }
+__device__ __forceinline__ d3 operator-(d3 a, d3 b) { return mk(a.x - b.x, a.y - b.y, a.z - b.z); }
+__device__ __forceinline__ d3 operator*(double s, d3 a) { return mk(s * a.x, s * a.y, s * a.z); }
+__device__ __forceinline__ double dot(d3 a, d3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ d3 cross(d3 a, d3 b) {
+  return mk(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ double nrm(d3 a) { return sqrt(dot(a, a)); }
+__device__ __forceinline__ d3 mv(const double* R, d3 y) {
+  return mk(R[0] * y.x + R[1] * y.y + R[2] * y.z, R[3] * y.x + R[4] * y.y + R[5] * y.z,
+            R[6] * y.x + R[7] * y.y + R[8] * y.z);
+}
+__device__ __forceinline__ d3 ld3(const double* a) { return mk(a[0], a[1], a[2]); }
+
+__device__ __forceinline__ void atomic_max_pos(unsigned* a, float v) {  // v >= 0
+  if (v > 0.f) atomicMax(a, __float_as_uint(v));
+}
+__device__ __forceinline__ void atomic_min_pos(unsigned* a, float v) {
+  if (v >= 0.f) atomicMin(a, __float_as_uint(v));
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_min(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+// block-wide sum of one double into *out (atomic), block of up to 1024 threads (1D)
+__device__ void block_sum_atomic(double v, double* out, double* sm) {
+  v = warp_sum(v);
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sm[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    int nw = (blockDim.x + 31) >> 5;
+    double s = lane < nw ? sm[lane] : 0.0;
+    s = warp_sum(s);
+    if (lane == 0 && s != 0.0) atomicAdd(out, s);
+  }
+}
+
+// ---- SO(3), fp64 (R18) ----
+__device__ void quat_R(const float* q7, double* R) {
+  double w = q7[3], x = q7[4], y = q7[5], z = q7[6];
+  double n = sqrt(w * w + x * x + y * y + z * z);
+  w /= n; x /= n; y /= n; z /= n;
+  R[0] = 1 - 2 * (y * y + z * z); R[1] = 2 * (x * y - w * z); R[2] = 2 * (x * z + w * y);
+  R[3] = 2 * (x * y + w * z); R[4] = 1 - 2 * (x * x + z * z); R[5] = 2 * (y * z - w * x);
+  R[6] = 2 * (x * z - w * y); R[7] = 2 * (y * z + w * x); R[8] = 1 - 2 * (x * x + y * y);
+}
+__device__ void mm3(const double* A, const double* B, double* C) {
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) C[3 * i + j] = A[3 * i] * B[j] + A[3 * i + 1] * B[3 + j] + A[3 * i + 2] * B[6 + j];
+}
+__device__ void mmT(const double* A, const double* B, double* C) {  // A B^T
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) C[3 * i + j] = A[3 * i] * B[3 * j] + A[3 * i + 1] * B[3 * j + 1] + A[3 * i + 2] * B[3 * j + 2];
+}
+__device__ void rodrigues(d3 w, double* R) {
+  double th = nrm(w);
+  double a, b;
+  if (th < 1e-8) { a = 1 - th * th / 6; b = 0.5 - th * th / 24; }
+  else { a = sin(th) / th; b = (1 - cos(th)) / (th * th); }
+  double K[9] = {0, -w.z, w.y, w.z, 0, -w.x, -w.y, w.x, 0};
+  double K2[9];
+  mm3(K, K, K2);
+  for (int i = 0; i < 9; ++i) R[i] = (i % 4 == 0 ? 1.0 : 0.0) + a * K[i] + b * K2[i];
+}
+__device__ d3 so3_log(const double* R) {
+  double tr = R[0] + R[4] + R[8];
+  double c = fmax(-1.0, fmin(1.0, 0.5 * (tr - 1)));
+  double th = acos(c);
+  d3 v = mk(R[7] - R[5], R[2] - R[6], R[3] - R[1]);
+  if (th < 1e-6) return (0.5 * (1 + th * th / 6)) * v;
+  if (M_PI - th < 1e-6) {
+    int i = (R[0] >= R[4] && R[0] >= R[8]) ? 0 : (R[4] >= R[8] ? 1 : 2);
+    double a[3];
+    a[i] = sqrt(fmax(0.0, 0.5 * (R[4 * i] + 1)));
+    for (int j = 0; j < 3; ++j)
+      if (j != i) a[j] = (R[3 * i + j] + R[3 * j + i]) / (4 * a[i]);
+    d3 ax = mk(a[0], a[1], a[2]);
+    return (th / nrm(ax)) * ax;
+  }
+  return (th / (2 * sin(th))) * v;
+}
+// force-capped pose spring weight psi'(r)/r (R18)
+__device__ __forceinline__ double spring_w(double r, double k, double cap) { return r <= cap / k ? k : cap / r; }
+__device__ __forceinline__ double spring_e(double r, double k, double cap) {
+  double rho = cap / k;
+  return r <= rho ? 0.5 * k * r * r : cap * (r - 0.5 * rho);
+}
+
+// ---- barrier (R3) and mollifier ----
+__device__ __forceinline__ double bar_b(double x, double dh) { return -(x - dh) * (x - dh) * log(x / dh); }
+__device__ __forceinline__ double bar_db(double x, double dh) {
+  return -2 * (x - dh) * log(x / dh) - (x - dh) * (x - dh) / x;
+}
+__device__ __forceinline__ double bar_ddb(double x, double dh) {
+  return -2 * log(x / dh) - 4 * (x - dh) / x + (x - dh) * (x - dh) / (x * x);
+}
+__device__ __forceinline__ double moll_f(double s, double eps) {
+  return s >= eps ? s : (-s * s * s / (3 * eps * eps) + s * s / eps + eps / 3);
+}
+__device__ __forceinline__ double moll_f1(double s, double eps) { return s >= eps ? 1.0 / s : (2 / eps - s / (eps * eps)); }
+
+// ---- exact primitive distances, fp64; r = sum_k w_k z_k, d = |r| ----
+struct DR {
+  double d, w[4];
+};
+__device__ __forceinline__ double seg_t(d3 p, d3 a, d3 b) {
+  d3 e = b - a;
+  return fmin(1.0, fmax(0.0, dot(p - a, e) / dot(e, e)));
+}
+__device__ DR dist_pt(d3 p, d3 t0, d3 t1, d3 t2) {
+  DR r;
+  d3 e1 = t1 - t0, e2 = t2 - t0, q = p - t0;
+  double a11 = dot(e1, e1), a12 = dot(e1, e2), a22 = dot(e2, e2), r1 = dot(q, e1), r2 = dot(q, e2);
+  double det = a11 * a22 - a12 * a12;
+  double s = (a22 * r1 - a12 * r2) / det, t = (a11 * r2 - a12 * r1) / det;
+  if (s >= 0 && t >= 0 && s + t <= 1) {
+    r.d = nrm(q - s * e1 - t * e2);
+    r.w[0] = 1; r.w[1] = -(1 - s - t); r.w[2] = -s; r.w[3] = -t;
+    return r;
+  }
+  r.d = DBL_MAX;
+  d3 T[3] = {t0, t1, t2};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    int i = k, j = (k + 1) % 3;
+    double u = seg_t(p, T[i], T[j]);
+    double dd = nrm(p - ((1 - u) * T[i] + u * T[j]));
+    if (dd < r.d) {
+      r.d = dd;
+      r.w[0] = 1; r.w[1] = 0; r.w[2] = 0; r.w[3] = 0;
+      r.w[1 + i] = -(1 - u);
+      r.w[1 + j] = -u;
+    }
+  }
+  return r;
+}
+__device__ DR dist_ee(d3 a0, d3 a1, d3 b0, d3 b1) {
+  DR r;
+  d3 d1 = a1 - a0, d2 = b1 - b0, q = a0 - b0;
+  double a = dot(d1, d1), e = dot(d2, d2), b = dot(d1, d2), c = dot(d1, q), f = dot(d2, q);
+  double den = a * e - b * b;
+  if (den > 1e-12 * a * e) {
+    double s = (b * f - c * e) / den, t = (a * f - b * c) / den;
+    if (s > 0 && s < 1 && t > 0 && t < 1) {
+      r.d = nrm(q + s * d1 - t * d2);
+      r.w[0] = 1 - s; r.w[1] = s; r.w[2] = -(1 - t); r.w[3] = -t;
+      return r;
+    }
+  }
+  r.d = DBL_MAX;
+  {
+    double t = seg_t(a0, b0, b1), dd = nrm(a0 - ((1 - t) * b0 + t * b1));
+    if (dd < r.d) { r.d = dd; r.w[0] = 1; r.w[1] = 0; r.w[2] = -(1 - t); r.w[3] = -t; }
+  }
+  {
+    double t = seg_t(a1, b0, b1), dd = nrm(a1 - ((1 - t) * b0 + t * b1));
+    if (dd < r.d) { r.d = dd; r.w[0] = 0; r.w[1] = 1; r.w[2] = -(1 - t); r.w[3] = -t; }
+  }
+  {
+    double s = seg_t(b0, a0, a1), dd = nrm((1 - s) * a0 + s * a1 - b0);
+    if (dd < r.d) { r.d = dd; r.w[0] = 1 - s; r.w[1] = s; r.w[2] = -1; r.w[3] = 0; }
+  }
+  {
+    double s = seg_t(b1, a0, a1), dd = nrm((1 - s) * a0 + s * a1 - b1);
+    if (dd < r.d) { r.d = dd; r.w[0] = 1 - s; r.w[1] = s; r.w[2] = 0; r.w[3] = -1; }
+  }
+  return r;
+}
+
+// corners of a candidate / anchor: ids and sides (gel or indenter)
+struct Corners {
+  int id[4];
+  bool ind[4];
+  int na;  // corners on the first side
+};
+__device__ __forceinline__ Corners corners_of(const Dev& d, int kind, int a, int b) {
+  Corners c;
+  if (kind == 0) {
+    c.id[0] = d.sv[a]; c.ind[0] = false;
+    int4 t = d.it[b];
+    c.id[1] = t.x; c.id[2] = t.y; c.id[3] = t.z;
+    c.ind[1] = c.ind[2] = c.ind[3] = true;
+    c.na = 1;
+  } else if (kind == 1) {
+    c.id[0] = a; c.ind[0] = true;
+    int4 t = d.st[b];
+    c.id[1] = t.x; c.id[2] = t.y; c.id[3] = t.z;
+    c.ind[1] = c.ind[2] = c.ind[3] = false;
+    c.na = 1;
+  } else {
+    int2 ge = d.se[a], ie = d.ie[b];
+    c.id[0] = ge.x; c.id[1] = ge.y; c.id[2] = ie.x; c.id[3] = ie.y;
+    c.ind[0] = c.ind[1] = false;
+    c.ind[2] = c.ind[3] = true;
+    c.na = 2;
+  }
+  return c;
+}
+__device__ __forceinline__ d3 gel_pos(const Dev& d, const float* u, int v, int e) {
+  float4 X = d.X[v];
+  return mk((double)X.x + (double)u[vidx(d, 0, v, e)], (double)X.y + (double)u[vidx(d, 1, v, e)],
+            (double)X.z + (double)u[vidx(d, 2, v, e)]);
+}
+__device__ __forceinline__ d3 gel_vec(const Dev& d, const float* a, int v, int e) {
+  return mk(a[vidx(d, 0, v, e)], a[vidx(d, 1, v, e)], a[vidx(d, 2, v, e)]);
+}
+__device__ __forceinline__ d3 ind_body(const Dev& d, int j) {
+  float4 y = d.Y[j];
+  return mk(y.x, y.y, y.z);
+}
+__device__ __forceinline__ DR pair_dist(int kind, const d3* z) {
+  return kind == 2 ? dist_ee(z[0], z[1], z[2], z[3]) : dist_pt(z[0], z[1], z[2], z[3]);
+}
+
+// ------------------------------------------------------------------ a1: step setup
+__global__ void k_step_setup(Dev d, const float* poses) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= d.E) return;
+  EnvS& s = d.es[e];
+  const float* q = poses + 7 * e;
+  s.cs[0] = q[0]; s.cs[1] = q[1]; s.cs[2] = q[2];
+  quat_R(q, s.Rs);
+  for (int i = 0; i < 3; ++i) { s.c[i] = s.ct[i]; s.cp[i] = s.ct[i]; }
+  for (int i = 0; i < 9; ++i) { s.R[i] = s.Rt[i]; s.Rp[i] = s.Rt[i]; }
+  double RRt[9];
+  mmT(s.Rs, s.Rt, RRt);
+  d3 dc = ld3(s.cs) - ld3(s.ct);
+  s.flags = (nrm(dc) > 2e-3 || nrm(so3_log(RRt)) > 5 * M_PI / 180) ? 16 : 0;
+  s.iter = 0; s.halv = 0; s.restart = 1; s.reeval = 0; s.mode = kActive; s.best_it = 0; s.accepted = 0;
+  s.rebuild = 0; s.ncand_over = 0;
+  s.alpha = 0; s.S = 0; s.best_pg = INFINITY; s.pg = 0; s.E = 0; s.Eprev = 0; s.gp_prev = 0; s.beta = 0;
+  for (int i = 0; i < 6; ++i) s.pr[i] = 0;
+  d.dalpha[e] = 0.f;
+  d.beta[e] = 0.f;
+  d.run[e] = 1;
+  d.ncand[e] = 0;
+  d.nanc[e] = 0;
+  for (int k = 0; k < kNAcc; ++k) d.acc[(size_t)k * d.Es + e] = 0.0;
+  for (int k = 0; k < kNAccU; ++k) d.accu[(size_t)k * d.Es + e] = (k == U_ACCD) ? 0x7f800000u : 0u;
+}
+
+// x^ = x^t + h v^t on free vertices; u = u^t
+__global__ void k_vert_setup(Dev d, float h) {
+  int e = blockIdx.x * 32 + threadIdx.x;
+  if (e >= d.E) return;
+  for (int v = blockIdx.y * 8 + threadIdx.y; v < d.nv; v += gridDim.y * 8) {
+    bool fixed = d.vflag[v] & 1;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      size_t i = vidx(d, c, v, e);
+      float ut = d.ut[i];
+      d.u[i] = ut;
+      d.uh[i] = fixed ? 0.f : ut + h * d.vt[i];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ a2: broad phase
+// Candidates: (gel vert, ind tri), (ind vert, gel tri), (gel edge, ind edge) whose
+// world AABBs are within r on every axis (R16).  Traversal of the static body-frame
+// BVH tests the world AABB of each rotated node box (conservative, +eps); leaves run
+// the exact fp64 predicate with the oracle's rounding: gel x = X + u, indenter
+// y = ((R0 Y0 + R1 Y1) + R2 Y2) + c, no contraction (__dmul_rn / __dadd_rn).
+__device__ __forceinline__ double ind_world_exact(const double* R, const double* c, float4 y, int a) {
+  double t0 = __dmul_rn(R[3 * a], (double)y.x);
+  double t1 = __dmul_rn(R[3 * a + 1], (double)y.y);
+  double t2 = __dmul_rn(R[3 * a + 2], (double)y.z);
+  return __dadd_rn(__dadd_rn(__dadd_rn(t0, t1), t2), c[a]);
+}
+
+template <int NGEL, int NIND>
+__device__ void bp_query(const Dev& d, int e, int kind, int gid, const int* gv, const double* gxlo,
+                         const double* gxhi, const double* R, const double* c, const float* Rf, const float* cf,
+                         double r, int root, unsigned long long* out, int* cnt, int cap, bool* over) {
+  // query box (fp32, inflated by r + eps)
+  float qlo[3], qhi[3];
+  const float eps = 1e-7f;
+  for (int a = 0; a < 3; ++a) {
+    qlo[a] = (float)(gxlo[a] - r) - eps;
+    qhi[a] = (float)(gxhi[a] + r) + eps;
+  }
+  int stack[40];
+  int sp = 0;
+  stack[sp++] = root;
+  while (sp > 0) {
+    int ni = stack[--sp];
+    BNode nd = d.bvh[ni];
+    // world AABB of the rotated node box: centre R cN + c, half |R| hN
+    float cn[3] = {0.5f * (nd.lo[0] + nd.hi[0]), 0.5f * (nd.lo[1] + nd.hi[1]), 0.5f * (nd.lo[2] + nd.hi[2])};
+    float hn[3] = {0.5f * (nd.hi[0] - nd.lo[0]), 0.5f * (nd.hi[1] - nd.lo[1]), 0.5f * (nd.hi[2] - nd.lo[2])};
+    bool hit = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      float wc = Rf[3 * a] * cn[0] + Rf[3 * a + 1] * cn[1] + Rf[3 * a + 2] * cn[2] + cf[a];
+      float wh = fabsf(Rf[3 * a]) * hn[0] + fabsf(Rf[3 * a + 1]) * hn[1] + fabsf(Rf[3 * a + 2]) * hn[2] + eps;
+      if (wc - wh > qhi[a] || wc + wh < qlo[a]) hit = false;
+    }
+    if (!hit) continue;
+    if (nd.left >= 0) {
+      stack[sp++] = nd.left;
+      stack[sp++] = nd.right;
+      continue;
+    }
+    int p0 = -nd.left - 1;
+    for (int k = 0; k < nd.right; ++k) {
+      int prim = d.bvh_prims[p0 + k];
+      int vid[3];
+      if (NIND == 3) { int4 t = d.it[prim]; vid[0] = t.x; vid[1] = t.y; vid[2] = t.z; }
+      else if (NIND == 2) { int2 t = d.ie[prim]; vid[0] = t.x; vid[1] = t.y; }
+      else vid[0] = prim;
+      double lo[3], hi[3];
+      for (int a = 0; a < 3; ++a) {
+        double x = ind_world_exact(R, c, d.Y[vid[0]], a);
+        lo[a] = x; hi[a] = x;
+        for (int j = 1; j < NIND; ++j) {
+          double xj = ind_world_exact(R, c, d.Y[vid[j]], a);
+          lo[a] = fmin(lo[a], xj);
+          hi[a] = fmax(hi[a], xj);
+        }
+      }
+      bool ok = true;
+      for (int a = 0; a < 3; ++a) {
+        if (gxlo[a] > __dadd_rn(hi[a], r)) ok = false;
+        if (lo[a] > __dadd_rn(gxhi[a], r)) ok = false;
+      }
+      if (!ok) continue;
+      unsigned long long a_id = (kind == 1) ? (unsigned long long)prim : (unsigned long long)gid;
+      unsigned long long b_id = (kind == 1) ? (unsigned long long)gid : (unsigned long long)prim;
+      int slot = atomicAdd(cnt, 1);
+      if (slot < cap) out[slot] = ((unsigned long long)kind << 62) | (a_id << 31) | b_id;
+      else *over = true;
+    }
+  }
+}
+
+__global__ void k_broadphase(Dev d, int masked, double r, unsigned long long* out_override, int* cnt_override,
+                             int cap_override) {
+  int e = blockIdx.y;
+  if (e >= d.E) return;
+  const EnvS& s = d.es[e];
+  if (s.mode != kActive) return;
+  if (masked && !(d.run[e] & 4)) return;
+  __shared__ double R[9], c[3];
+  __shared__ float Rf[9], cf[3];
+  if (threadIdx.x < 9) { R[threadIdx.x] = s.R[threadIdx.x]; Rf[threadIdx.x] = (float)s.R[threadIdx.x]; }
+  if (threadIdx.x < 3) { c[threadIdx.x] = s.c[threadIdx.x]; cf[threadIdx.x] = (float)s.c[threadIdx.x]; }
+  __syncthreads();
+  unsigned long long* out = out_override ? out_override : d.cand + (size_t)e * d.kmax;
+  int* cnt = cnt_override ? cnt_override : d.ncand + e;
+  int cap = out_override ? cap_override : d.kmax;
+  bool over = false;
+  int ntot = d.nsv + d.nse + d.nst;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ntot; i += gridDim.x * blockDim.x) {
+    double lo[3], hi[3];
+    if (i < d.nsv) {
+      int v = d.sv[i];
+      d3 x = gel_pos(d, d.u, v, e);
+      lo[0] = hi[0] = x.x; lo[1] = hi[1] = x.y; lo[2] = hi[2] = x.z;
+      bp_query<1, 3>(d, e, 0, i, nullptr, lo, hi, R, c, Rf, cf, r, d.root_tri, out, cnt, cap, &over);
+    } else if (i < d.nsv + d.nse) {
+      int k = i - d.nsv;
+      int2 ed = d.se[k];
+      d3 x0 = gel_pos(d, d.u, ed.x, e), x1 = gel_pos(d, d.u, ed.y, e);
+      lo[0] = fmin(x0.x, x1.x); hi[0] = fmax(x0.x, x1.x);
+      lo[1] = fmin(x0.y, x1.y); hi[1] = fmax(x0.y, x1.y);
+      lo[2] = fmin(x0.z, x1.z); hi[2] = fmax(x0.z, x1.z);
+      bp_query<2, 2>(d, e, 2, k, nullptr, lo, hi, R, c, Rf, cf, r, d.root_edge, out, cnt, cap, &over);
+    } else {
+      int k = i - d.nsv - d.nse;
+      int4 t = d.st[k];
+      d3 x0 = gel_pos(d, d.u, t.x, e), x1 = gel_pos(d, d.u, t.y, e), x2 = gel_pos(d, d.u, t.z, e);
+      lo[0] = fmin(fmin(x0.x, x1.x), x2.x); hi[0] = fmax(fmax(x0.x, x1.x), x2.x);
+      lo[1] = fmin(fmin(x0.y, x1.y), x2.y); hi[1] = fmax(fmax(x0.y, x1.y), x2.y);
+      lo[2] = fmin(fmin(x0.z, x1.z), x2.z); hi[2] = fmax(fmax(x0.z, x1.z), x2.z);
+      bp_query<3, 1>(d, e, 1, k, nullptr, lo, hi, R, c, Rf, cf, r, d.root_vert, out, cnt, cap, &over);
+    }
+  }
+  if (over && !out_override) d.es[e].ncand_over = 1;
+}
+
+// ------------------------------------------------------------------ a3: friction anchors
+// pairs with d(x^t) < dhat: lambda = -kappa b'(d), frozen weights, tangent basis (R7)
+__global__ void k_anchors(Dev d, double kappa) {
+  int e = blockIdx.y;
+  if (e >= d.E || d.es[e].mode != kActive) return;
+  const EnvS& s = d.es[e];
+  int n = min(d.ncand[e], d.kmax);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    unsigned long long rec = d.cand[(size_t)e * d.kmax + i];
+    int kind = (int)(rec >> 62), a = (int)((rec >> 31) & 0x7fffffffu), b = (int)(rec & 0x7fffffffu);
+    Corners C = corners_of(d, kind, a, b);
+    d3 z[4];
+    for (int k = 0; k < 4; ++k) z[k] = C.ind[k] ? mv(s.R, ind_body(d, C.id[k])) + ld3(s.c) : gel_pos(d, d.u, C.id[k], e);
+    DR D = pair_dist(kind, z);
+    if (!(D.d < d.dhat) || !(D.d > 0)) continue;
+    d3 rr = mk(0, 0, 0);
+    for (int k = 0; k < 4; ++k) rr = rr + D.w[k] * z[k];
+    d3 nn = (1.0 / D.d) * rr;
+    double ax = fabs(nn.x), ay = fabs(nn.y), az = fabs(nn.z);
+    d3 ee = (ax <= ay && ax <= az) ? mk(1, 0, 0) : (ay <= az ? mk(0, 1, 0) : mk(0, 0, 1));
+    d3 t1 = cross(nn, ee);
+    t1 = (1.0 / nrm(t1)) * t1;
+    d3 t2 = cross(nn, t1);
+    int slot = atomicAdd(d.nanc + e, 1);
+    if (slot >= d.amax) { d.es[e].ncand_over = 1; continue; }
+    Anchor A;
+    A.kind = kind; A.a = a; A.b = b; A.pad = 0;
+    for (int k = 0; k < 4; ++k) A.w[k] = (float)D.w[k];
+    A.t1[0] = t1.x; A.t1[1] = t1.y; A.t1[2] = t1.z;
+    A.t2[0] = t2.x; A.t2[1] = t2.y; A.t2[2] = t2.z;
+    A.lam = (float)fmax(0.0, -kappa * bar_db(D.d, d.dhat));
+    A.pad2 = 0;
+    d.anc[(size_t)e * d.amax + slot] = A;
+  }
+}
+
+// ------------------------------------------------------------------ a4: vertex pre-pass
+// applies the pending update u += dalpha p (a8), then the inertia term
+// 1/2 m |u - u^|^2, g = m (u - u^), D = m I (lumped M)
+__global__ void k_vert_pre(Dev d) {
+  int e = blockIdx.x * 32 + threadIdx.x;
+  bool act = e < d.E && (d.run[e] & 1);
+  if (!__any_sync(0xffffffffu, act)) return;
+  float da = act ? d.dalpha[e] : 0.f;
+  double ein = 0;
+  for (int v = blockIdx.y * 8 + threadIdx.y; v < d.nv; v += gridDim.y * 8) {
+    if (!act) continue;
+    if (d.vflag[v] & 1) continue;
+    float m = d.mass[v];
+    float gg[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      size_t i = vidx(d, c, v, e);
+      float u = d.u[i];
+      if (da != 0.f) {
+        u = u + da * d.p[i];
+        d.u[i] = u;
+      }
+      float du = u - d.uh[i];
+      gg[c] = m * du;
+      ein += 0.5 * (double)m * (double)du * (double)du;
+      d.g[i] = gg[c];
+    }
+    d.D[vidx(d, 0, v, e)] = m;
+    d.D[vidx(d, 1, v, e)] = m;
+    d.D[vidx(d, 2, v, e)] = m;
+    d.D[vidx(d, 3, v, e)] = 0.f;
+    d.D[vidx(d, 4, v, e)] = 0.f;
+    d.D[vidx(d, 5, v, e)] = 0.f;
+  }
+  if (act && ein != 0.0) atomicAdd(d.acc + (size_t)A_EIN * d.Es + e, ein);
+}
+
+// ------------------------------------------------------------------ a4: element gradient
+// Stable Neo-Hookean (R1) on displacements: G = sum_k (u_k - u_0) b_k^T, F = I + G,
+//   Psi = mu (|G|^2/2 - i2(G) - det G) + lambda'/2 (J-1)^2,  J-1 = trG + i2 + detG
+//   P = mu (G + G^T - trG I - cof G) + lambda'(J-1) cof F
+//   f_k = h^2 V P b_k,  D_kk += h^2 V (mu |b_k|^2 I + lambda' c_k c_k^T),  c_k = cof(F) b_k
+// (cancellation-free forms of Psi, P; App. B diagonal blocks, exact and PSD)
+struct TetData {
+  float b[3][3];
+  float vol;
+};
+__device__ __forceinline__ TetData load_tet(const Dev& d, int t) {
+  TetData T;
+  float4 r0 = __ldg(d.tetb + 3 * t), r1 = __ldg(d.tetb + 3 * t + 1), r2 = __ldg(d.tetb + 3 * t + 2);
+  T.b[0][0] = r0.x; T.b[0][1] = r0.y; T.b[0][2] = r0.z; T.vol = r0.w;
+  T.b[1][0] = r1.x; T.b[1][1] = r1.y; T.b[1][2] = r1.z;
+  T.b[2][0] = r2.x; T.b[2][1] = r2.y; T.b[2][2] = r2.z;
+  return T;
+}
+__device__ __forceinline__ void cof33(const float* A, float* C) {
+  C[0] = A[4] * A[8] - A[5] * A[7]; C[1] = A[5] * A[6] - A[3] * A[8]; C[2] = A[3] * A[7] - A[4] * A[6];
+  C[3] = A[2] * A[7] - A[1] * A[8]; C[4] = A[0] * A[8] - A[2] * A[6]; C[5] = A[1] * A[6] - A[0] * A[7];
+  C[6] = A[1] * A[5] - A[2] * A[4]; C[7] = A[2] * A[3] - A[0] * A[5]; C[8] = A[0] * A[4] - A[1] * A[3];
+}
+
+__global__ void __launch_bounds__(256) k_elem_grad(Dev d, float h2) {
+  int e = blockIdx.x * 32 + threadIdx.x;
+  bool act = e < d.E && (d.run[e] & 1);
+  if (!__any_sync(0xffffffffu, act)) return;
+  const float mu = d.mu, l2 = d.lam2;
+  double esum = 0;
+  for (int t = blockIdx.y * 8 + threadIdx.y; t < d.nt; t += gridDim.y * 8) {
+    int4 tv = __ldg(d.tets + t);
+    int vv[4] = {tv.x, tv.y, tv.z, tv.w};
+    TetData T = load_tet(d, t);
+    if (!act) continue;
+    float uu[4][3];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) uu[k][c] = d.u[vidx(d, c, vv[k], e)];
+    float G[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        float s = 0.f;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) s = fmaf(uu[k + 1][i] - uu[0][i], T.b[k][j], s);
+        G[3 * i + j] = s;
+      }
+    float trG = G[0] + G[4] + G[8];
+    float i2 = (G[0] * G[4] - G[1] * G[3]) + (G[0] * G[8] - G[2] * G[6]) + (G[4] * G[8] - G[5] * G[7]);
+    float cG[9];
+    cof33(G, cG);
+    float detG = G[0] * cG[0] + G[1] * cG[1] + G[2] * cG[2];
+    float Jm1 = trG + i2 + detG;
+    float GG = 0.f;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) GG = fmaf(G[i], G[i], GG);
+    float w = h2 * T.vol;
+    float psi = mu * (0.5f * GG - i2 - detG) + 0.5f * l2 * Jm1 * Jm1;
+    esum += (double)(w * psi);
+    // cof F = (1 + trG) I - G^T + cof G
+    float cF[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) cF[3 * i + j] = (i == j ? 1.f + trG : 0.f) - G[3 * j + i] + cG[3 * i + j];
+    float PK[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        PK[3 * i + j] = mu * (G[3 * i + j] + G[3 * j + i] - (i == j ? trG : 0.f) - cG[3 * i + j]) + l2 * Jm1 * cF[3 * i + j];
+    float f[4][3], cv[4][3], bb[4];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) { f[0][c] = 0.f; cv[0][c] = 0.f; }
+    float b0[3] = {-(T.b[0][0] + T.b[1][0] + T.b[2][0]), -(T.b[0][1] + T.b[1][1] + T.b[2][1]),
+                   -(T.b[0][2] + T.b[1][2] + T.b[2][2])};
+    bb[0] = b0[0] * b0[0] + b0[1] * b0[1] + b0[2] * b0[2];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      bb[k + 1] = T.b[k][0] * T.b[k][0] + T.b[k][1] * T.b[k][1] + T.b[k][2] * T.b[k][2];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        float fi = w * (PK[3 * i] * T.b[k][0] + PK[3 * i + 1] * T.b[k][1] + PK[3 * i + 2] * T.b[k][2]);
+        float ci = cF[3 * i] * T.b[k][0] + cF[3 * i + 1] * T.b[k][1] + cF[3 * i + 2] * T.b[k][2];
+        f[k + 1][i] = fi;
+        cv[k + 1][i] = ci;
+        f[0][i] -= fi;
+        cv[0][i] -= ci;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int v = vv[k];
+      if (d.vflag[v] & 1) continue;
+      atomicAdd(d.g + vidx(d, 0, v, e), f[k][0]);
+      atomicAdd(d.g + vidx(d, 1, v, e), f[k][1]);
+      atomicAdd(d.g + vidx(d, 2, v, e), f[k][2]);
+      float a = w * mu * bb[k], lc = w * l2;
+      atomicAdd(d.D + vidx(d, 0, v, e), a + lc * cv[k][0] * cv[k][0]);
+      atomicAdd(d.D + vidx(d, 1, v, e), a + lc * cv[k][1] * cv[k][1]);
+      atomicAdd(d.D + vidx(d, 2, v, e), a + lc * cv[k][2] * cv[k][2]);
+      atomicAdd(d.D + vidx(d, 3, v, e), lc * cv[k][0] * cv[k][1]);
+      atomicAdd(d.D + vidx(d, 4, v, e), lc * cv[k][0] * cv[k][2]);
+      atomicAdd(d.D + vidx(d, 5, v, e), lc * cv[k][1] * cv[k][2]);
+    }
+  }
+  if (act) atomicAdd(d.acc + (size_t)A_EEL * d.Es + e, esum);
+}
+
+// ------------------------------------------------------------------ a5: contact gradient
+// barrier kappa b(d) over candidates with d < dhat, Gauss-Newton diagonal
+// kappa b'' w_k^2 n n^T (R8); friction mu_f lambda f(|T^T Delta|) over anchors
+// with GN diagonal mu lambda f1 w_k^2 T T^T; indenter corners reduce to the
+// rigid wrench (g_c += f, g_theta += (y - c) x f).
+__device__ __forceinline__ void add_sym(double* A, d3 a, double s) {  // A(6) += s a a^T
+  A[0] += s * a.x * a.x; A[1] += s * a.y * a.y; A[2] += s * a.z * a.z;
+  A[3] += s * a.x * a.y; A[4] += s * a.x * a.z; A[5] += s * a.y * a.z;
+}
+__device__ __forceinline__ void scatter_gel(const Dev& d, int v, int e, d3 f, double s, d3 n) {
+  if (d.vflag[v] & 1) return;
+  atomicAdd(d.g + vidx(d, 0, v, e), (float)f.x);
+  atomicAdd(d.g + vidx(d, 1, v, e), (float)f.y);
+  atomicAdd(d.g + vidx(d, 2, v, e), (float)f.z);
+  if (s != 0.0) {
+    atomicAdd(d.D + vidx(d, 0, v, e), (float)(s * n.x * n.x));
+    atomicAdd(d.D + vidx(d, 1, v, e), (float)(s * n.y * n.y));
+    atomicAdd(d.D + vidx(d, 2, v, e), (float)(s * n.z * n.z));
+    atomicAdd(d.D + vidx(d, 3, v, e), (float)(s * n.x * n.y));
+    atomicAdd(d.D + vidx(d, 4, v, e), (float)(s * n.x * n.z));
+    atomicAdd(d.D + vidx(d, 5, v, e), (float)(s * n.y * n.z));
+  }
+}
+
+
+__global__ void __launch_bounds__(128) k_contact_grad(Dev d, double kappa, double eps_f) {
+  int e = blockIdx.y;
+  if (e >= d.E || !(d.run[e] & 1)) return;
+  const EnvS& s = d.es[e];
+  __shared__ double R[9], c[3], Rt[9], ct[3];
+  __shared__ double sm[32];
+  if (threadIdx.x < 9) { R[threadIdx.x] = s.R[threadIdx.x]; Rt[threadIdx.x] = s.Rt[threadIdx.x]; }
+  if (threadIdx.x < 3) { c[threadIdx.x] = s.c[threadIdx.x]; ct[threadIdx.x] = s.ct[threadIdx.x]; }
+  __syncthreads();
+  double Eb = 0, Ef = 0, gr[6] = {0, 0, 0, 0, 0, 0}, Dc[6] = {0, 0, 0, 0, 0, 0}, Dt[6] = {0, 0, 0, 0, 0, 0};
+  d3 cc = ld3(c);
+  int n = min(d.ncand[e], d.kmax);
+  int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    unsigned long long rec = d.cand[(size_t)e * d.kmax + i];
+    int kind = (int)(rec >> 62), a = (int)((rec >> 31) & 0x7fffffffu), b = (int)(rec & 0x7fffffffu);
+    Corners C = corners_of(d, kind, a, b);
+    d3 z[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) z[k] = C.ind[k] ? mv(R, ind_body(d, C.id[k])) + cc : gel_pos(d, d.u, C.id[k], e);
+    DR D = pair_dist(kind, z);
+    if (!(D.d > 0)) { Eb = INFINITY; continue; }
+    if (D.d >= d.dhat) continue;
+    d3 rr = mk(0, 0, 0);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) rr = rr + D.w[k] * z[k];
+    d3 nn = (1.0 / D.d) * rr;
+    Eb += kappa * bar_b(D.d, d.dhat);
+    double db = kappa * bar_db(D.d, d.dhat), ddb = kappa * bar_ddb(D.d, d.dhat);
+    double sig = 0;
+    d3 rho = mk(0, 0, 0);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      d3 f = (db * D.w[k]) * nn;
+      if (!C.ind[k]) {
+        scatter_gel(d, C.id[k], e, f, ddb * D.w[k] * D.w[k], nn);
+      } else {
+        d3 arm = z[k] - cc;
+        d3 tq = cross(arm, f);
+        gr[0] += f.x; gr[1] += f.y; gr[2] += f.z; gr[3] += tq.x; gr[4] += tq.y; gr[5] += tq.z;
+        sig += D.w[k];
+        rho = rho + D.w[k] * arm;
+      }
+    }
+    add_sym(Dc, nn, ddb * sig * sig);
+    add_sym(Dt, cross(rho, nn), ddb);
+  }
+  int na = min(d.nanc[e], d.amax);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += stride) {
+    Anchor A = d.anc[(size_t)e * d.amax + i];
+    Corners C = corners_of(d, A.kind, A.a, A.b);
+    d3 Dl = mk(0, 0, 0), z[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      d3 dz;
+      if (C.ind[k]) {
+        d3 y = ind_body(d, C.id[k]);
+        z[k] = mv(R, y) + cc;
+        dz = z[k] - (mv(Rt, y) + ld3(ct));
+      } else {
+        dz = gel_vec(d, d.u, C.id[k], e) - gel_vec(d, d.ut, C.id[k], e);
+      }
+      Dl = Dl + (double)A.w[k] * dz;
+    }
+    d3 t1 = mk(A.t1[0], A.t1[1], A.t1[2]), t2 = mk(A.t2[0], A.t2[1], A.t2[2]);
+    double ta = dot(t1, Dl), tb = dot(t2, Dl);
+    double sn = sqrt(ta * ta + tb * tb);
+    double ml = d.mu_f * (double)A.lam;
+    Ef += ml * moll_f(sn, eps_f);
+    double f1 = ml * moll_f1(sn, eps_f);
+    d3 Tt = ta * t1 + tb * t2;
+    double sig = 0;
+    d3 rho = mk(0, 0, 0);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      double wk = A.w[k];
+      d3 f = (f1 * wk) * Tt;
+      if (!C.ind[k]) {
+        int v = C.id[k];
+        if (d.vflag[v] & 1) continue;
+        atomicAdd(d.g + vidx(d, 0, v, e), (float)f.x);
+        atomicAdd(d.g + vidx(d, 1, v, e), (float)f.y);
+        atomicAdd(d.g + vidx(d, 2, v, e), (float)f.z);
+        double sw = f1 * wk * wk;  // GN: f1 w^2 T T^T (R8)
+        atomicAdd(d.D + vidx(d, 0, v, e), (float)(sw * (t1.x * t1.x + t2.x * t2.x)));
+        atomicAdd(d.D + vidx(d, 1, v, e), (float)(sw * (t1.y * t1.y + t2.y * t2.y)));
+        atomicAdd(d.D + vidx(d, 2, v, e), (float)(sw * (t1.z * t1.z + t2.z * t2.z)));
+        atomicAdd(d.D + vidx(d, 3, v, e), (float)(sw * (t1.x * t1.y + t2.x * t2.y)));
+        atomicAdd(d.D + vidx(d, 4, v, e), (float)(sw * (t1.x * t1.z + t2.x * t2.z)));
+        atomicAdd(d.D + vidx(d, 5, v, e), (float)(sw * (t1.y * t1.z + t2.y * t2.z)));
+      } else {
+        d3 arm = z[k] - cc;
+        d3 tq = cross(arm, f);
+        gr[0] += f.x; gr[1] += f.y; gr[2] += f.z; gr[3] += tq.x; gr[4] += tq.y; gr[5] += tq.z;
+        sig += wk;
+        rho = rho + wk * arm;
+      }
+    }
+    add_sym(Dc, t1, f1 * sig * sig);
+    add_sym(Dc, t2, f1 * sig * sig);
+    add_sym(Dt, cross(rho, t1), f1);
+    add_sym(Dt, cross(rho, t2), f1);
+  }
+  block_sum_atomic(Eb, d.acc + (size_t)A_EB * d.Es + e, sm);
+  block_sum_atomic(Ef, d.acc + (size_t)A_EF * d.Es + e, sm);
+  for (int k = 0; k < 6; ++k) block_sum_atomic(gr[k], d.acc + (size_t)(A_GR + k) * d.Es + e, sm);
+  for (int k = 0; k < 6; ++k) block_sum_atomic(Dc[k], d.acc + (size_t)(A_DR + k) * d.Es + e, sm);
+  for (int k = 0; k < 6; ++k) block_sum_atomic(Dt[k], d.acc + (size_t)(A_DR + 6 + k) * d.Es + e, sm);
+}
+
+// ------------------------------------------------------------------ a8: Armijo accept (per env)
+// E_k = inertia + elastic + barrier + friction + pose spring; accept if
+// E <= E_prev + c1 alpha g^T p + eps_E |E_prev| (R14); otherwise halve alpha from x_k,
+// after max_halvings go back to x_k and restart along -P g.
+__device__ void sym6_to_9(const double* a, double* M) {
+  M[0] = a[0]; M[4] = a[1]; M[8] = a[2];
+  M[1] = M[3] = a[3]; M[2] = M[6] = a[4]; M[5] = M[7] = a[5];
+}
+__device__ void apply_pose(EnvS& s, double a) {  // (c, R) = (c_p + a p_c, exp([a p_theta]) R_p)
+  for (int i = 0; i < 3; ++i) s.c[i] = s.cp[i] + a * s.pr[i];
+  double Q[9];
+  rodrigues(a * mk(s.pr[3], s.pr[4], s.pr[5]), Q);
+  mm3(Q, s.Rp, s.R);
+}
+
+__global__ void k_accept(Dev d, double h) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= d.E || !(d.run[e] & 1)) return;
+  EnvS& s = d.es[e];
+  double* A = d.acc;
+  size_t Es = d.Es;
+  double h2 = h * h;
+  d3 dc = ld3(s.c) - ld3(s.cs);
+  double RRs[9];
+  mmT(s.R, s.Rs, RRs);
+  d3 phi = so3_log(RRs);
+  double wt = spring_w(nrm(dc), d.k_t, d.f_max), wr = spring_w(nrm(phi), d.k_r, d.t_max);
+  double Eb = A[A_EB * Es + e];
+  double E = A[A_EIN * Es + e] + A[A_EEL * Es + e] + Eb + A[A_EF * Es + e] +
+             h2 * (spring_e(nrm(dc), d.k_t, d.f_max) + spring_e(nrm(phi), d.k_r, d.t_max));
+  double gr[6], Dc6[6], Dt6[6];
+  for (int k = 0; k < 6; ++k) gr[k] = A[(A_GR + k) * Es + e];
+  for (int k = 0; k < 6; ++k) { Dc6[k] = A[(A_DR + k) * Es + e]; Dt6[k] = A[(A_DR + 6 + k) * Es + e]; }
+  s.Ep[0] = A[A_EIN * Es + e]; s.Ep[1] = A[A_EEL * Es + e]; s.Ep[2] = Eb; s.Ep[3] = A[A_EF * Es + e];
+  s.Ep[4] = h2 * (spring_e(nrm(dc), d.k_t, d.f_max) + spring_e(nrm(phi), d.k_r, d.t_max));
+  for (int k = 0; k < 28; ++k) A[k * Es + e] = 0.0;
+  gr[0] += h2 * wt * dc.x; gr[1] += h2 * wt * dc.y; gr[2] += h2 * wt * dc.z;
+  gr[3] += h2 * wr * phi.x; gr[4] += h2 * wr * phi.y; gr[5] += h2 * wr * phi.z;
+  for (int k = 0; k < 3; ++k) { Dc6[k] += h2 * wt; Dt6[k] += h2 * wr; }
+  s.iter += 1;
+  d.dalpha[e] = 0.f;
+  bool first = (s.iter == 1);
+  if (first && !isfinite(E)) {  // infeasible / NaN at the step start: roll back
+    s.flags |= isfinite(Eb) ? 4 : 8;
+    s.mode = kDone;
+    d.run[e] = 0;
+    return;
+  }
+  bool ok = first || s.reeval || (isfinite(E) && E <= s.E + d.c1 * s.alpha * s.gp_prev + d.eps_E * fabs(s.E));
+  if (ok) {
+    s.E = E;
+    for (int k = 0; k < 6; ++k) s.gr[k] = gr[k];
+    sym6_to_9(Dc6, s.Dc);
+    sym6_to_9(Dt6, s.Dth);
+    s.halv = 0;
+    s.reeval = 0;
+    s.accepted = 1;
+    d.run[e] = 2;
+    return;
+  }
+  s.accepted = 0;
+  s.halv += 1;
+  if (s.halv <= d.max_halv) {
+    double an = 0.5 * s.alpha;
+    d.dalpha[e] = (float)(an - s.alpha);
+    s.alpha = an;
+    apply_pose(s, an);
+  } else {
+    d.dalpha[e] = (float)(-s.alpha);
+    s.alpha = 0;
+    for (int i = 0; i < 3; ++i) s.c[i] = s.cp[i];
+    for (int i = 0; i < 9; ++i) s.R[i] = s.Rp[i];
+    s.restart = 1;
+    s.reeval = 1;
+    s.halv = 0;
+  }
+  d.run[e] = 1;
+}
+
+// ------------------------------------------------------------------ a6: direction
+// P = 3x3 block inverse (default) or scalar Jacobi diag(H)^-1 (R9)
+__device__ __forceinline__ void precond(const float* D, int scalar, const float* x, float* y) {
+  if (scalar) {
+    y[0] = x[0] / D[0]; y[1] = x[1] / D[1]; y[2] = x[2] / D[2];
+    return;
+  }
+  // D = [xx xy xz; xy yy yz; xz yz zz] stored (xx, yy, zz, xy, xz, yz)
+  float a = D[0], b = D[1], c = D[2], xy = D[3], xz = D[4], yz = D[5];
+  float c00 = b * c - yz * yz, c01 = xz * yz - xy * c, c02 = xy * yz - b * xz;
+  float c11 = a * c - xz * xz, c12 = xy * xz - a * yz, c22 = a * b - xy * xy;
+  float inv = 1.f / (a * c00 + xy * c01 + xz * c02);
+  y[0] = inv * (c00 * x[0] + c01 * x[1] + c02 * x[2]);
+  y[1] = inv * (c01 * x[0] + c11 * x[1] + c12 * x[2]);
+  y[2] = inv * (c02 * x[0] + c12 * x[1] + c22 * x[2]);
+}
+
+__global__ void __launch_bounds__(256) k_dir_reduce(Dev d) {
+  int e = blockIdx.x * 32 + threadIdx.x;
+  bool act = e < d.E && (d.run[e] & 2);
+  if (!__any_sync(0xffffffffu, act)) return;
+  double gPy = 0, yp = 0, yPy = 0, pg = 0, gPg = 0, gg = 0, pp = 0;
+  float pgmax = 0.f;
+  for (int v = blockIdx.y * 8 + threadIdx.y; v < d.nv; v += gridDim.y * 8) {
+    if (!act || (d.vflag[v] & 1)) continue;
+    float g[3], gq[3], p[3], D[6], y[3], Pg[3], Py[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      g[c] = d.g[vidx(d, c, v, e)];
+      gq[c] = d.gp[vidx(d, c, v, e)];
+      p[c] = d.p[vidx(d, c, v, e)];
+      y[c] = g[c] - gq[c];
+    }
+#pragma unroll
+    for (int c = 0; c < 6; ++c) D[c] = d.D[vidx(d, c, v, e)];
+    precond(D, d.precond, g, Pg);
+    precond(D, d.precond, y, Py);
+    gPy += g[0] * Py[0] + g[1] * Py[1] + g[2] * Py[2];
+    yp += y[0] * p[0] + y[1] * p[1] + y[2] * p[2];
+    yPy += y[0] * Py[0] + y[1] * Py[1] + y[2] * Py[2];
+    pg += p[0] * g[0] + p[1] * g[1] + p[2] * g[2];
+    gPg += g[0] * Pg[0] + g[1] * Pg[1] + g[2] * Pg[2];
+    gg += g[0] * g[0] + g[1] * g[1] + g[2] * g[2];
+    pp += p[0] * p[0] + p[1] * p[1] + p[2] * p[2];
+    pgmax = fmaxf(pgmax, sqrtf(Pg[0] * Pg[0] + Pg[1] * Pg[1] + Pg[2] * Pg[2]));
+  }
+  // reduce over threadIdx.y in shared memory, one atomic per (block, env)
+  __shared__ double sm[8][8][32];
+  __shared__ float smx[8][32];
+  double vals[7] = {gPy, yp, yPy, pg, gPg, gg, pp};
+  for (int k = 0; k < 7; ++k) sm[k][threadIdx.y][threadIdx.x] = vals[k];
+  smx[threadIdx.y][threadIdx.x] = pgmax;
+  __syncthreads();
+  if (threadIdx.y == 0 && act) {
+    for (int k = 0; k < 7; ++k) {
+      double s = 0;
+      for (int j = 0; j < 8; ++j) s += sm[k][j][threadIdx.x];
+      atomicAdd(d.acc + (size_t)(A_DOT + k) * d.Es + e, s);
+    }
+    float m = 0.f;
+    for (int j = 0; j < 8; ++j) m = fmaxf(m, smx[j][threadIdx.x]);
+    atomic_max_pos(d.accu + (size_t)U_PGMAX * d.Es + e, m);
+  }
+}
+
+__device__ void rigid_P(const EnvS& s, int scalar, const double* x, double* y) {  // blockdiag(Dc, Dth)^-1 x
+  for (int b = 0; b < 2; ++b) {
+    const double* M = b == 0 ? s.Dc : s.Dth;
+    const double* xx = x + 3 * b;
+    double* yy = y + 3 * b;
+    if (scalar) {
+      for (int i = 0; i < 3; ++i) yy[i] = xx[i] / M[4 * i];
+      continue;
+    }
+    double c00 = M[4] * M[8] - M[5] * M[7], c01 = M[5] * M[6] - M[3] * M[8], c02 = M[3] * M[7] - M[4] * M[6];
+    double c11 = M[0] * M[8] - M[2] * M[6], c12 = M[2] * M[3] - M[0] * M[5], c22 = M[0] * M[4] - M[1] * M[3];
+    double inv = 1.0 / (M[0] * c00 + M[1] * c01 + M[2] * c02);
+    yy[0] = inv * (c00 * xx[0] + c01 * xx[1] + c02 * xx[2]);
+    yy[1] = inv * (c01 * xx[0] + c11 * xx[1] + c12 * xx[2]);
+    yy[2] = inv * (c02 * xx[0] + c12 * xx[1] + c22 * xx[2]);
+  }
+}
+
+// per env: convergence on |P g|_disp (R17), Dai-Kou beta with restarts (R13),
+// rigid part of the direction
+__global__ void k_dir_scalar(Dev d) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= d.E || !(d.run[e] & 2)) return;
+  EnvS& s = d.es[e];
+  size_t Es = d.Es;
+  double dt[7];
+  for (int k = 0; k < 7; ++k) { dt[k] = d.acc[(A_DOT + k) * Es + e]; d.acc[(A_DOT + k) * Es + e] = 0.0; }
+  float pgmax = __uint_as_float(d.accu[U_PGMAX * Es + e]);
+  d.accu[U_PGMAX * Es + e] = 0u;
+  double Pg[6], y[6], Py[6];
+  rigid_P(s, d.precond, s.gr, Pg);
+  for (int k = 0; k < 6; ++k) y[k] = s.gr[k] - s.grp[k];
+  rigid_P(s, d.precond, y, Py);
+  for (int k = 0; k < 6; ++k) {
+    dt[0] += s.gr[k] * Py[k];
+    dt[1] += y[k] * s.pr[k];
+    dt[2] += y[k] * Py[k];
+    dt[3] += s.pr[k] * s.gr[k];
+    dt[4] += s.gr[k] * Pg[k];
+    dt[5] += s.gr[k] * s.gr[k];
+    dt[6] += s.pr[k] * s.pr[k];
+  }
+  double pgd = fmax((double)pgmax, nrm(mk(Pg[0], Pg[1], Pg[2])) + d.rho_max * nrm(mk(Pg[3], Pg[4], Pg[5])));
+  s.pg = pgd;
+  if (d.fixed_iters == 0) {
+    if (pgd <= d.tol_x) {
+      s.mode = kDone; s.flags |= 1; d.run[e] = 0;
+      return;
+    }
+    if (pgd < s.best_pg * (1 - 1e-3)) { s.best_pg = pgd; s.best_it = s.iter; }
+    if (d.stagnation > 0 && s.iter - s.best_it > d.stagnation) {
+      s.mode = kDone; s.flags |= 64; d.run[e] = 0;
+      return;
+    }
+  }
+  double gPy = dt[0], yp = dt[1], yPy = dt[2], pg = dt[3], gPg = dt[4], gg = dt[5], pp = dt[6];
+  bool rs = s.restart || s.iter == 1;
+  double beta = 0;
+  if (!rs) {
+    if (fabs(yp) <= 1e-30 * sqrt(gg) * sqrt(pp)) rs = true;
+    else if (d.beta_rule == 1) beta = fmax(0.0, gPy / s.gPg_prev);
+    else if (d.beta_rule == 2) beta = gPg / s.gPg_prev;
+    else beta = gPy / yp - (yPy / yp) * (pg / yp);
+    if (!isfinite(beta)) rs = true;
+  }
+  if (rs) beta = 0;
+  double gp = -gPg + beta * pg;
+  if (gp >= 0) { beta = 0; gp = -gPg; }
+  s.restart = 0;
+  s.beta = beta;
+  d.beta[e] = (float)beta;
+  s.gp_prev = gp;
+  s.gPg_prev = gPg;
+  for (int k = 0; k < 6; ++k) {
+    s.pr[k] = -Pg[k] + (beta != 0 ? beta * s.pr[k] : 0.0);
+    s.grp[k] = s.gr[k];
+  }
+  d.pcf[e] = make_float4((float)s.pr[0], (float)s.pr[1], (float)s.pr[2], 0.f);
+}
+
+// p = -P g + beta p_prev; g_prev = g; M = max |p_v|, L_rel = max_surface |p_v - p_c|, inertia p^T M p
+__global__ void __launch_bounds__(256) k_dir_apply(Dev d) {
+  int e = blockIdx.x * 32 + threadIdx.x;
+  bool act = e < d.E && (d.run[e] & 2);
+  if (!__any_sync(0xffffffffu, act)) return;
+  float beta = act ? d.beta[e] : 0.f;
+  float4 pc = act ? d.pcf[e] : make_float4(0, 0, 0, 0);
+  float M = 0.f, L = 0.f;
+  double q = 0;
+  for (int v = blockIdx.y * 8 + threadIdx.y; v < d.nv; v += gridDim.y * 8) {
+    unsigned char fl = d.vflag[v];
+    if (!act || (fl & 1)) continue;
+    float g[3], D[6], Pg[3], p[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) g[c] = d.g[vidx(d, c, v, e)];
+#pragma unroll
+    for (int c = 0; c < 6; ++c) D[c] = d.D[vidx(d, c, v, e)];
+    precond(D, d.precond, g, Pg);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      size_t i = vidx(d, c, v, e);
+      p[c] = beta != 0.f ? -Pg[c] + beta * d.p[i] : -Pg[c];
+      d.p[i] = p[c];
+      d.gp[i] = g[c];
+    }
+    float pn = sqrtf(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
+    M = fmaxf(M, pn);
+    if (fl & 2) {
+      float a = p[0] - pc.x, b = p[1] - pc.y, c = p[2] - pc.z;
+      L = fmaxf(L, sqrtf(a * a + b * b + c * c));
+    }
+    q += (double)d.mass[v] * (double)(pn * pn);
+  }
+  __shared__ double sq[8][32];
+  __shared__ float sM[8][32], sL[8][32];
+  sq[threadIdx.y][threadIdx.x] = q;
+  sM[threadIdx.y][threadIdx.x] = M;
+  sL[threadIdx.y][threadIdx.x] = L;
+  __syncthreads();
+  if (threadIdx.y == 0 && act) {
+    double t = 0;
+    float m = 0.f, l = 0.f;
+    for (int j = 0; j < 8; ++j) { t += sq[j][threadIdx.x]; m = fmaxf(m, sM[j][threadIdx.x]); l = fmaxf(l, sL[j][threadIdx.x]); }
+    atomicAdd(d.acc + (size_t)A_PHP * d.Es + e, t);
+    atomic_max_pos(d.accu + (size_t)U_M * d.Es + e, m);
+    atomic_max_pos(d.accu + (size_t)U_LREL * d.Es + e, l);
+  }
+}
+
+// ------------------------------------------------------------------ a7: curvature
+// p^T H_e p = h^2 V [mu |dF|^2 + lambda' (cof F : dF)^2 + 2 (lambda'(J-1) - mu) F : cof(dF)]  (App. B)
+__global__ void __launch_bounds__(256) k_elem_curv(Dev d, float h2) {
+  int e = blockIdx.x * 32 + threadIdx.x;
+  bool act = e < d.E && (d.run[e] & 2);
+  if (!__any_sync(0xffffffffu, act)) return;
+  const float mu = d.mu, l2 = d.lam2;
+  double qsum = 0;
+  for (int t = blockIdx.y * 8 + threadIdx.y; t < d.nt; t += gridDim.y * 8) {
+    int4 tv = __ldg(d.tets + t);
+    int vv[4] = {tv.x, tv.y, tv.z, tv.w};
+    TetData T = load_tet(d, t);
+    if (!act) continue;
+    float du[3][3], dp[3][3];
+    float u0[3], p0[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) { u0[c] = d.u[vidx(d, c, vv[0], e)]; p0[c] = d.p[vidx(d, c, vv[0], e)]; }
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        du[k][c] = d.u[vidx(d, c, vv[k + 1], e)] - u0[c];
+        dp[k][c] = d.p[vidx(d, c, vv[k + 1], e)] - p0[c];
+      }
+    float G[9], dF[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        float s = 0.f, r = 0.f;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) { s = fmaf(du[k][i], T.b[k][j], s); r = fmaf(dp[k][i], T.b[k][j], r); }
+        G[3 * i + j] = s;
+        dF[3 * i + j] = r;
+      }
+    float trG = G[0] + G[4] + G[8];
+    float i2 = (G[0] * G[4] - G[1] * G[3]) + (G[0] * G[8] - G[2] * G[6]) + (G[4] * G[8] - G[5] * G[7]);
+    float cG[9], cd[9];
+    cof33(G, cG);
+    cof33(dF, cd);
+    float detG = G[0] * cG[0] + G[1] * cG[1] + G[2] * cG[2];
+    float Jm1 = trG + i2 + detG;
+    float dd = 0.f, cfd = 0.f, fcd = 0.f;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        float cF = (i == j ? 1.f + trG : 0.f) - G[3 * j + i] + cG[3 * i + j];
+        float Fij = (i == j ? 1.f : 0.f) + G[3 * i + j];
+        dd = fmaf(dF[3 * i + j], dF[3 * i + j], dd);
+        cfd = fmaf(cF, dF[3 * i + j], cfd);
+        fcd = fmaf(Fij, cd[3 * i + j], fcd);
+      }
+    qsum += (double)(h2 * T.vol * (mu * dd + l2 * cfd * cfd + 2.f * (l2 * Jm1 - mu) * fcd));
+  }
+  if (act) atomicAdd(d.acc + (size_t)A_PHP * d.Es + e, qsum);
+}
+
+// contact curvature (GN, R8) and the conservative step bound alpha_ccd (R15):
+// d(alpha) >= d - alpha l_n, l_n = max_A(-n.dz) + max_B(n.dz) + |p_theta| dhat/4
+__global__ void __launch_bounds__(128) k_contact_curv(Dev d, double kappa, double eps_f, int ccd_only) {
+  int e = blockIdx.y;
+  if (e >= d.E) return;
+  int rb = d.run[e];
+  if (ccd_only ? !(rb & 4) : !(rb & 2)) return;
+  const EnvS& s = d.es[e];
+  __shared__ double R[9], c[3], Rt[9], ct[3], pr[6];
+  __shared__ double sm[32];
+  if (threadIdx.x < 9) { R[threadIdx.x] = s.R[threadIdx.x]; Rt[threadIdx.x] = s.Rt[threadIdx.x]; }
+  if (threadIdx.x < 3) { c[threadIdx.x] = s.c[threadIdx.x]; ct[threadIdx.x] = s.ct[threadIdx.x]; }
+  if (threadIdx.x < 6) pr[threadIdx.x] = s.pr[threadIdx.x];
+  __syncthreads();
+  d3 cc = ld3(c), pc = mk(pr[0], pr[1], pr[2]), pth = mk(pr[3], pr[4], pr[5]);
+  double extra = nrm(pth) * d.dhat * 0.25;
+  double q = 0, amin = INFINITY;
+  int n = min(d.ncand[e], d.kmax);
+  int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    unsigned long long rec = d.cand[(size_t)e * d.kmax + i];
+    int kind = (int)(rec >> 62), a = (int)((rec >> 31) & 0x7fffffffu), b = (int)(rec & 0x7fffffffu);
+    Corners C = corners_of(d, kind, a, b);
+    d3 z[4], dz[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (C.ind[k]) {
+        z[k] = mv(R, ind_body(d, C.id[k])) + cc;
+        dz[k] = pc + cross(pth, z[k] - cc);
+      } else {
+        z[k] = gel_pos(d, d.u, C.id[k], e);
+        dz[k] = gel_vec(d, d.p, C.id[k], e);
+      }
+    }
+    DR D = pair_dist(kind, z);
+    d3 rr = mk(0, 0, 0), dr = mk(0, 0, 0);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { rr = rr + D.w[k] * z[k]; dr = dr + D.w[k] * dz[k]; }
+    d3 nn = (1.0 / D.d) * rr;
+    if (!ccd_only && D.d < d.dhat) {
+      double dn = dot(nn, dr);
+      q += kappa * bar_ddb(D.d, d.dhat) * dn * dn;
+    }
+    double la = -INFINITY, lb = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < C.na) la = fmax(la, -dot(nn, dz[k]));
+      else lb = fmax(lb, dot(nn, dz[k]));
+    }
+    double l = la + lb + extra;
+    if (l > 0) amin = fmin(amin, (1 - d.ccd_s) * D.d / l);
+  }
+  if (!ccd_only) {
+    int na = min(d.nanc[e], d.amax);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += stride) {
+      Anchor A = d.anc[(size_t)e * d.amax + i];
+      Corners C = corners_of(d, A.kind, A.a, A.b);
+      d3 Dl = mk(0, 0, 0), dD = mk(0, 0, 0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        d3 dz, mvz;
+        if (C.ind[k]) {
+          d3 y = ind_body(d, C.id[k]);
+          d3 z = mv(R, y) + cc;
+          dz = z - (mv(Rt, y) + ld3(ct));
+          mvz = pc + cross(pth, z - cc);
+        } else {
+          dz = gel_vec(d, d.u, C.id[k], e) - gel_vec(d, d.ut, C.id[k], e);
+          mvz = gel_vec(d, d.p, C.id[k], e);
+        }
+        Dl = Dl + (double)A.w[k] * dz;
+        dD = dD + (double)A.w[k] * mvz;
+      }
+      d3 t1 = mk(A.t1[0], A.t1[1], A.t1[2]), t2 = mk(A.t2[0], A.t2[1], A.t2[2]);
+      double sn = sqrt(dot(t1, Dl) * dot(t1, Dl) + dot(t2, Dl) * dot(t2, Dl));
+      double ta = dot(t1, dD), tb = dot(t2, dD);
+      q += d.mu_f * (double)A.lam * moll_f1(sn, eps_f) * (ta * ta + tb * tb);
+    }
+    block_sum_atomic(q, d.acc + (size_t)A_PHP * d.Es + e, sm);
+  }
+  // block min of amin
+  amin = warp_min(amin);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = amin;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = INFINITY;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmin(m, sm[w]);
+    if (m < INFINITY) atomic_min_pos(d.accu + (size_t)U_ACCD * d.Es + e, (float)m);
+  }
+}
+
+// ------------------------------------------------------------------ a7/a8: step length (per env)
+// alpha = min(alpha_upper = dhat / (2 |p|_disp), alpha_bar = -g^T p / p^T H p,
+// alpha_ccd (R15)); rebuild the candidates first if S + alpha L_rel > m_r (R16)
+__device__ void commit_alpha(const Dev& d, EnvS& s, int e, double a, double L) {
+  if (!isfinite(a)) a = 0;
+  for (int i = 0; i < 3; ++i) s.cp[i] = s.c[i];
+  for (int i = 0; i < 9; ++i) s.Rp[i] = s.R[i];
+  s.alpha = a;
+  apply_pose(s, a);
+  d.dalpha[e] = (float)a;
+  s.S += a * L;
+  d.run[e] = 1;
+}
+
+__global__ void k_alpha(Dev d, double h, int pass) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= d.E) return;
+  int rb = d.run[e];
+  size_t Es = d.Es;
+  EnvS& s = d.es[e];
+  if (pass == 1) {
+    if (!(rb & 2)) return;
+    double h2 = h * h;
+    d3 pc = mk(s.pr[0], s.pr[1], s.pr[2]), pth = mk(s.pr[3], s.pr[4], s.pr[5]);
+    double Mg = __uint_as_float(d.accu[U_M * Es + e]);
+    double Lg = __uint_as_float(d.accu[U_LREL * Es + e]);
+    double M = fmax(Mg, nrm(pc) + d.rho_max * nrm(pth));
+    double L = fmax(Lg, nrm(pc)) + d.rho_max * nrm(pth);
+    d3 dc = ld3(s.c) - ld3(s.cs);
+    double RRs[9];
+    mmT(s.R, s.Rs, RRs);
+    d3 phi = so3_log(RRs);
+    double q = d.acc[A_PHP * Es + e] + h2 * (spring_w(nrm(dc), d.k_t, d.f_max) * dot(pc, pc) +
+                                             spring_w(nrm(phi), d.k_r, d.t_max) * dot(pth, pth));
+    d.acc[A_PHP * Es + e] = 0.0;
+    d.accu[U_M * Es + e] = 0u;
+    d.accu[U_LREL * Es + e] = 0u;
+    double accd = (double)__uint_as_float(d.accu[U_ACCD * Es + e]);
+    d.accu[U_ACCD * Es + e] = 0x7f800000u;
+    double aup = M > 0 ? d.dhat / (2 * M) : INFINITY;
+    double abar = q > 0 ? -s.gp_prev / q : INFINITY;
+    double a = fmin(aup, fmin(abar, accd));
+    if (s.S + a * L > d.bp_margin) {  // rebuild before moving (O4f)
+      s.alpha = fmin(aup, abar);
+      s.Lrel_last = L;
+      d.ncand[e] = 0;
+      d.run[e] = 2 | 4;
+      return;
+    }
+    commit_alpha(d, s, e, a, L);
+  } else {
+    if (!(rb & 4)) return;
+    double accd = (double)__uint_as_float(d.accu[U_ACCD * Es + e]);
+    d.accu[U_ACCD * Es + e] = 0x7f800000u;
+    s.S = 0;
+    commit_alpha(d, s, e, fmin(s.alpha, accd), s.Lrel_last);
+  }
+}
+
+// ------------------------------------------------------------------ a9: finalize
+__global__ void k_finalize_vert(Dev d, float inv_h) {
+  int e = blockIdx.x * 32 + threadIdx.x;
+  if (e >= d.E) return;
+  bool failed = d.es[e].flags & (4 | 8);
+  float da = d.dalpha[e];
+  for (int v = blockIdx.y * 8 + threadIdx.y; v < d.nv; v += gridDim.y * 8) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      size_t i = vidx(d, c, v, e);
+      float ut = d.ut[i];
+      if (failed) {
+        d.u[i] = ut;
+        d.vt[i] = 0.f;
+        continue;
+      }
+      float u = d.u[i];
+      if (da != 0.f) u += da * d.p[i];
+      d.u[i] = u;
+      d.vt[i] = (u - ut) * inv_h;
+      d.ut[i] = u;
+    }
+  }
+}
+__global__ void k_finalize_env(Dev d) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= d.E) return;
+  EnvS& s = d.es[e];
+  if (s.flags & (4 | 8)) {
+    for (int i = 0; i < 3; ++i) s.c[i] = s.ct[i];
+    for (int i = 0; i < 9; ++i) s.R[i] = s.Rt[i];
+  } else {
+    for (int i = 0; i < 3; ++i) s.ct[i] = s.c[i];
+    for (int i = 0; i < 9; ++i) s.Rt[i] = s.R[i];
+  }
+  if (s.mode == kActive) s.flags |= 2;
+  if (s.ncand_over) s.flags |= 32;
+  s.mode = kDone;
+  d.run[e] = 0;
+  d.dalpha[e] = 0.f;
+  d3 dc = ld3(s.c) - ld3(s.cs);
+  double RRs[9];
+  mmT(s.R, s.Rs, RRs);
+  s.pose_res = nrm(dc) + d.rho_max * nrm(so3_log(RRs));
+}
+
+// ------------------------------------------------------------------ a10: markers
+// u_m = sum_j w_mj u_j; out[e][m] = (u_m.t1, u_m.t2[, u_m.n])
+__global__ void k_markers(Dev d, float* out, int ncomp, float4 t1, float4 t2, float4 nn) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= d.E * d.nm) return;
+  int e = i / d.nm, m = i - e * d.nm;
+  int4 id = __ldg(d.mk_idx + m);
+  float4 w = __ldg(d.mk_w + m);
+  int vv[4] = {id.x, id.y, id.z, id.w};
+  float ww[4] = {w.x, w.y, w.z, w.w};
+  float um[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) um[c] = fmaf(ww[k], d.ut[vidx(d, c, vv[k], e)], um[c]);
+  float* o = out + (size_t)i * ncomp;
+  o[0] = um[0] * t1.x + um[1] * t1.y + um[2] * t1.z;
+  o[1] = um[0] * t2.x + um[1] * t2.y + um[2] * t2.z;
+  if (ncomp == 3) o[2] = um[0] * nn.x + um[1] * nn.y + um[2] * nn.z;
+}
+
+__global__ void k_reset_env(Dev d, const unsigned char* mask, const float* poses) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= d.E || !mask[e]) return;
+  EnvS& s = d.es[e];
+  const float* q = poses + 7 * e;
+  for (int i = 0; i < 3; ++i) s.ct[i] = s.c[i] = q[i];
+  quat_R(q, s.Rt);
+  for (int i = 0; i < 9; ++i) s.R[i] = s.Rt[i];
+  s.flags = 0;
+  s.iter = 0;
+  s.pg = 0;
+}
+__global__ void k_reset_vert(Dev d, const unsigned char* mask) {
+  int e = blockIdx.x * 32 + threadIdx.x;
+  if (e >= d.E || !mask[e]) return;
+  for (int v = blockIdx.y * 8 + threadIdx.y; v < d.nv; v += gridDim.y * 8)
+    for (int c = 0; c < 3; ++c) {
+      size_t i = vidx(d, c, v, e);
+      d.u[i] = d.ut[i] = d.vt[i] = d.p[i] = d.gp[i] = 0.f;
+    }
+}
+__global__ void k_status(Dev d, int* iters, float* pg, unsigned* flags) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= d.E) return;
+  if (iters) iters[e] = d.es[e].iter;
+  if (pg) pg[e] = (float)d.es[e].pg;
+  if (flags) flags[e] = (unsigned)d.es[e].flags;
+}
+__global__ void k_any_active(Dev d, int* out) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  int a = (e < d.E && d.es[e].mode == kActive) ? 1 : 0;
+  if (__any_sync(0xffffffffu, a) && (threadIdx.x & 31) == 0) atomicOr(out, 1);
+}
+
+// ------------------------------------------------------------------ launchers
+static dim3 vgrid(const Dev& d, int n) {
+  int gx = d.Es / 32;
+  int gy = (2 * 148 * 8 + gx - 1) / gx;  // ~16 blocks of 256 threads per SM over the grid
+  gy = std::max(1, std::min(gy, (n + 7) / 8));
+  return dim3(gx, gy);
+}
+static dim3 cgrid(const Dev& d) {
+  int nb = std::max(1, std::min(64, 1184 / std::max(1, d.E)));
+  return dim3(nb, d.E);
+}
+static int eblocks(const Dev& d) { return (d.E + 127) / 128; }
+#define LAUNCHK(kid, s, ...)         \
+  do {                                \
+    if (g_prof) prof_begin(kid, s);   \
+    __VA_ARGS__;                      \
+    if (g_prof) prof_end(kid, s);     \
+    ++g_launches;                     \
+  } while (0)
+
+void launch_step_setup(const Dev& d, const float* poses, double h, cudaStream_t s) {
+  LAUNCHK(KID_STEP_SETUP, s, (k_step_setup<<<eblocks(d), 128, 0, s>>>(d, poses)));
+  LAUNCHK(KID_VERT_SETUP, s, (k_vert_setup<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d, (float)h)));
+}
+void launch_vert_setup(const Dev& d, double h, cudaStream_t s) {
+  LAUNCHK(KID_VERT_SETUP, s, (k_vert_setup<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d, (float)h)));
+}
+void launch_broadphase(const Dev& d, bool masked, cudaStream_t s) {
+  int ntot = d.nsv + d.nse + d.nst;
+  int nb = std::max(1, std::min((ntot + 127) / 128, 2368 / std::max(1, d.E)));
+  LAUNCHK(KID_BROADPHASE, s, (k_broadphase<<<dim3(nb, d.E), 128, 0, s>>>(d, masked ? 1 : 0, d.dhat + d.bp_margin, nullptr, nullptr, 0)));
+}
+void launch_anchors(const Dev& d, double h, cudaStream_t s) {
+  LAUNCHK(KID_ANCHORS, s, (k_anchors<<<cgrid(d), 128, 0, s>>>(d, h * h * d.kappa_phys)));
+}
+void launch_eval(const Dev& d, double h, cudaStream_t s) {
+  LAUNCHK(KID_VERT_PRE, s, (k_vert_pre<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d)));
+  LAUNCHK(KID_ELEM_GRAD, s, (k_elem_grad<<<vgrid(d, d.nt), dim3(32, 8), 0, s>>>(d, (float)(h * h))));
+  LAUNCHK(KID_CONTACT_GRAD, s, (k_contact_grad<<<cgrid(d), 128, 0, s>>>(d, h * h * d.kappa_phys, d.eps_v * h)));
+  LAUNCHK(KID_ACCEPT, s, (k_accept<<<eblocks(d), 128, 0, s>>>(d, h)));
+}
+void launch_direction(const Dev& d, cudaStream_t s) {
+  LAUNCHK(KID_DIR_REDUCE, s, (k_dir_reduce<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d)));
+  LAUNCHK(KID_DIR_SCALAR, s, (k_dir_scalar<<<eblocks(d), 128, 0, s>>>(d)));
+  LAUNCHK(KID_DIR_APPLY, s, (k_dir_apply<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d)));
+}
+void launch_curvature(const Dev& d, double h, cudaStream_t s) {
+  LAUNCHK(KID_ELEM_CURV, s, (k_elem_curv<<<vgrid(d, d.nt), dim3(32, 8), 0, s>>>(d, (float)(h * h))));
+  LAUNCHK(KID_CONTACT_CURV, s, (k_contact_curv<<<cgrid(d), 128, 0, s>>>(d, h * h * d.kappa_phys, d.eps_v * h, 0)));
+}
+void launch_alpha(const Dev& d, double h, cudaStream_t s) {
+  LAUNCHK(KID_ALPHA, s, (k_alpha<<<eblocks(d), 128, 0, s>>>(d, h, 1)));
+  launch_broadphase(d, true, s);
+  LAUNCHK(KID_CCD, s, (k_contact_curv<<<cgrid(d), 128, 0, s>>>(d, h * h * d.kappa_phys, d.eps_v * h, 1)));
+  LAUNCHK(KID_ALPHA, s, (k_alpha<<<eblocks(d), 128, 0, s>>>(d, h, 2)));
+}
+void launch_finalize(const Dev& d, double h, cudaStream_t s) {
+  LAUNCHK(KID_FIN_VERT, s, (k_finalize_vert<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d, (float)(1.0 / h))));
+  LAUNCHK(KID_FIN_ENV, s, (k_finalize_env<<<eblocks(d), 128, 0, s>>>(d)));
+}
+void launch_markers(const Dev& d, float* out, int ncomp, cudaStream_t s) {
+  int n = d.E * d.nm;
+  float4 t1 = make_float4(d.t1[0], d.t1[1], d.t1[2], 0), t2 = make_float4(d.t2[0], d.t2[1], d.t2[2], 0),
+         nn = make_float4(d.nrm[0], d.nrm[1], d.nrm[2], 0);
+  LAUNCHK(KID_MARKERS, s, (k_markers<<<(n + 255) / 256, 256, 0, s>>>(d, out, ncomp, t1, t2, nn)));
+}
+void launch_reset(const Dev& d, const unsigned char* mask, const float* poses, cudaStream_t s) {
+  LAUNCHK(KID_OTHER, s, (k_reset_env<<<eblocks(d), 128, 0, s>>>(d, mask, poses)));
+  LAUNCHK(KID_OTHER, s, (k_reset_vert<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d, mask)));
+}
+void launch_status(const Dev& d, int* iters, float* pg, unsigned* flags, cudaStream_t s) {
+  LAUNCHK(KID_OTHER, s, (k_status<<<eblocks(d), 128, 0, s>>>(d, iters, pg, flags)));
+}
+void launch_any_active(const Dev& d, int* out, cudaStream_t s) {
+  LAUNCHK(KID_OTHER, s, (k_any_active<<<eblocks(d), 128, 0, s>>>(d, out)));
+}
+void launch_debug_broadphase(const Dev& d, double r, unsigned long long* out, int* cnt, int cap, cudaStream_t s) {
+  int ntot = d.nsv + d.nse + d.nst;
+  LAUNCHK(KID_BROADPHASE, s, (k_broadphase<<<dim3((ntot + 127) / 128, d.E), 128, 0, s>>>(d, 0, r, out, cnt, cap)));
+}
+int launches_per_iteration() { return 4 + 3 + 2 + 4; }
+
+}  // namespace tac

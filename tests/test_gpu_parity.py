@@ -1,0 +1,197 @@
+"""CUDA path vs the fp64 oracle, through the C ABI (SURVEY §8c gates).
+
+Bars (BASELINE north_star):
+  * broad-phase candidate sets: bit-exact on identical fp32 inputs;
+  * marker -> tet indices: bit-exact;
+  * kernel level on identical inputs: gradient and diagonal blocks <= 1e-5 relative;
+  * converged steps: marker displacement within 1e-3 of the max marker displacement
+    (relative L-inf), gel positions within 1e-4 of the pad size.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as w
+from helpers import c1_press_scene, rot_exp
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _sim(scene, **kw):
+    import paper_2603_28475_b200 as P
+    return P.TacSim.from_scene(scene, **kw)
+
+
+def _canon(pairs, surf, tris):
+    """Map (kind, a, b) to vertex-id keys so both sides' numbering can differ."""
+    sv, se, st, ie = surf
+    out = set()
+    for k, a, b in pairs:
+        if k == 0:
+            out.add((0, int(sv[a]), tuple(sorted(tris[b]))))
+        elif k == 1:
+            out.add((1, int(a), tuple(sorted(st[b]))))
+        else:
+            out.add((2, tuple(sorted(se[a])), tuple(sorted(ie[b]))))
+    return out
+
+
+def _pressed_state():
+    s = c1_press_scene(mu_f=1.0, steps=4, depth=0.25e-3)
+    s.params.tol_x = 1e-10
+    o = O.Oracle(s)
+    for k in range(3):
+        o.step(s.poses[k])
+    st = o.get_state(0)
+    o.step(s.poses[3])
+    u, _, c, R = o.get_state(0)
+    rng = np.random.default_rng(5)
+    u = u + 2e-7 * rng.standard_normal(u.shape)
+    u[s.fixed] = 0
+    u = u.astype(np.float32).astype(np.float64)  # identical fp32 inputs on both sides
+    c = c + 1e-7 * rng.standard_normal(3)
+    R = rot_exp(1e-5 * rng.standard_normal(3)) @ R
+    tgt = s.poses[3][0].copy()
+    tgt[2] -= 2e-5
+    return s, o, st, (u, c, R), tgt
+
+
+def test_marker_map_bitexact(torch_cuda):
+    for scene in (w.scene_c1(), w.scene_c2(steps=1)):
+        sim = _sim(scene)
+        o = O.Oracle(scene)
+        t1, i1, w1 = sim.debug_marker_map()
+        t2, i2, w2 = o.marker_map()
+        assert np.array_equal(t1, t2)
+        assert np.array_equal(i1, i2)
+        assert np.abs(w1 - w2).max() < 1e-12
+
+
+def test_surface_matches(torch_cuda):
+    s = w.scene_c1()
+    sim = _sim(s)
+    o = O.Oracle(s)
+    for a, b in zip(sim.debug_surface(), o.surface()):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
+
+
+@pytest.mark.parametrize("case", ["c1_pressed", "peg_c2_mesh"])
+def test_broadphase_bitexact(torch_cuda, case):
+    if case == "c1_pressed":
+        s, o, _, (u, c, R), _ = _pressed_state()
+        states = [(u, c, R)]
+    else:
+        s = w.scene_c3(n_envs=3, n_steps=8)
+        o = O.Oracle(s)
+        rng = np.random.default_rng(1)
+        states = []
+        for e in range(3):
+            p = s.poses[6, e]
+            R = O.quat_to_R(p)
+            c = p[:3].astype(np.float64) + np.array([0, 0, 0.35e-3])
+            u = np.zeros_like(s.X)
+            u[:, 2] = -2e-4 * np.exp(-((s.X[:, 0] - c[0]) ** 2 + (s.X[:, 1] - c[1]) ** 2) / (3e-3) ** 2)
+            u *= (1 + s.X[:, 2] / 5e-3)[:, None]
+            u += 1e-6 * rng.standard_normal(u.shape)
+            u[s.fixed] = 0
+            states.append((u.astype(np.float32).astype(np.float64), c, R))
+    sim = _sim(s)
+    gsurf = sim.debug_surface()
+    osurf = o.surface()
+    for env, (u, c, R) in enumerate(states):
+        for r in (3e-4, 1e-4):
+            gpu = sim.debug_broadphase(min(env, s.n_envs - 1), u, c, R, r)
+            ref = o.broadphase_state(u, c, R, r)
+            assert len(ref) > 0
+            assert len(gpu) == len(ref)
+            assert _canon(gpu, gsurf, s.tris) == _canon(ref, osurf, s.tris)
+
+
+def test_kernel_parity_gradient_diag(torch_cuda):
+    s, o, (u_t, v_t, c_t, R_t), (u, c, R), tgt = _pressed_state()
+    sim = _sim(s)
+    ut32 = u_t.astype(np.float32).astype(np.float64)
+    vt32 = v_t.astype(np.float32).astype(np.float64)
+    ref = o.eval(ut32, vt32, c_t, R_t, u, c, R, tgt)
+    gpu = sim.debug_eval(0, ut32, vt32, c_t, R_t, u, c, R, tgt, s.dt)
+    free = np.setdiff1d(np.arange(len(u)), s.fixed)
+    g_ref, g_gpu = ref["g"][free], gpu["g"][free]
+    assert np.linalg.norm(g_gpu - g_ref) <= 1e-5 * np.linalg.norm(g_ref)
+    D_ref, D_gpu = ref["D"][free], gpu["D"][free]
+    assert np.abs(D_gpu - D_ref).max() <= 1e-5 * np.abs(D_ref).max()
+    assert np.linalg.norm(gpu["grig"] - ref["grig"]) <= 1e-5 * np.linalg.norm(ref["grig"])
+    for k in range(5):
+        assert abs(gpu["parts"][k] - ref["parts"][k]) <= 1e-5 * abs(ref["E"]) + 1e-30, k
+
+
+def _run_both(scene, steps, tol_gpu=1e-9, tol_or=1e-11):
+    import torch
+    scene.params.tol_x = tol_gpu
+    scene.params.max_iters = 5000
+    scene.params.stagnation = 300
+    sim = _sim(scene)
+    p_or = w.Params(**{**scene.params.__dict__})
+    p_or.tol_x = tol_or
+    p_or.stagnation = 3000
+    o = O.Oracle(scene, params=p_or)
+    E = scene.n_envs
+    mk = torch.empty((E, 63, 2), device="cuda", dtype=torch.float32)
+    for k in range(steps):
+        tgt = torch.tensor(scene.poses[k], dtype=torch.float32, device="cuda").contiguous()
+        sim.step(tgt, scene.dt)
+        o.step(scene.poses[k], threads=min(E, 8))
+    sim.markers(mk)
+    torch.cuda.synchronize()
+    return sim, o, mk.cpu().numpy()
+
+
+def _assert_parity(scene, sim, o, mk, env):
+    u_g, _, c_g, _ = sim.get_state(env)
+    u_o, _, c_o, _ = o.get_state(env)
+    pad = max(scene.extent)
+    assert np.abs(u_g - u_o).max() <= 1e-4 * pad
+    m_o = o.markers(env)
+    scale = np.abs(m_o).max()
+    if scale > 1e-7:
+        assert np.abs(mk[env] - m_o).max() <= 1e-3 * scale
+    assert np.all(u_g[scene.fixed] == 0)
+
+
+def test_converged_step_parity_c1(torch_cuda):
+    s = c1_press_scene(mu_f=1.0, steps=3, depth=0.2e-3)
+    sim, o, mk = _run_both(s, 3)
+    it, pg, fl = sim.env_status()
+    assert int(fl[0]) & 1, int(fl[0])  # converged
+    _assert_parity(s, sim, o, mk, 0)
+
+
+def test_converged_parity_multi_env_ragged(torch_cuda):
+    s = w.scene_small_peg(n_envs=5, n_steps=4)
+    sim, o, mk = _run_both(s, 4)
+    for e in range(s.n_envs):
+        _assert_parity(s, sim, o, mk, e)
+
+
+def test_fixed_iteration_mode_runs_and_is_finite(torch_cuda):
+    import torch
+    s = w.scene_small_peg(n_envs=33, n_steps=3)
+    s.params.fixed_iters = 50
+    sim = _sim(s)
+    for k in range(3):
+        sim.step(torch.tensor(s.poses[k], dtype=torch.float32, device="cuda"), s.dt)
+    it, pg, fl = sim.env_status()
+    assert torch.all(it == 50)
+    m = sim.markers()
+    assert torch.isfinite(m).all()
+    for e in (0, 17, 32):
+        u, _, c, R = sim.get_state(e)
+        assert np.all(np.isfinite(u)) and np.all(u[s.fixed] == 0)
+        assert O.Oracle(s).dmin(u, c, R) > 0
