@@ -1,0 +1,337 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the batched PNCG-IPC tactile step (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One "step" = one pass of the whole hot path for every env
+of the rank: tac_step (fixed 50 PNCG iterations, the paper's "tens") +
+tac_markers.  Workload at N=1: BASELINE configs[2] (C3: 1,024 envs of peg-insertion
+trajectories on the 19,800-tet GelSight-Mini-like pad).  N>1 (torchrun): weak scaling,
+1,024 envs per GPU with distinct env ids, plus an NCCL all-gather of the marker fields
+every step (configs[3], C4).  Timing: CUDA events on the stream, barrier + synchronize
+on both sides, max over ranks.  The per-env state (~470 MB/GPU) exceeds the 126 MB L2,
+so no L2 flush is needed between steps.
+
+--impl reference times the fp64 CPU oracle (oracle/) on this host as the reference
+arm (the paper's code is not available).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FIXED_ITERS = 50
+ENVS_PER_GPU = 1024
+METRIC = "env-steps/sec (marker fields/sec) at 1/2/4/8 B200; % of HBM roofline"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws == 1:
+        return 0, 0, 1
+    import torch.distributed as dist
+    rank = int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    import torch
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    return rank, local, ws
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows]
+        load = [s for s in sm if s > 300] or sm
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for n, v in zip(names, r[5:9]):
+                if "Active" in v and "Not" not in v:
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": float(rows[0][2]), "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+# algorithmic work per launch (DESIGN.md §Kernels and roofline)
+def kernel_models(nv_free, nt, E):
+    return {
+        "elem_grad": ("alu", 350.0 * nt * E, "flop", "350 flop per tet-env (SURVEY §8d.2 phase A)"),
+        "elem_curv": ("alu", 140.0 * nt * E, "flop", "140 flop per tet-env (phase C)"),
+        "vert_pre": ("hbm", 84.0 * nv_free * E, "B", "84 B per free vertex-env: read u,p,u^; write u,g,D"),
+        "dir_reduce": ("hbm", 60.0 * nv_free * E, "B", "60 B per free vertex-env: read g,g_prev,p,D"),
+        "dir_apply": ("hbm", 72.0 * nv_free * E, "B", "72 B per free vertex-env: read g,D,p; write p,g_prev"),
+        "finalize_vert": ("hbm", 48.0 * nv_free * E, "B", "48 B per vertex-env"),
+    }
+
+
+def run_ours(args, rank, local, ws):
+    import torch
+    import paper_2603_28475_b200 as P
+    import workloads as w
+
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    nsteps = max(64, args.warmup + args.steps + 1)
+    E = args.envs
+    scene = w.scene_c3(n_envs=E, n_steps=nsteps, seed0=20260000 + rank * E)
+    scene.params.fixed_iters = FIXED_ITERS
+    sim = P.TacSim.from_scene(scene, device=local)
+    poses = torch.tensor(scene.poses, dtype=torch.float32, device=dev).contiguous()  # resident in HBM
+    nm = scene.markers.shape[0]
+    if ws > 1:
+        gather = torch.empty((ws * E, nm, 2), dtype=torch.float32, device=dev)
+        mk = gather[rank * E:(rank + 1) * E]  # tac_markers writes the rank's slot: in-place all-gather
+    else:
+        gather = None
+        mk = torch.empty((E, nm, 2), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def one_step(k):
+        sim.step(poses[k], scene.dt)
+        sim.markers(mk)
+        if gather is not None:
+            import torch.distributed as dist
+            dist.all_gather_into_tensor(gather, mk)
+
+    launches = 0
+    for k in range(args.warmup):
+        one_step(k)
+    torch.cuda.synchronize()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    sim.profile_enable(True)
+    sim.profile_read()
+    clocks = Clocks(local)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for k in range(args.warmup, args.warmup + args.steps):
+        one_step(k)
+        launches += sim.last_launch_count()  # markers call
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    cl = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    prof = sim.profile_read()
+    sim.profile_enable(False)
+    launches = sum(c for _, c in prof.values())
+    if ws > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = ws * E * args.steps / (ms / 1e3)
+
+    # roofline of the dominant kernel (live CUDA-event timing over the timed region)
+    nfree = scene.X.shape[0] - len(scene.fixed)
+    models = kernel_models(nfree, scene.tets.shape[0], E)
+    tot = {k: v for k, v in prof.items() if v[1] > 0}
+    dom = max(tot, key=lambda k: tot[k][0])
+    peaks, src = _peaks()
+    share = {k: round(v[0] / ms, 4) for k, v in sorted(tot.items(), key=lambda kv: -kv[1][0])}
+    dom_model = dom if dom in models else max((k for k in tot if k in models), key=lambda k: tot[k][0])
+    bound, work, wunit, note = models[dom_model]
+    avg_s = tot[dom_model][0] / tot[dom_model][1] / 1e3
+    if bound == "hbm":
+        achieved = work / avg_s / 1e9
+        peak = float(peaks["hbm_gbs"])
+        unit = "GB/s"
+    else:
+        achieved = work / avg_s / 1e12
+        peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+        unit = "TFLOP/s"
+    roof = {"bound": bound, "kernel": dom_model, "achieved": round(achieved, 3), "peak": round(peak, 1),
+            "unit": unit, "frac": round(achieved / peak, 4), "traffic": None,
+            "peak_source": f"{src} ({'MEASURED_PEAKS.json hbm_gbs' if bound == 'hbm' else '148 SM x 128 FP32 lanes x 2 flop x sm_max_mhz'})",
+            "work_per_launch": work, "work_note": note, "avg_launch_us": round(avg_s * 1e6, 2),
+            "dominant_by_time": dom, "share_of_step": share}
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            tr = json.load(open(tfile)).get(dom_model)
+            if tr:
+                roof["traffic"] = tr
+        except Exception:
+            pass
+
+    # e2e through the public API with host buffers (pinned), copies inside the timed region
+    host_poses = torch.tensor(scene.poses, dtype=torch.float32).pin_memory()
+    host_mk = torch.empty((E, nm, 2), dtype=torch.float32).pin_memory()
+    dpose = torch.empty((E, 7), dtype=torch.float32, device=dev)
+    nsteps_e2e = min(args.steps, nsteps - args.warmup - args.steps) if nsteps - args.warmup - args.steps > 0 else args.steps
+    nsteps_e2e = max(1, nsteps_e2e)
+    # reset to the warm state cheaply: continue the trajectory (poses are continuous)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    w0 = time.perf_counter()
+    base = args.warmup + args.steps
+    for j in range(nsteps_e2e):
+        k = min(base + j, nsteps - 1)
+        dpose.copy_(host_poses[k], non_blocking=True)
+        sim.step(dpose, scene.dt)
+        sim.markers(mk)
+        if gather is not None:
+            dist.all_gather_into_tensor(gather, mk)
+        host_mk.copy_(mk, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    w1 = time.perf_counter()
+    e2e_s = w1 - w0
+    if ws > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": round(ws * E * nsteps_e2e / e2e_s, 2), "unit": "env-steps/s",
+           "h2d_bytes_per_step": E * 7 * 4, "d2h_bytes_per_step": E * nm * 2 * 4,
+           "timing": "wall clock, synchronize per step (result read on host)", "steps": nsteps_e2e}
+
+    it, pg, fl = sim.env_status()
+    out = {
+        "metric": METRIC, "value": round(value, 2), "unit": "env-steps/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp64 per-env reductions and rigid DOFs)",
+        "data": "synthetic (seeded generators: workloads/)",
+        "config": {"workload": "C3: 1024 envs/GPU peg-insertion trajectories (press, shear, twist, release), "
+                               "19,800-tet / 4,278-vertex pad, Ø8 mm cylinder peg, 7x9 markers",
+                   "envs_per_gpu": E, "iters_per_step": FIXED_ITERS, "iteration_mode": "fixed",
+                   "parallelism": f"env-sharded dp{ws}" + (" + NCCL all-gather of markers" if ws > 1 else ""),
+                   "l2": "per-env state ~470 MB/GPU > 126 MB L2 (no flush needed)"},
+        "roofline": roof,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": cl,
+        "solver": {"mean_iters": float(it.float().mean()), "flags_or": int(torch.bitwise_or.reduce(fl).item())
+                   if hasattr(torch.bitwise_or, "reduce") else None},
+    }
+    return out, scene, sim
+
+
+def cpu_baseline(scene_envs=None, budget_s=12.0):
+    """The oracle (fp64, one env per thread on all host cores), fixed 50 iterations, on a
+    bounded sample of the C3 workload: 2 x nproc envs, steps until ~budget_s of CPU time."""
+    import oracle as O
+    import workloads as w
+    nproc = os.cpu_count() or 1
+    n = 2 * nproc
+    s = w.scene_c3(n_envs=n, n_steps=64)
+    s.params.fixed_iters = FIXED_ITERS
+    o = O.Oracle(s)
+    t0 = time.perf_counter()
+    steps = 0
+    while steps < 64:
+        o.step(s.poses[steps], threads=nproc)
+        steps += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": round(n * steps / dt, 3), "unit": "env-steps/s", "cores": nproc, "kind": "oracle",
+            "sample": f"C3 workload, {n} envs x {steps} steps (first steps of each trajectory), "
+                      f"{FIXED_ITERS} iterations/step, fp64 C++ oracle, one env per thread"}
+
+
+def run_reference(args, rank, ws):
+    if rank != 0:
+        return None
+    import oracle as O
+    import workloads as w
+    nproc = os.cpu_count() or 1
+    n = nproc
+    s = w.scene_c3(n_envs=n, n_steps=max(64, args.warmup + args.steps))
+    s.params.fixed_iters = FIXED_ITERS
+    o = O.Oracle(s)
+    for k in range(args.warmup):
+        o.step(s.poses[k], threads=nproc)
+    t0 = time.perf_counter()
+    for k in range(args.warmup, args.warmup + args.steps):
+        o.step(s.poses[k], threads=nproc)
+    dt = time.perf_counter() - t0
+    v = n * args.steps / dt
+    return {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "env-steps/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C3 peg-insertion trajectories (bounded sample: one env per host core per step)",
+                       "envs_per_step": n, "iters_per_step": FIXED_ITERS, "iteration_mode": "fixed"},
+            "cpu_baseline": {"value": round(v, 3), "unit": "env-steps/s", "cores": nproc, "kind": "oracle",
+                             "sample": f"{n} envs x {args.steps} steps, {FIXED_ITERS} iterations/step"},
+            "e2e": {"value": round(v, 3), "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--envs", type=int, default=ENVS_PER_GPU)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    assert args.warmup >= 1
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        ws = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+        out = run_reference(args, rank, ws)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    rank, local, ws = _dist()
+    out, scene, sim = run_ours(args, rank, local, ws)
+    if rank == 0:
+        if ws == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline()
+        else:
+            out["cpu_baseline"] = None
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
