@@ -232,6 +232,7 @@ def run_ours(args, rank, local, ws):
            "timing": "wall clock, synchronize per step (result read on host)", "steps": nsteps_e2e}
 
     it, pg, fl = sim.env_status()
+    stt = sim.env_stats().float()
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": "env-steps/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
@@ -246,8 +247,10 @@ def run_ours(args, rank, local, ws):
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": cl,
-        "solver": {"mean_iters": float(it.float().mean()), "flags_or": int(torch.bitwise_or.reduce(fl).item())
-                   if hasattr(torch.bitwise_or, "reduce") else None},
+        "solver": {"mean_iters": float(it.float().mean()), "mean_peak_candidates": float(stt[:, 1].mean()),
+                   "max_peak_candidates": int(stt[:, 1].max()), "mean_anchors": float(stt[:, 2].mean()),
+                   "mean_rebuilds_per_step": float(stt[:, 3].mean()),
+                   "envs_flagged_overflow": int(((fl & 32) != 0).sum()), "envs_nan": int(((fl & 12) != 0).sum())},
     }
     return out, scene, sim
 

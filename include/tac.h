@@ -151,6 +151,10 @@ tac_status tac_reset(tac_sim* sim, const uint8_t* env_mask, const float* poses, 
  * iterations used, |P g|_disp at exit, flags (TAC_FLAG_*). */
 tac_status tac_env_status(tac_sim* sim, int32_t* iters, float* pg_norm, uint32_t* flags, void* stream);
 
+/* Per-env statistics of the last step (device int32 [n_envs][4]): iterations,
+ * peak candidate-pair count, friction anchors, candidate rebuilds inside the loop. */
+tac_status tac_env_stats(tac_sim* sim, int32_t* out, void* stream);
+
 /* Sizes: out[0..7] = n_verts, n_tets, n_envs, env_stride, n_markers, n_surface_verts,
  * n_surface_edges, n_surface_tris. */
 tac_status tac_info(const tac_sim* sim, int32_t* out);

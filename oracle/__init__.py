@@ -60,8 +60,8 @@ def lib():
         L.or_curvature.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, C.c_double]
         L.or_alpha_ccd.restype = C.c_double
         L.or_alpha_ccd.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _dp]
-        L.or_broadphase_world.restype = C.c_int
-        L.or_broadphase_world.argtypes = [C.c_void_p, _dp, _dp, C.c_double, _ip, C.c_int]
+        L.or_broadphase_body.restype = C.c_int
+        L.or_broadphase_body.argtypes = [C.c_void_p, _dp, C.c_double, _ip, C.c_int]
         L.or_broadphase_state.restype = C.c_int
         L.or_broadphase_state.argtypes = [C.c_void_p, _dp, _dp, _dp, C.c_double, _ip, C.c_int]
         L.or_dmin.restype = C.c_double
@@ -273,12 +273,12 @@ class Oracle:
         ins = [_d(a) for a in (u, c, np.asarray(R).reshape(9), p, prig)]
         return lib().or_alpha_ccd(self.h, *(a[1] for a in ins))
 
-    def broadphase_world(self, gx, iy, r):
-        gx, gp = _d(gx)
-        iy, ip = _d(iy)
-        n = lib().or_broadphase_world(self.h, gp, ip, r, None, 0)
+    def broadphase_body(self, gb, r):
+        """Candidates for gel vertices given in the indenter body frame gb [nv, 3]."""
+        gb, gp = _d(gb)
+        n = lib().or_broadphase_body(self.h, gp, r, None, 0)
         out = np.zeros((n, 3), np.int32)
-        lib().or_broadphase_world(self.h, gp, ip, r, out.ctypes.data_as(_ip), n)
+        lib().or_broadphase_body(self.h, gp, r, out.ctypes.data_as(_ip), n)
         return out
 
     def broadphase_state(self, u, c, R, r):

@@ -450,8 +450,9 @@ Dist pair_dist(const Problem& P, const State& s, const Pair& pr) {
 
 // ---------------------------------------------------------------------------
 // broad phase (R16): all (gel vert, ind tri), (ind vert,
-// gel tri), (gel edge, ind edge) pairs whose axis-aligned boxes are within r on
-// every axis.  Brute force O(n m), fp64, no FMA contraction (built with
+// gel tri), (gel edge, ind edge) pairs whose axis-aligned boxes IN THE INDENTER BODY
+// FRAME are within r on every axis (complete: a pair at distance <= r has every axis
+// gap <= r in any frame).  Brute force O(n m), fp64, no FMA contraction (built with
 // -ffp-contract=off) -> the exact predicate the device path must match bit for bit.
 // ---------------------------------------------------------------------------
 struct Box { double lo[3], hi[3]; };
@@ -470,13 +471,13 @@ bool near_boxes(const Box& A, const Box& B, double r) {
   }
   return true;
 }
-// world coordinates used by the predicate: gel x = X + u (exact in fp64 for fp32 inputs),
-// indenter y = R Y + c evaluated as ((R0 Y0 + R1 Y1) + R2 Y2) + c without contraction.
-std::vector<Pair> broad_phase(const Problem& P, const std::vector<V3>& gx, const std::vector<V3>& iy, double r) {
+// gb: gel vertices in the body frame; the indenter boxes come from its rest shape Y
+std::vector<Pair> broad_phase(const Problem& P, const std::vector<V3>& gb, double r) {
+  const std::vector<V3>& iy = P.Y;
   std::vector<Box> bsv(P.sv.size()), bse(P.se.size()), bst(P.st.size()), biv(P.niv), bie(P.ie.size()), bit(P.it.size());
-  for (size_t i = 0; i < P.sv.size(); ++i) bsv[i] = box_of(&gx[P.sv[i]], 1);
-  for (size_t i = 0; i < P.se.size(); ++i) { V3 z[2] = {gx[P.se[i][0]], gx[P.se[i][1]]}; bse[i] = box_of(z, 2); }
-  for (size_t i = 0; i < P.st.size(); ++i) { V3 z[3] = {gx[P.st[i][0]], gx[P.st[i][1]], gx[P.st[i][2]]}; bst[i] = box_of(z, 3); }
+  for (size_t i = 0; i < P.sv.size(); ++i) bsv[i] = box_of(&gb[P.sv[i]], 1);
+  for (size_t i = 0; i < P.se.size(); ++i) { V3 z[2] = {gb[P.se[i][0]], gb[P.se[i][1]]}; bse[i] = box_of(z, 2); }
+  for (size_t i = 0; i < P.st.size(); ++i) { V3 z[3] = {gb[P.st[i][0]], gb[P.st[i][1]], gb[P.st[i][2]]}; bst[i] = box_of(z, 3); }
   for (int i = 0; i < P.niv; ++i) biv[i] = box_of(&iy[i], 1);
   for (size_t i = 0; i < P.ie.size(); ++i) { V3 z[2] = {iy[P.ie[i][0]], iy[P.ie[i][1]]}; bie[i] = box_of(z, 2); }
   for (size_t i = 0; i < P.it.size(); ++i) { V3 z[3] = {iy[P.it[i][0]], iy[P.it[i][1]], iy[P.it[i][2]]}; bit[i] = box_of(z, 3); }
@@ -492,24 +493,25 @@ std::vector<Pair> broad_phase(const Problem& P, const std::vector<V3>& gx, const
       if (near_boxes(bse[a], bie[b], r)) out.push_back({EE, (int)a, (int)b});
   return out;
 }
-void world_coords(const Problem& P, const State& s, std::vector<V3>& gx, std::vector<V3>& iy) {
-  gx.resize(P.nv);
-  iy.resize(P.niv);
-  for (int v = 0; v < P.nv; ++v) gx[v] = add(P.X[v], s.u[v]);
-  for (int j = 0; j < P.niv; ++j) {
-    const V3& y = P.Y[j];
+// gel vertices in the body frame: b = R^T (x - c), x = X + u (exact in fp64 for fp32
+// inputs), b_a = (R_0a dx_0 + R_1a dx_1) + R_2a dx_2 evaluated left to right
+void body_coords(const Problem& P, const State& s, std::vector<V3>& gb) {
+  gb.resize(P.nv);
+  for (int v = 0; v < P.nv; ++v) {
+    V3 x = add(P.X[v], s.u[v]);
+    double d0 = x[0] - s.c[0], d1 = x[1] - s.c[1], d2 = x[2] - s.c[2];
     for (int a = 0; a < 3; ++a) {
-      double t0 = s.R[3 * a] * y[0];
-      double t1 = s.R[3 * a + 1] * y[1];
-      double t2 = s.R[3 * a + 2] * y[2];
-      iy[j][a] = ((t0 + t1) + t2) + s.c[a];
+      double t0 = s.R[a] * d0;
+      double t1 = s.R[3 + a] * d1;
+      double t2 = s.R[6 + a] * d2;
+      gb[v][a] = (t0 + t1) + t2;
     }
   }
 }
 std::vector<Pair> broad_phase_state(const Problem& P, const State& s, double r) {
-  std::vector<V3> gx, iy;
-  world_coords(P, s, gx, iy);
-  return broad_phase(P, gx, iy, r);
+  std::vector<V3> gb;
+  body_coords(P, s, gb);
+  return broad_phase(P, gb, r);
 }
 
 // ---------------------------------------------------------------------------
@@ -845,29 +847,56 @@ Vecs to_vecs(const Grad& G) { return Vecs{G.g, G.gc, G.gth}; }
 // the last term bounds the rotation's curvature for alpha <= alpha_upper
 // (|exp(t[w])r - r - t w x r| <= (t|w|)^2 |r|/2 and alpha |w| rho_max <= dhat/2).
 // alpha <= (1-s) d / l_n keeps d(alpha) >= s d.
+// Cheap certificate for far pairs: if the world boxes of the two primitives are
+// separated along an axis by g >= dhat, that axis is a separating plane with
+// separation g (every point of A is beyond every point of B along it), so the same
+// bound applies with (g, +-e_axis) in place of (d, n), and the pair carries no
+// barrier term.  Returns false if no axis separates the boxes by dhat.
+bool axis_separation(const V3* z, int na, double dhat, double* g, V3* n) {
+  double best = -INF;
+  V3 bn{0, 0, 0};
+  for (int a = 0; a < 3; ++a) {
+    double loA = INF, hiA = -INF, loB = INF, hiB = -INF;
+    for (int k = 0; k < 4; ++k) {
+      if (k < na) { loA = std::min(loA, z[k][a]); hiA = std::max(hiA, z[k][a]); }
+      else { loB = std::min(loB, z[k][a]); hiB = std::max(hiB, z[k][a]); }
+    }
+    if (loA - hiB > best) { best = loA - hiB; bn = V3{0, 0, 0}; bn[a] = 1; }   // A above B along +a
+    if (loB - hiA > best) { best = loB - hiA; bn = V3{0, 0, 0}; bn[a] = -1; }  // A below B
+  }
+  *g = best;
+  *n = bn;
+  return best >= dhat;
+}
 double alpha_ccd(const Problem& P, const State& s, const std::vector<Pair>& C, const Vecs& p) {
   double pth = norm(p.th);
   double a = INF;
   for (const Pair& pr : C) {
-    Dist D = pair_dist(P, s, pr);
     int ci[4];
     bool ind[4];
     pair_corners(P, pr, ci, ind);
-    V3 z[4], dz[4], r{0, 0, 0};
+    V3 z[4], dz[4];
     for (int k = 0; k < 4; ++k) {
       z[k] = corner_pos(P, s, ci[k], ind[k]);
       dz[k] = ind[k] ? add(p.c, cross(p.th, sub(z[k], s.c))) : p.v[ci[k]];
-      r = add(r, scl(D.w[k], z[k]));
     }
-    V3 n = scl(1.0 / D.d, r);
     int na = (pr.kind == EE) ? 2 : 1;
+    double dist;
+    V3 n;
+    if (!axis_separation(z, na, P.dhat, &dist, &n)) {
+      Dist D = pair_dist(P, s, pr);
+      V3 r{0, 0, 0};
+      for (int k = 0; k < 4; ++k) r = add(r, scl(D.w[k], z[k]));
+      dist = D.d;
+      n = scl(1.0 / D.d, r);
+    }
     double la = -INF, lb = -INF;
     for (int k = 0; k < 4; ++k) {
       if (k < na) la = std::max(la, -dot(n, dz[k]));
       else lb = std::max(lb, dot(n, dz[k]));
     }
     double l = la + lb + pth * P.dhat / 4;
-    if (l > 0) a = std::min(a, (1 - P.ccd_s) * D.d / l);
+    if (l > 0) a = std::min(a, (1 - P.ccd_s) * dist / l);
   }
   return a;
 }
@@ -1020,6 +1049,7 @@ void env_step(const Problem& P, Env& E, const double* target7, double h) {
       Sacc = 0;
       a_ccd = alpha_ccd(P, s, C, p);
       alpha = std::min(a_up, std::min(a_bar, a_ccd));
+      if (!std::isfinite(alpha)) alpha = 0;
       rebuilt = 1;
     }
     if (E.want_trace) {
@@ -1298,14 +1328,13 @@ double or_alpha_ccd(void* h, const double* u, const double* c, const double* R, 
   pv.th = {prig[3], prig[4], prig[5]};
   return alpha_ccd(P, s, broad_phase_state(P, s, P.dhat + P.bp_margin), pv);
 }
-// broad phase on explicit world coordinates: gx [nv*3] (gel), iy [niv*3] (indenter)
+// broad phase on explicit gel vertex coordinates in the indenter body frame gb [nv*3]
 // out: (kind, a, b) triples; returns count (may exceed cap)
-int or_broadphase_world(void* h, const double* gx, const double* iy, double r, int* out, int cap) {
+int or_broadphase_body(void* h, const double* gb, double r, int* out, int cap) {
   Problem& P = ((Oracle*)h)->P;
-  std::vector<V3> g(P.nv), y(P.niv);
-  for (int v = 0; v < P.nv; ++v) g[v] = {gx[3 * v], gx[3 * v + 1], gx[3 * v + 2]};
-  for (int j = 0; j < P.niv; ++j) y[j] = {iy[3 * j], iy[3 * j + 1], iy[3 * j + 2]};
-  std::vector<Pair> C = broad_phase(P, g, y, r);
+  std::vector<V3> g(P.nv);
+  for (int v = 0; v < P.nv; ++v) g[v] = {gb[3 * v], gb[3 * v + 1], gb[3 * v + 2]};
+  std::vector<Pair> C = broad_phase(P, g, r);
   for (size_t i = 0; i < C.size() && (int)i < cap; ++i) { out[3 * i] = C[i].kind; out[3 * i + 1] = C[i].a; out[3 * i + 2] = C[i].b; }
   return (int)C.size();
 }

@@ -390,6 +390,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
   d.beta_rule = P.beta_rule; d.precond = P.precond; d.max_halv = P.max_halvings; d.stagnation = P.stagnation;
   d.fixed_iters = P.fixed_iters;
   for (int a = 0; a < 3; ++a) { d.t1[a] = MS.t1[a]; d.t2[a] = MS.t2[a]; d.nrm[a] = MS.n[a]; }
+  if (6.0 * nv * (double)d.Es >= 4294967296.0) { delete sim; return fail(TAC_EINVAL, "n_verts x n_envs too large for 32-bit offsets"); }
   sim->max_iters = P.max_iters;
   sim->fixed_iters = P.fixed_iters;
   sim->check_every = P.check_every > 0 ? P.check_every : 25;
@@ -445,7 +446,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
         (rc = zalloc(sim, (size_t)kNAcc * d.Es, &d.acc)) || (rc = zalloc(sim, (size_t)kNAccU * d.Es, &d.accu)) ||
         (rc = zalloc(sim, (size_t)d.Es, &d.dalpha)) || (rc = zalloc(sim, (size_t)d.Es, &d.beta)) ||
         (rc = zalloc(sim, (size_t)d.Es, &d.run)) || (rc = zalloc(sim, (size_t)d.Es, &d.pcf)) ||
-        (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.cand)) || (rc = zalloc(sim, (size_t)d.E, &d.ncand)) ||
+        (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.cand)) || (rc = zalloc(sim, 2 * (size_t)d.E * d.kmax, &d.cgeo)) || (rc = zalloc(sim, (size_t)d.E, &d.ncand)) ||
         (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc)) || (rc = zalloc(sim, (size_t)d.E, &d.nanc)) ||
         (rc = zalloc(sim, 1, &sim->d_flag)) || (rc = zalloc(sim, (size_t)d.kmax, &sim->d_dbg_cand)) ||
         (rc = zalloc(sim, 1, &sim->d_dbg_cnt)) || (rc = zalloc(sim, 3 * (size_t)nv, &sim->d_scratch)))
@@ -618,6 +619,15 @@ tac_status tac_profile_read(tac_sim* sim, double* ms, int64_t* counts, int32_t n
 }
 
 const char* tac_profile_kernel_name(int32_t id) { return tac::kernel_name(id); }
+
+tac_status tac_env_stats(tac_sim* sim, int32_t* out, void* stream) {
+  tac_status st = check_sim(sim);
+  if (st) return st;
+  if (!out) return TAC_EINVAL;
+  cudaSetDevice(sim->device);
+  launch_stats(sim->d, (int4*)out, (cudaStream_t)stream);
+  return post_launch(sim);
+}
 
 // ---------------------------------------------------------------- debug hooks
 static tac_status gather_vec(tac_sim* sim, const float* dsrc, int env, double* out) {

@@ -40,6 +40,7 @@ struct EnvS {
   double Lrel_last;
   double Ep[5];                // energy parts of the last evaluation (diagnostics)
   int iter, halv, restart, reeval, mode, flags, best_it, accepted, rebuild, ncand_over;
+  int ncand_max, nanc_last;   // per-step statistics (tac_env_stats)
 };
 
 // modes
@@ -88,6 +89,7 @@ struct Dev {
   int* run;              // [Es] bit0 evaluate, bit1 direction, bit2 rebuild
   float4* pcf;           // [Es] rigid p_c (float) for L_rel
   unsigned long long* cand;  // [E][kmax] (kind<<62 | a<<31 | b)
+  float4* cgeo;          // [E][kmax][2] pair geometry of the last evaluation: (d, n), (w0..w3)
   int* ncand;            // [E]
   Anchor* anc;           // [E][amax]
   int* nanc;             // [E]
@@ -112,6 +114,7 @@ void launch_markers(const Dev& d, float* out, int ncomp, cudaStream_t s);
 void launch_reset(const Dev& d, const unsigned char* mask, const float* poses, cudaStream_t s);
 void launch_status(const Dev& d, int* iters, float* pg, unsigned* flags, cudaStream_t s);
 void launch_any_active(const Dev& d, int* out, cudaStream_t s);
+void launch_stats(const Dev& d, int4* out, cudaStream_t s);
 // debug
 void launch_debug_broadphase(const Dev& d, double r, unsigned long long* out, int* cnt, int cap, cudaStream_t s);
 int launches_per_iteration();

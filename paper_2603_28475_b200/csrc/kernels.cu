@@ -24,8 +24,9 @@ static const char* kNames[KID_COUNT] = {
 const char* kernel_name(int kid) { return (kid >= 0 && kid < KID_COUNT) ? kNames[kid] : "?"; }
 
 // ------------------------------------------------------------------ small helpers
-__device__ __forceinline__ size_t vidx(const Dev& d, int c, int v, int e) {
-  return ((size_t)c * d.nv + v) * d.Es + e;
+// 32-bit offsets: tac_create guarantees 6 nv Es < 2^32
+__device__ __forceinline__ unsigned vidx(const Dev& d, int c, int v, int e) {
+  return ((unsigned)c * (unsigned)d.nv + (unsigned)v) * (unsigned)d.Es + (unsigned)e;
 }
 struct d3 {
   double x, y, z;
@@ -253,6 +254,28 @@ __device__ __forceinline__ DR pair_dist(int kind, const d3* z) {
   return kind == 2 ? dist_ee(z[0], z[1], z[2], z[3]) : dist_pt(z[0], z[1], z[2], z[3]);
 }
 
+// far-pair certificate (R15): world boxes separated along an axis by g >= dhat ->
+// separating plane (g, +-e_axis); no barrier term, no exact distance needed
+__device__ __forceinline__ bool axis_sep(const d3* z, int na, double dhat, double* g, d3* n) {
+  double best = -INFINITY;
+  d3 bn = mk(0, 0, 0);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double loA = INFINITY, hiA = -INFINITY, loB = INFINITY, hiB = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      double v = a == 0 ? z[k].x : (a == 1 ? z[k].y : z[k].z);
+      if (k < na) { loA = fmin(loA, v); hiA = fmax(hiA, v); }
+      else { loB = fmin(loB, v); hiB = fmax(hiB, v); }
+    }
+    if (loA - hiB > best) { best = loA - hiB; bn = mk(a == 0, a == 1, a == 2); }
+    if (loB - hiA > best) { best = loB - hiA; bn = mk(-(a == 0), -(a == 1), -(a == 2)); }
+  }
+  *g = best;
+  *n = bn;
+  return best >= dhat;
+}
+
 // ------------------------------------------------------------------ a1: step setup
 __global__ void k_step_setup(Dev d, const float* poses) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -268,7 +291,7 @@ __global__ void k_step_setup(Dev d, const float* poses) {
   d3 dc = ld3(s.cs) - ld3(s.ct);
   s.flags = (nrm(dc) > 2e-3 || nrm(so3_log(RRt)) > 5 * M_PI / 180) ? 16 : 0;
   s.iter = 0; s.halv = 0; s.restart = 1; s.reeval = 0; s.mode = kActive; s.best_it = 0; s.accepted = 0;
-  s.rebuild = 0; s.ncand_over = 0;
+  s.rebuild = 0; s.ncand_over = 0; s.ncand_max = 0; s.nanc_last = 0;
   s.alpha = 0; s.S = 0; s.best_pg = INFINITY; s.pg = 0; s.E = 0; s.Eprev = 0; s.gp_prev = 0; s.beta = 0;
   for (int i = 0; i < 6; ++i) s.pr[i] = 0;
   d.dalpha[e] = 0.f;
@@ -288,7 +311,7 @@ __global__ void k_vert_setup(Dev d, float h) {
     bool fixed = d.vflag[v] & 1;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      size_t i = vidx(d, c, v, e);
+      unsigned i = vidx(d, c, v, e);
       float ut = d.ut[i];
       d.u[i] = ut;
       d.uh[i] = fixed ? 0.f : ut + h * d.vt[i];
@@ -297,46 +320,36 @@ __global__ void k_vert_setup(Dev d, float h) {
 }
 
 // ------------------------------------------------------------------ a2: broad phase
-// Candidates: (gel vert, ind tri), (ind vert, gel tri), (gel edge, ind edge) whose
-// world AABBs are within r on every axis (R16).  Traversal of the static body-frame
-// BVH tests the world AABB of each rotated node box (conservative, +eps); leaves run
-// the exact fp64 predicate with the oracle's rounding: gel x = X + u, indenter
-// y = ((R0 Y0 + R1 Y1) + R2 Y2) + c, no contraction (__dmul_rn / __dadd_rn).
-__device__ __forceinline__ double ind_world_exact(const double* R, const double* c, float4 y, int a) {
-  double t0 = __dmul_rn(R[3 * a], (double)y.x);
-  double t1 = __dmul_rn(R[3 * a + 1], (double)y.y);
-  double t2 = __dmul_rn(R[3 * a + 2], (double)y.z);
-  return __dadd_rn(__dadd_rn(__dadd_rn(t0, t1), t2), c[a]);
+// Candidates (R16): (gel vert, ind tri), (ind vert, gel tri), (gel edge, ind edge) whose
+// axis-aligned boxes in the indenter BODY frame are within r on every axis (complete:
+// distance >= the largest axis gap in any frame).  Gel vertices go to the body frame
+// as b = R^T (x - c) with the oracle's rounding, x = X + u exact in fp64,
+// b_a = (R_0a dx_0 + R_1a dx_1) + R_2a dx_2, no contraction (__dmul_rn / __dadd_rn);
+// indenter boxes come straight from Y.  The static body-frame BVH is traversed with a
+// conservatively inflated fp32 query; leaves run the exact fp64 predicate.
+__device__ __forceinline__ double to_body_exact(const double* R, const double* c, d3 x, int a) {
+  double d0 = __dsub_rn(x.x, c[0]), d1 = __dsub_rn(x.y, c[1]), d2 = __dsub_rn(x.z, c[2]);
+  double t0 = __dmul_rn(R[a], d0), t1 = __dmul_rn(R[3 + a], d1), t2 = __dmul_rn(R[6 + a], d2);
+  return __dadd_rn(__dadd_rn(t0, t1), t2);
 }
 
-template <int NGEL, int NIND>
-__device__ void bp_query(const Dev& d, int e, int kind, int gid, const int* gv, const double* gxlo,
-                         const double* gxhi, const double* R, const double* c, const float* Rf, const float* cf,
-                         double r, int root, unsigned long long* out, int* cnt, int cap, bool* over) {
-  // query box (fp32, inflated by r + eps)
-  float qlo[3], qhi[3];
+template <int NIND>
+__device__ void bp_query(const Dev& d, int kind, int gid, const double* glo, const double* ghi, double r, int root,
+                         unsigned long long* out, int* cnt, int cap, bool* over) {
   const float eps = 1e-7f;
+  float qlo[3], qhi[3];
   for (int a = 0; a < 3; ++a) {
-    qlo[a] = (float)(gxlo[a] - r) - eps;
-    qhi[a] = (float)(gxhi[a] + r) + eps;
+    qlo[a] = (float)(glo[a] - r) - eps;
+    qhi[a] = (float)(ghi[a] + r) + eps;
   }
-  int stack[40];
+  int stack[48];
   int sp = 0;
   stack[sp++] = root;
   while (sp > 0) {
-    int ni = stack[--sp];
-    BNode nd = d.bvh[ni];
-    // world AABB of the rotated node box: centre R cN + c, half |R| hN
-    float cn[3] = {0.5f * (nd.lo[0] + nd.hi[0]), 0.5f * (nd.lo[1] + nd.hi[1]), 0.5f * (nd.lo[2] + nd.hi[2])};
-    float hn[3] = {0.5f * (nd.hi[0] - nd.lo[0]), 0.5f * (nd.hi[1] - nd.lo[1]), 0.5f * (nd.hi[2] - nd.lo[2])};
-    bool hit = true;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      float wc = Rf[3 * a] * cn[0] + Rf[3 * a + 1] * cn[1] + Rf[3 * a + 2] * cn[2] + cf[a];
-      float wh = fabsf(Rf[3 * a]) * hn[0] + fabsf(Rf[3 * a + 1]) * hn[1] + fabsf(Rf[3 * a + 2]) * hn[2] + eps;
-      if (wc - wh > qhi[a] || wc + wh < qlo[a]) hit = false;
-    }
-    if (!hit) continue;
+    BNode nd = d.bvh[stack[--sp]];
+    if (nd.lo[0] > qhi[0] || nd.hi[0] < qlo[0] || nd.lo[1] > qhi[1] || nd.hi[1] < qlo[1] || nd.lo[2] > qhi[2] ||
+        nd.hi[2] < qlo[2])
+      continue;
     if (nd.left >= 0) {
       stack[sp++] = nd.left;
       stack[sp++] = nd.right;
@@ -349,20 +362,18 @@ __device__ void bp_query(const Dev& d, int e, int kind, int gid, const int* gv, 
       if (NIND == 3) { int4 t = d.it[prim]; vid[0] = t.x; vid[1] = t.y; vid[2] = t.z; }
       else if (NIND == 2) { int2 t = d.ie[prim]; vid[0] = t.x; vid[1] = t.y; }
       else vid[0] = prim;
-      double lo[3], hi[3];
-      for (int a = 0; a < 3; ++a) {
-        double x = ind_world_exact(R, c, d.Y[vid[0]], a);
-        lo[a] = x; hi[a] = x;
-        for (int j = 1; j < NIND; ++j) {
-          double xj = ind_world_exact(R, c, d.Y[vid[j]], a);
-          lo[a] = fmin(lo[a], xj);
-          hi[a] = fmax(hi[a], xj);
-        }
-      }
       bool ok = true;
+#pragma unroll
       for (int a = 0; a < 3; ++a) {
-        if (gxlo[a] > __dadd_rn(hi[a], r)) ok = false;
-        if (lo[a] > __dadd_rn(gxhi[a], r)) ok = false;
+        float4 y0 = d.Y[vid[0]];
+        double lo = (a == 0 ? y0.x : a == 1 ? y0.y : y0.z), hi = lo;
+        for (int j = 1; j < NIND; ++j) {
+          float4 yj = d.Y[vid[j]];
+          double v = (a == 0 ? yj.x : a == 1 ? yj.y : yj.z);
+          lo = fmin(lo, v);
+          hi = fmax(hi, v);
+        }
+        if (glo[a] > __dadd_rn(hi, r) || lo > __dadd_rn(ghi[a], r)) ok = false;
       }
       if (!ok) continue;
       unsigned long long a_id = (kind == 1) ? (unsigned long long)prim : (unsigned long long)gid;
@@ -374,17 +385,16 @@ __device__ void bp_query(const Dev& d, int e, int kind, int gid, const int* gv, 
   }
 }
 
-__global__ void k_broadphase(Dev d, int masked, double r, unsigned long long* out_override, int* cnt_override,
-                             int cap_override) {
+__global__ void __launch_bounds__(128) k_broadphase(Dev d, int masked, double r, unsigned long long* out_override,
+                                                    int* cnt_override, int cap_override) {
   int e = blockIdx.y;
   if (e >= d.E) return;
   const EnvS& s = d.es[e];
   if (s.mode != kActive) return;
   if (masked && !(d.run[e] & 4)) return;
   __shared__ double R[9], c[3];
-  __shared__ float Rf[9], cf[3];
-  if (threadIdx.x < 9) { R[threadIdx.x] = s.R[threadIdx.x]; Rf[threadIdx.x] = (float)s.R[threadIdx.x]; }
-  if (threadIdx.x < 3) { c[threadIdx.x] = s.c[threadIdx.x]; cf[threadIdx.x] = (float)s.c[threadIdx.x]; }
+  if (threadIdx.x < 9) R[threadIdx.x] = s.R[threadIdx.x];
+  if (threadIdx.x < 3) c[threadIdx.x] = s.c[threadIdx.x];
   __syncthreads();
   unsigned long long* out = out_override ? out_override : d.cand + (size_t)e * d.kmax;
   int* cnt = cnt_override ? cnt_override : d.ncand + e;
@@ -392,29 +402,30 @@ __global__ void k_broadphase(Dev d, int masked, double r, unsigned long long* ou
   bool over = false;
   int ntot = d.nsv + d.nse + d.nst;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ntot; i += gridDim.x * blockDim.x) {
-    double lo[3], hi[3];
+    int vv[3], nvx, kind, gid, root;
     if (i < d.nsv) {
-      int v = d.sv[i];
-      d3 x = gel_pos(d, d.u, v, e);
-      lo[0] = hi[0] = x.x; lo[1] = hi[1] = x.y; lo[2] = hi[2] = x.z;
-      bp_query<1, 3>(d, e, 0, i, nullptr, lo, hi, R, c, Rf, cf, r, d.root_tri, out, cnt, cap, &over);
+      vv[0] = d.sv[i]; nvx = 1; kind = 0; gid = i; root = d.root_tri;
     } else if (i < d.nsv + d.nse) {
-      int k = i - d.nsv;
-      int2 ed = d.se[k];
-      d3 x0 = gel_pos(d, d.u, ed.x, e), x1 = gel_pos(d, d.u, ed.y, e);
-      lo[0] = fmin(x0.x, x1.x); hi[0] = fmax(x0.x, x1.x);
-      lo[1] = fmin(x0.y, x1.y); hi[1] = fmax(x0.y, x1.y);
-      lo[2] = fmin(x0.z, x1.z); hi[2] = fmax(x0.z, x1.z);
-      bp_query<2, 2>(d, e, 2, k, nullptr, lo, hi, R, c, Rf, cf, r, d.root_edge, out, cnt, cap, &over);
+      gid = i - d.nsv;
+      int2 ed = d.se[gid];
+      vv[0] = ed.x; vv[1] = ed.y; nvx = 2; kind = 2; root = d.root_edge;
     } else {
-      int k = i - d.nsv - d.nse;
-      int4 t = d.st[k];
-      d3 x0 = gel_pos(d, d.u, t.x, e), x1 = gel_pos(d, d.u, t.y, e), x2 = gel_pos(d, d.u, t.z, e);
-      lo[0] = fmin(fmin(x0.x, x1.x), x2.x); hi[0] = fmax(fmax(x0.x, x1.x), x2.x);
-      lo[1] = fmin(fmin(x0.y, x1.y), x2.y); hi[1] = fmax(fmax(x0.y, x1.y), x2.y);
-      lo[2] = fmin(fmin(x0.z, x1.z), x2.z); hi[2] = fmax(fmax(x0.z, x1.z), x2.z);
-      bp_query<3, 1>(d, e, 1, k, nullptr, lo, hi, R, c, Rf, cf, r, d.root_vert, out, cnt, cap, &over);
+      gid = i - d.nsv - d.nse;
+      int4 t = d.st[gid];
+      vv[0] = t.x; vv[1] = t.y; vv[2] = t.z; nvx = 3; kind = 1; root = d.root_vert;
     }
+    double lo[3], hi[3];
+    for (int j = 0; j < nvx; ++j) {
+      d3 x = gel_pos(d, d.u, vv[j], e);
+      for (int a = 0; a < 3; ++a) {
+        double b = to_body_exact(R, c, x, a);
+        lo[a] = j ? fmin(lo[a], b) : b;
+        hi[a] = j ? fmax(hi[a], b) : b;
+      }
+    }
+    if (kind == 0) bp_query<3>(d, 0, gid, lo, hi, r, root, out, cnt, cap, &over);
+    else if (kind == 2) bp_query<2>(d, 2, gid, lo, hi, r, root, out, cnt, cap, &over);
+    else bp_query<1>(d, 1, gid, lo, hi, r, root, out, cnt, cap, &over);
   }
   if (over && !out_override) d.es[e].ncand_over = 1;
 }
@@ -471,7 +482,7 @@ __global__ void k_vert_pre(Dev d) {
     float gg[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      size_t i = vidx(d, c, v, e);
+      unsigned i = vidx(d, c, v, e);
       float u = d.u[i];
       if (da != 0.f) {
         u = u + da * d.p[i];
@@ -649,13 +660,30 @@ __global__ void __launch_bounds__(128) k_contact_grad(Dev d, double kappa, doubl
     d3 z[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) z[k] = C.ind[k] ? mv(R, ind_body(d, C.id[k])) + cc : gel_pos(d, d.u, C.id[k], e);
+    float4* geo = d.cgeo + 2 * ((size_t)e * d.kmax + i);
+    {
+      double gsep;
+      d3 nsep;
+      if (axis_sep(z, C.na, d.dhat, &gsep, &nsep)) {  // far pair: certificate only
+        geo[0] = make_float4((float)gsep, (float)nsep.x, (float)nsep.y, (float)nsep.z);
+        continue;
+      }
+    }
     DR D = pair_dist(kind, z);
-    if (!(D.d > 0)) { Eb = INFINITY; continue; }
-    if (D.d >= d.dhat) continue;
+    if (!(D.d > 0)) {
+      Eb = INFINITY;
+      geo[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+      geo[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+      continue;
+    }
     d3 rr = mk(0, 0, 0);
 #pragma unroll
     for (int k = 0; k < 4; ++k) rr = rr + D.w[k] * z[k];
     d3 nn = (1.0 / D.d) * rr;
+    // cache the pair geometry at this iterate for the curvature / step-bound pass
+    geo[0] = make_float4((float)D.d, (float)nn.x, (float)nn.y, (float)nn.z);
+    geo[1] = make_float4((float)D.w[0], (float)D.w[1], (float)D.w[2], (float)D.w[3]);
+    if (D.d >= d.dhat) continue;
     Eb += kappa * bar_b(D.d, d.dhat);
     double db = kappa * bar_db(D.d, d.dhat), ddb = kappa * bar_ddb(D.d, d.dhat);
     double sig = 0;
@@ -983,7 +1011,7 @@ __global__ void __launch_bounds__(256) k_dir_apply(Dev d) {
     precond(D, d.precond, g, Pg);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      size_t i = vidx(d, c, v, e);
+      unsigned i = vidx(d, c, v, e);
       p[c] = beta != 0.f ? -Pg[c] + beta * d.p[i] : -Pg[c];
       d.p[i] = p[c];
       d.gp[i] = g[c];
@@ -1093,25 +1121,57 @@ __global__ void __launch_bounds__(128) k_contact_curv(Dev d, double kappa, doubl
     unsigned long long rec = d.cand[(size_t)e * d.kmax + i];
     int kind = (int)(rec >> 62), a = (int)((rec >> 31) & 0x7fffffffu), b = (int)(rec & 0x7fffffffu);
     Corners C = corners_of(d, kind, a, b);
-    d3 z[4], dz[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (C.ind[k]) {
-        z[k] = mv(R, ind_body(d, C.id[k])) + cc;
-        dz[k] = pc + cross(pth, z[k] - cc);
+    d3 dz[4], nn;
+    double dist, w[4];
+    if (!ccd_only) {  // geometry cached by k_contact_grad at this same iterate
+      const float4* geo = d.cgeo + 2 * ((size_t)e * d.kmax + i);
+      float4 g0 = geo[0];
+      dist = g0.x;
+      nn = mk(g0.y, g0.z, g0.w);
+      if (dist < d.dhat) {
+        float4 g1 = geo[1];
+        w[0] = g1.x; w[1] = g1.y; w[2] = g1.z; w[3] = g1.w;
       } else {
-        z[k] = gel_pos(d, d.u, C.id[k], e);
-        dz[k] = gel_vec(d, d.p, C.id[k], e);
+        w[0] = w[1] = w[2] = w[3] = 0;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        dz[k] = C.ind[k] ? pc + cross(pth, mv(R, ind_body(d, C.id[k]))) : gel_vec(d, d.p, C.id[k], e);
+    } else {  // fresh candidates after a rebuild: distances at the current iterate
+      d3 z[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (C.ind[k]) {
+          z[k] = mv(R, ind_body(d, C.id[k])) + cc;
+          dz[k] = pc + cross(pth, z[k] - cc);
+        } else {
+          z[k] = gel_pos(d, d.u, C.id[k], e);
+          dz[k] = gel_vec(d, d.p, C.id[k], e);
+        }
+      }
+      double gsep;
+      d3 nsep;
+      if (axis_sep(z, C.na, d.dhat, &gsep, &nsep)) {
+        dist = gsep;
+        nn = nsep;
+        w[0] = w[1] = w[2] = w[3] = 0;
+      } else {
+        DR D = pair_dist(kind, z);
+        d3 rr = mk(0, 0, 0);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) rr = rr + D.w[k] * z[k];
+        dist = D.d;
+        nn = (1.0 / D.d) * rr;
+        for (int k = 0; k < 4; ++k) w[k] = D.w[k];
       }
     }
-    DR D = pair_dist(kind, z);
-    d3 rr = mk(0, 0, 0), dr = mk(0, 0, 0);
+    if (!(dist > 0)) continue;
+    if (!ccd_only && dist < d.dhat) {
+      d3 dr = mk(0, 0, 0);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) { rr = rr + D.w[k] * z[k]; dr = dr + D.w[k] * dz[k]; }
-    d3 nn = (1.0 / D.d) * rr;
-    if (!ccd_only && D.d < d.dhat) {
+      for (int k = 0; k < 4; ++k) dr = dr + w[k] * dz[k];
       double dn = dot(nn, dr);
-      q += kappa * bar_ddb(D.d, d.dhat) * dn * dn;
+      q += kappa * bar_ddb(dist, d.dhat) * dn * dn;
     }
     double la = -INFINITY, lb = -INFINITY;
 #pragma unroll
@@ -1120,7 +1180,7 @@ __global__ void __launch_bounds__(128) k_contact_curv(Dev d, double kappa, doubl
       else lb = fmax(lb, dot(nn, dz[k]));
     }
     double l = la + lb + extra;
-    if (l > 0) amin = fmin(amin, (1 - d.ccd_s) * D.d / l);
+    if (l > 0) amin = fmin(amin, (1 - d.ccd_s) * dist / l);
   }
   if (!ccd_only) {
     int na = min(d.nanc[e], d.amax);
@@ -1207,6 +1267,8 @@ __global__ void k_alpha(Dev d, double h, int pass) {
     if (s.S + a * L > d.bp_margin) {  // rebuild before moving (O4f)
       s.alpha = fmin(aup, abar);
       s.Lrel_last = L;
+      s.ncand_max = max(s.ncand_max, d.ncand[e]);
+      s.rebuild += 1;
       d.ncand[e] = 0;
       d.run[e] = 2 | 4;
       return;
@@ -1230,7 +1292,7 @@ __global__ void k_finalize_vert(Dev d, float inv_h) {
   for (int v = blockIdx.y * 8 + threadIdx.y; v < d.nv; v += gridDim.y * 8) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      size_t i = vidx(d, c, v, e);
+      unsigned i = vidx(d, c, v, e);
       float ut = d.ut[i];
       if (failed) {
         d.u[i] = ut;
@@ -1258,6 +1320,8 @@ __global__ void k_finalize_env(Dev d) {
   }
   if (s.mode == kActive) s.flags |= 2;
   if (s.ncand_over) s.flags |= 32;
+  s.ncand_max = max(s.ncand_max, d.ncand[e]);
+  s.nanc_last = d.nanc[e];
   s.mode = kDone;
   d.run[e] = 0;
   d.dalpha[e] = 0.f;
@@ -1305,7 +1369,7 @@ __global__ void k_reset_vert(Dev d, const unsigned char* mask) {
   if (e >= d.E || !mask[e]) return;
   for (int v = blockIdx.y * 8 + threadIdx.y; v < d.nv; v += gridDim.y * 8)
     for (int c = 0; c < 3; ++c) {
-      size_t i = vidx(d, c, v, e);
+      unsigned i = vidx(d, c, v, e);
       d.u[i] = d.ut[i] = d.vt[i] = d.p[i] = d.gp[i] = 0.f;
     }
 }
@@ -1315,6 +1379,12 @@ __global__ void k_status(Dev d, int* iters, float* pg, unsigned* flags) {
   if (iters) iters[e] = d.es[e].iter;
   if (pg) pg[e] = (float)d.es[e].pg;
   if (flags) flags[e] = (unsigned)d.es[e].flags;
+}
+__global__ void k_stats(Dev d, int4* out) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= d.E) return;
+  const EnvS& s = d.es[e];
+  out[e] = make_int4(s.iter, s.ncand_max, s.nanc_last, s.rebuild);
 }
 __global__ void k_any_active(Dev d, int* out) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1330,7 +1400,7 @@ static dim3 vgrid(const Dev& d, int n) {
   return dim3(gx, gy);
 }
 static dim3 cgrid(const Dev& d) {
-  int nb = std::max(1, std::min(64, 1184 / std::max(1, d.E)));
+  int nb = std::max(1, std::min(64, 8192 / std::max(1, d.E)));
   return dim3(nb, d.E);
 }
 static int eblocks(const Dev& d) { return (d.E + 127) / 128; }
@@ -1351,7 +1421,7 @@ void launch_vert_setup(const Dev& d, double h, cudaStream_t s) {
 }
 void launch_broadphase(const Dev& d, bool masked, cudaStream_t s) {
   int ntot = d.nsv + d.nse + d.nst;
-  int nb = std::max(1, std::min((ntot + 127) / 128, 2368 / std::max(1, d.E)));
+  int nb = std::max(1, std::min((ntot + 127) / 128, (masked ? 16384 : 4736) / std::max(1, d.E)));
   LAUNCHK(KID_BROADPHASE, s, (k_broadphase<<<dim3(nb, d.E), 128, 0, s>>>(d, masked ? 1 : 0, d.dhat + d.bp_margin, nullptr, nullptr, 0)));
 }
 void launch_anchors(const Dev& d, double h, cudaStream_t s) {
@@ -1394,6 +1464,9 @@ void launch_reset(const Dev& d, const unsigned char* mask, const float* poses, c
 }
 void launch_status(const Dev& d, int* iters, float* pg, unsigned* flags, cudaStream_t s) {
   LAUNCHK(KID_OTHER, s, (k_status<<<eblocks(d), 128, 0, s>>>(d, iters, pg, flags)));
+}
+void launch_stats(const Dev& d, int4* out, cudaStream_t s) {
+  LAUNCHK(KID_OTHER, s, (k_stats<<<eblocks(d), 128, 0, s>>>(d, out)));
 }
 void launch_any_active(const Dev& d, int* out, cudaStream_t s) {
   LAUNCHK(KID_OTHER, s, (k_any_active<<<eblocks(d), 128, 0, s>>>(d, out)));

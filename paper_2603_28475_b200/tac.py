@@ -85,6 +85,7 @@ def lib():
         L.tac_debug_surface.argtypes = [vp, _ip, _ip, _ip, _ip, _ip]
         L.tac_debug_marker_map.argtypes = [vp, _ip, _ip, _dp]
         L.tac_profile_enable.argtypes = [vp, C.c_int32]
+        L.tac_env_stats.argtypes = [vp, vp, vp]
         L.tac_profile_read.argtypes = [vp, _dp, C.POINTER(C.c_int64), C.c_int32]
         L.tac_profile_kernel_name.argtypes = [C.c_int32]
         L.tac_profile_kernel_name.restype = C.c_char_p
@@ -97,7 +98,7 @@ def lib():
 EXPORTED = ["tac_create", "tac_step", "tac_markers", "tac_reset", "tac_env_status", "tac_info",
             "tac_last_launch_count", "tac_destroy", "tac_last_error", "tac_get_state", "tac_set_state",
             "tac_debug_broadphase", "tac_debug_surface", "tac_debug_marker_map", "tac_debug_eval",
-            "tac_profile_enable", "tac_profile_read", "tac_profile_kernel_name"]
+            "tac_profile_enable", "tac_profile_read", "tac_profile_kernel_name", "tac_env_stats"]
 N_KERNEL_IDS = 19
 
 
@@ -216,6 +217,13 @@ class TacSim:
         self._check(lib().tac_env_status(self.h, C.c_void_p(it.data_ptr()), C.c_void_p(pg.data_ptr()),
                                          C.c_void_p(fl.data_ptr()), _stream_ptr(stream)), "tac_env_status")
         return it, pg, fl
+
+    def env_stats(self, stream=None):
+        """int32 tensor [n_envs, 4]: iterations, peak candidates, anchors, rebuilds (last step)."""
+        import torch
+        out = torch.empty((self.n_envs, 4), dtype=torch.int32, device=f"cuda:{self.device}")
+        self._check(lib().tac_env_stats(self.h, C.c_void_p(out.data_ptr()), _stream_ptr(stream)), "tac_env_stats")
+        return out
 
     def profile_enable(self, on=True):
         self._check(lib().tac_profile_enable(self.h, int(on)), "tac_profile_enable")

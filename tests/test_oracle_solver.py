@@ -134,8 +134,14 @@ def test_rest_rotation_patch_and_diag_blocks():
         assert np.abs(Hb - r["D"][v]).max() <= 1e-6 * np.abs(r["D"][v]).max()
 
 
+def _body(X, u, c, R):
+    """Gel vertices in the indenter body frame, b_a = (R_0a d_0 + R_1a d_1) + R_2a d_2 (no FMA)."""
+    d = (X + u) - c
+    return np.stack([(R[0, a] * d[:, 0] + R[1, a] * d[:, 1]) + R[2, a] * d[:, 2] for a in range(3)], axis=1)
+
+
 def _box_pairs(o, gx, iy, r):
-    """Independent numpy evaluation of the inflated-box predicate (SURVEY §8a a2)."""
+    """Independent numpy evaluation of the inflated-box predicate (SURVEY §8a a2, R16)."""
     sv, se, st, ie = o.surface()
     it = o.scene.tris
 
@@ -158,12 +164,13 @@ def _box_pairs(o, gx, iy, r):
 def test_broadphase_matches_box_predicate_and_is_complete(pressed):
     s, o, st, (u, c, R), tgt = pressed
     r = 3e-4
-    gx = s.X + u
-    iy = s.Y @ R.T + c
-    got = sorted(map(tuple, o.broadphase_world(gx, iy, r).tolist()))
+    gx = _body(s.X, u, c, R)
+    iy = s.Y
+    got = sorted(map(tuple, o.broadphase_body(gx, r).tolist()))
     assert got == _box_pairs(o, gx, iy, r)
+    assert sorted(map(tuple, o.broadphase_state(u, c, R, r).tolist())) == got
     # completeness: every primitive pair closer than r is a candidate (brute-force distances)
-    allp = o.broadphase_world(gx, iy, 1.0)
+    allp = o.broadphase_body(gx, 1.0)
     sv, se, stri, ie = o.surface()
     cand = set(got)
     for kind, a, b in allp.tolist():
