@@ -868,9 +868,14 @@ bool axis_separation(const V3* z, int na, double dhat, double* g, V3* n) {
   *n = bn;
   return best >= dhat;
 }
+double rel_motion(const Problem& P, const Vecs& p);
+// Pairs without an axis certificate ("near") use their exact closest-point plane.
+// All axis-certified ("far") pairs share one bound: each has d(alpha) >= g_i - alpha L_rel
+// >= g_min - alpha L_rel (L_rel bounds the relative motion of any gel surface point vs any
+// indenter point, see rel_motion), so alpha <= (1-s) g_min / L_rel keeps them >= s g_min.
 double alpha_ccd(const Problem& P, const State& s, const std::vector<Pair>& C, const Vecs& p) {
   double pth = norm(p.th);
-  double a = INF;
+  double a = INF, gmin = INF;
   for (const Pair& pr : C) {
     int ci[4];
     bool ind[4];
@@ -881,23 +886,26 @@ double alpha_ccd(const Problem& P, const State& s, const std::vector<Pair>& C, c
       dz[k] = ind[k] ? add(p.c, cross(p.th, sub(z[k], s.c))) : p.v[ci[k]];
     }
     int na = (pr.kind == EE) ? 2 : 1;
-    double dist;
+    double g;
     V3 n;
-    if (!axis_separation(z, na, P.dhat, &dist, &n)) {
-      Dist D = pair_dist(P, s, pr);
-      V3 r{0, 0, 0};
-      for (int k = 0; k < 4; ++k) r = add(r, scl(D.w[k], z[k]));
-      dist = D.d;
-      n = scl(1.0 / D.d, r);
+    if (axis_separation(z, na, P.dhat, &g, &n)) {
+      gmin = std::min(gmin, g);
+      continue;
     }
+    Dist D = pair_dist(P, s, pr);
+    V3 r{0, 0, 0};
+    for (int k = 0; k < 4; ++k) r = add(r, scl(D.w[k], z[k]));
+    n = scl(1.0 / D.d, r);
     double la = -INF, lb = -INF;
     for (int k = 0; k < 4; ++k) {
       if (k < na) la = std::max(la, -dot(n, dz[k]));
       else lb = std::max(lb, dot(n, dz[k]));
     }
     double l = la + lb + pth * P.dhat / 4;
-    if (l > 0) a = std::min(a, (1 - P.ccd_s) * dist / l);
+    if (l > 0) a = std::min(a, (1 - P.ccd_s) * D.d / l);
   }
+  double L = rel_motion(P, p);
+  if (gmin < INF && L > 0) a = std::min(a, (1 - P.ccd_s) * gmin / L);
   return a;
 }
 // bound on the relative motion of any gel surface point vs any indenter point per unit alpha

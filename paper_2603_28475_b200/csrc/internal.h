@@ -56,7 +56,7 @@ enum AccIdx {
   kNAcc = 36
 };
 // uint accumulators [kNAccU][Es] (non-negative floats compared as uint)
-enum AccUIdx { U_PGMAX = 0, U_M, U_LREL, U_ACCD, kNAccU };
+enum AccUIdx { U_PGMAX = 0, U_M, U_LREL, U_ACCD, U_GFAR, kNAccU };
 
 struct Dev {
   // sizes
@@ -91,6 +91,8 @@ struct Dev {
   unsigned long long* cand;  // [E][kmax] (kind<<62 | a<<31 | b)
   float4* cgeo;          // [E][kmax][2] pair geometry of the last evaluation: (d, n), (w0..w3)
   int* ncand;            // [E]
+  int* nearl;            // [E][kmax] indices of near candidates (no separating-axis certificate)
+  int* nnear;            // [E]
   Anchor* anc;           // [E][amax]
   int* nanc;             // [E]
   // material / params
@@ -124,7 +126,7 @@ extern thread_local long long g_launches;
 enum KernelId {
   KID_STEP_SETUP = 0, KID_VERT_SETUP, KID_BROADPHASE, KID_ANCHORS, KID_VERT_PRE, KID_ELEM_GRAD, KID_CONTACT_GRAD,
   KID_ACCEPT, KID_DIR_REDUCE, KID_DIR_SCALAR, KID_DIR_APPLY, KID_ELEM_CURV, KID_CONTACT_CURV, KID_ALPHA,
-  KID_CCD, KID_FIN_VERT, KID_FIN_ENV, KID_MARKERS, KID_OTHER, KID_COUNT
+  KID_CCD, KID_FIN_VERT, KID_FIN_ENV, KID_MARKERS, KID_OTHER, KID_CONTACT_CLASSIFY, KID_COUNT
 };
 struct Profiler;
 extern thread_local Profiler* g_prof;

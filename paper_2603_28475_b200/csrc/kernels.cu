@@ -20,7 +20,7 @@ thread_local Profiler* g_prof = nullptr;
 static const char* kNames[KID_COUNT] = {
     "step_setup", "vert_setup", "broadphase", "anchors", "vert_pre", "elem_grad", "contact_grad", "accept",
     "dir_reduce", "dir_scalar", "dir_apply", "elem_curv", "contact_curv", "alpha", "ccd", "finalize_vert",
-    "finalize_env", "markers", "other"};
+    "finalize_env", "markers", "other", "contact_classify"};
 const char* kernel_name(int kid) { return (kid >= 0 && kid < KID_COUNT) ? kNames[kid] : "?"; }
 
 // ------------------------------------------------------------------ small helpers
@@ -300,7 +300,7 @@ __global__ void k_step_setup(Dev d, const float* poses) {
   d.ncand[e] = 0;
   d.nanc[e] = 0;
   for (int k = 0; k < kNAcc; ++k) d.acc[(size_t)k * d.Es + e] = 0.0;
-  for (int k = 0; k < kNAccU; ++k) d.accu[(size_t)k * d.Es + e] = (k == U_ACCD) ? 0x7f800000u : 0u;
+  for (int k = 0; k < kNAccU; ++k) d.accu[(size_t)k * d.Es + e] = (k == U_ACCD || k == U_GFAR) ? 0x7f800000u : 0u;
 }
 
 // x^ = x^t + h v^t on free vertices; u = u^t
@@ -474,6 +474,7 @@ __global__ void k_vert_pre(Dev d) {
   bool act = e < d.E && (d.run[e] & 1);
   if (!__any_sync(0xffffffffu, act)) return;
   float da = act ? d.dalpha[e] : 0.f;
+  if (act && blockIdx.y == 0 && threadIdx.y == 0) d.nnear[e] = 0;  // consumed by the contact passes
   double ein = 0;
   for (int v = blockIdx.y * 8 + threadIdx.y; v < d.nv; v += gridDim.y * 8) {
     if (!act) continue;
@@ -640,6 +641,51 @@ __device__ __forceinline__ void scatter_gel(const Dev& d, int v, int e, d3 f, do
 }
 
 
+// pass 1 over all candidates: far pairs (separating-axis certificate, R15) only cache
+// (g, n); near pairs are compacted into the env's near list (warp-aggregated atomics)
+// so the exact-distance pass below runs on convergent warps
+__global__ void __launch_bounds__(128) k_contact_classify(Dev d) {
+  int e = blockIdx.y;
+  if (e >= d.E || !(d.run[e] & 1)) return;
+  const EnvS& s = d.es[e];
+  __shared__ double R[9], c[3];
+  if (threadIdx.x < 9) R[threadIdx.x] = s.R[threadIdx.x];
+  if (threadIdx.x < 3) c[threadIdx.x] = s.c[threadIdx.x];
+  __syncthreads();
+  d3 cc = ld3(c);
+  int n = min(d.ncand[e], d.kmax);
+  int stride = gridDim.x * blockDim.x;
+  int lane = threadIdx.x & 31;
+  int* nearl = d.nearl + (size_t)e * d.kmax;
+  // uniform trip count per warp so the ballot below is warp-wide
+  int base0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+  double gmin = INFINITY;
+  for (int base = base0; base < n; base += stride) {
+    int i = base + lane;
+    bool near = false;
+    if (i < n) {
+      unsigned long long rec = d.cand[(size_t)e * d.kmax + i];
+      int kind = (int)(rec >> 62), a = (int)((rec >> 31) & 0x7fffffffu), b = (int)(rec & 0x7fffffffu);
+      Corners C = corners_of(d, kind, a, b);
+      d3 z[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) z[k] = C.ind[k] ? mv(R, ind_body(d, C.id[k])) + cc : gel_pos(d, d.u, C.id[k], e);
+      double gsep;
+      d3 nsep;
+      if (axis_sep(z, C.na, d.dhat, &gsep, &nsep)) gmin = fmin(gmin, gsep);
+      else near = true;
+    }
+    unsigned m = __ballot_sync(0xffffffffu, near);
+    int cnt = __popc(m);
+    int slot0 = 0;
+    if (lane == 0 && cnt) slot0 = atomicAdd(d.nnear + e, cnt);
+    slot0 = __shfl_sync(0xffffffffu, slot0, 0);
+    if (near) nearl[slot0 + __popc(m & ((1u << lane) - 1))] = i;
+  }
+  gmin = warp_min(gmin);  // far pairs: one shared bound (R15)
+  if (lane == 0 && gmin < INFINITY) atomic_min_pos(d.accu + (size_t)U_GFAR * d.Es + e, (float)gmin);
+}
+
 __global__ void __launch_bounds__(128) k_contact_grad(Dev d, double kappa, double eps_f) {
   int e = blockIdx.y;
   if (e >= d.E || !(d.run[e] & 1)) return;
@@ -651,9 +697,10 @@ __global__ void __launch_bounds__(128) k_contact_grad(Dev d, double kappa, doubl
   __syncthreads();
   double Eb = 0, Ef = 0, gr[6] = {0, 0, 0, 0, 0, 0}, Dc[6] = {0, 0, 0, 0, 0, 0}, Dt[6] = {0, 0, 0, 0, 0, 0};
   d3 cc = ld3(c);
-  int n = min(d.ncand[e], d.kmax);
+  int n = d.nnear[e];
   int stride = gridDim.x * blockDim.x;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+    int i = d.nearl[(size_t)e * d.kmax + j];
     unsigned long long rec = d.cand[(size_t)e * d.kmax + i];
     int kind = (int)(rec >> 62), a = (int)((rec >> 31) & 0x7fffffffu), b = (int)(rec & 0x7fffffffu);
     Corners C = corners_of(d, kind, a, b);
@@ -661,14 +708,6 @@ __global__ void __launch_bounds__(128) k_contact_grad(Dev d, double kappa, doubl
 #pragma unroll
     for (int k = 0; k < 4; ++k) z[k] = C.ind[k] ? mv(R, ind_body(d, C.id[k])) + cc : gel_pos(d, d.u, C.id[k], e);
     float4* geo = d.cgeo + 2 * ((size_t)e * d.kmax + i);
-    {
-      double gsep;
-      d3 nsep;
-      if (axis_sep(z, C.na, d.dhat, &gsep, &nsep)) {  // far pair: certificate only
-        geo[0] = make_float4((float)gsep, (float)nsep.x, (float)nsep.y, (float)nsep.z);
-        continue;
-      }
-    }
     DR D = pair_dist(kind, z);
     if (!(D.d > 0)) {
       Eb = INFINITY;
@@ -684,8 +723,11 @@ __global__ void __launch_bounds__(128) k_contact_grad(Dev d, double kappa, doubl
     geo[0] = make_float4((float)D.d, (float)nn.x, (float)nn.y, (float)nn.z);
     geo[1] = make_float4((float)D.w[0], (float)D.w[1], (float)D.w[2], (float)D.w[3]);
     if (D.d >= d.dhat) continue;
-    Eb += kappa * bar_b(D.d, d.dhat);
-    double db = kappa * bar_db(D.d, d.dhat), ddb = kappa * bar_ddb(D.d, d.dhat);
+    double lg = log(D.d / d.dhat), dm = D.d - d.dhat, inv = 1.0 / D.d;
+    Eb += kappa * (-dm * dm * lg);                                   // b
+    double db = kappa * (-2 * dm * lg - dm * dm * inv);              // b'
+    double ddb = kappa * (-2 * lg - 4 * dm * inv + dm * dm * inv * inv);  // b''
+
     double sig = 0;
     d3 rho = mk(0, 0, 0);
 #pragma unroll
@@ -828,6 +870,7 @@ __global__ void k_accept(Dev d, double h) {
     return;
   }
   s.accepted = 0;
+  d.accu[U_GFAR * Es + e] = 0x7f800000u;  // the next evaluation re-classifies
   s.halv += 1;
   if (s.halv <= d.max_halv) {
     double an = 0.5 * s.alpha;
@@ -1115,9 +1158,11 @@ __global__ void __launch_bounds__(128) k_contact_curv(Dev d, double kappa, doubl
   d3 cc = ld3(c), pc = mk(pr[0], pr[1], pr[2]), pth = mk(pr[3], pr[4], pr[5]);
   double extra = nrm(pth) * d.dhat * 0.25;
   double q = 0, amin = INFINITY;
-  int n = min(d.ncand[e], d.kmax);
+  int n = ccd_only ? min(d.ncand[e], d.kmax) : d.nnear[e];
   int stride = gridDim.x * blockDim.x;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+  double gmin = INFINITY;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+    int i = ccd_only ? j : d.nearl[(size_t)e * d.kmax + j];
     unsigned long long rec = d.cand[(size_t)e * d.kmax + i];
     int kind = (int)(rec >> 62), a = (int)((rec >> 31) & 0x7fffffffu), b = (int)(rec & 0x7fffffffu);
     Corners C = corners_of(d, kind, a, b);
@@ -1128,12 +1173,8 @@ __global__ void __launch_bounds__(128) k_contact_curv(Dev d, double kappa, doubl
       float4 g0 = geo[0];
       dist = g0.x;
       nn = mk(g0.y, g0.z, g0.w);
-      if (dist < d.dhat) {
-        float4 g1 = geo[1];
-        w[0] = g1.x; w[1] = g1.y; w[2] = g1.z; w[3] = g1.w;
-      } else {
-        w[0] = w[1] = w[2] = w[3] = 0;
-      }
+      float4 g1 = geo[1];
+      w[0] = g1.x; w[1] = g1.y; w[2] = g1.z; w[3] = g1.w;
 #pragma unroll
       for (int k = 0; k < 4; ++k)
         dz[k] = C.ind[k] ? pc + cross(pth, mv(R, ind_body(d, C.id[k]))) : gel_vec(d, d.p, C.id[k], e);
@@ -1152,9 +1193,8 @@ __global__ void __launch_bounds__(128) k_contact_curv(Dev d, double kappa, doubl
       double gsep;
       d3 nsep;
       if (axis_sep(z, C.na, d.dhat, &gsep, &nsep)) {
-        dist = gsep;
-        nn = nsep;
-        w[0] = w[1] = w[2] = w[3] = 0;
+        gmin = fmin(gmin, gsep);
+        continue;
       } else {
         DR D = pair_dist(kind, z);
         d3 rr = mk(0, 0, 0);
@@ -1210,6 +1250,10 @@ __global__ void __launch_bounds__(128) k_contact_curv(Dev d, double kappa, doubl
     }
     block_sum_atomic(q, d.acc + (size_t)A_PHP * d.Es + e, sm);
   }
+  if (ccd_only) {
+    gmin = warp_min(gmin);
+    if ((threadIdx.x & 31) == 0 && gmin < INFINITY) atomic_min_pos(d.accu + (size_t)U_GFAR * d.Es + e, (float)gmin);
+  }
   // block min of amin
   amin = warp_min(amin);
   __syncthreads();
@@ -1260,7 +1304,10 @@ __global__ void k_alpha(Dev d, double h, int pass) {
     d.accu[U_M * Es + e] = 0u;
     d.accu[U_LREL * Es + e] = 0u;
     double accd = (double)__uint_as_float(d.accu[U_ACCD * Es + e]);
+    double gfar = (double)__uint_as_float(d.accu[U_GFAR * Es + e]);
+    if (gfar < INFINITY && L > 0) accd = fmin(accd, (1 - d.ccd_s) * gfar / L);  // far pairs (R15)
     d.accu[U_ACCD * Es + e] = 0x7f800000u;
+    d.accu[U_GFAR * Es + e] = 0x7f800000u;
     double aup = M > 0 ? d.dhat / (2 * M) : INFINITY;
     double abar = q > 0 ? -s.gp_prev / q : INFINITY;
     double a = fmin(aup, fmin(abar, accd));
@@ -1277,7 +1324,10 @@ __global__ void k_alpha(Dev d, double h, int pass) {
   } else {
     if (!(rb & 4)) return;
     double accd = (double)__uint_as_float(d.accu[U_ACCD * Es + e]);
+    double gfar = (double)__uint_as_float(d.accu[U_GFAR * Es + e]);
+    if (gfar < INFINITY && s.Lrel_last > 0) accd = fmin(accd, (1 - d.ccd_s) * gfar / s.Lrel_last);
     d.accu[U_ACCD * Es + e] = 0x7f800000u;
+    d.accu[U_GFAR * Es + e] = 0x7f800000u;
     s.S = 0;
     commit_alpha(d, s, e, fmin(s.alpha, accd), s.Lrel_last);
   }
@@ -1430,6 +1480,7 @@ void launch_anchors(const Dev& d, double h, cudaStream_t s) {
 void launch_eval(const Dev& d, double h, cudaStream_t s) {
   LAUNCHK(KID_VERT_PRE, s, (k_vert_pre<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d)));
   LAUNCHK(KID_ELEM_GRAD, s, (k_elem_grad<<<vgrid(d, d.nt), dim3(32, 8), 0, s>>>(d, (float)(h * h))));
+  LAUNCHK(KID_CONTACT_CLASSIFY, s, (k_contact_classify<<<cgrid(d), 128, 0, s>>>(d)));
   LAUNCHK(KID_CONTACT_GRAD, s, (k_contact_grad<<<cgrid(d), 128, 0, s>>>(d, h * h * d.kappa_phys, d.eps_v * h)));
   LAUNCHK(KID_ACCEPT, s, (k_accept<<<eblocks(d), 128, 0, s>>>(d, h)));
 }
@@ -1475,6 +1526,6 @@ void launch_debug_broadphase(const Dev& d, double r, unsigned long long* out, in
   int ntot = d.nsv + d.nse + d.nst;
   LAUNCHK(KID_BROADPHASE, s, (k_broadphase<<<dim3((ntot + 127) / 128, d.E), 128, 0, s>>>(d, 0, r, out, cnt, cap)));
 }
-int launches_per_iteration() { return 4 + 3 + 2 + 4; }
+int launches_per_iteration() { return 5 + 3 + 2 + 4; }
 
 }  // namespace tac
