@@ -112,27 +112,28 @@ def run_ours(args, rank, local, ws):
 
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
+    from paper_2603_28475_b200.dist import MarkerGather, env_range
     nsteps = max(64, args.warmup + args.steps + 1)
-    E = args.envs
-    scene = w.scene_c3(n_envs=E, n_steps=nsteps, seed0=20260000 + rank * E)
+    if args.scaling == "strong":  # C4 strong: a fixed total split over the ranks
+        e0, e1 = env_range(rank, ws, args.total_envs)
+    else:  # weak: a fixed env count per GPU, distinct env ids per rank
+        e0, e1 = rank * args.envs, (rank + 1) * args.envs
+    E = e1 - e0
+    scene = w.scene_c3(n_envs=E, n_steps=nsteps, seed0=20260000 + e0)
     scene.params.fixed_iters = FIXED_ITERS
     sim = P.TacSim.from_scene(scene, device=local)
     poses = torch.tensor(scene.poses, dtype=torch.float32, device=dev).contiguous()  # resident in HBM
     nm = scene.markers.shape[0]
-    if ws > 1:
-        gather = torch.empty((ws * E, nm, 2), dtype=torch.float32, device=dev)
-        mk = gather[rank * E:(rank + 1) * E]  # tac_markers writes the rank's slot: in-place all-gather
-    else:
-        gather = None
-        mk = torch.empty((E, nm, 2), dtype=torch.float32, device=dev)
+    mg = MarkerGather(E, nm, 2, rank, ws, dev)
+    mk = mg.slot  # tac_markers writes the rank's slot; in-place all-gather to every rank (C4)
+    gather = mg if ws > 1 else None
     stream = torch.cuda.current_stream()
 
     def one_step(k):
         sim.step(poses[k], scene.dt)
         sim.markers(mk)
         if gather is not None:
-            import torch.distributed as dist
-            dist.all_gather_into_tensor(gather, mk)
+            gather.gather()
 
     launches = 0
     for k in range(args.warmup):
@@ -166,7 +167,8 @@ def run_ours(args, rank, local, ws):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = ws * E * args.steps / (ms / 1e3)
+    n_all = args.total_envs if args.scaling == "strong" else ws * E
+    value = n_all * args.steps / (ms / 1e3)
 
     # roofline of the dominant kernel (live CUDA-event timing over the timed region)
     nfree = scene.X.shape[0] - len(scene.fixed)
@@ -218,7 +220,7 @@ def run_ours(args, rank, local, ws):
         sim.step(dpose, scene.dt)
         sim.markers(mk)
         if gather is not None:
-            dist.all_gather_into_tensor(gather, mk)
+            gather.gather()
         host_mk.copy_(mk, non_blocking=True)
         torch.cuda.current_stream().synchronize()
     w1 = time.perf_counter()
@@ -227,7 +229,7 @@ def run_ours(args, rank, local, ws):
         t = torch.tensor([e2e_s], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = {"value": round(ws * E * nsteps_e2e / e2e_s, 2), "unit": "env-steps/s",
+    e2e = {"value": round(n_all * nsteps_e2e / e2e_s, 2), "unit": "env-steps/s",
            "h2d_bytes_per_step": E * 7 * 4, "d2h_bytes_per_step": E * nm * 2 * 4,
            "timing": "wall clock, synchronize per step (result read on host)", "steps": nsteps_e2e}
 
@@ -236,11 +238,11 @@ def run_ours(args, rank, local, ws):
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": "env-steps/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp64 per-env reductions and rigid DOFs)",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f32 (fp64 per-env reductions and rigid DOFs)",
         "data": "synthetic (seeded generators: workloads/)",
         "config": {"workload": "C3: 1024 envs/GPU peg-insertion trajectories (press, shear, twist, release), "
                                "19,800-tet / 4,278-vertex pad, Ø8 mm cylinder peg, 7x9 markers",
-                   "envs_per_gpu": E, "iters_per_step": FIXED_ITERS, "iteration_mode": "fixed",
+                   "envs_per_gpu": E, "total_envs": n_all, "iters_per_step": FIXED_ITERS, "iteration_mode": "fixed",
                    "parallelism": f"env-sharded dp{ws}" + (" + NCCL all-gather of markers" if ws > 1 else ""),
                    "l2": "per-env state ~470 MB/GPU > 126 MB L2 (no flush needed)"},
         "roofline": roof,
@@ -313,6 +315,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--envs", type=int, default=ENVS_PER_GPU)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--total-envs", type=int, default=8192, help="strong scaling: envs over all ranks (C4)")
     args = ap.parse_args()
     assert args.warmup >= 1
     if args.impl == "reference":

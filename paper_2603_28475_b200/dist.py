@@ -1,0 +1,42 @@
+"""Env sharding across GPUs ("a set of environments" per GPU).
+
+Environments are independent, so each rank owns a contiguous env range and no
+collective runs inside the solver.  The only exchange is the optional all-gather
+of the marker fields to the policy rank: tac_markers writes the rank's
+slot of one gather buffer and an in-place all_gather_into_tensor (NCCL over
+NVLink / NVSwitch on GPUs; gloo in the CPU tests) fills the other slots.
+"""
+from __future__ import annotations
+
+
+def env_range(rank: int, world: int, n_total: int):
+    """Contiguous [start, stop) of env ids owned by `rank` (ragged splits allowed)."""
+    if not (0 <= rank < world) or n_total < 0:
+        raise ValueError("bad rank / world / n_total")
+    base, rem = divmod(n_total, world)
+    start = rank * base + min(rank, rem)
+    return start, start + base + (1 if rank < rem else 0)
+
+
+class MarkerGather:
+    """Gather buffer [world * n_local, n_markers, ncomp]; `slot` is this rank's view.
+
+    Requires equal n_local on every rank (weak scaling, or strong scaling with
+    n_total divisible by world), as all_gather_into_tensor does."""
+
+    def __init__(self, n_local, n_markers, ncomp, rank, world, device, group=None):
+        import torch
+        self.rank, self.world, self.group = rank, world, group
+        self.buffer = torch.empty((world * n_local, n_markers, ncomp), dtype=torch.float32, device=device)
+        self.slot = self.buffer[rank * n_local:(rank + 1) * n_local]
+
+    def gather(self):
+        import torch.distributed as dist
+        if self.world == 1:
+            return self.buffer
+        try:
+            dist.all_gather_into_tensor(self.buffer, self.slot, group=self.group)
+        except (RuntimeError, NotImplementedError):  # backends without the fused collective
+            parts = list(self.buffer.chunk(self.world))
+            dist.all_gather(parts, self.slot.clone(), group=self.group)
+        return self.buffer
