@@ -192,7 +192,8 @@ def run_ours(args, rank, local, ws):
             "unit": unit, "frac": round(achieved / peak, 4), "traffic": None,
             "peak_source": f"{src} ({'MEASURED_PEAKS.json hbm_gbs' if bound == 'hbm' else '148 SM x 128 FP32 lanes x 2 flop x sm_max_mhz'})",
             "work_per_launch": work, "work_note": note, "avg_launch_us": round(avg_s * 1e6, 2),
-            "dominant_by_time": dom, "share_of_step": share}
+            "dominant_by_time": dom, "share_of_step": share,
+            "kernel_ms_total_and_launches": {k: [round(v[0], 3), v[1]] for k, v in tot.items()}}
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
         try:

@@ -296,6 +296,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     delete sim;
     return fail(TAC_ECUDA, "cudaSetDevice failed");
   }
+  kernels_init();
   sim->sv.assign(svs.begin(), svs.end());
   for (auto& f : st) for (int k = 0; k < 3; ++k) sim->st_flat.push_back(f[k]);
   for (auto& e : ses) { sim->se_flat.push_back(e.first); sim->se_flat.push_back(e.second); }
@@ -365,6 +366,106 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
   d.root_tri = build_bvh(nodes, prims, btri);
   d.root_edge = build_bvh(nodes, prims, bedge);
   d.root_vert = build_bvh(nodes, prims, bvert);
+  // element tiles: Morton order of tet centroids, greedy cut at kTileT tets / kTileV
+  // vertices, then greedy rounds of <= kTileW vertex-disjoint tets
+  std::vector<int> tile_vstart{0}, tile_verts, tile_tstart{0}, tile_rstart{0};
+  std::vector<unsigned char> tile_vfl;
+  std::vector<uchar4> tile_tv;
+  std::vector<float4> tile_tb;
+  std::vector<short> tile_sched;
+  {
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (auto& x : X) for (int c = 0; c < 3; ++c) { lo[c] = std::min(lo[c], x[c]); hi[c] = std::max(hi[c], x[c]); }
+    auto spread = [](unsigned v) {  // 10 bits -> every third bit
+      v &= 1023u;
+      v = (v | (v << 16)) & 0x030000FFu;
+      v = (v | (v << 8)) & 0x0300F00Fu;
+      v = (v | (v << 4)) & 0x030C30C3u;
+      v = (v | (v << 2)) & 0x09249249u;
+      return v;
+    };
+    std::vector<std::pair<unsigned, int>> order(nt);
+    for (int e = 0; e < nt; ++e) {
+      unsigned q[3];
+      for (int c = 0; c < 3; ++c) {
+        double m = 0;
+        for (int k = 0; k < 4; ++k) m += X[G.tets[4 * e + k]][c];
+        m /= 4;
+        q[c] = (unsigned)std::min(1023.0, std::max(0.0, (m - lo[c]) / std::max(1e-30, hi[c] - lo[c]) * 1023.0));
+      }
+      order[e] = {spread(q[0]) | (spread(q[1]) << 1) | (spread(q[2]) << 2), e};
+    }
+    std::sort(order.begin(), order.end());
+    std::vector<int> vtile(nv, -1), vcount_tiles(nv, 0), vlocal(nv, -1);
+    std::vector<std::vector<int>> tiles;
+    {
+      std::vector<int> cur;
+      std::set<int> cv;
+      for (auto& pr : order) {
+        int e = pr.second;
+        std::set<int> add;
+        for (int k = 0; k < 4; ++k)
+          if (!cv.count(G.tets[4 * e + k])) add.insert(G.tets[4 * e + k]);
+        if (!cur.empty() && ((int)cur.size() >= kTileT || (int)(cv.size() + add.size()) > kTileV)) {
+          tiles.push_back(cur);
+          cur.clear();
+          cv.clear();
+          for (int k = 0; k < 4; ++k) add.insert(G.tets[4 * e + k]);
+        }
+        cur.push_back(e);
+        cv.insert(add.begin(), add.end());
+      }
+      if (!cur.empty()) tiles.push_back(cur);
+    }
+    // how many tiles touch each vertex (exclusive vertices can be flushed without atomics)
+    for (size_t ti = 0; ti < tiles.size(); ++ti) {
+      std::set<int> vs;
+      for (int e : tiles[ti]) for (int k = 0; k < 4; ++k) vs.insert(G.tets[4 * e + k]);
+      for (int v : vs) vcount_tiles[v] += 1;
+    }
+    for (size_t ti = 0; ti < tiles.size(); ++ti) {
+      std::vector<int> verts;
+      for (int e : tiles[ti]) for (int k = 0; k < 4; ++k) {
+        int v = G.tets[4 * e + k];
+        if (vlocal[v] < 0) { vlocal[v] = (int)verts.size(); verts.push_back(v); }
+      }
+      for (int v : verts) {
+        tile_verts.push_back(v);
+        tile_vfl.push_back((unsigned char)((vflag[v] & 1) | (vcount_tiles[v] == 1 ? 2 : 0)));
+      }
+      tile_vstart.push_back((int)tile_verts.size());
+      for (int e : tiles[ti]) {
+        const int* t = G.tets + 4 * e;
+        tile_tv.push_back(make_uchar4((unsigned char)vlocal[t[0]], (unsigned char)vlocal[t[1]],
+                                      (unsigned char)vlocal[t[2]], (unsigned char)vlocal[t[3]]));
+        for (int r = 0; r < 3; ++r) tile_tb.push_back(tetb[3 * e + r]);
+      }
+      tile_tstart.push_back((int)tile_tv.size());
+      // rounds: greedy, each round <= kTileW tets with pairwise disjoint vertices
+      std::vector<int> left(tiles[ti].size());
+      std::iota(left.begin(), left.end(), 0);
+      while (!left.empty()) {
+        std::vector<int> round, rest;
+        std::set<int> used;
+        for (int li : left) {
+          const int* t = G.tets + 4 * tiles[ti][li];
+          bool ok = (int)round.size() < kTileW;
+          for (int k = 0; k < 4 && ok; ++k) ok = !used.count(t[k]);
+          if (ok) {
+            round.push_back(li);
+            for (int k = 0; k < 4; ++k) used.insert(t[k]);
+          } else {
+            rest.push_back(li);
+          }
+        }
+        for (int wslot = 0; wslot < kTileW; ++wslot)
+          tile_sched.push_back(wslot < (int)round.size() ? (short)round[wslot] : (short)-1);
+        left.swap(rest);
+      }
+      tile_rstart.push_back((int)tile_sched.size() / kTileW);
+      for (int v : verts) vlocal[v] = -1;
+    }
+  }
   // sizes and parameters
   d.nv = nv; d.nt = nt; d.nsv = (int)sim->sv.size(); d.nse = (int)ses.size(); d.nst = (int)st.size();
   d.niv = niv; d.nie = (int)ies.size(); d.nit = nit; d.nm = nm;
@@ -439,6 +540,15 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     UP(prims, d.bvh_prims);
     UP(mki, d.mk_idx);
     UP(mkw, d.mk_w);
+    UP(tile_vstart, d.tile_vstart);
+    UP(tile_verts, d.tile_verts);
+    UP(tile_vfl, d.tile_vfl);
+    UP(tile_tstart, d.tile_tstart);
+    UP(tile_tv, d.tile_tv);
+    UP(tile_tb, d.tile_tb);
+    UP(tile_rstart, d.tile_rstart);
+    UP(tile_sched, d.tile_sched);
+    d.ntiles = (int)tile_vstart.size() - 1;
     size_t nvec = 3 * (size_t)nv * d.Es;
     if ((rc = zalloc(sim, nvec, &d.u)) || (rc = zalloc(sim, nvec, &d.ut)) || (rc = zalloc(sim, nvec, &d.vt)) ||
         (rc = zalloc(sim, nvec, &d.uh)) || (rc = zalloc(sim, nvec, &d.g)) || (rc = zalloc(sim, nvec, &d.gp)) ||

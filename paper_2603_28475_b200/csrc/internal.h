@@ -12,6 +12,10 @@
 namespace tac {
 
 constexpr int kNodeLeaf = 4;
+// element tiles (k_elem_*_tiled): Morton-ordered tets grouped into tiles of <= kTileT tets
+// touching <= kTileV vertices; each tile is scheduled into rounds of <= kTileW
+// vertex-disjoint tets (one per warp) so shared-memory accumulation needs no atomics
+constexpr int kTileT = 128, kTileV = 64, kTileW = 8;
 
 struct BNode {  // indenter BVH node, body frame; leaf if left < 0: prims [-left-1, -left-1+right)
   float lo[3];
@@ -99,6 +103,16 @@ struct Dev {
   float mu, lam2;        // mu, lambda' = lambda + mu
   double rho_max, dhat, kappa_phys, eps_v, tol_x, k_t, k_r, f_max, t_max, ccd_s, bp_margin, c1, eps_E, mu_f;
   int beta_rule, precond, max_halv, stagnation, fixed_iters;
+  // element tiles
+  int ntiles;
+  const int* tile_vstart;        // [ntiles + 1] into tile_verts
+  const int* tile_verts;         // global vertex ids
+  const unsigned char* tile_vfl; // bit0 fixed, bit1 touched only by this tile
+  const int* tile_tstart;        // [ntiles + 1] into tile_tv / tile_tb
+  const uchar4* tile_tv;         // tile-local vertex indices of each tile tet
+  const float4* tile_tb;         // [3 per tile tet] (b1, vol), (b2, 0), (b3, 0)
+  const int* tile_rstart;        // [ntiles + 1] into tile_sched (in rounds)
+  const short* tile_sched;       // [rounds][kTileW] tile-local tet index or -1
   double t1[3], t2[3], nrm[3];
 };
 
@@ -120,6 +134,7 @@ void launch_stats(const Dev& d, int4* out, cudaStream_t s);
 // debug
 void launch_debug_broadphase(const Dev& d, double r, unsigned long long* out, int* cnt, int cap, cudaStream_t s);
 int launches_per_iteration();
+void kernels_init();  // per-device kernel attributes (call after cudaSetDevice)
 extern thread_local long long g_launches;
 
 // ---- optional per-kernel CUDA-event profiling (bench.py roofline; off by default) ----
