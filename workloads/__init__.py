@@ -268,7 +268,7 @@ class Params:
     beta_rule: int = 0      # 0 DK, 1 PR+, 2 FR
     precond: int = 0        # 0 3x3 block Jacobi, 1 scalar Jacobi
     max_halvings: int = 10
-    stagnation: int = 200
+    stagnation: int = 3000
 
 
 @dataclass
