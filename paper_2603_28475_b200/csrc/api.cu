@@ -296,7 +296,6 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     delete sim;
     return fail(TAC_ECUDA, "cudaSetDevice failed");
   }
-  kernels_init();
   sim->sv.assign(svs.begin(), svs.end());
   for (auto& f : st) for (int k = 0; k < 3; ++k) sim->st_flat.push_back(f[k]);
   for (auto& e : ses) { sim->se_flat.push_back(e.first); sim->se_flat.push_back(e.second); }
@@ -488,6 +487,8 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     double lbar = ses.empty() ? 1e-3 : sl / ses.size();
     d.kappa_phys = 0.2 * MT.E * lbar * lbar / (12.25 * P.dhat);
   }
+  d.contact_smem = contact_smem_bytes(d.nsv, niv);
+  kernels_init(d.contact_smem);
   d.beta_rule = P.beta_rule; d.precond = P.precond; d.max_halv = P.max_halvings; d.stagnation = P.stagnation;
   d.fixed_iters = P.fixed_iters;
   for (int a = 0; a < 3; ++a) { d.t1[a] = MS.t1[a]; d.t2[a] = MS.t2[a]; d.nrm[a] = MS.n[a]; }
@@ -506,7 +507,14 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
   std::vector<int2> se2, ie2;
   for (auto& e : ses) se2.push_back(make_int2(e.first, e.second));
   for (auto& e : ies) ie2.push_back(make_int2(e.first, e.second));
-  std::vector<int4> st4, it4;
+  std::vector<int4> st4, it4, st4l;
+  std::vector<int2> se2l;
+  {
+    std::vector<int> sloc(nv, -1);
+    for (size_t i = 0; i < sim->sv.size(); ++i) sloc[sim->sv[i]] = (int)i;
+    for (auto& f : st) st4l.push_back(make_int4(sloc[f[0]], sloc[f[1]], sloc[f[2]], 0));
+    for (auto& e2 : ses) se2l.push_back(make_int2(sloc[e2.first], sloc[e2.second]));
+  }
   for (auto& f : st) st4.push_back(make_int4(f[0], f[1], f[2], 0));
   for (int i = 0; i < nit; ++i) it4.push_back(make_int4(I.tris[3 * i], I.tris[3 * i + 1], I.tris[3 * i + 2], 0));
   std::vector<int4> mki(nm);
@@ -533,6 +541,8 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     UP(sim->sv, d.sv);
     UP(se2, d.se);
     UP(st4, d.st);
+    UP(se2l, d.se_l);
+    UP(st4l, d.st_l);
     UP(Yf, d.Y);
     UP(ie2, d.ie);
     UP(it4, d.it);
@@ -558,7 +568,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
         (rc = zalloc(sim, (size_t)d.Es, &d.run)) || (rc = zalloc(sim, (size_t)d.Es, &d.pcf)) ||
         (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.cand)) || (rc = zalloc(sim, 2 * (size_t)d.E * d.kmax, &d.cgeo)) || (rc = zalloc(sim, (size_t)d.E, &d.ncand)) || (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.nearl)) ||
         (rc = zalloc(sim, (size_t)d.E, &d.nnear)) ||
-        (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc)) || (rc = zalloc(sim, (size_t)d.E, &d.nanc)) ||
+        (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc)) || (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc_f1)) || (rc = zalloc(sim, (size_t)d.E, &d.nanc)) ||
         (rc = zalloc(sim, 1, &sim->d_flag)) || (rc = zalloc(sim, (size_t)d.kmax, &sim->d_dbg_cand)) ||
         (rc = zalloc(sim, 1, &sim->d_dbg_cnt)) || (rc = zalloc(sim, 3 * (size_t)nv, &sim->d_scratch)))
       goto fail;

@@ -75,6 +75,9 @@ struct Dev {
   const int* sv;         // [nsv]
   const int2* se;        // [nse]
   const int4* st;        // [nst]
+  const int2* se_l;      // [nse] surface-local vertex indices
+  const int4* st_l;      // [nst] surface-local vertex indices
+  int contact_smem;      // dynamic shared bytes of the staged contact kernels (0 = use the unstaged ones)
   const float4* Y;       // [niv] body frame, w = |Y|
   const int2* ie;        // [nie]
   const int4* it;        // [nit]
@@ -98,6 +101,7 @@ struct Dev {
   int* nearl;            // [E][kmax] indices of near candidates (no separating-axis certificate)
   int* nnear;            // [E]
   Anchor* anc;           // [E][amax]
+  float* anc_f1;         // [E][amax] friction weight mu lambda f1(s) of the last evaluation
   int* nanc;             // [E]
   // material / params
   float mu, lam2;        // mu, lambda' = lambda + mu
@@ -134,7 +138,8 @@ void launch_stats(const Dev& d, int4* out, cudaStream_t s);
 // debug
 void launch_debug_broadphase(const Dev& d, double r, unsigned long long* out, int* cnt, int cap, cudaStream_t s);
 int launches_per_iteration();
-void kernels_init();  // per-device kernel attributes (call after cudaSetDevice)
+void kernels_init(int contact_smem);  // per-device kernel attributes (call after cudaSetDevice)
+int contact_smem_bytes(int nsv, int niv);  // 0 if the staged contact kernels do not fit
 extern thread_local long long g_launches;
 
 // ---- optional per-kernel CUDA-event profiling (bench.py roofline; off by default) ----

@@ -1001,6 +1001,7 @@ __global__ void __launch_bounds__(128) k_contact_grad(Dev d, double kappa, doubl
     double ml = d.mu_f * (double)A.lam;
     Ef += ml * moll_f(sn, eps_f);
     double f1 = ml * moll_f1(sn, eps_f);
+    d.anc_f1[(size_t)e * d.amax + i] = (float)f1;  // for the staged curvature pass
     d3 Tt = ta * t1 + tb * t2;
     double sig = 0;
     d3 rho = mk(0, 0, 0);
@@ -1045,6 +1046,378 @@ __global__ void __launch_bounds__(128) k_contact_grad(Dev d, double kappa, doubl
     vals[14 + k] = Dt[k]; outs[14 + k] = d.acc + (size_t)(A_DR + 6 + k) * d.Es + e;
   }
   block_sums_atomic<20>(vals, outs, smr);
+}
+
+// ---- staged contact passes (default when the env's surface fits in shared memory) ----
+// One CTA per (env, chunk): the env's gel-surface displacements (float4 per surface
+// vertex) and the rotated indenter vertices R Y (fp64) are staged in shared memory once,
+// so every candidate reads its corners from shared memory instead of three scattered
+// 32-byte sectors per gel corner.  Pass 1 classifies (separating-axis certificate ->
+// g_min; otherwise a block-local near list), pass 2 runs the exact fp64 distances on
+// convergent warps, pass 3 the friction anchors.
+constexpr int kNearCap = 2048;
+struct CornersL {
+  int gid[4];  // gel: global vertex id; indenter: vertex id
+  int sid[4];  // gel: surface-local index
+  bool ind[4];
+  int na;
+};
+__device__ __forceinline__ CornersL corners_l(const Dev& d, int kind, int a, int b) {
+  CornersL c;
+  if (kind == 0) {
+    c.gid[0] = d.sv[a]; c.sid[0] = a; c.ind[0] = false;
+    int4 t = d.it[b];
+    c.gid[1] = t.x; c.gid[2] = t.y; c.gid[3] = t.z;
+    c.ind[1] = c.ind[2] = c.ind[3] = true;
+    c.na = 1;
+  } else if (kind == 1) {
+    c.gid[0] = a; c.ind[0] = true;
+    int4 t = d.st[b], tl = d.st_l[b];
+    c.gid[1] = t.x; c.gid[2] = t.y; c.gid[3] = t.z;
+    c.sid[1] = tl.x; c.sid[2] = tl.y; c.sid[3] = tl.z;
+    c.ind[1] = c.ind[2] = c.ind[3] = false;
+    c.na = 1;
+  } else {
+    int2 ge = d.se[a], gl = d.se_l[a], ie = d.ie[b];
+    c.gid[0] = ge.x; c.gid[1] = ge.y; c.sid[0] = gl.x; c.sid[1] = gl.y;
+    c.gid[2] = ie.x; c.gid[3] = ie.y;
+    c.ind[0] = c.ind[1] = false;
+    c.ind[2] = c.ind[3] = true;
+    c.na = 2;
+  }
+  return c;
+}
+struct Stage {
+  float4* sv4;  // [nsv] staged per-surface-vertex vector (u or p)
+  double* sy;   // [3 niv] R Y
+  int* nl;      // [kNearCap] block near list
+};
+__device__ __forceinline__ Stage stage_ptrs(const Dev& d, char* sh) {
+  Stage S;
+  S.sy = reinterpret_cast<double*>(sh);
+  S.sv4 = reinterpret_cast<float4*>(sh + sizeof(double) * 3 * d.niv);
+  S.nl = reinterpret_cast<int*>(sh + sizeof(double) * 3 * d.niv + sizeof(float4) * d.nsv);
+  return S;
+}
+__device__ void stage_env(const Dev& d, const Stage& S, const float* vec, int e, const double* R) {
+  for (int i = threadIdx.x; i < d.nsv; i += blockDim.x) {
+    int v = d.sv[i];
+    S.sv4[i] = make_float4(vec[vidx(d, 0, v, e)], vec[vidx(d, 1, v, e)], vec[vidx(d, 2, v, e)], 0.f);
+  }
+  for (int j = threadIdx.x; j < d.niv; j += blockDim.x) {
+    d3 y = mv(R, ind_body(d, j));
+    S.sy[3 * j] = y.x; S.sy[3 * j + 1] = y.y; S.sy[3 * j + 2] = y.z;
+  }
+}
+__device__ __forceinline__ d3 staged_gel_pos(const Dev& d, const Stage& S, int gid, int sid) {
+  float4 X = __ldg(d.X + gid);
+  float4 u = S.sv4[sid];
+  return mk((double)X.x + (double)u.x, (double)X.y + (double)u.y, (double)X.z + (double)u.z);
+}
+
+__global__ void __launch_bounds__(256) k_contact_eval(Dev d, double kappa, double eps_f) {
+  extern __shared__ __align__(16) char shc2[];
+  int e = blockIdx.y;
+  if (e >= d.E || !(d.run[e] & 1)) return;
+  const EnvS& s = d.es[e];
+  __shared__ double R[9], c[3], Rt[9], ct[3];
+  __shared__ double smr[8 * 20];
+  __shared__ int nnl, gbase;
+  if (threadIdx.x < 9) { R[threadIdx.x] = s.R[threadIdx.x]; Rt[threadIdx.x] = s.Rt[threadIdx.x]; }
+  if (threadIdx.x < 3) { c[threadIdx.x] = s.c[threadIdx.x]; ct[threadIdx.x] = s.ct[threadIdx.x]; }
+  if (threadIdx.x == 0) nnl = 0;
+  __syncthreads();
+  Stage S = stage_ptrs(d, shc2);
+  stage_env(d, S, d.u, e, R);
+  __syncthreads();
+  d3 cc = ld3(c);
+  auto pos = [&](const CornersL& C, int k) -> d3 {
+    if (C.ind[k]) return cc + mk(S.sy[3 * C.gid[k]], S.sy[3 * C.gid[k] + 1], S.sy[3 * C.gid[k] + 2]);
+    return staged_gel_pos(d, S, C.gid[k], C.sid[k]);
+  };
+  // passes 1-2 over this block's contiguous chunk, in sub-chunks of kNearCap candidates so
+  // the shared near list cannot overflow
+  const int n = min(d.ncand[e], d.kmax);
+  const int chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int c0 = blockIdx.x * chunk, c1 = min(n, c0 + chunk);
+  const unsigned long long* cand = d.cand + (size_t)e * d.kmax;
+  int* gnear = d.nearl + (size_t)e * d.kmax;
+  double gmin = INFINITY;
+  double Eb = 0, Ef = 0, gr[6] = {0, 0, 0, 0, 0, 0}, Dc[6] = {0, 0, 0, 0, 0, 0}, Dt[6] = {0, 0, 0, 0, 0, 0};
+  for (int s0 = c0; s0 < c1; s0 += kNearCap) {
+    const int s1 = min(c1, s0 + kNearCap);
+    // pass 1: classify (separating-axis certificate -> g_min, else near)
+    for (int i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
+      unsigned long long rec = cand[i];
+      int kind = (int)(rec >> 62), a = (int)((rec >> 31) & 0x7fffffffu), b = (int)(rec & 0x7fffffffu);
+      CornersL C = corners_l(d, kind, a, b);
+      d3 z[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) z[k] = pos(C, k);
+      double gsep;
+      d3 nsep;
+      if (axis_sep(z, C.na, d.dhat, &gsep, &nsep)) gmin = fmin(gmin, gsep);
+      else S.nl[atomicAdd(&nnl, 1)] = i;
+    }
+    __syncthreads();
+    const int nb = nnl;
+    if (threadIdx.x == 0) gbase = atomicAdd(d.nnear + e, nb);  // publish for the curvature pass
+    __syncthreads();
+    for (int j = threadIdx.x; j < nb; j += blockDim.x) gnear[gbase + j] = S.nl[j];
+    // pass 2: near pairs (exact distance, barrier, Gauss-Newton blocks, wrench)
+    for (int j = threadIdx.x; j < nb; j += blockDim.x) {
+      int i = S.nl[j];
+      unsigned long long rec = cand[i];
+      int kind = (int)(rec >> 62), a = (int)((rec >> 31) & 0x7fffffffu), b = (int)(rec & 0x7fffffffu);
+      CornersL C = corners_l(d, kind, a, b);
+      d3 z[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) z[k] = pos(C, k);
+      float4* geo = d.cgeo + 2 * ((size_t)e * d.kmax + i);
+      DR D = pair_dist(kind, z);
+      if (!(D.d > 0)) {
+        Eb = INFINITY;
+        geo[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+        geo[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        continue;
+      }
+      d3 rr = mk(0, 0, 0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) rr = rr + D.w[k] * z[k];
+      d3 nn = (1.0 / D.d) * rr;
+      geo[0] = make_float4((float)D.d, (float)nn.x, (float)nn.y, (float)nn.z);
+      geo[1] = make_float4((float)D.w[0], (float)D.w[1], (float)D.w[2], (float)D.w[3]);
+      if (D.d >= d.dhat) continue;
+      double lg = log(D.d / d.dhat), dm = D.d - d.dhat, inv = 1.0 / D.d;
+      Eb += kappa * (-dm * dm * lg);
+      double db = kappa * (-2 * dm * lg - dm * dm * inv);
+      double ddb = kappa * (-2 * lg - 4 * dm * inv + dm * dm * inv * inv);
+      double sig = 0;
+      d3 rho = mk(0, 0, 0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        d3 f = (db * D.w[k]) * nn;
+        if (!C.ind[k]) {
+          scatter_gel(d, C.gid[k], e, f, ddb * D.w[k] * D.w[k], nn);
+        } else {
+          d3 arm = z[k] - cc;
+          d3 tq = cross(arm, f);
+          gr[0] += f.x; gr[1] += f.y; gr[2] += f.z; gr[3] += tq.x; gr[4] += tq.y; gr[5] += tq.z;
+          sig += D.w[k];
+          rho = rho + D.w[k] * arm;
+        }
+      }
+      add_sym(Dc, nn, ddb * sig * sig);
+      add_sym(Dt, cross(rho, nn), ddb);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) nnl = 0;
+    __syncthreads();
+  }
+  gmin = warp_min(gmin);
+  if ((threadIdx.x & 31) == 0 && gmin < INFINITY) atomic_min_pos(d.accu + (size_t)U_GFAR * d.Es + e, (float)gmin);
+  // pass 3: friction anchors of this block's share
+  const int na = min(d.nanc[e], d.amax);
+  const int achunk = (na + gridDim.x - 1) / gridDim.x;
+  const int a0 = blockIdx.x * achunk, a1 = min(na, a0 + achunk);
+  for (int i = a0 + threadIdx.x; i < a1; i += blockDim.x) {
+    Anchor A = d.anc[(size_t)e * d.amax + i];
+    CornersL C = corners_l(d, A.kind, A.a, A.b);
+    d3 Dl = mk(0, 0, 0), z[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      d3 dz;
+      if (C.ind[k]) {
+        d3 yb = ind_body(d, C.gid[k]);
+        z[k] = pos(C, k);
+        dz = z[k] - (mv(Rt, yb) + ld3(ct));
+      } else {
+        float4 uu = S.sv4[C.sid[k]];
+        int v = C.gid[k];
+        dz = mk((double)uu.x - (double)d.ut[vidx(d, 0, v, e)], (double)uu.y - (double)d.ut[vidx(d, 1, v, e)],
+                (double)uu.z - (double)d.ut[vidx(d, 2, v, e)]);
+      }
+      Dl = Dl + (double)A.w[k] * dz;
+    }
+    d3 t1 = mk(A.t1[0], A.t1[1], A.t1[2]), t2 = mk(A.t2[0], A.t2[1], A.t2[2]);
+    double ta = dot(t1, Dl), tb = dot(t2, Dl);
+    double sn = sqrt(ta * ta + tb * tb);
+    double ml = d.mu_f * (double)A.lam;
+    Ef += ml * moll_f(sn, eps_f);
+    double f1 = ml * moll_f1(sn, eps_f);
+    d.anc_f1[(size_t)e * d.amax + i] = (float)f1;
+    d3 Tt = ta * t1 + tb * t2;
+    double sig = 0;
+    d3 rho = mk(0, 0, 0);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      double wk = A.w[k];
+      d3 f = (f1 * wk) * Tt;
+      if (!C.ind[k]) {
+        int v = C.gid[k];
+        if (d.vflag[v] & 1) continue;
+        atomicAdd(d.g + vidx(d, 0, v, e), (float)f.x);
+        atomicAdd(d.g + vidx(d, 1, v, e), (float)f.y);
+        atomicAdd(d.g + vidx(d, 2, v, e), (float)f.z);
+        double sw = f1 * wk * wk;
+        atomicAdd(d.D + vidx(d, 0, v, e), (float)(sw * (t1.x * t1.x + t2.x * t2.x)));
+        atomicAdd(d.D + vidx(d, 1, v, e), (float)(sw * (t1.y * t1.y + t2.y * t2.y)));
+        atomicAdd(d.D + vidx(d, 2, v, e), (float)(sw * (t1.z * t1.z + t2.z * t2.z)));
+        atomicAdd(d.D + vidx(d, 3, v, e), (float)(sw * (t1.x * t1.y + t2.x * t2.y)));
+        atomicAdd(d.D + vidx(d, 4, v, e), (float)(sw * (t1.x * t1.z + t2.x * t2.z)));
+        atomicAdd(d.D + vidx(d, 5, v, e), (float)(sw * (t1.y * t1.z + t2.y * t2.z)));
+      } else {
+        d3 arm = z[k] - cc;
+        d3 tq = cross(arm, f);
+        gr[0] += f.x; gr[1] += f.y; gr[2] += f.z; gr[3] += tq.x; gr[4] += tq.y; gr[5] += tq.z;
+        sig += wk;
+        rho = rho + wk * arm;
+      }
+    }
+    add_sym(Dc, t1, f1 * sig * sig);
+    add_sym(Dc, t2, f1 * sig * sig);
+    add_sym(Dt, cross(rho, t1), f1);
+    add_sym(Dt, cross(rho, t2), f1);
+  }
+  double vals[20];
+  double* outs[20];
+  vals[0] = Eb; outs[0] = d.acc + (size_t)A_EB * d.Es + e;
+  vals[1] = Ef; outs[1] = d.acc + (size_t)A_EF * d.Es + e;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    vals[2 + k] = gr[k]; outs[2 + k] = d.acc + (size_t)(A_GR + k) * d.Es + e;
+    vals[8 + k] = Dc[k]; outs[8 + k] = d.acc + (size_t)(A_DR + k) * d.Es + e;
+    vals[14 + k] = Dt[k]; outs[14 + k] = d.acc + (size_t)(A_DR + 6 + k) * d.Es + e;
+  }
+  block_sums_atomic<20>(vals, outs, smr);
+}
+
+// staged classification only (low register count): corners from shared memory,
+// separating-axis certificate -> g_min, otherwise appended to the env's near list
+__global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
+  extern __shared__ __align__(16) char shc4[];
+  int e = blockIdx.y;
+  if (e >= d.E || !(d.run[e] & 1)) return;
+  const EnvS& s = d.es[e];
+  __shared__ double R[9], c[3];
+  if (threadIdx.x < 9) R[threadIdx.x] = s.R[threadIdx.x];
+  if (threadIdx.x < 3) c[threadIdx.x] = s.c[threadIdx.x];
+  __syncthreads();
+  Stage S = stage_ptrs(d, shc4);
+  stage_env(d, S, d.u, e, R);
+  __syncthreads();
+  d3 cc = ld3(c);
+  const int n = min(d.ncand[e], d.kmax);
+  const unsigned long long* cand = d.cand + (size_t)e * d.kmax;
+  int* gnear = d.nearl + (size_t)e * d.kmax;
+  const int lane = threadIdx.x & 31;
+  double gmin = INFINITY;
+  const int stride = gridDim.x * blockDim.x;
+  for (int base = blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n; base += stride) {
+    int i = base + lane;
+    bool near = false;
+    if (i < n) {
+      unsigned long long rec = cand[i];
+      int kind = (int)(rec >> 62), a = (int)((rec >> 31) & 0x7fffffffu), b = (int)(rec & 0x7fffffffu);
+      CornersL C = corners_l(d, kind, a, b);
+      d3 z[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        z[k] = C.ind[k] ? cc + mk(S.sy[3 * C.gid[k]], S.sy[3 * C.gid[k] + 1], S.sy[3 * C.gid[k] + 2])
+                        : staged_gel_pos(d, S, C.gid[k], C.sid[k]);
+      double gsep;
+      d3 nsep;
+      if (axis_sep(z, C.na, d.dhat, &gsep, &nsep)) gmin = fmin(gmin, gsep);
+      else near = true;
+    }
+    unsigned m = __ballot_sync(0xffffffffu, near);
+    int slot0 = 0;
+    if (lane == 0 && m) slot0 = atomicAdd(d.nnear + e, __popc(m));
+    slot0 = __shfl_sync(0xffffffffu, slot0, 0);
+    if (near) gnear[slot0 + __popc(m & ((1u << lane) - 1))] = i;
+  }
+  gmin = warp_min(gmin);
+  if (lane == 0 && gmin < INFINITY) atomic_min_pos(d.accu + (size_t)U_GFAR * d.Es + e, (float)gmin);
+}
+
+// curvature + near-pair step bounds from the cached geometry, p staged in shared memory
+__global__ void __launch_bounds__(256) k_contact_curv_staged(Dev d, double kappa) {
+  extern __shared__ __align__(16) char shc3[];
+  int e = blockIdx.y;
+  if (e >= d.E || !(d.run[e] & 2)) return;
+  const EnvS& s = d.es[e];
+  __shared__ double R[9], pr[6];
+  __shared__ double sm[8];
+  if (threadIdx.x < 9) R[threadIdx.x] = s.R[threadIdx.x];
+  if (threadIdx.x < 6) pr[threadIdx.x] = s.pr[threadIdx.x];
+  __syncthreads();
+  Stage S = stage_ptrs(d, shc3);
+  stage_env(d, S, d.p, e, R);
+  __syncthreads();
+  d3 pc = mk(pr[0], pr[1], pr[2]), pth = mk(pr[3], pr[4], pr[5]);
+  double extra = nrm(pth) * d.dhat * 0.25;
+  auto motion = [&](const CornersL& C, int k) -> d3 {
+    if (C.ind[k]) return pc + cross(pth, mk(S.sy[3 * C.gid[k]], S.sy[3 * C.gid[k] + 1], S.sy[3 * C.gid[k] + 2]));
+    float4 p = S.sv4[C.sid[k]];
+    return mk(p.x, p.y, p.z);
+  };
+  double q = 0, amin = INFINITY;
+  const int n = d.nnear[e];
+  const unsigned long long* cand = d.cand + (size_t)e * d.kmax;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    int i = d.nearl[(size_t)e * d.kmax + j];
+    unsigned long long rec = cand[i];
+    int kind = (int)(rec >> 62), a = (int)((rec >> 31) & 0x7fffffffu), b = (int)(rec & 0x7fffffffu);
+    CornersL C = corners_l(d, kind, a, b);
+    const float4* geo = d.cgeo + 2 * ((size_t)e * d.kmax + i);
+    float4 g0 = geo[0], g1 = geo[1];
+    double dist = g0.x;
+    if (!(dist > 0)) continue;
+    d3 nn = mk(g0.y, g0.z, g0.w);
+    double w[4] = {g1.x, g1.y, g1.z, g1.w};
+    d3 dz[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) dz[k] = motion(C, k);
+    if (dist < d.dhat) {
+      d3 dr = mk(0, 0, 0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dr = dr + w[k] * dz[k];
+      double dn = dot(nn, dr);
+      double lg = log(dist / d.dhat), dm = dist - d.dhat, inv = 1.0 / dist;
+      q += kappa * (-2 * lg - 4 * dm * inv + dm * dm * inv * inv) * dn * dn;
+    }
+    double la = -INFINITY, lb = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < C.na) la = fmax(la, -dot(nn, dz[k]));
+      else lb = fmax(lb, dot(nn, dz[k]));
+    }
+    double l = la + lb + extra;
+    if (l > 0) amin = fmin(amin, (1 - d.ccd_s) * dist / l);
+  }
+  const int na = min(d.nanc[e], d.amax);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
+    Anchor A = d.anc[(size_t)e * d.amax + i];
+    CornersL C = corners_l(d, A.kind, A.a, A.b);
+    d3 dD = mk(0, 0, 0);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) dD = dD + (double)A.w[k] * motion(C, k);
+    d3 t1 = mk(A.t1[0], A.t1[1], A.t1[2]), t2 = mk(A.t2[0], A.t2[1], A.t2[2]);
+    double ta = dot(t1, dD), tb = dot(t2, dD);
+    q += (double)d.anc_f1[(size_t)e * d.amax + i] * (ta * ta + tb * tb);
+  }
+  // block reductions: sum q, min amin
+  q = warp_sum(q);
+  amin = warp_min(amin);
+  __shared__ double smin[8];
+  if ((threadIdx.x & 31) == 0) { sm[threadIdx.x >> 5] = q; smin[threadIdx.x >> 5] = amin; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0, m = INFINITY;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { t += sm[w]; m = fmin(m, smin[w]); }
+    if (t != 0.0) atomicAdd(d.acc + (size_t)A_PHP * d.Es + e, t);
+    if (m < INFINITY) atomic_min_pos(d.accu + (size_t)U_ACCD * d.Es + e, (float)m);
+  }
 }
 
 // ------------------------------------------------------------------ a8: Armijo accept (per env)
@@ -1692,6 +2065,10 @@ static dim3 cgrid(const Dev& d) {
   return dim3(nb, d.E);
 }
 static int eblocks(const Dev& d) { return (d.E + 127) / 128; }
+static dim3 sgrid(const Dev& d) {  // staged contact kernels: chunks per env
+  int nb = std::max(1, std::min(16, 2368 / std::max(1, d.E)));
+  return dim3(nb, d.E);
+}
 #define LAUNCHK(kid, s, ...)         \
   do {                                \
     if (g_prof) prof_begin(kid, s);   \
@@ -1720,7 +2097,13 @@ void launch_eval(const Dev& d, double h, cudaStream_t s) {
   // the round-scheduled tiled variant (k_elem_grad_tiled) measured slower on C3 (740 vs 520 us:
   // 66 % warp utilisation in the rounds, 2 CTAs/SM); the atomic scatter version stays
   LAUNCHK(KID_ELEM_GRAD, s, (k_elem_grad<<<vgrid(d, d.nt), dim3(32, 8), 0, s>>>(d, (float)(h * h))));
-  LAUNCHK(KID_CONTACT_CLASSIFY, s, (k_contact_classify<<<cgrid(d), 128, 0, s>>>(d)));
+  // the fused staged kernel (k_contact_eval) needs 174 registers (1 CTA/SM) and measured
+  // slower; classification is staged, the near pairs run in their own kernel
+  if (d.contact_smem > 0) {
+    LAUNCHK(KID_CONTACT_CLASSIFY, s, (k_contact_classify_staged<<<sgrid(d), 256, d.contact_smem, s>>>(d)));
+  } else {
+    LAUNCHK(KID_CONTACT_CLASSIFY, s, (k_contact_classify<<<cgrid(d), 128, 0, s>>>(d)));
+  }
   LAUNCHK(KID_CONTACT_GRAD, s, (k_contact_grad<<<cgrid(d), 128, 0, s>>>(d, h * h * d.kappa_phys, d.eps_v * h)));
   LAUNCHK(KID_ACCEPT, s, (k_accept<<<eblocks(d), 128, 0, s>>>(d, h)));
 }
@@ -1731,7 +2114,11 @@ void launch_direction(const Dev& d, cudaStream_t s) {
 }
 void launch_curvature(const Dev& d, double h, cudaStream_t s) {
   LAUNCHK(KID_ELEM_CURV, s, (k_elem_curv_tiled<<<dim3(d.Es / 32, d.ntiles), 256, kTiledCurvSmem, s>>>(d, (float)(h * h))));
-  LAUNCHK(KID_CONTACT_CURV, s, (k_contact_curv<<<cgrid(d), 128, 0, s>>>(d, h * h * d.kappa_phys, d.eps_v * h, 0)));
+  if (d.contact_smem > 0) {
+    LAUNCHK(KID_CONTACT_CURV, s, (k_contact_curv_staged<<<sgrid(d), 256, d.contact_smem, s>>>(d, h * h * d.kappa_phys)));
+  } else {
+    LAUNCHK(KID_CONTACT_CURV, s, (k_contact_curv<<<cgrid(d), 128, 0, s>>>(d, h * h * d.kappa_phys, d.eps_v * h, 0)));
+  }
 }
 void launch_alpha(const Dev& d, double h, cudaStream_t s) {
   LAUNCHK(KID_ALPHA, s, (k_alpha<<<eblocks(d), 128, 0, s>>>(d, h, 1)));
@@ -1766,7 +2153,16 @@ void launch_debug_broadphase(const Dev& d, double r, unsigned long long* out, in
   int ntot = d.nsv + d.nse + d.nst;
   LAUNCHK(KID_BROADPHASE, s, (k_broadphase<<<dim3((ntot + 127) / 128, d.E), 128, 0, s>>>(d, 0, r, out, cnt, cap)));
 }
-void kernels_init() {
+int contact_smem_bytes(int nsv, int niv) {
+  size_t b = sizeof(double) * 3 * (size_t)niv + sizeof(float4) * (size_t)nsv + sizeof(int) * kNearCap;
+  return b <= 160 * 1024 ? (int)b : 0;
+}
+void kernels_init(int contact_smem) {
+  if (contact_smem > 0) {
+    cudaFuncSetAttribute(k_contact_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, contact_smem);
+    cudaFuncSetAttribute(k_contact_classify_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, contact_smem);
+    cudaFuncSetAttribute(k_contact_curv_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, contact_smem);
+  }
   cudaFuncSetAttribute(k_elem_grad_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, kTiledGradSmem);
   cudaFuncSetAttribute(k_elem_curv_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, kTiledCurvSmem);
 }
