@@ -488,6 +488,10 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     d.kappa_phys = 0.2 * MT.E * lbar * lbar / (12.25 * P.dhat);
   }
   d.contact_smem = contact_smem_bytes(d.nsv, niv);
+  if (d.contact_smem == 0) {
+    delete sim;
+    return fail(TAC_EINVAL, "gel surface + indenter too large for the shared-memory staged contact passes");
+  }
   kernels_init(d.contact_smem);
   d.beta_rule = P.beta_rule; d.precond = P.precond; d.max_halv = P.max_halvings; d.stagnation = P.stagnation;
   d.fixed_iters = P.fixed_iters;
@@ -509,9 +513,11 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
   for (auto& e : ies) ie2.push_back(make_int2(e.first, e.second));
   std::vector<int4> st4, it4, st4l;
   std::vector<int2> se2l;
+  std::vector<int> sidx_h(nv, -1);
   {
     std::vector<int> sloc(nv, -1);
     for (size_t i = 0; i < sim->sv.size(); ++i) sloc[sim->sv[i]] = (int)i;
+    sidx_h = sloc;
     for (auto& f : st) st4l.push_back(make_int4(sloc[f[0]], sloc[f[1]], sloc[f[2]], 0));
     for (auto& e2 : ses) se2l.push_back(make_int2(sloc[e2.first], sloc[e2.second]));
   }
@@ -543,6 +549,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     UP(st4, d.st);
     UP(se2l, d.se_l);
     UP(st4l, d.st_l);
+    UP(sidx_h, d.sidx);
     UP(Yf, d.Y);
     UP(ie2, d.ie);
     UP(it4, d.it);
@@ -566,8 +573,9 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
         (rc = zalloc(sim, (size_t)kNAcc * d.Es, &d.acc)) || (rc = zalloc(sim, (size_t)kNAccU * d.Es, &d.accu)) ||
         (rc = zalloc(sim, (size_t)d.Es, &d.dalpha)) || (rc = zalloc(sim, (size_t)d.Es, &d.beta)) ||
         (rc = zalloc(sim, (size_t)d.Es, &d.run)) || (rc = zalloc(sim, (size_t)d.Es, &d.pcf)) ||
-        (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.cand)) || (rc = zalloc(sim, 2 * (size_t)d.E * d.kmax, &d.cgeo)) || (rc = zalloc(sim, (size_t)d.E, &d.ncand)) || (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.nearl)) ||
-        (rc = zalloc(sim, (size_t)d.E, &d.nnear)) ||
+        (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.cand)) || (rc = zalloc(sim, 2 * (size_t)d.E * d.kmax, &d.cgeo)) || (rc = zalloc(sim, (size_t)d.E, &d.ncand)) || (rc = zalloc(sim, 3 * (size_t)d.E * d.kmax, &d.nearl)) ||
+        (rc = zalloc(sim, 3 * (size_t)d.E, &d.nnear)) ||
+        (rc = zalloc(sim, (size_t)std::max(1, d.nsv) * d.Es, &d.usurf)) || (rc = zalloc(sim, (size_t)std::max(1, d.nsv) * d.Es, &d.psurf)) ||
         (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc)) || (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc_f1)) || (rc = zalloc(sim, (size_t)d.E, &d.nanc)) ||
         (rc = zalloc(sim, 1, &sim->d_flag)) || (rc = zalloc(sim, (size_t)d.kmax, &sim->d_dbg_cand)) ||
         (rc = zalloc(sim, 1, &sim->d_dbg_cnt)) || (rc = zalloc(sim, 3 * (size_t)nv, &sim->d_scratch)))

@@ -98,8 +98,11 @@ struct Dev {
   unsigned long long* cand;  // [E][kmax] (kind<<62 | a<<31 | b)
   float4* cgeo;          // [E][kmax][2] pair geometry of the last evaluation: (d, n), (w0..w3)
   int* ncand;            // [E]
-  int* nearl;            // [E][kmax] indices of near candidates (no separating-axis certificate)
-  int* nnear;            // [E]
+  int* nearl;            // [E][3][kmax] indices of near candidates (no separating-axis certificate), per pair kind
+  int* nnear;            // [E][3]
+  const int* sidx;       // [nv] surface-local index of a gel vertex, -1 if not on the surface
+  float4* usurf;         // [nsv][Es] u of the surface vertices at the last evaluation
+  float4* psurf;         // [nsv][Es] p of the surface vertices (current direction)
   Anchor* anc;           // [E][amax]
   float* anc_f1;         // [E][amax] friction weight mu lambda f1(s) of the last evaluation
   int* nanc;             // [E]
