@@ -34,6 +34,12 @@ sys.path.insert(0, ROOT)
 FIXED_ITERS = 50
 ENVS_PER_GPU = 1024
 METRIC = "env-steps/sec (marker fields/sec) at 1/2/4/8 B200; % of HBM roofline"
+WORKLOADS = {
+    "c3": "C3: 1024 envs/GPU peg-insertion trajectories (press, shear, twist, release), 19,800-tet / 4,278-vertex pad, "
+          "8 mm diameter cylinder peg, 7x9 markers",
+    "c3u": "C3 on the unstructured pad (jittered interior, random vertex/tet numbering; SURVEY 8f-1)",
+    "c5": "C5 stress: 103,680-tet / 19,943-vertex pad, sharp 8x8 mm square peg (face / edge press, slide, twist)",
+}
 
 
 def _peaks():
@@ -119,7 +125,12 @@ def run_ours(args, rank, local, ws):
     else:  # weak: a fixed env count per GPU, distinct env ids per rank
         e0, e1 = rank * args.envs, (rank + 1) * args.envs
     E = e1 - e0
-    scene = w.scene_c3(n_envs=E, n_steps=nsteps, seed0=20260000 + e0)
+    if args.config == "c5":
+        scene = w.scene_c5(n_envs=E, n_steps=nsteps, seed0=20270000 + e0)
+    elif args.config == "c3u":
+        scene = w.scene_c3_unstructured(n_envs=E, n_steps=nsteps, seed0=20260000 + e0)
+    else:
+        scene = w.scene_c3(n_envs=E, n_steps=nsteps, seed0=20260000 + e0)
     scene.params.fixed_iters = FIXED_ITERS
     sim = P.TacSim.from_scene(scene, device=local)
     poses = torch.tensor(scene.poses, dtype=torch.float32, device=dev).contiguous()  # resident in HBM
@@ -241,8 +252,7 @@ def run_ours(args, rank, local, ws):
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": "f32 (fp64 per-env reductions and rigid DOFs)",
         "data": "synthetic (seeded generators: workloads/)",
-        "config": {"workload": "C3: 1024 envs/GPU peg-insertion trajectories (press, shear, twist, release), "
-                               "19,800-tet / 4,278-vertex pad, Ø8 mm cylinder peg, 7x9 markers",
+        "config": {"workload": WORKLOADS[args.config],
                    "envs_per_gpu": E, "total_envs": n_all, "iters_per_step": FIXED_ITERS, "iteration_mode": "fixed",
                    "parallelism": f"env-sharded dp{ws}" + (" + NCCL all-gather of markers" if ws > 1 else ""),
                    "l2": "per-env state ~470 MB/GPU > 126 MB L2 (no flush needed)"},
@@ -314,12 +324,15 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--envs", type=int, default=ENVS_PER_GPU)
+    ap.add_argument("--envs", type=int, default=None, help="envs per GPU (default 1024; 256 for c5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--config", default="c3", choices=["c3", "c3u", "c5"])
     ap.add_argument("--total-envs", type=int, default=8192, help="strong scaling: envs over all ranks (C4)")
     args = ap.parse_args()
     assert args.warmup >= 1
+    if args.envs is None:
+        args.envs = 256 if args.config == "c5" else ENVS_PER_GPU
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
         ws = int(os.environ.get("WORLD_SIZE", str(args.gpus)))

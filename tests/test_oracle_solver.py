@@ -424,3 +424,17 @@ def test_newton_pins_whole_step_minimiser():
     u_n, c_n, R_n = x
     assert np.abs(u_n - u_ref).max() <= 1e-9 * 16e-3
     assert np.linalg.norm(c_n - c_ref) <= 1e-9 * 16e-3
+
+
+def test_unstructured_mesh_invariants():
+    """§8f-1: the oracle on a jittered, renumbered pad keeps its invariants (monotone E,
+    brute-force d_min > 0, fixed vertices 0) and converges."""
+    s = c1_press_scene(mu_f=1.0, steps=2, depth=0.1e-3)
+    s.X, s.tets, s.fixed = w.make_pad_unstructured(s.extent, s.cells)
+    o, trs = _run_steps(s, trace=True, debug=True, tol=1e-10)
+    for tr in trs:
+        acc = tr[tr[:, 2] == 1]
+        assert np.all(np.diff(acc[:, 1]) <= 0) and np.all(acc[:, 12] > 0)
+    assert o.status_of(0)["flags"] & 1
+    u = o.get_state(0)[0]
+    assert np.all(u[s.fixed] == 0) and np.abs(u).max() > 1e-6

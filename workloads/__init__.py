@@ -269,6 +269,8 @@ class Params:
     precond: int = 0        # 0 3x3 block Jacobi, 1 scalar Jacobi
     max_halvings: int = 10
     stagnation: int = 3000
+    max_candidates: int = 0   # 0 -> library default (16384 per env)
+    max_anchors: int = 0      # 0 -> library default (4096 per env)
 
 
 @dataclass
@@ -435,3 +437,80 @@ def scene_small_peg(n_envs=5, n_steps=4, seed0=20260000):
         poses.append(p)
     return Scene("small_peg", X, T, Fx, Y, tris, M, frame, np.stack(inits), np.stack(poses, axis=1),
                  extent=ext, cells=cells)
+
+
+# ----------------------------------------------------------------------------
+# §8f-1: unstructured-mesh workload ("unstructured mesh", 1,665 vs 4,465 FPS)
+# ----------------------------------------------------------------------------
+def make_pad_unstructured(extent, cells, jitter=0.2, seed=7, shuffle=True):
+    """Kuhn pad with every strictly interior vertex jittered by up to `jitter` cells per
+    axis (irregular element shapes) and, with `shuffle`, random vertex and tet numbering
+    (irregular memory access).  Boundary vertices keep their grid positions so the faces
+    stay planar and the fixed base / contact face are unchanged.  Positive volumes are
+    asserted."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    X, T, F = make_pad(extent, cells)
+    Lx, Ly, Lz = extent
+    c = np.array([Lx / cells[0], Ly / cells[1], Lz / cells[2]])
+    lo = np.array([-Lx / 2, -Ly / 2, -Lz])
+    hi = np.array([Lx / 2, Ly / 2, 0.0])
+    interior = np.all((X > lo + 1e-9) & (X < hi - 1e-9), axis=1)
+    X = X.copy()
+    X[interior] += rng.uniform(-jitter, jitter, (interior.sum(), 3)) * c
+    X = f32(X)
+    if shuffle:
+        perm = rng.permutation(len(X))          # new id -> old id
+        inv = np.empty_like(perm)
+        inv[perm] = np.arange(len(X))
+        X = X[perm]
+        T = inv[T]
+        F = np.sort(inv[F]).astype(np.int32)
+        T = T[rng.permutation(len(T))]
+    T = np.asarray(T, dtype=np.int32)
+    vol = np.einsum("ij,ij->i", np.cross(X[T[:, 1]] - X[T[:, 0]], X[T[:, 2]] - X[T[:, 0]]), X[T[:, 3]] - X[T[:, 0]])
+    assert vol.min() > 0, vol.min()
+    return X, T, np.asarray(F, dtype=np.int32)
+
+
+def scene_c3_unstructured(n_envs=1024, n_steps=64, seed0=20260000, cells=(30, 22, 5)):
+    s = scene_c3(n_envs=n_envs, n_steps=n_steps, seed0=seed0, cells=cells)
+    s.X, s.tets, s.fixed = make_pad_unstructured(s.extent, cells)
+    s.name = "C3u"
+    return s
+
+
+def scene_c5(n_envs=256, n_steps=64, seed0=20270000):
+    """C5 stress: 32x24x5 mm pad, 48x36x10 cells (103,680 tets / 19,943 verts); sharp-edged
+    8x8x24 mm square peg, faces split at 0.5 mm; press onto a face, then onto an edge
+    (rolled 45 deg), slide 2 mm, twist at 0.5 deg/step."""
+    ext, cells = (32 * MM, 24 * MM, 5 * MM), (48, 36, 10)
+    X, T, Fx = make_pad(ext, cells)
+    Y, tris = make_square_peg(8 * MM, 24 * MM, 0.5 * MM)
+    M, frame = make_markers(ext, cells)
+    inits, poses = [], []
+    for e in range(n_envs):
+        rng = np.random.Generator(np.random.PCG64(seed0 + e))
+        edge = e % 2 == 1  # half the envs press onto an edge
+        roll = quat_axis_angle((1, 0, 0), np.pi / 4) if edge else np.array([1.0, 0, 0, 0])
+        yaw = np.deg2rad(rng.uniform(-35, 35))
+        q0 = quat_mul(quat_axis_angle((0, 0, 1), yaw), roll)
+        h = 4 * MM * (2 ** 0.5 if edge else 1.0)
+        c = np.array([rng.uniform(-2, 2) * MM, rng.uniform(-2, 2) * MM, h + 0.1 * MM])
+        init = pose(c, q0)
+        traj = []
+        ang = 0.0
+        d = np.array([np.cos(yaw), np.sin(yaw), 0.0])
+        for s_ in range(n_steps):
+            if s_ < 11:
+                c = c + (0, 0, -0.1 * MM)
+            elif s_ < 31:
+                c = c + d * 0.1 * MM
+            elif s_ < 51:
+                ang += np.deg2rad(0.5) * (1 if s_ < 41 else -1)
+            traj.append(pose(c, quat_mul(quat_axis_angle((0, 0, 1), ang), q0)))
+        inits.append(init)
+        poses.append(np.stack(traj))
+    sc = Scene("C5", X, T, Fx, Y, tris, M, frame, np.stack(inits), np.stack(poses, axis=1), extent=ext, cells=cells)
+    sc.params.max_candidates = 65536  # edge presses of the split square peg reach ~46k pairs per env
+    sc.params.max_anchors = 16384
+    return sc
