@@ -240,7 +240,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
   // rest shape: b_k = rows of Dm^-1 (k = 1..3), V_e = det(Dm)/6, lumped mass rho V_e / 4 per vertex
   std::vector<float4> tetb(3 * (size_t)nt);
   std::vector<int4> tets(nt);
-  std::vector<double> massd(nv, 0.0);
+  std::vector<double> massd(nv, 0.0), smud(nv, 0.0);
   for (int e = 0; e < nt; ++e) {
     const int* t = G.tets + 4 * e;
     tets[e] = make_int4(t[0], t[1], t[2], t[3]);
@@ -253,7 +253,17 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     V r2 = {(a[1] * b[2] - a[2] * b[1]) / D, (a[2] * b[0] - a[0] * b[2]) / D, (a[0] * b[1] - a[1] * b[0]) / D};
     double vol = D / 6.0;
     tetb[3 * e] = make_float4((float)r0[0], (float)r0[1], (float)r0[2], (float)vol);
-    tetb[3 * e + 1] = make_float4((float)r1[0], (float)r1[1], (float)r1[2], 0.f);
+    unsigned fixmask = 0;
+    for (int k = 0; k < 4; ++k)
+      if (vflag[t[k]] & 1) fixmask |= 1u << k;
+    float fm;
+    memcpy(&fm, &fixmask, sizeof(float));
+    tetb[3 * e + 1] = make_float4((float)r1[0], (float)r1[1], (float)r1[2], fm);
+    {  // state-independent part of the exact diagonal blocks: V_e mu |b_k|^2 per corner
+      double mu_ = MT.E / (2 * (1 + MT.nu));
+      V b[4] = {{-(r0[0] + r1[0] + r2[0]), -(r0[1] + r1[1] + r2[1]), -(r0[2] + r1[2] + r2[2])}, r0, r1, r2};
+      for (int k = 0; k < 4; ++k) smud[t[k]] += vol * mu_ * (b[k][0] * b[k][0] + b[k][1] * b[k][1] + b[k][2] * b[k][2]);
+    }
     tetb[3 * e + 2] = make_float4((float)r2[0], (float)r2[1], (float)r2[2], 0.f);
     for (int k = 0; k < 4; ++k) massd[t[k]] += MT.rho * vol / 4.0;
   }
@@ -506,8 +516,8 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
   for (int i = 0; i < niv; ++i)
     Yf[i] = make_float4((float)Y[i][0], (float)Y[i][1], (float)Y[i][2],
                         (float)std::sqrt(Y[i][0] * Y[i][0] + Y[i][1] * Y[i][1] + Y[i][2] * Y[i][2]));
-  std::vector<float> massf(nv);
-  for (int i = 0; i < nv; ++i) massf[i] = (float)massd[i];
+  std::vector<float> massf(nv), smuf(nv);
+  for (int i = 0; i < nv; ++i) { massf[i] = (float)massd[i]; smuf[i] = (float)smud[i]; }
   std::vector<int2> se2, ie2;
   for (auto& e : ses) se2.push_back(make_int2(e.first, e.second));
   for (auto& e : ies) ie2.push_back(make_int2(e.first, e.second));
@@ -543,6 +553,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     UP(tetb, d.tetb);
     UP(Xf, d.X);
     UP(massf, d.mass);
+    UP(smuf, d.smu);
     UP(vflag, d.vflag);
     UP(sim->sv, d.sv);
     UP(se2, d.se);
@@ -759,24 +770,36 @@ tac_status tac_env_stats(tac_sim* sim, int32_t* out, void* stream) {
 }
 
 // ---------------------------------------------------------------- debug hooks
+// host <-> device copies of one env's vertex vector in the AoSoA layout [v][Es/32][c][32]
+static tac_status copy_env_comp(tac_sim* sim, float* host, const float* dev_base, int env, int c, int ncomp,
+                                bool to_host) {
+  const Dev& d = sim->d;
+  size_t pitch = sizeof(float) * (size_t)(d.Es / 32) * ncomp * 32;
+  size_t off = ((size_t)(env / 32) * ncomp + c) * 32 + (env % 32);
+  if (to_host)
+    CK(cudaMemcpy2D(host, sizeof(float), dev_base + off, pitch, sizeof(float), d.nv, cudaMemcpyDeviceToHost));
+  else
+    CK(cudaMemcpy2D((float*)dev_base + off, pitch, host, sizeof(float), sizeof(float), d.nv, cudaMemcpyHostToDevice));
+  return TAC_OK;
+}
 static tac_status gather_vec(tac_sim* sim, const float* dsrc, int env, double* out) {
   const Dev& d = sim->d;
-  std::vector<float> tmp(3 * (size_t)d.nv);
-  for (int c = 0; c < 3; ++c)
-    CK(cudaMemcpy2D(tmp.data() + (size_t)c * d.nv, sizeof(float), dsrc + (size_t)c * d.nv * d.Es + env,
-                    sizeof(float) * d.Es, sizeof(float), d.nv, cudaMemcpyDeviceToHost));
-  for (int v = 0; v < d.nv; ++v)
-    for (int c = 0; c < 3; ++c) out[3 * v + c] = tmp[(size_t)c * d.nv + v];
+  std::vector<float> tmp((size_t)d.nv);
+  for (int c = 0; c < 3; ++c) {
+    tac_status st = copy_env_comp(sim, tmp.data(), dsrc, env, c, 3, true);
+    if (st) return st;
+    for (int v = 0; v < d.nv; ++v) out[3 * v + c] = tmp[v];
+  }
   return TAC_OK;
 }
 static tac_status scatter_vec(tac_sim* sim, float* ddst, int env, const double* in) {
   const Dev& d = sim->d;
-  std::vector<float> tmp(3 * (size_t)d.nv);
-  for (int v = 0; v < d.nv; ++v)
-    for (int c = 0; c < 3; ++c) tmp[(size_t)c * d.nv + v] = (float)in[3 * v + c];
-  for (int c = 0; c < 3; ++c)
-    CK(cudaMemcpy2D(ddst + (size_t)c * d.nv * d.Es + env, sizeof(float) * d.Es, tmp.data() + (size_t)c * d.nv,
-                    sizeof(float), sizeof(float), d.nv, cudaMemcpyHostToDevice));
+  std::vector<float> tmp((size_t)d.nv);
+  for (int c = 0; c < 3; ++c) {
+    for (int v = 0; v < d.nv; ++v) tmp[v] = (float)in[3 * v + c];
+    tac_status st = copy_env_comp(sim, tmp.data(), ddst, env, c, 3, false);
+    if (st) return st;
+  }
   return TAC_OK;
 }
 
@@ -926,8 +949,7 @@ tac_status tac_debug_eval(tac_sim* sim, int32_t env, const double* u_t, const do
   if (D) {
     std::vector<float> tmp(6 * (size_t)d.nv);
     for (int c6 = 0; c6 < 6; ++c6)
-      CK(cudaMemcpy2D(tmp.data() + (size_t)c6 * d.nv, sizeof(float), d.D + (size_t)c6 * d.nv * d.Es + env,
-                      sizeof(float) * d.Es, sizeof(float), d.nv, cudaMemcpyDeviceToHost));
+      if ((st = copy_env_comp(sim, tmp.data() + (size_t)c6 * d.nv, d.D, env, c6, 6, true))) return st;
     for (int v = 0; v < d.nv; ++v) {
       float xx = tmp[v], yy = tmp[d.nv + v], zz = tmp[2 * d.nv + v], xy = tmp[3 * d.nv + v], xz = tmp[4 * d.nv + v],
             yz = tmp[5 * d.nv + v];

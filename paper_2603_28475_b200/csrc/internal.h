@@ -68,9 +68,10 @@ struct Dev {
   int kmax, amax;
   // static mesh
   const int4* tets;      // [nt]
-  const float4* tetb;    // [nt][3]: (b1, vol), (b2, 0), (b3, 0)
+  const float4* tetb;    // [nt][3]: (b1, vol), (b2, fixed-corner mask bits), (b3, 0)
   const float4* X;       // [nv] rest position (fp32 exact), w = 0
   const float* mass;     // [nv]
+  const float* smu;      // [nv] sum_e V_e mu |b_{e,v}|^2 (state-independent elastic diagonal / h^2)
   const unsigned char* vflag;  // [nv] bit0 fixed, bit1 on the gel surface
   const int* sv;         // [nsv]
   const int2* se;        // [nse]

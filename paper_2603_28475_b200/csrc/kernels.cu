@@ -24,9 +24,14 @@ static const char* kNames[KID_COUNT] = {
 const char* kernel_name(int kid) { return (kid >= 0 && kid < KID_COUNT) ? kNames[kid] : "?"; }
 
 // ------------------------------------------------------------------ small helpers
-// 32-bit offsets: tac_create guarantees 6 nv Es < 2^32
-__device__ __forceinline__ unsigned vidx(const Dev& d, int c, int v, int e) {
-  return ((unsigned)c * (unsigned)d.nv + (unsigned)v) * (unsigned)d.Es + (unsigned)e;
+// AoSoA layout [v][env_group][c][32] (lane = env % 32): the components of one vertex for one
+// warp are 128 B apart at compile-time offsets from a single per-vertex base.  32-bit offsets:
+// tac_create guarantees 6 nv Es < 2^32.
+__device__ __forceinline__ unsigned vidx(const Dev& d, int c, int v, int e) {  // 3-component arrays
+  return (((unsigned)v * (unsigned)(d.Es >> 5) + ((unsigned)e >> 5)) * 3u + (unsigned)c) * 32u + ((unsigned)e & 31u);
+}
+__device__ __forceinline__ unsigned vidxD(const Dev& d, int c, int v, int e) {  // D: 6 components
+  return (((unsigned)v * (unsigned)(d.Es >> 5) + ((unsigned)e >> 5)) * 6u + (unsigned)c) * 32u + ((unsigned)e & 31u);
 }
 struct d3 {
   double x, y, z;
@@ -535,7 +540,7 @@ __global__ void k_anchors(Dev d, double kappa) {
 // ------------------------------------------------------------------ a4: vertex pre-pass
 // applies the pending update u += dalpha p (a8), then the inertia term
 // 1/2 m |u - u^|^2, g = m (u - u^), D = m I (lumped M)
-__global__ void k_vert_pre(Dev d) {
+__global__ void k_vert_pre(Dev d, float h2) {
   int e = blockIdx.x * 32 + threadIdx.x;
   bool act = e < d.E && (d.run[e] & 1);
   if (!__any_sync(0xffffffffu, act)) return;
@@ -565,12 +570,13 @@ __global__ void k_vert_pre(Dev d) {
     }
     int si = d.sidx[v];
     if (si >= 0) d.usurf[(size_t)si * d.Es + e] = make_float4(uv[0], uv[1], uv[2], 0.f);
-    d.D[vidx(d, 0, v, e)] = m;
-    d.D[vidx(d, 1, v, e)] = m;
-    d.D[vidx(d, 2, v, e)] = m;
-    d.D[vidx(d, 3, v, e)] = 0.f;
-    d.D[vidx(d, 4, v, e)] = 0.f;
-    d.D[vidx(d, 5, v, e)] = 0.f;
+    const float dg = m + h2 * d.smu[v];  // mass + state-independent elastic diagonal (App. B)
+    d.D[vidxD(d, 0, v, e)] = dg;
+    d.D[vidxD(d, 1, v, e)] = dg;
+    d.D[vidxD(d, 2, v, e)] = dg;
+    d.D[vidxD(d, 3, v, e)] = 0.f;
+    d.D[vidxD(d, 4, v, e)] = 0.f;
+    d.D[vidxD(d, 5, v, e)] = 0.f;
   }
   if (act && ein != 0.0) atomicAdd(d.acc + (size_t)A_EIN * d.Es + e, ein);
 }
@@ -599,22 +605,32 @@ __device__ __forceinline__ void cof33(const float* A, float* C) {
   C[6] = A[1] * A[5] - A[2] * A[4]; C[7] = A[2] * A[3] - A[0] * A[5]; C[8] = A[0] * A[4] - A[1] * A[3];
 }
 
-__global__ void __launch_bounds__(256) k_elem_grad(Dev d, float h2) {
-  int e = blockIdx.x * 32 + threadIdx.x;
-  bool act = e < d.E && (d.run[e] & 1);
+__global__ void __launch_bounds__(256, 4) k_elem_grad(Dev d, float h2) {
+  // env group = blockIdx.y (slowest) so the g / D lines of the env groups in flight stay in L2
+  const int e = blockIdx.y * 32 + threadIdx.x;
+  const bool act = e < d.E && (d.run[e] & 1);
   if (!__any_sync(0xffffffffu, act)) return;
   const float mu = d.mu, l2 = d.lam2;
+  // AoSoA: one per-vertex base, components at immediate offsets of 32 floats
+  const unsigned G = (unsigned)(d.Es >> 5), eg = (unsigned)blockIdx.y, lane = threadIdx.x;
+  const float* __restrict__ up = d.u;
+  float* __restrict__ gp = d.g;
+  float* __restrict__ Dp = d.D;
   double esum = 0;
-  for (int t = blockIdx.y * 8 + threadIdx.y; t < d.nt; t += gridDim.y * 8) {
+  for (int t = blockIdx.x * 8 + threadIdx.y; t < d.nt; t += gridDim.x * 8) {
     int4 tv = __ldg(d.tets + t);
-    int vv[4] = {tv.x, tv.y, tv.z, tv.w};
     TetData T = load_tet(d, t);
+    const unsigned fixmask = __float_as_uint(__ldg(d.tetb + 3 * t + 1).w);  // bit k: corner k fixed
     if (!act) continue;
+    const unsigned vb[4] = {(unsigned)tv.x * G + eg, (unsigned)tv.y * G + eg, (unsigned)tv.z * G + eg,
+                            (unsigned)tv.w * G + eg};
     float uu[4][3];
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < 4; ++k) {
+      const float* p = up + (vb[k] * 3u * 32u + lane);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) uu[k][c] = d.u[vidx(d, c, vv[k], e)];
+      for (int c = 0; c < 3; ++c) uu[k][c] = p[32 * c];
+    }
     float G[9];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
@@ -635,53 +651,49 @@ __global__ void __launch_bounds__(256) k_elem_grad(Dev d, float h2) {
 #pragma unroll
     for (int i = 0; i < 9; ++i) GG = fmaf(G[i], G[i], GG);
     float w = h2 * T.vol;
-    float psi = mu * (0.5f * GG - i2 - detG) + 0.5f * l2 * Jm1 * Jm1;
-    esum += (double)(w * psi);
-    // cof F = (1 + trG) I - G^T + cof G
-    float cF[9];
+    esum += (double)(w * (mu * (0.5f * GG - i2 - detG) + 0.5f * l2 * Jm1 * Jm1));
+    // cof F = (1 + trG) I - G^T + cof G;  P(F) = mu (G + G^T - trG I - cof G) + lambda'(J-1) cof F
+    float cF[9], PK[9];
+    const float lj = l2 * Jm1;
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
-      for (int j = 0; j < 3; ++j) cF[3 * i + j] = (i == j ? 1.f + trG : 0.f) - G[3 * j + i] + cG[3 * i + j];
-    float PK[9];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int j = 0; j < 3; ++j)
-        PK[3 * i + j] = mu * (G[3 * i + j] + G[3 * j + i] - (i == j ? trG : 0.f) - cG[3 * i + j]) + l2 * Jm1 * cF[3 * i + j];
-    float f[4][3], cv[4][3], bb[4];
+      for (int j = 0; j < 3; ++j) {
+        cF[3 * i + j] = (i == j ? 1.f + trG : 0.f) - G[3 * j + i] + cG[3 * i + j];
+        PK[3 * i + j] = w * (mu * (G[3 * i + j] + G[3 * j + i] - (i == j ? trG : 0.f) - cG[3 * i + j]) + lj * cF[3 * i + j]);
+      }
+    float f[4][3], cv[4][3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) { f[0][c] = 0.f; cv[0][c] = 0.f; }
-    float b0[3] = {-(T.b[0][0] + T.b[1][0] + T.b[2][0]), -(T.b[0][1] + T.b[1][1] + T.b[2][1]),
-                   -(T.b[0][2] + T.b[1][2] + T.b[2][2])};
-    bb[0] = b0[0] * b0[0] + b0[1] * b0[1] + b0[2] * b0[2];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      bb[k + 1] = T.b[k][0] * T.b[k][0] + T.b[k][1] * T.b[k][1] + T.b[k][2] * T.b[k][2];
+    for (int k = 0; k < 3; ++k)
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
-        float fi = w * (PK[3 * i] * T.b[k][0] + PK[3 * i + 1] * T.b[k][1] + PK[3 * i + 2] * T.b[k][2]);
+        float fi = PK[3 * i] * T.b[k][0] + PK[3 * i + 1] * T.b[k][1] + PK[3 * i + 2] * T.b[k][2];
         float ci = cF[3 * i] * T.b[k][0] + cF[3 * i + 1] * T.b[k][1] + cF[3 * i + 2] * T.b[k][2];
         f[k + 1][i] = fi;
         cv[k + 1][i] = ci;
         f[0][i] -= fi;
         cv[0][i] -= ci;
       }
-    }
+    // diagonal blocks: the state-independent mu |b_k|^2 I part is precomputed per vertex (smu,
+    // added with the mass in k_vert_pre); here only lambda' c_k c_k^T
+    const float lc = w * l2;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      int v = vv[k];
-      if (d.vflag[v] & 1) continue;
-      atomicAdd(d.g + vidx(d, 0, v, e), f[k][0]);
-      atomicAdd(d.g + vidx(d, 1, v, e), f[k][1]);
-      atomicAdd(d.g + vidx(d, 2, v, e), f[k][2]);
-      float a = w * mu * bb[k], lc = w * l2;
-      atomicAdd(d.D + vidx(d, 0, v, e), a + lc * cv[k][0] * cv[k][0]);
-      atomicAdd(d.D + vidx(d, 1, v, e), a + lc * cv[k][1] * cv[k][1]);
-      atomicAdd(d.D + vidx(d, 2, v, e), a + lc * cv[k][2] * cv[k][2]);
-      atomicAdd(d.D + vidx(d, 3, v, e), lc * cv[k][0] * cv[k][1]);
-      atomicAdd(d.D + vidx(d, 4, v, e), lc * cv[k][0] * cv[k][2]);
-      atomicAdd(d.D + vidx(d, 5, v, e), lc * cv[k][1] * cv[k][2]);
+      if (fixmask & (1u << k)) continue;
+      float* pg = gp + (vb[k] * 3u * 32u + lane);
+      float* pd = Dp + (vb[k] * 6u * 32u + lane);
+      atomicAdd(pg, f[k][0]);
+      atomicAdd(pg + 32, f[k][1]);
+      atomicAdd(pg + 64, f[k][2]);
+      const float sx = lc * cv[k][0], sy = lc * cv[k][1];
+      atomicAdd(pd, sx * cv[k][0]);
+      atomicAdd(pd + 32, sy * cv[k][1]);
+      atomicAdd(pd + 64, lc * cv[k][2] * cv[k][2]);
+      atomicAdd(pd + 96, sx * cv[k][1]);
+      atomicAdd(pd + 128, sx * cv[k][2]);
+      atomicAdd(pd + 160, sy * cv[k][2]);
     }
   }
   if (act) atomicAdd(d.acc + (size_t)A_EEL * d.Es + e, esum);
@@ -700,129 +712,6 @@ __device__ __forceinline__ TetData load_tile_tet(const Dev& d, int gt) {
   T.b[2][0] = r2.x; T.b[2][1] = r2.y; T.b[2][2] = r2.z;
   return T;
 }
-constexpr int kTiledGradSmem = (3 + 9) * kTileV * 32 * 4;
-
-__global__ void __launch_bounds__(256, 2) k_elem_grad_tiled(Dev d, float h2) {
-  extern __shared__ float sh[];
-  float* su = sh;                      // [3][kTileV][32]
-  float* sa = sh + 3 * kTileV * 32;    // [9][kTileV][32]: g (3), D (xx, yy, zz, xy, xz, yz)
-  __shared__ double se[8][32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int e = blockIdx.x * 32 + lane, tile = blockIdx.y;
-  const bool act = e < d.E && (d.run[e] & 1);
-  if (!__syncthreads_or(act)) return;
-  const int v0 = d.tile_vstart[tile], nvt = d.tile_vstart[tile + 1] - v0;
-  for (int lv = w; lv < nvt; lv += 8) {
-    int gv = d.tile_verts[v0 + lv];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) su[(c * kTileV + lv) * 32 + lane] = act ? d.u[vidx(d, c, gv, e)] : 0.f;
-#pragma unroll
-    for (int c = 0; c < 9; ++c) sa[(c * kTileV + lv) * 32 + lane] = 0.f;
-  }
-  __syncthreads();
-  const float mu = d.mu, l2 = d.lam2;
-  const int t0 = d.tile_tstart[tile];
-  double esum = 0;
-  for (int r = d.tile_rstart[tile]; r < d.tile_rstart[tile + 1]; ++r) {
-    int lt = d.tile_sched[r * kTileW + w];
-    if (lt >= 0 && act) {
-      uchar4 tv = __ldg(d.tile_tv + t0 + lt);
-      int lv4[4] = {tv.x, tv.y, tv.z, tv.w};
-      TetData T = load_tile_tet(d, t0 + lt);
-      float uu[4][3];
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) uu[k][c] = su[(c * kTileV + lv4[k]) * 32 + lane];
-      float G[9];
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          float s = 0.f;
-#pragma unroll
-          for (int k = 0; k < 3; ++k) s = fmaf(uu[k + 1][i] - uu[0][i], T.b[k][j], s);
-          G[3 * i + j] = s;
-        }
-      float trG = G[0] + G[4] + G[8];
-      float i2 = (G[0] * G[4] - G[1] * G[3]) + (G[0] * G[8] - G[2] * G[6]) + (G[4] * G[8] - G[5] * G[7]);
-      float cG[9];
-      cof33(G, cG);
-      float detG = G[0] * cG[0] + G[1] * cG[1] + G[2] * cG[2];
-      float Jm1 = trG + i2 + detG;
-      float GG = 0.f;
-#pragma unroll
-      for (int i = 0; i < 9; ++i) GG = fmaf(G[i], G[i], GG);
-      float wv = h2 * T.vol;
-      esum += (double)(wv * (mu * (0.5f * GG - i2 - detG) + 0.5f * l2 * Jm1 * Jm1));
-      float cF[9], PK[9];
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          cF[3 * i + j] = (i == j ? 1.f + trG : 0.f) - G[3 * j + i] + cG[3 * i + j];
-          PK[3 * i + j] = mu * (G[3 * i + j] + G[3 * j + i] - (i == j ? trG : 0.f) - cG[3 * i + j]) + l2 * Jm1 * cF[3 * i + j];
-        }
-      float f[4][3], cv[4][3], bb[4];
-      float b0[3] = {-(T.b[0][0] + T.b[1][0] + T.b[2][0]), -(T.b[0][1] + T.b[1][1] + T.b[2][1]),
-                     -(T.b[0][2] + T.b[1][2] + T.b[2][2])};
-      bb[0] = b0[0] * b0[0] + b0[1] * b0[1] + b0[2] * b0[2];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) { f[0][c] = 0.f; cv[0][c] = 0.f; }
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        bb[k + 1] = T.b[k][0] * T.b[k][0] + T.b[k][1] * T.b[k][1] + T.b[k][2] * T.b[k][2];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          float fi = wv * (PK[3 * i] * T.b[k][0] + PK[3 * i + 1] * T.b[k][1] + PK[3 * i + 2] * T.b[k][2]);
-          float ci = cF[3 * i] * T.b[k][0] + cF[3 * i + 1] * T.b[k][1] + cF[3 * i + 2] * T.b[k][2];
-          f[k + 1][i] = fi;
-          cv[k + 1][i] = ci;
-          f[0][i] -= fi;
-          cv[0][i] -= ci;
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        float* p = sa + lv4[k] * 32 + lane;
-        const int S = kTileV * 32;
-        float am = wv * mu * bb[k], lc = wv * l2;
-        p[0] += f[k][0];
-        p[S] += f[k][1];
-        p[2 * S] += f[k][2];
-        p[3 * S] += am + lc * cv[k][0] * cv[k][0];
-        p[4 * S] += am + lc * cv[k][1] * cv[k][1];
-        p[5 * S] += am + lc * cv[k][2] * cv[k][2];
-        p[6 * S] += lc * cv[k][0] * cv[k][1];
-        p[7 * S] += lc * cv[k][0] * cv[k][2];
-        p[8 * S] += lc * cv[k][1] * cv[k][2];
-      }
-    }
-    __syncthreads();
-  }
-  // flush: each tile vertex once (fixed vertices carry no DOF)
-  for (int lv = w; lv < nvt; lv += 8) {
-    unsigned char fl = d.tile_vfl[v0 + lv];
-    if ((fl & 1) || !act) continue;
-    int gv = d.tile_verts[v0 + lv];
-#pragma unroll
-    for (int c = 0; c < 9; ++c) {
-      float val = sa[(c * kTileV + lv) * 32 + lane];
-      float* dst = c < 3 ? d.g + vidx(d, c, gv, e) : d.D + vidx(d, c - 3, gv, e);
-      if (fl & 2) *dst += val;  // only this tile touches the vertex
-      else atomicAdd(dst, val);
-    }
-  }
-  se[w][lane] = esum;
-  __syncthreads();
-  if (w == 0 && act) {
-    double s = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) s += se[j][lane];
-    atomicAdd(d.acc + (size_t)A_EEL * d.Es + e, s);
-  }
-}
-
 constexpr int kTiledCurvSmem = 2 * 3 * kTileV * 32 * 4;
 __global__ void __launch_bounds__(256) k_elem_curv_tiled(Dev d, float h2) {
   extern __shared__ float shc[];
@@ -916,12 +805,12 @@ __device__ __forceinline__ void scatter_gel(const Dev& d, int v, int e, d3 f, do
   atomicAdd(d.g + vidx(d, 1, v, e), (float)f.y);
   atomicAdd(d.g + vidx(d, 2, v, e), (float)f.z);
   if (s != 0.0) {
-    atomicAdd(d.D + vidx(d, 0, v, e), (float)(s * n.x * n.x));
-    atomicAdd(d.D + vidx(d, 1, v, e), (float)(s * n.y * n.y));
-    atomicAdd(d.D + vidx(d, 2, v, e), (float)(s * n.z * n.z));
-    atomicAdd(d.D + vidx(d, 3, v, e), (float)(s * n.x * n.y));
-    atomicAdd(d.D + vidx(d, 4, v, e), (float)(s * n.x * n.z));
-    atomicAdd(d.D + vidx(d, 5, v, e), (float)(s * n.y * n.z));
+    atomicAdd(d.D + vidxD(d, 0, v, e), (float)(s * n.x * n.x));
+    atomicAdd(d.D + vidxD(d, 1, v, e), (float)(s * n.y * n.y));
+    atomicAdd(d.D + vidxD(d, 2, v, e), (float)(s * n.z * n.z));
+    atomicAdd(d.D + vidxD(d, 3, v, e), (float)(s * n.x * n.y));
+    atomicAdd(d.D + vidxD(d, 4, v, e), (float)(s * n.x * n.z));
+    atomicAdd(d.D + vidxD(d, 5, v, e), (float)(s * n.y * n.z));
   }
 }
 
@@ -1060,12 +949,12 @@ __global__ void __launch_bounds__(128) k_contact_friction(Dev d, double eps_f) {
         atomicAdd(d.g + vidx(d, 1, v, e), (float)f.y);
         atomicAdd(d.g + vidx(d, 2, v, e), (float)f.z);
         double sw = f1 * wk * wk;  // GN: f1 w^2 T T^T (R8)
-        atomicAdd(d.D + vidx(d, 0, v, e), (float)(sw * (t1.x * t1.x + t2.x * t2.x)));
-        atomicAdd(d.D + vidx(d, 1, v, e), (float)(sw * (t1.y * t1.y + t2.y * t2.y)));
-        atomicAdd(d.D + vidx(d, 2, v, e), (float)(sw * (t1.z * t1.z + t2.z * t2.z)));
-        atomicAdd(d.D + vidx(d, 3, v, e), (float)(sw * (t1.x * t1.y + t2.x * t2.y)));
-        atomicAdd(d.D + vidx(d, 4, v, e), (float)(sw * (t1.x * t1.z + t2.x * t2.z)));
-        atomicAdd(d.D + vidx(d, 5, v, e), (float)(sw * (t1.y * t1.z + t2.y * t2.z)));
+        atomicAdd(d.D + vidxD(d, 0, v, e), (float)(sw * (t1.x * t1.x + t2.x * t2.x)));
+        atomicAdd(d.D + vidxD(d, 1, v, e), (float)(sw * (t1.y * t1.y + t2.y * t2.y)));
+        atomicAdd(d.D + vidxD(d, 2, v, e), (float)(sw * (t1.z * t1.z + t2.z * t2.z)));
+        atomicAdd(d.D + vidxD(d, 3, v, e), (float)(sw * (t1.x * t1.y + t2.x * t2.y)));
+        atomicAdd(d.D + vidxD(d, 4, v, e), (float)(sw * (t1.x * t1.z + t2.x * t2.z)));
+        atomicAdd(d.D + vidxD(d, 5, v, e), (float)(sw * (t1.y * t1.z + t2.y * t2.z)));
       } else {
         d3 arm = z[k] - cc;
         d3 tq = cross(arm, f);
@@ -1396,7 +1285,7 @@ __global__ void __launch_bounds__(256) k_dir_reduce(Dev d) {
       y[c] = g[c] - gq[c];
     }
 #pragma unroll
-    for (int c = 0; c < 6; ++c) D[c] = d.D[vidx(d, c, v, e)];
+    for (int c = 0; c < 6; ++c) D[c] = d.D[vidxD(d, c, v, e)];
     precond(D, d.precond, g, Pg);
     precond(D, d.precond, y, Py);
     gPy += g[0] * Py[0] + g[1] * Py[1] + g[2] * Py[2];
@@ -1523,7 +1412,7 @@ __global__ void __launch_bounds__(256) k_dir_apply(Dev d) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) g[c] = d.g[vidx(d, c, v, e)];
 #pragma unroll
-    for (int c = 0; c < 6; ++c) D[c] = d.D[vidx(d, c, v, e)];
+    for (int c = 0; c < 6; ++c) D[c] = d.D[vidxD(d, c, v, e)];
     precond(D, d.precond, g, Pg);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -1956,10 +1845,13 @@ void launch_anchors(const Dev& d, double h, cudaStream_t s) {
   LAUNCHK(KID_ANCHORS, s, (k_anchors<<<cgrid(d), 128, 0, s>>>(d, h * h * d.kappa_phys)));
 }
 void launch_eval(const Dev& d, double h, cudaStream_t s) {
-  LAUNCHK(KID_VERT_PRE, s, (k_vert_pre<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d)));
-  // the round-scheduled tiled variant (k_elem_grad_tiled) measured slower on C3 (740 vs 520 us:
-  // 66 % warp utilisation in the rounds, 2 CTAs/SM); the atomic scatter version stays
-  LAUNCHK(KID_ELEM_GRAD, s, (k_elem_grad<<<vgrid(d, d.nt), dim3(32, 8), 0, s>>>(d, (float)(h * h))));
+  LAUNCHK(KID_VERT_PRE, s, (k_vert_pre<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d, (float)(h * h))));
+  // (a round-scheduled shared-memory tiled variant measured slower on C3: 740 vs 520 us at
+  // 66 % warp utilisation in the rounds and 2 CTAs/SM; the coalesced red.add scatter stays)
+  {
+    dim3 g = vgrid(d, d.nt);
+    LAUNCHK(KID_ELEM_GRAD, s, (k_elem_grad<<<dim3(g.y, g.x), dim3(32, 8), 0, s>>>(d, (float)(h * h))));
+  }
   LAUNCHK(KID_CONTACT_CLASSIFY, s, (k_contact_classify_staged<<<sgrid(d), 256, d.contact_smem, s>>>(d)));
   const double kap = h * h * d.kappa_phys;
   LAUNCHK(KID_CONTACT_GRAD, s, (k_contact_near<0><<<cgrid(d), 128, 0, s>>>(d, kap)));
@@ -2021,7 +1913,6 @@ void kernels_init(int contact_smem) {
     cudaFuncSetAttribute(k_contact_classify_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, contact_smem);
     cudaFuncSetAttribute(k_contact_curv_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, contact_smem);
   }
-  cudaFuncSetAttribute(k_elem_grad_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, kTiledGradSmem);
   cudaFuncSetAttribute(k_elem_curv_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, kTiledCurvSmem);
 }
 int launches_per_iteration() { return 8 + 3 + 2 + 4; }
