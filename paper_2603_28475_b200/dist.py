@@ -32,7 +32,7 @@ class MarkerGather:
 
     def gather(self):
         import torch.distributed as dist
-        if self.world == 1:
+        if self.world == 1 and not dist.is_initialized():
             return self.buffer
         try:
             dist.all_gather_into_tensor(self.buffer, self.slot, group=self.group)
