@@ -155,8 +155,9 @@ tac_status tac_env_status(tac_sim* sim, int32_t* iters, float* pg_norm, uint32_t
  * peak candidate-pair count, friction anchors, candidate rebuilds inside the loop. */
 tac_status tac_env_stats(tac_sim* sim, int32_t* out, void* stream);
 
-/* Sizes: out[0..7] = n_verts, n_tets, n_envs, env_stride, n_markers, n_surface_verts,
- * n_surface_edges, n_surface_tris. */
+/* Sizes: out[0..9] = n_verts, n_tets, n_envs, env_stride, n_markers, n_surface_verts,
+ * n_surface_edges, n_surface_tris, n_kuhn_cells (6 tets each, register-blocked gradient),
+ * n_other_tets (generic gradient). */
 tac_status tac_info(const tac_sim* sim, int32_t* out);
 
 /* Number of kernel launches issued by the last tac_step / tac_markers call. */

@@ -9,6 +9,7 @@
 #include <array>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -375,6 +376,137 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
   d.root_tri = build_bvh(nodes, prims, btri);
   d.root_edge = build_bvh(nodes, prims, bedge);
   d.root_vert = build_bvh(nodes, prims, bvert);
+  // Kuhn cells: groups of 6 tets sharing an edge (the cell diagonal 0-7) whose other corners
+  // form the 6-cycle 1-3-2-6-4-5; relabelled to the canonical pattern (tet j = 0 -> 1<<p0 ->
+  // (1<<p0)|(1<<p1) -> 7 for the j-th permutation p of the axes) with geometry deciding which
+  // diagonal end is corner 0 and which axis each 1-bit corner lies along
+  std::vector<int4> cell_v;
+  std::vector<unsigned> cell_fix;
+  std::vector<float4> cell_tb;
+  std::vector<int> rest_tets;
+  {
+    static const int kTet[6][4] = {{0, 1, 3, 7}, {0, 1, 5, 7}, {0, 2, 3, 7}, {0, 2, 6, 7}, {0, 4, 5, 7}, {0, 4, 6, 7}};
+    std::map<std::pair<int, int>, std::vector<int>> edge_tets;
+    for (int e = 0; e < nt; ++e) {
+      const int* t = G.tets + 4 * e;
+      for (int i = 0; i < 4; ++i)
+        for (int j = i + 1; j < 4; ++j) edge_tets[{std::min(t[i], t[j]), std::max(t[i], t[j])}].push_back(e);
+    }
+    std::vector<char> used(nt, 0);
+    auto dist2 = [&](int p, int q) { V r = sub(X[p], X[q]); return r[0] * r[0] + r[1] * r[1] + r[2] * r[2]; };
+    // candidate diagonals: edges shared by exactly 6 tets, longest first globally (a cell
+    // diagonal, ~1.7 cells, is claimed before an interior axis edge, ~1 cell, whose link is
+    // also a 6-cycle could take the same tets)
+    std::vector<std::pair<double, std::pair<int, int>>> cands;
+    for (auto& kv : edge_tets)
+      if (kv.second.size() == 6) cands.push_back({-dist2(kv.first.first, kv.first.second), kv.first});
+    std::sort(cands.begin(), cands.end());
+    for (auto& cand : cands) {
+      {
+        {
+          auto it = edge_tets.find(cand.second);
+          const std::vector<int>& grp = it->second;
+          bool free_ = true;
+          for (int g : grp) free_ = free_ && !used[g];
+          if (!free_) continue;
+          int A = it->first.first, B = it->first.second;
+          const bool dbg = getenv("TAC_DEBUG_CELLS") != nullptr;
+          // non-diagonal corners of each tet
+          std::vector<std::pair<int, int>> pairs;
+          std::map<int, std::vector<int>> nb;
+          for (int g : grp) {
+            int o[2], n = 0;
+            for (int k = 0; k < 4; ++k) {
+              int v = G.tets[4 * g + k];
+              if (v != A && v != B && n < 2) o[n++] = v;
+            }
+            if (n != 2) { n = -1; break; }
+            pairs.push_back({o[0], o[1]});
+            nb[o[0]].push_back(o[1]);
+            nb[o[1]].push_back(o[0]);
+          }
+          if (pairs.size() != 6 || nb.size() != 6) { if (dbg) fprintf(stderr, "cell %d-%d: pairs %zu nb %zu\n", A, B, pairs.size(), nb.size()); continue; }
+          bool cyc = true;
+          for (auto& kv : nb) cyc = cyc && kv.second.size() == 2;
+          if (!cyc) { if (dbg) fprintf(stderr, "cell %d-%d: cycle\n", A, B); continue; }
+          // bipartition of the 6-cycle
+          std::map<int, int> side;
+          int start = nb.begin()->first, prev = -1, cur = start;
+          for (int s = 0; s < 6; ++s) {
+            side[cur] = s & 1;
+            int nx = nb[cur][0] == prev ? nb[cur][1] : nb[cur][0];
+            prev = cur;
+            cur = nx;
+          }
+          if (cur != start || side.size() != 6) { if (dbg) fprintf(stderr, "cell %d-%d: closed\n", A, B); continue; }
+          double m0[2] = {0, 0}, m1[2] = {0, 0};
+          for (auto& kv : side) { m0[kv.second] += dist2(kv.first, A); m1[kv.second] += dist2(kv.first, B); }
+          int one_bit = m0[0] < m0[1] ? 0 : 1;  // class nearer to corner 0
+          int c0 = A, c7 = B;
+          if (!(m1[1 - one_bit] < m1[one_bit])) {  // then A is corner 7
+            c0 = B; c7 = A;
+            one_bit = 1 - one_bit;
+          }
+          int lab[8] = {c0, -1, -1, -1, -1, -1, -1, c7};
+          bool ok = true;
+          std::map<int, int> bitof;  // 1-bit corner -> axis bit
+          for (auto& kv : side) {
+            if (kv.second != one_bit) continue;
+            V d = sub(X[kv.first], X[c0]);
+            int ax = (std::fabs(d[0]) >= std::fabs(d[1]) && std::fabs(d[0]) >= std::fabs(d[2])) ? 0
+                     : (std::fabs(d[1]) >= std::fabs(d[2]) ? 1 : 2);
+            if (lab[1 << ax] != -1) ok = false;
+            lab[1 << ax] = kv.first;
+            bitof[kv.first] = 1 << ax;
+          }
+          if (!ok) { if (dbg) fprintf(stderr, "cell %d-%d: axis\n", A, B); continue; }
+          for (auto& kv : side) {
+            if (kv.second == one_bit) continue;
+            int l = bitof[nb[kv.first][0]] | bitof[nb[kv.first][1]];
+            if (l == 0 || lab[l] != -1) ok = false;
+            else lab[l] = kv.first;
+          }
+          for (int s = 0; s < 8; ++s) ok = ok && lab[s] >= 0;
+          if (!ok) { if (dbg) fprintf(stderr, "cell %d-%d: twobit\n", A, B); continue; }
+          // every canonical tet must be one of the group's tets
+          std::set<std::array<int, 4>> have;
+          for (int g : grp) {
+            std::array<int, 4> q;
+            for (int k = 0; k < 4; ++k) q[k] = G.tets[4 * g + k];
+            std::sort(q.begin(), q.end());
+            have.insert(q);
+          }
+          for (int jt = 0; jt < 6 && ok; ++jt) {
+            std::array<int, 4> q;
+            for (int k = 0; k < 4; ++k) q[k] = lab[kTet[jt][k]];
+            std::sort(q.begin(), q.end());
+            ok = have.count(q) > 0;
+          }
+          if (!ok) { if (dbg) fprintf(stderr, "cell %d-%d: canon\n", A, B); continue; }
+          cell_v.push_back(make_int4(lab[0], lab[1], lab[2], lab[3]));
+          cell_v.push_back(make_int4(lab[4], lab[5], lab[6], lab[7]));
+          unsigned fm = 0;
+          for (int s = 0; s < 8; ++s)
+            if (vflag[lab[s]] & 1) fm |= 1u << s;
+          cell_fix.push_back(fm);
+          for (int jt = 0; jt < 6; ++jt) {  // b-vectors of the canonical corner order, |det|/6
+            V a0 = X[lab[kTet[jt][0]]];
+            V a = sub(X[lab[kTet[jt][1]]], a0), b = sub(X[lab[kTet[jt][2]]], a0), c = sub(X[lab[kTet[jt][3]]], a0);
+            double D = det(a, b, c);
+            V r0 = {(b[1] * c[2] - b[2] * c[1]) / D, (b[2] * c[0] - b[0] * c[2]) / D, (b[0] * c[1] - b[1] * c[0]) / D};
+            V r1 = {(c[1] * a[2] - c[2] * a[1]) / D, (c[2] * a[0] - c[0] * a[2]) / D, (c[0] * a[1] - c[1] * a[0]) / D};
+            V r2 = {(a[1] * b[2] - a[2] * b[1]) / D, (a[2] * b[0] - a[0] * b[2]) / D, (a[0] * b[1] - a[1] * b[0]) / D};
+            cell_tb.push_back(make_float4((float)r0[0], (float)r0[1], (float)r0[2], (float)(std::fabs(D) / 6.0)));
+            cell_tb.push_back(make_float4((float)r1[0], (float)r1[1], (float)r1[2], 0.f));
+            cell_tb.push_back(make_float4((float)r2[0], (float)r2[1], (float)r2[2], 0.f));
+          }
+          for (int g : grp) used[g] = 1;
+        }
+      }
+    }
+    for (int e = 0; e < nt; ++e)
+      if (!used[e]) rest_tets.push_back(e);
+  }
   // element tiles: Morton order of tet centroids, greedy cut at kTileT tets / kTileV
   // vertices, then greedy rounds of <= kTileW vertex-disjoint tets
   std::vector<int> tile_vstart{0}, tile_verts, tile_tstart{0}, tile_rstart{0};
@@ -576,6 +708,12 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     UP(tile_tb, d.tile_tb);
     UP(tile_rstart, d.tile_rstart);
     UP(tile_sched, d.tile_sched);
+    UP(cell_v, d.cell_v);
+    UP(cell_fix, d.cell_fix);
+    UP(cell_tb, d.cell_tb);
+    UP(rest_tets, d.rest_tets);
+    d.ncells = (int)cell_fix.size();
+    d.nrest = (int)rest_tets.size();
     d.ntiles = (int)tile_vstart.size() - 1;
     size_t nvec = 3 * (size_t)nv * d.Es;
     if ((rc = zalloc(sim, nvec, &d.u)) || (rc = zalloc(sim, nvec, &d.ut)) || (rc = zalloc(sim, nvec, &d.vt)) ||
@@ -730,7 +868,7 @@ tac_status tac_env_status(tac_sim* sim, int32_t* iters, float* pg_norm, uint32_t
 tac_status tac_info(const tac_sim* sim, int32_t* out) {
   if (!sim || !out) return TAC_EINVAL;
   const Dev& d = sim->d;
-  int v[8] = {d.nv, d.nt, d.E, d.Es, d.nm, d.nsv, d.nse, d.nst};
+  int v[10] = {d.nv, d.nt, d.E, d.Es, d.nm, d.nsv, d.nse, d.nst, d.ncells, d.nrest};
   memcpy(out, v, sizeof(v));
   return TAC_OK;
 }

@@ -121,6 +121,13 @@ struct Dev {
   const float4* tile_tb;         // [3 per tile tet] (b1, vol), (b2, 0), (b3, 0)
   const int* tile_rstart;        // [ntiles + 1] into tile_sched (in rounds)
   const short* tile_sched;       // [rounds][kTileW] tile-local tet index or -1
+  // Kuhn cells (k_elem_grad_cells): 6 tets sharing a cell diagonal, corners relabelled to the
+  // canonical pattern kCellTet; leftover tets go through the generic k_elem_grad
+  int ncells, nrest;
+  const int4* cell_v;            // [ncells][2] local corners 0-3, 4-7 (global vertex ids)
+  const unsigned* cell_fix;      // [ncells] bit s: corner s fixed
+  const float4* cell_tb;         // [ncells][6][3] (b1, vol), (b2, 0), (b3, 0) in canonical corner order
+  const int* rest_tets;          // [nrest] tets not in any cell
   double t1[3], t2[3], nrm[3];
 };
 

@@ -617,7 +617,8 @@ __global__ void __launch_bounds__(256, 4) k_elem_grad(Dev d, float h2) {
   float* __restrict__ gp = d.g;
   float* __restrict__ Dp = d.D;
   double esum = 0;
-  for (int t = blockIdx.x * 8 + threadIdx.y; t < d.nt; t += gridDim.x * 8) {
+  for (int it = blockIdx.x * 8 + threadIdx.y; it < d.nrest; it += gridDim.x * 8) {
+    const int t = __ldg(d.rest_tets + it);  // tets not covered by k_elem_grad_cells
     int4 tv = __ldg(d.tets + t);
     TetData T = load_tet(d, t);
     const unsigned fixmask = __float_as_uint(__ldg(d.tetb + 3 * t + 1).w);  // bit k: corner k fixed
@@ -694,6 +695,117 @@ __global__ void __launch_bounds__(256, 4) k_elem_grad(Dev d, float h2) {
       atomicAdd(pd + 96, sx * cv[k][1]);
       atomicAdd(pd + 128, sx * cv[k][2]);
       atomicAdd(pd + 160, sy * cv[k][2]);
+    }
+  }
+  if (act) atomicAdd(d.acc + (size_t)A_EEL * d.Es + e, esum);
+}
+
+// ---- Kuhn-cell element gradient: one warp = one cell (6 tets, 8 corners) x 32 envs ----
+// The 8 corners' u and their 8 x 9 accumulators live in registers with compile-time
+// indexing (canonical corner pattern kCellTet), so a cell costs 24 row loads and <= 72
+// coalesced red.add instead of 72 and 216 for six independent tets.
+// canonical tets (corner slots): {0,1,3,7} {0,1,5,7} {0,2,3,7} {0,2,6,7} {0,4,5,7} {0,4,6,7}
+#define CELL_TET(j, k) ((k) == 0 ? 0 : (k) == 3 ? 7 : (j) < 2 ? ((k) == 1 ? 1 : ((j) == 0 ? 3 : 5)) \
+                        : (j) < 4 ? ((k) == 1 ? 2 : ((j) == 2 ? 3 : 6)) : ((k) == 1 ? 4 : ((j) == 4 ? 5 : 6)))
+
+__global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
+  const int e = blockIdx.y * 32 + threadIdx.x;
+  const bool act = e < d.E && (d.run[e] & 1);
+  if (!__any_sync(0xffffffffu, act)) return;
+  const float mu = d.mu, l2 = d.lam2;
+  const unsigned G = (unsigned)(d.Es >> 5), eg = (unsigned)blockIdx.y, lane = threadIdx.x;
+  double esum = 0;
+  for (int cidx = blockIdx.x * 8 + threadIdx.y; cidx < d.ncells; cidx += gridDim.x * 8) {
+    const int4 va = __ldg(d.cell_v + 2 * cidx), vb4 = __ldg(d.cell_v + 2 * cidx + 1);
+    const unsigned fix = __ldg(d.cell_fix + cidx);
+    if (!act) continue;
+    const unsigned vb[8] = {(unsigned)va.x * G + eg, (unsigned)va.y * G + eg, (unsigned)va.z * G + eg,
+                            (unsigned)va.w * G + eg, (unsigned)vb4.x * G + eg, (unsigned)vb4.y * G + eg,
+                            (unsigned)vb4.z * G + eg, (unsigned)vb4.w * G + eg};
+    float u[8][3];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const float* p = d.u + (vb[s] * 3u * 32u + lane);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) u[s][c] = p[32 * c];
+    }
+    float ag[8][3], aD[8][6];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) ag[s][c] = 0.f;
+#pragma unroll
+      for (int c = 0; c < 6; ++c) aD[s][c] = 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+      const float4 r0 = __ldg(d.cell_tb + 18 * cidx + 3 * j), r1 = __ldg(d.cell_tb + 18 * cidx + 3 * j + 1),
+                   r2 = __ldg(d.cell_tb + 18 * cidx + 3 * j + 2);
+      const float b[3][3] = {{r0.x, r0.y, r0.z}, {r1.x, r1.y, r1.z}, {r2.x, r2.y, r2.z}};
+      const int s0 = CELL_TET(j, 0), s1 = CELL_TET(j, 1), s2 = CELL_TET(j, 2), s3 = CELL_TET(j, 3);
+      float du[3][3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        du[0][c] = u[s1][c] - u[s0][c];
+        du[1][c] = u[s2][c] - u[s0][c];
+        du[2][c] = u[s3][c] - u[s0][c];
+      }
+      float Gm[9];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj) Gm[3 * i + jj] = du[0][i] * b[0][jj] + du[1][i] * b[1][jj] + du[2][i] * b[2][jj];
+      float trG = Gm[0] + Gm[4] + Gm[8];
+      float i2 = (Gm[0] * Gm[4] - Gm[1] * Gm[3]) + (Gm[0] * Gm[8] - Gm[2] * Gm[6]) + (Gm[4] * Gm[8] - Gm[5] * Gm[7]);
+      float cG[9];
+      cof33(Gm, cG);
+      float detG = Gm[0] * cG[0] + Gm[1] * cG[1] + Gm[2] * cG[2];
+      float Jm1 = trG + i2 + detG;
+      float GG = 0.f;
+#pragma unroll
+      for (int i = 0; i < 9; ++i) GG = fmaf(Gm[i], Gm[i], GG);
+      float w = h2 * r0.w;
+      esum += (double)(w * (mu * (0.5f * GG - i2 - detG) + 0.5f * l2 * Jm1 * Jm1));
+      float cF[9], PK[9];
+      const float lj = l2 * Jm1;
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj) {
+          cF[3 * i + jj] = (i == jj ? 1.f + trG : 0.f) - Gm[3 * jj + i] + cG[3 * i + jj];
+          PK[3 * i + jj] = w * (mu * (Gm[3 * i + jj] + Gm[3 * jj + i] - (i == jj ? trG : 0.f) - cG[3 * i + jj]) + lj * cF[3 * i + jj]);
+        }
+      const float lc = w * l2;
+      float f0[3] = {0.f, 0.f, 0.f}, c0[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+      for (int kk = 0; kk < 3; ++kk) {
+        const int sk = kk == 0 ? s1 : (kk == 1 ? s2 : s3);
+        float fv[3], cv[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          fv[i] = PK[3 * i] * b[kk][0] + PK[3 * i + 1] * b[kk][1] + PK[3 * i + 2] * b[kk][2];
+          cv[i] = cF[3 * i] * b[kk][0] + cF[3 * i + 1] * b[kk][1] + cF[3 * i + 2] * b[kk][2];
+          f0[i] -= fv[i];
+          c0[i] -= cv[i];
+          ag[sk][i] += fv[i];
+        }
+        aD[sk][0] += lc * cv[0] * cv[0]; aD[sk][1] += lc * cv[1] * cv[1]; aD[sk][2] += lc * cv[2] * cv[2];
+        aD[sk][3] += lc * cv[0] * cv[1]; aD[sk][4] += lc * cv[0] * cv[2]; aD[sk][5] += lc * cv[1] * cv[2];
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i) ag[s0][i] += f0[i];
+      aD[s0][0] += lc * c0[0] * c0[0]; aD[s0][1] += lc * c0[1] * c0[1]; aD[s0][2] += lc * c0[2] * c0[2];
+      aD[s0][3] += lc * c0[0] * c0[1]; aD[s0][4] += lc * c0[0] * c0[2]; aD[s0][5] += lc * c0[1] * c0[2];
+    }
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      if (fix & (1u << s)) continue;
+      float* pg = d.g + (vb[s] * 3u * 32u + lane);
+      float* pd = d.D + (vb[s] * 6u * 32u + lane);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) atomicAdd(pg + 32 * c, ag[s][c]);
+#pragma unroll
+      for (int c = 0; c < 6; ++c) atomicAdd(pd + 32 * c, aD[s][c]);
     }
   }
   if (act) atomicAdd(d.acc + (size_t)A_EEL * d.Es + e, esum);
@@ -1848,8 +1960,12 @@ void launch_eval(const Dev& d, double h, cudaStream_t s) {
   LAUNCHK(KID_VERT_PRE, s, (k_vert_pre<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d, (float)(h * h))));
   // (a round-scheduled shared-memory tiled variant measured slower on C3: 740 vs 520 us at
   // 66 % warp utilisation in the rounds and 2 CTAs/SM; the coalesced red.add scatter stays)
-  {
-    dim3 g = vgrid(d, d.nt);
+  if (d.ncells > 0) {
+    dim3 g = vgrid(d, d.ncells);
+    LAUNCHK(KID_ELEM_GRAD, s, (k_elem_grad_cells<<<dim3(g.y, g.x), dim3(32, 8), 0, s>>>(d, (float)(h * h))));
+  }
+  if (d.nrest > 0) {
+    dim3 g = vgrid(d, d.nrest);
     LAUNCHK(KID_ELEM_GRAD, s, (k_elem_grad<<<dim3(g.y, g.x), dim3(32, 8), 0, s>>>(d, (float)(h * h))));
   }
   LAUNCHK(KID_CONTACT_CLASSIFY, s, (k_contact_classify_staged<<<sgrid(d), 256, d.contact_smem, s>>>(d)));

@@ -162,9 +162,10 @@ class TacSim:
         self.h = h
         self.device = device
         self.n_envs = n_envs
-        info8 = np.zeros(8, np.int32)
-        L.tac_info(self.h, info8.ctypes.data_as(_ip))
-        self.nv, self.nt, _, self.env_stride, self.nm, self.nsv, self.nse, self.nst = map(int, info8)
+        info = np.zeros(10, np.int32)
+        L.tac_info(self.h, info.ctypes.data_as(_ip))
+        (self.nv, self.nt, _, self.env_stride, self.nm, self.nsv, self.nse, self.nst, self.n_cells,
+         self.n_other_tets) = map(int, info)
 
     @classmethod
     def from_scene(cls, scene, params=None, material=None, n_envs=None, init_poses=None, **kw):

@@ -76,6 +76,20 @@ def test_marker_map_bitexact(torch_cuda):
         assert np.abs(w1 - w2).max() < 1e-12
 
 
+def test_kuhn_cell_decomposition(torch_cuda):
+    """The register-blocked gradient covers every tet of the (pseudo-structured and jittered,
+    renumbered) Kuhn pads; a mesh without cells falls back to the generic kernel."""
+    for s in (w.scene_c1(), w.scene_c2(steps=1), _small_unstructured()):
+        sim = _sim(s)
+        assert sim.n_cells * 6 == sim.nt and sim.n_other_tets == 0
+    s = w.scene_c1()
+    s.tets = s.tets[1:]  # break one cell: its 5 remaining tets go to the generic kernel
+    s.markers = s.markers[:1] * 0 + np.array([[0.0, 0.0, -1.0e-3]])
+    s.markers = np.repeat(s.markers, 63, axis=0)
+    sim = _sim(s)
+    assert sim.n_other_tets == 5 and sim.n_cells * 6 + 5 == sim.nt
+
+
 def test_surface_matches(torch_cuda):
     s = w.scene_c1()
     sim = _sim(s)
