@@ -25,11 +25,16 @@ struct BNode {  // indenter BVH node, body frame; leaf if left < 0: prims [-left
 };
 
 // friction anchor: frozen at the step start
+// Delta_k(x) = sum_gel w u(x) + R Y_w + sig c - C0 with the indenter side folded into
+// Y_w = sum_ind w Y (body frame), sig = sum_ind w, C0 = sum_gel w u^t + R^t Y_w + sig c^t
 struct Anchor {
-  int kind, a, b, pad;
+  int kind, a, b;
+  float sig;
   float w[4];
   float t1[3], lam;
-  float t2[3], pad2;
+  float t2[3], pad;
+  float yw[3], pad2;
+  double c0[3], pad3;
 };
 
 // per-env solver state (fp64 control, one thread per env in the scalar kernels)
@@ -157,7 +162,8 @@ extern thread_local long long g_launches;
 enum KernelId {
   KID_STEP_SETUP = 0, KID_VERT_SETUP, KID_BROADPHASE, KID_ANCHORS, KID_VERT_PRE, KID_ELEM_GRAD, KID_CONTACT_GRAD,
   KID_ACCEPT, KID_DIR_REDUCE, KID_DIR_SCALAR, KID_DIR_APPLY, KID_ELEM_CURV, KID_CONTACT_CURV, KID_ALPHA,
-  KID_CCD, KID_FIN_VERT, KID_FIN_ENV, KID_MARKERS, KID_OTHER, KID_CONTACT_CLASSIFY, KID_COUNT
+  KID_CCD, KID_FIN_VERT, KID_FIN_ENV, KID_MARKERS, KID_OTHER, KID_CONTACT_CLASSIFY,
+  KID_CONTACT_NEAR_IG, KID_CONTACT_NEAR_EE, KID_CONTACT_FRICTION, KID_COUNT
 };
 struct Profiler;
 extern thread_local Profiler* g_prof;

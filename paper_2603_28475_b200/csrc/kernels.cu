@@ -18,9 +18,10 @@ thread_local long long g_launches = 0;
 thread_local Profiler* g_prof = nullptr;
 
 static const char* kNames[KID_COUNT] = {
-    "step_setup", "vert_setup", "broadphase", "anchors", "vert_pre", "elem_grad", "contact_grad", "accept",
+    "step_setup", "vert_setup", "broadphase", "anchors", "vert_pre", "elem_grad", "contact_near_gi", "accept",
     "dir_reduce", "dir_scalar", "dir_apply", "elem_curv", "contact_curv", "alpha", "ccd", "finalize_vert",
-    "finalize_env", "markers", "other", "contact_classify"};
+    "finalize_env", "markers", "other", "contact_classify", "contact_near_ig", "contact_near_ee",
+    "contact_friction"};
 const char* kernel_name(int kid) { return (kid >= 0 && kid < KID_COUNT) ? kNames[kid] : "?"; }
 
 // ------------------------------------------------------------------ small helpers
@@ -527,12 +528,25 @@ __global__ void k_anchors(Dev d, double kappa) {
     int slot = atomicAdd(d.nanc + e, 1);
     if (slot >= d.amax) { d.es[e].ncand_over = 1; continue; }
     Anchor A;
-    A.kind = kind; A.a = a; A.b = b; A.pad = 0;
+    A.kind = kind; A.a = a; A.b = b;
     for (int k = 0; k < 4; ++k) A.w[k] = (float)D.w[k];
     A.t1[0] = t1.x; A.t1[1] = t1.y; A.t1[2] = t1.z;
     A.t2[0] = t2.x; A.t2[1] = t2.y; A.t2[2] = t2.z;
     A.lam = (float)fmax(0.0, -kappa * bar_db(D.d, d.dhat));
-    A.pad2 = 0;
+    A.pad = 0; A.pad2 = 0; A.pad3 = 0;
+    // fold the rigid side: Y_w = sum_ind w Y, sig = sum_ind w; C0 = sum_gel w u^t + R^t Y_w + sig c^t
+    d3 yw = mk(0, 0, 0), c0 = mk(0, 0, 0);
+    double sig = 0;
+    for (int k = 0; k < 4; ++k) {
+      double wk = (double)A.w[k];
+      if (C.ind[k]) { yw = yw + wk * ind_body(d, C.id[k]); sig += wk; }
+      else c0 = c0 + wk * gel_vec(d, d.u, C.id[k], e);
+    }
+    A.sig = (float)sig;
+    A.yw[0] = (float)yw.x; A.yw[1] = (float)yw.y; A.yw[2] = (float)yw.z;
+    // C0 from the stored (rounded) Y_w and sig, so Delta(x^t) = 0 exactly
+    c0 = c0 + mv(s.R, mk(A.yw[0], A.yw[1], A.yw[2])) + (double)A.sig * ld3(s.c);
+    A.c0[0] = c0.x; A.c0[1] = c0.y; A.c0[2] = c0.z;
     d.anc[(size_t)e * d.amax + slot] = A;
   }
 }
@@ -811,6 +825,72 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
   if (act) atomicAdd(d.acc + (size_t)A_EEL * d.Es + e, esum);
 }
 
+// ---- Kuhn-cell element curvature: one warp = one cell x 32 envs, u and p of the 8 corners
+// in registers; p^T H_e p summed over the 6 tets (App. B quadratic form)
+__global__ void __launch_bounds__(256, 2) k_elem_curv_cells(Dev d, float h2) {
+  const int e = blockIdx.y * 32 + threadIdx.x;
+  const bool act = e < d.E && (d.run[e] & 2);
+  if (!__any_sync(0xffffffffu, act)) return;
+  const float mu = d.mu, l2 = d.lam2;
+  const unsigned G = (unsigned)(d.Es >> 5), eg = (unsigned)blockIdx.y, lane = threadIdx.x;
+  double qsum = 0;
+  for (int cidx = blockIdx.x * 8 + threadIdx.y; cidx < d.ncells; cidx += gridDim.x * 8) {
+    const int4 va = __ldg(d.cell_v + 2 * cidx), vb4 = __ldg(d.cell_v + 2 * cidx + 1);
+    if (!act) continue;
+    const unsigned vb[8] = {(unsigned)va.x * G + eg, (unsigned)va.y * G + eg, (unsigned)va.z * G + eg,
+                            (unsigned)va.w * G + eg, (unsigned)vb4.x * G + eg, (unsigned)vb4.y * G + eg,
+                            (unsigned)vb4.z * G + eg, (unsigned)vb4.w * G + eg};
+    float u[8][3], p[8][3];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const float* pu = d.u + (vb[s] * 3u * 32u + lane);
+      const float* pp = d.p + (vb[s] * 3u * 32u + lane);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) { u[s][c] = pu[32 * c]; p[s][c] = pp[32 * c]; }
+    }
+    float q = 0.f;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+      const float4 r0 = __ldg(d.cell_tb + 18 * cidx + 3 * j), r1 = __ldg(d.cell_tb + 18 * cidx + 3 * j + 1),
+                   r2 = __ldg(d.cell_tb + 18 * cidx + 3 * j + 2);
+      const float b[3][3] = {{r0.x, r0.y, r0.z}, {r1.x, r1.y, r1.z}, {r2.x, r2.y, r2.z}};
+      const int s0 = CELL_TET(j, 0), s1 = CELL_TET(j, 1), s2 = CELL_TET(j, 2), s3 = CELL_TET(j, 3);
+      float Gm[9], dF[9];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const float du0 = u[s1][i] - u[s0][i], du1 = u[s2][i] - u[s0][i], du2 = u[s3][i] - u[s0][i];
+        const float dp0 = p[s1][i] - p[s0][i], dp1 = p[s2][i] - p[s0][i], dp2 = p[s3][i] - p[s0][i];
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj) {
+          Gm[3 * i + jj] = du0 * b[0][jj] + du1 * b[1][jj] + du2 * b[2][jj];
+          dF[3 * i + jj] = dp0 * b[0][jj] + dp1 * b[1][jj] + dp2 * b[2][jj];
+        }
+      }
+      float trG = Gm[0] + Gm[4] + Gm[8];
+      float i2 = (Gm[0] * Gm[4] - Gm[1] * Gm[3]) + (Gm[0] * Gm[8] - Gm[2] * Gm[6]) + (Gm[4] * Gm[8] - Gm[5] * Gm[7]);
+      float cG[9], cd[9];
+      cof33(Gm, cG);
+      cof33(dF, cd);
+      float detG = Gm[0] * cG[0] + Gm[1] * cG[1] + Gm[2] * cG[2];
+      float Jm1 = trG + i2 + detG;
+      float dd = 0.f, cfd = 0.f, fcd = 0.f;
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj) {
+          float cF = (i == jj ? 1.f + trG : 0.f) - Gm[3 * jj + i] + cG[3 * i + jj];
+          float Fij = (i == jj ? 1.f : 0.f) + Gm[3 * i + jj];
+          dd = fmaf(dF[3 * i + jj], dF[3 * i + jj], dd);
+          cfd = fmaf(cF, dF[3 * i + jj], cfd);
+          fcd = fmaf(Fij, cd[3 * i + jj], fcd);
+        }
+      q += r0.w * (mu * dd + l2 * cfd * cfd + 2.f * (l2 * Jm1 - mu) * fcd);
+    }
+    qsum += (double)(h2 * q);
+  }
+  if (act) atomicAdd(d.acc + (size_t)A_PHP * d.Es + e, qsum);
+}
+
 // ---- tiled element passes: one CTA = one tile x 32 envs (lane = env) ----
 // Vertex rows of the tile are staged in shared memory once (instead of once per tet);
 // gradient and diagonal blocks accumulate in shared memory in rounds of vertex-disjoint
@@ -1013,32 +1093,25 @@ __global__ void __launch_bounds__(128) k_contact_friction(Dev d, double eps_f) {
   int e = blockIdx.y;
   if (e >= d.E || !(d.run[e] & 1)) return;
   const EnvS& s = d.es[e];
-  __shared__ double R[9], c[3], Rt[9], ct[3];
+  __shared__ double R[9], c[3];
   __shared__ double smr[4 * 20];
-  if (threadIdx.x < 9) { R[threadIdx.x] = s.R[threadIdx.x]; Rt[threadIdx.x] = s.Rt[threadIdx.x]; }
-  if (threadIdx.x < 3) { c[threadIdx.x] = s.c[threadIdx.x]; ct[threadIdx.x] = s.ct[threadIdx.x]; }
+  if (threadIdx.x < 9) R[threadIdx.x] = s.R[threadIdx.x];
+  if (threadIdx.x < 3) c[threadIdx.x] = s.c[threadIdx.x];
   __syncthreads();
   double Ef = 0, gr[6] = {0, 0, 0, 0, 0, 0}, Dc[6] = {0, 0, 0, 0, 0, 0}, Dt[6] = {0, 0, 0, 0, 0, 0};
-  d3 cc = ld3(c);
+  const d3 cc = ld3(c);
   const int na = min(d.nanc[e], d.amax);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
-    Anchor A = d.anc[(size_t)e * d.amax + i];
+    const Anchor& A = d.anc[(size_t)e * d.amax + i];
     CornersL C = corners_l(d, A.kind, A.a, A.b);
-    d3 Dl = mk(0, 0, 0), z[4];
+    const d3 rho = mv(R, mk(A.yw[0], A.yw[1], A.yw[2]));  // sum_ind w (y - c) = R Y_w
+    const double sig = A.sig;
+    d3 Dl = rho + sig * cc - mk(A.c0[0], A.c0[1], A.c0[2]);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      d3 dz;
-      if (C.ind[k]) {
-        d3 y = ind_body(d, C.gid[k]);
-        z[k] = mv(R, y) + cc;
-        dz = z[k] - (mv(Rt, y) + ld3(ct));
-      } else {
-        int v = C.gid[k];
-        float4 u = d.usurf[(size_t)C.sid[k] * d.Es + e];
-        dz = mk((double)u.x - (double)d.ut[vidx(d, 0, v, e)], (double)u.y - (double)d.ut[vidx(d, 1, v, e)],
-                (double)u.z - (double)d.ut[vidx(d, 2, v, e)]);
-      }
-      Dl = Dl + (double)A.w[k] * dz;
+      if (C.ind[k]) continue;
+      float4 u = d.usurf[(size_t)C.sid[k] * d.Es + e];
+      Dl = Dl + (double)A.w[k] * mk(u.x, u.y, u.z);
     }
     d3 t1 = mk(A.t1[0], A.t1[1], A.t1[2]), t2 = mk(A.t2[0], A.t2[1], A.t2[2]);
     double ta = dot(t1, Dl), tb = dot(t2, Dl);
@@ -1048,33 +1121,27 @@ __global__ void __launch_bounds__(128) k_contact_friction(Dev d, double eps_f) {
     double f1 = ml * moll_f1(sn, eps_f);
     d.anc_f1[(size_t)e * d.amax + i] = (float)f1;
     d3 Tt = ta * t1 + tb * t2;
-    double sig = 0;
-    d3 rho = mk(0, 0, 0);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
+      if (C.ind[k]) continue;
+      int v = C.gid[k];
+      if (d.vflag[v] & 1) continue;
       double wk = A.w[k];
       d3 f = (f1 * wk) * Tt;
-      if (!C.ind[k]) {
-        int v = C.gid[k];
-        if (d.vflag[v] & 1) continue;
-        atomicAdd(d.g + vidx(d, 0, v, e), (float)f.x);
-        atomicAdd(d.g + vidx(d, 1, v, e), (float)f.y);
-        atomicAdd(d.g + vidx(d, 2, v, e), (float)f.z);
-        double sw = f1 * wk * wk;  // GN: f1 w^2 T T^T (R8)
-        atomicAdd(d.D + vidxD(d, 0, v, e), (float)(sw * (t1.x * t1.x + t2.x * t2.x)));
-        atomicAdd(d.D + vidxD(d, 1, v, e), (float)(sw * (t1.y * t1.y + t2.y * t2.y)));
-        atomicAdd(d.D + vidxD(d, 2, v, e), (float)(sw * (t1.z * t1.z + t2.z * t2.z)));
-        atomicAdd(d.D + vidxD(d, 3, v, e), (float)(sw * (t1.x * t1.y + t2.x * t2.y)));
-        atomicAdd(d.D + vidxD(d, 4, v, e), (float)(sw * (t1.x * t1.z + t2.x * t2.z)));
-        atomicAdd(d.D + vidxD(d, 5, v, e), (float)(sw * (t1.y * t1.z + t2.y * t2.z)));
-      } else {
-        d3 arm = z[k] - cc;
-        d3 tq = cross(arm, f);
-        gr[0] += f.x; gr[1] += f.y; gr[2] += f.z; gr[3] += tq.x; gr[4] += tq.y; gr[5] += tq.z;
-        sig += wk;
-        rho = rho + wk * arm;
-      }
+      atomicAdd(d.g + vidx(d, 0, v, e), (float)f.x);
+      atomicAdd(d.g + vidx(d, 1, v, e), (float)f.y);
+      atomicAdd(d.g + vidx(d, 2, v, e), (float)f.z);
+      double sw = f1 * wk * wk;  // GN: f1 w^2 T T^T (R8)
+      atomicAdd(d.D + vidxD(d, 0, v, e), (float)(sw * (t1.x * t1.x + t2.x * t2.x)));
+      atomicAdd(d.D + vidxD(d, 1, v, e), (float)(sw * (t1.y * t1.y + t2.y * t2.y)));
+      atomicAdd(d.D + vidxD(d, 2, v, e), (float)(sw * (t1.z * t1.z + t2.z * t2.z)));
+      atomicAdd(d.D + vidxD(d, 3, v, e), (float)(sw * (t1.x * t1.y + t2.x * t2.y)));
+      atomicAdd(d.D + vidxD(d, 4, v, e), (float)(sw * (t1.x * t1.z + t2.x * t2.z)));
+      atomicAdd(d.D + vidxD(d, 5, v, e), (float)(sw * (t1.y * t1.z + t2.y * t2.z)));
     }
+    // indenter side: force f1 sig T tau on c, torque rho x (f1 T tau)
+    d3 F = (f1 * sig) * Tt, tq = cross(rho, f1 * Tt);
+    gr[0] += F.x; gr[1] += F.y; gr[2] += F.z; gr[3] += tq.x; gr[4] += tq.y; gr[5] += tq.z;
     add_sym(Dc, t1, f1 * sig * sig);
     add_sym(Dc, t2, f1 * sig * sig);
     add_sym(Dt, cross(rho, t1), f1);
@@ -1260,11 +1327,13 @@ __global__ void __launch_bounds__(256) k_contact_curv_staged(Dev d, double kappa
   }
   const int na = min(d.nanc[e], d.amax);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
-    Anchor A = d.anc[(size_t)e * d.amax + i];
+    const Anchor& A = d.anc[(size_t)e * d.amax + i];
     CornersL C = corners_l(d, A.kind, A.a, A.b);
-    d3 dD = mk(0, 0, 0);
+    // indenter side folded: sig p_c + p_theta x (R Y_w)
+    d3 dD = (double)A.sig * pc + cross(pth, mv(R, mk(A.yw[0], A.yw[1], A.yw[2])));
 #pragma unroll
-    for (int k = 0; k < 4; ++k) dD = dD + (double)A.w[k] * motion(C, k);
+    for (int k = 0; k < 4; ++k)
+      if (!C.ind[k]) dD = dD + (double)A.w[k] * motion(C, k);
     d3 t1 = mk(A.t1[0], A.t1[1], A.t1[2]), t2 = mk(A.t2[0], A.t2[1], A.t2[2]);
     double ta = dot(t1, dD), tb = dot(t2, dD);
     q += (double)d.anc_f1[(size_t)e * d.amax + i] * (ta * ta + tb * tb);
@@ -1971,9 +2040,9 @@ void launch_eval(const Dev& d, double h, cudaStream_t s) {
   LAUNCHK(KID_CONTACT_CLASSIFY, s, (k_contact_classify_staged<<<sgrid(d), 256, d.contact_smem, s>>>(d)));
   const double kap = h * h * d.kappa_phys;
   LAUNCHK(KID_CONTACT_GRAD, s, (k_contact_near<0><<<cgrid(d), 128, 0, s>>>(d, kap)));
-  LAUNCHK(KID_CONTACT_GRAD, s, (k_contact_near<1><<<cgrid(d), 128, 0, s>>>(d, kap)));
-  LAUNCHK(KID_CONTACT_GRAD, s, (k_contact_near<2><<<cgrid(d), 128, 0, s>>>(d, kap)));
-  LAUNCHK(KID_CONTACT_GRAD, s, (k_contact_friction<<<cgrid(d), 128, 0, s>>>(d, d.eps_v * h)));
+  LAUNCHK(KID_CONTACT_NEAR_IG, s, (k_contact_near<1><<<cgrid(d), 128, 0, s>>>(d, kap)));
+  LAUNCHK(KID_CONTACT_NEAR_EE, s, (k_contact_near<2><<<cgrid(d), 128, 0, s>>>(d, kap)));
+  LAUNCHK(KID_CONTACT_FRICTION, s, (k_contact_friction<<<cgrid(d), 128, 0, s>>>(d, d.eps_v * h)));
   LAUNCHK(KID_ACCEPT, s, (k_accept<<<eblocks(d), 128, 0, s>>>(d, h)));
 }
 void launch_direction(const Dev& d, cudaStream_t s) {
@@ -1982,7 +2051,12 @@ void launch_direction(const Dev& d, cudaStream_t s) {
   LAUNCHK(KID_DIR_APPLY, s, (k_dir_apply<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d)));
 }
 void launch_curvature(const Dev& d, double h, cudaStream_t s) {
-  LAUNCHK(KID_ELEM_CURV, s, (k_elem_curv_tiled<<<dim3(d.Es / 32, d.ntiles), 256, kTiledCurvSmem, s>>>(d, (float)(h * h))));
+  if (d.nrest == 0) {  // every tet is in a Kuhn cell: register-blocked cells
+    dim3 g = vgrid(d, d.ncells);
+    LAUNCHK(KID_ELEM_CURV, s, (k_elem_curv_cells<<<dim3(g.y, g.x), dim3(32, 8), 0, s>>>(d, (float)(h * h))));
+  } else {
+    LAUNCHK(KID_ELEM_CURV, s, (k_elem_curv_tiled<<<dim3(d.Es / 32, d.ntiles), 256, kTiledCurvSmem, s>>>(d, (float)(h * h))));
+  }
   LAUNCHK(KID_CONTACT_CURV, s, (k_contact_curv_staged<<<sgrid(d), 256, d.contact_smem, s>>>(d, h * h * d.kappa_phys)));
 }
 void launch_alpha(const Dev& d, double h, cudaStream_t s) {
