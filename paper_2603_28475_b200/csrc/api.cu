@@ -725,7 +725,8 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
         (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.cand)) || (rc = zalloc(sim, 2 * (size_t)d.E * d.kmax, &d.cgeo)) || (rc = zalloc(sim, (size_t)d.E, &d.ncand)) || (rc = zalloc(sim, 3 * (size_t)d.E * d.kmax, &d.nearl)) ||
         (rc = zalloc(sim, 3 * (size_t)d.E, &d.nnear)) ||
         (rc = zalloc(sim, (size_t)std::max(1, d.nsv) * d.Es, &d.usurf)) || (rc = zalloc(sim, (size_t)std::max(1, d.nsv) * d.Es, &d.psurf)) ||
-        (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc)) || (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc_f1)) || (rc = zalloc(sim, (size_t)d.E, &d.nanc)) ||
+        (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc)) || (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc_f1)) || (rc = zalloc(sim, (size_t)d.E, &d.nanc)) || (rc = zalloc(sim, (size_t)d.E, &d.reb_list)) ||
+        (rc = zalloc(sim, 1, &d.nreb)) ||
         (rc = zalloc(sim, 1, &sim->d_flag)) || (rc = zalloc(sim, (size_t)d.kmax, &sim->d_dbg_cand)) ||
         (rc = zalloc(sim, 1, &sim->d_dbg_cnt)) || (rc = zalloc(sim, 3 * (size_t)nv, &sim->d_scratch)))
       goto fail;

@@ -112,6 +112,8 @@ struct Dev {
   Anchor* anc;           // [E][amax]
   float* anc_f1;         // [E][amax] friction weight mu lambda f1(s) of the last evaluation
   int* nanc;             // [E]
+  int* reb_list;         // [E] envs that rebuild their candidates in this iteration
+  int* nreb;             // [1]
   // material / params
   float mu, lam2;        // mu, lambda' = lambda + mu
   double rho_max, dhat, kappa_phys, eps_v, tol_x, k_t, k_r, f_max, t_max, ccd_s, bp_margin, c1, eps_E, mu_f;
@@ -163,7 +165,7 @@ enum KernelId {
   KID_STEP_SETUP = 0, KID_VERT_SETUP, KID_BROADPHASE, KID_ANCHORS, KID_VERT_PRE, KID_ELEM_GRAD, KID_CONTACT_GRAD,
   KID_ACCEPT, KID_DIR_REDUCE, KID_DIR_SCALAR, KID_DIR_APPLY, KID_ELEM_CURV, KID_CONTACT_CURV, KID_ALPHA,
   KID_CCD, KID_FIN_VERT, KID_FIN_ENV, KID_MARKERS, KID_OTHER, KID_CONTACT_CLASSIFY,
-  KID_CONTACT_NEAR_IG, KID_CONTACT_NEAR_EE, KID_CONTACT_FRICTION, KID_COUNT
+  KID_CONTACT_NEAR_IG, KID_CONTACT_NEAR_EE, KID_CONTACT_FRICTION, KID_BROADPHASE_LIST, KID_COUNT
 };
 struct Profiler;
 extern thread_local Profiler* g_prof;

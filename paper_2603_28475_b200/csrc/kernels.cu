@@ -21,7 +21,7 @@ static const char* kNames[KID_COUNT] = {
     "step_setup", "vert_setup", "broadphase", "anchors", "vert_pre", "elem_grad", "contact_near_gi", "accept",
     "dir_reduce", "dir_scalar", "dir_apply", "elem_curv", "contact_curv", "alpha", "ccd", "finalize_vert",
     "finalize_env", "markers", "other", "contact_classify", "contact_near_ig", "contact_near_ee",
-    "contact_friction"};
+    "contact_friction", "broadphase_rebuild"};
 const char* kernel_name(int kid) { return (kid >= 0 && kid < KID_COUNT) ? kNames[kid] : "?"; }
 
 // ------------------------------------------------------------------ small helpers
@@ -405,6 +405,10 @@ __device__ __forceinline__ double to_body_exact(const double* R, const double* c
   return __dadd_rn(__dadd_rn(t0, t1), t2);
 }
 
+constexpr int kBpStage = 3072;  // candidates staged per block before one global reservation
+__shared__ unsigned long long g_bp_sbuf[kBpStage];
+__shared__ int g_bp_scnt;
+
 template <int NIND>
 __device__ void bp_query(const Dev& d, int kind, int gid, const double* glo, const double* ghi, double r, int root,
                          unsigned long long* out, int* cnt, int cap, bool* over) {
@@ -450,30 +454,24 @@ __device__ void bp_query(const Dev& d, int kind, int gid, const double* glo, con
       if (!ok) continue;
       unsigned long long a_id = (kind == 1) ? (unsigned long long)prim : (unsigned long long)gid;
       unsigned long long b_id = (kind == 1) ? (unsigned long long)gid : (unsigned long long)prim;
-      int slot = atomicAdd(cnt, 1);
-      if (slot < cap) out[slot] = ((unsigned long long)kind << 62) | (a_id << 31) | b_id;
-      else *over = true;
+      const unsigned long long rec = ((unsigned long long)kind << 62) | (a_id << 31) | b_id;
+      int ss = atomicAdd(&g_bp_scnt, 1);  // block-local staging (native shared int atomic)
+      if (ss < kBpStage) {
+        g_bp_sbuf[ss] = rec;
+      } else {  // staging full: reserve directly
+        int slot = atomicAdd(cnt, 1);
+        if (slot < cap) out[slot] = rec;
+        else *over = true;
+      }
     }
   }
 }
 
-__global__ void __launch_bounds__(128) k_broadphase(Dev d, int masked, double r, unsigned long long* out_override,
-                                                    int* cnt_override, int cap_override) {
-  int e = blockIdx.y;
-  if (e >= d.E) return;
-  const EnvS& s = d.es[e];
-  if (s.mode != kActive) return;
-  if (masked && !(d.run[e] & 4)) return;
-  __shared__ double R[9], c[3];
-  if (threadIdx.x < 9) R[threadIdx.x] = s.R[threadIdx.x];
-  if (threadIdx.x < 3) c[threadIdx.x] = s.c[threadIdx.x];
-  __syncthreads();
-  unsigned long long* out = out_override ? out_override : d.cand + (size_t)e * d.kmax;
-  int* cnt = cnt_override ? cnt_override : d.ncand + e;
-  int cap = out_override ? cap_override : d.kmax;
+// candidates of gel-surface primitives [i0, i1) (strided) of env e
+__device__ void bp_range(const Dev& d, int e, int i0, int i1, int stride, double r, unsigned long long* out, int* cnt,
+                         int cap, const double* R, const double* c) {
   bool over = false;
-  int ntot = d.nsv + d.nse + d.nst;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ntot; i += gridDim.x * blockDim.x) {
+  for (int i = i0; i < i1; i += stride) {
     int vv[3], nvx, kind, gid, root;
     if (i < d.nsv) {
       vv[0] = d.sv[i]; nvx = 1; kind = 0; gid = i; root = d.root_tri;
@@ -499,7 +497,69 @@ __global__ void __launch_bounds__(128) k_broadphase(Dev d, int masked, double r,
     else if (kind == 2) bp_query<2>(d, 2, gid, lo, hi, r, root, out, cnt, cap, &over);
     else bp_query<1>(d, 1, gid, lo, hi, r, root, out, cnt, cap, &over);
   }
-  if (over && !out_override) d.es[e].ncand_over = 1;
+  if (over) d.es[e].ncand_over = 1;
+}
+
+__device__ void bp_flush(unsigned long long* out, int* cnt, int cap, bool* over) {
+  __syncthreads();
+  __shared__ int base;
+  const int n = min(g_bp_scnt, kBpStage);
+  if (threadIdx.x == 0) base = n ? atomicAdd(cnt, n) : 0;
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    if (base + j < cap) out[base + j] = g_bp_sbuf[j];
+    else *over = true;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) g_bp_scnt = 0;
+  __syncthreads();
+}
+
+// all active envs (step start): blockIdx.y = env, blocks stride over its primitives
+__global__ void __launch_bounds__(128) k_broadphase(Dev d, double r, unsigned long long* out_override,
+                                                    int* cnt_override, int cap_override) {
+  int e = blockIdx.y;
+  if (e >= d.E) return;
+  const EnvS& s = d.es[e];
+  if (s.mode != kActive) return;
+  __shared__ double R[9], c[3];
+  if (threadIdx.x < 9) R[threadIdx.x] = s.R[threadIdx.x];
+  if (threadIdx.x < 3) c[threadIdx.x] = s.c[threadIdx.x];
+  __syncthreads();
+  unsigned long long* out = out_override ? out_override : d.cand + (size_t)e * d.kmax;
+  int* cnt = cnt_override ? cnt_override : d.ncand + e;
+  int cap = out_override ? cap_override : d.kmax;
+  int ntot = d.nsv + d.nse + d.nst;
+  if (threadIdx.x == 0) g_bp_scnt = 0;
+  __syncthreads();
+  bp_range(d, e, blockIdx.x * blockDim.x + threadIdx.x, ntot, gridDim.x * blockDim.x, r, out, cnt, cap, R, c);
+  bool over = false;
+  bp_flush(out, cnt, cap, &over);
+  if (over) d.es[e].ncand_over = 1;
+}
+
+// rebuilds inside the loop: only the envs k_alpha listed; work items = (listed env,
+// 128-primitive chunk) spread over a fixed grid, so cost follows the actual rebuild count
+__global__ void __launch_bounds__(128) k_broadphase_list(Dev d, double r) {
+  const int nreb = *d.nreb;
+  const int ntot = d.nsv + d.nse + d.nst;
+  const int nchunk = (ntot + blockDim.x - 1) / blockDim.x;
+  __shared__ double R[9], c[3];
+  for (int item = blockIdx.x; item < nreb * nchunk; item += gridDim.x) {
+    const int e = d.reb_list[item / nchunk], ch = item % nchunk;
+    const EnvS& s = d.es[e];
+    __syncthreads();
+    if (threadIdx.x < 9) R[threadIdx.x] = s.R[threadIdx.x];
+    if (threadIdx.x < 3) c[threadIdx.x] = s.c[threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x == 0) g_bp_scnt = 0;
+    __syncthreads();
+    const int i = ch * blockDim.x + threadIdx.x;
+    bp_range(d, e, i, min(ntot, i + 1), 1, r, d.cand + (size_t)e * d.kmax, d.ncand + e, d.kmax, R, c);
+    bool over = false;
+    bp_flush(d.cand + (size_t)e * d.kmax, d.ncand + e, d.kmax, &over);
+    if (over) d.es[e].ncand_over = 1;
+  }
 }
 
 // ------------------------------------------------------------------ a3: friction anchors
@@ -1687,6 +1747,78 @@ __global__ void __launch_bounds__(256) k_elem_curv(Dev d, float h2) {
 
 // contact curvature (GN, R8) and the conservative step bound alpha_ccd (R15):
 // d(alpha) >= d - alpha l_n, l_n = max_A(-n.dz) + max_B(n.dz) + |p_theta| dhat/4
+// step bound over the fresh candidates of the envs that rebuilt (k_alpha list): work items
+// = (listed env, 128-candidate chunk); separating-axis certificate -> g_min, else exact
+// fp64 distance and the closest-point plane bound (R15)
+__global__ void __launch_bounds__(128) k_ccd_list(Dev d) {
+  const int nreb = *d.nreb;
+  __shared__ double R[9], c[3], pr[6];
+  __shared__ double smin[4], sg[4];
+  // items: (listed env j = item % nreb, chunk = item / nreb); chunks past an env's count skip
+  const int maxch = (d.kmax + blockDim.x - 1) / blockDim.x;
+  for (int item = blockIdx.x; item < nreb * maxch; item += gridDim.x) {
+    const int e = d.reb_list[item % nreb], ch = item / nreb;
+    if (ch * (int)blockDim.x >= min(d.ncand[e], d.kmax)) continue;  // uniform across the block
+    const EnvS& s = d.es[e];
+    __syncthreads();
+    if (threadIdx.x < 9) R[threadIdx.x] = s.R[threadIdx.x];
+    if (threadIdx.x < 3) c[threadIdx.x] = s.c[threadIdx.x];
+    if (threadIdx.x < 6) pr[threadIdx.x] = s.pr[threadIdx.x];
+    __syncthreads();
+    const d3 cc = ld3(c), pc = mk(pr[0], pr[1], pr[2]), pth = mk(pr[3], pr[4], pr[5]);
+    const double extra = nrm(pth) * d.dhat * 0.25;
+    double amin = INFINITY, gmin = INFINITY;
+    const int i = ch * blockDim.x + threadIdx.x;
+    if (i < min(d.ncand[e], d.kmax)) {
+      unsigned long long rec = d.cand[(size_t)e * d.kmax + i];
+      int kind = (int)(rec >> 62), a = (int)((rec >> 31) & 0x7fffffffu), b = (int)(rec & 0x7fffffffu);
+      Corners C = corners_of(d, kind, a, b);
+      d3 z[4], dz[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (C.ind[k]) {
+          z[k] = mv(R, ind_body(d, C.id[k])) + cc;
+          dz[k] = pc + cross(pth, z[k] - cc);
+        } else {
+          z[k] = gel_pos(d, d.u, C.id[k], e);
+          dz[k] = gel_vec(d, d.p, C.id[k], e);
+        }
+      }
+      double gsep;
+      d3 nsep;
+      if (axis_sep(z, C.na, d.dhat, &gsep, &nsep)) {
+        gmin = gsep;
+      } else {
+        DR D = pair_dist(kind, z);
+        d3 rr = mk(0, 0, 0);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) rr = rr + D.w[k] * z[k];
+        if (D.d > 0) {
+          d3 nn = (1.0 / D.d) * rr;
+          double la = -INFINITY, lb = -INFINITY;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (k < C.na) la = fmax(la, -dot(nn, dz[k]));
+            else lb = fmax(lb, dot(nn, dz[k]));
+          }
+          double l = la + lb + extra;
+          if (l > 0) amin = (1 - d.ccd_s) * D.d / l;
+        }
+      }
+    }
+    amin = warp_min(amin);
+    gmin = warp_min(gmin);
+    if ((threadIdx.x & 31) == 0) { smin[threadIdx.x >> 5] = amin; sg[threadIdx.x >> 5] = gmin; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m = INFINITY, g = INFINITY;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { m = fmin(m, smin[w]); g = fmin(g, sg[w]); }
+      if (m < INFINITY) atomic_min_pos(d.accu + (size_t)U_ACCD * d.Es + e, (float)m);
+      if (g < INFINITY) atomic_min_pos(d.accu + (size_t)U_GFAR * d.Es + e, (float)g);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(128) k_contact_curv(Dev d, double kappa, double eps_f, int ccd_only) {
   int e = blockIdx.y;
   if (e >= d.E) return;
@@ -1862,6 +1994,7 @@ __global__ void k_alpha(Dev d, double h, int pass) {
       s.rebuild += 1;
       d.ncand[e] = 0;
       d.run[e] = 2 | 4;
+      d.reb_list[atomicAdd(d.nreb, 1)] = e;  // compact list for k_broadphase_list / k_ccd_list
       return;
     }
     commit_alpha(d, s, e, a, L);
@@ -2018,9 +2151,13 @@ void launch_vert_setup(const Dev& d, double h, cudaStream_t s) {
   LAUNCHK(KID_VERT_SETUP, s, (k_vert_setup<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d, (float)h)));
 }
 void launch_broadphase(const Dev& d, bool masked, cudaStream_t s) {
+  if (masked) {  // envs listed by k_alpha
+    LAUNCHK(KID_BROADPHASE_LIST, s, (k_broadphase_list<<<4 * 148, 128, 0, s>>>(d, d.dhat + d.bp_margin)));
+    return;
+  }
   int ntot = d.nsv + d.nse + d.nst;
-  int nb = std::max(1, std::min((ntot + 127) / 128, (masked ? 16384 : 4736) / std::max(1, d.E)));
-  LAUNCHK(KID_BROADPHASE, s, (k_broadphase<<<dim3(nb, d.E), 128, 0, s>>>(d, masked ? 1 : 0, d.dhat + d.bp_margin, nullptr, nullptr, 0)));
+  int nb = std::max(1, std::min((ntot + 127) / 128, 4736 / std::max(1, d.E)));
+  LAUNCHK(KID_BROADPHASE, s, (k_broadphase<<<dim3(nb, d.E), 128, 0, s>>>(d, d.dhat + d.bp_margin, nullptr, nullptr, 0)));
 }
 void launch_anchors(const Dev& d, double h, cudaStream_t s) {
   LAUNCHK(KID_ANCHORS, s, (k_anchors<<<cgrid(d), 128, 0, s>>>(d, h * h * d.kappa_phys)));
@@ -2060,11 +2197,10 @@ void launch_curvature(const Dev& d, double h, cudaStream_t s) {
   LAUNCHK(KID_CONTACT_CURV, s, (k_contact_curv_staged<<<sgrid(d), 256, d.contact_smem, s>>>(d, h * h * d.kappa_phys)));
 }
 void launch_alpha(const Dev& d, double h, cudaStream_t s) {
+  cudaMemsetAsync(d.nreb, 0, sizeof(int), s);
   LAUNCHK(KID_ALPHA, s, (k_alpha<<<eblocks(d), 128, 0, s>>>(d, h, 1)));
   launch_broadphase(d, true, s);
-  // rebuild pass: only the few envs that rebuilt do work, so give each many blocks
-  LAUNCHK(KID_CCD, s, (k_contact_curv<<<dim3(std::max(1, std::min(32, 32768 / std::max(1, d.E))), d.E), 128, 0, s>>>(
-                           d, h * h * d.kappa_phys, d.eps_v * h, 1)));
+  LAUNCHK(KID_CCD, s, (k_ccd_list<<<4 * 148, 128, 0, s>>>(d)));
   LAUNCHK(KID_ALPHA, s, (k_alpha<<<eblocks(d), 128, 0, s>>>(d, h, 2)));
 }
 void launch_finalize(const Dev& d, double h, cudaStream_t s) {
@@ -2092,7 +2228,7 @@ void launch_any_active(const Dev& d, int* out, cudaStream_t s) {
 }
 void launch_debug_broadphase(const Dev& d, double r, unsigned long long* out, int* cnt, int cap, cudaStream_t s) {
   int ntot = d.nsv + d.nse + d.nst;
-  LAUNCHK(KID_BROADPHASE, s, (k_broadphase<<<dim3((ntot + 127) / 128, d.E), 128, 0, s>>>(d, 0, r, out, cnt, cap)));
+  LAUNCHK(KID_BROADPHASE, s, (k_broadphase<<<dim3((ntot + 127) / 128, d.E), 128, 0, s>>>(d, r, out, cnt, cap)));
 }
 int contact_smem_bytes(int nsv, int niv) {
   size_t b = sizeof(double) * 3 * (size_t)niv + sizeof(float4) * (size_t)nsv + sizeof(int) * kNearCap;

@@ -99,7 +99,7 @@ EXPORTED = ["tac_create", "tac_step", "tac_markers", "tac_reset", "tac_env_statu
             "tac_last_launch_count", "tac_destroy", "tac_last_error", "tac_get_state", "tac_set_state",
             "tac_debug_broadphase", "tac_debug_surface", "tac_debug_marker_map", "tac_debug_eval",
             "tac_profile_enable", "tac_profile_read", "tac_profile_kernel_name", "tac_env_stats"]
-N_KERNEL_IDS = 23
+N_KERNEL_IDS = 24
 
 
 class TacError(RuntimeError):
