@@ -132,6 +132,8 @@ def run_ours(args, rank, local, ws):
     else:
         scene = w.scene_c3(n_envs=E, n_steps=nsteps, seed0=20260000 + e0)
     scene.params.fixed_iters = FIXED_ITERS
+    if os.environ.get("TAC_BP_MARGIN"):  # experiments only (candidate margin sweep)
+        scene.params.bp_margin = float(os.environ["TAC_BP_MARGIN"])
     sim = P.TacSim.from_scene(scene, device=local)
     poses = torch.tensor(scene.poses, dtype=torch.float32, device=dev).contiguous()  # resident in HBM
     nm = scene.markers.shape[0]

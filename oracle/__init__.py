@@ -74,6 +74,8 @@ def lib():
         L.or_dist_pt.argtypes = [_dp, _dp, _dp, _dp, _dp]
         L.or_dist_ee.restype = C.c_double
         L.or_dist_ee.argtypes = [_dp, _dp, _dp, _dp, _dp]
+        L.or_certificate.restype = C.c_int
+        L.or_certificate.argtypes = [_dp, C.c_int, C.c_double, _dp, _dp]
         L.or_psi.restype = C.c_double
         L.or_psi.argtypes = [C.c_double, C.c_double, _dp]
         L.or_so3.argtypes = [_dp, _dp, _dp]
@@ -113,6 +115,15 @@ def dist_ee(a0, a1, b0, b1):
     args = [_d(x) for x in (a0, a1, b0, b1)]
     d = lib().or_dist_ee(*[a[1] for a in args], w.ctypes.data_as(_dp))
     return d, w
+
+
+def certificate(z, na, dhat):
+    """R15 far-pair certificate on corners z[4][3] (side A = first na): (ok, g, n)."""
+    z, zp = _d(np.asarray(z).reshape(12))
+    g = np.zeros(1)
+    n = np.zeros(3)
+    ok = lib().or_certificate(zp, int(na), float(dhat), g.ctypes.data_as(_dp), n.ctypes.data_as(_dp))
+    return bool(ok), float(g[0]), n
 
 
 def psi(E, nu, F):

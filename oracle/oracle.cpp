@@ -851,7 +851,7 @@ Vecs to_vecs(const Grad& G) { return Vecs{G.g, G.gc, G.gth}; }
 // separated along an axis by g >= dhat, that axis is a separating plane with
 // separation g (every point of A is beyond every point of B along it), so the same
 // bound applies with (g, +-e_axis) in place of (d, n), and the pair carries no
-// barrier term.  Returns false if no axis separates the boxes by dhat.
+// barrier term (d >= g >= dhat).  Returns false if no axis separates the boxes by dhat.
 bool axis_separation(const V3* z, int na, double dhat, double* g, V3* n) {
   double best = -INF;
   V3 bn{0, 0, 0};
@@ -1383,6 +1383,16 @@ double or_dist_ee(const double* a0, const double* a1, const double* b0, const do
   Dist D = dist_ee({a0[0], a0[1], a0[2]}, {a1[0], a1[1], a1[2]}, {b0[0], b0[1], b0[2]}, {b1[0], b1[1], b1[2]});
   for (int k = 0; k < 4; ++k) w[k] = D.w[k];
   return D.d;
+}
+// far-pair certificate of R15 on 4 corners z[12] (side A = first na corners): returns
+// 1 if certified (separation >= dhat), g = the best separation found, n its plane normal
+int or_certificate(const double* z12, int na, double dhat, double* g, double* n3) {
+  V3 z[4];
+  for (int k = 0; k < 4; ++k) z[k] = V3{z12[3 * k], z12[3 * k + 1], z12[3 * k + 2]};
+  V3 n;
+  bool ok = axis_separation(z, na, dhat, g, &n);
+  for (int a = 0; a < 3; ++a) n3[a] = n[a];
+  return ok ? 1 : 0;
 }
 double or_psi(double E, double nu, const double* F9) {
   Problem P;

@@ -128,6 +128,43 @@ def test_distance_random_vs_bruteforce():
         assert np.linalg.norm(r) == pytest.approx(d, rel=1e-10)
 
 
+def test_certificate_closed_forms():
+    """R15 far-pair certificate: the largest axis gap between the two corner boxes,
+    with its axis as the separating-plane normal (n oriented from side B to side A)."""
+    t0, t1, t2 = np.array([0, 0, 0.0]), np.array([1e-3, 0, 0]), np.array([0, 1e-3, 0])
+    ok, g, n = O.certificate(np.stack([[2e-4, 3e-4, 2 * DHAT], t0, t1, t2]), 1, DHAT)
+    assert ok and g == pytest.approx(2 * DHAT, rel=1e-12) and np.array_equal(n, [0, 0, 1])
+    ok, g, n = O.certificate(np.stack([[2e-4, 3e-4, -0.5 * DHAT], t0, t1, t2]), 1, DHAT)
+    assert not ok and g == pytest.approx(0.5 * DHAT, rel=1e-12) and np.array_equal(n, [0, 0, -1])
+    # a point over a tilted triangle: boxes overlap on every axis -> never certified,
+    # however far the point is along the normal (the plane bound takes over, near pair)
+    c, s = math.cos(0.6), math.sin(0.6)
+    t0, t1, t2 = np.array([-1e-3, -1e-3 * c, -1e-3 * s]), np.array([1e-3, -1e-3 * c, -1e-3 * s]), \
+        np.array([0, 1e-3 * c, 1e-3 * s])
+    nrm = np.cross(t1 - t0, t2 - t0)
+    nrm /= np.linalg.norm(nrm)
+    ok, g, _ = O.certificate(np.stack([5 * DHAT * nrm, t0, t1, t2]), 1, DHAT)
+    assert not ok and g < 0
+    # edges separated along y by 1.5 dhat with x-overlapping boxes
+    z = np.array([[0, 0, 0], [1e-3, 0, 1e-4], [5e-4, 1.5 * DHAT, -1e-3], [6e-4, 1.5 * DHAT + 1e-4, 1e-3]])
+    ok, g, n = O.certificate(z, 2, DHAT)
+    assert ok and g == pytest.approx(1.5 * DHAT, rel=1e-12) and np.array_equal(n, [0, -1, 0])
+
+
+def test_certificate_never_exceeds_distance():
+    """Any certified separation is a lower bound of the exact distance (brute force)."""
+    rng = np.random.default_rng(11)
+    n_ok = 0
+    for _ in range(200):
+        z = rng.standard_normal((4, 3)) * 1e-3
+        for na in (1, 2):
+            ok, g, _ = O.certificate(z, na, DHAT)
+            bf = _bf_pt(*z) if na == 1 else _bf_ee(*z)
+            assert g <= bf * (1 + 1e-9) + 1e-15
+            n_ok += ok
+    assert 50 < n_ok < 400
+
+
 # ---------------------------------------------------------------- DK-NCG (P:450-461)
 def _pcg(A, b, x0, iters, Pdiag):
     """Textbook preconditioned CG (Hestenes-Stiefel / Saad Alg. 9.1)."""
