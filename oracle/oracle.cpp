@@ -871,11 +871,13 @@ bool axis_separation(const V3* z, int na, double dhat, double* g, V3* n) {
 double rel_motion(const Problem& P, const Vecs& p);
 // Pairs without an axis certificate ("near") use their exact closest-point plane.
 // All axis-certified ("far") pairs share one bound: each has d(alpha) >= g_i - alpha L_rel
-// >= g_min - alpha L_rel (L_rel bounds the relative motion of any gel surface point vs any
-// indenter point, see rel_motion), so alpha <= (1-s) g_min / L_rel keeps them >= s g_min.
+// >= dhat - alpha L_rel (L_rel bounds the relative motion of any gel surface point vs any
+// indenter point, see rel_motion), so alpha <= (1-s) dhat / L_rel keeps them >= s dhat
+// (R15: the bound depends only on whether a far pair exists, not on its gap).
 double alpha_ccd(const Problem& P, const State& s, const std::vector<Pair>& C, const Vecs& p) {
   double pth = norm(p.th);
-  double a = INF, gmin = INF;
+  double a = INF;
+  bool any_far = false;
   for (const Pair& pr : C) {
     int ci[4];
     bool ind[4];
@@ -889,7 +891,7 @@ double alpha_ccd(const Problem& P, const State& s, const std::vector<Pair>& C, c
     double g;
     V3 n;
     if (axis_separation(z, na, P.dhat, &g, &n)) {
-      gmin = std::min(gmin, g);
+      any_far = true;
       continue;
     }
     Dist D = pair_dist(P, s, pr);
@@ -905,7 +907,7 @@ double alpha_ccd(const Problem& P, const State& s, const std::vector<Pair>& C, c
     if (l > 0) a = std::min(a, (1 - P.ccd_s) * D.d / l);
   }
   double L = rel_motion(P, p);
-  if (gmin < INF && L > 0) a = std::min(a, (1 - P.ccd_s) * gmin / L);
+  if (any_far && L > 0) a = std::min(a, (1 - P.ccd_s) * P.dhat / L);
   return a;
 }
 // bound on the relative motion of any gel surface point vs any indenter point per unit alpha

@@ -629,6 +629,10 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     double lbar = ses.empty() ? 1e-3 : sl / ses.size();
     d.kappa_phys = 0.2 * MT.E * lbar * lbar / (12.25 * P.dhat);
   }
+  if (d.nsv >= 65536 || niv >= 65536) {  // candidate corner ids are packed 16 bit (Dev::ccorn)
+    delete sim;
+    return fail(TAC_EINVAL, "more than 65535 gel-surface or indenter vertices");
+  }
   d.contact_smem = contact_smem_bytes(d.nsv, niv);
   if (d.contact_smem == 0) {
     delete sim;
@@ -684,6 +688,11 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     UP(tets, d.tets);
     UP(tetb, d.tetb);
     UP(Xf, d.X);
+    {
+      std::vector<float4> Xs(sim->sv.size());  // surface-ordered rest positions (staged passes)
+      for (size_t i = 0; i < sim->sv.size(); ++i) Xs[i] = Xf[sim->sv[i]];
+      UP(Xs, d.Xs);
+    }
     UP(massf, d.mass);
     UP(smuf, d.smu);
     UP(vflag, d.vflag);
@@ -722,7 +731,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
         (rc = zalloc(sim, (size_t)kNAcc * d.Es, &d.acc)) || (rc = zalloc(sim, (size_t)kNAccU * d.Es, &d.accu)) ||
         (rc = zalloc(sim, (size_t)d.Es, &d.dalpha)) || (rc = zalloc(sim, (size_t)d.Es, &d.beta)) ||
         (rc = zalloc(sim, (size_t)d.Es, &d.run)) || (rc = zalloc(sim, (size_t)d.Es, &d.pcf)) ||
-        (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.cand)) || (rc = zalloc(sim, 2 * (size_t)d.E * d.kmax, &d.cgeo)) || (rc = zalloc(sim, (size_t)d.E, &d.ncand)) || (rc = zalloc(sim, 3 * (size_t)d.E * d.kmax, &d.nearl)) ||
+        (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.cand)) || (rc = zalloc(sim, 2 * (size_t)d.E * d.kmax, &d.cgeo)) || (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.cgap)) || (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.ccorn)) || (rc = zalloc(sim, (size_t)d.E, &d.ncand)) || (rc = zalloc(sim, 3 * (size_t)d.E * d.kmax, &d.nearl)) ||
         (rc = zalloc(sim, 3 * (size_t)d.E, &d.nnear)) ||
         (rc = zalloc(sim, (size_t)std::max(1, d.nsv) * d.Es, &d.usurf)) || (rc = zalloc(sim, (size_t)std::max(1, d.nsv) * d.Es, &d.psurf)) ||
         (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc)) || (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc_f1)) || (rc = zalloc(sim, (size_t)d.E, &d.nanc)) || (rc = zalloc(sim, (size_t)d.E, &d.reb_list)) ||

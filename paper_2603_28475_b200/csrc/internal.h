@@ -47,6 +47,10 @@ struct EnvS {
   double Dc[9], Dth[9];       // rigid diagonal blocks of the last accepted evaluation
   double E, Eprev, alpha, gp_prev, gPg_prev, S, beta, best_pg, pg, pose_res;
   double Lrel_last;
+  double odo, odo_base, Lc;   // classification odometer (R15 cache): path-length coordinate of the
+                              // trial point / of x_k, L_rel of the current direction
+  int cache_ok;               // candidate gap cache valid (same candidate list, classified once)
+  int pad_cache;
   double Ep[5];                // energy parts of the last evaluation (diagnostics)
   int iter, halv, restart, reeval, mode, flags, best_it, accepted, rebuild, ncand_over;
   int ncand_max, nanc_last;   // per-step statistics (tac_env_stats)
@@ -75,6 +79,7 @@ struct Dev {
   const int4* tets;      // [nt]
   const float4* tetb;    // [nt][3]: (b1, vol), (b2, fixed-corner mask bits), (b3, 0)
   const float4* X;       // [nv] rest position (fp32 exact), w = 0
+  const float4* Xs;      // [nsv] rest positions of the gel-surface vertices (surface-local order)
   const float* mass;     // [nv]
   const float* smu;      // [nv] sum_e V_e mu |b_{e,v}|^2 (state-independent elastic diagonal / h^2)
   const unsigned char* vflag;  // [nv] bit0 fixed, bit1 on the gel surface
@@ -102,6 +107,9 @@ struct Dev {
   int* run;              // [Es] bit0 evaluate, bit1 direction, bit2 rebuild
   float4* pcf;           // [Es] rigid p_c (float) for L_rel
   unsigned long long* cand;  // [E][kmax] (kind<<62 | a<<31 | b)
+  uint2* ccorn;           // [E][kmax] corner ids of each candidate, 4 x 16 bit (gel: surface-local id,
+                         // indenter: vertex id), written with the candidate list
+  float* cgap;            // [E][kmax] certified axis gap + odometer at certification (rounded down)
   float4* cgeo;          // [E][kmax][2] pair geometry of the last evaluation: (d, n), (w0..w3)
   int* ncand;            // [E]
   int* nearl;            // [E][3][kmax] indices of near candidates (no separating-axis certificate), per pair kind

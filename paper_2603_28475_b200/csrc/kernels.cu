@@ -310,6 +310,16 @@ __device__ __forceinline__ CornersL corners_l(const Dev& d, int kind, int a, int
   }
   return c;
 }
+// corner ids of a candidate record packed 4 x 16 bit: gel corners by surface-local id,
+// indenter corners by vertex id (kind decides which); nsv, niv < 65536 (checked at create)
+__device__ __forceinline__ uint2 pack_corners(const Dev& d, unsigned long long rec) {
+  int kind = (int)(rec >> 62), a = (int)((rec >> 31) & 0x7fffffffu), b = (int)(rec & 0x7fffffffu);
+  CornersL C = corners_l(d, kind, a, b);
+  unsigned id[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) id[k] = (unsigned)(C.ind[k] ? C.gid[k] : C.sid[k]);
+  return make_uint2(id[0] | (id[1] << 16), id[2] | (id[3] << 16));
+}
 __device__ __forceinline__ d3 gel_pos(const Dev& d, const float* u, int v, int e) {
   float4 X = d.X[v];
   return mk((double)X.x + (double)u[vidx(d, 0, v, e)], (double)X.y + (double)u[vidx(d, 1, v, e)],
@@ -364,6 +374,7 @@ __global__ void k_step_setup(Dev d, const float* poses) {
   s.flags = (nrm(dc) > 2e-3 || nrm(so3_log(RRt)) > 5 * M_PI / 180) ? 16 : 0;
   s.iter = 0; s.halv = 0; s.restart = 1; s.reeval = 0; s.mode = kActive; s.best_it = 0; s.accepted = 0;
   s.rebuild = 0; s.ncand_over = 0; s.ncand_max = 0; s.nanc_last = 0;
+  s.odo = 0; s.odo_base = 0; s.Lc = 0; s.cache_ok = 0;
   s.alpha = 0; s.S = 0; s.best_pg = INFINITY; s.pg = 0; s.E = 0; s.Eprev = 0; s.gp_prev = 0; s.beta = 0;
   for (int i = 0; i < 6; ++i) s.pr[i] = 0;
   d.dalpha[e] = 0.f;
@@ -411,7 +422,7 @@ __shared__ int g_bp_scnt;
 
 template <int NIND>
 __device__ void bp_query(const Dev& d, int kind, int gid, const double* glo, const double* ghi, double r, int root,
-                         unsigned long long* out, int* cnt, int cap, bool* over) {
+                         unsigned long long* out, uint2* cc, int* cnt, int cap, bool* over) {
   const float eps = 1e-7f;
   float qlo[3], qhi[3];
   for (int a = 0; a < 3; ++a) {
@@ -460,16 +471,20 @@ __device__ void bp_query(const Dev& d, int kind, int gid, const double* glo, con
         g_bp_sbuf[ss] = rec;
       } else {  // staging full: reserve directly
         int slot = atomicAdd(cnt, 1);
-        if (slot < cap) out[slot] = rec;
-        else *over = true;
+        if (slot < cap) {
+          out[slot] = rec;
+          if (cc) cc[slot] = pack_corners(d, rec);
+        } else {
+          *over = true;
+        }
       }
     }
   }
 }
 
 // candidates of gel-surface primitives [i0, i1) (strided) of env e
-__device__ void bp_range(const Dev& d, int e, int i0, int i1, int stride, double r, unsigned long long* out, int* cnt,
-                         int cap, const double* R, const double* c) {
+__device__ void bp_range(const Dev& d, int e, int i0, int i1, int stride, double r, unsigned long long* out, uint2* cc,
+                         int* cnt, int cap, const double* R, const double* c) {
   bool over = false;
   for (int i = i0; i < i1; i += stride) {
     int vv[3], nvx, kind, gid, root;
@@ -493,22 +508,26 @@ __device__ void bp_range(const Dev& d, int e, int i0, int i1, int stride, double
         hi[a] = j ? fmax(hi[a], b) : b;
       }
     }
-    if (kind == 0) bp_query<3>(d, 0, gid, lo, hi, r, root, out, cnt, cap, &over);
-    else if (kind == 2) bp_query<2>(d, 2, gid, lo, hi, r, root, out, cnt, cap, &over);
-    else bp_query<1>(d, 1, gid, lo, hi, r, root, out, cnt, cap, &over);
+    if (kind == 0) bp_query<3>(d, 0, gid, lo, hi, r, root, out, cc, cnt, cap, &over);
+    else if (kind == 2) bp_query<2>(d, 2, gid, lo, hi, r, root, out, cc, cnt, cap, &over);
+    else bp_query<1>(d, 1, gid, lo, hi, r, root, out, cc, cnt, cap, &over);
   }
   if (over) d.es[e].ncand_over = 1;
 }
 
-__device__ void bp_flush(unsigned long long* out, int* cnt, int cap, bool* over) {
+__device__ void bp_flush(const Dev& d, unsigned long long* out, uint2* cc, int* cnt, int cap, bool* over) {
   __syncthreads();
   __shared__ int base;
   const int n = min(g_bp_scnt, kBpStage);
   if (threadIdx.x == 0) base = n ? atomicAdd(cnt, n) : 0;
   __syncthreads();
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
-    if (base + j < cap) out[base + j] = g_bp_sbuf[j];
-    else *over = true;
+    if (base + j < cap) {
+      out[base + j] = g_bp_sbuf[j];
+      if (cc) cc[base + j] = pack_corners(d, g_bp_sbuf[j]);
+    } else {
+      *over = true;
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) g_bp_scnt = 0;
@@ -529,12 +548,14 @@ __global__ void __launch_bounds__(128) k_broadphase(Dev d, double r, unsigned lo
   unsigned long long* out = out_override ? out_override : d.cand + (size_t)e * d.kmax;
   int* cnt = cnt_override ? cnt_override : d.ncand + e;
   int cap = out_override ? cap_override : d.kmax;
+  uint2* cc = out_override ? nullptr : d.ccorn + (size_t)e * d.kmax;
   int ntot = d.nsv + d.nse + d.nst;
   if (threadIdx.x == 0) g_bp_scnt = 0;
   __syncthreads();
-  bp_range(d, e, blockIdx.x * blockDim.x + threadIdx.x, ntot, gridDim.x * blockDim.x, r, out, cnt, cap, R, c);
+  if (!out_override && blockIdx.x == 0 && threadIdx.x == 0) d.es[e].cache_ok = 0;  // new candidate list
+  bp_range(d, e, blockIdx.x * blockDim.x + threadIdx.x, ntot, gridDim.x * blockDim.x, r, out, cc, cnt, cap, R, c);
   bool over = false;
-  bp_flush(out, cnt, cap, &over);
+  bp_flush(d, out, cc, cnt, cap, &over);
   if (over) d.es[e].ncand_over = 1;
 }
 
@@ -555,9 +576,10 @@ __global__ void __launch_bounds__(128) k_broadphase_list(Dev d, double r) {
     if (threadIdx.x == 0) g_bp_scnt = 0;
     __syncthreads();
     const int i = ch * blockDim.x + threadIdx.x;
-    bp_range(d, e, i, min(ntot, i + 1), 1, r, d.cand + (size_t)e * d.kmax, d.ncand + e, d.kmax, R, c);
+    bp_range(d, e, i, min(ntot, i + 1), 1, r, d.cand + (size_t)e * d.kmax, d.ccorn + (size_t)e * d.kmax, d.ncand + e,
+             d.kmax, R, c);
     bool over = false;
-    bp_flush(d.cand + (size_t)e * d.kmax, d.ncand + e, d.kmax, &over);
+    bp_flush(d, d.cand + (size_t)e * d.kmax, d.ccorn + (size_t)e * d.kmax, d.ncand + e, d.kmax, &over);
     if (over) d.es[e].ncand_over = 1;
   }
 }
@@ -1239,11 +1261,38 @@ __device__ __forceinline__ Stage stage_ptrs(const Dev& d, char* sh) {
   S.nl = reinterpret_cast<int*>(sh + sizeof(double) * 3 * d.niv + sizeof(float4) * d.nsv);
   return S;
 }
+// staging loops issue kStageILP independent loads per thread before the shared stores
+// (one load round trip per kStageILP x blockDim elements instead of one per blockDim)
+constexpr int kStageILP = 4;
 __device__ void stage_env(const Dev& d, const Stage& S, const float4* surf, int e, const double* R) {
-  for (int i = threadIdx.x; i < d.nsv; i += blockDim.x) S.sv4[i] = surf[(size_t)i * d.Es + e];
-  for (int j = threadIdx.x; j < d.niv; j += blockDim.x) {
-    d3 y = mv(R, ind_body(d, j));
-    S.sy[3 * j] = y.x; S.sy[3 * j + 1] = y.y; S.sy[3 * j + 2] = y.z;
+  for (int i0 = threadIdx.x; i0 < d.nsv; i0 += kStageILP * blockDim.x) {
+    float4 v[kStageILP];
+#pragma unroll
+    for (int k = 0; k < kStageILP; ++k) {
+      const int i = i0 + k * blockDim.x;
+      if (i < d.nsv) v[k] = surf[(size_t)i * d.Es + e];
+    }
+#pragma unroll
+    for (int k = 0; k < kStageILP; ++k) {
+      const int i = i0 + k * blockDim.x;
+      if (i < d.nsv) S.sv4[i] = v[k];
+    }
+  }
+  for (int j0 = threadIdx.x; j0 < d.niv; j0 += kStageILP * blockDim.x) {
+    float4 yb[kStageILP];
+#pragma unroll
+    for (int k = 0; k < kStageILP; ++k) {
+      const int j = j0 + k * blockDim.x;
+      if (j < d.niv) yb[k] = __ldg(d.Y + j);
+    }
+#pragma unroll
+    for (int k = 0; k < kStageILP; ++k) {
+      const int j = j0 + k * blockDim.x;
+      if (j < d.niv) {
+        d3 y = mv(R, mk(yb[k].x, yb[k].y, yb[k].z));
+        S.sy[3 * j] = y.x; S.sy[3 * j + 1] = y.y; S.sy[3 * j + 2] = y.z;
+      }
+    }
   }
 }
 __device__ __forceinline__ d3 staged_gel_pos(const Dev& d, const Stage& S, int gid, int sid) {
@@ -1252,80 +1301,181 @@ __device__ __forceinline__ d3 staged_gel_pos(const Dev& d, const Stage& S, int g
   return mk((double)X.x + (double)u.x, (double)X.y + (double)u.y, (double)X.z + (double)u.z);
 }
 
-// staged classification only (low register count): corners from shared memory,
-// separating-axis certificate -> g_min, otherwise appended to the env's near list
+// staged classification.  Phase A reads each candidate's cached certificate h = g +
+// odometer-at-certification: the pair's axis gap now is >= h - odo (the gap changes by at
+// most the relative motion, which the odometer bounds along the path of evaluated
+// points), so h - odo >= dhat keeps it far without touching its geometry (R15 cache).
+// The rest (every pair after a new candidate list) is queued in shared memory and phase
+// B runs the axis test on them densely with corners from shared memory: certificate ->
+// cache refresh, otherwise the block-local near list of its kind, flushed with one global
+// reservation per kind.  Work per CTA = chunks of kClassChunk candidates, so the number
+// of dependent global round trips per CTA is a handful, not one per candidate batch.
+constexpr int kClassChunk = 4096;  // candidates per chunk (queue offsets fit 16 bits)
+constexpr int kClassA = kClassChunk / 256;  // phase-A candidates per thread
+constexpr int kClassNL = 1024;     // block-local near-list capacity per kind and chunk
+__device__ __forceinline__ void push_local(bool mine, int lane, int* cnt, unsigned short* list, int cap, int off,
+                                           int* gcnt, int* glist, int chunk0) {
+  unsigned m = __ballot_sync(0xffffffffu, mine);
+  if (!m) return;
+  int slot0 = 0;
+  if (lane == 0) slot0 = atomicAdd(cnt, __popc(m));
+  slot0 = __shfl_sync(0xffffffffu, slot0, 0);
+  const int slot = slot0 + __popc(m & ((1u << lane) - 1));
+  if (!mine) return;
+  if (slot < cap) list[slot] = (unsigned short)off;
+  else glist[atomicAdd(gcnt, 1)] = chunk0 + off;  // local list full: direct global append
+}
 __global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
   // fp32 positions (gel X + u, indenter c + R Y) carry absolute errors <= ~6e-9 m at the
   // pad scale, so a pair is certified far only if its fp32 gap exceeds dhat + kClassMargin
-  // and g_min is lowered by the same margin: both certificates stay conservative (R15)
+  // and the cached gap is lowered by the same margin: the certificate stays conservative
   constexpr float kClassMargin = 1e-7f;
   extern __shared__ __align__(16) char shc4[];
+  __shared__ unsigned short q[kClassChunk];
+  __shared__ unsigned short nl[3][kClassNL];
+  __shared__ int qn, nn[3], nbase[3];
+  __shared__ double Rs[9], cs[3];
   int e = blockIdx.y;
   if (e >= d.E || !(d.run[e] & 1)) return;
+  if ((int)blockIdx.x * kClassChunk >= min(d.ncand[e], d.kmax)) return;  // no chunk: skip the staging
   const EnvS& s = d.es[e];
-  float4* su = reinterpret_cast<float4*>(shc4);                 // [nsv] u
+  float4* sx = reinterpret_cast<float4*>(shc4);                 // [nsv] gel X + u
   float4* sy = reinterpret_cast<float4*>(shc4 + sizeof(float4) * d.nsv);  // [niv] c + R Y
-  for (int i = threadIdx.x; i < d.nsv; i += blockDim.x) su[i] = d.usurf[(size_t)i * d.Es + e];
-  for (int j = threadIdx.x; j < d.niv; j += blockDim.x) {
-    d3 y = mv(s.R, ind_body(d, j)) + ld3(s.c);
-    sy[j] = make_float4((float)y.x, (float)y.y, (float)y.z, 0.f);
+  if (threadIdx.x < 9) Rs[threadIdx.x] = s.R[threadIdx.x];
+  if (threadIdx.x < 3) cs[threadIdx.x] = s.c[threadIdx.x];
+  for (int i0 = threadIdx.x; i0 < d.nsv; i0 += kStageILP * blockDim.x) {
+    float4 X[kStageILP], u[kStageILP];
+#pragma unroll
+    for (int k = 0; k < kStageILP; ++k) {
+      const int i = i0 + k * blockDim.x;
+      if (i < d.nsv) { X[k] = __ldg(d.Xs + i); u[k] = d.usurf[(size_t)i * d.Es + e]; }
+    }
+#pragma unroll
+    for (int k = 0; k < kStageILP; ++k) {
+      const int i = i0 + k * blockDim.x;
+      if (i < d.nsv) sx[i] = make_float4(X[k].x + u[k].x, X[k].y + u[k].y, X[k].z + u[k].z, 0.f);
+    }
   }
-  __syncthreads();
+  __syncthreads();  // Rs, cs
+  for (int j0 = threadIdx.x; j0 < d.niv; j0 += kStageILP * blockDim.x) {
+    float4 yb[kStageILP];
+#pragma unroll
+    for (int k = 0; k < kStageILP; ++k) {
+      const int j = j0 + k * blockDim.x;
+      if (j < d.niv) yb[k] = __ldg(d.Y + j);
+    }
+#pragma unroll
+    for (int k = 0; k < kStageILP; ++k) {
+      const int j = j0 + k * blockDim.x;
+      if (j < d.niv) {
+        d3 y = mv(Rs, mk(yb[k].x, yb[k].y, yb[k].z)) + ld3(cs);
+        sy[j] = make_float4((float)y.x, (float)y.y, (float)y.z, 0.f);
+      }
+    }
+  }
+  const bool cached = s.cache_ok;
+  const double odo = s.odo, thr = d.dhat + odo;
   const float dh = (float)d.dhat + kClassMargin;
   const int n = min(d.ncand[e], d.kmax);
   const unsigned long long* cand = d.cand + (size_t)e * d.kmax;
+  float* hc = d.cgap + (size_t)e * d.kmax;
+  const uint2* ccorn = d.ccorn + (size_t)e * d.kmax;
+  int* gcnt = d.nnear + 3 * e;
+  int* glist = d.nearl + (size_t)e * 3 * d.kmax;
   const int lane = threadIdx.x & 31;
-  float gmin = INFINITY;
-  const int stride = gridDim.x * blockDim.x;
-  for (int base = blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n; base += stride) {
-    int i = base + lane;
-    bool near = false;
-    int kind = 0;
-    if (i < n) {
-      unsigned long long rec = cand[i];
-      kind = (int)(rec >> 62);
-      int a = (int)((rec >> 31) & 0x7fffffffu), b = (int)(rec & 0x7fffffffu);
-      CornersL C = corners_l(d, kind, a, b);
-      float zx[4], zy[4], zz[4];
+  bool any_far = false;
+  for (int c0 = blockIdx.x * kClassChunk; c0 < n; c0 += gridDim.x * kClassChunk) {
+    if (threadIdx.x < 3) nn[threadIdx.x] = 0;
+    if (threadIdx.x == 0) qn = 0;
+    __syncthreads();  // (also orders the staging above before phase B)
+    // phase A: all cache loads first, then the decisions and the warp-aggregated queue push
+    float h[kClassA];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        float4 p;
-        if (C.ind[k]) {
-          p = sy[C.gid[k]];
-        } else {
-          float4 X = __ldg(d.X + C.gid[k]), u = su[C.sid[k]];
-          p = make_float4(X.x + u.x, X.y + u.y, X.z + u.z, 0.f);
-        }
-        zx[k] = p.x; zy[k] = p.y; zz[k] = p.z;
-      }
-      float best = -INFINITY;
-      const float* zs[3] = {zx, zy, zz};
-#pragma unroll
-      for (int ax = 0; ax < 3; ++ax) {
-        const float* z = zs[ax];
-        float loA = INFINITY, hiA = -INFINITY, loB = INFINITY, hiB = -INFINITY;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (k < C.na) { loA = fminf(loA, z[k]); hiA = fmaxf(hiA, z[k]); }
-          else { loB = fminf(loB, z[k]); hiB = fmaxf(hiB, z[k]); }
-        }
-        best = fmaxf(best, fmaxf(loA - hiB, loB - hiA));
-      }
-      if (best >= dh) gmin = fminf(gmin, best - kClassMargin);
-      else near = true;
+    for (int k = 0; k < kClassA; ++k) {
+      const int i = c0 + k * 256 + threadIdx.x;
+      h[k] = (cached && i < n) ? hc[i] : -INFINITY;
     }
 #pragma unroll
-    for (int kk = 0; kk < 3; ++kk) {  // per-kind near lists (convergent near-pair passes)
-      bool mine = near && kind == kk;
-      unsigned m = __ballot_sync(0xffffffffu, mine);
+    for (int k = 0; k < kClassA; ++k) {
+      const int off = k * 256 + threadIdx.x;
+      const bool in = c0 + off < n;
+      const bool hit = in && (double)h[k] >= thr;
+      any_far |= hit;
+      const bool need = in && !hit;
+      unsigned m = __ballot_sync(0xffffffffu, need);
       int slot0 = 0;
-      if (lane == 0 && m) slot0 = atomicAdd(d.nnear + 3 * e + kk, __popc(m));
+      if (lane == 0 && m) slot0 = atomicAdd(&qn, __popc(m));
       slot0 = __shfl_sync(0xffffffffu, slot0, 0);
-      if (mine) d.nearl[((size_t)e * 3 + kk) * d.kmax + slot0 + __popc(m & ((1u << lane) - 1))] = i;
+      if (need) q[slot0 + __popc(m & ((1u << lane) - 1))] = (unsigned short)off;
     }
+    __syncthreads();
+    const int nq = qn;
+    // phase B: queued pairs, two per thread in flight
+    for (int jb = threadIdx.x & ~31; jb < nq; jb += 2 * blockDim.x) {
+      int off[2], kind[2];
+      uint2 cc[2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int jq = jb + t * blockDim.x + lane;
+        off[t] = jq < nq ? q[jq] : -1;
+        kind[t] = 0;
+        if (off[t] >= 0) { kind[t] = (int)(cand[c0 + off[t]] >> 62); cc[t] = ccorn[c0 + off[t]]; }
+      }
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        bool near = false;
+        if (off[t] >= 0) {
+          const int i = c0 + off[t];
+          const unsigned id[4] = {cc[t].x & 0xffffu, cc[t].x >> 16, cc[t].y & 0xffffu, cc[t].y >> 16};
+          // corner k is on the indenter: kind 0 (gel point, indenter triangle) k >= 1,
+          // kind 1 (indenter point, gel triangle) k == 0, kind 2 (gel edge, indenter edge) k >= 2
+          const int kd = kind[t], na = kd == 2 ? 2 : 1;
+          float zx[4], zy[4], zz[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const bool ind = kd == 0 ? k >= 1 : (kd == 1 ? k == 0 : k >= 2);
+            const float4 p = ind ? sy[id[k]] : sx[id[k]];
+            zx[k] = p.x; zy[k] = p.y; zz[k] = p.z;
+          }
+          float best = -INFINITY;
+          const float* zs[3] = {zx, zy, zz};
+#pragma unroll
+          for (int ax = 0; ax < 3; ++ax) {
+            const float* z = zs[ax];
+            float loA = INFINITY, hiA = -INFINITY, loB = INFINITY, hiB = -INFINITY;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              if (k < na) { loA = fminf(loA, z[k]); hiA = fmaxf(hiA, z[k]); }
+              else { loB = fminf(loB, z[k]); hiB = fmaxf(hiB, z[k]); }
+            }
+            best = fmaxf(best, fmaxf(loA - hiB, loB - hiA));
+          }
+          if (best >= dh) {
+            any_far = true;
+            hc[i] = __double2float_rd(((double)best - (double)kClassMargin) + odo);
+          } else {
+            near = true;
+            if (!cached) hc[i] = -INFINITY;  // slot of a fresh list: never valid until re-certified
+          }
+        }
+#pragma unroll
+        for (int kk = 0; kk < 3; ++kk)  // per-kind near lists (convergent near-pair passes)
+          push_local(near && kind[t] == kk, lane, &nn[kk], nl[kk], kClassNL, off[t], gcnt + kk,
+                     glist + (size_t)kk * d.kmax, c0);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) nbase[threadIdx.x] = atomicAdd(gcnt + threadIdx.x, min(nn[threadIdx.x], kClassNL));
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 3; ++kk) {
+      const int m = min(nn[kk], kClassNL);
+      for (int t = threadIdx.x; t < m; t += blockDim.x) glist[(size_t)kk * d.kmax + nbase[kk] + t] = c0 + nl[kk][t];
+    }
+    __syncthreads();  // q / nl / counters reuse
   }
-  for (int o = 16; o > 0; o >>= 1) gmin = fminf(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
-  if (lane == 0 && gmin < INFINITY) atomic_min_pos(d.accu + (size_t)U_GFAR * d.Es + e, gmin);
+  // far pairs share the bound (1 - s) dhat / L_rel (R15): only their existence is recorded
+  if (__any_sync(0xffffffffu, any_far) && lane == 0) atomic_min_pos(d.accu + (size_t)U_GFAR * d.Es + e, (float)d.dhat);
 }
 
 // curvature + near-pair step bounds from the cached geometry, p staged in shared memory
@@ -1461,7 +1611,9 @@ __global__ void k_accept(Dev d, double h) {
     return;
   }
   bool ok = first || s.reeval || (isfinite(E) && E <= s.E + d.c1 * s.alpha * s.gp_prev + d.eps_E * fabs(s.E));
+  s.cache_ok = 1;  // this evaluation classified every candidate of the current list
   if (ok) {
+    s.odo_base = s.odo;
     s.E = E;
     for (int k = 0; k < 6; ++k) s.gr[k] = gr[k];
     sym6_to_9(Dc6, s.Dc);
@@ -1475,14 +1627,17 @@ __global__ void k_accept(Dev d, double h) {
   s.accepted = 0;
   d.accu[U_GFAR * Es + e] = 0x7f800000u;  // the next evaluation re-classifies
   s.halv += 1;
+  s.odo_base = s.odo + s.alpha * s.Lc;  // the odometer path returns to x_k
   if (s.halv <= d.max_halv) {
     double an = 0.5 * s.alpha;
+    s.odo = s.odo_base + an * s.Lc;
     d.dalpha[e] = (float)(an - s.alpha);
     s.alpha = an;
     apply_pose(s, an);
   } else {
     d.dalpha[e] = (float)(-s.alpha);
     s.alpha = 0;
+    s.odo = s.odo_base;
     for (int i = 0; i < 3; ++i) s.c[i] = s.cp[i];
     for (int i = 0; i < 9; ++i) s.R[i] = s.Rp[i];
     s.restart = 1;
@@ -1953,6 +2108,8 @@ __device__ void commit_alpha(const Dev& d, EnvS& s, int e, double a, double L) {
   apply_pose(s, a);
   d.dalpha[e] = (float)a;
   s.S += a * L;
+  s.odo = s.odo_base + a * L;  // trial point x_k + a p on the odometer path
+  s.Lc = L;
   d.run[e] = 1;
 }
 
@@ -1981,7 +2138,7 @@ __global__ void k_alpha(Dev d, double h, int pass) {
     d.accu[U_LREL * Es + e] = 0u;
     double accd = (double)__uint_as_float(d.accu[U_ACCD * Es + e]);
     double gfar = (double)__uint_as_float(d.accu[U_GFAR * Es + e]);
-    if (gfar < INFINITY && L > 0) accd = fmin(accd, (1 - d.ccd_s) * gfar / L);  // far pairs (R15)
+    if (gfar < INFINITY && L > 0) accd = fmin(accd, (1 - d.ccd_s) * d.dhat / L);  // far pairs (R15)
     d.accu[U_ACCD * Es + e] = 0x7f800000u;
     d.accu[U_GFAR * Es + e] = 0x7f800000u;
     double aup = M > 0 ? d.dhat / (2 * M) : INFINITY;
@@ -1992,6 +2149,7 @@ __global__ void k_alpha(Dev d, double h, int pass) {
       s.Lrel_last = L;
       s.ncand_max = max(s.ncand_max, d.ncand[e]);
       s.rebuild += 1;
+      s.cache_ok = 0;
       d.ncand[e] = 0;
       d.run[e] = 2 | 4;
       d.reb_list[atomicAdd(d.nreb, 1)] = e;  // compact list for k_broadphase_list / k_ccd_list
@@ -2002,7 +2160,7 @@ __global__ void k_alpha(Dev d, double h, int pass) {
     if (!(rb & 4)) return;
     double accd = (double)__uint_as_float(d.accu[U_ACCD * Es + e]);
     double gfar = (double)__uint_as_float(d.accu[U_GFAR * Es + e]);
-    if (gfar < INFINITY && s.Lrel_last > 0) accd = fmin(accd, (1 - d.ccd_s) * gfar / s.Lrel_last);
+    if (gfar < INFINITY && s.Lrel_last > 0) accd = fmin(accd, (1 - d.ccd_s) * d.dhat / s.Lrel_last);
     d.accu[U_ACCD * Es + e] = 0x7f800000u;
     d.accu[U_GFAR * Es + e] = 0x7f800000u;
     s.S = 0;
@@ -2174,7 +2332,8 @@ void launch_eval(const Dev& d, double h, cudaStream_t s) {
     dim3 g = vgrid(d, d.nrest);
     LAUNCHK(KID_ELEM_GRAD, s, (k_elem_grad<<<dim3(g.y, g.x), dim3(32, 8), 0, s>>>(d, (float)(h * h))));
   }
-  LAUNCHK(KID_CONTACT_CLASSIFY, s, (k_contact_classify_staged<<<sgrid(d), 256, d.contact_smem, s>>>(d)));
+  const size_t cls_smem = sizeof(float4) * (size_t)(d.nsv + d.niv);  // [nsv] X + u, [niv] c + R Y
+  LAUNCHK(KID_CONTACT_CLASSIFY, s, (k_contact_classify_staged<<<sgrid(d), 256, cls_smem, s>>>(d)));
   const double kap = h * h * d.kappa_phys;
   LAUNCHK(KID_CONTACT_GRAD, s, (k_contact_near<0><<<cgrid(d), 128, 0, s>>>(d, kap)));
   LAUNCHK(KID_CONTACT_NEAR_IG, s, (k_contact_near<1><<<cgrid(d), 128, 0, s>>>(d, kap)));
