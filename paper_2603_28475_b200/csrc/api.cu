@@ -707,6 +707,31 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     UP(it4, d.it);
     UP(nodes, d.bvh);
     UP(prims, d.bvh_prims);
+    {
+      // per-prim body-frame boxes in leaf order (lo.xyz | prim id bits, hi.xyz): the exact
+      // min / max of the float Y the kernels use, so the leaf test needs one load per prim
+      std::vector<float4> pbox(2 * prims.size());
+      const int nie_ = (int)ies.size();
+      for (size_t p = 0; p < prims.size(); ++p) {
+        const int prim = prims[p];
+        int ids[3], n;
+        if ((int)p < nit) { ids[0] = I.tris[3 * prim]; ids[1] = I.tris[3 * prim + 1]; ids[2] = I.tris[3 * prim + 2]; n = 3; }
+        else if ((int)p < nit + nie_) { ids[0] = sim->ie_flat[2 * prim]; ids[1] = sim->ie_flat[2 * prim + 1]; n = 2; }
+        else { ids[0] = prim; n = 1; }
+        float lo[3], hi[3];
+        for (int a = 0; a < 3; ++a) {
+          auto comp = [&](int v) { return a == 0 ? Yf[v].x : (a == 1 ? Yf[v].y : Yf[v].z); };
+          lo[a] = hi[a] = comp(ids[0]);
+          for (int j = 1; j < n; ++j) { lo[a] = std::min(lo[a], comp(ids[j])); hi[a] = std::max(hi[a], comp(ids[j])); }
+        }
+        int bits = prim;
+        float fb;
+        memcpy(&fb, &bits, sizeof(float));
+        pbox[2 * p] = make_float4(lo[0], lo[1], lo[2], fb);
+        pbox[2 * p + 1] = make_float4(hi[0], hi[1], hi[2], 0.f);
+      }
+      UP(pbox, d.bvh_pbox);
+    }
     UP(mki, d.mk_idx);
     UP(mkw, d.mk_w);
     UP(tile_vstart, d.tile_vstart);

@@ -94,6 +94,7 @@ struct Dev {
   const int4* it;        // [nit]
   const BNode* bvh;      // nodes of the 3 BVHs
   const int* bvh_prims;  // prim lists
+  const float4* bvh_pbox;  // [2 n_prims] per-prim box in leaf order: (lo, prim id bits), (hi, 0)
   int root_tri, root_edge, root_vert;
   const int4* mk_idx;    // [nm]
   const float4* mk_w;    // [nm]

@@ -442,26 +442,16 @@ __device__ void bp_query(const Dev& d, int kind, int gid, const double* glo, con
       stack[sp++] = nd.right;
       continue;
     }
-    int p0 = -nd.left - 1;
-    for (int k = 0; k < nd.right; ++k) {
-      int prim = d.bvh_prims[p0 + k];
-      int vid[3];
-      if (NIND == 3) { int4 t = d.it[prim]; vid[0] = t.x; vid[1] = t.y; vid[2] = t.z; }
-      else if (NIND == 2) { int2 t = d.ie[prim]; vid[0] = t.x; vid[1] = t.y; }
-      else vid[0] = prim;
+    const int p0 = -nd.left - 1, np = nd.right;
+    for (int k = 0; k < np; ++k) {
+      const float4 blo = __ldg(d.bvh_pbox + 2 * (p0 + k)), bhi = __ldg(d.bvh_pbox + 2 * (p0 + k) + 1);
+      const int prim = __float_as_int(blo.w);
+      // exact prim box (min / max of its float Y corners), tested in double as before
+      const double lo[3] = {blo.x, blo.y, blo.z}, hi[3] = {bhi.x, bhi.y, bhi.z};
       bool ok = true;
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        float4 y0 = d.Y[vid[0]];
-        double lo = (a == 0 ? y0.x : a == 1 ? y0.y : y0.z), hi = lo;
-        for (int j = 1; j < NIND; ++j) {
-          float4 yj = d.Y[vid[j]];
-          double v = (a == 0 ? yj.x : a == 1 ? yj.y : yj.z);
-          lo = fmin(lo, v);
-          hi = fmax(hi, v);
-        }
-        if (glo[a] > __dadd_rn(hi, r) || lo > __dadd_rn(ghi[a], r)) ok = false;
-      }
+      for (int a = 0; a < 3; ++a)
+        if (glo[a] > __dadd_rn(hi[a], r) || lo[a] > __dadd_rn(ghi[a], r)) ok = false;
       if (!ok) continue;
       unsigned long long a_id = (kind == 1) ? (unsigned long long)prim : (unsigned long long)gid;
       unsigned long long b_id = (kind == 1) ? (unsigned long long)gid : (unsigned long long)prim;
