@@ -416,9 +416,13 @@ __device__ __forceinline__ double to_body_exact(const double* R, const double* c
   return __dadd_rn(__dadd_rn(t0, t1), t2);
 }
 
-constexpr int kBpStage = 3072;  // candidates staged per block before one global reservation
-__shared__ unsigned long long g_bp_sbuf[kBpStage];
-__shared__ int g_bp_scnt;
+// candidates are staged per WARP in shared memory (its own region and counter) and
+// flushed with one global reservation per warp: no block barrier, so a warp whose queries
+// run near the indenter never holds up the others
+constexpr int kBpWarps = 4;             // 128-thread blocks
+constexpr int kBpStageW = 768;          // staged candidates per warp
+__shared__ unsigned long long g_bp_sbuf[kBpWarps * kBpStageW];
+__shared__ int g_bp_wcnt[kBpWarps];
 
 template <int NIND>
 __device__ void bp_query(const Dev& d, int kind, int gid, const double* glo, const double* ghi, double r, int root,
@@ -456,9 +460,10 @@ __device__ void bp_query(const Dev& d, int kind, int gid, const double* glo, con
       unsigned long long a_id = (kind == 1) ? (unsigned long long)prim : (unsigned long long)gid;
       unsigned long long b_id = (kind == 1) ? (unsigned long long)gid : (unsigned long long)prim;
       const unsigned long long rec = ((unsigned long long)kind << 62) | (a_id << 31) | b_id;
-      int ss = atomicAdd(&g_bp_scnt, 1);  // block-local staging (native shared int atomic)
-      if (ss < kBpStage) {
-        g_bp_sbuf[ss] = rec;
+      const int w = threadIdx.x >> 5;
+      int ss = atomicAdd(&g_bp_wcnt[w], 1);  // warp-local staging (native shared int atomic)
+      if (ss < kBpStageW) {
+        g_bp_sbuf[w * kBpStageW + ss] = rec;
       } else {  // staging full: reserve directly
         int slot = atomicAdd(cnt, 1);
         if (slot < cap) {
@@ -472,11 +477,38 @@ __device__ void bp_query(const Dev& d, int kind, int gid, const double* glo, con
   }
 }
 
-// candidates of gel-surface primitives [i0, i1) (strided) of env e
+// flush this warp's staged candidates (all 32 lanes call it, convergent)
+__device__ void bp_flush_warp(const Dev& d, unsigned long long* out, uint2* cc, int* cnt, int cap, bool* over) {
+  __syncwarp();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = min(g_bp_wcnt[w], kBpStageW);
+  int base = 0;
+  if (lane == 0 && n) base = atomicAdd(cnt, n);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  const unsigned long long* sb = g_bp_sbuf + w * kBpStageW;
+  for (int j = lane; j < n; j += 32) {
+    if (base + j < cap) {
+      out[base + j] = sb[j];
+      if (cc) cc[base + j] = pack_corners(d, sb[j]);
+    } else {
+      *over = true;
+    }
+  }
+  __syncwarp();
+  if (lane == 0) g_bp_wcnt[w] = 0;
+  __syncwarp();
+}
+
+// candidates of gel-surface primitives [i0, i1) (strided) of env e.  Called by whole
+// warps (lane i0 = warp base + lane, uniform stride); between rounds the warp flushes its
+// staging region once it is half full
 __device__ void bp_range(const Dev& d, int e, int i0, int i1, int stride, double r, unsigned long long* out, uint2* cc,
                          int* cnt, int cap, const double* R, const double* c) {
   bool over = false;
-  for (int i = i0; i < i1; i += stride) {
+  const int lane = threadIdx.x & 31;
+  for (int b = i0 - lane; b < i1; b += stride) {
+    const int i = b + lane;
+    if (i < i1) {
     int vv[3], nvx, kind, gid, root;
     if (i < d.nsv) {
       vv[0] = d.sv[i]; nvx = 1; kind = 0; gid = i; root = d.root_tri;
@@ -501,30 +533,15 @@ __device__ void bp_range(const Dev& d, int e, int i0, int i1, int stride, double
     if (kind == 0) bp_query<3>(d, 0, gid, lo, hi, r, root, out, cc, cnt, cap, &over);
     else if (kind == 2) bp_query<2>(d, 2, gid, lo, hi, r, root, out, cc, cnt, cap, &over);
     else bp_query<1>(d, 1, gid, lo, hi, r, root, out, cc, cnt, cap, &over);
+    }
+    __syncwarp();
+    if (g_bp_wcnt[threadIdx.x >> 5] > kBpStageW / 2) bp_flush_warp(d, out, cc, cnt, cap, &over);
   }
   if (over) d.es[e].ncand_over = 1;
 }
 
-__device__ void bp_flush(const Dev& d, unsigned long long* out, uint2* cc, int* cnt, int cap, bool* over) {
-  __syncthreads();
-  __shared__ int base;
-  const int n = min(g_bp_scnt, kBpStage);
-  if (threadIdx.x == 0) base = n ? atomicAdd(cnt, n) : 0;
-  __syncthreads();
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {
-    if (base + j < cap) {
-      out[base + j] = g_bp_sbuf[j];
-      if (cc) cc[base + j] = pack_corners(d, g_bp_sbuf[j]);
-    } else {
-      *over = true;
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) g_bp_scnt = 0;
-  __syncthreads();
-}
 
-// all active envs (step start): blockIdx.y = env, blocks stride over its primitives
+
 __global__ void __launch_bounds__(128) k_broadphase(Dev d, double r, unsigned long long* out_override,
                                                     int* cnt_override, int cap_override) {
   int e = blockIdx.y;
@@ -534,42 +551,42 @@ __global__ void __launch_bounds__(128) k_broadphase(Dev d, double r, unsigned lo
   __shared__ double R[9], c[3];
   if (threadIdx.x < 9) R[threadIdx.x] = s.R[threadIdx.x];
   if (threadIdx.x < 3) c[threadIdx.x] = s.c[threadIdx.x];
-  __syncthreads();
+  if (threadIdx.x < kBpWarps) g_bp_wcnt[threadIdx.x] = 0;
+  __syncthreads();  // the only block barrier: R, c and the counters before any query
   unsigned long long* out = out_override ? out_override : d.cand + (size_t)e * d.kmax;
   int* cnt = cnt_override ? cnt_override : d.ncand + e;
   int cap = out_override ? cap_override : d.kmax;
   uint2* cc = out_override ? nullptr : d.ccorn + (size_t)e * d.kmax;
   int ntot = d.nsv + d.nse + d.nst;
-  if (threadIdx.x == 0) g_bp_scnt = 0;
-  __syncthreads();
   if (!out_override && blockIdx.x == 0 && threadIdx.x == 0) d.es[e].cache_ok = 0;  // new candidate list
   bp_range(d, e, blockIdx.x * blockDim.x + threadIdx.x, ntot, gridDim.x * blockDim.x, r, out, cc, cnt, cap, R, c);
   bool over = false;
-  bp_flush(d, out, cc, cnt, cap, &over);
+  bp_flush_warp(d, out, cc, cnt, cap, &over);
   if (over) d.es[e].ncand_over = 1;
 }
 
 // rebuilds inside the loop: only the envs k_alpha listed; work items = (listed env,
-// 128-primitive chunk) spread over a fixed grid, so cost follows the actual rebuild count
+// 32-primitive chunk) per WARP over a fixed grid, so cost follows the actual rebuild count
+// and no warp waits for another
 __global__ void __launch_bounds__(128) k_broadphase_list(Dev d, double r) {
   const int nreb = *d.nreb;
   const int ntot = d.nsv + d.nse + d.nst;
-  const int nchunk = (ntot + blockDim.x - 1) / blockDim.x;
-  __shared__ double R[9], c[3];
-  for (int item = blockIdx.x; item < nreb * nchunk; item += gridDim.x) {
+  const int nchunk = (ntot + 31) / 32;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ double Rw[kBpWarps][12];  // per-warp R, c of its current env
+  if (lane == 0) g_bp_wcnt[w] = 0;
+  __syncwarp();
+  const int nw = gridDim.x * kBpWarps;
+  for (int item = blockIdx.x * kBpWarps + w; item < nreb * nchunk; item += nw) {
     const int e = d.reb_list[item / nchunk], ch = item % nchunk;
     const EnvS& s = d.es[e];
-    __syncthreads();
-    if (threadIdx.x < 9) R[threadIdx.x] = s.R[threadIdx.x];
-    if (threadIdx.x < 3) c[threadIdx.x] = s.c[threadIdx.x];
-    __syncthreads();
-    if (threadIdx.x == 0) g_bp_scnt = 0;
-    __syncthreads();
-    const int i = ch * blockDim.x + threadIdx.x;
-    bp_range(d, e, i, min(ntot, i + 1), 1, r, d.cand + (size_t)e * d.kmax, d.ccorn + (size_t)e * d.kmax, d.ncand + e,
-             d.kmax, R, c);
+    if (lane < 9) Rw[w][lane] = s.R[lane];
+    else if (lane < 12) Rw[w][lane] = s.c[lane - 9];
+    __syncwarp();
+    bp_range(d, e, ch * 32 + lane, ntot, ntot, r, d.cand + (size_t)e * d.kmax, d.ccorn + (size_t)e * d.kmax,
+             d.ncand + e, d.kmax, Rw[w], Rw[w] + 9);  // one round: prims [32 ch, 32 ch + 32)
     bool over = false;
-    bp_flush(d, d.cand + (size_t)e * d.kmax, d.ccorn + (size_t)e * d.kmax, d.ncand + e, d.kmax, &over);
+    bp_flush_warp(d, d.cand + (size_t)e * d.kmax, d.ccorn + (size_t)e * d.kmax, d.ncand + e, d.kmax, &over);
     if (over) d.es[e].ncand_over = 1;
   }
 }
@@ -2300,7 +2317,7 @@ void launch_vert_setup(const Dev& d, double h, cudaStream_t s) {
 }
 void launch_broadphase(const Dev& d, bool masked, cudaStream_t s) {
   if (masked) {  // envs listed by k_alpha
-    LAUNCHK(KID_BROADPHASE_LIST, s, (k_broadphase_list<<<4 * 148, 128, 0, s>>>(d, d.dhat + d.bp_margin)));
+    LAUNCHK(KID_BROADPHASE_LIST, s, (k_broadphase_list<<<16 * 148, 128, 0, s>>>(d, d.dhat + d.bp_margin)));
     return;
   }
   int ntot = d.nsv + d.nse + d.nst;
