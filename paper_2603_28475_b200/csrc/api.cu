@@ -705,7 +705,38 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     UP(Yf, d.Y);
     UP(ie2, d.ie);
     UP(it4, d.it);
-    UP(nodes, d.bvh);
+    {
+      // wide (child-box) form of the three BVHs: one 64-byte node per internal node holding
+      // both children's boxes and refs (>= 0 internal, < 0 leaf: -1 - (first prim << 3 | count)),
+      // plus one virtual root per tree whose child 0 is the tree root and child 1 never hits
+      std::vector<int> widx(nodes.size(), -1);
+      int nw = 3;
+      for (size_t k = 0; k < nodes.size(); ++k)
+        if (nodes[k].left >= 0) widx[k] = nw++;
+      auto ref = [&](int k) {
+        const BNode& n = nodes[k];
+        return n.left >= 0 ? widx[k] : -1 - (((-n.left - 1) << 3) | n.right);
+      };
+      std::vector<float4> wide(4 * (size_t)nw);
+      auto put = [&](int w, const BNode& a, int ra, const BNode* b, int rb) {
+        const float inf = INFINITY;
+        float lo1[3] = {inf, inf, inf}, hi1[3] = {-inf, -inf, -inf};
+        if (b) for (int t = 0; t < 3; ++t) { lo1[t] = b->lo[t]; hi1[t] = b->hi[t]; }
+        float r0, r1;
+        memcpy(&r0, &ra, 4);
+        memcpy(&r1, &rb, 4);
+        wide[4 * w] = make_float4(a.lo[0], a.lo[1], a.lo[2], a.hi[0]);
+        wide[4 * w + 1] = make_float4(a.hi[1], a.hi[2], lo1[0], lo1[1]);
+        wide[4 * w + 2] = make_float4(lo1[2], hi1[0], hi1[1], hi1[2]);
+        wide[4 * w + 3] = make_float4(r0, r1, 0.f, 0.f);
+      };
+      const int roots[3] = {d.root_tri, d.root_edge, d.root_vert};
+      for (int t = 0; t < 3; ++t) put(t, nodes[roots[t]], ref(roots[t]), nullptr, -1);  // child 1 empty leaf
+      for (size_t k = 0; k < nodes.size(); ++k)
+        if (nodes[k].left >= 0)
+          put(widx[k], nodes[nodes[k].left], ref(nodes[k].left), &nodes[nodes[k].right], ref(nodes[k].right));
+      UP(wide, d.bvhw);
+    }
     UP(prims, d.bvh_prims);
     {
       // per-prim body-frame boxes in leaf order (lo.xyz | prim id bits, hi.xyz): the exact

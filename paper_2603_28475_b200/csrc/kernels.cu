@@ -433,44 +433,47 @@ __device__ void bp_query(const Dev& d, int kind, int gid, const double* glo, con
     qlo[a] = (float)(glo[a] - r) - eps;
     qhi[a] = (float)(ghi[a] + r) + eps;
   }
+  // wide BVH (child boxes in the parent): a popped node is loaded once (64 bytes) and both
+  // children are tested from it, so rejected children and leaves cost no node load
   int stack[48];
   int sp = 0;
-  stack[sp++] = root;
+  stack[sp++] = root;  // virtual root of the tree
   while (sp > 0) {
-    BNode nd = d.bvh[stack[--sp]];
-    if (nd.lo[0] > qhi[0] || nd.hi[0] < qlo[0] || nd.lo[1] > qhi[1] || nd.hi[1] < qlo[1] || nd.lo[2] > qhi[2] ||
-        nd.hi[2] < qlo[2])
-      continue;
-    if (nd.left >= 0) {
-      stack[sp++] = nd.left;
-      stack[sp++] = nd.right;
-      continue;
-    }
-    const int p0 = -nd.left - 1, np = nd.right;
-    for (int k = 0; k < np; ++k) {
-      const float4 blo = __ldg(d.bvh_pbox + 2 * (p0 + k)), bhi = __ldg(d.bvh_pbox + 2 * (p0 + k) + 1);
-      const int prim = __float_as_int(blo.w);
-      // exact prim box (min / max of its float Y corners), tested in double as before
-      const double lo[3] = {blo.x, blo.y, blo.z}, hi[3] = {bhi.x, bhi.y, bhi.z};
-      bool ok = true;
+    const float4* wn = d.bvhw + 4 * stack[--sp];
+    const float4 w0 = __ldg(wn), w1 = __ldg(wn + 1), w2 = __ldg(wn + 2), w3 = __ldg(wn + 3);
 #pragma unroll
-      for (int a = 0; a < 3; ++a)
-        if (glo[a] > __dadd_rn(hi[a], r) || lo[a] > __dadd_rn(ghi[a], r)) ok = false;
-      if (!ok) continue;
-      unsigned long long a_id = (kind == 1) ? (unsigned long long)prim : (unsigned long long)gid;
-      unsigned long long b_id = (kind == 1) ? (unsigned long long)gid : (unsigned long long)prim;
-      const unsigned long long rec = ((unsigned long long)kind << 62) | (a_id << 31) | b_id;
-      const int w = threadIdx.x >> 5;
-      int ss = atomicAdd(&g_bp_wcnt[w], 1);  // warp-local staging (native shared int atomic)
-      if (ss < kBpStageW) {
-        g_bp_sbuf[w * kBpStageW + ss] = rec;
-      } else {  // staging full: reserve directly
-        int slot = atomicAdd(cnt, 1);
-        if (slot < cap) {
-          out[slot] = rec;
-          if (cc) cc[slot] = pack_corners(d, rec);
-        } else {
-          *over = true;
+    for (int chd = 0; chd < 2; ++chd) {
+      const float lx = chd ? w1.z : w0.x, ly = chd ? w1.w : w0.y, lz = chd ? w2.x : w0.z;
+      const float hx = chd ? w2.y : w0.w, hy = chd ? w2.z : w1.x, hz = chd ? w2.w : w1.y;
+      if (lx > qhi[0] || hx < qlo[0] || ly > qhi[1] || hy < qlo[1] || lz > qhi[2] || hz < qlo[2]) continue;
+      const int rf = __float_as_int(chd ? w3.y : w3.x);
+      if (rf >= 0) { stack[sp++] = rf; continue; }
+      const int code = -1 - rf, p0 = code >> 3, np = code & 7;
+      for (int k = 0; k < np; ++k) {
+        const float4 blo = __ldg(d.bvh_pbox + 2 * (p0 + k)), bhi = __ldg(d.bvh_pbox + 2 * (p0 + k) + 1);
+        const int prim = __float_as_int(blo.w);
+        // exact prim box (min / max of its float Y corners), tested in double as before
+        const double lo[3] = {blo.x, blo.y, blo.z}, hi[3] = {bhi.x, bhi.y, bhi.z};
+        bool ok = true;
+  #pragma unroll
+        for (int a = 0; a < 3; ++a)
+          if (glo[a] > __dadd_rn(hi[a], r) || lo[a] > __dadd_rn(ghi[a], r)) ok = false;
+        if (!ok) continue;
+        unsigned long long a_id = (kind == 1) ? (unsigned long long)prim : (unsigned long long)gid;
+        unsigned long long b_id = (kind == 1) ? (unsigned long long)gid : (unsigned long long)prim;
+        const unsigned long long rec = ((unsigned long long)kind << 62) | (a_id << 31) | b_id;
+        const int w = threadIdx.x >> 5;
+        int ss = atomicAdd(&g_bp_wcnt[w], 1);  // warp-local staging (native shared int atomic)
+        if (ss < kBpStageW) {
+          g_bp_sbuf[w * kBpStageW + ss] = rec;
+        } else {  // staging full: reserve directly
+          int slot = atomicAdd(cnt, 1);
+          if (slot < cap) {
+            out[slot] = rec;
+            if (cc) cc[slot] = pack_corners(d, rec);
+          } else {
+            *over = true;
+          }
         }
       }
     }
@@ -511,15 +514,15 @@ __device__ void bp_range(const Dev& d, int e, int i0, int i1, int stride, double
     if (i < i1) {
     int vv[3], nvx, kind, gid, root;
     if (i < d.nsv) {
-      vv[0] = d.sv[i]; nvx = 1; kind = 0; gid = i; root = d.root_tri;
+      vv[0] = d.sv[i]; nvx = 1; kind = 0; gid = i; root = 0;  // virtual wide roots: 0 tri, 1 edge, 2 vert
     } else if (i < d.nsv + d.nse) {
       gid = i - d.nsv;
       int2 ed = d.se[gid];
-      vv[0] = ed.x; vv[1] = ed.y; nvx = 2; kind = 2; root = d.root_edge;
+      vv[0] = ed.x; vv[1] = ed.y; nvx = 2; kind = 2; root = 1;
     } else {
       gid = i - d.nsv - d.nse;
       int4 t = d.st[gid];
-      vv[0] = t.x; vv[1] = t.y; vv[2] = t.z; nvx = 3; kind = 1; root = d.root_vert;
+      vv[0] = t.x; vv[1] = t.y; vv[2] = t.z; nvx = 3; kind = 1; root = 2;
     }
     double lo[3], hi[3];
     for (int j = 0; j < nvx; ++j) {
