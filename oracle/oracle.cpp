@@ -847,11 +847,12 @@ Vecs to_vecs(const Grad& G) { return Vecs{G.g, G.gc, G.gth}; }
 // the last term bounds the rotation's curvature for alpha <= alpha_upper
 // (|exp(t[w])r - r - t w x r| <= (t|w|)^2 |r|/2 and alpha |w| rho_max <= dhat/2).
 // alpha <= (1-s) d / l_n keeps d(alpha) >= s d.
-// Cheap certificate for far pairs: if the world boxes of the two primitives are
+// Cheap certificates for far pairs: if the world boxes of the two primitives are
 // separated along an axis by g >= dhat, that axis is a separating plane with
-// separation g (every point of A is beyond every point of B along it), so the same
-// bound applies with (g, +-e_axis) in place of (d, n), and the pair carries no
-// barrier term (d >= g >= dhat).  Returns false if no axis separates the boxes by dhat.
+// separation g (every point of A is beyond every point of B along it); failing that,
+// the supporting plane of the pair's primitives (below) is tried.  Either way the same
+// bound applies with (g, n) in place of (d, n), and the pair carries no barrier term
+// (d >= g >= dhat).  Returns false if neither separates the pair by dhat.
 bool axis_separation(const V3* z, int na, double dhat, double* g, V3* n) {
   double best = -INF;
   V3 bn{0, 0, 0};
@@ -864,13 +865,27 @@ bool axis_separation(const V3* z, int na, double dhat, double* g, V3* n) {
     if (loA - hiB > best) { best = loA - hiB; bn = V3{0, 0, 0}; bn[a] = 1; }   // A above B along +a
     if (loB - hiA > best) { best = loB - hiA; bn = V3{0, 0, 0}; bn[a] = -1; }  // A below B
   }
+  if (best < dhat) {
+    // primitive-plane certificate: for point-triangle the triangle's supporting plane,
+    // for edge-edge the plane spanned by both edge directions (skipped when they are
+    // within 1e-3 rad of parallel).  One side lies in the plane and the other is at
+    // |m.(z_A - z_B)| / |m| from it, so that plane separates them by that much.
+    V3 e1 = sub(z[1], z[0]), e2 = sub(z[3], z[2]), o = sub(z[0], z[2]);
+    if (na == 1) { e1 = sub(z[2], z[1]); e2 = sub(z[3], z[1]); o = sub(z[0], z[1]); }
+    V3 m = cross(e1, e2);
+    double l = norm(m);
+    if (l >= 1e-3 * norm(e1) * norm(e2) && l > 0) {
+      double sp = std::fabs(dot(m, o)) / l;
+      if (sp > best) { best = sp; bn = scl((dot(m, o) >= 0 ? 1.0 : -1.0) / l, m); }
+    }
+  }
   *g = best;
   *n = bn;
   return best >= dhat;
 }
 double rel_motion(const Problem& P, const Vecs& p);
-// Pairs without an axis certificate ("near") use their exact closest-point plane.
-// All axis-certified ("far") pairs share one bound: each has d(alpha) >= g_i - alpha L_rel
+// Pairs without a certificate ("near") use their exact closest-point plane.
+// All certified ("far") pairs share one bound: each has d(alpha) >= g_i - alpha L_rel
 // >= dhat - alpha L_rel (L_rel bounds the relative motion of any gel surface point vs any
 // indenter point, see rel_motion), so alpha <= (1-s) dhat / L_rel keeps them >= s dhat
 // (R15: the bound depends only on whether a far pair exists, not on its gap).

@@ -357,6 +357,24 @@ __device__ __forceinline__ bool axis_sep(const d3* z, int na, double dhat, doubl
   *n = bn;
   return best >= dhat;
 }
+// primitive-plane gap (R15, same formula as the oracle's certificate): the supporting
+// plane of the triangle (point-triangle) or of both edge directions (edge-edge, unless
+// within 1e-3 rad of parallel) holds one side; the other lies |m.(z_A - z_B)|/|m| from it
+__device__ __forceinline__ double plane_gap(const d3* z, int na) {
+  d3 e1 = z[1] - z[0], e2 = z[3] - z[2], o = z[0] - z[2];
+  if (na == 1) { e1 = z[2] - z[1]; e2 = z[3] - z[1]; o = z[0] - z[1]; }
+  d3 m = cross(e1, e2);
+  double l = nrm(m);
+  if (!(l >= 1e-3 * nrm(e1) * nrm(e2) && l > 0)) return -INFINITY;
+  return fabs(dot(m, o)) / l;
+}
+// full far-pair certificate: axis gap, else primitive-plane gap; g = best separation
+__device__ __forceinline__ bool far_cert(const d3* z, int na, double dhat, double* g) {
+  d3 n;
+  if (axis_sep(z, na, dhat, g, &n)) return true;
+  *g = fmax(*g, plane_gap(z, na));
+  return *g >= dhat;
+}
 
 // ------------------------------------------------------------------ a1: step setup
 __global__ void k_step_setup(Dev d, const float* poses) {
@@ -1460,9 +1478,19 @@ __global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
             }
             best = fmaxf(best, fmaxf(loA - hiB, loB - hiA));
           }
-          if (best >= dh) {
+          double gcert = (double)best;
+          if (!(best >= dh)) {
+            // no axis certificate: the primitive-plane gap in fp64 on the same fp32 corners
+            // (moving each corner by <= eps changes the separation along any fixed normal by
+            // <= 2 eps, so the margin keeps it conservative for the exact positions)
+            d3 zd[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) zd[k] = mk(zx[k], zy[k], zz[k]);
+            gcert = fmax(gcert, plane_gap(zd, na));
+          }
+          if (gcert >= (double)dh) {
             any_far = true;
-            hc[i] = __double2float_rd(((double)best - (double)kClassMargin) + odo);
+            hc[i] = __double2float_rd((gcert - (double)kClassMargin) + odo);
           } else {
             near = true;
             if (!cached) hc[i] = -INFINITY;  // slot of a fresh list: never valid until re-certified
@@ -1950,8 +1978,7 @@ __global__ void __launch_bounds__(128) k_ccd_list(Dev d) {
         }
       }
       double gsep;
-      d3 nsep;
-      if (axis_sep(z, C.na, d.dhat, &gsep, &nsep)) {
+      if (far_cert(z, C.na, d.dhat, &gsep)) {
         gmin = gsep;
       } else {
         DR D = pair_dist(kind, z);
@@ -2032,8 +2059,7 @@ __global__ void __launch_bounds__(128) k_contact_curv(Dev d, double kappa, doubl
         }
       }
       double gsep;
-      d3 nsep;
-      if (axis_sep(z, C.na, d.dhat, &gsep, &nsep)) {
+      if (far_cert(z, C.na, d.dhat, &gsep)) {
         gmin = fmin(gmin, gsep);
         continue;
       } else {

@@ -129,26 +129,39 @@ def test_distance_random_vs_bruteforce():
 
 
 def test_certificate_closed_forms():
-    """R15 far-pair certificate: the largest axis gap between the two corner boxes,
-    with its axis as the separating-plane normal (n oriented from side B to side A)."""
+    """R15 far-pair certificates: the largest axis gap between the corner boxes (normal =
+    that axis, oriented from side B to side A); failing that, the primitive-plane gap,
+    which equals the exact distance when the closest points are interior."""
     t0, t1, t2 = np.array([0, 0, 0.0]), np.array([1e-3, 0, 0]), np.array([0, 1e-3, 0])
     ok, g, n = O.certificate(np.stack([[2e-4, 3e-4, 2 * DHAT], t0, t1, t2]), 1, DHAT)
     assert ok and g == pytest.approx(2 * DHAT, rel=1e-12) and np.array_equal(n, [0, 0, 1])
     ok, g, n = O.certificate(np.stack([[2e-4, 3e-4, -0.5 * DHAT], t0, t1, t2]), 1, DHAT)
-    assert not ok and g == pytest.approx(0.5 * DHAT, rel=1e-12) and np.array_equal(n, [0, 0, -1])
-    # a point over a tilted triangle: boxes overlap on every axis -> never certified,
-    # however far the point is along the normal (the plane bound takes over, near pair)
+    assert not ok and g == pytest.approx(0.5 * DHAT, rel=1e-12)
+    # triangle tilted about x, point 2 dhat above its interior along the normal: the boxes
+    # overlap on every axis, the triangle's plane certifies the exact distance
     c, s = math.cos(0.6), math.sin(0.6)
     t0, t1, t2 = np.array([-1e-3, -1e-3 * c, -1e-3 * s]), np.array([1e-3, -1e-3 * c, -1e-3 * s]), \
         np.array([0, 1e-3 * c, 1e-3 * s])
     nrm = np.cross(t1 - t0, t2 - t0)
     nrm /= np.linalg.norm(nrm)
-    ok, g, _ = O.certificate(np.stack([5 * DHAT * nrm, t0, t1, t2]), 1, DHAT)
-    assert not ok and g < 0
-    # edges separated along y by 1.5 dhat with x-overlapping boxes
-    z = np.array([[0, 0, 0], [1e-3, 0, 1e-4], [5e-4, 1.5 * DHAT, -1e-3], [6e-4, 1.5 * DHAT + 1e-4, 1e-3]])
-    ok, g, n = O.certificate(z, 2, DHAT)
-    assert ok and g == pytest.approx(1.5 * DHAT, rel=1e-12) and np.array_equal(n, [0, -1, 0])
+    p = 2 * DHAT * nrm
+    z = np.stack([p, t0, t1, t2])
+    assert np.all((p > z[1:].min(0)) & (p < z[1:].max(0)))
+    ok, g, n = O.certificate(z, 1, DHAT)
+    assert ok and g == pytest.approx(2 * DHAT, rel=1e-9) and n @ nrm == pytest.approx(1, abs=1e-12)
+    assert g <= O.dist_pt(p, t0, t1, t2)[0] * (1 + 1e-12)
+    ok, g, _ = O.certificate(np.stack([0.5 * DHAT * nrm, t0, t1, t2]), 1, DHAT)
+    assert not ok and g == pytest.approx(0.5 * DHAT, rel=1e-9)
+    # crossing skew segments 1.5 dhat apart along a tilted common normal
+    e = np.array([0, c, s])
+    m = np.cross([1, 0, 0], e)
+    z = np.stack([[-1e-3, 0, 0], [1e-3, 0, 0], -1e-3 * e + 1.5 * DHAT * m, 1e-3 * e + 1.5 * DHAT * m])
+    ok, g, _ = O.certificate(z, 2, DHAT)
+    assert ok and g == pytest.approx(1.5 * DHAT, rel=1e-9)
+    # parallel segments: no plane certificate from the degenerate cross product
+    z = np.stack([[0, 0, 0], [1e-3, 0, 0], [2e-4, 0, 0.5 * DHAT], [1.2e-3, 1e-9, 0.5 * DHAT]])
+    ok, g, _ = O.certificate(z, 2, DHAT)
+    assert not ok and g < DHAT
 
 
 def test_certificate_never_exceeds_distance():
