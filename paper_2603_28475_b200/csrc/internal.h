@@ -27,14 +27,15 @@ struct BNode {  // indenter BVH node, body frame; leaf if left < 0: prims [-left
 // friction anchor: frozen at the step start
 // Delta_k(x) = sum_gel w u(x) + R Y_w + sig c - C0 with the indenter side folded into
 // Y_w = sum_ind w Y (body frame), sig = sum_ind w, C0 = sum_gel w u^t + R^t Y_w + sig c^t
-struct Anchor {
-  int kind, a, b;
-  float sig;
-  float w[4];
+struct Anchor {  // friction anchor (R7): free gel corners carried by id, indenter side folded
+  int gid[3];       // free gel corners: global vertex id, -1 if absent (fixed corners have u = 0)
+  unsigned sid01;   // surface-local ids of gel corners 0 and 1 (16 bit each)
+  float w[3], sig;  // weights of the gel corners; sig = sum of the indenter weights
   float t1[3], lam;
-  float t2[3], pad;
-  float yw[3], pad2;
-  double c0[3], pad3;
+  float t2[3];
+  unsigned sid2;    // surface-local id of gel corner 2
+  float yw[3], pad2;  // Y_w = sum_ind w Y (body frame)
+  double c0[3], pad3;  // C0 = sum_gel w u^t + R^t Y_w + sig c^t (Delta(x^t) = 0)
 };
 
 // per-env solver state (fp64 control, one thread per env in the scalar kernels)

@@ -186,35 +186,40 @@ __device__ __forceinline__ double moll_f1(double s, double eps) { return s >= ep
 struct DR {
   double d, w[4];
 };
-__device__ __forceinline__ double seg_t(d3 p, d3 a, d3 b) {
-  d3 e = b - a;
-  return fmin(1.0, fmax(0.0, dot(p - a, e) / dot(e, e)));
+// closest point of segment a + u e (u in [0, 1], inv_ee = 1 / e.e) to p: u and |r|^2
+__device__ __forceinline__ double seg_u(d3 p, d3 a, d3 e, double inv_ee) {
+  return fmin(1.0, fmax(0.0, dot(p - a, e) * inv_ee));
 }
+// Same case logic as the oracle (interior solve, else the best boundary candidate), with
+// shared reciprocals and squared-distance comparisons: one sqrt per call
 __device__ DR dist_pt(d3 p, d3 t0, d3 t1, d3 t2) {
   DR r;
   d3 e1 = t1 - t0, e2 = t2 - t0, q = p - t0;
   double a11 = dot(e1, e1), a12 = dot(e1, e2), a22 = dot(e2, e2), r1 = dot(q, e1), r2 = dot(q, e2);
-  double det = a11 * a22 - a12 * a12;
-  double s = (a22 * r1 - a12 * r2) / det, t = (a11 * r2 - a12 * r1) / det;
+  double idet = 1.0 / (a11 * a22 - a12 * a12);
+  double s = (a22 * r1 - a12 * r2) * idet, t = (a11 * r2 - a12 * r1) * idet;
   if (s >= 0 && t >= 0 && s + t <= 1) {
     r.d = nrm(q - s * e1 - t * e2);
     r.w[0] = 1; r.w[1] = -(1 - s - t); r.w[2] = -s; r.w[3] = -t;
     return r;
   }
-  r.d = DBL_MAX;
+  double best = DBL_MAX;
   d3 T[3] = {t0, t1, t2};
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     int i = k, j = (k + 1) % 3;
-    double u = seg_t(p, T[i], T[j]);
-    double dd = nrm(p - ((1 - u) * T[i] + u * T[j]));
-    if (dd < r.d) {
-      r.d = dd;
+    d3 e = T[j] - T[i];
+    double u = seg_u(p, T[i], e, 1.0 / dot(e, e));
+    d3 v = p - (T[i] + u * e);
+    double dd = dot(v, v);
+    if (dd < best) {
+      best = dd;
       r.w[0] = 1; r.w[1] = 0; r.w[2] = 0; r.w[3] = 0;
       r.w[1 + i] = -(1 - u);
       r.w[1 + j] = -u;
     }
   }
+  r.d = sqrt(best);
   return r;
 }
 __device__ DR dist_ee(d3 a0, d3 a1, d3 b0, d3 b1) {
@@ -223,30 +228,40 @@ __device__ DR dist_ee(d3 a0, d3 a1, d3 b0, d3 b1) {
   double a = dot(d1, d1), e = dot(d2, d2), b = dot(d1, d2), c = dot(d1, q), f = dot(d2, q);
   double den = a * e - b * b;
   if (den > 1e-12 * a * e) {
-    double s = (b * f - c * e) / den, t = (a * f - b * c) / den;
+    double iden = 1.0 / den;
+    double s = (b * f - c * e) * iden, t = (a * f - b * c) * iden;
     if (s > 0 && s < 1 && t > 0 && t < 1) {
       r.d = nrm(q + s * d1 - t * d2);
       r.w[0] = 1 - s; r.w[1] = s; r.w[2] = -(1 - t); r.w[3] = -t;
       return r;
     }
   }
-  r.d = DBL_MAX;
+  const double ia = 1.0 / a, ie = 1.0 / e;
+  double best;
   {
-    double t = seg_t(a0, b0, b1), dd = nrm(a0 - ((1 - t) * b0 + t * b1));
-    if (dd < r.d) { r.d = dd; r.w[0] = 1; r.w[1] = 0; r.w[2] = -(1 - t); r.w[3] = -t; }
+    double t = seg_u(a0, b0, d2, ie);
+    d3 v = a0 - (b0 + t * d2);
+    best = dot(v, v); r.w[0] = 1; r.w[1] = 0; r.w[2] = -(1 - t); r.w[3] = -t;
   }
   {
-    double t = seg_t(a1, b0, b1), dd = nrm(a1 - ((1 - t) * b0 + t * b1));
-    if (dd < r.d) { r.d = dd; r.w[0] = 0; r.w[1] = 1; r.w[2] = -(1 - t); r.w[3] = -t; }
+    double t = seg_u(a1, b0, d2, ie);
+    d3 v = a1 - (b0 + t * d2);
+    double dd = dot(v, v);
+    if (dd < best) { best = dd; r.w[0] = 0; r.w[1] = 1; r.w[2] = -(1 - t); r.w[3] = -t; }
   }
   {
-    double s = seg_t(b0, a0, a1), dd = nrm((1 - s) * a0 + s * a1 - b0);
-    if (dd < r.d) { r.d = dd; r.w[0] = 1 - s; r.w[1] = s; r.w[2] = -1; r.w[3] = 0; }
+    double s = seg_u(b0, a0, d1, ia);
+    d3 v = (a0 + s * d1) - b0;
+    double dd = dot(v, v);
+    if (dd < best) { best = dd; r.w[0] = 1 - s; r.w[1] = s; r.w[2] = -1; r.w[3] = 0; }
   }
   {
-    double s = seg_t(b1, a0, a1), dd = nrm((1 - s) * a0 + s * a1 - b1);
-    if (dd < r.d) { r.d = dd; r.w[0] = 1 - s; r.w[1] = s; r.w[2] = 0; r.w[3] = -1; }
+    double s = seg_u(b1, a0, d1, ia);
+    d3 v = (a0 + s * d1) - b1;
+    double dd = dot(v, v);
+    if (dd < best) { best = dd; r.w[0] = 1 - s; r.w[1] = s; r.w[2] = 0; r.w[3] = -1; }
   }
+  r.d = sqrt(best);
   return r;
 }
 
@@ -638,20 +653,29 @@ __global__ void k_anchors(Dev d, double kappa) {
     int slot = atomicAdd(d.nanc + e, 1);
     if (slot >= d.amax) { d.es[e].ncand_over = 1; continue; }
     Anchor A;
-    A.kind = kind; A.a = a; A.b = b;
-    for (int k = 0; k < 4; ++k) A.w[k] = (float)D.w[k];
+    CornersL L = corners_l(d, kind, a, b);
+    int ng = 0;
+    unsigned sid[3] = {0, 0, 0};
+    for (int k = 0; k < 3; ++k) { A.gid[k] = -1; A.w[k] = 0.f; }
     A.t1[0] = t1.x; A.t1[1] = t1.y; A.t1[2] = t1.z;
     A.t2[0] = t2.x; A.t2[1] = t2.y; A.t2[2] = t2.z;
     A.lam = (float)fmax(0.0, -kappa * bar_db(D.d, d.dhat));
-    A.pad = 0; A.pad2 = 0; A.pad3 = 0;
-    // fold the rigid side: Y_w = sum_ind w Y, sig = sum_ind w; C0 = sum_gel w u^t + R^t Y_w + sig c^t
+    A.pad2 = 0; A.pad3 = 0;
+    // fold the rigid side: Y_w = sum_ind w Y, sig = sum_ind w; C0 = sum_gel w u^t + R^t Y_w + sig c^t.
+    // Fixed gel corners are dropped: u = 0 there, so they add nothing to Delta and take no force
     d3 yw = mk(0, 0, 0), c0 = mk(0, 0, 0);
     double sig = 0;
     for (int k = 0; k < 4; ++k) {
-      double wk = (double)A.w[k];
+      const float wf = (float)D.w[k];
+      const double wk = (double)wf;
       if (C.ind[k]) { yw = yw + wk * ind_body(d, C.id[k]); sig += wk; }
-      else c0 = c0 + wk * gel_vec(d, d.u, C.id[k], e);
+      else if (!(d.vflag[C.id[k]] & 1)) {
+        c0 = c0 + wk * gel_vec(d, d.u, C.id[k], e);
+        A.gid[ng] = C.id[k]; A.w[ng] = wf; sid[ng] = (unsigned)L.sid[k]; ++ng;
+      }
     }
+    A.sid01 = sid[0] | (sid[1] << 16);
+    A.sid2 = sid[2];
     A.sig = (float)sig;
     A.yw[0] = (float)yw.x; A.yw[1] = (float)yw.y; A.yw[2] = (float)yw.z;
     // C0 from the stored (rounded) Y_w and sig, so Delta(x^t) = 0 exactly
@@ -935,6 +959,9 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
   if (act) atomicAdd(d.acc + (size_t)A_EEL * d.Es + e, esum);
 }
 
+// ------------------------------------------------------------------ a7: curvature
+// p^T H_e p = h^2 V [mu |dF|^2 + lambda' (cof F : dF)^2 + 2 (lambda'(J-1) - mu) F : cof(dF)]  (App. B)
+
 // ---- Kuhn-cell element curvature: one warp = one cell x 32 envs, u and p of the 8 corners
 // in registers; p^T H_e p summed over the 6 tets (App. B quadratic form)
 __global__ void __launch_bounds__(256, 2) k_elem_curv_cells(Dev d, float h2) {
@@ -1213,16 +1240,18 @@ __global__ void __launch_bounds__(128) k_contact_friction(Dev d, double eps_f) {
   const int na = min(d.nanc[e], d.amax);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
     const Anchor& A = d.anc[(size_t)e * d.amax + i];
-    CornersL C = corners_l(d, A.kind, A.a, A.b);
+    const int gid[3] = {A.gid[0], A.gid[1], A.gid[2]};
+    const unsigned sid[3] = {A.sid01 & 0xffffu, A.sid01 >> 16, A.sid2};
+    float4 us[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)  // all corner loads in flight at once
+      if (gid[k] >= 0) us[k] = d.usurf[(size_t)sid[k] * d.Es + e];
     const d3 rho = mv(R, mk(A.yw[0], A.yw[1], A.yw[2]));  // sum_ind w (y - c) = R Y_w
     const double sig = A.sig;
     d3 Dl = rho + sig * cc - mk(A.c0[0], A.c0[1], A.c0[2]);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (C.ind[k]) continue;
-      float4 u = d.usurf[(size_t)C.sid[k] * d.Es + e];
-      Dl = Dl + (double)A.w[k] * mk(u.x, u.y, u.z);
-    }
+    for (int k = 0; k < 3; ++k)
+      if (gid[k] >= 0) Dl = Dl + (double)A.w[k] * mk(us[k].x, us[k].y, us[k].z);
     d3 t1 = mk(A.t1[0], A.t1[1], A.t1[2]), t2 = mk(A.t2[0], A.t2[1], A.t2[2]);
     double ta = dot(t1, Dl), tb = dot(t2, Dl);
     double sn = sqrt(ta * ta + tb * tb);
@@ -1232,10 +1261,9 @@ __global__ void __launch_bounds__(128) k_contact_friction(Dev d, double eps_f) {
     d.anc_f1[(size_t)e * d.amax + i] = (float)f1;
     d3 Tt = ta * t1 + tb * t2;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (C.ind[k]) continue;
-      int v = C.gid[k];
-      if (d.vflag[v] & 1) continue;
+    for (int k = 0; k < 3; ++k) {
+      const int v = gid[k];
+      if (v < 0) continue;
       double wk = A.w[k];
       d3 f = (f1 * wk) * Tt;
       atomicAdd(d.g + vidx(d, 0, v, e), (float)f.x);
@@ -1532,21 +1560,21 @@ __global__ void __launch_bounds__(256) k_contact_curv_staged(Dev d, double kappa
   __syncthreads();
   d3 pc = mk(pr[0], pr[1], pr[2]), pth = mk(pr[3], pr[4], pr[5]);
   double extra = nrm(pth) * d.dhat * 0.25;
-  auto motion = [&](const CornersL& C, int k) -> d3 {
-    if (C.ind[k]) return pc + cross(pth, mk(S.sy[3 * C.gid[k]], S.sy[3 * C.gid[k] + 1], S.sy[3 * C.gid[k] + 2]));
-    float4 p = S.sv4[C.sid[k]];
+  // motion per unit alpha of corner id (indenter vertex or surface-local gel id)
+  auto motion = [&](bool ind, unsigned id) -> d3 {
+    if (ind) return pc + cross(pth, mk(S.sy[3 * id], S.sy[3 * id + 1], S.sy[3 * id + 2]));
+    float4 p = S.sv4[id];
     return mk(p.x, p.y, p.z);
   };
   double q = 0, amin = INFINITY;
   const int n0 = d.nnear[3 * e], n1 = d.nnear[3 * e + 1], n = n0 + n1 + d.nnear[3 * e + 2];
-  const unsigned long long* cand = d.cand + (size_t)e * d.kmax;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     int kk = j < n0 ? 0 : (j < n0 + n1 ? 1 : 2);
     int jj = j - (kk == 0 ? 0 : (kk == 1 ? n0 : n0 + n1));
     int i = d.nearl[((size_t)e * 3 + kk) * d.kmax + jj];
-    unsigned long long rec = cand[i];
-    int kind = (int)(rec >> 62), a = (int)((rec >> 31) & 0x7fffffffu), b = (int)(rec & 0x7fffffffu);
-    CornersL C = corners_l(d, kind, a, b);
+    const uint2 cc = d.ccorn[(size_t)e * d.kmax + i];
+    const unsigned id[4] = {cc.x & 0xffffu, cc.x >> 16, cc.y & 0xffffu, cc.y >> 16};
+    const int na = kk == 2 ? 2 : 1;
     const float4* geo = d.cgeo + 2 * ((size_t)e * d.kmax + i);
     float4 g0 = geo[0], g1 = geo[1];
     double dist = g0.x;
@@ -1555,7 +1583,7 @@ __global__ void __launch_bounds__(256) k_contact_curv_staged(Dev d, double kappa
     double w[4] = {g1.x, g1.y, g1.z, g1.w};
     d3 dz[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) dz[k] = motion(C, k);
+    for (int k = 0; k < 4; ++k) dz[k] = motion(kk == 0 ? k >= 1 : (kk == 1 ? k == 0 : k >= 2), id[k]);
     if (dist < d.dhat) {
       d3 dr = mk(0, 0, 0);
 #pragma unroll
@@ -1567,7 +1595,7 @@ __global__ void __launch_bounds__(256) k_contact_curv_staged(Dev d, double kappa
     double la = -INFINITY, lb = -INFINITY;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      if (k < C.na) la = fmax(la, -dot(nn, dz[k]));
+      if (k < na) la = fmax(la, -dot(nn, dz[k]));
       else lb = fmax(lb, dot(nn, dz[k]));
     }
     double l = la + lb + extra;
@@ -1576,12 +1604,15 @@ __global__ void __launch_bounds__(256) k_contact_curv_staged(Dev d, double kappa
   const int na = min(d.nanc[e], d.amax);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
     const Anchor& A = d.anc[(size_t)e * d.amax + i];
-    CornersL C = corners_l(d, A.kind, A.a, A.b);
+    const unsigned sid[3] = {A.sid01 & 0xffffu, A.sid01 >> 16, A.sid2};
     // indenter side folded: sig p_c + p_theta x (R Y_w)
     d3 dD = (double)A.sig * pc + cross(pth, mv(R, mk(A.yw[0], A.yw[1], A.yw[2])));
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (!C.ind[k]) dD = dD + (double)A.w[k] * motion(C, k);
+    for (int k = 0; k < 3; ++k)
+      if (A.gid[k] >= 0) {
+        const float4 pv = S.sv4[sid[k]];
+        dD = dD + (double)A.w[k] * mk(pv.x, pv.y, pv.z);
+      }
     d3 t1 = mk(A.t1[0], A.t1[1], A.t1[2]), t2 = mk(A.t2[0], A.t2[1], A.t2[2]);
     double ta = dot(t1, dD), tb = dot(t2, dD);
     q += (double)d.anc_f1[(size_t)e * d.amax + i] * (ta * ta + tb * tb);
@@ -1880,64 +1911,6 @@ __global__ void __launch_bounds__(256) k_dir_apply(Dev d) {
   }
 }
 
-// ------------------------------------------------------------------ a7: curvature
-// p^T H_e p = h^2 V [mu |dF|^2 + lambda' (cof F : dF)^2 + 2 (lambda'(J-1) - mu) F : cof(dF)]  (App. B)
-__global__ void __launch_bounds__(256) k_elem_curv(Dev d, float h2) {
-  int e = blockIdx.x * 32 + threadIdx.x;
-  bool act = e < d.E && (d.run[e] & 2);
-  if (!__any_sync(0xffffffffu, act)) return;
-  const float mu = d.mu, l2 = d.lam2;
-  double qsum = 0;
-  for (int t = blockIdx.y * 8 + threadIdx.y; t < d.nt; t += gridDim.y * 8) {
-    int4 tv = __ldg(d.tets + t);
-    int vv[4] = {tv.x, tv.y, tv.z, tv.w};
-    TetData T = load_tet(d, t);
-    if (!act) continue;
-    float du[3][3], dp[3][3];
-    float u0[3], p0[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) { u0[c] = d.u[vidx(d, c, vv[0], e)]; p0[c] = d.p[vidx(d, c, vv[0], e)]; }
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        du[k][c] = d.u[vidx(d, c, vv[k + 1], e)] - u0[c];
-        dp[k][c] = d.p[vidx(d, c, vv[k + 1], e)] - p0[c];
-      }
-    float G[9], dF[9];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        float s = 0.f, r = 0.f;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) { s = fmaf(du[k][i], T.b[k][j], s); r = fmaf(dp[k][i], T.b[k][j], r); }
-        G[3 * i + j] = s;
-        dF[3 * i + j] = r;
-      }
-    float trG = G[0] + G[4] + G[8];
-    float i2 = (G[0] * G[4] - G[1] * G[3]) + (G[0] * G[8] - G[2] * G[6]) + (G[4] * G[8] - G[5] * G[7]);
-    float cG[9], cd[9];
-    cof33(G, cG);
-    cof33(dF, cd);
-    float detG = G[0] * cG[0] + G[1] * cG[1] + G[2] * cG[2];
-    float Jm1 = trG + i2 + detG;
-    float dd = 0.f, cfd = 0.f, fcd = 0.f;
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        float cF = (i == j ? 1.f + trG : 0.f) - G[3 * j + i] + cG[3 * i + j];
-        float Fij = (i == j ? 1.f : 0.f) + G[3 * i + j];
-        dd = fmaf(dF[3 * i + j], dF[3 * i + j], dd);
-        cfd = fmaf(cF, dF[3 * i + j], cfd);
-        fcd = fmaf(Fij, cd[3 * i + j], fcd);
-      }
-    qsum += (double)(h2 * T.vol * (mu * dd + l2 * cfd * cfd + 2.f * (l2 * Jm1 - mu) * fcd));
-  }
-  if (act) atomicAdd(d.acc + (size_t)A_PHP * d.Es + e, qsum);
-}
-
 // contact curvature (GN, R8) and the conservative step bound alpha_ccd (R15):
 // d(alpha) >= d - alpha l_n, l_n = max_A(-n.dz) + max_B(n.dz) + |p_theta| dhat/4
 // step bound over the fresh candidates of the envs that rebuilt (k_alpha list): work items
@@ -2008,128 +1981,6 @@ __global__ void __launch_bounds__(128) k_ccd_list(Dev d) {
       if (m < INFINITY) atomic_min_pos(d.accu + (size_t)U_ACCD * d.Es + e, (float)m);
       if (g < INFINITY) atomic_min_pos(d.accu + (size_t)U_GFAR * d.Es + e, (float)g);
     }
-  }
-}
-
-__global__ void __launch_bounds__(128) k_contact_curv(Dev d, double kappa, double eps_f, int ccd_only) {
-  int e = blockIdx.y;
-  if (e >= d.E) return;
-  int rb = d.run[e];
-  if (ccd_only ? !(rb & 4) : !(rb & 2)) return;
-  const EnvS& s = d.es[e];
-  __shared__ double R[9], c[3], Rt[9], ct[3], pr[6];
-  __shared__ double sm[32];
-  if (threadIdx.x < 9) { R[threadIdx.x] = s.R[threadIdx.x]; Rt[threadIdx.x] = s.Rt[threadIdx.x]; }
-  if (threadIdx.x < 3) { c[threadIdx.x] = s.c[threadIdx.x]; ct[threadIdx.x] = s.ct[threadIdx.x]; }
-  if (threadIdx.x < 6) pr[threadIdx.x] = s.pr[threadIdx.x];
-  __syncthreads();
-  d3 cc = ld3(c), pc = mk(pr[0], pr[1], pr[2]), pth = mk(pr[3], pr[4], pr[5]);
-  double extra = nrm(pth) * d.dhat * 0.25;
-  double q = 0, amin = INFINITY;
-  int n = min(d.ncand[e], d.kmax);  // launched with ccd_only = 1 only (fresh candidates after a rebuild)
-  int stride = gridDim.x * blockDim.x;
-  double gmin = INFINITY;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
-    int i = j;
-    unsigned long long rec = d.cand[(size_t)e * d.kmax + i];
-    int kind = (int)(rec >> 62), a = (int)((rec >> 31) & 0x7fffffffu), b = (int)(rec & 0x7fffffffu);
-    Corners C = corners_of(d, kind, a, b);
-    d3 dz[4], nn;
-    double dist, w[4];
-    if (!ccd_only) {  // geometry cached by k_contact_grad at this same iterate
-      const float4* geo = d.cgeo + 2 * ((size_t)e * d.kmax + i);
-      float4 g0 = geo[0];
-      dist = g0.x;
-      nn = mk(g0.y, g0.z, g0.w);
-      float4 g1 = geo[1];
-      w[0] = g1.x; w[1] = g1.y; w[2] = g1.z; w[3] = g1.w;
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        dz[k] = C.ind[k] ? pc + cross(pth, mv(R, ind_body(d, C.id[k]))) : gel_vec(d, d.p, C.id[k], e);
-    } else {  // fresh candidates after a rebuild: distances at the current iterate
-      d3 z[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (C.ind[k]) {
-          z[k] = mv(R, ind_body(d, C.id[k])) + cc;
-          dz[k] = pc + cross(pth, z[k] - cc);
-        } else {
-          z[k] = gel_pos(d, d.u, C.id[k], e);
-          dz[k] = gel_vec(d, d.p, C.id[k], e);
-        }
-      }
-      double gsep;
-      if (far_cert(z, C.na, d.dhat, &gsep)) {
-        gmin = fmin(gmin, gsep);
-        continue;
-      } else {
-        DR D = pair_dist(kind, z);
-        d3 rr = mk(0, 0, 0);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) rr = rr + D.w[k] * z[k];
-        dist = D.d;
-        nn = (1.0 / D.d) * rr;
-        for (int k = 0; k < 4; ++k) w[k] = D.w[k];
-      }
-    }
-    if (!(dist > 0)) continue;
-    if (!ccd_only && dist < d.dhat) {
-      d3 dr = mk(0, 0, 0);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) dr = dr + w[k] * dz[k];
-      double dn = dot(nn, dr);
-      q += kappa * bar_ddb(dist, d.dhat) * dn * dn;
-    }
-    double la = -INFINITY, lb = -INFINITY;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (k < C.na) la = fmax(la, -dot(nn, dz[k]));
-      else lb = fmax(lb, dot(nn, dz[k]));
-    }
-    double l = la + lb + extra;
-    if (l > 0) amin = fmin(amin, (1 - d.ccd_s) * dist / l);
-  }
-  if (!ccd_only) {
-    int na = min(d.nanc[e], d.amax);
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += stride) {
-      Anchor A = d.anc[(size_t)e * d.amax + i];
-      Corners C = corners_of(d, A.kind, A.a, A.b);
-      d3 Dl = mk(0, 0, 0), dD = mk(0, 0, 0);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        d3 dz, mvz;
-        if (C.ind[k]) {
-          d3 y = ind_body(d, C.id[k]);
-          d3 z = mv(R, y) + cc;
-          dz = z - (mv(Rt, y) + ld3(ct));
-          mvz = pc + cross(pth, z - cc);
-        } else {
-          dz = gel_vec(d, d.u, C.id[k], e) - gel_vec(d, d.ut, C.id[k], e);
-          mvz = gel_vec(d, d.p, C.id[k], e);
-        }
-        Dl = Dl + (double)A.w[k] * dz;
-        dD = dD + (double)A.w[k] * mvz;
-      }
-      d3 t1 = mk(A.t1[0], A.t1[1], A.t1[2]), t2 = mk(A.t2[0], A.t2[1], A.t2[2]);
-      double sn = sqrt(dot(t1, Dl) * dot(t1, Dl) + dot(t2, Dl) * dot(t2, Dl));
-      double ta = dot(t1, dD), tb = dot(t2, dD);
-      q += d.mu_f * (double)A.lam * moll_f1(sn, eps_f) * (ta * ta + tb * tb);
-    }
-    block_sum_atomic(q, d.acc + (size_t)A_PHP * d.Es + e, sm);
-  }
-  if (ccd_only) {
-    gmin = warp_min(gmin);
-    if ((threadIdx.x & 31) == 0 && gmin < INFINITY) atomic_min_pos(d.accu + (size_t)U_GFAR * d.Es + e, (float)gmin);
-  }
-  // block min of amin
-  amin = warp_min(amin);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = amin;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double m = INFINITY;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmin(m, sm[w]);
-    if (m < INFINITY) atomic_min_pos(d.accu + (size_t)U_ACCD * d.Es + e, (float)m);
   }
 }
 
