@@ -697,34 +697,55 @@ __global__ void k_vert_pre(Dev d, float h2) {
     d.nnear[3 * e] = 0; d.nnear[3 * e + 1] = 0; d.nnear[3 * e + 2] = 0;
   }
   double ein = 0;
-  for (int v = blockIdx.y * 8 + threadIdx.y; v < d.nv; v += gridDim.y * 8) {
-    if (!act) continue;
-    if (d.vflag[v] & 1) continue;
-    float m = d.mass[v];
-    float gg[3], uv[3];
+  // two vertices per iteration, every load issued before any store (the stores to u
+  // could otherwise alias the next loads and serialise them): twice the bytes in flight
+  const int stride = gridDim.y * 8;
+  for (int v0 = blockIdx.y * 8 + threadIdx.y; v0 < d.nv; v0 += 2 * stride) {
+    float u[2][3], pv[2][3], uh[2][3], m[2], sm[2];
+    int si[2];
+    bool ok[2];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      unsigned i = vidx(d, c, v, e);
-      float u = d.u[i];
-      if (da != 0.f) {
-        u = u + da * d.p[i];
-        d.u[i] = u;
+    for (int t = 0; t < 2; ++t) {
+      const int v = v0 + t * stride;
+      ok[t] = act && v < d.nv && !(d.vflag[v] & 1);
+      if (!ok[t]) continue;
+      m[t] = d.mass[v];
+      sm[t] = d.smu[v];
+      si[t] = d.sidx[v];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const unsigned i = vidx(d, c, v, e);
+        u[t][c] = d.u[i];
+        uh[t][c] = d.uh[i];
+        pv[t][c] = da != 0.f ? d.p[i] : 0.f;
       }
-      float du = u - d.uh[i];
-      gg[c] = m * du;
-      ein += 0.5 * (double)m * (double)du * (double)du;
-      d.g[i] = gg[c];
-      uv[c] = u;
     }
-    int si = d.sidx[v];
-    if (si >= 0) d.usurf[(size_t)si * d.Es + e] = make_float4(uv[0], uv[1], uv[2], 0.f);
-    const float dg = m + h2 * d.smu[v];  // mass + state-independent elastic diagonal (App. B)
-    d.D[vidxD(d, 0, v, e)] = dg;
-    d.D[vidxD(d, 1, v, e)] = dg;
-    d.D[vidxD(d, 2, v, e)] = dg;
-    d.D[vidxD(d, 3, v, e)] = 0.f;
-    d.D[vidxD(d, 4, v, e)] = 0.f;
-    d.D[vidxD(d, 5, v, e)] = 0.f;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      if (!ok[t]) continue;
+      const int v = v0 + t * stride;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const unsigned i = vidx(d, c, v, e);
+        float uu = u[t][c];
+        if (da != 0.f) {
+          uu = uu + da * pv[t][c];
+          d.u[i] = uu;
+        }
+        const float du = uu - uh[t][c];
+        ein += 0.5 * (double)m[t] * (double)du * (double)du;
+        d.g[i] = m[t] * du;
+        u[t][c] = uu;
+      }
+      if (si[t] >= 0) d.usurf[(size_t)si[t] * d.Es + e] = make_float4(u[t][0], u[t][1], u[t][2], 0.f);
+      const float dg = m[t] + h2 * sm[t];  // mass + state-independent elastic diagonal (App. B)
+      d.D[vidxD(d, 0, v, e)] = dg;
+      d.D[vidxD(d, 1, v, e)] = dg;
+      d.D[vidxD(d, 2, v, e)] = dg;
+      d.D[vidxD(d, 3, v, e)] = 0.f;
+      d.D[vidxD(d, 4, v, e)] = 0.f;
+      d.D[vidxD(d, 5, v, e)] = 0.f;
+    }
   }
   if (act && ein != 0.0) atomicAdd(d.acc + (size_t)A_EIN * d.Es + e, ein);
 }
@@ -1739,28 +1760,43 @@ __global__ void __launch_bounds__(256) k_dir_reduce(Dev d) {
   if (!__any_sync(0xffffffffu, act)) return;
   double gPy = 0, yp = 0, yPy = 0, pg = 0, gPg = 0, gg = 0, pp = 0;
   float pgmax = 0.f;
-  for (int v = blockIdx.y * 8 + threadIdx.y; v < d.nv; v += gridDim.y * 8) {
-    if (!act || (d.vflag[v] & 1)) continue;
-    float g[3], gq[3], p[3], D[6], y[3], Pg[3], Py[3];
+  const int stride = gridDim.y * 8;
+  for (int v0 = blockIdx.y * 8 + threadIdx.y; v0 < d.nv; v0 += 2 * stride) {  // two vertices in flight
+    float g[2][3], gq[2][3], p[2][3], D[2][6];
+    bool ok[2];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      g[c] = d.g[vidx(d, c, v, e)];
-      gq[c] = d.gp[vidx(d, c, v, e)];
-      p[c] = d.p[vidx(d, c, v, e)];
-      y[c] = g[c] - gq[c];
+    for (int t = 0; t < 2; ++t) {
+      const int v = v0 + t * stride;
+      ok[t] = act && v < d.nv && !(d.vflag[v] & 1);
+      if (!ok[t]) continue;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        g[t][c] = d.g[vidx(d, c, v, e)];
+        gq[t][c] = d.gp[vidx(d, c, v, e)];
+        p[t][c] = d.p[vidx(d, c, v, e)];
+      }
+#pragma unroll
+      for (int c = 0; c < 6; ++c) D[t][c] = d.D[vidxD(d, c, v, e)];
     }
 #pragma unroll
-    for (int c = 0; c < 6; ++c) D[c] = d.D[vidxD(d, c, v, e)];
-    precond(D, d.precond, g, Pg);
-    precond(D, d.precond, y, Py);
-    gPy += g[0] * Py[0] + g[1] * Py[1] + g[2] * Py[2];
-    yp += y[0] * p[0] + y[1] * p[1] + y[2] * p[2];
-    yPy += y[0] * Py[0] + y[1] * Py[1] + y[2] * Py[2];
-    pg += p[0] * g[0] + p[1] * g[1] + p[2] * g[2];
-    gPg += g[0] * Pg[0] + g[1] * Pg[1] + g[2] * Pg[2];
-    gg += g[0] * g[0] + g[1] * g[1] + g[2] * g[2];
-    pp += p[0] * p[0] + p[1] * p[1] + p[2] * p[2];
-    pgmax = fmaxf(pgmax, sqrtf(Pg[0] * Pg[0] + Pg[1] * Pg[1] + Pg[2] * Pg[2]));
+    for (int t = 0; t < 2; ++t) {
+      if (!ok[t]) continue;
+      float y[3], Pg[3], Py[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) y[c] = g[t][c] - gq[t][c];
+      precond(D[t], d.precond, g[t], Pg);
+      precond(D[t], d.precond, y, Py);
+      const float* gv = g[t];
+      const float* pv = p[t];
+      gPy += gv[0] * Py[0] + gv[1] * Py[1] + gv[2] * Py[2];
+      yp += y[0] * pv[0] + y[1] * pv[1] + y[2] * pv[2];
+      yPy += y[0] * Py[0] + y[1] * Py[1] + y[2] * Py[2];
+      pg += pv[0] * gv[0] + pv[1] * gv[1] + pv[2] * gv[2];
+      gPg += gv[0] * Pg[0] + gv[1] * Pg[1] + gv[2] * Pg[2];
+      gg += gv[0] * gv[0] + gv[1] * gv[1] + gv[2] * gv[2];
+      pp += pv[0] * pv[0] + pv[1] * pv[1] + pv[2] * pv[2];
+      pgmax = fmaxf(pgmax, sqrtf(Pg[0] * Pg[0] + Pg[1] * Pg[1] + Pg[2] * Pg[2]));
+    }
   }
   // reduce over threadIdx.y in shared memory, one atomic per (block, env)
   __shared__ double sm[8][8][32];
@@ -1870,30 +1906,51 @@ __global__ void __launch_bounds__(256) k_dir_apply(Dev d) {
   float4 pc = act ? d.pcf[e] : make_float4(0, 0, 0, 0);
   float M = 0.f, L = 0.f;
   double q = 0;
-  for (int v = blockIdx.y * 8 + threadIdx.y; v < d.nv; v += gridDim.y * 8) {
-    unsigned char fl = d.vflag[v];
-    if (!act || (fl & 1)) continue;
-    float g[3], D[6], Pg[3], p[3];
+  const int stride = gridDim.y * 8;
+  for (int v0 = blockIdx.y * 8 + threadIdx.y; v0 < d.nv; v0 += 2 * stride) {  // loads of two vertices first
+    float g[2][3], D[2][6], po[2][3], m[2];
+    int si[2];
+    bool ok[2];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) g[c] = d.g[vidx(d, c, v, e)];
+    for (int t = 0; t < 2; ++t) {
+      const int v = v0 + t * stride;
+      ok[t] = false;
+      if (!act || v >= d.nv) continue;
+      const unsigned char fl = d.vflag[v];
+      ok[t] = !(fl & 1);
+      if (!ok[t]) continue;
+      m[t] = d.mass[v];
+      si[t] = (fl & 2) ? d.sidx[v] : -1;
 #pragma unroll
-    for (int c = 0; c < 6; ++c) D[c] = d.D[vidxD(d, c, v, e)];
-    precond(D, d.precond, g, Pg);
+      for (int c = 0; c < 3; ++c) {
+        g[t][c] = d.g[vidx(d, c, v, e)];
+        po[t][c] = beta != 0.f ? d.p[vidx(d, c, v, e)] : 0.f;
+      }
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      unsigned i = vidx(d, c, v, e);
-      p[c] = beta != 0.f ? -Pg[c] + beta * d.p[i] : -Pg[c];
-      d.p[i] = p[c];
-      d.gp[i] = g[c];
+      for (int c = 0; c < 6; ++c) D[t][c] = d.D[vidxD(d, c, v, e)];
     }
-    float pn = sqrtf(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
-    M = fmaxf(M, pn);
-    if (fl & 2) {
-      float a = p[0] - pc.x, b = p[1] - pc.y, c = p[2] - pc.z;
-      L = fmaxf(L, sqrtf(a * a + b * b + c * c));
-      d.psurf[(size_t)d.sidx[v] * d.Es + e] = make_float4(p[0], p[1], p[2], 0.f);
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      if (!ok[t]) continue;
+      const int v = v0 + t * stride;
+      float Pg[3], p[3];
+      precond(D[t], d.precond, g[t], Pg);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const unsigned i = vidx(d, c, v, e);
+        p[c] = beta != 0.f ? -Pg[c] + beta * po[t][c] : -Pg[c];
+        d.p[i] = p[c];
+        d.gp[i] = g[t][c];
+      }
+      const float pn = sqrtf(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
+      M = fmaxf(M, pn);
+      if (si[t] >= 0) {
+        const float a = p[0] - pc.x, b = p[1] - pc.y, c = p[2] - pc.z;
+        L = fmaxf(L, sqrtf(a * a + b * b + c * c));
+        d.psurf[(size_t)si[t] * d.Es + e] = make_float4(p[0], p[1], p[2], 0.f);
+      }
+      q += (double)m[t] * (double)(pn * pn);
     }
-    q += (double)d.mass[v] * (double)(pn * pn);
   }
   __shared__ double sq[8][32];
   __shared__ float sM[8][32], sL[8][32];
