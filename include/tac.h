@@ -147,6 +147,17 @@ tac_status tac_markers(tac_sim* sim, float* out, int32_t ncomp, void* stream);
  * zero velocity and pose poses[e] (device fp32 [n_envs][7]). */
 tac_status tac_reset(tac_sim* sim, const uint8_t* env_mask, const float* poses, void* stream);
 
+/* Per-env material theta_e = [E, nu, rho, mu_f] (PAPER.md Sec. "material calibration",
+ * Eqs. 6-7: the calibration searches theta over a batch of environments;
+ * SURVEY §8f-2).  Each pointer is a HOST array of n_envs doubles, or NULL to keep that
+ * parameter; E > 0, 0 <= nu < 0.5, rho > 0, mu_f >= 0 per env, else TAC_EINVAL and
+ * nothing changes.  Takes effect at the next tac_step: Lame parameters (SNH),
+ * lumped masses, the elastic diagonal blocks, the friction coefficient and,
+ * with the default kappa rule (kappa_phys == 0 at create, R4), the barrier stiffness
+ * 0.2 E lbar^2 / (12.25 dhat).  Synchronous (blocking host-to-device copy). */
+tac_status tac_set_env_material(tac_sim* sim, const double* E, const double* nu, const double* rho,
+                                const double* mu_f);
+
 /* Per-env diagnostics of the last step (device outputs [n_envs], any may be NULL):
  * iterations used, |P g|_disp at exit, flags (TAC_FLAG_*). */
 tac_status tac_env_status(tac_sim* sim, int32_t* iters, float* pg_norm, uint32_t* flags, void* stream);

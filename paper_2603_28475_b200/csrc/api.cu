@@ -40,6 +40,10 @@ struct tac_sim {
   int* d_dbg_cnt = nullptr;
   float* d_scratch = nullptr;  // [nv][3] host<->device staging
   tac::Profiler* prof = nullptr;
+  // per-env material (tac_set_env_material): create-time base and the current values
+  double E0 = 0, nu0 = 0, rho0 = 0, lbar = 0;
+  bool kappa_fixed = false;
+  std::vector<double> thE, thNu, thRho, thMu;
 };
 
 static thread_local std::string g_create_err;
@@ -191,6 +195,29 @@ int build_bvh(std::vector<BNode>& nodes, std::vector<int>& prims, const std::vec
     return (int)nodes.size() - 1;
   }
   return build_node(B, ids, 0, (int)ids.size());
+}
+
+// per-env material tables from the current theta (padding lanes take env 0's values)
+tac_status upload_env_material(tac_sim* sim) {
+  const Dev& d = sim->d;
+  std::vector<float> em(4 * (size_t)d.Es);
+  std::vector<double> ed(2 * (size_t)d.Es);
+  const double mu0 = sim->E0 / (2 * (1 + sim->nu0));
+  for (int e = 0; e < d.Es; ++e) {
+    const int s = e < d.E ? e : 0;
+    const double E = sim->thE[s], nu = sim->thNu[s];
+    const double mu = E / (2 * (1 + nu)), lam = E * nu / ((1 + nu) * (1 - 2 * nu));
+    em[e] = (float)mu;
+    em[d.Es + e] = (float)(lam + mu);
+    em[2 * (size_t)d.Es + e] = (float)(sim->thRho[s] / sim->rho0);
+    em[3 * (size_t)d.Es + e] = (float)(mu / mu0);
+    ed[e] = sim->kappa_fixed ? d.kappa_phys : 0.2 * E * sim->lbar * sim->lbar / (12.25 * d.dhat);  // R4 per env
+    ed[d.Es + e] = sim->thMu[s];
+  }
+  if (cudaMemcpy(d.emat, em.data(), sizeof(float) * em.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(d.edbl, ed.data(), sizeof(double) * ed.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+    return TAC_ECUDA;
+  return TAC_OK;
 }
 
 float down(double x) { float f = (float)x; return (double)f > x ? std::nextafter(f, -INFINITY) : f; }
@@ -628,7 +655,12 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     for (auto& e : ses) { V q = sub(X[e.first], X[e.second]); sl += std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2]); }
     double lbar = ses.empty() ? 1e-3 : sl / ses.size();
     d.kappa_phys = 0.2 * MT.E * lbar * lbar / (12.25 * P.dhat);
+    sim->lbar = lbar;
+  } else {
+    sim->kappa_fixed = true;
   }
+  sim->E0 = MT.E; sim->nu0 = MT.nu; sim->rho0 = MT.rho;
+  sim->thE.assign(d.E, MT.E); sim->thNu.assign(d.E, MT.nu); sim->thRho.assign(d.E, MT.rho); sim->thMu.assign(d.E, MT.mu_f);
   if (d.nsv >= 65536 || niv >= 65536) {  // candidate corner ids are packed 16 bit (Dev::ccorn)
     delete sim;
     return fail(TAC_EINVAL, "more than 65535 gel-surface or indenter vertices");
@@ -784,6 +816,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     if ((rc = zalloc(sim, nvec, &d.u)) || (rc = zalloc(sim, nvec, &d.ut)) || (rc = zalloc(sim, nvec, &d.vt)) ||
         (rc = zalloc(sim, nvec, &d.uh)) || (rc = zalloc(sim, nvec, &d.g)) || (rc = zalloc(sim, nvec, &d.gp)) ||
         (rc = zalloc(sim, nvec, &d.p)) || (rc = zalloc(sim, 2 * nvec, &d.D)) || (rc = zalloc(sim, (size_t)d.E, &d.es)) ||
+        (rc = zalloc(sim, 4 * (size_t)d.Es, &d.emat)) || (rc = zalloc(sim, 2 * (size_t)d.Es, &d.edbl)) ||
         (rc = zalloc(sim, (size_t)kNAcc * d.Es, &d.acc)) || (rc = zalloc(sim, (size_t)kNAccU * d.Es, &d.accu)) ||
         (rc = zalloc(sim, (size_t)d.Es, &d.dalpha)) || (rc = zalloc(sim, (size_t)d.Es, &d.beta)) ||
         (rc = zalloc(sim, (size_t)d.Es, &d.run)) || (rc = zalloc(sim, (size_t)d.Es, &d.pcf)) ||
@@ -796,6 +829,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
         (rc = zalloc(sim, 1, &sim->d_dbg_cnt)) || (rc = zalloc(sim, 3 * (size_t)nv, &sim->d_scratch)))
       goto fail;
     if (cudaMallocHost(&sim->h_flag, sizeof(int)) != cudaSuccess) { rc = TAC_ENOMEM; goto fail; }
+    if ((rc = upload_env_material(sim))) { sim->err = "upload per-env material"; goto fail; }
     // initial poses: per-env fp64 state on the host, then upload
     std::vector<EnvS> es(d.E);
     for (int e = 0; e < d.E; ++e) {
@@ -921,6 +955,29 @@ tac_status tac_reset(tac_sim* sim, const uint8_t* env_mask, const float* poses, 
   cudaSetDevice(sim->device);
   launch_reset(sim->d, env_mask, poses, (cudaStream_t)stream);
   return post_launch(sim);
+}
+
+tac_status tac_set_env_material(tac_sim* sim, const double* E, const double* nu, const double* rho,
+                                const double* mu_f) {
+  tac_status st = check_sim(sim);
+  if (st) return st;
+  const int n = sim->d.E;
+  for (int e = 0; e < n; ++e) {  // validate everything before changing anything
+    if ((E && !(E[e] > 0)) || (nu && !(nu[e] >= 0 && nu[e] < 0.5)) || (rho && !(rho[e] > 0)) ||
+        (mu_f && !(mu_f[e] >= 0))) {
+      sim->err = "tac_set_env_material: invalid material for env " + std::to_string(e);
+      return TAC_EINVAL;
+    }
+  }
+  for (int e = 0; e < n; ++e) {
+    if (E) sim->thE[e] = E[e];
+    if (nu) sim->thNu[e] = nu[e];
+    if (rho) sim->thRho[e] = rho[e];
+    if (mu_f) sim->thMu[e] = mu_f[e];
+  }
+  cudaSetDevice(sim->device);
+  if ((st = upload_env_material(sim))) { sim->err = "tac_set_env_material: upload failed"; return st; }
+  return TAC_OK;
 }
 
 tac_status tac_env_status(tac_sim* sim, int32_t* iters, float* pg_norm, uint32_t* flags, void* stream) {

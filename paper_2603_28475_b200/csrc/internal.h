@@ -125,7 +125,10 @@ struct Dev {
   int* reb_list;         // [E] envs that rebuild their candidates in this iteration
   int* nreb;             // [1]
   // material / params
-  float mu, lam2;        // mu, lambda' = lambda + mu
+  float mu, lam2;        // mu, lambda' = lambda + mu of the create-time material (defaults)
+  float* emat;           // [4][Es] per-env material: mu, lambda', mass scale rho_e / rho_0,
+                         // elastic-diagonal scale mu_e / mu_0 (mass and sum V mu |b|^2 are stored for env 0's material)
+  double* edbl;          // [2][Es] per-env kappa_phys, mu_f
   double rho_max, dhat, kappa_phys, eps_v, tol_x, k_t, k_r, f_max, t_max, ccd_s, bp_margin, c1, eps_E, mu_f;
   int beta_rule, precond, max_halv, stagnation, fixed_iters;
   // element tiles

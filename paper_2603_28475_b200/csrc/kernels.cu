@@ -629,10 +629,11 @@ __global__ void __launch_bounds__(128) k_broadphase_list(Dev d, double r) {
 
 // ------------------------------------------------------------------ a3: friction anchors
 // pairs with d(x^t) < dhat: lambda = -kappa b'(d), frozen weights, tangent basis (R7)
-__global__ void k_anchors(Dev d, double kappa) {
+__global__ void k_anchors(Dev d, double h2) {
   int e = blockIdx.y;
   if (e >= d.E || d.es[e].mode != kActive) return;
   const EnvS& s = d.es[e];
+  const double kappa = h2 * d.edbl[e];  // h^2 kappa_phys of this env
   int n = min(d.ncand[e], d.kmax);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     unsigned long long rec = d.cand[(size_t)e * d.kmax + i];
@@ -709,8 +710,8 @@ __global__ void k_vert_pre(Dev d, float h2) {
       const int v = v0 + t * stride;
       ok[t] = act && v < d.nv && !(d.vflag[v] & 1);
       if (!ok[t]) continue;
-      m[t] = d.mass[v];
-      sm[t] = d.smu[v];
+      m[t] = d.mass[v] * d.emat[2 * d.Es + e];  // per-env density and shear modulus scales
+      sm[t] = d.smu[v] * d.emat[3 * d.Es + e];
       si[t] = d.sidx[v];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -779,7 +780,7 @@ __global__ void __launch_bounds__(256, 4) k_elem_grad(Dev d, float h2) {
   const int e = blockIdx.y * 32 + threadIdx.x;
   const bool act = e < d.E && (d.run[e] & 1);
   if (!__any_sync(0xffffffffu, act)) return;
-  const float mu = d.mu, l2 = d.lam2;
+  const float mu = d.emat[e], l2 = d.emat[d.Es + e];  // per-env material
   // AoSoA: one per-vertex base, components at immediate offsets of 32 floats
   const unsigned G = (unsigned)(d.Es >> 5), eg = (unsigned)blockIdx.y, lane = threadIdx.x;
   const float* __restrict__ up = d.u;
@@ -881,7 +882,7 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
   const int e = blockIdx.y * 32 + threadIdx.x;
   const bool act = e < d.E && (d.run[e] & 1);
   if (!__any_sync(0xffffffffu, act)) return;
-  const float mu = d.mu, l2 = d.lam2;
+  const float mu = d.emat[e], l2 = d.emat[d.Es + e];  // per-env material
   const unsigned G = (unsigned)(d.Es >> 5), eg = (unsigned)blockIdx.y, lane = threadIdx.x;
   double esum = 0;
   for (int cidx = blockIdx.x * 8 + threadIdx.y; cidx < d.ncells; cidx += gridDim.x * 8) {
@@ -989,7 +990,7 @@ __global__ void __launch_bounds__(256, 2) k_elem_curv_cells(Dev d, float h2) {
   const int e = blockIdx.y * 32 + threadIdx.x;
   const bool act = e < d.E && (d.run[e] & 2);
   if (!__any_sync(0xffffffffu, act)) return;
-  const float mu = d.mu, l2 = d.lam2;
+  const float mu = d.emat[e], l2 = d.emat[d.Es + e];  // per-env material
   const unsigned G = (unsigned)(d.Es >> 5), eg = (unsigned)blockIdx.y, lane = threadIdx.x;
   double qsum = 0;
   for (int cidx = blockIdx.x * 8 + threadIdx.y; cidx < d.ncells; cidx += gridDim.x * 8) {
@@ -1082,7 +1083,7 @@ __global__ void __launch_bounds__(256) k_elem_curv_tiled(Dev d, float h2) {
     }
   }
   __syncthreads();
-  const float mu = d.mu, l2 = d.lam2;
+  const float mu = d.emat[e], l2 = d.emat[d.Es + e];  // per-env material
   const int t0 = d.tile_tstart[tile], nt = d.tile_tstart[tile + 1] - t0;
   double qsum = 0;
   if (act) {
@@ -1166,9 +1167,10 @@ __device__ __forceinline__ void scatter_gel(const Dev& d, int v, int e, d3 f, do
 
 
 template <int KIND>
-__global__ void __launch_bounds__(128) k_contact_near(Dev d, double kappa) {
+__global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
   int e = blockIdx.y;
   if (e >= d.E || !(d.run[e] & 1)) return;
+  const double kappa = h2 * d.edbl[e];  // h^2 kappa_phys of this env
   const EnvS& s = d.es[e];
   __shared__ double R[9], c[3];
   __shared__ double smr[4 * 20];
@@ -1276,7 +1278,7 @@ __global__ void __launch_bounds__(128) k_contact_friction(Dev d, double eps_f) {
     d3 t1 = mk(A.t1[0], A.t1[1], A.t1[2]), t2 = mk(A.t2[0], A.t2[1], A.t2[2]);
     double ta = dot(t1, Dl), tb = dot(t2, Dl);
     double sn = sqrt(ta * ta + tb * tb);
-    double ml = d.mu_f * (double)A.lam;
+    double ml = d.edbl[d.Es + e] * (double)A.lam;  // per-env mu_f
     Ef += ml * moll_f(sn, eps_f);
     double f1 = ml * moll_f1(sn, eps_f);
     d.anc_f1[(size_t)e * d.amax + i] = (float)f1;
@@ -1566,10 +1568,11 @@ __global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
 }
 
 // curvature + near-pair step bounds from the cached geometry, p staged in shared memory
-__global__ void __launch_bounds__(256) k_contact_curv_staged(Dev d, double kappa) {
+__global__ void __launch_bounds__(256) k_contact_curv_staged(Dev d, double h2) {
   extern __shared__ __align__(16) char shc3[];
   int e = blockIdx.y;
   if (e >= d.E || !(d.run[e] & 2)) return;
+  const double kappa = h2 * d.edbl[e];  // h^2 kappa_phys of this env
   const EnvS& s = d.es[e];
   __shared__ double R[9], pr[6];
   __shared__ double sm[8];
@@ -1919,7 +1922,7 @@ __global__ void __launch_bounds__(256) k_dir_apply(Dev d) {
       const unsigned char fl = d.vflag[v];
       ok[t] = !(fl & 1);
       if (!ok[t]) continue;
-      m[t] = d.mass[v];
+      m[t] = d.mass[v] * d.emat[2 * d.Es + e];
       si[t] = (fl & 2) ? d.sidx[v] : -1;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -2262,7 +2265,7 @@ void launch_broadphase(const Dev& d, bool masked, cudaStream_t s) {
   LAUNCHK(KID_BROADPHASE, s, (k_broadphase<<<dim3(nb, d.E), 128, 0, s>>>(d, d.dhat + d.bp_margin, nullptr, nullptr, 0)));
 }
 void launch_anchors(const Dev& d, double h, cudaStream_t s) {
-  LAUNCHK(KID_ANCHORS, s, (k_anchors<<<cgrid(d), 128, 0, s>>>(d, h * h * d.kappa_phys)));
+  LAUNCHK(KID_ANCHORS, s, (k_anchors<<<cgrid(d), 128, 0, s>>>(d, h * h)));
 }
 void launch_eval(const Dev& d, double h, cudaStream_t s) {
   LAUNCHK(KID_VERT_PRE, s, (k_vert_pre<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d, (float)(h * h))));
@@ -2278,7 +2281,7 @@ void launch_eval(const Dev& d, double h, cudaStream_t s) {
   }
   const size_t cls_smem = sizeof(float4) * (size_t)(d.nsv + d.niv);  // [nsv] X + u, [niv] c + R Y
   LAUNCHK(KID_CONTACT_CLASSIFY, s, (k_contact_classify_staged<<<sgrid(d), 256, cls_smem, s>>>(d)));
-  const double kap = h * h * d.kappa_phys;
+  const double kap = h * h;  // kernels scale by their env's kappa_phys
   LAUNCHK(KID_CONTACT_GRAD, s, (k_contact_near<0><<<cgrid(d), 128, 0, s>>>(d, kap)));
   LAUNCHK(KID_CONTACT_NEAR_IG, s, (k_contact_near<1><<<cgrid(d), 128, 0, s>>>(d, kap)));
   LAUNCHK(KID_CONTACT_NEAR_EE, s, (k_contact_near<2><<<cgrid(d), 128, 0, s>>>(d, kap)));
@@ -2297,7 +2300,7 @@ void launch_curvature(const Dev& d, double h, cudaStream_t s) {
   } else {
     LAUNCHK(KID_ELEM_CURV, s, (k_elem_curv_tiled<<<dim3(d.Es / 32, d.ntiles), 256, kTiledCurvSmem, s>>>(d, (float)(h * h))));
   }
-  LAUNCHK(KID_CONTACT_CURV, s, (k_contact_curv_staged<<<sgrid(d), 256, d.contact_smem, s>>>(d, h * h * d.kappa_phys)));
+  LAUNCHK(KID_CONTACT_CURV, s, (k_contact_curv_staged<<<sgrid(d), 256, d.contact_smem, s>>>(d, h * h)));
 }
 void launch_alpha(const Dev& d, double h, cudaStream_t s) {
   cudaMemsetAsync(d.nreb, 0, sizeof(int), s);

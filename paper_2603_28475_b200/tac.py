@@ -73,6 +73,7 @@ def lib():
         L.tac_markers.argtypes = [vp, vp, C.c_int32, vp]
         L.tac_reset.argtypes = [vp, vp, vp, vp]
         L.tac_env_status.argtypes = [vp, vp, vp, vp, vp]
+        L.tac_set_env_material.argtypes = [vp, _dp, _dp, _dp, _dp]
         L.tac_info.argtypes = [vp, _ip]
         L.tac_last_launch_count.argtypes = [vp]
         L.tac_last_launch_count.restype = C.c_int64
@@ -98,7 +99,8 @@ def lib():
 EXPORTED = ["tac_create", "tac_step", "tac_markers", "tac_reset", "tac_env_status", "tac_info",
             "tac_last_launch_count", "tac_destroy", "tac_last_error", "tac_get_state", "tac_set_state",
             "tac_debug_broadphase", "tac_debug_surface", "tac_debug_marker_map", "tac_debug_eval",
-            "tac_profile_enable", "tac_profile_read", "tac_profile_kernel_name", "tac_env_stats"]
+            "tac_profile_enable", "tac_profile_read", "tac_profile_kernel_name", "tac_env_stats",
+            "tac_set_env_material"]
 N_KERNEL_IDS = 24
 
 
@@ -208,6 +210,17 @@ class TacSim:
     def reset(self, mask, poses, stream=None):
         self._check(lib().tac_reset(self.h, C.c_void_p(mask.data_ptr()), C.c_void_p(poses.data_ptr()),
                                     _stream_ptr(stream)), "tac_reset")
+
+    def set_env_material(self, E=None, nu=None, rho=None, mu_f=None):
+        """Per-env material theta_e: each argument None or n_envs values."""
+        arrs = []
+        for a in (E, nu, rho, mu_f):
+            if a is None:
+                arrs.append((None, None))
+            else:
+                a = np.ascontiguousarray(np.broadcast_to(np.asarray(a, dtype=np.float64), (self.n_envs,)))
+                arrs.append((a, a.ctypes.data_as(_dp)))
+        self._check(lib().tac_set_env_material(self.h, *[p for _, p in arrs]), "tac_set_env_material")
 
     def env_status(self, stream=None):
         import torch

@@ -188,6 +188,79 @@ def test_converged_step_parity_c1(torch_cuda):
     _assert_parity(s, sim, o, mk, 0)
 
 
+@pytest.mark.parametrize("beta_rule,precond", [(1, 0), (0, 1)])
+def test_solver_variants_converged_parity(torch_cuda, beta_rule, precond):
+    """SURVEY 8f-3 switches (beta rule PR+ of P:454's family, scalar Jacobi of P:457):
+    GPU and oracle converge to the same states, with comparable iteration counts."""
+    s = w.scene_small_peg(n_envs=2, n_steps=3)
+    s.params.beta_rule = beta_rule
+    s.params.precond = precond
+    sim, o, mk = _run_both(s, 3)
+    it, pg, fl = sim.env_status()
+    for e in range(2):
+        assert int(fl[e]) & 1, (e, int(fl[e]))
+        assert o.status_of(e)["flags"] & 1
+        _assert_parity(s, sim, o, mk, e)
+        it_o = o.status_of(e)["iters"]
+        assert int(it[e]) <= 3 * it_o + 50 and it_o <= 3 * int(it[e]) + 50, (int(it[e]), it_o)
+
+
+def test_fletcher_reeves_matches_oracle_behaviour(torch_cuda):
+    """FR (beta rule 2) without restarts jams on the second C1 press step in the fp64
+    oracle (stagnation); the GPU reproduces the converged first step and the jam."""
+    s = c1_press_scene(mu_f=1.0, steps=2, depth=0.2e-3)
+    s.params.beta_rule = 2
+    sim, o, mk = _run_both(s, 1)
+    it, pg, fl = sim.env_status()
+    assert int(fl[0]) & 1 and o.status_of(0)["flags"] & 1
+    _assert_parity(s, sim, o, mk, 0)
+    import torch
+    sim.step(torch.tensor(s.poses[1], dtype=torch.float32, device="cuda").contiguous(), s.dt)
+    o.step(s.poses[1])
+    it, pg, fl = sim.env_status()
+    assert not (int(fl[0]) & 1) and int(fl[0]) & (2 | 64), int(fl[0])
+    assert not (o.status_of(0)["flags"] & 1)
+
+
+def test_per_env_material_converged_parity(torch_cuda):
+    """per-env theta = [E, nu, rho, mu_f] in one batch (the calibration of
+    Eqs. 6-7, evaluates a CMA-ES population as envs): every env matches an
+    oracle built with that env's material; an invalid theta is refused."""
+    import copy
+    import torch
+    s = w.scene_small_peg(n_envs=3, n_steps=3)
+    s.params.tol_x = 1e-9
+    s.params.max_iters = 8000
+    s.params.stagnation = 3000
+    th = dict(E=[0.6e5, 1.0e5, 1.8e5], nu=[0.40, 0.45, 0.48], rho=[900.0, 1100.0, 1500.0], mu_f=[0.4, 1.0, 1.5])
+    sim = _sim(s)
+    sim.set_env_material(**th)
+    with pytest.raises(Exception):
+        sim.set_env_material(nu=[0.3, 0.5, 0.4])
+    for k in range(3):
+        sim.step(torch.tensor(s.poses[k], dtype=torch.float32, device="cuda").contiguous(), s.dt)
+    mk = sim.markers().cpu().numpy()
+    it, pg, fl = sim.env_status()
+    for e in range(3):
+        assert int(fl[e]) & 1, (e, int(fl[e]))
+        se = copy.deepcopy(s)
+        se.material = w.Material(E=th["E"][e], nu=th["nu"][e], rho=th["rho"][e], mu_f=th["mu_f"][e])
+        se.init_poses = s.init_poses[e:e + 1]
+        se.poses = s.poses[:, e:e + 1]
+        p_or = w.Params(**{**s.params.__dict__})
+        p_or.tol_x = 1e-11
+        o = O.Oracle(se, params=p_or)
+        for k in range(3):
+            o.step(se.poses[k])
+        u_g, _, c_g, _ = sim.get_state(e)
+        u_o, _, c_o, _ = o.get_state(0)
+        assert np.abs(u_g - u_o).max() <= 1e-4 * max(s.extent)
+        m_o = o.markers(0)
+        assert np.abs(mk[e] - m_o).max() <= 1e-3 * np.abs(m_o).max()
+    # the materials differ enough to matter: env responses are not interchangeable
+    assert np.abs(mk[0] - mk[2]).max() > 1e-2 * np.abs(mk[2]).max()
+
+
 def test_converged_parity_multi_env_ragged(torch_cuda):
     s = w.scene_small_peg(n_envs=5, n_steps=4)
     sim, o, mk = _run_both(s, 4)
