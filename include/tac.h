@@ -143,6 +143,13 @@ tac_status tac_step(tac_sim* sim, const float* target_poses, float dt, void* str
  * = (u_m.t1, u_m.t2[, u_m.n]) with u_m = sum_j w_mj u_j.  ncomp in {2, 3}. */
 tac_status tac_markers(tac_sim* sim, float* out, int32_t ncomp, void* stream);
 
+/* Calibration loss term (Eq. 6, L = 1/(K N) sum_k sum_i |u_sim - u_real|^2):
+ * acc[e] += sum over markers and the ncomp components of (u_m(theta_e) - ref[e][m])^2,
+ * u_m computed exactly as tac_markers does.  ref: device fp32 [n_envs][rows*cols][ncomp];
+ * acc: device fp64 [n_envs], accumulated (zero it once per trajectory).  ncomp in {2, 3}.
+ * Asynchronous on `stream`. */
+tac_status tac_marker_sqerr(tac_sim* sim, const float* ref, double* acc, int32_t ncomp, void* stream);
+
 /* Re-initialise the envs with env_mask[e] != 0 (device uint8 [n_envs]) to rest,
  * zero velocity and pose poses[e] (device fp32 [n_envs][7]). */
 tac_status tac_reset(tac_sim* sim, const uint8_t* env_mask, const float* poses, void* stream);

@@ -948,6 +948,19 @@ tac_status tac_markers(tac_sim* sim, float* out, int32_t ncomp, void* stream) {
   return post_launch(sim);
 }
 
+tac_status tac_marker_sqerr(tac_sim* sim, const float* ref, double* acc, int32_t ncomp, void* stream) {
+  tac_status st = check_sim(sim);
+  if (st) return st;
+  if (!ref || !acc || (ncomp != 2 && ncomp != 3)) { sim->err = "tac_marker_sqerr: bad pointer or ncomp"; return TAC_EINVAL; }
+  cudaSetDevice(sim->device);
+  g_launches = 0;
+  g_prof = sim->prof;
+  launch_marker_sqerr(sim->d, ref, acc, ncomp, (cudaStream_t)stream);
+  g_prof = nullptr;
+  sim->launches = g_launches;
+  return post_launch(sim);
+}
+
 tac_status tac_reset(tac_sim* sim, const uint8_t* env_mask, const float* poses, void* stream) {
   tac_status st = check_sim(sim);
   if (st) return st;

@@ -162,6 +162,7 @@ void launch_curvature(const Dev& d, double h, cudaStream_t s);
 void launch_alpha(const Dev& d, double h, cudaStream_t s);
 void launch_finalize(const Dev& d, double h, cudaStream_t s);
 void launch_markers(const Dev& d, float* out, int ncomp, cudaStream_t s);
+void launch_marker_sqerr(const Dev& d, const float* ref, double* acc, int ncomp, cudaStream_t s);
 void launch_reset(const Dev& d, const unsigned char* mask, const float* poses, cudaStream_t s);
 void launch_status(const Dev& d, int* iters, float* pg, unsigned* flags, cudaStream_t s);
 void launch_any_active(const Dev& d, int* out, cudaStream_t s);

@@ -2184,6 +2184,43 @@ __global__ void k_markers(Dev d, float* out, int ncomp, float4 t1, float4 t2, fl
   if (ncomp == 3) o[2] = um[0] * nn.x + um[1] * nn.y + um[2] * nn.z;
 }
 
+// calibration loss term (Eq. 6): acc[e] += sum_m |u_m(theta_e) - u_ref[e][m]|^2 over
+// the marker field computed exactly as k_markers does; one CTA per env (sole writer)
+__global__ void __launch_bounds__(128) k_marker_sqerr(Dev d, const float* ref, double* acc, int ncomp, float4 t1,
+                                                      float4 t2, float4 nn) {
+  const int e = blockIdx.x;
+  __shared__ double sw[4];
+  double se = 0;
+  for (int m = threadIdx.x; m < d.nm; m += blockDim.x) {
+    int4 id = __ldg(d.mk_idx + m);
+    float4 w = __ldg(d.mk_w + m);
+    int vv[4] = {id.x, id.y, id.z, id.w};
+    float ww[4] = {w.x, w.y, w.z, w.w};
+    float um[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) um[c] = fmaf(ww[k], d.ut[vidx(d, c, vv[k], e)], um[c]);
+    float o[3];
+    o[0] = um[0] * t1.x + um[1] * t1.y + um[2] * t1.z;
+    o[1] = um[0] * t2.x + um[1] * t2.y + um[2] * t2.z;
+    o[2] = um[0] * nn.x + um[1] * nn.y + um[2] * nn.z;
+    const float* r = ref + ((size_t)e * d.nm + m) * ncomp;
+    for (int c = 0; c < ncomp; ++c) {
+      const double df = (double)o[c] - (double)r[c];
+      se += df * df;
+    }
+  }
+  se = warp_sum(se);
+  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = se;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sw[w];
+    acc[e] += t;
+  }
+}
+
 __global__ void k_reset_env(Dev d, const unsigned char* mask, const float* poses) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= d.E || !mask[e]) return;
@@ -2318,6 +2355,11 @@ void launch_markers(const Dev& d, float* out, int ncomp, cudaStream_t s) {
   float4 t1 = make_float4(d.t1[0], d.t1[1], d.t1[2], 0), t2 = make_float4(d.t2[0], d.t2[1], d.t2[2], 0),
          nn = make_float4(d.nrm[0], d.nrm[1], d.nrm[2], 0);
   LAUNCHK(KID_MARKERS, s, (k_markers<<<(n + 255) / 256, 256, 0, s>>>(d, out, ncomp, t1, t2, nn)));
+}
+void launch_marker_sqerr(const Dev& d, const float* ref, double* acc, int ncomp, cudaStream_t s) {
+  float4 t1 = make_float4(d.t1[0], d.t1[1], d.t1[2], 0), t2 = make_float4(d.t2[0], d.t2[1], d.t2[2], 0),
+         nn = make_float4(d.nrm[0], d.nrm[1], d.nrm[2], 0);
+  LAUNCHK(KID_MARKERS, s, (k_marker_sqerr<<<d.E, 128, 0, s>>>(d, ref, acc, ncomp, t1, t2, nn)));
 }
 void launch_reset(const Dev& d, const unsigned char* mask, const float* poses, cudaStream_t s) {
   LAUNCHK(KID_OTHER, s, (k_reset_env<<<eblocks(d), 128, 0, s>>>(d, mask, poses)));

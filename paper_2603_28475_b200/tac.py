@@ -74,6 +74,7 @@ def lib():
         L.tac_reset.argtypes = [vp, vp, vp, vp]
         L.tac_env_status.argtypes = [vp, vp, vp, vp, vp]
         L.tac_set_env_material.argtypes = [vp, _dp, _dp, _dp, _dp]
+        L.tac_marker_sqerr.argtypes = [vp, vp, vp, C.c_int32, vp]
         L.tac_info.argtypes = [vp, _ip]
         L.tac_last_launch_count.argtypes = [vp]
         L.tac_last_launch_count.restype = C.c_int64
@@ -100,7 +101,7 @@ EXPORTED = ["tac_create", "tac_step", "tac_markers", "tac_reset", "tac_env_statu
             "tac_last_launch_count", "tac_destroy", "tac_last_error", "tac_get_state", "tac_set_state",
             "tac_debug_broadphase", "tac_debug_surface", "tac_debug_marker_map", "tac_debug_eval",
             "tac_profile_enable", "tac_profile_read", "tac_profile_kernel_name", "tac_env_stats",
-            "tac_set_env_material"]
+            "tac_set_env_material", "tac_marker_sqerr"]
 N_KERNEL_IDS = 24
 
 
@@ -206,6 +207,15 @@ class TacSim:
         assert out.is_cuda and out.is_contiguous() and out.numel() >= self.n_envs * self.nm * ncomp
         self._check(lib().tac_markers(self.h, C.c_void_p(out.data_ptr()), ncomp, _stream_ptr(stream)), "tac_markers")
         return out
+
+    def marker_sqerr(self, ref, acc, stream=None):
+        """acc[e] += |markers(e) - ref[e]|^2 (calibration loss term, Eq. 6); ref [E, nm, ncomp] fp32,
+        acc [E] fp64, both on this device."""
+        assert ref.is_cuda and ref.is_contiguous() and acc.is_cuda and acc.is_contiguous()
+        ncomp = int(ref.shape[-1])
+        self._check(lib().tac_marker_sqerr(self.h, C.c_void_p(ref.data_ptr()), C.c_void_p(acc.data_ptr()), ncomp,
+                                           _stream_ptr(stream)), "tac_marker_sqerr")
+        return acc
 
     def reset(self, mask, poses, stream=None):
         self._check(lib().tac_reset(self.h, C.c_void_p(mask.data_ptr()), C.c_void_p(poses.data_ptr()),

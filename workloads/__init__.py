@@ -514,3 +514,46 @@ def scene_c5(n_envs=256, n_steps=64, seed0=20270000):
     sc.params.max_candidates = 65536  # edge presses of the split square peg reach ~46k pairs per env
     sc.params.max_anchors = 16384
     return sc
+
+# ----------------------------------------------------------------------------
+# §8f-2: batched material calibration (Eqs. 6-7)
+# ----------------------------------------------------------------------------
+def scene_calib(frames=6, cells=(16, 12, 4), f_max=0.2):
+    """Calibration workload: N = 4 indentation trajectories of a 3 mm sphere on a
+    16x12x4 mm pad ("different deformation modes": press + shear x, off-centre
+    press + shear y, deep press, press + twist), `frames` frames each.  The pose spring's
+    force cap f_max (R18) is lowered so the deep frames are force-limited: with a purely
+    displacement-driven indenter the quasi-static marker field carries almost no
+    information about E.  Poses [frames][4][7]; the reference fields come from the
+    simulator at a hidden theta_true (synthetic)."""
+    ext = (16 * MM, 12 * MM, 4 * MM)
+    X, T, Fx = make_pad(ext, cells)
+    R = 3 * MM
+    Y, tris = make_icosphere(R, 2)
+    M, frame = make_markers(ext, cells)
+    q0 = [1.0, 0, 0, 0]
+    gap = 0.05 * MM
+    half = frames // 2
+    trajs = []
+    specs = [((0.0, 0.0), 0.4 * MM, (0.3 * MM, 0.0), 0.0),
+             ((2.0 * MM, -1.0 * MM), 0.3 * MM, (0.0, 0.3 * MM), 0.0),
+             ((-1.5 * MM, 1.0 * MM), 0.9 * MM, (0.0, 0.0), 0.0),
+             ((0.0, 1.0 * MM), 0.35 * MM, (0.0, 0.0), 5.0)]
+    inits = []
+    for (x0, y0), depth, (sx, sy), twist_deg in specs:
+        inits.append(pose((x0, y0, R + gap), q0))
+        fr = []
+        for k in range(frames):
+            if k < half:
+                t = (k + 1) / half
+                fr.append(pose((x0, y0, R + gap - t * (gap + depth)), q0))
+            else:
+                t = (k + 1 - half) / (frames - half)
+                a = np.deg2rad(twist_deg) * t
+                q = [np.cos(a / 2), 0.0, 0.0, np.sin(a / 2)]
+                fr.append(pose((x0 + t * sx, y0 + t * sy, R - depth), q))
+        trajs.append(fr)
+    poses = np.stack([np.stack([trajs[i][k] for i in range(len(specs))]) for k in range(frames)])
+    sc = Scene("calib", X, T, Fx, Y, tris, M, frame, np.stack(inits), poses, extent=ext, cells=cells)
+    sc.params.f_max = f_max
+    return sc
