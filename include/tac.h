@@ -143,6 +143,16 @@ tac_status tac_step(tac_sim* sim, const float* target_poses, float dt, void* str
  * = (u_m.t1, u_m.t2[, u_m.n]) with u_m = sum_j w_mj u_j.  ncomp in {2, 3}. */
 tac_status tac_markers(tac_sim* sim, float* out, int32_t ncomp, void* stream);
 
+/* Per-step target pose noise (PAPER.md Table "Parameters Randomization Range", P:693-694,
+ * "IPC Rand. Move. Noise", and P:726 "a small random movement on holding object" at each
+ * timestep; reading DESIGN.md R27).  From the next tac_step on, env e's target
+ * at step k (k = number of tac_step calls since create) is c_s += sigma_t (u0, u1, u2) [m],
+ * R_s <- exp([sigma_r (u3, u4, u5)]) R_s [rad], u uniform on (-1, 1) from Philox4x32-10 with
+ * key = seed and counter = (env_offset + e, k_lo, k_hi, 0 / 1).  sigma_t = sigma_r = 0 turns
+ * it off (the default).  env_offset >= 0 is this simulator's first global env id (sharded
+ * ranks reproduce a single-process run).  TAC_EINVAL on negative arguments. */
+tac_status tac_set_pose_noise(tac_sim* sim, double sigma_t, double sigma_r, uint64_t seed, int64_t env_offset);
+
 /* Calibration loss term (Eq. 6, L = 1/(K N) sum_k sum_i |u_sim - u_real|^2):
  * acc[e] += sum over markers and the ncomp components of (u_m(theta_e) - ref[e][m])^2,
  * u_m computed exactly as tac_markers does.  ref: device fp32 [n_envs][rows*cols][ncomp];

@@ -74,6 +74,8 @@ def lib():
         L.or_dist_pt.argtypes = [_dp, _dp, _dp, _dp, _dp]
         L.or_dist_ee.restype = C.c_double
         L.or_dist_ee.argtypes = [_dp, _dp, _dp, _dp, _dp]
+        L.or_set_pose_noise.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_uint64, C.c_int64]
+        L.or_philox.argtypes = [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
         L.or_certificate.restype = C.c_int
         L.or_certificate.argtypes = [_dp, C.c_int, C.c_double, _dp, _dp]
         L.or_psi.restype = C.c_double
@@ -115,6 +117,16 @@ def dist_ee(a0, a1, b0, b1):
     args = [_d(x) for x in (a0, a1, b0, b1)]
     d = lib().or_dist_ee(*[a[1] for a in args], w.ctypes.data_as(_dp))
     return d, w
+
+
+def philox4x32_10(ctr, key):
+    """Philox4x32-10 block (the pose-noise generator, R27): 4 uint32 counter, 2 uint32 key."""
+    c = np.ascontiguousarray(ctr, dtype=np.uint32)
+    k = np.ascontiguousarray(key, dtype=np.uint32)
+    o = np.zeros(4, dtype=np.uint32)
+    P32 = C.POINTER(C.c_uint32)
+    lib().or_philox(c.ctypes.data_as(P32), k.ctypes.data_as(P32), o.ctypes.data_as(P32))
+    return o
 
 
 def certificate(z, na, dhat):
@@ -229,6 +241,10 @@ class Oracle:
     def step(self, targets, dt=None, threads=1, env0=0, n=0):
         targets, tp = _d(targets)
         lib().or_step(self.h, tp, float(self.scene.dt if dt is None else dt), threads, env0, n)
+
+    def set_pose_noise(self, sigma_t, sigma_r, seed, env_offset=0):
+        """Per-step target-pose noise (R27); one step() call = one step of the envs it covers."""
+        lib().or_set_pose_noise(self.h, float(sigma_t), float(sigma_r), int(seed), int(env_offset))
 
     def status_of(self, env):
         o = np.zeros(5)

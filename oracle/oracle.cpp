@@ -309,7 +309,43 @@ struct Env {
 struct Oracle {
   Problem P;
   std::vector<Env> env;
+  // per-step target pose noise (R27): amplitudes, Philox key, step count
+  double noise_t = 0, noise_r = 0;
+  uint64_t noise_seed = 0, step_count = 0;
+  int64_t env_offset = 0;
 };
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (Salmon, Moraes, Dror, Shaw, "Parallel random numbers: as easy as 1, 2,
+// 3", SC'11): 10 rounds of (hi, lo) = M * x products with key bumps by the Weyl constants
+// ---------------------------------------------------------------------------
+void philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+  uint32_t c[4] = {ctr_in[0], ctr_in[1], ctr_in[2], ctr_in[3]}, k[2] = {key_in[0], key_in[1]};
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) { k[0] += W0; k[1] += W1; }
+    const uint64_t p0 = (uint64_t)M0 * c[0], p1 = (uint64_t)M1 * c[2];
+    const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0, hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    const uint32_t n0 = hi1 ^ c[1] ^ k[0], n1 = lo1, n2 = hi0 ^ c[3] ^ k[1], n3 = lo0;
+    c[0] = n0; c[1] = n1; c[2] = n2; c[3] = n3;
+  }
+  for (int i = 0; i < 4; ++i) out[i] = c[i];
+}
+// uniform on (-1, 1) from the top 24 bits (exact in fp32 and fp64)
+double unit_sym(uint32_t x) { return ((double)(x >> 8) + 0.5) * (2.0 / 16777216.0) - 1.0; }
+// R27: target of env `env` at step `step`: c_s += s_t (u0, u1, u2), R_s <- exp([s_r (u3, u4, u5)]) R_s
+// with u from Philox4x32-10(key = seed, counter = (env, step_lo, step_hi, 0 / 1))
+void perturb_target(uint64_t seed, uint64_t step, uint64_t env, double s_t, double s_r, V3* cs, M3* Rs) {
+  const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t a[4], b[4];
+  const uint32_t c0[4] = {(uint32_t)env, (uint32_t)step, (uint32_t)(step >> 32), 0u};
+  const uint32_t c1[4] = {(uint32_t)env, (uint32_t)step, (uint32_t)(step >> 32), 1u};
+  philox4x32_10(c0, key, a);
+  philox4x32_10(c1, key, b);
+  const double u[6] = {unit_sym(a[0]), unit_sym(a[1]), unit_sym(a[2]), unit_sym(a[3]), unit_sym(b[0]), unit_sym(b[1])};
+  *cs = add(*cs, V3{s_t * u[0], s_t * u[1], s_t * u[2]});
+  *Rs = matmul(so3_exp(V3{s_r * u[3], s_r * u[4], s_r * u[5]}), *Rs);
+}
 
 // ---------------------------------------------------------------------------
 // setup (DESIGN.md §Oracle "precompute")
@@ -971,13 +1007,17 @@ void build_anchors(const Problem& P, Step& S, const State& s, const std::vector<
   }
 }
 
-void env_step(const Problem& P, Env& E, const double* target7, double h) {
+void env_step(const Problem& P, Env& E, const double* target7, double h, const Oracle* O = nullptr,
+              int64_t env_id = 0) {
   Step S;
   S.h = h;
   S.kappa = h * h * P.kappa_phys;  // kappa = h^2 kappa_phys (R4)
   S.eps = P.eps_v * h;             // eps = eps_v h
   S.cs = {target7[0], target7[1], target7[2]};
   S.Rs = quat_to_R(target7);
+  if (O && (O->noise_t != 0 || O->noise_r != 0))
+    perturb_target(O->noise_seed, O->step_count, (uint64_t)(env_id + O->env_offset), O->noise_t, O->noise_r, &S.cs,
+                   &S.Rs);
   E.flags = 0;
   E.trace.clear();
   // large-motion flag (diagnostic only)
@@ -1220,10 +1260,16 @@ void or_step(void* h, const double* targets7, double dt, int n_threads, int env0
   std::vector<std::thread> th;
   for (int t = 0; t < n_threads; ++t)
     th.emplace_back([=]() {
-      for (int e = env0 + t; e < env0 + n; e += n_threads) env_step(O->P, O->env[e], targets7 + 7 * e, dt);
+      for (int e = env0 + t; e < env0 + n; e += n_threads) env_step(O->P, O->env[e], targets7 + 7 * e, dt, O, e);
     });
   for (auto& x : th) x.join();
+  O->step_count += 1;
 }
+void or_set_pose_noise(void* h, double sigma_t, double sigma_r, uint64_t seed, int64_t env_offset) {
+  Oracle* O = (Oracle*)h;
+  O->noise_t = sigma_t; O->noise_r = sigma_r; O->noise_seed = seed; O->env_offset = env_offset;
+}
+void or_philox(const uint32_t* ctr, const uint32_t* key, uint32_t* out) { philox4x32_10(ctr, key, out); }
 void or_env_status(void* h, int env, double* out) {  // iters, flags, |Pg|, dmin, pose residual
   Env& E = ((Oracle*)h)->env[env];
   out[0] = E.iters; out[1] = E.flags; out[2] = E.pg; out[3] = E.dmin; out[4] = E.pose_res;

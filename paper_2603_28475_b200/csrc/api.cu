@@ -43,6 +43,7 @@ struct tac_sim {
   // per-env material (tac_set_env_material): create-time base and the current values
   double E0 = 0, nu0 = 0, rho0 = 0, lbar = 0;
   bool kappa_fixed = false;
+  unsigned long long step_count = 0;  // tac_step calls so far (pose-noise counter, R27)
   std::vector<double> thE, thNu, thRho, thMu;
 };
 
@@ -328,7 +329,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
       int a = I.tris[3 * i + k], b = I.tris[3 * i + (k + 1) % 3];
       ies.insert({std::min(a, b), std::max(a, b)});
     }
-  tac_sim* sim = new tac_sim;
+  tac_sim* sim = new tac_sim();  // value-initialised: every Dev field starts at 0
   sim->device = info->device;
   if (cudaSetDevice(info->device) != cudaSuccess) {
     delete sim;
@@ -912,7 +913,7 @@ tac_status tac_step(tac_sim* sim, const float* target_poses, float dt, void* str
   double h = dt;
   g_launches = 0;
   g_prof = sim->prof;
-  launch_step_setup(d, target_poses, h, s);  // a1
+  launch_step_setup(d, target_poses, h, sim->step_count++, s);  // a1
   launch_broadphase(d, false, s);            // a2
   launch_anchors(d, h, s);                   // a3
   int K = sim->fixed_iters > 0 ? sim->fixed_iters : sim->max_iters;
@@ -990,6 +991,17 @@ tac_status tac_set_env_material(tac_sim* sim, const double* E, const double* nu,
   }
   cudaSetDevice(sim->device);
   if ((st = upload_env_material(sim))) { sim->err = "tac_set_env_material: upload failed"; return st; }
+  return TAC_OK;
+}
+
+tac_status tac_set_pose_noise(tac_sim* sim, double sigma_t, double sigma_r, uint64_t seed, int64_t env_offset) {
+  tac_status st = check_sim(sim);
+  if (st) return st;
+  if (!(sigma_t >= 0) || !(sigma_r >= 0) || env_offset < 0) { sim->err = "tac_set_pose_noise: bad arguments"; return TAC_EINVAL; }
+  sim->d.noise_t = sigma_t;
+  sim->d.noise_r = sigma_r;
+  sim->d.noise_seed = seed;
+  sim->d.env_offset = env_offset;
   return TAC_OK;
 }
 
@@ -1197,7 +1209,7 @@ tac_status tac_debug_eval(tac_sim* sim, int32_t env, const double* u_t, const do
   float* dp = nullptr;
   CK(cudaMalloc(&dp, sizeof(float) * poses.size()));
   CK(cudaMemcpy(dp, poses.data(), sizeof(float) * poses.size(), cudaMemcpyHostToDevice));
-  launch_step_setup(d, dp, dt, 0);
+  launch_step_setup(d, dp, dt, 0ull, 0);
   CK(cudaDeviceSynchronize());
   cudaFree(dp);
   std::vector<EnvS> es(d.E);

@@ -129,6 +129,9 @@ struct Dev {
   float* emat;           // [4][Es] per-env material: mu, lambda', mass scale rho_e / rho_0,
                          // elastic-diagonal scale mu_e / mu_0 (mass and sum V mu |b|^2 are stored for env 0's material)
   double* edbl;          // [2][Es] per-env kappa_phys, mu_f
+  double noise_t, noise_r;  // per-step target pose noise amplitudes (R27; 0 = off)
+  unsigned long long noise_seed;
+  long long env_offset;  // global id of env 0 (sharded ranks draw the streams of their global envs)
   double rho_max, dhat, kappa_phys, eps_v, tol_x, k_t, k_r, f_max, t_max, ccd_s, bp_margin, c1, eps_E, mu_f;
   int beta_rule, precond, max_halv, stagnation, fixed_iters;
   // element tiles
@@ -152,7 +155,7 @@ struct Dev {
 };
 
 // ---- launchers (kernels.cu) ----
-void launch_step_setup(const Dev& d, const float* poses, double h, cudaStream_t s);
+void launch_step_setup(const Dev& d, const float* poses, double h, unsigned long long step, cudaStream_t s);
 void launch_vert_setup(const Dev& d, double h, cudaStream_t s);
 void launch_broadphase(const Dev& d, bool masked, cudaStream_t s);
 void launch_anchors(const Dev& d, double h, cudaStream_t s);

@@ -392,13 +392,42 @@ __device__ __forceinline__ bool far_cert(const d3* z, int na, double dhat, doubl
 }
 
 // ------------------------------------------------------------------ a1: step setup
-__global__ void k_step_setup(Dev d, const float* poses) {
+// Philox4x32-10 (Salmon et al., SC'11): counter-based, so env e's noise at step k is a
+// pure function of (seed, e, k) -- the same stream in the oracle's own implementation
+__device__ void philox4x32_10(uint4 c, uint2 k, unsigned* out) {
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) { k.x += 0x9E3779B9u; k.y += 0xBB67AE85u; }
+    const unsigned lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const unsigned lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+  }
+  out[0] = c.x; out[1] = c.y; out[2] = c.z; out[3] = c.w;
+}
+__device__ __forceinline__ double unit_sym(unsigned x) { return ((double)(x >> 8) + 0.5) * (2.0 / 16777216.0) - 1.0; }
+
+// a1: step setup.  R27: with pose noise on, the target of env e at step k is perturbed
+// c_s += s_t (u0, u1, u2), R_s <- exp([s_r (u3, u4, u5)]) R_s, u = Philox(seed; e, k, 0 / 1)
+__global__ void k_step_setup(Dev d, const float* poses, unsigned long long step) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= d.E) return;
   EnvS& s = d.es[e];
   const float* q = poses + 7 * e;
   s.cs[0] = q[0]; s.cs[1] = q[1]; s.cs[2] = q[2];
   quat_R(q, s.Rs);
+  if (d.noise_t != 0.0 || d.noise_r != 0.0) {
+    const unsigned long long gid = (unsigned long long)(e + d.env_offset);
+    const uint2 key = make_uint2((unsigned)d.noise_seed, (unsigned)(d.noise_seed >> 32));
+    unsigned a[4], b[4];
+    philox4x32_10(make_uint4((unsigned)gid, (unsigned)step, (unsigned)(step >> 32), 0u), key, a);
+    philox4x32_10(make_uint4((unsigned)gid, (unsigned)step, (unsigned)(step >> 32), 1u), key, b);
+    s.cs[0] += d.noise_t * unit_sym(a[0]);
+    s.cs[1] += d.noise_t * unit_sym(a[1]);
+    s.cs[2] += d.noise_t * unit_sym(a[2]);
+    double Q[9], Rn[9];
+    rodrigues(mk(d.noise_r * unit_sym(a[3]), d.noise_r * unit_sym(b[0]), d.noise_r * unit_sym(b[1])), Q);
+    mm3(Q, s.Rs, Rn);
+    for (int i = 0; i < 9; ++i) s.Rs[i] = Rn[i];
+  }
   for (int i = 0; i < 3; ++i) { s.c[i] = s.ct[i]; s.cp[i] = s.ct[i]; }
   for (int i = 0; i < 9; ++i) { s.R[i] = s.Rt[i]; s.Rp[i] = s.Rt[i]; }
   double RRt[9];
@@ -2285,8 +2314,8 @@ static dim3 sgrid(const Dev& d) {  // staged contact kernels: chunks per env
     ++g_launches;                     \
   } while (0)
 
-void launch_step_setup(const Dev& d, const float* poses, double h, cudaStream_t s) {
-  LAUNCHK(KID_STEP_SETUP, s, (k_step_setup<<<eblocks(d), 128, 0, s>>>(d, poses)));
+void launch_step_setup(const Dev& d, const float* poses, double h, unsigned long long step, cudaStream_t s) {
+  LAUNCHK(KID_STEP_SETUP, s, (k_step_setup<<<eblocks(d), 128, 0, s>>>(d, poses, step)));
   LAUNCHK(KID_VERT_SETUP, s, (k_vert_setup<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d, (float)h)));
 }
 void launch_vert_setup(const Dev& d, double h, cudaStream_t s) {

@@ -75,6 +75,7 @@ def lib():
         L.tac_env_status.argtypes = [vp, vp, vp, vp, vp]
         L.tac_set_env_material.argtypes = [vp, _dp, _dp, _dp, _dp]
         L.tac_marker_sqerr.argtypes = [vp, vp, vp, C.c_int32, vp]
+        L.tac_set_pose_noise.argtypes = [vp, C.c_double, C.c_double, C.c_uint64, C.c_int64]
         L.tac_info.argtypes = [vp, _ip]
         L.tac_last_launch_count.argtypes = [vp]
         L.tac_last_launch_count.restype = C.c_int64
@@ -101,7 +102,7 @@ EXPORTED = ["tac_create", "tac_step", "tac_markers", "tac_reset", "tac_env_statu
             "tac_last_launch_count", "tac_destroy", "tac_last_error", "tac_get_state", "tac_set_state",
             "tac_debug_broadphase", "tac_debug_surface", "tac_debug_marker_map", "tac_debug_eval",
             "tac_profile_enable", "tac_profile_read", "tac_profile_kernel_name", "tac_env_stats",
-            "tac_set_env_material", "tac_marker_sqerr"]
+            "tac_set_env_material", "tac_marker_sqerr", "tac_set_pose_noise"]
 N_KERNEL_IDS = 24
 
 
@@ -207,6 +208,11 @@ class TacSim:
         assert out.is_cuda and out.is_contiguous() and out.numel() >= self.n_envs * self.nm * ncomp
         self._check(lib().tac_markers(self.h, C.c_void_p(out.data_ptr()), ncomp, _stream_ptr(stream)), "tac_markers")
         return out
+
+    def set_pose_noise(self, sigma_t, sigma_r, seed, env_offset=0):
+        """Per-step target pose noise (R27): translation amplitude [m], rotation [rad]."""
+        self._check(lib().tac_set_pose_noise(self.h, float(sigma_t), float(sigma_r), int(seed), int(env_offset)),
+                    "tac_set_pose_noise")
 
     def marker_sqerr(self, ref, acc, stream=None):
         """acc[e] += |markers(e) - ref[e]|^2 (calibration loss term, Eq. 6); ref [E, nm, ncomp] fp32,

@@ -413,3 +413,63 @@ def test_c5_stress_bench_config_sampled(torch_cuda):
         assert np.linalg.norm(gpu["g"][free] - ref["g"][free]) <= 1e-5 * np.linalg.norm(ref["g"][free])
         assert np.abs(gpu["D"][free] - ref["D"][free]).max() <= 1e-5 * np.abs(ref["D"][free]).max()
         assert abs(gpu["E"] - ref["E"]) <= 1e-5 * abs(ref["E"])
+
+
+# ---------------------------------------------------------------- pose noise (R27)
+def test_pose_noise_streams_match_oracle(torch_cuda):
+    """Free indenter: each step ends at the perturbed target, so the GPU's converged pose
+    equals the oracle's to far below the noise amplitude -- both implementations of
+    Philox4x32-10 and of the perturbation draw the same stream."""
+    import torch
+    s = w.scene_c1(n_envs=40, steps=3)
+    s.init_poses[:, 2] = 3e-3 + 5e-3
+    s.poses[:, :, 2] = 3e-3 + 5e-3
+    s.params.tol_x = 1e-12
+    st, sr, seed = 2e-5, 1e-3, 1234
+    sim = _sim(s)
+    sim.set_pose_noise(st, sr, seed)
+    o = O.Oracle(s)
+    o.set_pose_noise(st, sr, seed)
+    for k in range(3):
+        sim.step(torch.tensor(s.poses[k], dtype=torch.float32, device="cuda").contiguous(), s.dt)
+        o.step(s.poses[k], threads=8)
+        for e in (0, 17, 39):
+            _, _, c_g, R_g = sim.get_state(e)
+            _, _, c_o, R_o = o.get_state(e)
+            assert np.abs(c_g - c_o).max() < 1e-3 * st, (k, e)
+            assert np.abs(R_g - R_o).max() < 1e-3 * sr, (k, e)
+            assert np.abs(c_g - s.poses[k][e][:3]).max() > 1e-3 * st  # the noise is applied
+
+
+def test_pose_noise_contact_parity_and_env_offset(torch_cuda):
+    """Contact steps with noise converge to the oracle's states; a simulator holding envs
+    [1, 3) with env_offset = 1 draws the same streams as the full batch."""
+    import copy
+    import torch
+    s = w.scene_small_peg(n_envs=3, n_steps=3)
+    st, sr, seed = 3e-5, 2e-3, 99
+    s.params.tol_x = 1e-9
+    s.params.max_iters = 8000
+    s.params.stagnation = 3000
+    sim = _sim(s)
+    sim.set_pose_noise(st, sr, seed)
+    p_or = w.Params(**{**s.params.__dict__})
+    p_or.tol_x = 1e-11
+    o = O.Oracle(s, params=p_or)
+    o.set_pose_noise(st, sr, seed)
+    sub = copy.deepcopy(s)
+    sub.init_poses = s.init_poses[1:]
+    sub.poses = s.poses[:, 1:]
+    sim2 = _sim(sub)
+    sim2.set_pose_noise(st, sr, seed, env_offset=1)
+    for k in range(3):
+        tgt = torch.tensor(s.poses[k], dtype=torch.float32, device="cuda").contiguous()
+        sim.step(tgt, s.dt)
+        sim2.step(tgt[1:].contiguous(), s.dt)
+        o.step(s.poses[k], threads=3)
+    mk = sim.markers().cpu().numpy()
+    mk2 = sim2.markers().cpu().numpy()
+    for e in range(3):
+        _assert_parity(s, sim, o, mk, e)
+    scale = np.abs(mk[1:]).max()
+    assert np.abs(mk2 - mk[1:]).max() <= 1e-3 * scale

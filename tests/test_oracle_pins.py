@@ -237,3 +237,53 @@ def test_so3_and_quaternion():
         assert np.allclose(l, wv, rtol=1e-9, atol=1e-15)
         q = rng.standard_normal(4)
         assert np.allclose(O.quat_to_R(np.concatenate([[0, 0, 0], q])), quat_R(q), atol=1e-15)
+
+
+# ---------------------------------------------------------------- pose noise (R27)
+def _kat():
+    import os
+    rows = []
+    for line in open(os.path.join(os.path.dirname(__file__), "golden", "philox4x32_10_kat.txt")):
+        if line.strip() and not line.startswith("#"):
+            v = [int(x, 16) for x in line.split()]
+            rows.append((v[:4], v[4:6], v[6:10]))
+    return rows
+
+
+def test_philox_known_answers():
+    rows = _kat()
+    assert len(rows) == 3
+    for ctr, key, out in rows:
+        assert [int(x) for x in O.philox4x32_10(ctr, key)] == out
+
+
+def test_pose_noise_statistics_and_determinism():
+    """Free indenter (no contact): one step ends at the perturbed target, so c - c_target
+    samples s_t * U(-1, 1)^3 and the rotation vector of R R_target^T samples s_r *
+    U(-1, 1)^3 (scipy's rotation-vector map, independent of the oracle); per-env streams
+    are reproducible and distinct."""
+    from scipy.spatial.transform import Rotation
+    s = w.scene_c1(n_envs=96)
+    R0 = 3e-3
+    s.init_poses[:, 2] = R0 + 5e-3
+    s.poses[:, :, 2] = R0 + 5e-3
+    s.params.tol_x = 1e-12
+    st, sr = 2e-5, 1e-3
+    outs = []
+    for seed in (7, 7, 8):
+        o = O.Oracle(s)
+        o.set_pose_noise(st, sr, seed)
+        o.step(s.poses[0], threads=8)
+        dc, rv = [], []
+        for e in range(s.n_envs):
+            _, _, c, R = o.get_state(e)
+            dc.append(c - s.poses[0][e][:3])
+            rv.append(Rotation.from_matrix(R @ O.quat_to_R(s.poses[0][e]).T).as_rotvec())
+        outs.append((np.array(dc), np.array(rv)))
+    (dc, rv), (dc2, rv2), (dc3, _) = outs
+    assert np.array_equal(dc, dc2) and np.array_equal(rv, rv2) and not np.allclose(dc, dc3)
+    assert len({tuple(np.round(d / st, 9)) for d in dc}) == s.n_envs
+    for x, sig in ((dc, st), (rv, sr)):
+        assert np.abs(x).max() <= sig * (1 + 1e-5)
+        assert abs(x.mean()) < 0.15 * sig
+        assert abs((x ** 2).mean() / (sig ** 2 / 3) - 1) < 0.2
