@@ -2302,6 +2302,9 @@ static dim3 cgrid(const Dev& d) {
   return dim3(nb, d.E);
 }
 static int eblocks(const Dev& d) { return (d.E + 127) / 128; }
+// per-env control kernels (long serial fp64 chains per thread): one warp per block spreads
+// the envs over E / 32 SMs instead of E / 128
+static int eblocks32(const Dev& d) { return (d.E + 31) / 32; }
 static dim3 sgrid(const Dev& d) {  // staged contact kernels: chunks per env
   int nb = std::max(1, std::min(16, 2368 / std::max(1, d.E)));
   return dim3(nb, d.E);
@@ -2315,7 +2318,7 @@ static dim3 sgrid(const Dev& d) {  // staged contact kernels: chunks per env
   } while (0)
 
 void launch_step_setup(const Dev& d, const float* poses, double h, unsigned long long step, cudaStream_t s) {
-  LAUNCHK(KID_STEP_SETUP, s, (k_step_setup<<<eblocks(d), 128, 0, s>>>(d, poses, step)));
+  LAUNCHK(KID_STEP_SETUP, s, (k_step_setup<<<eblocks32(d), 32, 0, s>>>(d, poses, step)));
   LAUNCHK(KID_VERT_SETUP, s, (k_vert_setup<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d, (float)h)));
 }
 void launch_vert_setup(const Dev& d, double h, cudaStream_t s) {
@@ -2352,11 +2355,11 @@ void launch_eval(const Dev& d, double h, cudaStream_t s) {
   LAUNCHK(KID_CONTACT_NEAR_IG, s, (k_contact_near<1><<<cgrid(d), 128, 0, s>>>(d, kap)));
   LAUNCHK(KID_CONTACT_NEAR_EE, s, (k_contact_near<2><<<cgrid(d), 128, 0, s>>>(d, kap)));
   LAUNCHK(KID_CONTACT_FRICTION, s, (k_contact_friction<<<cgrid(d), 128, 0, s>>>(d, d.eps_v * h)));
-  LAUNCHK(KID_ACCEPT, s, (k_accept<<<eblocks(d), 128, 0, s>>>(d, h)));
+  LAUNCHK(KID_ACCEPT, s, (k_accept<<<eblocks32(d), 32, 0, s>>>(d, h)));
 }
 void launch_direction(const Dev& d, cudaStream_t s) {
   LAUNCHK(KID_DIR_REDUCE, s, (k_dir_reduce<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d)));
-  LAUNCHK(KID_DIR_SCALAR, s, (k_dir_scalar<<<eblocks(d), 128, 0, s>>>(d)));
+  LAUNCHK(KID_DIR_SCALAR, s, (k_dir_scalar<<<eblocks32(d), 32, 0, s>>>(d)));
   LAUNCHK(KID_DIR_APPLY, s, (k_dir_apply<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d)));
 }
 void launch_curvature(const Dev& d, double h, cudaStream_t s) {
@@ -2370,14 +2373,14 @@ void launch_curvature(const Dev& d, double h, cudaStream_t s) {
 }
 void launch_alpha(const Dev& d, double h, cudaStream_t s) {
   cudaMemsetAsync(d.nreb, 0, sizeof(int), s);
-  LAUNCHK(KID_ALPHA, s, (k_alpha<<<eblocks(d), 128, 0, s>>>(d, h, 1)));
+  LAUNCHK(KID_ALPHA, s, (k_alpha<<<eblocks32(d), 32, 0, s>>>(d, h, 1)));
   launch_broadphase(d, true, s);
   LAUNCHK(KID_CCD, s, (k_ccd_list<<<4 * 148, 128, 0, s>>>(d)));
-  LAUNCHK(KID_ALPHA, s, (k_alpha<<<eblocks(d), 128, 0, s>>>(d, h, 2)));
+  LAUNCHK(KID_ALPHA, s, (k_alpha<<<eblocks32(d), 32, 0, s>>>(d, h, 2)));
 }
 void launch_finalize(const Dev& d, double h, cudaStream_t s) {
   LAUNCHK(KID_FIN_VERT, s, (k_finalize_vert<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d, (float)(1.0 / h))));
-  LAUNCHK(KID_FIN_ENV, s, (k_finalize_env<<<eblocks(d), 128, 0, s>>>(d)));
+  LAUNCHK(KID_FIN_ENV, s, (k_finalize_env<<<eblocks32(d), 32, 0, s>>>(d)));
 }
 void launch_markers(const Dev& d, float* out, int ncomp, cudaStream_t s) {
   int n = d.E * d.nm;
