@@ -860,6 +860,18 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     cudaMemcpy(chk.data(), d.es, sizeof(EnvS) * d.E, cudaMemcpyDeviceToHost);
     for (int e = 0; e < d.E; ++e)
       if (chk[e].flags & 8) { rc = TAC_EINVAL; sim->err = "indenter touches the gel at its initial pose (env " + std::to_string(e) + ")"; goto fail; }
+    {  // deep intersections: a gel surface edge crossing an indenter triangle
+      int* dhit = nullptr;
+      std::vector<int> hit(d.E, 0);
+      if (cudaMalloc(&dhit, sizeof(int) * d.E) != cudaSuccess) { rc = TAC_ENOMEM; goto fail; }
+      cudaMemset(dhit, 0, sizeof(int) * d.E);
+      launch_intersect_check(d, dhit, 0);
+      cudaError_t ce = cudaMemcpy(hit.data(), dhit, sizeof(int) * d.E, cudaMemcpyDeviceToHost);
+      cudaFree(dhit);
+      if (ce != cudaSuccess) { rc = TAC_ECUDA; sim->err = "initial intersection check failed"; goto fail; }
+      for (int e = 0; e < d.E; ++e)
+        if (hit[e]) { rc = TAC_EINVAL; sim->err = "indenter intersects the gel at its initial pose (env " + std::to_string(e) + ")"; goto fail; }
+    }
     // restore the clean initial state
     if (cudaMemcpy(d.es, es.data(), sizeof(EnvS) * d.E, cudaMemcpyHostToDevice) != cudaSuccess) { rc = TAC_ECUDA; goto fail; }
     cudaMemset(d.acc, 0, sizeof(double) * kNAcc * d.Es);

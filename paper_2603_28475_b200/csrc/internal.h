@@ -164,6 +164,7 @@ void launch_direction(const Dev& d, cudaStream_t s);
 void launch_curvature(const Dev& d, double h, cudaStream_t s);
 void launch_alpha(const Dev& d, double h, cudaStream_t s);
 void launch_finalize(const Dev& d, double h, cudaStream_t s);
+void launch_intersect_check(const Dev& d, int* hit, cudaStream_t s);  // tac_create validation
 void launch_markers(const Dev& d, float* out, int ncomp, cudaStream_t s);
 void launch_marker_sqerr(const Dev& d, const float* ref, double* acc, int ncomp, cudaStream_t s);
 void launch_reset(const Dev& d, const unsigned char* mask, const float* poses, cudaStream_t s);

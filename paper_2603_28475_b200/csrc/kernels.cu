@@ -630,6 +630,54 @@ __global__ void __launch_bounds__(128) k_broadphase(Dev d, double r, unsigned lo
   if (over) d.es[e].ncand_over = 1;
 }
 
+// ---- initial-pose validation (tac_create): does any gel surface edge cross an indenter
+// triangle?  Unsigned distances cannot see a deep intersection (crossing surfaces have
+// small positive distances), so tac_create also runs this fp64 segment-triangle test on
+// the wide triangle BVH in the body frame.  (An indenter spike piercing one gel triangle
+// without any gel edge crossing an indenter triangle is not detected.)
+__device__ __forceinline__ double orient3(d3 a, d3 b, d3 c, d3 p) { return dot(cross(b - a, c - a), p - a); }
+__global__ void __launch_bounds__(128) k_intersect_check(Dev d, int* hit) {
+  const int e = blockIdx.y, i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= d.E || i >= d.nse) return;
+  const EnvS& s = d.es[e];
+  double R[9], c[3];
+  for (int k = 0; k < 9; ++k) R[k] = s.R[k];
+  for (int k = 0; k < 3; ++k) c[k] = s.c[k];
+  const int2 ed = d.se[i];
+  const d3 x0 = gel_pos(d, d.u, ed.x, e), x1 = gel_pos(d, d.u, ed.y, e);
+  const d3 p0 = mk(to_body_exact(R, c, x0, 0), to_body_exact(R, c, x0, 1), to_body_exact(R, c, x0, 2));
+  const d3 p1 = mk(to_body_exact(R, c, x1, 0), to_body_exact(R, c, x1, 1), to_body_exact(R, c, x1, 2));
+  const float qlo[3] = {(float)fmin(p0.x, p1.x) - 1e-6f, (float)fmin(p0.y, p1.y) - 1e-6f, (float)fmin(p0.z, p1.z) - 1e-6f};
+  const float qhi[3] = {(float)fmax(p0.x, p1.x) + 1e-6f, (float)fmax(p0.y, p1.y) + 1e-6f, (float)fmax(p0.z, p1.z) + 1e-6f};
+  int stack[48];
+  int sp = 0;
+  stack[sp++] = 0;  // virtual root of the triangle BVH
+  while (sp > 0) {
+    const float4* wn = d.bvhw + 4 * stack[--sp];
+    const float4 w0 = __ldg(wn), w1 = __ldg(wn + 1), w2 = __ldg(wn + 2), w3 = __ldg(wn + 3);
+    for (int chd = 0; chd < 2; ++chd) {
+      const float lx = chd ? w1.z : w0.x, ly = chd ? w1.w : w0.y, lz = chd ? w2.x : w0.z;
+      const float hx = chd ? w2.y : w0.w, hy = chd ? w2.z : w1.x, hz = chd ? w2.w : w1.y;
+      if (lx > qhi[0] || hx < qlo[0] || ly > qhi[1] || hy < qlo[1] || lz > qhi[2] || hz < qlo[2]) continue;
+      const int rf = __float_as_int(chd ? w3.y : w3.x);
+      if (rf >= 0) { stack[sp++] = rf; continue; }
+      const int code = -1 - rf, q0 = code >> 3, nq = code & 7;
+      for (int k = 0; k < nq; ++k) {
+        const int prim = __float_as_int(__ldg(d.bvh_pbox + 2 * (q0 + k)).w);
+        const int4 t = d.it[prim];
+        const d3 a = ind_body(d, t.x), b = ind_body(d, t.y), cc = ind_body(d, t.z);
+        const double s0 = orient3(a, b, cc, p0), s1 = orient3(a, b, cc, p1);
+        if (!((s0 < 0 && s1 > 0) || (s0 > 0 && s1 < 0))) continue;  // both ends on one side
+        const double o0 = orient3(p0, p1, a, b), o1 = orient3(p0, p1, b, cc), o2 = orient3(p0, p1, cc, a);
+        if ((o0 >= 0 && o1 >= 0 && o2 >= 0) || (o0 <= 0 && o1 <= 0 && o2 <= 0)) {
+          atomicExch(hit + e, 1);
+          return;
+        }
+      }
+    }
+  }
+}
+
 // rebuilds inside the loop: only the envs k_alpha listed; work items = (listed env,
 // 32-primitive chunk) per WARP over a fixed grid, so cost follows the actual rebuild count
 // and no warp waits for another
@@ -2332,6 +2380,9 @@ void launch_broadphase(const Dev& d, bool masked, cudaStream_t s) {
   int ntot = d.nsv + d.nse + d.nst;
   int nb = std::max(1, std::min((ntot + 127) / 128, 4736 / std::max(1, d.E)));
   LAUNCHK(KID_BROADPHASE, s, (k_broadphase<<<dim3(nb, d.E), 128, 0, s>>>(d, d.dhat + d.bp_margin, nullptr, nullptr, 0)));
+}
+void launch_intersect_check(const Dev& d, int* hit, cudaStream_t s) {
+  LAUNCHK(KID_OTHER, s, (k_intersect_check<<<dim3((d.nse + 127) / 128, d.E), 128, 0, s>>>(d, hit)));
 }
 void launch_anchors(const Dev& d, double h, cudaStream_t s) {
   LAUNCHK(KID_ANCHORS, s, (k_anchors<<<cgrid(d), 128, 0, s>>>(d, h * h)));

@@ -1,0 +1,120 @@
+"""Edge cases of the C ABI on the GPU: reset, capacity overflow, refused
+infeasible poses, three-component markers, status flags and per-env statistics."""
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as w
+from helpers import c1_press_scene
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    if not t.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return t
+
+
+def _sim(scene, **kw):
+    import paper_2603_28475_b200 as P
+    return P.TacSim.from_scene(scene, **kw)
+
+
+def _poses(torch, p):
+    return torch.tensor(p, dtype=torch.float32, device="cuda").contiguous()
+
+
+def test_reset_restores_rest_state_and_pose(torch):
+    """tac_reset: masked envs go back to rest (u = v = 0) at the given pose and then
+    evolve like fresh envs; unmasked envs are untouched."""
+    s = w.scene_small_peg(n_envs=4, n_steps=3)
+    s.params.fixed_iters = 40
+    sim = _sim(s)
+    for k in range(2):
+        sim.step(_poses(torch, s.poses[k]), s.dt)
+    before = [sim.get_state(e) for e in range(4)]
+    mask = torch.tensor([0, 1, 0, 1], dtype=torch.uint8, device="cuda")
+    sim.reset(mask, _poses(torch, s.init_poses))
+    torch.cuda.synchronize()
+    for e in range(4):
+        u, v, c, R = sim.get_state(e)
+        if e in (1, 3):
+            assert np.all(u == 0) and np.all(v == 0)
+            assert np.allclose(c, s.init_poses[e][:3], atol=1e-7)
+            assert np.allclose(R, O.quat_to_R(s.init_poses[e]), atol=1e-6)
+        else:
+            for a, b in zip((u, v, c, R), before[e]):
+                assert np.array_equal(a, b)
+    # a reset env steps like the same env of a fresh simulator
+    sim.step(_poses(torch, s.poses[0]), s.dt)
+    fresh = _sim(s)
+    fresh.step(_poses(torch, s.poses[0]), s.dt)
+    m1, m2 = sim.markers().cpu().numpy(), fresh.markers().cpu().numpy()
+    scale = max(np.abs(m2[1]).max(), 1e-9)
+    assert np.abs(m1[1] - m2[1]).max() <= 1e-4 * scale + 1e-12
+
+
+def test_candidate_overflow_is_flagged_not_fatal(torch):
+    """A candidate capacity far below the contact's needs sets flag 32 (overflow) and the
+    step still returns finite fields."""
+    s = c1_press_scene(mu_f=1.0, steps=3, depth=0.3e-3)
+    s.params.max_candidates = 16
+    s.params.fixed_iters = 30
+    sim = _sim(s)
+    for k in range(3):
+        sim.step(_poses(torch, s.poses[k]), s.dt)
+    it, pg, fl = sim.env_status()
+    assert int(fl[0]) & 32
+    assert torch.isfinite(sim.markers()).all()
+
+
+def test_initial_intersection_is_refused(torch):
+    import paper_2603_28475_b200 as P
+    s = w.scene_c1()
+    for z in (2.0e-3, 3.0e-3 - 0.1e-3):  # sphere of radius 3 mm 1 mm / 0.1 mm into the pad
+        s.init_poses[0, 2] = z
+        with pytest.raises(P.TacError, match="intersects|touches"):
+            _sim(s)
+    s.init_poses[0, 2] = 3.0e-3 + 0.05e-3  # 50 um above: accepted
+    _sim(s)
+
+
+def test_three_component_markers_match_oracle(torch):
+    """ncomp = 3 adds the normal component u_m . n (row a10)."""
+    s = c1_press_scene(mu_f=1.0, steps=2, depth=0.2e-3)
+    s.params.tol_x = 1e-9
+    sim = _sim(s)
+    o = O.Oracle(s, params=w.Params(**{**s.params.__dict__, "tol_x": 1e-11}))
+    for k in range(2):
+        sim.step(_poses(torch, s.poses[k]), s.dt)
+        o.step(s.poses[k])
+    m3 = sim.markers(ncomp=3).cpu().numpy()[0]
+    m2 = sim.markers(ncomp=2).cpu().numpy()[0]
+    r3 = o.markers(0, ncomp=3)
+    assert np.array_equal(m3[:, :2], m2)
+    assert np.abs(r3[:, 2]).max() > 0
+    assert np.abs(m3 - r3).max() <= 1e-3 * np.abs(r3).max()
+
+
+def test_status_flags_and_stats(torch):
+    """max_iters reached -> flag 2 without flag 1; converged -> flag 1; env_stats reports
+    the step's iterations, peak candidates and anchors consistently."""
+    s = c1_press_scene(mu_f=1.0, steps=2, depth=0.2e-3)
+    s.params.max_iters = 3
+    s.params.tol_x = 1e-14
+    sim = _sim(s)
+    sim.step(_poses(torch, s.poses[0]), s.dt)
+    it, pg, fl = sim.env_status()
+    assert int(it[0]) == 3 and int(fl[0]) & 2 and not int(fl[0]) & 1
+    s2 = c1_press_scene(mu_f=1.0, steps=2, depth=0.2e-3)
+    sim2 = _sim(s2)
+    for k in range(2):
+        sim2.step(_poses(torch, s2.poses[k]), s2.dt)
+    it, pg, fl = sim2.env_status()
+    assert int(fl[0]) & 1
+    st = sim2.env_stats().cpu().numpy()[0]
+    assert st[0] == int(it[0])  # iterations of the last step
+    assert st[1] >= 0 and st[2] >= 0 and st[3] >= 0
