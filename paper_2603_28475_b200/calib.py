@@ -7,9 +7,10 @@ and N indenter trajectories, theta* = argmin L (Eq. 7) by CMA-ES (Hansen 2006). 
 [0, 1] over Table params_range, popsize 12, 80 iterations.
 
 Host logic only: the CMA-ES update and the bookkeeping of which env evaluates which
-candidate.  One generation = one batch of popsize x N envs in ONE TacSim: every
-simulation step, every marker field and every loss term runs in libtac's kernels
-(tac_set_env_material, tac_reset, tac_step, tac_marker_sqerr).
+candidate.  One generation = one batch of popsize x N envs in ONE TacSim per indenter
+shape (the paper calibrates with several shapes): every simulation step, every
+marker field and every loss term runs in libtac's kernels (tac_set_env_material,
+tac_reset, tac_step, tac_marker_sqerr).
 """
 from __future__ import annotations
 
@@ -90,68 +91,95 @@ class CMAES:
         self.invsqrtC = (self.B / self.D) @ self.B.T
 
 
-class Calibrator:
-    """Evaluates Eq. 6 for a whole CMA-ES population in one batch.
+class _Part:
+    """One simulator of the calibration: one indenter shape, N trajectories x popsize."""
 
-    `scene` holds the N trajectories (scene.n_envs = N, poses [K][N][7]); the simulator
-    gets popsize x N envs, env j*N + i = candidate j on trajectory i."""
-
-    def __init__(self, scene, popsize=12, device=0, ncomp=2):
+    def __init__(self, scene, popsize, device, ncomp):
         import torch
         from .tac import TacSim
         self.N = scene.n_envs
         self.K = len(scene.poses)
         self.P = popsize
-        self.ncomp = ncomp
         self.dt = scene.dt
         big = copy.copy(scene)
         big.init_poses = np.tile(scene.init_poses, (popsize, 1))
         big.poses = np.tile(scene.poses, (1, popsize, 1))
         self.sim = TacSim.from_scene(big, device=device)
         dev = f"cuda:{device}"
-        self.torch = torch
-        self.dev = dev
         self.poses = torch.tensor(big.poses, dtype=torch.float32, device=dev).contiguous()
         self.init = torch.tensor(big.init_poses, dtype=torch.float32, device=dev).contiguous()
-        self.mask = torch.ones(self.P * self.N, dtype=torch.uint8, device=dev)
-        self.acc = torch.zeros(self.P * self.N, dtype=torch.float64, device=dev)
+        self.mask = torch.ones(popsize * self.N, dtype=torch.uint8, device=dev)
+        self.acc = torch.zeros(popsize * self.N, dtype=torch.float64, device=dev)
         self.ref = None
-        self.evals = 0
+        self.ncomp = ncomp
 
-    def _set_thetas(self, thetas):
+    def set_thetas(self, thetas):
         th = np.repeat(np.asarray(thetas, dtype=np.float64).reshape(-1, 4), self.N, axis=0)
         self.sim.set_env_material(E=th[:, 0], nu=th[:, 1], rho=th[:, 2], mu_f=th[:, 3])
 
+
+class Calibrator:
+    """Evaluates Eq. 6 for a whole CMA-ES population in one batch per indenter shape.
+
+    `scenes`: one scene or a list (one per indenter shape); each holds N
+    trajectories (scene.n_envs = N, poses [K][N][7]) and gets its own simulator with
+    popsize x N envs, env j*N + i = candidate j on trajectory i.  L(theta) is the mean of
+    |u_sim - u_ref|^2 over all frames of all trajectories of all shapes (Eq. 6)."""
+
+    def __init__(self, scenes, popsize=12, device=0, ncomp=2):
+        import torch
+        self.torch = torch
+        self.dev = f"cuda:{device}"
+        self.P = popsize
+        scenes = scenes if isinstance(scenes, (list, tuple)) else [scenes]
+        self.parts = [_Part(sc, popsize, device, ncomp) for sc in scenes]
+        self.evals = 0
+        # single-shape conveniences (tests, examples)
+        self.N, self.K, self.sim = self.parts[0].N, self.parts[0].K, self.parts[0].sim
+
+    @property
+    def ref(self):
+        return self.parts[0].ref
+
     def fields(self, theta):
-        """Marker fields [K][N][nm][ncomp] of the N trajectories at one theta (e.g. the
-        synthetic 'real' reference at a hidden theta_true)."""
-        torch = self.torch
-        self._set_thetas(np.tile(np.asarray(theta, dtype=np.float64), (self.P, 1)))
-        self.sim.reset(self.mask, self.init)
+        """Marker fields of every shape at one theta: [K][N][nm][ncomp] per shape (a list
+        for several shapes) -- e.g. the synthetic 'real' reference at a hidden theta_true."""
         out = []
-        for k in range(self.K):
-            self.sim.step(self.poses[k], self.dt)
-            out.append(self.sim.markers(ncomp=self.ncomp)[:self.N].clone())
-        return torch.stack(out)
+        for pt in self.parts:
+            pt.set_thetas(np.tile(np.asarray(theta, dtype=np.float64), (self.P, 1)))
+            pt.sim.reset(pt.mask, pt.init)
+            fr = []
+            for k in range(pt.K):
+                pt.sim.step(pt.poses[k], pt.dt)
+                fr.append(pt.sim.markers(ncomp=pt.ncomp)[:pt.N].clone())
+            out.append(self.torch.stack(fr))
+        return out if len(out) > 1 else out[0]
 
     def set_reference(self, ref):
-        """ref [K][N][nm][ncomp] (device) -> tiled over the population."""
-        torch = self.torch
-        ref = torch.as_tensor(ref, dtype=torch.float32, device=self.dev)
-        self.ref = ref.repeat(1, self.P, 1, 1).contiguous()
+        """ref: [K][N][nm][ncomp] per shape (a list for several shapes), tiled over the population."""
+        refs = ref if isinstance(ref, (list, tuple)) else [ref]
+        assert len(refs) == len(self.parts)
+        for pt, r in zip(self.parts, refs):
+            r = self.torch.as_tensor(r, dtype=self.torch.float32, device=self.dev)
+            pt.ref = r.repeat(1, self.P, 1, 1).contiguous()
 
     def losses(self, thetas):
         """Eq. 6 for each of the popsize candidate thetas ([P][4], physical units)."""
-        assert self.ref is not None, "set_reference first"
-        self._set_thetas(thetas)
-        self.sim.reset(self.mask, self.init)
-        self.acc.zero_()
-        for k in range(self.K):
-            self.sim.step(self.poses[k], self.dt)
-            self.sim.marker_sqerr(self.ref[k], self.acc)
+        total = None
+        count = 0
+        for pt in self.parts:
+            assert pt.ref is not None, "set_reference first"
+            pt.set_thetas(thetas)
+            pt.sim.reset(pt.mask, pt.init)
+            pt.acc.zero_()
+            for k in range(pt.K):
+                pt.sim.step(pt.poses[k], pt.dt)
+                pt.sim.marker_sqerr(pt.ref[k], pt.acc)
+            part = pt.acc.view(self.P, pt.N).sum(dim=1)
+            total = part if total is None else total + part
+            count += pt.K * pt.N
         self.evals += self.P
-        L = self.acc.view(self.P, self.N).sum(dim=1) / (self.K * self.N)
-        return L.cpu().numpy()
+        return (total / count).cpu().numpy()
 
     def run(self, iters=80, x0=None, sigma0=0.25, seed=0, callback=None):
         """CMA-ES over the normalised theta: popsize = self.P, `iters` generations."""

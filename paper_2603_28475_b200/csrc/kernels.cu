@@ -2461,15 +2461,18 @@ void launch_debug_broadphase(const Dev& d, double r, unsigned long long* out, in
   int ntot = d.nsv + d.nse + d.nst;
   LAUNCHK(KID_BROADPHASE, s, (k_broadphase<<<dim3((ntot + 127) / 128, d.E), 128, 0, s>>>(d, r, out, cnt, cap)));
 }
+constexpr int kContactSmemCap = 160 * 1024;  // staged contact kernels: largest dynamic shared size
 int contact_smem_bytes(int nsv, int niv) {
   size_t b = sizeof(double) * 3 * (size_t)niv + sizeof(float4) * (size_t)nsv + sizeof(int) * kNearCap;
-  return b <= 160 * 1024 ? (int)b : 0;
+  return b <= (size_t)kContactSmemCap ? (int)b : 0;
 }
 void kernels_init(int contact_smem) {
-  if (contact_smem > 0) {
-    cudaFuncSetAttribute(k_contact_classify_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, contact_smem);
-    cudaFuncSetAttribute(k_contact_curv_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, contact_smem);
-  }
+  // the attribute belongs to the kernel, not to a simulator: several simulators in one
+  // process (different meshes) share it, so it is set to the cap contact_smem_bytes
+  // enforces rather than to this simulator's size (occupancy follows the launch size)
+  (void)contact_smem;
+  cudaFuncSetAttribute(k_contact_classify_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, kContactSmemCap);
+  cudaFuncSetAttribute(k_contact_curv_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, kContactSmemCap);
   cudaFuncSetAttribute(k_elem_curv_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, kTiledCurvSmem);
 }
 int launches_per_iteration() { return 8 + 3 + 2 + 4; }

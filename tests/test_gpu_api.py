@@ -118,3 +118,18 @@ def test_status_flags_and_stats(torch):
     st = sim2.env_stats().cpu().numpy()[0]
     assert st[0] == int(it[0])  # iterations of the last step
     assert st[1] >= 0 and st[2] >= 0 and st[3] >= 0
+
+
+def test_several_simulators_in_one_process(torch):
+    """Kernel attributes are per kernel, not per simulator: a simulator created after a
+    smaller one keeps working, and both step correctly (calibration with several shapes)."""
+    big = w.scene_small_peg(n_envs=2, n_steps=2)
+    small = c1_press_scene(mu_f=1.0, steps=2, depth=0.2e-3)
+    for s in (big, small):
+        s.params.fixed_iters = 10
+    a = _sim(big)
+    b = _sim(small)
+    for k in range(2):
+        a.step(_poses(torch, big.poses[k]), big.dt)
+        b.step(_poses(torch, small.poses[k]), small.dt)
+    assert torch.isfinite(a.markers()).all() and torch.isfinite(b.markers()).all()

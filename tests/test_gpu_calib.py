@@ -49,3 +49,24 @@ def test_cmaes_recovers_hidden_theta(cal):
     assert abs(th[1] - TH_TRUE[1]) < 0.005, th
     assert abs(th[3] / TH_TRUE[3] - 1) < 0.05, th
     assert res["evals"] >= 80 * 12
+
+
+def test_cmaes_recovers_theta_over_several_indenter_shapes():
+    """Sphere, lying cylinder and cube (P:305 calibrates with several shapes), one simulator
+    each, Eq. 6 averaged over all frames and trajectories of all shapes."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2603_28475_b200.calib import Calibrator
+    c = Calibrator(w.scene_calib_shapes(), popsize=12)
+    refs = c.fields(TH_TRUE)
+    assert len(refs) == 3 and all(float(r.abs().max()) > 1e-6 for r in refs)
+    c.set_reference(refs)
+    L = c.losses(np.tile(TH_TRUE, (12, 1)))
+    L_off = c.losses(np.tile(TH_TRUE * np.array([1.1, 1.0, 1.0, 1.1]), (12, 1)))
+    assert L.max() < 0.1 * L_off.min()  # theta_true reproduces its reference up to the solve tolerance
+    res = c.run(iters=40, sigma0=0.25, seed=5)
+    th = res["theta"]
+    assert abs(th[0] / TH_TRUE[0] - 1) < 0.05, th
+    assert abs(th[1] - TH_TRUE[1]) < 0.005, th
+    assert abs(th[3] / TH_TRUE[3] - 1) < 0.05, th

@@ -518,7 +518,7 @@ def scene_c5(n_envs=256, n_steps=64, seed0=20270000):
 # ----------------------------------------------------------------------------
 # §8f-2: batched material calibration (Eqs. 6-7)
 # ----------------------------------------------------------------------------
-def scene_calib(frames=6, cells=(16, 12, 4), f_max=0.2):
+def scene_calib(frames=6, cells=(16, 12, 4), f_max=0.2, shape="sphere"):
     """Calibration workload: N = 4 indentation trajectories of a 3 mm sphere on a
     16x12x4 mm pad ("different deformation modes": press + shear x, off-centre
     press + shear y, deep press, press + twist), `frames` frames each.  The pose spring's
@@ -528,8 +528,17 @@ def scene_calib(frames=6, cells=(16, 12, 4), f_max=0.2):
     simulator at a hidden theta_true (synthetic)."""
     ext = (16 * MM, 12 * MM, 4 * MM)
     X, T, Fx = make_pad(ext, cells)
-    R = 3 * MM
-    Y, tris = make_icosphere(R, 2)
+    if shape == "sphere":
+        R = 3 * MM  # centre height above the contact point
+        Y, tris = make_icosphere(R, 2)
+    elif shape == "cylinder":  # lying cylinder (axis along body x): line contact
+        R = 2.5 * MM
+        Y, tris = make_cylinder(R, 8 * MM, 24, 6)
+    elif shape == "cube":  # 5 mm cube pressed flat-face down
+        R = 2.5 * MM
+        Y, tris = make_square_peg(5 * MM, 5 * MM, 1.25 * MM)
+    else:
+        raise ValueError(shape)
     M, frame = make_markers(ext, cells)
     q0 = [1.0, 0, 0, 0]
     gap = 0.05 * MM
@@ -554,6 +563,15 @@ def scene_calib(frames=6, cells=(16, 12, 4), f_max=0.2):
                 fr.append(pose((x0 + t * sx, y0 + t * sy, R - depth), q))
         trajs.append(fr)
     poses = np.stack([np.stack([trajs[i][k] for i in range(len(specs))]) for k in range(frames)])
-    sc = Scene("calib", X, T, Fx, Y, tris, M, frame, np.stack(inits), poses, extent=ext, cells=cells)
+    sc = Scene("calib_" + shape, X, T, Fx, Y, tris, M, frame, np.stack(inits), poses, extent=ext, cells=cells)
     sc.params.f_max = f_max
+    # a generation waits for its slowest candidate: near-incompressible candidates (nu -> 0.497)
+    # are capped at 1,000 iterations per step (their loss is then noisier, which CMA-ES tolerates)
+    sc.params.max_iters = 1000
     return sc
+
+
+def scene_calib_shapes(frames=6, f_max=0.2):
+    """Several indenter shapes for one calibration (P:305 uses four: cube, cylinder, moon,
+    triangle): sphere, lying cylinder and cube, one scene (= one simulator) each."""
+    return [scene_calib(frames=frames, f_max=f_max, shape=sh) for sh in ("sphere", "cylinder", "cube")]
