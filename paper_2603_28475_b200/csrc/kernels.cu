@@ -12,6 +12,10 @@
 
 #include "internal.h"
 
+// programmatic dependent launch: wait for the stream predecessor (first statement of
+// every kernel; see pdl_launch)
+#define TAC_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+
 namespace tac {
 
 thread_local long long g_launches = 0;
@@ -408,6 +412,7 @@ __device__ __forceinline__ double unit_sym(unsigned x) { return ((double)(x >> 8
 // a1: step setup.  R27: with pose noise on, the target of env e at step k is perturbed
 // c_s += s_t (u0, u1, u2), R_s <- exp([s_r (u3, u4, u5)]) R_s, u = Philox(seed; e, k, 0 / 1)
 __global__ void k_step_setup(Dev d, const float* poses, unsigned long long step) {
+  TAC_PDL_WAIT();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= d.E) return;
   EnvS& s = d.es[e];
@@ -450,6 +455,7 @@ __global__ void k_step_setup(Dev d, const float* poses, unsigned long long step)
 
 // x^ = x^t + h v^t on free vertices; u = u^t
 __global__ void k_vert_setup(Dev d, float h) {
+  TAC_PDL_WAIT();
   int e = blockIdx.x * 32 + threadIdx.x;
   if (e >= d.E) return;
   for (int v = blockIdx.y * 8 + threadIdx.y; v < d.nv; v += gridDim.y * 8) {
@@ -609,6 +615,7 @@ __device__ void bp_range(const Dev& d, int e, int i0, int i1, int stride, double
 
 __global__ void __launch_bounds__(128) k_broadphase(Dev d, double r, unsigned long long* out_override,
                                                     int* cnt_override, int cap_override) {
+  TAC_PDL_WAIT();
   int e = blockIdx.y;
   if (e >= d.E) return;
   const EnvS& s = d.es[e];
@@ -637,6 +644,7 @@ __global__ void __launch_bounds__(128) k_broadphase(Dev d, double r, unsigned lo
 // without any gel edge crossing an indenter triangle is not detected.)
 __device__ __forceinline__ double orient3(d3 a, d3 b, d3 c, d3 p) { return dot(cross(b - a, c - a), p - a); }
 __global__ void __launch_bounds__(128) k_intersect_check(Dev d, int* hit) {
+  TAC_PDL_WAIT();
   const int e = blockIdx.y, i = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= d.E || i >= d.nse) return;
   const EnvS& s = d.es[e];
@@ -682,6 +690,7 @@ __global__ void __launch_bounds__(128) k_intersect_check(Dev d, int* hit) {
 // 32-primitive chunk) per WARP over a fixed grid, so cost follows the actual rebuild count
 // and no warp waits for another
 __global__ void __launch_bounds__(128) k_broadphase_list(Dev d, double r) {
+  TAC_PDL_WAIT();
   const int nreb = *d.nreb;
   const int ntot = d.nsv + d.nse + d.nst;
   const int nchunk = (ntot + 31) / 32;
@@ -707,6 +716,7 @@ __global__ void __launch_bounds__(128) k_broadphase_list(Dev d, double r) {
 // ------------------------------------------------------------------ a3: friction anchors
 // pairs with d(x^t) < dhat: lambda = -kappa b'(d), frozen weights, tangent basis (R7)
 __global__ void k_anchors(Dev d, double h2) {
+  TAC_PDL_WAIT();
   int e = blockIdx.y;
   if (e >= d.E || d.es[e].mode != kActive) return;
   const EnvS& s = d.es[e];
@@ -767,6 +777,7 @@ __global__ void k_anchors(Dev d, double h2) {
 // applies the pending update u += dalpha p (a8), then the inertia term
 // 1/2 m |u - u^|^2, g = m (u - u^), D = m I (lumped M)
 __global__ void k_vert_pre(Dev d, float h2) {
+  TAC_PDL_WAIT();
   int e = blockIdx.x * 32 + threadIdx.x;
   bool act = e < d.E && (d.run[e] & 1);
   if (!__any_sync(0xffffffffu, act)) return;
@@ -853,6 +864,7 @@ __device__ __forceinline__ void cof33(const float* A, float* C) {
 }
 
 __global__ void __launch_bounds__(256, 4) k_elem_grad(Dev d, float h2) {
+  TAC_PDL_WAIT();
   // env group = blockIdx.y (slowest) so the g / D lines of the env groups in flight stay in L2
   const int e = blockIdx.y * 32 + threadIdx.x;
   const bool act = e < d.E && (d.run[e] & 1);
@@ -956,6 +968,7 @@ __global__ void __launch_bounds__(256, 4) k_elem_grad(Dev d, float h2) {
                         : (j) < 4 ? ((k) == 1 ? 2 : ((j) == 2 ? 3 : 6)) : ((k) == 1 ? 4 : ((j) == 4 ? 5 : 6)))
 
 __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
+  TAC_PDL_WAIT();
   const int e = blockIdx.y * 32 + threadIdx.x;
   const bool act = e < d.E && (d.run[e] & 1);
   if (!__any_sync(0xffffffffu, act)) return;
@@ -1064,6 +1077,7 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
 // ---- Kuhn-cell element curvature: one warp = one cell x 32 envs, u and p of the 8 corners
 // in registers; p^T H_e p summed over the 6 tets (App. B quadratic form)
 __global__ void __launch_bounds__(256, 2) k_elem_curv_cells(Dev d, float h2) {
+  TAC_PDL_WAIT();
   const int e = blockIdx.y * 32 + threadIdx.x;
   const bool act = e < d.E && (d.run[e] & 2);
   if (!__any_sync(0xffffffffu, act)) return;
@@ -1142,6 +1156,7 @@ __device__ __forceinline__ TetData load_tile_tet(const Dev& d, int gt) {
 }
 constexpr int kTiledCurvSmem = 2 * 3 * kTileV * 32 * 4;
 __global__ void __launch_bounds__(256) k_elem_curv_tiled(Dev d, float h2) {
+  TAC_PDL_WAIT();
   extern __shared__ float shc[];
   float (*su)[kTileV][32] = reinterpret_cast<float (*)[kTileV][32]>(shc);
   float (*sp)[kTileV][32] = reinterpret_cast<float (*)[kTileV][32]>(shc + 3 * kTileV * 32);
@@ -1245,6 +1260,7 @@ __device__ __forceinline__ void scatter_gel(const Dev& d, int v, int e, d3 f, do
 
 template <int KIND>
 __global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
+  TAC_PDL_WAIT();
   int e = blockIdx.y;
   if (e >= d.E || !(d.run[e] & 1)) return;
   const double kappa = h2 * d.edbl[e];  // h^2 kappa_phys of this env
@@ -1327,6 +1343,7 @@ __global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
 // friction over the anchors: value, gradient, GN blocks, wrench; caches
 // mu lambda f1(s) per anchor for the curvature pass
 __global__ void __launch_bounds__(128) k_contact_friction(Dev d, double eps_f) {
+  TAC_PDL_WAIT();
   int e = blockIdx.y;
   if (e >= d.E || !(d.run[e] & 1)) return;
   const EnvS& s = d.es[e];
@@ -1482,6 +1499,7 @@ __device__ __forceinline__ void push_local(bool mine, int lane, int* cnt, unsign
   else glist[atomicAdd(gcnt, 1)] = chunk0 + off;  // local list full: direct global append
 }
 __global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
+  TAC_PDL_WAIT();
   // fp32 positions (gel X + u, indenter c + R Y) carry absolute errors <= ~6e-9 m at the
   // pad scale, so a pair is certified far only if its fp32 gap exceeds dhat + kClassMargin
   // and the cached gap is lowered by the same margin: the certificate stays conservative
@@ -1646,6 +1664,7 @@ __global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
 
 // curvature + near-pair step bounds from the cached geometry, p staged in shared memory
 __global__ void __launch_bounds__(256) k_contact_curv_staged(Dev d, double h2) {
+  TAC_PDL_WAIT();
   extern __shared__ __align__(16) char shc3[];
   int e = blockIdx.y;
   if (e >= d.E || !(d.run[e] & 2)) return;
@@ -1748,6 +1767,7 @@ __device__ void apply_pose(EnvS& s, double a) {  // (c, R) = (c_p + a p_c, exp([
 }
 
 __global__ void k_accept(Dev d, double h) {
+  TAC_PDL_WAIT();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= d.E || !(d.run[e] & 1)) return;
   EnvS& s = d.es[e];
@@ -1835,6 +1855,7 @@ __device__ __forceinline__ void precond(const float* D, int scalar, const float*
 }
 
 __global__ void __launch_bounds__(256) k_dir_reduce(Dev d) {
+  TAC_PDL_WAIT();
   int e = blockIdx.x * 32 + threadIdx.x;
   bool act = e < d.E && (d.run[e] & 2);
   if (!__any_sync(0xffffffffu, act)) return;
@@ -1918,6 +1939,7 @@ __device__ void rigid_P(const EnvS& s, int scalar, const double* x, double* y) {
 // per env: convergence on |P g|_disp (R17), Dai-Kou beta with restarts (R13),
 // rigid part of the direction
 __global__ void k_dir_scalar(Dev d) {
+  TAC_PDL_WAIT();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= d.E || !(d.run[e] & 2)) return;
   EnvS& s = d.es[e];
@@ -1979,6 +2001,7 @@ __global__ void k_dir_scalar(Dev d) {
 
 // p = -P g + beta p_prev; g_prev = g; M = max |p_v|, L_rel = max_surface |p_v - p_c|, inertia p^T M p
 __global__ void __launch_bounds__(256) k_dir_apply(Dev d) {
+  TAC_PDL_WAIT();
   int e = blockIdx.x * 32 + threadIdx.x;
   bool act = e < d.E && (d.run[e] & 2);
   if (!__any_sync(0xffffffffu, act)) return;
@@ -2054,6 +2077,7 @@ __global__ void __launch_bounds__(256) k_dir_apply(Dev d) {
 // = (listed env, 128-candidate chunk); separating-axis certificate -> g_min, else exact
 // fp64 distance and the closest-point plane bound (R15)
 __global__ void __launch_bounds__(128) k_ccd_list(Dev d) {
+  TAC_PDL_WAIT();
   const int nreb = *d.nreb;
   __shared__ double R[9], c[3], pr[6];
   __shared__ double smin[4], sg[4];
@@ -2138,6 +2162,7 @@ __device__ void commit_alpha(const Dev& d, EnvS& s, int e, double a, double L) {
 }
 
 __global__ void k_alpha(Dev d, double h, int pass) {
+  TAC_PDL_WAIT();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= d.E) return;
   int rb = d.run[e];
@@ -2194,6 +2219,7 @@ __global__ void k_alpha(Dev d, double h, int pass) {
 
 // ------------------------------------------------------------------ a9: finalize
 __global__ void k_finalize_vert(Dev d, float inv_h) {
+  TAC_PDL_WAIT();
   int e = blockIdx.x * 32 + threadIdx.x;
   if (e >= d.E) return;
   bool failed = d.es[e].flags & (4 | 8);
@@ -2217,6 +2243,7 @@ __global__ void k_finalize_vert(Dev d, float inv_h) {
   }
 }
 __global__ void k_finalize_env(Dev d) {
+  TAC_PDL_WAIT();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= d.E) return;
   EnvS& s = d.es[e];
@@ -2243,6 +2270,7 @@ __global__ void k_finalize_env(Dev d) {
 // ------------------------------------------------------------------ a10: markers
 // u_m = sum_j w_mj u_j; out[e][m] = (u_m.t1, u_m.t2[, u_m.n])
 __global__ void k_markers(Dev d, float* out, int ncomp, float4 t1, float4 t2, float4 nn) {
+  TAC_PDL_WAIT();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= d.E * d.nm) return;
   int e = i / d.nm, m = i - e * d.nm;
@@ -2265,6 +2293,7 @@ __global__ void k_markers(Dev d, float* out, int ncomp, float4 t1, float4 t2, fl
 // the marker field computed exactly as k_markers does; one CTA per env (sole writer)
 __global__ void __launch_bounds__(128) k_marker_sqerr(Dev d, const float* ref, double* acc, int ncomp, float4 t1,
                                                       float4 t2, float4 nn) {
+  TAC_PDL_WAIT();
   const int e = blockIdx.x;
   __shared__ double sw[4];
   double se = 0;
@@ -2299,6 +2328,7 @@ __global__ void __launch_bounds__(128) k_marker_sqerr(Dev d, const float* ref, d
 }
 
 __global__ void k_reset_env(Dev d, const unsigned char* mask, const float* poses) {
+  TAC_PDL_WAIT();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= d.E || !mask[e]) return;
   EnvS& s = d.es[e];
@@ -2311,6 +2341,7 @@ __global__ void k_reset_env(Dev d, const unsigned char* mask, const float* poses
   s.pg = 0;
 }
 __global__ void k_reset_vert(Dev d, const unsigned char* mask) {
+  TAC_PDL_WAIT();
   int e = blockIdx.x * 32 + threadIdx.x;
   if (e >= d.E || !mask[e]) return;
   for (int v = blockIdx.y * 8 + threadIdx.y; v < d.nv; v += gridDim.y * 8)
@@ -2320,6 +2351,7 @@ __global__ void k_reset_vert(Dev d, const unsigned char* mask) {
     }
 }
 __global__ void k_status(Dev d, int* iters, float* pg, unsigned* flags) {
+  TAC_PDL_WAIT();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= d.E) return;
   if (iters) iters[e] = d.es[e].iter;
@@ -2327,12 +2359,14 @@ __global__ void k_status(Dev d, int* iters, float* pg, unsigned* flags) {
   if (flags) flags[e] = (unsigned)d.es[e].flags;
 }
 __global__ void k_stats(Dev d, int4* out) {
+  TAC_PDL_WAIT();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= d.E) return;
   const EnvS& s = d.es[e];
   out[e] = make_int4(s.iter, s.ncand_max, s.nanc_last, s.rebuild);
 }
 __global__ void k_any_active(Dev d, int* out) {
+  TAC_PDL_WAIT();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   int a = (e < d.E && d.es[e].mode == kActive) ? 1 : 0;
   if (__any_sync(0xffffffffu, a) && (threadIdx.x & 31) == 0) atomicOr(out, 1);
@@ -2357,109 +2391,127 @@ static dim3 sgrid(const Dev& d) {  // staged contact kernels: chunks per env
   int nb = std::max(1, std::min(16, 2368 / std::max(1, d.E)));
   return dim3(nb, d.E);
 }
-#define LAUNCHK(kid, s, ...)         \
-  do {                                \
-    if (g_prof) prof_begin(kid, s);   \
-    __VA_ARGS__;                      \
-    if (g_prof) prof_end(kid, s);     \
-    ++g_launches;                     \
+// Every launch is a programmatic dependent launch: the next kernel's CTAs may be resident
+// while this one drains, and each kernel starts with griddepcontrol.wait (TAC_PDL_WAIT),
+// which blocks until its stream predecessor has completed and flushed.  Memsets and
+// profiling events between kernels fall back to ordinary stream serialisation.
+template <typename... KArgs, typename... Args>
+static void pdl_launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+#define LAUNCHP(kid, s, kern, grid, block, smem, ...)      \
+  do {                                                   \
+    if (g_prof) prof_begin(kid, s);                      \
+    pdl_launch(kern, dim3(grid), dim3(block), (size_t)(smem), s, ##__VA_ARGS__); \
+    if (g_prof) prof_end(kid, s);                        \
+    ++g_launches;                                        \
   } while (0)
 
 void launch_step_setup(const Dev& d, const float* poses, double h, unsigned long long step, cudaStream_t s) {
-  LAUNCHK(KID_STEP_SETUP, s, (k_step_setup<<<eblocks32(d), 32, 0, s>>>(d, poses, step)));
-  LAUNCHK(KID_VERT_SETUP, s, (k_vert_setup<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d, (float)h)));
+  LAUNCHP(KID_STEP_SETUP, s, k_step_setup, eblocks32(d), 32, 0, d, poses, step);
+  LAUNCHP(KID_VERT_SETUP, s, k_vert_setup, vgrid(d, d.nv), dim3(32, 8), 0, d, (float)h);
 }
 void launch_vert_setup(const Dev& d, double h, cudaStream_t s) {
-  LAUNCHK(KID_VERT_SETUP, s, (k_vert_setup<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d, (float)h)));
+  LAUNCHP(KID_VERT_SETUP, s, k_vert_setup, vgrid(d, d.nv), dim3(32, 8), 0, d, (float)h);
 }
 void launch_broadphase(const Dev& d, bool masked, cudaStream_t s) {
   if (masked) {  // envs listed by k_alpha
-    LAUNCHK(KID_BROADPHASE_LIST, s, (k_broadphase_list<<<16 * 148, 128, 0, s>>>(d, d.dhat + d.bp_margin)));
+    LAUNCHP(KID_BROADPHASE_LIST, s, k_broadphase_list, 16 * 148, 128, 0, d, d.dhat + d.bp_margin);
     return;
   }
   int ntot = d.nsv + d.nse + d.nst;
   int nb = std::max(1, std::min((ntot + 127) / 128, 4736 / std::max(1, d.E)));
-  LAUNCHK(KID_BROADPHASE, s, (k_broadphase<<<dim3(nb, d.E), 128, 0, s>>>(d, d.dhat + d.bp_margin, nullptr, nullptr, 0)));
+  LAUNCHP(KID_BROADPHASE, s, k_broadphase, dim3(nb, d.E), 128, 0, d, d.dhat + d.bp_margin, nullptr, nullptr, 0);
 }
 void launch_intersect_check(const Dev& d, int* hit, cudaStream_t s) {
-  LAUNCHK(KID_OTHER, s, (k_intersect_check<<<dim3((d.nse + 127) / 128, d.E), 128, 0, s>>>(d, hit)));
+  LAUNCHP(KID_OTHER, s, k_intersect_check, dim3((d.nse + 127) / 128, d.E), 128, 0, d, hit);
 }
 void launch_anchors(const Dev& d, double h, cudaStream_t s) {
-  LAUNCHK(KID_ANCHORS, s, (k_anchors<<<cgrid(d), 128, 0, s>>>(d, h * h)));
+  LAUNCHP(KID_ANCHORS, s, k_anchors, cgrid(d), 128, 0, d, h * h);
 }
 void launch_eval(const Dev& d, double h, cudaStream_t s) {
-  LAUNCHK(KID_VERT_PRE, s, (k_vert_pre<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d, (float)(h * h))));
+  LAUNCHP(KID_VERT_PRE, s, k_vert_pre, vgrid(d, d.nv), dim3(32, 8), 0, d, (float)(h * h));
   // (a round-scheduled shared-memory tiled variant measured slower on C3: 740 vs 520 us at
   // 66 % warp utilisation in the rounds and 2 CTAs/SM; the coalesced red.add scatter stays)
   if (d.ncells > 0) {
     dim3 g = vgrid(d, d.ncells);
-    LAUNCHK(KID_ELEM_GRAD, s, (k_elem_grad_cells<<<dim3(g.y, g.x), dim3(32, 8), 0, s>>>(d, (float)(h * h))));
+    LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad_cells, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
   }
   if (d.nrest > 0) {
     dim3 g = vgrid(d, d.nrest);
-    LAUNCHK(KID_ELEM_GRAD, s, (k_elem_grad<<<dim3(g.y, g.x), dim3(32, 8), 0, s>>>(d, (float)(h * h))));
+    LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
   }
   const size_t cls_smem = sizeof(float4) * (size_t)(d.nsv + d.niv);  // [nsv] X + u, [niv] c + R Y
-  LAUNCHK(KID_CONTACT_CLASSIFY, s, (k_contact_classify_staged<<<sgrid(d), 256, cls_smem, s>>>(d)));
+  LAUNCHP(KID_CONTACT_CLASSIFY, s, k_contact_classify_staged, sgrid(d), 256, cls_smem, d);
   const double kap = h * h;  // kernels scale by their env's kappa_phys
-  LAUNCHK(KID_CONTACT_GRAD, s, (k_contact_near<0><<<cgrid(d), 128, 0, s>>>(d, kap)));
-  LAUNCHK(KID_CONTACT_NEAR_IG, s, (k_contact_near<1><<<cgrid(d), 128, 0, s>>>(d, kap)));
-  LAUNCHK(KID_CONTACT_NEAR_EE, s, (k_contact_near<2><<<cgrid(d), 128, 0, s>>>(d, kap)));
-  LAUNCHK(KID_CONTACT_FRICTION, s, (k_contact_friction<<<cgrid(d), 128, 0, s>>>(d, d.eps_v * h)));
-  LAUNCHK(KID_ACCEPT, s, (k_accept<<<eblocks32(d), 32, 0, s>>>(d, h)));
+  LAUNCHP(KID_CONTACT_GRAD, s, k_contact_near<0>, cgrid(d), 128, 0, d, kap);
+  LAUNCHP(KID_CONTACT_NEAR_IG, s, k_contact_near<1>, cgrid(d), 128, 0, d, kap);
+  LAUNCHP(KID_CONTACT_NEAR_EE, s, k_contact_near<2>, cgrid(d), 128, 0, d, kap);
+  LAUNCHP(KID_CONTACT_FRICTION, s, k_contact_friction, cgrid(d), 128, 0, d, d.eps_v * h);
+  LAUNCHP(KID_ACCEPT, s, k_accept, eblocks32(d), 32, 0, d, h);
 }
 void launch_direction(const Dev& d, cudaStream_t s) {
-  LAUNCHK(KID_DIR_REDUCE, s, (k_dir_reduce<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d)));
-  LAUNCHK(KID_DIR_SCALAR, s, (k_dir_scalar<<<eblocks32(d), 32, 0, s>>>(d)));
-  LAUNCHK(KID_DIR_APPLY, s, (k_dir_apply<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d)));
+  LAUNCHP(KID_DIR_REDUCE, s, k_dir_reduce, vgrid(d, d.nv), dim3(32, 8), 0, d);
+  LAUNCHP(KID_DIR_SCALAR, s, k_dir_scalar, eblocks32(d), 32, 0, d);
+  LAUNCHP(KID_DIR_APPLY, s, k_dir_apply, vgrid(d, d.nv), dim3(32, 8), 0, d);
 }
 void launch_curvature(const Dev& d, double h, cudaStream_t s) {
   if (d.nrest == 0) {  // every tet is in a Kuhn cell: register-blocked cells
     dim3 g = vgrid(d, d.ncells);
-    LAUNCHK(KID_ELEM_CURV, s, (k_elem_curv_cells<<<dim3(g.y, g.x), dim3(32, 8), 0, s>>>(d, (float)(h * h))));
+    LAUNCHP(KID_ELEM_CURV, s, k_elem_curv_cells, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
   } else {
-    LAUNCHK(KID_ELEM_CURV, s, (k_elem_curv_tiled<<<dim3(d.Es / 32, d.ntiles), 256, kTiledCurvSmem, s>>>(d, (float)(h * h))));
+    LAUNCHP(KID_ELEM_CURV, s, k_elem_curv_tiled, dim3(d.Es / 32, d.ntiles), 256, kTiledCurvSmem, d, (float)(h * h));
   }
-  LAUNCHK(KID_CONTACT_CURV, s, (k_contact_curv_staged<<<sgrid(d), 256, d.contact_smem, s>>>(d, h * h)));
+  LAUNCHP(KID_CONTACT_CURV, s, k_contact_curv_staged, sgrid(d), 256, d.contact_smem, d, h * h);
 }
 void launch_alpha(const Dev& d, double h, cudaStream_t s) {
   cudaMemsetAsync(d.nreb, 0, sizeof(int), s);
-  LAUNCHK(KID_ALPHA, s, (k_alpha<<<eblocks32(d), 32, 0, s>>>(d, h, 1)));
+  LAUNCHP(KID_ALPHA, s, k_alpha, eblocks32(d), 32, 0, d, h, 1);
   launch_broadphase(d, true, s);
-  LAUNCHK(KID_CCD, s, (k_ccd_list<<<4 * 148, 128, 0, s>>>(d)));
-  LAUNCHK(KID_ALPHA, s, (k_alpha<<<eblocks32(d), 32, 0, s>>>(d, h, 2)));
+  LAUNCHP(KID_CCD, s, k_ccd_list, 4 * 148, 128, 0, d);
+  LAUNCHP(KID_ALPHA, s, k_alpha, eblocks32(d), 32, 0, d, h, 2);
 }
 void launch_finalize(const Dev& d, double h, cudaStream_t s) {
-  LAUNCHK(KID_FIN_VERT, s, (k_finalize_vert<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d, (float)(1.0 / h))));
-  LAUNCHK(KID_FIN_ENV, s, (k_finalize_env<<<eblocks32(d), 32, 0, s>>>(d)));
+  LAUNCHP(KID_FIN_VERT, s, k_finalize_vert, vgrid(d, d.nv), dim3(32, 8), 0, d, (float)(1.0 / h));
+  LAUNCHP(KID_FIN_ENV, s, k_finalize_env, eblocks32(d), 32, 0, d);
 }
 void launch_markers(const Dev& d, float* out, int ncomp, cudaStream_t s) {
   int n = d.E * d.nm;
   float4 t1 = make_float4(d.t1[0], d.t1[1], d.t1[2], 0), t2 = make_float4(d.t2[0], d.t2[1], d.t2[2], 0),
          nn = make_float4(d.nrm[0], d.nrm[1], d.nrm[2], 0);
-  LAUNCHK(KID_MARKERS, s, (k_markers<<<(n + 255) / 256, 256, 0, s>>>(d, out, ncomp, t1, t2, nn)));
+  LAUNCHP(KID_MARKERS, s, k_markers, (n + 255) / 256, 256, 0, d, out, ncomp, t1, t2, nn);
 }
 void launch_marker_sqerr(const Dev& d, const float* ref, double* acc, int ncomp, cudaStream_t s) {
   float4 t1 = make_float4(d.t1[0], d.t1[1], d.t1[2], 0), t2 = make_float4(d.t2[0], d.t2[1], d.t2[2], 0),
          nn = make_float4(d.nrm[0], d.nrm[1], d.nrm[2], 0);
-  LAUNCHK(KID_MARKERS, s, (k_marker_sqerr<<<d.E, 128, 0, s>>>(d, ref, acc, ncomp, t1, t2, nn)));
+  LAUNCHP(KID_MARKERS, s, k_marker_sqerr, d.E, 128, 0, d, ref, acc, ncomp, t1, t2, nn);
 }
 void launch_reset(const Dev& d, const unsigned char* mask, const float* poses, cudaStream_t s) {
-  LAUNCHK(KID_OTHER, s, (k_reset_env<<<eblocks(d), 128, 0, s>>>(d, mask, poses)));
-  LAUNCHK(KID_OTHER, s, (k_reset_vert<<<vgrid(d, d.nv), dim3(32, 8), 0, s>>>(d, mask)));
+  LAUNCHP(KID_OTHER, s, k_reset_env, eblocks(d), 128, 0, d, mask, poses);
+  LAUNCHP(KID_OTHER, s, k_reset_vert, vgrid(d, d.nv), dim3(32, 8), 0, d, mask);
 }
 void launch_status(const Dev& d, int* iters, float* pg, unsigned* flags, cudaStream_t s) {
-  LAUNCHK(KID_OTHER, s, (k_status<<<eblocks(d), 128, 0, s>>>(d, iters, pg, flags)));
+  LAUNCHP(KID_OTHER, s, k_status, eblocks(d), 128, 0, d, iters, pg, flags);
 }
 void launch_stats(const Dev& d, int4* out, cudaStream_t s) {
-  LAUNCHK(KID_OTHER, s, (k_stats<<<eblocks(d), 128, 0, s>>>(d, out)));
+  LAUNCHP(KID_OTHER, s, k_stats, eblocks(d), 128, 0, d, out);
 }
 void launch_any_active(const Dev& d, int* out, cudaStream_t s) {
-  LAUNCHK(KID_OTHER, s, (k_any_active<<<eblocks(d), 128, 0, s>>>(d, out)));
+  LAUNCHP(KID_OTHER, s, k_any_active, eblocks(d), 128, 0, d, out);
 }
 void launch_debug_broadphase(const Dev& d, double r, unsigned long long* out, int* cnt, int cap, cudaStream_t s) {
   int ntot = d.nsv + d.nse + d.nst;
-  LAUNCHK(KID_BROADPHASE, s, (k_broadphase<<<dim3((ntot + 127) / 128, d.E), 128, 0, s>>>(d, r, out, cnt, cap)));
+  LAUNCHP(KID_BROADPHASE, s, k_broadphase, dim3((ntot + 127) / 128, d.E), 128, 0, d, r, out, cnt, cap);
 }
 constexpr int kContactSmemCap = 160 * 1024;  // staged contact kernels: largest dynamic shared size
 int contact_smem_bytes(int nsv, int niv) {
