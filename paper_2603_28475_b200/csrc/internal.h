@@ -112,7 +112,8 @@ struct Dev {
   uint2* ccorn;           // [E][kmax] corner ids of each candidate, 4 x 16 bit (gel: surface-local id,
                          // indenter: vertex id), written with the candidate list
   float* cgap;            // [E][kmax] certified axis gap + odometer at certification (rounded down)
-  float4* cgeo;          // [E][kmax][2] pair geometry of the last evaluation: (d, n), (w0..w3)
+  float4* cgeo;          // [E][kmax][2] near-pair geometry (d, n), (w0..w3) in near order: kinds 0, 1, 2 concatenated
+  uint2* ncorn;          // [E][kmax] the near pairs' packed corner ids, same order as cgeo
   int* ncand;            // [E]
   int* nearl;            // [E][3][kmax] indices of near candidates (no separating-axis certificate), per pair kind
   int* nnear;            // [E][3]

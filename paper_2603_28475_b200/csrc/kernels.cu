@@ -1273,25 +1273,29 @@ __global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
   double Eb = 0, gr[6] = {0, 0, 0, 0, 0, 0}, Dc[6] = {0, 0, 0, 0, 0, 0}, Dt[6] = {0, 0, 0, 0, 0, 0};
   d3 cc = ld3(c);
   const int n = d.nnear[3 * e + KIND];
+  // near-ordered output slots: kinds 0, 1, 2 concatenated (the counts are final after classify)
+  const int base = (KIND >= 1 ? d.nnear[3 * e] : 0) + (KIND >= 2 ? d.nnear[3 * e + 1] : 0);
   const int* list = d.nearl + ((size_t)e * 3 + KIND) * d.kmax;
-  const unsigned long long* cand = d.cand + (size_t)e * d.kmax;
+  const uint2* ccorn = d.ccorn + (size_t)e * d.kmax;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    int i = list[j];
-    unsigned long long rec = cand[i];
-    int a = (int)((rec >> 31) & 0x7fffffffu), b = (int)(rec & 0x7fffffffu);
-    CornersL C = corners_l(d, KIND, a, b);
+    const int i = list[j];
+    const uint2 cw = ccorn[i];
+    const unsigned id[4] = {cw.x & 0xffffu, cw.x >> 16, cw.y & 0xffffu, cw.y >> 16};
+    bool ind[4];
     d3 z[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      if (C.ind[k]) {
-        z[k] = mv(R, ind_body(d, C.gid[k])) + cc;
+      ind[k] = KIND == 0 ? k >= 1 : (KIND == 1 ? k == 0 : k >= 2);
+      if (ind[k]) {
+        z[k] = mv(R, ind_body(d, id[k])) + cc;
       } else {
-        float4 X = __ldg(d.X + C.gid[k]);
-        float4 u = d.usurf[(size_t)C.sid[k] * d.Es + e];
+        const float4 X = __ldg(d.Xs + id[k]), u = d.usurf[(size_t)id[k] * d.Es + e];
         z[k] = mk((double)X.x + (double)u.x, (double)X.y + (double)u.y, (double)X.z + (double)u.z);
       }
     }
-    float4* geo = d.cgeo + 2 * ((size_t)e * d.kmax + i);
+    const size_t slot = (size_t)e * d.kmax + base + j;
+    d.ncorn[slot] = cw;
+    float4* geo = d.cgeo + 2 * slot;
     DR D = KIND == 2 ? dist_ee(z[0], z[1], z[2], z[3]) : dist_pt(z[0], z[1], z[2], z[3]);
     if (!(D.d > 0)) {
       Eb = INFINITY;
@@ -1315,8 +1319,8 @@ __global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       d3 f = (db * D.w[k]) * nn;
-      if (!C.ind[k]) {
-        scatter_gel(d, C.gid[k], e, f, ddb * D.w[k] * D.w[k], nn);
+      if (!ind[k]) {
+        scatter_gel(d, __ldg(d.sv + id[k]), e, f, ddb * D.w[k] * D.w[k], nn);
       } else {
         d3 arm = z[k] - cc;
         d3 tq = cross(arm, f);
@@ -1689,13 +1693,13 @@ __global__ void __launch_bounds__(256) k_contact_curv_staged(Dev d, double h2) {
   double q = 0, amin = INFINITY;
   const int n0 = d.nnear[3 * e], n1 = d.nnear[3 * e + 1], n = n0 + n1 + d.nnear[3 * e + 2];
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    int kk = j < n0 ? 0 : (j < n0 + n1 ? 1 : 2);
-    int jj = j - (kk == 0 ? 0 : (kk == 1 ? n0 : n0 + n1));
-    int i = d.nearl[((size_t)e * 3 + kk) * d.kmax + jj];
-    const uint2 cc = d.ccorn[(size_t)e * d.kmax + i];
+    const int kk = j < n0 ? 0 : (j < n0 + n1 ? 1 : 2);
+    // near-ordered geometry and corners (written by k_contact_near at this position)
+    const size_t slot = (size_t)e * d.kmax + j;
+    const uint2 cc = d.ncorn[slot];
     const unsigned id[4] = {cc.x & 0xffffu, cc.x >> 16, cc.y & 0xffffu, cc.y >> 16};
     const int na = kk == 2 ? 2 : 1;
-    const float4* geo = d.cgeo + 2 * ((size_t)e * d.kmax + i);
+    const float4* geo = d.cgeo + 2 * slot;
     float4 g0 = geo[0], g1 = geo[1];
     double dist = g0.x;
     if (!(dist > 0)) continue;
