@@ -115,7 +115,7 @@ struct Dev {
   float4* cgeo;          // [E][kmax][2] near-pair geometry (d, n), (w0..w3) in near order: kinds 0, 1, 2 concatenated
   uint2* ncorn;          // [E][kmax] the near pairs' packed corner ids, same order as cgeo
   int* ncand;            // [E]
-  int* nearl;            // [E][3][kmax] indices of near candidates (no separating-axis certificate), per pair kind
+  uint2* nearl;          // [E][3][kmax] packed corner ids of the near candidates (no far certificate), per pair kind
   int* nnear;            // [E][3]
   const int* sidx;       // [nv] surface-local index of a gel vertex, -1 if not on the surface
   float4* usurf;         // [nsv][Es] u of the surface vertices at the last evaluation

@@ -1275,11 +1275,9 @@ __global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
   const int n = d.nnear[3 * e + KIND];
   // near-ordered output slots: kinds 0, 1, 2 concatenated (the counts are final after classify)
   const int base = (KIND >= 1 ? d.nnear[3 * e] : 0) + (KIND >= 2 ? d.nnear[3 * e + 1] : 0);
-  const int* list = d.nearl + ((size_t)e * 3 + KIND) * d.kmax;
-  const uint2* ccorn = d.ccorn + (size_t)e * d.kmax;
+  const uint2* list = d.nearl + ((size_t)e * 3 + KIND) * d.kmax;  // packed corners of the near pairs
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    const int i = list[j];
-    const uint2 cw = ccorn[i];
+    const uint2 cw = list[j];
     const unsigned id[4] = {cw.x & 0xffffu, cw.x >> 16, cw.y & 0xffffu, cw.y >> 16};
     bool ind[4];
     d3 z[4];
@@ -1491,7 +1489,7 @@ constexpr int kClassChunk = 4096;  // candidates per chunk (queue offsets fit 16
 constexpr int kClassA = kClassChunk / 256;  // phase-A candidates per thread
 constexpr int kClassNL = 1024;     // block-local near-list capacity per kind and chunk
 __device__ __forceinline__ void push_local(bool mine, int lane, int* cnt, unsigned short* list, int cap, int off,
-                                           int* gcnt, int* glist, int chunk0) {
+                                           int* gcnt, uint2* glist, uint2 cw) {
   unsigned m = __ballot_sync(0xffffffffu, mine);
   if (!m) return;
   int slot0 = 0;
@@ -1500,7 +1498,7 @@ __device__ __forceinline__ void push_local(bool mine, int lane, int* cnt, unsign
   const int slot = slot0 + __popc(m & ((1u << lane) - 1));
   if (!mine) return;
   if (slot < cap) list[slot] = (unsigned short)off;
-  else glist[atomicAdd(gcnt, 1)] = chunk0 + off;  // local list full: direct global append
+  else glist[atomicAdd(gcnt, 1)] = cw;  // local list full: direct global append
 }
 __global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
   TAC_PDL_WAIT();
@@ -1559,7 +1557,7 @@ __global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
   float* hc = d.cgap + (size_t)e * d.kmax;
   const uint2* ccorn = d.ccorn + (size_t)e * d.kmax;
   int* gcnt = d.nnear + 3 * e;
-  int* glist = d.nearl + (size_t)e * 3 * d.kmax;
+  uint2* glist = d.nearl + (size_t)e * 3 * d.kmax;
   const int lane = threadIdx.x & 31;
   bool any_far = false;
   for (int c0 = blockIdx.x * kClassChunk; c0 < n; c0 += gridDim.x * kClassChunk) {
@@ -1649,7 +1647,7 @@ __global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
 #pragma unroll
         for (int kk = 0; kk < 3; ++kk)  // per-kind near lists (convergent near-pair passes)
           push_local(near && kind[t] == kk, lane, &nn[kk], nl[kk], kClassNL, off[t], gcnt + kk,
-                     glist + (size_t)kk * d.kmax, c0);
+                     glist + (size_t)kk * d.kmax, cc[t]);
       }
     }
     __syncthreads();
@@ -1658,7 +1656,7 @@ __global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
 #pragma unroll
     for (int kk = 0; kk < 3; ++kk) {
       const int m = min(nn[kk], kClassNL);
-      for (int t = threadIdx.x; t < m; t += blockDim.x) glist[(size_t)kk * d.kmax + nbase[kk] + t] = c0 + nl[kk][t];
+      for (int t = threadIdx.x; t < m; t += blockDim.x) glist[(size_t)kk * d.kmax + nbase[kk] + t] = ccorn[c0 + nl[kk][t]];
     }
     __syncthreads();  // q / nl / counters reuse
   }
