@@ -1342,6 +1342,29 @@ __global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
   block_sums_contact(vals, d.acc, d.Es, e, smr);
 }
 
+// Warp-aggregated scatter of one gel vertex's 9 contact terms (g xyz, D xx yy zz xy xz yz):
+// lanes holding the same vertex (neighbouring pairs / anchors share gel vertices) are found
+// with __match_any_sync, their terms summed by shuffles, and one leader issues the 9
+// red.add -- the contact passes' cost is the scattered global atomics.  All 32 lanes call
+// it; key = 0xffffffff marks a lane with nothing to add.
+__device__ __forceinline__ void red9_agg(const Dev& d, int e, unsigned key, const float* val) {
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  if (key == 0xffffffffu) return;
+  float acc[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) acc[k] = 0.f;
+  for (unsigned m = peers; m; m &= m - 1) {
+    const int src = __ffs(m) - 1;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) acc[k] += __shfl_sync(peers, val[k], src);
+  }
+  if ((int)(threadIdx.x & 31) != __ffs(peers) - 1) return;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) atomicAdd(d.g + vidx(d, c, key, e), acc[c]);
+#pragma unroll
+  for (int c = 0; c < 6; ++c) atomicAdd(d.D + vidxD(d, c, key, e), acc[3 + c]);
+}
+
 // friction over the anchors: value, gradient, GN blocks, wrench; caches
 // mu lambda f1(s) per anchor for the curvature pass
 __global__ void __launch_bounds__(128) k_contact_friction(Dev d, double eps_f) {
@@ -1357,7 +1380,13 @@ __global__ void __launch_bounds__(128) k_contact_friction(Dev d, double eps_f) {
   double Ef = 0, gr[6] = {0, 0, 0, 0, 0, 0}, Dc[6] = {0, 0, 0, 0, 0, 0}, Dt[6] = {0, 0, 0, 0, 0, 0};
   const d3 cc = ld3(c);
   const int na = min(d.nanc[e], d.amax);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  // warp-uniform trip count (the aggregated scatter is a warp collective)
+  for (int b0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); b0 < na; b0 += gridDim.x * blockDim.x) {
+    const int i = b0 + lane;
+    float sc[3][9];
+    unsigned key[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu};
+    if (i < na) {
     const Anchor& A = d.anc[(size_t)e * d.amax + i];
     const int gid[3] = {A.gid[0], A.gid[1], A.gid[2]};
     const unsigned sid[3] = {A.sid01 & 0xffffu, A.sid01 >> 16, A.sid2};
@@ -1385,16 +1414,15 @@ __global__ void __launch_bounds__(128) k_contact_friction(Dev d, double eps_f) {
       if (v < 0) continue;
       double wk = A.w[k];
       d3 f = (f1 * wk) * Tt;
-      atomicAdd(d.g + vidx(d, 0, v, e), (float)f.x);
-      atomicAdd(d.g + vidx(d, 1, v, e), (float)f.y);
-      atomicAdd(d.g + vidx(d, 2, v, e), (float)f.z);
       double sw = f1 * wk * wk;  // GN: f1 w^2 T T^T (R8)
-      atomicAdd(d.D + vidxD(d, 0, v, e), (float)(sw * (t1.x * t1.x + t2.x * t2.x)));
-      atomicAdd(d.D + vidxD(d, 1, v, e), (float)(sw * (t1.y * t1.y + t2.y * t2.y)));
-      atomicAdd(d.D + vidxD(d, 2, v, e), (float)(sw * (t1.z * t1.z + t2.z * t2.z)));
-      atomicAdd(d.D + vidxD(d, 3, v, e), (float)(sw * (t1.x * t1.y + t2.x * t2.y)));
-      atomicAdd(d.D + vidxD(d, 4, v, e), (float)(sw * (t1.x * t1.z + t2.x * t2.z)));
-      atomicAdd(d.D + vidxD(d, 5, v, e), (float)(sw * (t1.y * t1.z + t2.y * t2.z)));
+      key[k] = (unsigned)v;
+      sc[k][0] = (float)f.x; sc[k][1] = (float)f.y; sc[k][2] = (float)f.z;
+      sc[k][3] = (float)(sw * (t1.x * t1.x + t2.x * t2.x));
+      sc[k][4] = (float)(sw * (t1.y * t1.y + t2.y * t2.y));
+      sc[k][5] = (float)(sw * (t1.z * t1.z + t2.z * t2.z));
+      sc[k][6] = (float)(sw * (t1.x * t1.y + t2.x * t2.y));
+      sc[k][7] = (float)(sw * (t1.x * t1.z + t2.x * t2.z));
+      sc[k][8] = (float)(sw * (t1.y * t1.z + t2.y * t2.z));
     }
     // indenter side: force f1 sig T tau on c, torque rho x (f1 T tau)
     d3 F = (f1 * sig) * Tt, tq = cross(rho, f1 * Tt);
@@ -1403,6 +1431,9 @@ __global__ void __launch_bounds__(128) k_contact_friction(Dev d, double eps_f) {
     add_sym(Dc, t2, f1 * sig * sig);
     add_sym(Dt, cross(rho, t1), f1);
     add_sym(Dt, cross(rho, t2), f1);
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) red9_agg(d, e, key[k], sc[k]);
   }
   double vals[20];
   vals[0] = 0;
