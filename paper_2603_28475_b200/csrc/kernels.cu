@@ -689,11 +689,15 @@ __global__ void __launch_bounds__(128) k_intersect_check(Dev d, int* hit) {
 // rebuilds inside the loop: only the envs k_alpha listed; work items = (listed env,
 // 32-primitive chunk) per WARP over a fixed grid, so cost follows the actual rebuild count
 // and no warp waits for another
+// rebuild work items carry kRebuildChunk primitives per warp (lanes beyond it idle): the
+// launch is set by its slowest warp, a warp executes the union of its lanes' divergent BVH
+// paths, and the rebuild has far fewer items than warp slots -- thinner items, shorter tail
+constexpr int kRebuildChunk = 8;
 __global__ void __launch_bounds__(128) k_broadphase_list(Dev d, double r) {
   TAC_PDL_WAIT();
   const int nreb = *d.nreb;
   const int ntot = d.nsv + d.nse + d.nst;
-  const int nchunk = (ntot + 31) / 32;
+  const int nchunk = (ntot + kRebuildChunk - 1) / kRebuildChunk;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __shared__ double Rw[kBpWarps][12];  // per-warp R, c of its current env
   if (lane == 0) g_bp_wcnt[w] = 0;
@@ -705,8 +709,9 @@ __global__ void __launch_bounds__(128) k_broadphase_list(Dev d, double r) {
     if (lane < 9) Rw[w][lane] = s.R[lane];
     else if (lane < 12) Rw[w][lane] = s.c[lane - 9];
     __syncwarp();
-    bp_range(d, e, ch * 32 + lane, ntot, ntot, r, d.cand + (size_t)e * d.kmax, d.ccorn + (size_t)e * d.kmax,
-             d.ncand + e, d.kmax, Rw[w], Rw[w] + 9);  // one round: prims [32 ch, 32 ch + 32)
+    bp_range(d, e, ch * kRebuildChunk + lane, min(ntot, (ch + 1) * kRebuildChunk), ntot, r,
+             d.cand + (size_t)e * d.kmax, d.ccorn + (size_t)e * d.kmax, d.ncand + e, d.kmax, Rw[w],
+             Rw[w] + 9);  // one round: prims [Q ch, Q ch + Q)
     bool over = false;
     bp_flush_warp(d, d.cand + (size_t)e * d.kmax, d.ccorn + (size_t)e * d.kmax, d.ncand + e, d.kmax, &over);
     if (over) d.es[e].ncand_over = 1;
