@@ -975,6 +975,7 @@ double brute_dmin(const Problem& P, const State& s) {  // debug: all primitive p
   return m;
 }
 
+constexpr double kRebuildAt = 0.75;  // R16: rebuild once the odometer passes this fraction of m_r
 enum Flags { F_CONV = 1, F_MAXIT = 2, F_NAN = 4, F_INFEAS = 8, F_LARGE = 16, F_OVERFLOW = 32, F_STAG = 64 };
 
 void build_anchors(const Problem& P, Step& S, const State& s, const std::vector<Pair>& C) {
@@ -1035,7 +1036,7 @@ void env_step(const Problem& P, Env& E, const double* target7, double h, const O
   const double mr = P.bp_margin, rad = P.dhat + P.bp_margin;
   std::vector<Pair> C = broad_phase_state(P, s, rad);
   build_anchors(P, S, s, C);
-  double Sacc = 0;
+  double Sacc = 0, Lrel = 0;
 
   Grad G, Gprev;
   Vecs p, pprev;
@@ -1060,9 +1061,11 @@ void env_step(const Problem& P, Env& E, const double* target7, double h, const O
       if (!ok) {
         ++halvings;
         if (halvings <= P.max_halvings) {
+          Sacc += 0.5 * alpha * Lrel;  // odometer: the path back from the rejected trial (R16)
           alpha *= 0.5;
           s = advance(P, s_prev, alpha, p);
         } else {  // give up along p: back to x_k, restart with -P g
+          Sacc += alpha * Lrel;
           s = s_prev;
           restart = true;
           reeval = true;
@@ -1107,14 +1110,14 @@ void env_step(const Problem& P, Env& E, const double* target7, double h, const O
     double a_bar = step_alpha_bar(gp, q);
     double a_ccd = alpha_ccd(P, s, C, p);
     alpha = std::min(a_up, std::min(a_bar, a_ccd));
+    if (!std::isfinite(alpha)) alpha = 0;
     int rebuilt = 0;
-    double Lrel = rel_motion(P, p);
-    if (Sacc + alpha * Lrel > mr) {  // rebuild check before moving (O4f)
-      C = broad_phase_state(P, s, rad);
-      Sacc = 0;
-      a_ccd = alpha_ccd(P, s, C, p);
-      alpha = std::min(a_up, std::min(a_bar, a_ccd));
-      if (!std::isfinite(alpha)) alpha = 0;
+    Lrel = rel_motion(P, p);
+    // R16: the list stays valid while the odometer <= m_r.  A step that would pass m_r is
+    // capped at it; the list is rebuilt at the new state once the odometer passes
+    // kRebuildAt * m_r (so a later cap never cuts a step below half of alpha_upper)
+    if (Lrel > 0 && Sacc + alpha * Lrel > kRebuildAt * mr) {
+      if (Sacc + alpha * Lrel > mr) alpha = std::max(0.0, (mr - Sacc) / Lrel);
       rebuilt = 1;
     }
     if (E.want_trace) {
@@ -1131,6 +1134,10 @@ void env_step(const Problem& P, Env& E, const double* target7, double h, const O
     gPg_prev = gPg;
     s = advance(P, s_prev, alpha, p);
     Sacc += alpha * Lrel;
+    if (rebuilt) {  // new candidates at the state just reached (O4f)
+      C = broad_phase_state(P, s, rad);
+      Sacc = 0;
+    }
     E.pg = pgn;
   }
   E.iters = it;

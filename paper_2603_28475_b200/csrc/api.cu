@@ -831,6 +831,13 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
       goto fail;
     if (cudaMallocHost(&sim->h_flag, sizeof(int)) != cudaSuccess) { rc = TAC_ENOMEM; goto fail; }
     if ((rc = upload_env_material(sim))) { sim->err = "upload per-env material"; goto fail; }
+    int prio_lo = 0, prio_hi = 0;  // the rebuild's few long warps must start before the element pass fills the SMs
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    if (cudaStreamCreateWithPriority(&d.side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d.ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      rc = TAC_ECUDA; sim->err = "side stream / events"; goto fail;
+    }
     // initial poses: per-env fp64 state on the host, then upload
     std::vector<EnvS> es(d.E);
     for (int e = 0; e < d.E; ++e) {
@@ -854,6 +861,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     launch_broadphase(d, false, 0);
     std::vector<int> run(d.Es, 1);
     if (cudaMemcpy(d.run, run.data(), sizeof(int) * d.Es, cudaMemcpyHostToDevice) != cudaSuccess) { rc = TAC_ECUDA; goto fail; }
+    cudaMemset(d.nreb, 0, sizeof(int));
     launch_eval(d, 1e-3, 0);  // energies at rest: infinite barrier energy <=> touching / intersecting
     if (cudaDeviceSynchronize() != cudaSuccess) { rc = TAC_ECUDA; sim->err = "initial feasibility check failed"; goto fail; }
     std::vector<EnvS> chk(d.E);
@@ -893,6 +901,9 @@ fail:
 tac_status tac_destroy(tac_sim* sim) {
   if (!sim) return TAC_OK;
   cudaSetDevice(sim->device);
+  if (sim->d.side) { cudaStreamSynchronize(sim->d.side); cudaStreamDestroy(sim->d.side); }
+  if (sim->d.ev_fork) cudaEventDestroy(sim->d.ev_fork);
+  if (sim->d.ev_join) cudaEventDestroy(sim->d.ev_join);
   for (void* p : sim->allocs) cudaFree(p);
   if (sim->h_flag) cudaFreeHost(sim->h_flag);
   delete sim->prof;
@@ -926,6 +937,7 @@ tac_status tac_step(tac_sim* sim, const float* target_poses, float dt, void* str
   g_launches = 0;
   g_prof = sim->prof;
   launch_step_setup(d, target_poses, h, sim->step_count++, s);  // a1
+  cudaMemsetAsync(d.nreb, 0, sizeof(int), s);  // rebuilds flagged by the last step's final alpha are superseded
   launch_broadphase(d, false, s);            // a2
   launch_anchors(d, h, s);                   // a3
   int K = sim->fixed_iters > 0 ? sim->fixed_iters : sim->max_iters;
@@ -1238,6 +1250,7 @@ tac_status tac_debug_eval(tac_sim* sim, int32_t env, const double* u_t, const do
   if ((st = scatter_vec(sim, d.u, env, u)) || (st = set_pose_current(sim, env, c, R))) return st;
   CK(cudaMemset(d.ncand + env, 0, sizeof(int)));
   launch_broadphase(d, false, 0);
+  CK(cudaMemset(d.nreb, 0, sizeof(int)));
   launch_eval(d, dt, 0);
   CK(cudaDeviceSynchronize());
   // results: accept kernel stored the energy and rigid terms in EnvS; g / D in the vectors

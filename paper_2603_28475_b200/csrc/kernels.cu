@@ -1859,11 +1859,13 @@ __global__ void k_accept(Dev d, double h) {
   if (s.halv <= d.max_halv) {
     double an = 0.5 * s.alpha;
     s.odo = s.odo_base + an * s.Lc;
+    s.S += (s.alpha - an) * s.Lc;  // candidate-list odometer: the path back from the trial (R16)
     d.dalpha[e] = (float)(an - s.alpha);
     s.alpha = an;
     apply_pose(s, an);
   } else {
     d.dalpha[e] = (float)(-s.alpha);
+    s.S += s.alpha * s.Lc;
     s.alpha = 0;
     s.odo = s.odo_base;
     for (int i = 0; i < 3; ++i) s.c[i] = s.cp[i];
@@ -2109,79 +2111,6 @@ __global__ void __launch_bounds__(256) k_dir_apply(Dev d) {
   }
 }
 
-// contact curvature (GN, R8) and the conservative step bound alpha_ccd (R15):
-// d(alpha) >= d - alpha l_n, l_n = max_A(-n.dz) + max_B(n.dz) + |p_theta| dhat/4
-// step bound over the fresh candidates of the envs that rebuilt (k_alpha list): work items
-// = (listed env, 128-candidate chunk); separating-axis certificate -> g_min, else exact
-// fp64 distance and the closest-point plane bound (R15)
-__global__ void __launch_bounds__(128) k_ccd_list(Dev d) {
-  TAC_PDL_WAIT();
-  const int nreb = *d.nreb;
-  __shared__ double R[9], c[3], pr[6];
-  __shared__ double smin[4], sg[4];
-  // items: (listed env j = item % nreb, chunk = item / nreb); chunks past an env's count skip
-  const int maxch = (d.kmax + blockDim.x - 1) / blockDim.x;
-  for (int item = blockIdx.x; item < nreb * maxch; item += gridDim.x) {
-    const int e = d.reb_list[item % nreb], ch = item / nreb;
-    if (ch * (int)blockDim.x >= min(d.ncand[e], d.kmax)) continue;  // uniform across the block
-    const EnvS& s = d.es[e];
-    __syncthreads();
-    if (threadIdx.x < 9) R[threadIdx.x] = s.R[threadIdx.x];
-    if (threadIdx.x < 3) c[threadIdx.x] = s.c[threadIdx.x];
-    if (threadIdx.x < 6) pr[threadIdx.x] = s.pr[threadIdx.x];
-    __syncthreads();
-    const d3 cc = ld3(c), pc = mk(pr[0], pr[1], pr[2]), pth = mk(pr[3], pr[4], pr[5]);
-    const double extra = nrm(pth) * d.dhat * 0.25;
-    double amin = INFINITY, gmin = INFINITY;
-    const int i = ch * blockDim.x + threadIdx.x;
-    if (i < min(d.ncand[e], d.kmax)) {
-      unsigned long long rec = d.cand[(size_t)e * d.kmax + i];
-      int kind = (int)(rec >> 62), a = (int)((rec >> 31) & 0x7fffffffu), b = (int)(rec & 0x7fffffffu);
-      Corners C = corners_of(d, kind, a, b);
-      d3 z[4], dz[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (C.ind[k]) {
-          z[k] = mv(R, ind_body(d, C.id[k])) + cc;
-          dz[k] = pc + cross(pth, z[k] - cc);
-        } else {
-          z[k] = gel_pos(d, d.u, C.id[k], e);
-          dz[k] = gel_vec(d, d.p, C.id[k], e);
-        }
-      }
-      double gsep;
-      if (far_cert(z, C.na, d.dhat, &gsep)) {
-        gmin = gsep;
-      } else {
-        DR D = pair_dist(kind, z);
-        d3 rr = mk(0, 0, 0);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) rr = rr + D.w[k] * z[k];
-        if (D.d > 0) {
-          d3 nn = (1.0 / D.d) * rr;
-          double la = -INFINITY, lb = -INFINITY;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if (k < C.na) la = fmax(la, -dot(nn, dz[k]));
-            else lb = fmax(lb, dot(nn, dz[k]));
-          }
-          double l = la + lb + extra;
-          if (l > 0) amin = (1 - d.ccd_s) * D.d / l;
-        }
-      }
-    }
-    amin = warp_min(amin);
-    gmin = warp_min(gmin);
-    if ((threadIdx.x & 31) == 0) { smin[threadIdx.x >> 5] = amin; sg[threadIdx.x >> 5] = gmin; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double m = INFINITY, g = INFINITY;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { m = fmin(m, smin[w]); g = fmin(g, sg[w]); }
-      if (m < INFINITY) atomic_min_pos(d.accu + (size_t)U_ACCD * d.Es + e, (float)m);
-      if (g < INFINITY) atomic_min_pos(d.accu + (size_t)U_GFAR * d.Es + e, (float)g);
-    }
-  }
-}
 
 // ------------------------------------------------------------------ a7/a8: step length (per env)
 // alpha = min(alpha_upper = dhat / (2 |p|_disp), alpha_bar = -g^T p / p^T H p,
@@ -2199,59 +2128,57 @@ __device__ void commit_alpha(const Dev& d, EnvS& s, int e, double a, double L) {
   d.run[e] = 1;
 }
 
-__global__ void k_alpha(Dev d, double h, int pass) {
+// R16: the candidate list stays valid while the odometer S <= m_r.  A step that would pass
+// m_r is capped at it; once S + alpha L_rel passes kRebuildAt m_r the env is listed and its
+// candidates are rebuilt at the state it moves to -- by k_broadphase_list right after the
+// next k_vert_pre, on a side stream concurrent with the element pass.  kRebuildAt keeps a
+// later cap from cutting a step below half of alpha_upper.
+constexpr double kRebuildAt = 0.75;
+__global__ void k_alpha(Dev d, double h) {
   TAC_PDL_WAIT();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= d.E) return;
   int rb = d.run[e];
   size_t Es = d.Es;
   EnvS& s = d.es[e];
-  if (pass == 1) {
-    if (!(rb & 2)) return;
-    double h2 = h * h;
-    d3 pc = mk(s.pr[0], s.pr[1], s.pr[2]), pth = mk(s.pr[3], s.pr[4], s.pr[5]);
-    double Mg = __uint_as_float(d.accu[U_M * Es + e]);
-    double Lg = __uint_as_float(d.accu[U_LREL * Es + e]);
-    double M = fmax(Mg, nrm(pc) + d.rho_max * nrm(pth));
-    double L = fmax(Lg, nrm(pc)) + d.rho_max * nrm(pth);
-    d3 dc = ld3(s.c) - ld3(s.cs);
-    double RRs[9];
-    mmT(s.R, s.Rs, RRs);
-    d3 phi = so3_log(RRs);
-    double q = d.acc[A_PHP * Es + e] + h2 * (spring_w(nrm(dc), d.k_t, d.f_max) * dot(pc, pc) +
-                                             spring_w(nrm(phi), d.k_r, d.t_max) * dot(pth, pth));
-    d.acc[A_PHP * Es + e] = 0.0;
-    d.accu[U_M * Es + e] = 0u;
-    d.accu[U_LREL * Es + e] = 0u;
-    double accd = (double)__uint_as_float(d.accu[U_ACCD * Es + e]);
-    double gfar = (double)__uint_as_float(d.accu[U_GFAR * Es + e]);
-    if (gfar < INFINITY && L > 0) accd = fmin(accd, (1 - d.ccd_s) * d.dhat / L);  // far pairs (R15)
-    d.accu[U_ACCD * Es + e] = 0x7f800000u;
-    d.accu[U_GFAR * Es + e] = 0x7f800000u;
-    double aup = M > 0 ? d.dhat / (2 * M) : INFINITY;
-    double abar = q > 0 ? -s.gp_prev / q : INFINITY;
-    double a = fmin(aup, fmin(abar, accd));
-    if (s.S + a * L > d.bp_margin) {  // rebuild before moving (O4f)
-      s.alpha = fmin(aup, abar);
-      s.Lrel_last = L;
-      s.ncand_max = max(s.ncand_max, d.ncand[e]);
-      s.rebuild += 1;
-      s.cache_ok = 0;
-      d.ncand[e] = 0;
-      d.run[e] = 2 | 4;
-      d.reb_list[atomicAdd(d.nreb, 1)] = e;  // compact list for k_broadphase_list / k_ccd_list
-      return;
-    }
-    commit_alpha(d, s, e, a, L);
-  } else {
-    if (!(rb & 4)) return;
-    double accd = (double)__uint_as_float(d.accu[U_ACCD * Es + e]);
-    double gfar = (double)__uint_as_float(d.accu[U_GFAR * Es + e]);
-    if (gfar < INFINITY && s.Lrel_last > 0) accd = fmin(accd, (1 - d.ccd_s) * d.dhat / s.Lrel_last);
-    d.accu[U_ACCD * Es + e] = 0x7f800000u;
-    d.accu[U_GFAR * Es + e] = 0x7f800000u;
+  if (!(rb & 2)) return;
+  double h2 = h * h;
+  d3 pc = mk(s.pr[0], s.pr[1], s.pr[2]), pth = mk(s.pr[3], s.pr[4], s.pr[5]);
+  double Mg = __uint_as_float(d.accu[U_M * Es + e]);
+  double Lg = __uint_as_float(d.accu[U_LREL * Es + e]);
+  double M = fmax(Mg, nrm(pc) + d.rho_max * nrm(pth));
+  double L = fmax(Lg, nrm(pc)) + d.rho_max * nrm(pth);
+  d3 dc = ld3(s.c) - ld3(s.cs);
+  double RRs[9];
+  mmT(s.R, s.Rs, RRs);
+  d3 phi = so3_log(RRs);
+  double q = d.acc[A_PHP * Es + e] + h2 * (spring_w(nrm(dc), d.k_t, d.f_max) * dot(pc, pc) +
+                                           spring_w(nrm(phi), d.k_r, d.t_max) * dot(pth, pth));
+  d.acc[A_PHP * Es + e] = 0.0;
+  d.accu[U_M * Es + e] = 0u;
+  d.accu[U_LREL * Es + e] = 0u;
+  double accd = (double)__uint_as_float(d.accu[U_ACCD * Es + e]);
+  double gfar = (double)__uint_as_float(d.accu[U_GFAR * Es + e]);
+  if (gfar < INFINITY && L > 0) accd = fmin(accd, (1 - d.ccd_s) * d.dhat / L);  // far pairs (R15)
+  d.accu[U_ACCD * Es + e] = 0x7f800000u;
+  d.accu[U_GFAR * Es + e] = 0x7f800000u;
+  double aup = M > 0 ? d.dhat / (2 * M) : INFINITY;
+  double abar = q > 0 ? -s.gp_prev / q : INFINITY;
+  double a = fmin(aup, fmin(abar, accd));
+  if (!isfinite(a)) a = 0;
+  bool reb = false;
+  if (L > 0 && s.S + a * L > kRebuildAt * d.bp_margin) {
+    if (s.S + a * L > d.bp_margin) a = fmax(0.0, (d.bp_margin - s.S) / L);
+    reb = true;
+  }
+  commit_alpha(d, s, e, a, L);
+  if (reb) {  // new candidates at the state this step reaches (O4f)
     s.S = 0;
-    commit_alpha(d, s, e, fmin(s.alpha, accd), s.Lrel_last);
+    s.ncand_max = max(s.ncand_max, d.ncand[e]);
+    s.rebuild += 1;
+    s.cache_ok = 0;
+    d.ncand[e] = 0;
+    d.reb_list[atomicAdd(d.nreb, 1)] = e;  // compact list for k_broadphase_list
   }
 }
 
@@ -2479,6 +2406,12 @@ void launch_anchors(const Dev& d, double h, cudaStream_t s) {
 }
 void launch_eval(const Dev& d, double h, cudaStream_t s) {
   LAUNCHP(KID_VERT_PRE, s, k_vert_pre, vgrid(d, d.nv), dim3(32, 8), 0, d, (float)(h * h));
+  // R16: candidates of the envs k_alpha listed, rebuilt at the state k_vert_pre just reached,
+  // on the side stream concurrently with the element pass; joined before the classification
+  cudaEventRecord(d.ev_fork, s);
+  cudaStreamWaitEvent(d.side, d.ev_fork, 0);
+  launch_broadphase(d, true, d.side);
+  cudaEventRecord(d.ev_join, d.side);
   // (a round-scheduled shared-memory tiled variant measured slower on C3: 740 vs 520 us at
   // 66 % warp utilisation in the rounds and 2 CTAs/SM; the coalesced red.add scatter stays)
   if (d.ncells > 0) {
@@ -2489,6 +2422,7 @@ void launch_eval(const Dev& d, double h, cudaStream_t s) {
     dim3 g = vgrid(d, d.nrest);
     LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
   }
+  cudaStreamWaitEvent(s, d.ev_join, 0);
   const size_t cls_smem = sizeof(float4) * (size_t)(d.nsv + d.niv);  // [nsv] X + u, [niv] c + R Y
   LAUNCHP(KID_CONTACT_CLASSIFY, s, k_contact_classify_staged, sgrid(d), 256, cls_smem, d);
   const double kap = h * h;  // kernels scale by their env's kappa_phys
@@ -2514,10 +2448,7 @@ void launch_curvature(const Dev& d, double h, cudaStream_t s) {
 }
 void launch_alpha(const Dev& d, double h, cudaStream_t s) {
   cudaMemsetAsync(d.nreb, 0, sizeof(int), s);
-  LAUNCHP(KID_ALPHA, s, k_alpha, eblocks32(d), 32, 0, d, h, 1);
-  launch_broadphase(d, true, s);
-  LAUNCHP(KID_CCD, s, k_ccd_list, 4 * 148, 128, 0, d);
-  LAUNCHP(KID_ALPHA, s, k_alpha, eblocks32(d), 32, 0, d, h, 2);
+  LAUNCHP(KID_ALPHA, s, k_alpha, eblocks32(d), 32, 0, d, h);
 }
 void launch_finalize(const Dev& d, double h, cudaStream_t s) {
   LAUNCHP(KID_FIN_VERT, s, k_finalize_vert, vgrid(d, d.nv), dim3(32, 8), 0, d, (float)(1.0 / h));
