@@ -834,7 +834,10 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     int prio_lo = 0, prio_hi = 0;  // the rebuild's few long warps must start before the element pass fills the SMs
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
     if (cudaStreamCreateWithPriority(&d.side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&d.side2, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&d.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d.ev_cls, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d.ev_join2, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&d.ev_join, cudaEventDisableTiming) != cudaSuccess) {
       rc = TAC_ECUDA; sim->err = "side stream / events"; goto fail;
     }
@@ -902,8 +905,9 @@ tac_status tac_destroy(tac_sim* sim) {
   if (!sim) return TAC_OK;
   cudaSetDevice(sim->device);
   if (sim->d.side) { cudaStreamSynchronize(sim->d.side); cudaStreamDestroy(sim->d.side); }
-  if (sim->d.ev_fork) cudaEventDestroy(sim->d.ev_fork);
-  if (sim->d.ev_join) cudaEventDestroy(sim->d.ev_join);
+  if (sim->d.side2) { cudaStreamSynchronize(sim->d.side2); cudaStreamDestroy(sim->d.side2); }
+  for (cudaEvent_t ev : {sim->d.ev_fork, sim->d.ev_join, sim->d.ev_cls, sim->d.ev_join2})
+    if (ev) cudaEventDestroy(ev);
   for (void* p : sim->allocs) cudaFree(p);
   if (sim->h_flag) cudaFreeHost(sim->h_flag);
   delete sim->prof;

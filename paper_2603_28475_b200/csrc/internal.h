@@ -90,8 +90,8 @@ struct Dev {
   const int2* se_l;      // [nse] surface-local vertex indices
   const int4* st_l;      // [nst] surface-local vertex indices
   int contact_smem;      // dynamic shared bytes of the staged contact kernels (0 = use the unstaged ones)
-  cudaStream_t side;     // per-simulator side stream: candidate rebuilds concurrent with the element pass
-  cudaEvent_t ev_fork, ev_join;
+  cudaStream_t side, side2;  // per-simulator high-priority streams: the contact chain concurrent with the element pass
+  cudaEvent_t ev_fork, ev_join, ev_cls, ev_join2;
   const float4* Y;       // [niv] body frame, w = |Y|
   const int2* ie;        // [nie]
   const int4* it;        // [nit]

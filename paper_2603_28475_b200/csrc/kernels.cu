@@ -2404,14 +2404,39 @@ void launch_intersect_check(const Dev& d, int* hit, cudaStream_t s) {
 void launch_anchors(const Dev& d, double h, cudaStream_t s) {
   LAUNCHP(KID_ANCHORS, s, k_anchors, cgrid(d), 128, 0, d, h * h);
 }
+// The element pass and the contact chain of an evaluation (and of the curvature pass) are
+// independent -- both start from the positions k_vert_pre reached and add into g, D and the
+// energy accumulators with atomics -- so the contact chain (with the candidate rebuild it
+// depends on) runs on the high-priority side stream concurrently with the element kernels,
+// joined before k_accept / k_alpha.  With per-launch profiling on, everything stays on the
+// caller's stream so each kernel's time is its own.
 void launch_eval(const Dev& d, double h, cudaStream_t s) {
   LAUNCHP(KID_VERT_PRE, s, k_vert_pre, vgrid(d, d.nv), dim3(32, 8), 0, d, (float)(h * h));
-  // R16: candidates of the envs k_alpha listed, rebuilt at the state k_vert_pre just reached,
-  // on the side stream concurrently with the element pass; joined before the classification
-  cudaEventRecord(d.ev_fork, s);
-  cudaStreamWaitEvent(d.side, d.ev_fork, 0);
-  launch_broadphase(d, true, d.side);
-  cudaEventRecord(d.ev_join, d.side);
+  const bool fork = g_prof == nullptr;
+  cudaStream_t cs = fork ? d.side : s, cs2 = fork ? d.side2 : s;
+  if (fork) {
+    cudaEventRecord(d.ev_fork, s);
+    cudaStreamWaitEvent(cs, d.ev_fork, 0);
+    cudaStreamWaitEvent(cs2, d.ev_fork, 0);
+  }
+  // friction needs only the anchors (fixed for the step) and the surface displacements
+  LAUNCHP(KID_CONTACT_FRICTION, cs2, k_contact_friction, cgrid(d), 128, 0, d, d.eps_v * h);
+  // R16: candidates of the envs k_alpha listed, rebuilt at the state k_vert_pre just reached
+  launch_broadphase(d, true, cs);
+  const size_t cls_smem = sizeof(float4) * (size_t)(d.nsv + d.niv);  // [nsv] X + u, [niv] c + R Y
+  LAUNCHP(KID_CONTACT_CLASSIFY, cs, k_contact_classify_staged, sgrid(d), 256, cls_smem, d);
+  const double kap = h * h;  // kernels scale by their env's kappa_phys
+  if (fork) {
+    cudaEventRecord(d.ev_cls, cs);
+    cudaStreamWaitEvent(cs2, d.ev_cls, 0);
+  }
+  LAUNCHP(KID_CONTACT_NEAR_EE, cs, k_contact_near<2>, cgrid(d), 128, 0, d, kap);
+  LAUNCHP(KID_CONTACT_GRAD, cs2, k_contact_near<0>, cgrid(d), 128, 0, d, kap);
+  LAUNCHP(KID_CONTACT_NEAR_IG, cs2, k_contact_near<1>, cgrid(d), 128, 0, d, kap);
+  if (fork) {
+    cudaEventRecord(d.ev_join, cs);
+    cudaEventRecord(d.ev_join2, cs2);
+  }
   // (a round-scheduled shared-memory tiled variant measured slower on C3: 740 vs 520 us at
   // 66 % warp utilisation in the rounds and 2 CTAs/SM; the coalesced red.add scatter stays)
   if (d.ncells > 0) {
@@ -2422,14 +2447,10 @@ void launch_eval(const Dev& d, double h, cudaStream_t s) {
     dim3 g = vgrid(d, d.nrest);
     LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
   }
-  cudaStreamWaitEvent(s, d.ev_join, 0);
-  const size_t cls_smem = sizeof(float4) * (size_t)(d.nsv + d.niv);  // [nsv] X + u, [niv] c + R Y
-  LAUNCHP(KID_CONTACT_CLASSIFY, s, k_contact_classify_staged, sgrid(d), 256, cls_smem, d);
-  const double kap = h * h;  // kernels scale by their env's kappa_phys
-  LAUNCHP(KID_CONTACT_GRAD, s, k_contact_near<0>, cgrid(d), 128, 0, d, kap);
-  LAUNCHP(KID_CONTACT_NEAR_IG, s, k_contact_near<1>, cgrid(d), 128, 0, d, kap);
-  LAUNCHP(KID_CONTACT_NEAR_EE, s, k_contact_near<2>, cgrid(d), 128, 0, d, kap);
-  LAUNCHP(KID_CONTACT_FRICTION, s, k_contact_friction, cgrid(d), 128, 0, d, d.eps_v * h);
+  if (fork) {
+    cudaStreamWaitEvent(s, d.ev_join, 0);
+    cudaStreamWaitEvent(s, d.ev_join2, 0);
+  }
   LAUNCHP(KID_ACCEPT, s, k_accept, eblocks32(d), 32, 0, d, h);
 }
 void launch_direction(const Dev& d, cudaStream_t s) {
@@ -2438,13 +2459,21 @@ void launch_direction(const Dev& d, cudaStream_t s) {
   LAUNCHP(KID_DIR_APPLY, s, k_dir_apply, vgrid(d, d.nv), dim3(32, 8), 0, d);
 }
 void launch_curvature(const Dev& d, double h, cudaStream_t s) {
+  const bool fork = g_prof == nullptr;  // contact curvature concurrent with the element curvature
+  cudaStream_t cs = fork ? d.side : s;
+  if (fork) {
+    cudaEventRecord(d.ev_fork, s);
+    cudaStreamWaitEvent(cs, d.ev_fork, 0);
+  }
+  LAUNCHP(KID_CONTACT_CURV, cs, k_contact_curv_staged, sgrid(d), 256, d.contact_smem, d, h * h);
+  if (fork) cudaEventRecord(d.ev_join, cs);
   if (d.nrest == 0) {  // every tet is in a Kuhn cell: register-blocked cells
     dim3 g = vgrid(d, d.ncells);
     LAUNCHP(KID_ELEM_CURV, s, k_elem_curv_cells, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
   } else {
     LAUNCHP(KID_ELEM_CURV, s, k_elem_curv_tiled, dim3(d.Es / 32, d.ntiles), 256, kTiledCurvSmem, d, (float)(h * h));
   }
-  LAUNCHP(KID_CONTACT_CURV, s, k_contact_curv_staged, sgrid(d), 256, d.contact_smem, d, h * h);
+  if (fork) cudaStreamWaitEvent(s, d.ev_join, 0);
 }
 void launch_alpha(const Dev& d, double h, cudaStream_t s) {
   cudaMemsetAsync(d.nreb, 0, sizeof(int), s);
