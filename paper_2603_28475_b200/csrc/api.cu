@@ -410,6 +410,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
   // diagonal end is corner 0 and which axis each 1-bit corner lies along
   std::vector<int4> cell_v;
   std::vector<unsigned> cell_fix;
+  std::vector<float4> cell_aa;  // axis-aligned cells: (1/s0, 1/s1, 1/s2, 1) with corner bit b along axis b
   std::vector<float4> cell_tb;
   std::vector<int> rest_tets;
   {
@@ -517,6 +518,28 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
           for (int s = 0; s < 8; ++s)
             if (vflag[lab[s]] & 1) fm |= 1u << s;
           cell_fix.push_back(fm);
+          {  // axis-aligned box with corner bit b along coordinate axis b (signed edge s_b)?
+            const V o = X[lab[0]];
+            const V e[3] = {sub(X[lab[1]], o), sub(X[lab[2]], o), sub(X[lab[4]], o)};
+            double len = 0;
+            for (int b = 0; b < 3; ++b) len = std::max(len, std::fabs(e[b][b]));
+            const double tol = 1e-9 * len;
+            bool aa = len > 0;
+            for (int b = 0; b < 3 && aa; ++b)
+              for (int a = 0; a < 3; ++a)
+                if (a != b && std::fabs(e[b][a]) > tol) aa = false;
+            for (int sl = 0; sl < 8 && aa; ++sl)
+              for (int a = 0; a < 3; ++a) {
+                double want = o[a];
+                for (int b = 0; b < 3; ++b)
+                  if (sl & (1 << b)) want += e[b][a];
+                if (std::fabs(X[lab[sl]][a] - want) > tol) aa = false;
+              }
+            // w = the common volume |s0 s1 s2| / 6 of the cell's six tets (> 0 marks the cell)
+            cell_aa.push_back(aa ? make_float4((float)(1.0 / e[0][0]), (float)(1.0 / e[1][1]), (float)(1.0 / e[2][2]),
+                                               (float)(std::fabs(e[0][0] * e[1][1] * e[2][2]) / 6.0))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f));
+          }
           for (int jt = 0; jt < 6; ++jt) {  // b-vectors of the canonical corner order, |det|/6
             V a0 = X[lab[kTet[jt][0]]];
             V a = sub(X[lab[kTet[jt][1]]], a0), b = sub(X[lab[kTet[jt][2]]], a0), c = sub(X[lab[kTet[jt][3]]], a0);
@@ -808,6 +831,12 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     UP(tile_sched, d.tile_sched);
     UP(cell_v, d.cell_v);
     UP(cell_fix, d.cell_fix);
+    UP(cell_aa, d.cell_aa);
+    if (getenv("TAC_DEBUG_CELLS")) {
+      size_t naa = 0;
+      for (auto& a : cell_aa) naa += a.w != 0.f;
+      fprintf(stderr, "cells: %zu, axis-aligned (bit b along axis b): %zu\n", cell_aa.size(), naa);
+    }
     UP(cell_tb, d.cell_tb);
     UP(rest_tets, d.rest_tets);
     d.ncells = (int)cell_fix.size();

@@ -971,6 +971,14 @@ __global__ void __launch_bounds__(256, 4) k_elem_grad(Dev d, float h2) {
 // canonical tets (corner slots): {0,1,3,7} {0,1,5,7} {0,2,3,7} {0,2,6,7} {0,4,5,7} {0,4,6,7}
 #define CELL_TET(j, k) ((k) == 0 ? 0 : (k) == 3 ? 7 : (j) < 2 ? ((k) == 1 ? 1 : ((j) == 0 ? 3 : 5)) \
                         : (j) < 4 ? ((k) == 1 ? 2 : ((j) == 2 ? 3 : 6)) : ((k) == 1 ? 4 : ((j) == 4 ? 5 : 6)))
+// corner bit flipped along step i of tet j's path 0 -> CELL_TET(j,1) -> CELL_TET(j,2) -> 7
+#define CELL_Q(j, i) ((i) == 0 ? ((j) >> 1) : (i) == 1 ? (((j) >> 1) == 0 ? 1 + ((j) & 1) : ((j) >> 1) == 1 ? 2 * ((j) & 1) : ((j) & 1)) \
+                      : 3 - ((j) >> 1) - (((j) >> 1) == 0 ? 1 + ((j) & 1) : ((j) >> 1) == 1 ? 2 * ((j) & 1) : ((j) & 1)))
+// Axis-aligned cells (structured pads: corner bit b along axis b, signed edge s_b): column
+// q_i of G is the scaled difference (u_{c_{i+1}} - u_{c_i}) / s_{q_i} along the path, and the
+// b rows are e_q0/s_q0 - e_q1/s_q1, e_q1/s_q1 - e_q2/s_q2, e_q2/s_q2, so the corner forces and
+// cofactor vectors are differences of scaled columns -- the same quantities with no 3x3
+// products against stored b rows (cell_aa.w = tet volume > 0 marks such a cell)
 
 __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
   TAC_PDL_WAIT();
@@ -983,6 +991,9 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
   for (int cidx = blockIdx.x * 8 + threadIdx.y; cidx < d.ncells; cidx += gridDim.x * 8) {
     const int4 va = __ldg(d.cell_v + 2 * cidx), vb4 = __ldg(d.cell_v + 2 * cidx + 1);
     const unsigned fix = __ldg(d.cell_fix + cidx);
+    const float4 caa = __ldg(d.cell_aa + cidx);
+    const bool aa = caa.w > 0.f;  // warp-uniform (one cell per warp)
+    const float inv[3] = {caa.x, caa.y, caa.z};
     if (!act) continue;
     const unsigned vb[8] = {(unsigned)va.x * G + eg, (unsigned)va.y * G + eg, (unsigned)va.z * G + eg,
                             (unsigned)va.w * G + eg, (unsigned)vb4.x * G + eg, (unsigned)vb4.y * G + eg,
@@ -1004,22 +1015,36 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
     }
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
-      const float4 r0 = __ldg(d.cell_tb + 18 * cidx + 3 * j), r1 = __ldg(d.cell_tb + 18 * cidx + 3 * j + 1),
-                   r2 = __ldg(d.cell_tb + 18 * cidx + 3 * j + 2);
-      const float b[3][3] = {{r0.x, r0.y, r0.z}, {r1.x, r1.y, r1.z}, {r2.x, r2.y, r2.z}};
       const int s0 = CELL_TET(j, 0), s1 = CELL_TET(j, 1), s2 = CELL_TET(j, 2), s3 = CELL_TET(j, 3);
-      float du[3][3];
+      const int q0 = CELL_Q(j, 0), q1 = CELL_Q(j, 1), q2 = CELL_Q(j, 2);
+      float Gm[9], b[3][3], vol;
+      if (aa) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        du[0][c] = u[s1][c] - u[s0][c];
-        du[1][c] = u[s2][c] - u[s0][c];
-        du[2][c] = u[s3][c] - u[s0][c];
+        for (int r = 0; r < 3; ++r) {
+          Gm[3 * r + q0] = (u[s1][r] - u[s0][r]) * inv[q0];
+          Gm[3 * r + q1] = (u[s2][r] - u[s1][r]) * inv[q1];
+          Gm[3 * r + q2] = (u[s3][r] - u[s2][r]) * inv[q2];
+        }
+        vol = caa.w;
+      } else {
+        const float4 r0 = __ldg(d.cell_tb + 18 * cidx + 3 * j), r1 = __ldg(d.cell_tb + 18 * cidx + 3 * j + 1),
+                     r2 = __ldg(d.cell_tb + 18 * cidx + 3 * j + 2);
+        b[0][0] = r0.x; b[0][1] = r0.y; b[0][2] = r0.z;
+        b[1][0] = r1.x; b[1][1] = r1.y; b[1][2] = r1.z;
+        b[2][0] = r2.x; b[2][1] = r2.y; b[2][2] = r2.z;
+        vol = r0.w;
+        float du[3][3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          du[0][c] = u[s1][c] - u[s0][c];
+          du[1][c] = u[s2][c] - u[s0][c];
+          du[2][c] = u[s3][c] - u[s0][c];
+        }
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int jj = 0; jj < 3; ++jj) Gm[3 * i + jj] = du[0][i] * b[0][jj] + du[1][i] * b[1][jj] + du[2][i] * b[2][jj];
       }
-      float Gm[9];
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int jj = 0; jj < 3; ++jj) Gm[3 * i + jj] = du[0][i] * b[0][jj] + du[1][i] * b[1][jj] + du[2][i] * b[2][jj];
       float trG = Gm[0] + Gm[4] + Gm[8];
       float i2 = (Gm[0] * Gm[4] - Gm[1] * Gm[3]) + (Gm[0] * Gm[8] - Gm[2] * Gm[6]) + (Gm[4] * Gm[8] - Gm[5] * Gm[7]);
       float cG[9];
@@ -1029,7 +1054,7 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
       float GG = 0.f;
 #pragma unroll
       for (int i = 0; i < 9; ++i) GG = fmaf(Gm[i], Gm[i], GG);
-      float w = h2 * r0.w;
+      float w = h2 * vol;
       esum += (double)(w * (mu * (0.5f * GG - i2 - detG) + 0.5f * l2 * Jm1 * Jm1));
       float cF[9], PK[9];
       const float lj = l2 * Jm1;
@@ -1041,26 +1066,49 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
           PK[3 * i + jj] = w * (mu * (Gm[3 * i + jj] + Gm[3 * jj + i] - (i == jj ? trG : 0.f) - cG[3 * i + jj]) + lj * cF[3 * i + jj]);
         }
       const float lc = w * l2;
-      float f0[3] = {0.f, 0.f, 0.f}, c0[3] = {0.f, 0.f, 0.f};
+      if (aa) {  // corner c: force and cofactor vector = differences of scaled columns
+        float Pt[3][3], Ct[3][3];
 #pragma unroll
-      for (int kk = 0; kk < 3; ++kk) {
-        const int sk = kk == 0 ? s1 : (kk == 1 ? s2 : s3);
-        float fv[3], cv[3];
+        for (int a = 0; a < 3; ++a)
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          fv[i] = PK[3 * i] * b[kk][0] + PK[3 * i + 1] * b[kk][1] + PK[3 * i + 2] * b[kk][2];
-          cv[i] = cF[3 * i] * b[kk][0] + cF[3 * i + 1] * b[kk][1] + cF[3 * i + 2] * b[kk][2];
-          f0[i] -= fv[i];
-          c0[i] -= cv[i];
-          ag[sk][i] += fv[i];
+          for (int i = 0; i < 3; ++i) { Pt[a][i] = PK[3 * i + a] * inv[a]; Ct[a][i] = cF[3 * i + a] * inv[a]; }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int sk = k == 0 ? s0 : (k == 1 ? s1 : (k == 2 ? s2 : s3));
+          float fv[3], cv[3];
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            if (k == 0) { fv[i] = -Pt[q0][i]; cv[i] = -Ct[q0][i]; }
+            else if (k == 1) { fv[i] = Pt[q0][i] - Pt[q1][i]; cv[i] = Ct[q0][i] - Ct[q1][i]; }
+            else if (k == 2) { fv[i] = Pt[q1][i] - Pt[q2][i]; cv[i] = Ct[q1][i] - Ct[q2][i]; }
+            else { fv[i] = Pt[q2][i]; cv[i] = Ct[q2][i]; }
+            ag[sk][i] += fv[i];
+          }
+          aD[sk][0] += lc * cv[0] * cv[0]; aD[sk][1] += lc * cv[1] * cv[1]; aD[sk][2] += lc * cv[2] * cv[2];
+          aD[sk][3] += lc * cv[0] * cv[1]; aD[sk][4] += lc * cv[0] * cv[2]; aD[sk][5] += lc * cv[1] * cv[2];
         }
-        aD[sk][0] += lc * cv[0] * cv[0]; aD[sk][1] += lc * cv[1] * cv[1]; aD[sk][2] += lc * cv[2] * cv[2];
-        aD[sk][3] += lc * cv[0] * cv[1]; aD[sk][4] += lc * cv[0] * cv[2]; aD[sk][5] += lc * cv[1] * cv[2];
-      }
+      } else {
+        float f0[3] = {0.f, 0.f, 0.f}, c0[3] = {0.f, 0.f, 0.f};
 #pragma unroll
-      for (int i = 0; i < 3; ++i) ag[s0][i] += f0[i];
-      aD[s0][0] += lc * c0[0] * c0[0]; aD[s0][1] += lc * c0[1] * c0[1]; aD[s0][2] += lc * c0[2] * c0[2];
-      aD[s0][3] += lc * c0[0] * c0[1]; aD[s0][4] += lc * c0[0] * c0[2]; aD[s0][5] += lc * c0[1] * c0[2];
+        for (int kk = 0; kk < 3; ++kk) {
+          const int sk = kk == 0 ? s1 : (kk == 1 ? s2 : s3);
+          float fv[3], cv[3];
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            fv[i] = PK[3 * i] * b[kk][0] + PK[3 * i + 1] * b[kk][1] + PK[3 * i + 2] * b[kk][2];
+            cv[i] = cF[3 * i] * b[kk][0] + cF[3 * i + 1] * b[kk][1] + cF[3 * i + 2] * b[kk][2];
+            f0[i] -= fv[i];
+            c0[i] -= cv[i];
+            ag[sk][i] += fv[i];
+          }
+          aD[sk][0] += lc * cv[0] * cv[0]; aD[sk][1] += lc * cv[1] * cv[1]; aD[sk][2] += lc * cv[2] * cv[2];
+          aD[sk][3] += lc * cv[0] * cv[1]; aD[sk][4] += lc * cv[0] * cv[2]; aD[sk][5] += lc * cv[1] * cv[2];
+        }
+#pragma unroll
+        for (int i = 0; i < 3; ++i) ag[s0][i] += f0[i];
+        aD[s0][0] += lc * c0[0] * c0[0]; aD[s0][1] += lc * c0[1] * c0[1]; aD[s0][2] += lc * c0[2] * c0[2];
+        aD[s0][3] += lc * c0[0] * c0[1]; aD[s0][4] += lc * c0[0] * c0[2]; aD[s0][5] += lc * c0[1] * c0[2];
+      }
     }
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
@@ -1091,6 +1139,9 @@ __global__ void __launch_bounds__(256, 2) k_elem_curv_cells(Dev d, float h2) {
   double qsum = 0;
   for (int cidx = blockIdx.x * 8 + threadIdx.y; cidx < d.ncells; cidx += gridDim.x * 8) {
     const int4 va = __ldg(d.cell_v + 2 * cidx), vb4 = __ldg(d.cell_v + 2 * cidx + 1);
+    const float4 caa = __ldg(d.cell_aa + cidx);
+    const bool aa = caa.w > 0.f;  // warp-uniform (one cell per warp)
+    const float inv[3] = {caa.x, caa.y, caa.z};
     if (!act) continue;
     const unsigned vb[8] = {(unsigned)va.x * G + eg, (unsigned)va.y * G + eg, (unsigned)va.z * G + eg,
                             (unsigned)va.w * G + eg, (unsigned)vb4.x * G + eg, (unsigned)vb4.y * G + eg,
@@ -1106,19 +1157,34 @@ __global__ void __launch_bounds__(256, 2) k_elem_curv_cells(Dev d, float h2) {
     float q = 0.f;
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
-      const float4 r0 = __ldg(d.cell_tb + 18 * cidx + 3 * j), r1 = __ldg(d.cell_tb + 18 * cidx + 3 * j + 1),
-                   r2 = __ldg(d.cell_tb + 18 * cidx + 3 * j + 2);
-      const float b[3][3] = {{r0.x, r0.y, r0.z}, {r1.x, r1.y, r1.z}, {r2.x, r2.y, r2.z}};
       const int s0 = CELL_TET(j, 0), s1 = CELL_TET(j, 1), s2 = CELL_TET(j, 2), s3 = CELL_TET(j, 3);
-      float Gm[9], dF[9];
+      const int q0 = CELL_Q(j, 0), q1 = CELL_Q(j, 1), q2 = CELL_Q(j, 2);
+      float Gm[9], dF[9], vol;
+      if (aa) {  // axis-aligned cell: scaled differences along the path (see CELL_Q)
 #pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const float du0 = u[s1][i] - u[s0][i], du1 = u[s2][i] - u[s0][i], du2 = u[s3][i] - u[s0][i];
-        const float dp0 = p[s1][i] - p[s0][i], dp1 = p[s2][i] - p[s0][i], dp2 = p[s3][i] - p[s0][i];
+        for (int r = 0; r < 3; ++r) {
+          Gm[3 * r + q0] = (u[s1][r] - u[s0][r]) * inv[q0];
+          Gm[3 * r + q1] = (u[s2][r] - u[s1][r]) * inv[q1];
+          Gm[3 * r + q2] = (u[s3][r] - u[s2][r]) * inv[q2];
+          dF[3 * r + q0] = (p[s1][r] - p[s0][r]) * inv[q0];
+          dF[3 * r + q1] = (p[s2][r] - p[s1][r]) * inv[q1];
+          dF[3 * r + q2] = (p[s3][r] - p[s2][r]) * inv[q2];
+        }
+        vol = caa.w;
+      } else {
+        const float4 r0 = __ldg(d.cell_tb + 18 * cidx + 3 * j), r1 = __ldg(d.cell_tb + 18 * cidx + 3 * j + 1),
+                     r2 = __ldg(d.cell_tb + 18 * cidx + 3 * j + 2);
+        const float b[3][3] = {{r0.x, r0.y, r0.z}, {r1.x, r1.y, r1.z}, {r2.x, r2.y, r2.z}};
+        vol = r0.w;
 #pragma unroll
-        for (int jj = 0; jj < 3; ++jj) {
-          Gm[3 * i + jj] = du0 * b[0][jj] + du1 * b[1][jj] + du2 * b[2][jj];
-          dF[3 * i + jj] = dp0 * b[0][jj] + dp1 * b[1][jj] + dp2 * b[2][jj];
+        for (int i = 0; i < 3; ++i) {
+          const float du0 = u[s1][i] - u[s0][i], du1 = u[s2][i] - u[s0][i], du2 = u[s3][i] - u[s0][i];
+          const float dp0 = p[s1][i] - p[s0][i], dp1 = p[s2][i] - p[s0][i], dp2 = p[s3][i] - p[s0][i];
+#pragma unroll
+          for (int jj = 0; jj < 3; ++jj) {
+            Gm[3 * i + jj] = du0 * b[0][jj] + du1 * b[1][jj] + du2 * b[2][jj];
+            dF[3 * i + jj] = dp0 * b[0][jj] + dp1 * b[1][jj] + dp2 * b[2][jj];
+          }
         }
       }
       float trG = Gm[0] + Gm[4] + Gm[8];
@@ -1139,7 +1205,7 @@ __global__ void __launch_bounds__(256, 2) k_elem_curv_cells(Dev d, float h2) {
           cfd = fmaf(cF, dF[3 * i + jj], cfd);
           fcd = fmaf(Fij, cd[3 * i + jj], fcd);
         }
-      q += r0.w * (mu * dd + l2 * cfd * cfd + 2.f * (l2 * Jm1 - mu) * fcd);
+      q += vol * (mu * dd + l2 * cfd * cfd + 2.f * (l2 * Jm1 - mu) * fcd);
     }
     qsum += (double)(h2 * q);
   }
