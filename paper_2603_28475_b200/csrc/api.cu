@@ -832,6 +832,8 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     UP(cell_v, d.cell_v);
     UP(cell_fix, d.cell_fix);
     UP(cell_aa, d.cell_aa);
+    d.cells_all_aa = !cell_aa.empty();
+    for (auto& a : cell_aa) d.cells_all_aa = d.cells_all_aa && a.w > 0.f;
     if (getenv("TAC_DEBUG_CELLS")) {
       size_t naa = 0;
       for (auto& a : cell_aa) naa += a.w != 0.f;

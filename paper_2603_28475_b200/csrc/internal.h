@@ -154,6 +154,7 @@ struct Dev {
   const unsigned* cell_fix;      // [ncells] bit s: corner s fixed
   const float4* cell_tb;         // [ncells][6][3] (b1, vol), (b2, 0), (b3, 0) in canonical corner order
   const float4* cell_aa;         // [ncells] axis-aligned box (corner bit b along axis b): (1/s0, 1/s1, 1/s2, tet volume), else 0
+  int cells_all_aa;              // every cell axis-aligned: the cell kernels compile the stored-B branch out
   const int* rest_tets;          // [nrest] tets not in any cell
   double t1[3], t2[3], nrm[3];
 };

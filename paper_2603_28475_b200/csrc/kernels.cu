@@ -980,6 +980,9 @@ __global__ void __launch_bounds__(256, 4) k_elem_grad(Dev d, float h2) {
 // cofactor vectors are differences of scaled columns -- the same quantities with no 3x3
 // products against stored b rows (cell_aa.w = tet volume > 0 marks such a cell)
 
+// ALL_AA: every cell of the mesh is axis-aligned (structured pads) -- the stored-B branch is
+// compiled out, which frees the registers it would hold
+template <bool ALL_AA>
 __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
   TAC_PDL_WAIT();
   const int e = blockIdx.y * 32 + threadIdx.x;
@@ -992,7 +995,7 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
     const int4 va = __ldg(d.cell_v + 2 * cidx), vb4 = __ldg(d.cell_v + 2 * cidx + 1);
     const unsigned fix = __ldg(d.cell_fix + cidx);
     const float4 caa = __ldg(d.cell_aa + cidx);
-    const bool aa = caa.w > 0.f;  // warp-uniform (one cell per warp)
+    const bool aa = ALL_AA || caa.w > 0.f;  // warp-uniform (one cell per warp)
     const float inv[3] = {caa.x, caa.y, caa.z};
     if (!act) continue;
     const unsigned vb[8] = {(unsigned)va.x * G + eg, (unsigned)va.y * G + eg, (unsigned)va.z * G + eg,
@@ -1129,6 +1132,7 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
 
 // ---- Kuhn-cell element curvature: one warp = one cell x 32 envs, u and p of the 8 corners
 // in registers; p^T H_e p summed over the 6 tets (App. B quadratic form)
+template <bool ALL_AA>
 __global__ void __launch_bounds__(256, 2) k_elem_curv_cells(Dev d, float h2) {
   TAC_PDL_WAIT();
   const int e = blockIdx.y * 32 + threadIdx.x;
@@ -1140,7 +1144,7 @@ __global__ void __launch_bounds__(256, 2) k_elem_curv_cells(Dev d, float h2) {
   for (int cidx = blockIdx.x * 8 + threadIdx.y; cidx < d.ncells; cidx += gridDim.x * 8) {
     const int4 va = __ldg(d.cell_v + 2 * cidx), vb4 = __ldg(d.cell_v + 2 * cidx + 1);
     const float4 caa = __ldg(d.cell_aa + cidx);
-    const bool aa = caa.w > 0.f;  // warp-uniform (one cell per warp)
+    const bool aa = ALL_AA || caa.w > 0.f;  // warp-uniform (one cell per warp)
     const float inv[3] = {caa.x, caa.y, caa.z};
     if (!act) continue;
     const unsigned vb[8] = {(unsigned)va.x * G + eg, (unsigned)va.y * G + eg, (unsigned)va.z * G + eg,
@@ -2507,7 +2511,8 @@ void launch_eval(const Dev& d, double h, cudaStream_t s) {
   // 66 % warp utilisation in the rounds and 2 CTAs/SM; the coalesced red.add scatter stays)
   if (d.ncells > 0) {
     dim3 g = vgrid(d, d.ncells);
-    LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad_cells, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
+    if (d.cells_all_aa) LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad_cells<true>, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
+    else LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad_cells<false>, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
   }
   if (d.nrest > 0) {
     dim3 g = vgrid(d, d.nrest);
@@ -2535,7 +2540,8 @@ void launch_curvature(const Dev& d, double h, cudaStream_t s) {
   if (fork) cudaEventRecord(d.ev_join, cs);
   if (d.nrest == 0) {  // every tet is in a Kuhn cell: register-blocked cells
     dim3 g = vgrid(d, d.ncells);
-    LAUNCHP(KID_ELEM_CURV, s, k_elem_curv_cells, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
+    if (d.cells_all_aa) LAUNCHP(KID_ELEM_CURV, s, k_elem_curv_cells<true>, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
+    else LAUNCHP(KID_ELEM_CURV, s, k_elem_curv_cells<false>, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
   } else {
     LAUNCHP(KID_ELEM_CURV, s, k_elem_curv_tiled, dim3(d.Es / 32, d.ntiles), 256, kTiledCurvSmem, d, (float)(h * h));
   }
