@@ -105,7 +105,7 @@ typedef struct {
  *   max_halvings    Armijo halvings before restarting along -P g
  *   stagnation      iterations without |P g| progress before giving up (0 = off)
  *   max_candidates  per-env capacity of candidate pairs (0 = default 16384)
- *   max_anchors     per-env capacity of friction anchors (0 = default 4096)
+ *   max_anchors     per-env capacity of friction anchors (0 = default 4096; at most 16384)
  *   check_every     tolerance mode: host polls "all envs done" every N iterations */
 typedef struct {
   double dhat, kappa_phys, eps_v, tol_x, k_t, k_r, f_max, t_max, ccd_s, bp_margin, c1, eps_E;

@@ -665,6 +665,10 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
   d.Es = (d.E + 31) / 32 * 32;
   d.kmax = P.max_candidates > 0 ? P.max_candidates : 16384;
   d.amax = P.max_anchors > 0 ? P.max_anchors : 4096;
+  if (d.amax > 16384) {  // the per-step anchor sort holds next_pow2(max_anchors) keys in shared memory
+    delete sim;
+    return fail(TAC_EINVAL, "max_anchors > 16384");
+  }
   d.mu = (float)(MT.E / (2 * (1 + MT.nu)));
   double lam = MT.E * MT.nu / ((1 + MT.nu) * (1 - 2 * MT.nu));
   d.lam2 = (float)(lam + MT.E / (2 * (1 + MT.nu)));
@@ -855,7 +859,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
         (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.cand)) || (rc = zalloc(sim, 2 * (size_t)d.E * d.kmax, &d.cgeo)) || (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.cgap)) || (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.ccorn)) || (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.ncorn)) || (rc = zalloc(sim, (size_t)d.E, &d.ncand)) || (rc = zalloc(sim, 3 * (size_t)d.E * d.kmax, &d.nearl)) ||
         (rc = zalloc(sim, 3 * (size_t)d.E, &d.nnear)) ||
         (rc = zalloc(sim, (size_t)std::max(1, d.nsv) * d.Es, &d.usurf)) || (rc = zalloc(sim, (size_t)std::max(1, d.nsv) * d.Es, &d.psurf)) ||
-        (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc)) || (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc_f1)) || (rc = zalloc(sim, (size_t)d.E, &d.nanc)) || (rc = zalloc(sim, (size_t)d.E, &d.reb_list)) ||
+        (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc)) || (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc2)) || (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc_f1)) || (rc = zalloc(sim, (size_t)d.E, &d.nanc)) || (rc = zalloc(sim, (size_t)d.E, &d.reb_list)) ||
         (rc = zalloc(sim, 1, &d.nreb)) ||
         (rc = zalloc(sim, 1, &sim->d_flag)) || (rc = zalloc(sim, (size_t)d.kmax, &sim->d_dbg_cand)) ||
         (rc = zalloc(sim, 1, &sim->d_dbg_cnt)) || (rc = zalloc(sim, 3 * (size_t)nv, &sim->d_scratch)))
@@ -975,6 +979,8 @@ tac_status tac_step(tac_sim* sim, const float* target_poses, float dt, void* str
   cudaMemsetAsync(d.nreb, 0, sizeof(int), s);  // rebuilds flagged by the last step's final alpha are superseded
   launch_broadphase(d, false, s);            // a2
   launch_anchors(d, h, s);                   // a3
+  launch_sort_anchors(d, sim->d.anc2, s);    // neighbouring anchors share gel corners (friction scatter)
+  std::swap(sim->d.anc, sim->d.anc2);        // launches below read the sorted buffer
   int K = sim->fixed_iters > 0 ? sim->fixed_iters : sim->max_iters;
   for (int it = 0; it < K; ++it) {
     launch_eval(d, h, s);       // a4 + a5 + Armijo (a8)

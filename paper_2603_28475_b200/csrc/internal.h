@@ -122,7 +122,8 @@ struct Dev {
   const int* sidx;       // [nv] surface-local index of a gel vertex, -1 if not on the surface
   float4* usurf;         // [nsv][Es] u of the surface vertices at the last evaluation
   float4* psurf;         // [nsv][Es] p of the surface vertices (current direction)
-  Anchor* anc;           // [E][amax]
+  Anchor* anc;           // [E][amax] (sorted per step by gel corners; see k_sort_anchors)
+  Anchor* anc2;          // [E][amax] the other buffer of the per-step sort (pointers swapped)
   float* anc_f1;         // [E][amax] friction weight mu lambda f1(s) of the last evaluation
   int* nanc;             // [E]
   int* reb_list;         // [E] envs that rebuild their candidates in this iteration
@@ -170,6 +171,7 @@ void launch_curvature(const Dev& d, double h, cudaStream_t s);
 void launch_alpha(const Dev& d, double h, cudaStream_t s);
 void launch_finalize(const Dev& d, double h, cudaStream_t s);
 void launch_intersect_check(const Dev& d, int* hit, cudaStream_t s);  // tac_create validation
+void launch_sort_anchors(const Dev& d, Anchor* out, cudaStream_t s);  // per-step anchor order
 void launch_markers(const Dev& d, float* out, int ncomp, cudaStream_t s);
 void launch_marker_sqerr(const Dev& d, const float* ref, double* acc, int ncomp, cudaStream_t s);
 void launch_reset(const Dev& d, const unsigned char* mask, const float* poses, cudaStream_t s);

@@ -1417,27 +1417,65 @@ __global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
   block_sums_contact(vals, d.acc, d.Es, e, smr);
 }
 
-// Warp-aggregated scatter of one gel vertex's 9 contact terms (g xyz, D xx yy zz xy xz yz):
-// lanes holding the same vertex (neighbouring pairs / anchors share gel vertices) are found
-// with __match_any_sync, their terms summed by shuffles, and one leader issues the 9
-// red.add -- the contact passes' cost is the scattered global atomics.  All 32 lanes call
-// it; key = 0xffffffff marks a lane with nothing to add.
-__device__ __forceinline__ void red9_agg(const Dev& d, int e, unsigned key, const float* val) {
-  const unsigned peers = __match_any_sync(0xffffffffu, key);
-  if (key == 0xffffffffu) return;
-  float acc[9];
+
+// Run-based warp reduction of one gel vertex's 9 contact terms: maximal runs of equal
+// adjacent keys (anchors are sorted per step, so an anchor's gel primitive repeats in
+// neighbouring lanes) are summed by a log-step segmented scan and the run's last lane issues
+// the red.add.  Correct for any order (non-adjacent duplicates form separate runs).
+__device__ __forceinline__ void seg_red9(const Dev& d, int e, unsigned key, float* v) {
+  const int lane = threadIdx.x & 31;
+  const unsigned prev = __shfl_up_sync(0xffffffffu, key, 1), next = __shfl_down_sync(0xffffffffu, key, 1);
+  const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || prev != key);
+  const int start = 31 - __clz(heads & (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u)));
 #pragma unroll
-  for (int k = 0; k < 9; ++k) acc[k] = 0.f;
-  for (unsigned m = peers; m; m &= m - 1) {
-    const int src = __ffs(m) - 1;
+  for (int off = 1; off < 32; off <<= 1) {
 #pragma unroll
-    for (int k = 0; k < 9; ++k) acc[k] += __shfl_sync(peers, val[k], src);
+    for (int k = 0; k < 9; ++k) {
+      const float t = __shfl_up_sync(0xffffffffu, v[k], off);
+      if (lane - off >= start) v[k] += t;
+    }
   }
-  if ((int)(threadIdx.x & 31) != __ffs(peers) - 1) return;
+  if (key == 0xffffffffu || (lane != 31 && next == key)) return;  // only the run's last lane
 #pragma unroll
-  for (int c = 0; c < 3; ++c) atomicAdd(d.g + vidx(d, c, key, e), acc[c]);
+  for (int c = 0; c < 3; ++c) atomicAdd(d.g + vidx(d, c, key, e), v[c]);
 #pragma unroll
-  for (int c = 0; c < 6; ++c) atomicAdd(d.D + vidxD(d, c, key, e), acc[3 + c]);
+  for (int c = 0; c < 6; ++c) atomicAdd(d.D + vidxD(d, c, key, e), v[3 + c]);
+}
+
+// per-step anchor order: by (first, second) free gel corner, so anchors of one gel primitive
+// sit in neighbouring lanes of the friction pass (seg_red9).  One CTA per env, bitonic sort
+// of (key | index) in shared memory, then a gather into the second anchor buffer.
+__global__ void __launch_bounds__(1024) k_sort_anchors(Dev d, Anchor* out) {
+  TAC_PDL_WAIT();
+  extern __shared__ unsigned long long skey[];
+  const int e = blockIdx.x;
+  if (d.es[e].mode != kActive) return;
+  const int na = min(d.nanc[e], d.amax);
+  int n = 1;
+  while (n < na) n <<= 1;
+  const Anchor* in = d.anc + (size_t)e * d.amax;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    if (i < na) {
+      const unsigned long long g0 = (unsigned)(in[i].gid[0] + 1), g1 = (unsigned)(in[i].gid[1] + 1);
+      skey[i] = (g0 << 42) | (g1 << 20) | (unsigned long long)i;
+    } else {
+      skey[i] = ~0ull;
+    }
+  }
+  __syncthreads();
+  for (int k = 2; k <= n; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const unsigned long long a = skey[i], b = skey[l];
+          if (((i & k) == 0) == (a > b)) { skey[i] = b; skey[l] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  Anchor* o = out + (size_t)e * d.amax;
+  for (int i = threadIdx.x; i < na; i += blockDim.x) o[i] = in[skey[i] & 0xfffffull];
 }
 
 // friction over the anchors: value, gradient, GN blocks, wrench; caches
@@ -1508,7 +1546,13 @@ __global__ void __launch_bounds__(128) k_contact_friction(Dev d, double eps_f) {
     add_sym(Dt, cross(rho, t2), f1);
     }
 #pragma unroll
-    for (int k = 0; k < 3; ++k) red9_agg(d, e, key[k], sc[k]);
+    for (int k = 0; k < 3; ++k) {
+      if (key[k] == 0xffffffffu) {
+#pragma unroll
+        for (int m = 0; m < 9; ++m) sc[k][m] = 0.f;
+      }
+      seg_red9(d, e, key[k], sc[k]);
+    }
   }
   double vals[20];
   vals[0] = 0;
@@ -2474,6 +2518,11 @@ void launch_intersect_check(const Dev& d, int* hit, cudaStream_t s) {
 void launch_anchors(const Dev& d, double h, cudaStream_t s) {
   LAUNCHP(KID_ANCHORS, s, k_anchors, cgrid(d), 128, 0, d, h * h);
 }
+void launch_sort_anchors(const Dev& d, Anchor* out, cudaStream_t s) {
+  int n = 1;
+  while (n < d.amax) n <<= 1;
+  LAUNCHP(KID_ANCHORS, s, k_sort_anchors, d.E, 1024, sizeof(unsigned long long) * n, d, out);
+}
 // The element pass and the contact chain of an evaluation (and of the curvature pass) are
 // independent -- both start from the positions k_vert_pre reached and add into g, D and the
 // energy accumulators with atomics -- so the contact chain (with the candidate rebuild it
@@ -2589,6 +2638,7 @@ int contact_smem_bytes(int nsv, int niv) {
   return b <= (size_t)kContactSmemCap ? (int)b : 0;
 }
 void kernels_init(int contact_smem) {
+  cudaFuncSetAttribute(k_sort_anchors, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   // the attribute belongs to the kernel, not to a simulator: several simulators in one
   // process (different meshes) share it, so it is set to the cap contact_smem_bytes
   // enforces rather than to this simulator's size (occupancy follows the launch size)
