@@ -1573,17 +1573,14 @@ __global__ void __launch_bounds__(128) k_contact_friction(Dev d, double eps_f) {
 // 32-byte sectors per gel corner.  Pass 1 classifies (separating-axis certificate ->
 // g_min; otherwise a block-local near list), pass 2 runs the exact fp64 distances on
 // convergent warps, pass 3 the friction anchors.
-constexpr int kNearCap = 2048;
 struct Stage {
   float4* sv4;  // [nsv] staged per-surface-vertex vector (u or p)
-  double* sy;   // [3 niv] R Y
-  int* nl;      // [kNearCap] block near list
+  float4* sy;   // [niv] R Y (fp32: only motion bounds and GN terms use it)
 };
 __device__ __forceinline__ Stage stage_ptrs(const Dev& d, char* sh) {
   Stage S;
-  S.sy = reinterpret_cast<double*>(sh);
-  S.sv4 = reinterpret_cast<float4*>(sh + sizeof(double) * 3 * d.niv);
-  S.nl = reinterpret_cast<int*>(sh + sizeof(double) * 3 * d.niv + sizeof(float4) * d.nsv);
+  S.sy = reinterpret_cast<float4*>(sh);
+  S.sv4 = reinterpret_cast<float4*>(sh + sizeof(float4) * d.niv);
   return S;
 }
 // staging loops issue kStageILP independent loads per thread before the shared stores
@@ -1615,15 +1612,10 @@ __device__ void stage_env(const Dev& d, const Stage& S, const float4* surf, int 
       const int j = j0 + k * blockDim.x;
       if (j < d.niv) {
         d3 y = mv(R, mk(yb[k].x, yb[k].y, yb[k].z));
-        S.sy[3 * j] = y.x; S.sy[3 * j + 1] = y.y; S.sy[3 * j + 2] = y.z;
+        S.sy[j] = make_float4((float)y.x, (float)y.y, (float)y.z, 0.f);
       }
     }
   }
-}
-__device__ __forceinline__ d3 staged_gel_pos(const Dev& d, const Stage& S, int gid, int sid) {
-  float4 X = __ldg(d.X + gid);
-  float4 u = S.sv4[sid];
-  return mk((double)X.x + (double)u.x, (double)X.y + (double)u.y, (double)X.z + (double)u.z);
 }
 
 // staged classification.  Phase A reads each candidate's cached certificate h = g +
@@ -1834,7 +1826,10 @@ __global__ void __launch_bounds__(256) k_contact_curv_staged(Dev d, double h2) {
   double extra = nrm(pth) * d.dhat * 0.25;
   // motion per unit alpha of corner id (indenter vertex or surface-local gel id)
   auto motion = [&](bool ind, unsigned id) -> d3 {
-    if (ind) return pc + cross(pth, mk(S.sy[3 * id], S.sy[3 * id + 1], S.sy[3 * id + 2]));
+    if (ind) {
+      const float4 y = S.sy[id];
+      return pc + cross(pth, mk(y.x, y.y, y.z));
+    }
     float4 p = S.sv4[id];
     return mk(p.x, p.y, p.z);
   };
@@ -2634,7 +2629,8 @@ void launch_debug_broadphase(const Dev& d, double r, unsigned long long* out, in
 }
 constexpr int kContactSmemCap = 160 * 1024;  // staged contact kernels: largest dynamic shared size
 int contact_smem_bytes(int nsv, int niv) {
-  size_t b = sizeof(double) * 3 * (size_t)niv + sizeof(float4) * (size_t)nsv + sizeof(int) * kNearCap;
+  // classify and the staged curvature pass: [nsv + niv] float4
+  size_t b = sizeof(float4) * (size_t)(nsv + niv);
   return b <= (size_t)kContactSmemCap ? (int)b : 0;
 }
 void kernels_init(int contact_smem) {
