@@ -131,7 +131,12 @@ def run_ours(args, rank, local, ws):
         scene = w.scene_c3_unstructured(n_envs=E, n_steps=nsteps, seed0=20260000 + e0)
     else:
         scene = w.scene_c3(n_envs=E, n_steps=nsteps, seed0=20260000 + e0)
-    scene.params.fixed_iters = FIXED_ITERS
+    if args.tol is not None:  # tolerance mode (SURVEY §8d.1 timing protocol iii)
+        scene.params.fixed_iters = 0
+        scene.params.tol_x = args.tol
+        scene.params.max_iters = args.max_iters
+    else:
+        scene.params.fixed_iters = args.iters
     if os.environ.get("TAC_BP_MARGIN"):  # experiments only (candidate margin sweep)
         scene.params.bp_margin = float(os.environ["TAC_BP_MARGIN"])
     sim = P.TacSim.from_scene(scene, device=local)
@@ -163,6 +168,7 @@ def run_ours(args, rank, local, ws):
     t1 = torch.cuda.Event(enable_timing=True)
     # headline timed region: no per-launch events (they would add their own gaps)
     t0.record(stream)
+    iters_per_step = []
     for k in range(args.warmup, args.warmup + args.steps):
         sim.step(poses[k], scene.dt)
         launches += sim.last_launch_count()
@@ -170,6 +176,9 @@ def run_ours(args, rank, local, ws):
         launches += sim.last_launch_count()
         if gather is not None:
             gather.gather()
+        if args.tol is not None:  # tolerance mode: per-env iteration counts of this step
+            iters_per_step.append(sim.env_status()[0])
+            launches += 1
     t1.record(stream)
     torch.cuda.synchronize()
     if dist.is_initialized():
@@ -265,20 +274,36 @@ def run_ours(args, rank, local, ws):
 
     it, pg, fl = sim.env_status()
     stt = sim.env_stats().float()
+    if iters_per_step:
+        its = torch.stack(iters_per_step).float().flatten().cpu().numpy()
+    else:
+        its = np.full(E, float(args.iters))
+    mean_it = float(its.mean())
+    # whole-iteration HBM fraction (SURVEY §8d.2 "Reporting" 1): algorithmic bytes of one
+    # PNCG iteration of one env (phases A + B + C per free vertex, static mesh amortised)
+    b_iter = 180.0 * nfree + 112.0 * scene.tets.shape[0] / E
+    hbm_it = {"bytes_per_env_iter": round(b_iter, 1),
+              "achieved_gbs": round(value * mean_it * b_iter / 1e9, 1), "peak_gbs": float(peaks["hbm_gbs"]),
+              "note": "180 B per free vertex per iteration (read u,p,u^; write u,g,D | read g,g_prev,p,D; write p | "
+                      "read u,p) + 112 B per tet of static mesh shared by all envs; env-steps/s x mean iterations"}
+    hbm_it["frac"] = round(hbm_it["achieved_gbs"] / hbm_it["peak_gbs"], 4)
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": "env-steps/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": "f32 (fp64 per-env reductions and rigid DOFs)",
         "data": "synthetic (seeded generators: workloads/)",
         "config": {"workload": WORKLOADS[args.config],
-                   "envs_per_gpu": E, "total_envs": n_all, "iters_per_step": FIXED_ITERS, "iteration_mode": "fixed",
+                   "envs_per_gpu": E, "total_envs": n_all, "iters_per_step": args.iters if args.tol is None else None,
+                   "iteration_mode": "fixed" if args.tol is None else f"tolerance (tol_x {args.tol:g} m, max {args.max_iters})",
                    "parallelism": f"env-sharded dp{ws}" + (" + NCCL all-gather of markers" if ws > 1 else ""),
                    "l2": "per-env state ~470 MB/GPU > 126 MB L2 (no flush needed)"},
         "roofline": roof,
+        "hbm_iteration": hbm_it,
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": cl,
-        "solver": {"mean_iters": float(it.float().mean()), "mean_peak_candidates": float(stt[:, 1].mean()),
+        "solver": {"mean_iters": mean_it, "p95_iters": float(np.percentile(its, 95)),
+                   "max_iters": float(its.max()), "mean_peak_candidates": float(stt[:, 1].mean()),
                    "max_peak_candidates": int(stt[:, 1].max()), "mean_anchors": float(stt[:, 2].mean()),
                    "mean_rebuilds_per_step": float(stt[:, 3].mean()),
                    "envs_flagged_overflow": int(((fl & 32) != 0).sum()), "envs_nan": int(((fl & 12) != 0).sum())},
@@ -346,9 +371,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--config", default="c3", choices=["c3", "c3u", "c5"])
+    ap.add_argument("--iters", type=int, default=FIXED_ITERS, help="fixed PNCG iterations per step (headline 50)")
+    ap.add_argument("--tol", type=float, default=None, help="tolerance mode: tol_x [m] (SURVEY §8d.1: 1e-7)")
+    ap.add_argument("--max-iters", type=int, default=2000, help="tolerance mode iteration cap")
     ap.add_argument("--total-envs", type=int, default=8192, help="strong scaling: envs over all ranks (C4)")
     args = ap.parse_args()
-    assert args.warmup >= 1
+    assert args.warmup >= 1 and args.iters >= 1
     if args.envs is None:
         args.envs = 256 if args.config == "c5" else ENVS_PER_GPU
     if args.impl == "reference":

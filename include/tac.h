@@ -100,8 +100,9 @@ typedef struct {
  *   c1, eps_E       Armijo constant and relative energy noise allowance (R14)
  *   max_iters       iteration budget per step (tolerance mode)
  *   fixed_iters     > 0: run exactly this many iterations per step (benchmark mode)
- *   beta_rule       0 Dai-Kou, 1 PR+, 2 FR
- *   precond         0 3x3 block Jacobi, 1 scalar Jacobi P = diag(H)^-1
+ *   beta_rule       0 Dai-Kou, 1 PR+, 2 FR, 3 DK+ (max(beta_DK, 0.5 g^T p/|p|^2), R28);
+ *                   outside 0..3 -> TAC_EINVAL
+ *   precond         0 3x3 block Jacobi, 1 scalar Jacobi P = diag(H)^-1; else TAC_EINVAL
  *   max_halvings    Armijo halvings before restarting along -P g
  *   stagnation      iterations without |P g| progress before giving up (0 = off)
  *   max_candidates  per-env capacity of candidate pairs (0 = default 16384)

@@ -812,11 +812,14 @@ double curvature(const Problem& P, const Step& S, const State& s, const std::vec
 // PNCG pieces shared by the IPC step and the quadratic pin
 // ---------------------------------------------------------------------------
 // Dai-Kou beta, Eq. (dk_direction), written from the per-vector dot products.
-// rule 1 = PR+ , 2 = FR (variants).
-double ncg_beta(int rule, double gPy, double yp, double yPy, double pg, double gPg, double gPg_prev) {
+// rule 1 = PR+ , 2 = FR (variants), 3 = DK+ : Dai-Kou's truncation
+// beta+ = max(beta_DK, eta g_{k+1}^T p_k / |p_k|^2), eta = 0.5 (R28).
+double ncg_beta(int rule, double gPy, double yp, double yPy, double pg, double gPg, double gPg_prev, double pp) {
   if (rule == 1) return std::max(0.0, gPy / gPg_prev);
   if (rule == 2) return gPg / gPg_prev;
-  return gPy / yp - (yPy / yp) * (pg / yp);
+  double dk = gPy / yp - (yPy / yp) * (pg / yp);
+  if (rule == 3) return std::max(dk, 0.5 * pg / pp);
+  return dk;
 }
 // step size, Eq. (step_size): alpha = min(alpha_upper, alpha_bar) (+ alpha_ccd, R15)
 double step_alpha_bar(double gp, double pHp) { return pHp > 0 ? -gp / pHp : INF; }
@@ -1094,9 +1097,10 @@ void env_step(const Problem& P, Env& E, const double* target7, double h, const O
       Vecs y = vlin(P, 1.0, g, -1.0, gpv);
       Vecs Py = apply_P(P, G, y);  // P_{k+1} y
       double yp = vdot(P, y, pprev);
-      double scale = std::sqrt(vdot(P, g, g)) * std::sqrt(vdot(P, pprev, pprev));
+      double ppn = vdot(P, pprev, pprev);
+      double scale = std::sqrt(vdot(P, g, g)) * std::sqrt(ppn);
       if (std::fabs(yp) <= 1e-30 * scale) rs = true;
-      else beta = ncg_beta(P.beta_rule, vdot(P, g, Py), yp, vdot(P, y, Py), vdot(P, pprev, g), gPg, gPg_prev);
+      else beta = ncg_beta(P.beta_rule, vdot(P, g, Py), yp, vdot(P, y, Py), vdot(P, pprev, g), gPg, gPg_prev, ppn);
       if (!std::isfinite(beta)) rs = true;
     }
     p = rs ? vlin(P, -1.0, Pg, 0.0, Pg) : vlin(P, -1.0, Pg, beta, pprev);
@@ -1511,7 +1515,7 @@ void or_ncg_quadratic(int n, const double* A, const double* b, const double* x0,
     else {
       for (int i = 0; i < n; ++i) { y[i] = g[i] - gp[i]; Py[i] = Pm(i) * y[i]; }
       double yp = vd(y, pp);
-      double beta = ncg_beta(rule, vd(g, Py), yp, vd(y, Py), vd(pp, g), gPg, gPg_prev);
+      double beta = ncg_beta(rule, vd(g, Py), yp, vd(y, Py), vd(pp, g), gPg, gPg_prev, vd(pp, pp));
       if (!std::isfinite(beta)) beta = 0;
       for (int i = 0; i < n; ++i) p[i] = -Pg[i] + beta * pp[i];
     }

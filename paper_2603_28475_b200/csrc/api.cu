@@ -45,6 +45,19 @@ struct tac_sim {
   bool kappa_fixed = false;
   unsigned long long step_count = 0;  // tac_step calls so far (pose-noise counter, R27)
   std::vector<double> thE, thNu, thRho, thMu;
+  // CUDA graphs of the PNCG iteration loop: a chunk of n iterations (all K of the fixed mode,
+  // check_every of the tolerance mode) is captured once per (h, anchor buffer) and replayed.
+  // The Dev argument baked into the nodes differs between steps only in the anchor buffer
+  // (double-buffered by the per-step sort), so two cached graphs cover every step.
+  struct IterGraph {
+    cudaGraphExec_t exec = nullptr;
+    const void* anc = nullptr;
+    double h = 0;
+    int n = 0;
+    long long launches = 0;
+  } graphs[2];
+  cudaStream_t cap = nullptr;  // capture stream (graphs are launched on the caller's stream)
+  bool use_graphs = true;      // TAC_NO_GRAPH=1 at create disables (A/B measurements)
 };
 
 static thread_local std::string g_create_err;
@@ -249,7 +262,8 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
   if (!(MT.E > 0) || !(MT.nu >= 0 && MT.nu < 0.5) || !(MT.rho > 0) || !(MT.mu_f >= 0))
     return fail(TAC_EINVAL, "invalid material");
   if (!(P.dhat > 0) || !(P.bp_margin >= 0.5 * P.dhat) || !(P.ccd_s > 0 && P.ccd_s < 1) || !(P.k_t > 0) ||
-      !(P.k_r > 0) || !(P.f_max > 0) || !(P.t_max > 0) || !(P.eps_v > 0) || P.max_iters < 1 || P.fixed_iters < 0)
+      !(P.k_r > 0) || !(P.f_max > 0) || !(P.t_max > 0) || !(P.eps_v > 0) || P.max_iters < 1 || P.fixed_iters < 0 ||
+      P.beta_rule < 0 || P.beta_rule > 3 || P.precond < 0 || P.precond > 1)
     return fail(TAC_EINVAL, "invalid solver parameters");
   if (MS.rows * MS.cols < 1 || !MS.rest_xyz || (MS.mode != 0 && MS.mode != 1))
     return fail(TAC_EINVAL, "invalid marker set");
@@ -706,6 +720,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
   sim->max_iters = P.max_iters;
   sim->fixed_iters = P.fixed_iters;
   sim->check_every = P.check_every > 0 ? P.check_every : 25;
+  if (getenv("TAC_NO_GRAPH")) sim->use_graphs = false;
   // device upload
   std::vector<float4> Xf(nv), Yf(niv);
   for (int i = 0; i < nv; ++i) Xf[i] = make_float4((float)X[i][0], (float)X[i][1], (float)X[i][2], 0.f);
@@ -870,6 +885,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
     if (cudaStreamCreateWithPriority(&d.side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&d.side2, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&sim->cap, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&d.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&d.ev_cls, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&d.ev_join2, cudaEventDisableTiming) != cudaSuccess ||
@@ -941,6 +957,9 @@ tac_status tac_destroy(tac_sim* sim) {
   cudaSetDevice(sim->device);
   if (sim->d.side) { cudaStreamSynchronize(sim->d.side); cudaStreamDestroy(sim->d.side); }
   if (sim->d.side2) { cudaStreamSynchronize(sim->d.side2); cudaStreamDestroy(sim->d.side2); }
+  for (auto& g : sim->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (sim->cap) cudaStreamDestroy(sim->cap);
   for (cudaEvent_t ev : {sim->d.ev_fork, sim->d.ev_join, sim->d.ev_cls, sim->d.ev_join2})
     if (ev) cudaEventDestroy(ev);
   for (void* p : sim->allocs) cudaFree(p);
@@ -965,6 +984,64 @@ static tac_status post_launch(tac_sim* sim) {
   return TAC_OK;
 }
 
+static void launch_iterations(const Dev& d, double h, int n, cudaStream_t s) {
+  for (int it = 0; it < n; ++it) {
+    launch_eval(d, h, s);       // a4 + a5 + Armijo (a8)
+    launch_direction(d, s);     // a6
+    launch_curvature(d, h, s);  // a7
+    launch_alpha(d, h, s);      // a7/a8 (+ a2 rebuild)
+  }
+}
+
+// n PNCG iterations on stream s: replayed from a cached CUDA graph unless per-launch
+// profiling is on (its events sit between the launches) or graphs are disabled.
+static bool run_iterations(tac_sim* sim, double h, int n, cudaStream_t s) {
+  const Dev& d = sim->d;
+  if (sim->prof || !sim->use_graphs) {
+    launch_iterations(d, h, n, s);
+    return true;
+  }
+  tac_sim::IterGraph* G = nullptr;
+  for (auto& g : sim->graphs)
+    if (g.exec && g.anc == (const void*)d.anc && g.h == h && g.n == n) G = &g;
+  if (!G) {  // capture: reuse the slot of this anchor buffer, else an empty one, else slot 0
+    G = &sim->graphs[0];
+    for (auto& g : sim->graphs)
+      if (g.anc == (const void*)d.anc) { G = &g; break; }
+    if (G->anc != (const void*)d.anc)
+      for (auto& g : sim->graphs)
+        if (!g.exec) { G = &g; break; }
+    if (G->exec) { cudaGraphExecDestroy(G->exec); G->exec = nullptr; }
+    const long long l0 = g_launches;
+    cudaGraph_t gr = nullptr;
+    bool ok = cudaStreamBeginCapture(sim->cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      launch_iterations(d, h, n, sim->cap);
+      ok = cudaStreamEndCapture(sim->cap, &gr) == cudaSuccess && gr;
+    }
+    // kernel nodes keep their stream's priority (the contact chain's high priority)
+    ok = ok && cudaGraphInstantiateWithFlags(&G->exec, gr, cudaGraphInstantiateFlagUseNodePriority) == cudaSuccess;
+    if (gr) cudaGraphDestroy(gr);
+    if (!ok) {  // capture unsupported here: launch the same kernels directly from now on
+      cudaGetLastError();
+      if (G->exec) cudaGraphExecDestroy(G->exec);
+      *G = tac_sim::IterGraph{};
+      sim->use_graphs = false;
+      g_launches = l0;
+      if (getenv("TAC_GRAPH_DEBUG")) fprintf(stderr, "tac: iteration graph capture failed, direct launches\n");
+      launch_iterations(d, h, n, s);
+      return true;
+    }
+    G->anc = d.anc;
+    G->h = h;
+    G->n = n;
+    G->launches = g_launches - l0;
+    g_launches = l0;
+  }
+  g_launches += G->launches;
+  return cudaGraphLaunch(G->exec, s) == cudaSuccess;
+}
+
 tac_status tac_step(tac_sim* sim, const float* target_poses, float dt, void* stream) {
   tac_status st = check_sim(sim);
   if (st) return st;
@@ -982,12 +1059,12 @@ tac_status tac_step(tac_sim* sim, const float* target_poses, float dt, void* str
   launch_sort_anchors(d, sim->d.anc2, s);    // neighbouring anchors share gel corners (friction scatter)
   std::swap(sim->d.anc, sim->d.anc2);        // launches below read the sorted buffer
   int K = sim->fixed_iters > 0 ? sim->fixed_iters : sim->max_iters;
-  for (int it = 0; it < K; ++it) {
-    launch_eval(d, h, s);       // a4 + a5 + Armijo (a8)
-    launch_direction(d, s);     // a6
-    launch_curvature(d, h, s);  // a7
-    launch_alpha(d, h, s);      // a7/a8 (+ a2 rebuild)
-    if (sim->fixed_iters == 0 && (it + 1) % sim->check_every == 0) {
+  const int chunk = sim->fixed_iters > 0 ? K : std::min(K, sim->check_every);
+  for (int it = 0; it < K;) {
+    const int n = std::min(chunk, K - it);
+    if (!run_iterations(sim, h, n, s)) { g_prof = nullptr; return post_launch(sim); }
+    it += n;
+    if (sim->fixed_iters == 0 && it % sim->check_every == 0 && it < K) {  // all envs done?
       cudaMemsetAsync(sim->d_flag, 0, sizeof(int), s);
       launch_any_active(d, sim->d_flag, s);
       cudaMemcpyAsync(sim->h_flag, sim->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s);

@@ -974,11 +974,145 @@ __global__ void __launch_bounds__(256, 4) k_elem_grad(Dev d, float h2) {
 // corner bit flipped along step i of tet j's path 0 -> CELL_TET(j,1) -> CELL_TET(j,2) -> 7
 #define CELL_Q(j, i) ((i) == 0 ? ((j) >> 1) : (i) == 1 ? (((j) >> 1) == 0 ? 1 + ((j) & 1) : ((j) >> 1) == 1 ? 2 * ((j) & 1) : ((j) & 1)) \
                       : 3 - ((j) >> 1) - (((j) >> 1) == 0 ? 1 + ((j) & 1) : ((j) >> 1) == 1 ? 2 * ((j) & 1) : ((j) & 1)))
+// ---- packed fp32 pairs (sm_100 FADD2 / FMUL2 / FFMA2): one instruction evaluates the same
+// operation for two tets of a Kuhn cell (.x, .y), halving the issue slots of the elementwise
+// 3x3 algebra; each lane rounds exactly like the scalar instruction
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 fms2(float2 a, float2 b, float2 c) {  // c - a b
+  return __ffma2_rn(make_float2(-a.x, -a.y), b, c);
+}
+__device__ __forceinline__ float2 det2x2_2(float2 a, float2 b, float2 c, float2 e) { return fms2(c, e, mul2(a, b)); }  // ab - ce
+__device__ __forceinline__ void cof33_2(const float2* A, float2* C) {
+  C[0] = det2x2_2(A[4], A[8], A[5], A[7]); C[1] = det2x2_2(A[5], A[6], A[3], A[8]); C[2] = det2x2_2(A[3], A[7], A[4], A[6]);
+  C[3] = det2x2_2(A[2], A[7], A[1], A[8]); C[4] = det2x2_2(A[0], A[8], A[2], A[6]); C[5] = det2x2_2(A[1], A[6], A[0], A[7]);
+  C[6] = det2x2_2(A[1], A[5], A[2], A[4]); C[7] = det2x2_2(A[2], A[3], A[0], A[5]); C[8] = det2x2_2(A[0], A[4], A[1], A[3]);
+}
+// Axis-aligned cell, tets j = 2m and 2m+1 as one packed pair: both run 0 -> s1 -> s2 -> 7 with
+// the same first step (corner bit q0 = m, so column q0 of G is shared) and the other two steps
+// swapped (q1 of one tet is q2 of the other), so every column position of the pair's G is a
+// scaled difference of two corner rows per tet.
+template <int m>
+__device__ __forceinline__ void aa_pair_cols(const float (*u)[3], const float* inv, float2* G) {
+  constexpr int jA = 2 * m, jB = 2 * m + 1;
+  constexpr int s1 = CELL_TET(jA, 1), sA = CELL_TET(jA, 2), sB = CELL_TET(jB, 2);
+  constexpr int q0 = CELL_Q(jA, 0), qa = CELL_Q(jA, 1), qb = CELL_Q(jA, 2);  // tet B: q1 = qb, q2 = qa
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const float c0 = (u[s1][r] - u[0][r]) * inv[q0];
+    G[3 * r + q0] = make_float2(c0, c0);
+    G[3 * r + qa] = mul2(make_float2(u[sA][r] - u[s1][r], u[7][r] - u[sB][r]), f2(inv[qa]));
+    G[3 * r + qb] = mul2(make_float2(u[7][r] - u[sA][r], u[sB][r] - u[s1][r]), f2(inv[qb]));
+  }
+}
+// gradient of a packed tet pair: energy (per tet, without the factor w = h^2 V), and the
+// columns of P(F) and cof F scaled by 1/s_a (Pt[a][i] = w P_ia / s_a, Ct[a][i] = cof F_ia / s_a),
+// whose path differences are the corner forces and cofactor vectors (see aa branch below)
+__device__ __forceinline__ float2 grad_pair(const float2* Gm, float mu, float l2, float w, const float* inv,
+                                           float2 (*Pt)[3], float2 (*Ct)[3]) {
+  const float2 trG = add2(add2(Gm[0], Gm[4]), Gm[8]);
+  const float2 i2 = add2(add2(det2x2_2(Gm[0], Gm[4], Gm[1], Gm[3]), det2x2_2(Gm[0], Gm[8], Gm[2], Gm[6])),
+                         det2x2_2(Gm[4], Gm[8], Gm[5], Gm[7]));
+  float2 cG[9];
+  cof33_2(Gm, cG);
+  const float2 detG = fma2(Gm[2], cG[2], fma2(Gm[1], cG[1], mul2(Gm[0], cG[0])));
+  const float2 Jm1 = add2(add2(trG, i2), detG);
+  float2 GG = mul2(Gm[0], Gm[0]);
+#pragma unroll
+  for (int i = 1; i < 9; ++i) GG = fma2(Gm[i], Gm[i], GG);
+  // mu (GG/2 - i2 - detG) + l2/2 Jm1^2
+  const float2 psi = fma2(mul2(f2(0.5f * l2), Jm1), Jm1, mul2(f2(mu), sub2(sub2(mul2(f2(0.5f), GG), i2), detG)));
+  const float2 tr1 = add2(trG, f2(1.f));
+  const float2 lj = mul2(f2(l2), Jm1);
+  const float wmu = w * mu;
+  const float2 wlj = mul2(f2(w), lj);
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      // cof F = (1 + trG) I - G^T + cof G;  P(F) = mu (G + G^T - trG I - cof G) + lambda'(J-1) cof F
+      const float2 cF = i == a ? add2(sub2(tr1, Gm[3 * a + i]), cG[3 * i + a]) : sub2(cG[3 * i + a], Gm[3 * a + i]);
+      float2 sym = add2(Gm[3 * i + a], Gm[3 * a + i]);
+      if (i == a) sym = sub2(sym, trG);
+      const float2 PK = fma2(wlj, cF, mul2(f2(wmu), sub2(sym, cG[3 * i + a])));
+      Pt[a][i] = mul2(PK, f2(inv[a]));
+      Ct[a][i] = mul2(cF, f2(inv[a]));
+    }
+  return psi;
+}
+// p^T H_e p of a packed tet pair (App. B quadratic form, as in the scalar loop below), per tet
+// (without the common h^2 V factor)
+__device__ __forceinline__ float2 curv_pair(const float2* Gm, const float2* dF, float mu, float l2) {
+  const float2 trG = add2(add2(Gm[0], Gm[4]), Gm[8]);
+  const float2 i2 = add2(add2(det2x2_2(Gm[0], Gm[4], Gm[1], Gm[3]), det2x2_2(Gm[0], Gm[8], Gm[2], Gm[6])),
+                         det2x2_2(Gm[4], Gm[8], Gm[5], Gm[7]));
+  float2 cG[9], cd[9];
+  cof33_2(Gm, cG);
+  cof33_2(dF, cd);
+  const float2 detG = fma2(Gm[2], cG[2], fma2(Gm[1], cG[1], mul2(Gm[0], cG[0])));
+  const float2 Jm1 = add2(add2(trG, i2), detG);
+  const float2 tr1 = add2(trG, f2(1.f));
+  float2 dd = f2(0.f), cfd = f2(0.f), fcd = f2(0.f);
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int jj = 0; jj < 3; ++jj) {
+      const float2 cF = i == jj ? add2(sub2(tr1, Gm[3 * jj + i]), cG[3 * i + jj]) : sub2(cG[3 * i + jj], Gm[3 * jj + i]);
+      const float2 Fij = i == jj ? add2(Gm[3 * i + jj], f2(1.f)) : Gm[3 * i + jj];
+      dd = fma2(dF[3 * i + jj], dF[3 * i + jj], dd);
+      cfd = fma2(cF, dF[3 * i + jj], cfd);
+      fcd = fma2(Fij, cd[3 * i + jj], fcd);
+    }
+  // mu dd + l2 cfd^2 + 2 (l2 Jm1 - mu) fcd
+  const float2 c2 = mul2(fma2(f2(l2), Jm1, f2(-mu)), f2(2.f));
+  return fma2(c2, fcd, fma2(mul2(f2(l2), cfd), cfd, mul2(f2(mu), dd)));
+}
+
 // Axis-aligned cells (structured pads: corner bit b along axis b, signed edge s_b): column
 // q_i of G is the scaled difference (u_{c_{i+1}} - u_{c_i}) / s_{q_i} along the path, and the
 // b rows are e_q0/s_q0 - e_q1/s_q1, e_q1/s_q1 - e_q2/s_q2, e_q2/s_q2, so the corner forces and
 // cofactor vectors are differences of scaled columns -- the same quantities with no 3x3
 // products against stored b rows (cell_aa.w = tet volume > 0 marks such a cell)
+
+// one packed pair of an axis-aligned cell: forces and lambda' c c^T blocks of both tets into the
+// cell's corner accumulators.  Tet A (.x) runs 0 -> s1 -> sA -> 7 over columns q0, qa, qb, tet B
+// (.y) 0 -> s1 -> sB -> 7 over q0, qb, qa; corner k of a path gets column(k-1) - column(k).
+__device__ __forceinline__ void corner_acc(float* ag, float* aD, float lc, float f0, float f1, float f2_,
+                                           float c0, float c1, float c2) {
+  ag[0] += f0; ag[1] += f1; ag[2] += f2_;
+  const float sx = lc * c0, sy = lc * c1, sz = lc * c2;
+  aD[0] = fmaf(sx, c0, aD[0]); aD[1] = fmaf(sy, c1, aD[1]); aD[2] = fmaf(sz, c2, aD[2]);
+  aD[3] = fmaf(sx, c1, aD[3]); aD[4] = fmaf(sx, c2, aD[4]); aD[5] = fmaf(sy, c2, aD[5]);
+}
+template <int m>
+__device__ __forceinline__ void pair_grad_acc(const float (*u)[3], const float* inv, float mu, float l2, float w,
+                                              float lc, double& esum, float (*ag)[3], float (*aD)[6]) {
+  constexpr int jA = 2 * m, jB = 2 * m + 1;
+  constexpr int s1 = CELL_TET(jA, 1), sA = CELL_TET(jA, 2), sB = CELL_TET(jB, 2);
+  constexpr int q0 = CELL_Q(jA, 0), qa = CELL_Q(jA, 1), qb = CELL_Q(jA, 2);
+  float2 Gm[9], Pt[3][3], Ct[3][3];
+  aa_pair_cols<m>(u, inv, Gm);
+  const float2 psi = grad_pair(Gm, mu, l2, w, inv, Pt, Ct);
+  esum += (double)(w * psi.x);
+  esum += (double)(w * psi.y);
+  // tet A
+  corner_acc(ag[0], aD[0], lc, -Pt[q0][0].x, -Pt[q0][1].x, -Pt[q0][2].x, -Ct[q0][0].x, -Ct[q0][1].x, -Ct[q0][2].x);
+  corner_acc(ag[s1], aD[s1], lc, Pt[q0][0].x - Pt[qa][0].x, Pt[q0][1].x - Pt[qa][1].x, Pt[q0][2].x - Pt[qa][2].x,
+             Ct[q0][0].x - Ct[qa][0].x, Ct[q0][1].x - Ct[qa][1].x, Ct[q0][2].x - Ct[qa][2].x);
+  corner_acc(ag[sA], aD[sA], lc, Pt[qa][0].x - Pt[qb][0].x, Pt[qa][1].x - Pt[qb][1].x, Pt[qa][2].x - Pt[qb][2].x,
+             Ct[qa][0].x - Ct[qb][0].x, Ct[qa][1].x - Ct[qb][1].x, Ct[qa][2].x - Ct[qb][2].x);
+  corner_acc(ag[7], aD[7], lc, Pt[qb][0].x, Pt[qb][1].x, Pt[qb][2].x, Ct[qb][0].x, Ct[qb][1].x, Ct[qb][2].x);
+  // tet B
+  corner_acc(ag[0], aD[0], lc, -Pt[q0][0].y, -Pt[q0][1].y, -Pt[q0][2].y, -Ct[q0][0].y, -Ct[q0][1].y, -Ct[q0][2].y);
+  corner_acc(ag[s1], aD[s1], lc, Pt[q0][0].y - Pt[qb][0].y, Pt[q0][1].y - Pt[qb][1].y, Pt[q0][2].y - Pt[qb][2].y,
+             Ct[q0][0].y - Ct[qb][0].y, Ct[q0][1].y - Ct[qb][1].y, Ct[q0][2].y - Ct[qb][2].y);
+  corner_acc(ag[sB], aD[sB], lc, Pt[qb][0].y - Pt[qa][0].y, Pt[qb][1].y - Pt[qa][1].y, Pt[qb][2].y - Pt[qa][2].y,
+             Ct[qb][0].y - Ct[qa][0].y, Ct[qb][1].y - Ct[qa][1].y, Ct[qb][2].y - Ct[qa][2].y);
+  corner_acc(ag[7], aD[7], lc, Pt[qa][0].y, Pt[qa][1].y, Pt[qa][2].y, Ct[qa][0].y, Ct[qa][1].y, Ct[qa][2].y);
+}
 
 // ALL_AA: every cell of the mesh is axis-aligned (structured pads) -- the stored-B branch is
 // compiled out, which frees the registers it would hold
@@ -1016,6 +1150,12 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
 #pragma unroll
       for (int c = 0; c < 6; ++c) aD[s][c] = 0.f;
     }
+    if constexpr (ALL_AA) {  // packed tet pairs (0,1), (2,3), (4,5); every tet has volume caa.w
+      const float w = h2 * caa.w, lc = w * l2;
+      pair_grad_acc<0>(u, inv, mu, l2, w, lc, esum, ag, aD);
+      pair_grad_acc<1>(u, inv, mu, l2, w, lc, esum, ag, aD);
+      pair_grad_acc<2>(u, inv, mu, l2, w, lc, esum, ag, aD);
+    } else {
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
       const int s0 = CELL_TET(j, 0), s1 = CELL_TET(j, 1), s2 = CELL_TET(j, 2), s3 = CELL_TET(j, 3);
@@ -1113,6 +1253,7 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
         aD[s0][3] += lc * c0[0] * c0[1]; aD[s0][4] += lc * c0[0] * c0[2]; aD[s0][5] += lc * c0[1] * c0[2];
       }
     }
+    }
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
       if (fix & (1u << s)) continue;
@@ -1159,6 +1300,28 @@ __global__ void __launch_bounds__(256, 2) k_elem_curv_cells(Dev d, float h2) {
       for (int c = 0; c < 3; ++c) { u[s][c] = pu[32 * c]; p[s][c] = pp[32 * c]; }
     }
     float q = 0.f;
+    if constexpr (ALL_AA) {  // packed tet pairs (0,1), (2,3), (4,5); every tet has volume caa.w
+      float2 qp = f2(0.f);
+      {
+        float2 Gm[9], dF[9];
+        aa_pair_cols<0>(u, inv, Gm);
+        aa_pair_cols<0>(p, inv, dF);
+        qp = add2(qp, curv_pair(Gm, dF, mu, l2));
+      }
+      {
+        float2 Gm[9], dF[9];
+        aa_pair_cols<1>(u, inv, Gm);
+        aa_pair_cols<1>(p, inv, dF);
+        qp = add2(qp, curv_pair(Gm, dF, mu, l2));
+      }
+      {
+        float2 Gm[9], dF[9];
+        aa_pair_cols<2>(u, inv, Gm);
+        aa_pair_cols<2>(p, inv, dF);
+        qp = add2(qp, curv_pair(Gm, dF, mu, l2));
+      }
+      qsum += (double)(h2 * (caa.w * (qp.x + qp.y)));
+    } else {
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
       const int s0 = CELL_TET(j, 0), s1 = CELL_TET(j, 1), s2 = CELL_TET(j, 2), s3 = CELL_TET(j, 3);
@@ -1212,6 +1375,7 @@ __global__ void __launch_bounds__(256, 2) k_elem_curv_cells(Dev d, float h2) {
       q += vol * (mu * dd + l2 * cfd * cfd + 2.f * (l2 * Jm1 - mu) * fcd);
     }
     qsum += (double)(h2 * q);
+    }
   }
   if (act) atomicAdd(d.acc + (size_t)A_PHP * d.Es + e, qsum);
 }
@@ -1898,6 +2062,99 @@ __global__ void __launch_bounds__(256) k_contact_curv_staged(Dev d, double h2) {
   }
 }
 
+// curvature + near-pair step bounds from the cached geometry, corners gathered directly: the
+// gel corners' p from the compact per-env surface copy (written by k_dir_apply just before,
+// L2-resident), the indenter corners' R Y from the static body-frame vertices -- only the
+// corners the env's near pairs and anchors touch, instead of staging its whole surface and
+// indenter per CTA
+__global__ void __launch_bounds__(128) k_contact_curv_direct(Dev d, double h2) {
+  TAC_PDL_WAIT();
+  int e = blockIdx.y;
+  if (e >= d.E || !(d.run[e] & 2)) return;
+  const double kappa = h2 * d.edbl[e];  // h^2 kappa_phys of this env
+  const EnvS& s = d.es[e];
+  __shared__ double R[9], pr[6];
+  __shared__ double sm[8];
+  if (threadIdx.x < 9) R[threadIdx.x] = s.R[threadIdx.x];
+  if (threadIdx.x < 6) pr[threadIdx.x] = s.pr[threadIdx.x];
+  __syncthreads();
+  d3 pc = mk(pr[0], pr[1], pr[2]), pth = mk(pr[3], pr[4], pr[5]);
+  double extra = nrm(pth) * d.dhat * 0.25;
+  // motion per unit alpha of corner id (indenter vertex or surface-local gel id)
+  auto motion = [&](bool ind, unsigned id) -> d3 {
+    if (ind) {  // fp32 R Y exactly as the staged pass rounds it
+      const float4 yb = __ldg(d.Y + id);
+      const d3 y = mv(R, mk(yb.x, yb.y, yb.z));
+      return pc + cross(pth, mk((float)y.x, (float)y.y, (float)y.z));
+    }
+    const float4 p = d.psurf[(size_t)id * d.Es + e];
+    return mk(p.x, p.y, p.z);
+  };
+  double q = 0, amin = INFINITY;
+  const int n0 = d.nnear[3 * e], n1 = d.nnear[3 * e + 1], n = n0 + n1 + d.nnear[3 * e + 2];
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const int kk = j < n0 ? 0 : (j < n0 + n1 ? 1 : 2);
+    // near-ordered geometry and corners (written by k_contact_near at this position)
+    const size_t slot = (size_t)e * d.kmax + j;
+    const uint2 cc = d.ncorn[slot];
+    const unsigned id[4] = {cc.x & 0xffffu, cc.x >> 16, cc.y & 0xffffu, cc.y >> 16};
+    const int na = kk == 2 ? 2 : 1;
+    const float4* geo = d.cgeo + 2 * slot;
+    float4 g0 = geo[0], g1 = geo[1];
+    double dist = g0.x;
+    if (!(dist > 0)) continue;
+    d3 nn = mk(g0.y, g0.z, g0.w);
+    double w[4] = {g1.x, g1.y, g1.z, g1.w};
+    d3 dz[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) dz[k] = motion(kk == 0 ? k >= 1 : (kk == 1 ? k == 0 : k >= 2), id[k]);
+    if (dist < d.dhat) {
+      d3 dr = mk(0, 0, 0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dr = dr + w[k] * dz[k];
+      double dn = dot(nn, dr);
+      double lg = log(dist / d.dhat), dm = dist - d.dhat, inv = 1.0 / dist;
+      q += kappa * (-2 * lg - 4 * dm * inv + dm * dm * inv * inv) * dn * dn;
+    }
+    double la = -INFINITY, lb = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < na) la = fmax(la, -dot(nn, dz[k]));
+      else lb = fmax(lb, dot(nn, dz[k]));
+    }
+    double l = la + lb + extra;
+    if (l > 0) amin = fmin(amin, (1 - d.ccd_s) * dist / l);
+  }
+  const int na = min(d.nanc[e], d.amax);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
+    const Anchor& A = d.anc[(size_t)e * d.amax + i];
+    const unsigned sid[3] = {A.sid01 & 0xffffu, A.sid01 >> 16, A.sid2};
+    // indenter side folded: sig p_c + p_theta x (R Y_w)
+    d3 dD = (double)A.sig * pc + cross(pth, mv(R, mk(A.yw[0], A.yw[1], A.yw[2])));
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      if (A.gid[k] >= 0) {
+        const float4 pv = d.psurf[(size_t)sid[k] * d.Es + e];
+        dD = dD + (double)A.w[k] * mk(pv.x, pv.y, pv.z);
+      }
+    d3 t1 = mk(A.t1[0], A.t1[1], A.t1[2]), t2 = mk(A.t2[0], A.t2[1], A.t2[2]);
+    double ta = dot(t1, dD), tb = dot(t2, dD);
+    q += (double)d.anc_f1[(size_t)e * d.amax + i] * (ta * ta + tb * tb);
+  }
+  // block reductions: sum q, min amin
+  q = warp_sum(q);
+  amin = warp_min(amin);
+  __shared__ double smin[8];
+  if ((threadIdx.x & 31) == 0) { sm[threadIdx.x >> 5] = q; smin[threadIdx.x >> 5] = amin; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0, m = INFINITY;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { t += sm[w]; m = fmin(m, smin[w]); }
+    if (t != 0.0) atomicAdd(d.acc + (size_t)A_PHP * d.Es + e, t);
+    if (m < INFINITY) atomic_min_pos(d.accu + (size_t)U_ACCD * d.Es + e, (float)m);
+  }
+}
+
 // ------------------------------------------------------------------ a8: Armijo accept (per env)
 // E_k = inertia + elastic + barrier + friction + pose spring; accept if
 // E <= E_prev + c1 alpha g^T p + eps_E |E_prev| (R14); otherwise halve alpha from x_k,
@@ -2130,7 +2387,10 @@ __global__ void k_dir_scalar(Dev d) {
     if (fabs(yp) <= 1e-30 * sqrt(gg) * sqrt(pp)) rs = true;
     else if (d.beta_rule == 1) beta = fmax(0.0, gPy / s.gPg_prev);
     else if (d.beta_rule == 2) beta = gPg / s.gPg_prev;
-    else beta = gPy / yp - (yPy / yp) * (pg / yp);
+    else {
+      beta = gPy / yp - (yPy / yp) * (pg / yp);
+      if (d.beta_rule == 3) beta = fmax(beta, 0.5 * pg / pp);  // DK+ truncation (R28)
+    }
     if (!isfinite(beta)) rs = true;
   }
   if (rs) beta = 0;

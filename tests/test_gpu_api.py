@@ -82,6 +82,17 @@ def test_initial_intersection_is_refused(torch):
     _sim(s)
 
 
+@pytest.mark.parametrize("field,value", [("beta_rule", 4), ("beta_rule", -1), ("precond", 2)])
+def test_invalid_solver_switch_is_refused(torch, field, value):
+    """tac_create validates the solver switches (include/tac.h: outside their ranges ->
+    TAC_EINVAL) instead of running an undefined variant."""
+    import paper_2603_28475_b200 as P
+    s = w.scene_c1()
+    setattr(s.params, field, value)
+    with pytest.raises(P.TacError, match="invalid solver parameters"):
+        _sim(s)
+
+
 def test_three_component_markers_match_oracle(torch):
     """ncomp = 3 adds the normal component u_m . n (row a10)."""
     s = c1_press_scene(mu_f=1.0, steps=2, depth=0.2e-3)

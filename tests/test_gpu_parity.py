@@ -188,9 +188,10 @@ def test_converged_step_parity_c1(torch_cuda):
     _assert_parity(s, sim, o, mk, 0)
 
 
-@pytest.mark.parametrize("beta_rule,precond", [(1, 0), (0, 1)])
+@pytest.mark.parametrize("beta_rule,precond", [(1, 0), (0, 1), (3, 0)])
 def test_solver_variants_converged_parity(torch_cuda, beta_rule, precond):
-    """SURVEY 8f-3 switches (beta rule PR+ of P:454's family, scalar Jacobi of P:457):
+    """SURVEY 8f-3 switches (beta rule PR+ of P:454's family, DK+ truncation (R28), scalar
+    Jacobi of P:457):
     GPU and oracle converge to the same states, with comparable iteration counts."""
     s = w.scene_small_peg(n_envs=2, n_steps=3)
     s.params.beta_rule = beta_rule

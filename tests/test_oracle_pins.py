@@ -199,10 +199,13 @@ def _pcg(A, b, x0, iters, Pdiag):
     return np.array(xs)
 
 
+@pytest.mark.parametrize("rule", [0, 3])
 @pytest.mark.parametrize("identity", [True, False])
-def test_dk_equals_pcg_on_spd_quadratics(identity):
+def test_dk_equals_pcg_on_spd_quadratics(identity, rule):
     """On SPD quadratics with exact line search the paper's DK beta and
-    alpha_bar reproduce textbook (P)CG iterates."""
+    alpha_bar reproduce textbook (P)CG iterates.  DK+ (rule 3,
+    R28) truncates beta below at 0.5 g_{k+1}^T p_k / |p_k|^2, which is 0 under exact line
+    search while the PCG beta is positive: the same iterates."""
     rng = np.random.default_rng(3)
     for n in (5, 20, 40):
         Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
@@ -211,11 +214,11 @@ def test_dk_equals_pcg_on_spd_quadratics(identity):
         b = rng.standard_normal(n)
         x0 = rng.standard_normal(n)
         it = min(n, 15)
-        xs = O.ncg_quadratic(A, b, x0, it, precond_identity=identity)
+        xs = O.ncg_quadratic(A, b, x0, it, precond_identity=identity, rule=rule)
         ref = _pcg(A, b, x0, it, np.ones(n) if identity else 1 / np.diag(A))
         assert np.max(np.abs(xs - ref)) < 1e-9 * np.max(np.abs(ref))
         if n <= 20:  # converges within n (+5) iterations
-            xs = O.ncg_quadratic(A, b, x0, n + 5, precond_identity=identity)
+            xs = O.ncg_quadratic(A, b, x0, n + 5, precond_identity=identity, rule=rule)
             assert np.linalg.norm(A @ xs[-1] - b) < 1e-8 * np.linalg.norm(b)
 
 

@@ -265,7 +265,7 @@ class Params:
     eps_E: float = 1e-6
     max_iters: int = 5000
     fixed_iters: int = 0
-    beta_rule: int = 0      # 0 DK, 1 PR+, 2 FR
+    beta_rule: int = 0      # 0 DK, 1 PR+, 2 FR, 3 DK+
     precond: int = 0        # 0 3x3 block Jacobi, 1 scalar Jacobi
     max_halvings: int = 10
     stagnation: int = 3000
