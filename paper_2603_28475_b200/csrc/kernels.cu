@@ -2840,7 +2840,9 @@ void launch_curvature(const Dev& d, double h, cudaStream_t s) {
     cudaEventRecord(d.ev_fork, s);
     cudaStreamWaitEvent(cs, d.ev_fork, 0);
   }
-  LAUNCHP(KID_CONTACT_CURV, cs, k_contact_curv_staged, sgrid(d), 256, d.contact_smem, d, h * h);
+  static const bool staged = getenv("TAC_CURV_STAGED") != nullptr;  // A/B: the staged variant
+  if (staged) LAUNCHP(KID_CONTACT_CURV, cs, k_contact_curv_staged, sgrid(d), 256, d.contact_smem, d, h * h);
+  else LAUNCHP(KID_CONTACT_CURV, cs, k_contact_curv_direct, cgrid(d), 128, 0, d, h * h);
   if (fork) cudaEventRecord(d.ev_join, cs);
   if (d.nrest == 0) {  // every tet is in a Kuhn cell: register-blocked cells
     dim3 g = vgrid(d, d.ncells);
