@@ -772,6 +772,11 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     UP(smuf, d.smu);
     UP(vflag, d.vflag);
     UP(sim->sv, d.sv);
+    {
+      std::vector<int> svfree(sim->sv.size());  // surface-local id -> free gel vertex id, -1 if fixed
+      for (size_t i = 0; i < sim->sv.size(); ++i) svfree[i] = (vflag[sim->sv[i]] & 1) ? -1 : sim->sv[i];
+      UP(svfree, d.svfree);
+    }
     UP(se2, d.se);
     UP(st4, d.st);
     UP(se2l, d.se_l);

@@ -85,6 +85,7 @@ struct Dev {
   const float* smu;      // [nv] sum_e V_e mu |b_{e,v}|^2 (state-independent elastic diagonal / h^2)
   const unsigned char* vflag;  // [nv] bit0 fixed, bit1 on the gel surface
   const int* sv;         // [nsv]
+  const int* svfree;     // [nsv] gel vertex id of a free surface vertex, -1 if fixed (near-pair scatter)
   const int2* se;        // [nse]
   const int4* st;        // [nst]
   const int2* se_l;      // [nse] surface-local vertex indices

@@ -107,13 +107,32 @@ __device__ void block_sums_atomic(const double* v, double* const* out, double* s
 
 // the 20 per-env contact accumulators are contiguous: acc[A_EB .. A_DR + 11]
 static_assert(A_EF == A_EB + 1 && A_GR == A_EB + 2 && A_DR == A_EB + 8, "accumulator layout");
+// warp sums of 20 values by recursive halving: at offset o each lane keeps the half of its
+// values selected by (lane & o) and adds the partner's copy of that half, so after offsets
+// 16..1 lane L holds the warp total of value L -- 31 double shuffles instead of 20 x 5
+__device__ __forceinline__ double warp_sum20_transposed(const double* v) {
+  const int lane = threadIdx.x & 31;
+  double a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const double lo = v[i], hi = i + 16 < 20 ? v[i + 16] : 0.0;
+    const bool up = lane & 16;
+    a[i] = (up ? hi : lo) + __shfl_xor_sync(0xffffffffu, up ? lo : hi, 16);
+  }
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) {
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const bool up = lane & o;
+      a[i] = (up ? a[i + o] : a[i]) + __shfl_xor_sync(0xffffffffu, up ? a[i] : a[i + o], o);
+    }
+  }
+  return a[0];
+}
 __device__ void block_sums_contact(const double* v, double* acc, int Es, int e, double* sm /* [nwarps][20] */) {
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-#pragma unroll
-  for (int k = 0; k < 20; ++k) {
-    double x = warp_sum(v[k]);
-    if (lane == 0) sm[w * 20 + k] = x;
-  }
+  const double x = warp_sum20_transposed(v);
+  if (lane < 20) sm[w * 20 + lane] = x;
   __syncthreads();
   if (threadIdx.x < 20) {
     double s = 0;
@@ -348,7 +367,7 @@ __device__ __forceinline__ d3 gel_vec(const Dev& d, const float* a, int v, int e
   return mk(a[vidx(d, 0, v, e)], a[vidx(d, 1, v, e)], a[vidx(d, 2, v, e)]);
 }
 __device__ __forceinline__ d3 ind_body(const Dev& d, int j) {
-  float4 y = d.Y[j];
+  float4 y = __ldg(d.Y + j);
   return mk(y.x, y.y, y.z);
 }
 __device__ __forceinline__ DR pair_dist(int kind, const d3* z) {
@@ -1481,8 +1500,7 @@ __device__ __forceinline__ void add_sym(double* A, d3 a, double s) {  // A(6) +=
   A[0] += s * a.x * a.x; A[1] += s * a.y * a.y; A[2] += s * a.z * a.z;
   A[3] += s * a.x * a.y; A[4] += s * a.x * a.z; A[5] += s * a.y * a.z;
 }
-__device__ __forceinline__ void scatter_gel(const Dev& d, int v, int e, d3 f, double s, d3 n) {
-  if (d.vflag[v] & 1) return;
+__device__ __forceinline__ void scatter_gel_free(const Dev& d, int v, int e, d3 f, double s, d3 n) {
   atomicAdd(d.g + vidx(d, 0, v, e), (float)f.x);
   atomicAdd(d.g + vidx(d, 1, v, e), (float)f.y);
   atomicAdd(d.g + vidx(d, 2, v, e), (float)f.z);
@@ -1557,7 +1575,8 @@ __global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
     for (int k = 0; k < 4; ++k) {
       d3 f = (db * D.w[k]) * nn;
       if (!ind[k]) {
-        scatter_gel(d, __ldg(d.sv + id[k]), e, f, ddb * D.w[k] * D.w[k], nn);
+        const int v = __ldg(d.svfree + id[k]);  // one load: id and fixed flag
+        if (v >= 0) scatter_gel_free(d, v, e, f, ddb * D.w[k] * D.w[k], nn);
       } else {
         d3 arm = z[k] - cc;
         d3 tq = cross(arm, f);
