@@ -118,7 +118,7 @@ def run_ours(args, rank, local, ws):
 
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
-    from paper_2603_28475_b200.dist import MarkerGather, env_range
+    from paper_2603_28475_b200.dist import MarkerGather, NativeMarkerGather, env_range
     nsteps = max(64, args.warmup + 3 * args.steps + 1)  # warm-up, timed, profiled pass, e2e
     if args.scaling == "strong":  # C4 strong: a fixed total split over the ranks
         e0, e1 = env_range(rank, ws, args.total_envs)
@@ -142,16 +142,27 @@ def run_ours(args, rank, local, ws):
     sim = P.TacSim.from_scene(scene, device=local)
     poses = torch.tensor(scene.poses, dtype=torch.float32, device=dev).contiguous()  # resident in HBM
     nm = scene.markers.shape[0]
-    mg = MarkerGather(E, nm, 2, rank, ws, dev)
-    mk = mg.slot  # tac_markers writes the rank's slot; in-place all-gather to every rank (C4)
-    gather = mg if (ws > 1 or os.environ.get("TAC_FORCE_DIST")) else None
+    distributed = ws > 1 or bool(os.environ.get("TAC_FORCE_DIST"))
+    # N > 1 (C4): the marker fields of every rank are all-gathered in place every step --
+    # through the C ABI (tac_gather_markers: tac_markers into the rank's slot + ncclAllGather
+    # on the same stream) unless TAC_TORCH_GATHER selects torch.distributed's all-gather
+    native = distributed and not os.environ.get("TAC_TORCH_GATHER")
+    mg = NativeMarkerGather(sim, E, nm, 2, rank, ws, dev) if native else MarkerGather(E, nm, 2, rank, ws, dev)
+    mk = mg.slot  # this rank's slot of the gather buffer
+    gather = mg if distributed else None
     stream = torch.cuda.current_stream()
 
-    def one_step(k):
-        sim.step(poses[k], scene.dt)
+    def emit_markers():
+        if native:
+            gather.gather()
+            return
         sim.markers(mk)
         if gather is not None:
             gather.gather()
+
+    def one_step(k):
+        sim.step(poses[k], scene.dt)
+        emit_markers()
 
     launches = 0
     for k in range(args.warmup):
@@ -172,10 +183,8 @@ def run_ours(args, rank, local, ws):
     for k in range(args.warmup, args.warmup + args.steps):
         sim.step(poses[k], scene.dt)
         launches += sim.last_launch_count()
-        sim.markers(mk)
+        emit_markers()
         launches += sim.last_launch_count()
-        if gather is not None:
-            gather.gather()
         if args.tol is not None:  # tolerance mode: per-env iteration counts of this step
             iters_per_step.append(sim.env_status()[0])
             launches += 1
@@ -257,9 +266,7 @@ def run_ours(args, rank, local, ws):
         k = min(base + j, nsteps - 1)
         dpose.copy_(host_poses[k], non_blocking=True)
         sim.step(dpose, scene.dt)
-        sim.markers(mk)
-        if gather is not None:
-            gather.gather()
+        emit_markers()
         host_mk.copy_(mk, non_blocking=True)
         torch.cuda.current_stream().synchronize()
     w1 = time.perf_counter()
@@ -295,7 +302,8 @@ def run_ours(args, rank, local, ws):
         "config": {"workload": WORKLOADS[args.config],
                    "envs_per_gpu": E, "total_envs": n_all, "iters_per_step": args.iters if args.tol is None else None,
                    "iteration_mode": "fixed" if args.tol is None else f"tolerance (tol_x {args.tol:g} m, max {args.max_iters})",
-                   "parallelism": f"env-sharded dp{ws}" + (" + NCCL all-gather of markers" if ws > 1 else ""),
+                   "parallelism": f"env-sharded dp{ws}" + ((" + NCCL all-gather of markers ("
+                                  + ("tac_gather_markers, C ABI" if native else "torch.distributed") + ")") if distributed else ""),
                    "l2": "per-env state ~470 MB/GPU > 126 MB L2 (no flush needed)"},
         "roofline": roof,
         "hbm_iteration": hbm_it,

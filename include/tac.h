@@ -144,6 +144,28 @@ tac_status tac_step(tac_sim* sim, const float* target_poses, float dt, void* str
  * = (u_m.t1, u_m.t2[, u_m.n]) with u_m = sum_j w_mj u_j.  ncomp in {2, 3}. */
 tac_status tac_markers(tac_sim* sim, float* out, int32_t ncomp, void* stream);
 
+/* ---- marker all-gather to the policy rank (SURVEY §8b "L4", §8e; one
+ * set of environments per GPU, the marker fields go to the policy) ----
+ * NCCL is resolved at run time (dlopen of the libnccl.so.2 the process already loaded, e.g.
+ * torch's, else the system one): libtac.so itself has no NCCL dependency.  TAC_EINVAL if NCCL
+ * cannot be loaded.
+ *
+ * tac_nccl_unique_id: out = a fresh 128-byte ncclUniqueId (call on one rank, share the bytes
+ *   with the others out of band, e.g. a torch.distributed broadcast).
+ * tac_nccl_comm_create: ncclCommInitRank(nranks, id, rank) on CUDA device `device`; *comm is
+ *   an opaque ncclComm_t owned by the caller (collective call: every rank must enter it).
+ * tac_nccl_comm_destroy: ncclCommDestroy.
+ * tac_gather_markers: writes this simulator's marker field ([n_envs][rows*cols][ncomp], as
+ *   tac_markers) into slot `rank` of recvbuf (device fp32 [nranks * n_envs][rows*cols][ncomp],
+ *   rank = the comm's rank) and all-gathers the slots in place on `stream` (ncclAllGather,
+ *   NVLink / NVSwitch between the GPUs of a node).  Every rank must hold the same n_envs and
+ *   ncomp.  Asynchronous on `stream`; TAC_EINVAL on a null pointer or bad ncomp, TAC_ECUDA
+ *   on an NCCL failure (message in tac_last_error). */
+tac_status tac_nccl_unique_id(uint8_t out[128]);
+tac_status tac_nccl_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, int32_t device, void** comm);
+tac_status tac_nccl_comm_destroy(void* comm);
+tac_status tac_gather_markers(tac_sim* sim, void* nccl_comm, float* recvbuf, int32_t ncomp, void* stream);
+
 /* Per-step target pose noise (PAPER.md Table "Parameters Randomization Range", P:693-694,
  * "IPC Rand. Move. Noise", and P:726 "a small random movement on holding object" at each
  * timestep; reading DESIGN.md R27).  From the next tac_step on, env e's target

@@ -9,7 +9,7 @@ LIB = os.path.join(HERE, "libtac.so")
 SOURCES = ["api.cu", "kernels.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-         "-shared", "-Xptxas", "-warn-spills"]
+         "-shared", "-Xptxas", "-warn-spills", "-ldl"]
 
 
 def needs_build():

@@ -5,6 +5,8 @@
 // static, shared by all envs), fp64 marker location, device allocation in the
 // env-fastest layout of internal.h.  tac_step: the launch sequence of SURVEY §3.3
 // (rows a1-a9) on the caller's stream, no host synchronisation in fixed-iteration mode.
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <array>
 #include <cmath>
@@ -1094,6 +1096,99 @@ tac_status tac_markers(tac_sim* sim, float* out, int32_t ncomp, void* stream) {
   g_prof = nullptr;
   sim->launches = g_launches;
   return post_launch(sim);
+}
+
+// ------------------------------------------------------------ marker all-gather over NCCL
+// NCCL entry points resolved at run time (no link dependency; the process's already-loaded
+// libnccl.so.2 -- torch's -- is preferred so one NCCL serves the whole process).
+namespace {
+typedef struct { char internal[128]; } nccl_uid;
+typedef int (*nccl_get_uid_t)(nccl_uid*);
+typedef int (*nccl_init_rank_t)(void**, int, nccl_uid, int);
+typedef int (*nccl_destroy_t)(void*);
+typedef int (*nccl_allgather_t)(const void*, void*, size_t, int, void*, cudaStream_t);
+typedef int (*nccl_user_rank_t)(const void*, int*);
+typedef int (*nccl_count_t)(const void*, int*);
+typedef const char* (*nccl_errstr_t)(int);
+struct NcclApi {
+  bool ok = false;
+  nccl_get_uid_t get_uid = nullptr;
+  nccl_init_rank_t init_rank = nullptr;
+  nccl_destroy_t destroy = nullptr;
+  nccl_allgather_t allgather = nullptr;
+  nccl_user_rank_t user_rank = nullptr;
+  nccl_count_t count = nullptr;
+  nccl_errstr_t errstr = nullptr;
+};
+constexpr int kNcclFloat32 = 7;  // ncclFloat32 in nccl.h's ncclDataType_t
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
+    if (!h) return a;
+    a.get_uid = (nccl_get_uid_t)dlsym(h, "ncclGetUniqueId");
+    a.init_rank = (nccl_init_rank_t)dlsym(h, "ncclCommInitRank");
+    a.destroy = (nccl_destroy_t)dlsym(h, "ncclCommDestroy");
+    a.allgather = (nccl_allgather_t)dlsym(h, "ncclAllGather");
+    a.user_rank = (nccl_user_rank_t)dlsym(h, "ncclCommUserRank");
+    a.count = (nccl_count_t)dlsym(h, "ncclCommCount");
+    a.errstr = (nccl_errstr_t)dlsym(h, "ncclGetErrorString");
+    a.ok = a.get_uid && a.init_rank && a.destroy && a.allgather && a.user_rank && a.count && a.errstr;
+    return a;
+  }();
+  return api;
+}
+}  // namespace
+
+tac_status tac_nccl_unique_id(uint8_t out[128]) {
+  if (!out || !nccl().ok) return TAC_EINVAL;
+  nccl_uid id;
+  if (nccl().get_uid(&id) != 0) return TAC_ECUDA;
+  std::memcpy(out, id.internal, 128);
+  return TAC_OK;
+}
+
+tac_status tac_nccl_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, int32_t device, void** comm) {
+  if (!id || !comm || nranks < 1 || rank < 0 || rank >= nranks || !nccl().ok) return TAC_EINVAL;
+  *comm = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) return TAC_ECUDA;
+  nccl_uid u;
+  std::memcpy(u.internal, id, 128);
+  return nccl().init_rank(comm, nranks, u, rank) == 0 ? TAC_OK : TAC_ECUDA;
+}
+
+tac_status tac_nccl_comm_destroy(void* comm) {
+  if (!comm || !nccl().ok) return TAC_EINVAL;
+  return nccl().destroy(comm) == 0 ? TAC_OK : TAC_ECUDA;
+}
+
+tac_status tac_gather_markers(tac_sim* sim, void* comm, float* recvbuf, int32_t ncomp, void* stream) {
+  tac_status st = check_sim(sim);
+  if (st) return st;
+  if (!comm || !recvbuf || (ncomp != 2 && ncomp != 3)) { sim->err = "tac_gather_markers: bad argument"; return TAC_EINVAL; }
+  if (!nccl().ok) { sim->err = "tac_gather_markers: NCCL not available"; return TAC_EINVAL; }
+  int rank = 0, nranks = 0;
+  if (nccl().user_rank(comm, &rank) != 0 || nccl().count(comm, &nranks) != 0) {
+    sim->err = "tac_gather_markers: invalid communicator";
+    return TAC_EINVAL;
+  }
+  cudaSetDevice(sim->device);
+  const size_t count = (size_t)sim->d.E * sim->d.nm * ncomp;
+  float* slot = recvbuf + (size_t)rank * count;
+  g_launches = 0;
+  g_prof = sim->prof;
+  launch_markers(sim->d, slot, ncomp, (cudaStream_t)stream);  // this rank's slot, then in place
+  g_prof = nullptr;
+  sim->launches = g_launches;
+  if ((st = post_launch(sim))) return st;
+  const int rc = nccl().allgather(slot, recvbuf, count, kNcclFloat32, comm, (cudaStream_t)stream);
+  if (rc != 0) {
+    sim->err = std::string("ncclAllGather: ") + nccl().errstr(rc);
+    return TAC_ECUDA;
+  }
+  return TAC_OK;
 }
 
 tac_status tac_marker_sqerr(tac_sim* sim, const float* ref, double* acc, int32_t ncomp, void* stream) {

@@ -40,3 +40,29 @@ class MarkerGather:
             parts = list(self.buffer.chunk(self.world))
             dist.all_gather(parts, self.slot.clone(), group=self.group)
         return self.buffer
+
+
+class NativeMarkerGather:
+    """The same gather through the C ABI (tac_gather_markers: tac_markers into this rank's slot +
+    an in-place ncclAllGather on the caller's stream) with an NCCL communicator created by
+    tac_nccl_comm_create; the unique id travels over the existing torch.distributed group.
+    Requires equal n_local on every rank."""
+
+    def __init__(self, sim, n_local, n_markers, ncomp, rank, world, device):
+        import torch
+        import torch.distributed as dist
+        from .tac import NcclComm, nccl_unique_id
+        uid = [nccl_unique_id() if rank == 0 else None]
+        if dist.is_initialized():
+            dist.broadcast_object_list(uid, src=0)
+        dev = torch.device(device)
+        self.comm = NcclComm(uid[0], world, rank, dev.index if dev.index is not None else 0)
+        self.sim, self.ncomp = sim, ncomp
+        self.buffer = torch.empty((world * n_local, n_markers, ncomp), dtype=torch.float32, device=dev)
+        self.slot = self.buffer[rank * n_local:(rank + 1) * n_local]
+
+    def gather(self):
+        return self.sim.gather_markers(self.comm, self.buffer, self.ncomp)
+
+    def close(self):
+        self.comm.close()

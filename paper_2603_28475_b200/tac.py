@@ -77,6 +77,10 @@ def lib():
         L.tac_marker_sqerr.argtypes = [vp, vp, vp, C.c_int32, vp]
         L.tac_set_pose_noise.argtypes = [vp, C.c_double, C.c_double, C.c_uint64, C.c_int64]
         L.tac_info.argtypes = [vp, _ip]
+        L.tac_nccl_unique_id.argtypes = [vp]
+        L.tac_nccl_comm_create.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, C.POINTER(vp)]
+        L.tac_nccl_comm_destroy.argtypes = [vp]
+        L.tac_gather_markers.argtypes = [vp, vp, vp, C.c_int32, vp]
         L.tac_last_launch_count.argtypes = [vp]
         L.tac_last_launch_count.restype = C.c_int64
         L.tac_destroy.argtypes = [vp]
@@ -102,7 +106,8 @@ EXPORTED = ["tac_create", "tac_step", "tac_markers", "tac_reset", "tac_env_statu
             "tac_last_launch_count", "tac_destroy", "tac_last_error", "tac_get_state", "tac_set_state",
             "tac_debug_broadphase", "tac_debug_surface", "tac_debug_marker_map", "tac_debug_eval",
             "tac_profile_enable", "tac_profile_read", "tac_profile_kernel_name", "tac_env_stats",
-            "tac_set_env_material", "tac_marker_sqerr", "tac_set_pose_noise"]
+            "tac_set_env_material", "tac_marker_sqerr", "tac_set_pose_noise", "tac_nccl_unique_id",
+            "tac_nccl_comm_create", "tac_nccl_comm_destroy", "tac_gather_markers"]
 N_KERNEL_IDS = 24
 
 
@@ -209,6 +214,15 @@ class TacSim:
         self._check(lib().tac_markers(self.h, C.c_void_p(out.data_ptr()), ncomp, _stream_ptr(stream)), "tac_markers")
         return out
 
+    def gather_markers(self, comm, recvbuf, ncomp=2, stream=None):
+        """tac_gather_markers: this rank's marker field into its slot of recvbuf (CUDA fp32
+        [nranks * n_envs, n_markers, ncomp]) and an in-place NCCL all-gather of the slots."""
+        assert recvbuf.is_cuda and recvbuf.is_contiguous() and recvbuf.dtype.is_floating_point
+        assert recvbuf.numel() == comm.nranks * self.n_envs * self.nm * ncomp, "recvbuf size"
+        self._check(lib().tac_gather_markers(self.h, comm.handle, C.c_void_p(recvbuf.data_ptr()), ncomp,
+                                             _stream_ptr(stream)), "tac_gather_markers")
+        return recvbuf
+
     def set_pose_noise(self, sigma_t, sigma_r, seed, env_offset=0):
         """Per-step target pose noise (R27): translation amplitude [m], rotation [rad]."""
         self._check(lib().tac_set_pose_noise(self.h, float(sigma_t), float(sigma_r), int(seed), int(env_offset)),
@@ -311,3 +325,32 @@ class TacSim:
         self._check(lib().tac_debug_eval(self.h, env, *(a[1] for a in ins), float(dt),
                                          *(a.ctypes.data_as(_dp) for a in (parts, g, D, gr, Dr))), "tac_debug_eval")
         return dict(E=parts.sum(), parts=parts, g=g, D=D, grig=gr, Drig=Dr)
+
+
+def nccl_unique_id() -> bytes:
+    """tac_nccl_unique_id: a fresh 128-byte NCCL unique id (share it with the other ranks)."""
+    import torch  # noqa: F401  (load torch's libnccl.so.2 first: the C ABI then resolves that one)
+    buf = (C.c_uint8 * 128)()
+    st = lib().tac_nccl_unique_id(C.cast(buf, C.c_void_p))
+    if st != 0:
+        raise TacError(f"tac_nccl_unique_id failed ({st}): NCCL not loadable")
+    return bytes(buf)
+
+
+class NcclComm:
+    """An NCCL communicator created through the C ABI (tac_nccl_comm_create); collective."""
+
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: int):
+        assert len(uid) == 128
+        import torch  # noqa: F401  (torch's libnccl.so.2, as in nccl_unique_id)
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        st = lib().tac_nccl_comm_create(C.cast(buf, C.c_void_p), nranks, rank, device, C.byref(h))
+        if st != 0:
+            raise TacError(f"tac_nccl_comm_create failed ({st})")
+        self.handle, self.nranks, self.rank = h, nranks, rank
+
+    def close(self):
+        if self.handle:
+            lib().tac_nccl_comm_destroy(self.handle)
+            self.handle = None

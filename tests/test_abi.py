@@ -45,3 +45,19 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".h", ".cpp")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", txt).lower().replace("oracle-verified", ""), f
+
+
+def test_nccl_unique_id_through_the_c_abi():
+    """tac_nccl_unique_id resolves NCCL at run time (no link dependency of libtac.so) and
+    returns a fresh 128-byte id; host-only, no GPU needed."""
+    a, b = P.nccl_unique_id(), P.nccl_unique_id()
+    assert len(a) == 128 and len(b) == 128 and a != b
+    import subprocess
+    out = subprocess.run(["ldd", P.LIB_PATH], capture_output=True, text=True).stdout
+    assert "nccl" not in out
+
+
+def test_gather_markers_rejects_bad_arguments():
+    L = P.lib()
+    assert L.tac_gather_markers(None, None, None, 2, None) != 0
+    assert L.tac_nccl_comm_create(None, 1, 0, 0, None) != 0

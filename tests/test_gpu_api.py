@@ -144,3 +144,26 @@ def test_several_simulators_in_one_process(torch):
         a.step(_poses(torch, big.poses[k]), big.dt)
         b.step(_poses(torch, small.poses[k]), small.dt)
     assert torch.isfinite(a.markers()).all() and torch.isfinite(b.markers()).all()
+
+
+def test_native_marker_gather_world_of_one(torch):
+    """tac_gather_markers on a one-rank NCCL communicator created through the C ABI: the
+    gathered buffer equals tac_markers' field (the N > 1 exchange is
+    the same ncclAllGather over more ranks)."""
+    import paper_2603_28475_b200 as P
+    from paper_2603_28475_b200.dist import NativeMarkerGather
+    s = w.scene_small_peg(n_envs=5, n_steps=2)
+    s.params.fixed_iters = 20
+    sim = _sim(s)
+    sim.step(_poses(torch, s.poses[0]), s.dt)
+    g = NativeMarkerGather(sim, 5, sim.nm, 2, 0, 1, "cuda:0")
+    buf = g.gather()
+    ref = sim.markers()
+    torch.cuda.synchronize()
+    assert torch.equal(buf, ref)
+    g3 = NativeMarkerGather(sim, 5, sim.nm, 3, 0, 1, "cuda:0")
+    assert torch.equal(g3.gather(), sim.markers(ncomp=3))
+    with pytest.raises(P.TacError):
+        sim.gather_markers(g.comm, torch.empty((5, sim.nm, 4), device="cuda"), ncomp=4)
+    g.close()
+    g3.close()
