@@ -949,6 +949,10 @@ double alpha_ccd(const Problem& P, const State& s, const std::vector<Pair>& C, c
       continue;
     }
     Dist D = pair_dist(P, s, pr);
+    if (D.d >= P.dhat) {  // exact distance >= dhat: a far pair like the certified ones (R15)
+      any_far = true;
+      continue;
+    }
     V3 r{0, 0, 0};
     for (int k = 0; k < 4; ++k) r = add(r, scl(D.w[k], z[k]));
     n = scl(1.0 / D.d, r);

@@ -8,6 +8,7 @@
 //   contact kernels: blockIdx.y = env, threads stride over that env's candidate pairs;
 //   scalar kernels: one thread per env (fp64 control flow of the NCG).
 #include <cfloat>
+#include <cstdlib>
 #include <cmath>
 
 #include "internal.h"
@@ -288,6 +289,48 @@ __device__ DR dist_ee(d3 a0, d3 a1, d3 b0, d3 b1) {
   return r;
 }
 
+// ---- fp32 squared distances on coordinates relative to the pair's first corner: only a
+// far/near screen (the same case logic as dist_pt / dist_ee, no weights).  Rounding of the
+// relative coordinates and of the case solves stays below ~1e-9 m at pad scale, so a pair
+// screened with sqrt(d2) >= dhat + kNearScreen (1e-6 m) is far for the exact distance too.
+struct f3 {
+  float x, y, z;
+};
+__device__ __forceinline__ f3 f3sub(f3 a, f3 b) { return f3{a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ float f3dot(f3 a, f3 b) { return fmaf(a.x, b.x, fmaf(a.y, b.y, a.z * b.z)); }
+__device__ __forceinline__ f3 f3axpy(float s, f3 a, f3 b) { return f3{fmaf(s, a.x, b.x), fmaf(s, a.y, b.y), fmaf(s, a.z, b.z)}; }
+__device__ __forceinline__ float seg_d2f(f3 p, f3 a, f3 e, float iee) {  // |p - closest point of segment a + u e|^2
+  const float u = fminf(1.f, fmaxf(0.f, f3dot(f3sub(p, a), e) * iee));
+  const f3 v = f3sub(p, f3axpy(u, e, a));
+  return f3dot(v, v);
+}
+__device__ float dist2_pt_f(f3 p, f3 t0, f3 t1, f3 t2) {
+  const f3 e1 = f3sub(t1, t0), e2 = f3sub(t2, t0), q = f3sub(p, t0);
+  const float a11 = f3dot(e1, e1), a12 = f3dot(e1, e2), a22 = f3dot(e2, e2), r1 = f3dot(q, e1), r2 = f3dot(q, e2);
+  const float idet = 1.f / (a11 * a22 - a12 * a12);
+  const float s = (a22 * r1 - a12 * r2) * idet, t = (a11 * r2 - a12 * r1) * idet;
+  if (s >= 0.f && t >= 0.f && s + t <= 1.f) {
+    const f3 v = f3axpy(-t, e2, f3axpy(-s, e1, q));
+    return f3dot(v, v);
+  }
+  const f3 e3 = f3sub(t2, t1);
+  return fminf(fminf(seg_d2f(p, t0, e1, 1.f / a11), seg_d2f(p, t0, e2, 1.f / a22)), seg_d2f(p, t1, e3, 1.f / f3dot(e3, e3)));
+}
+__device__ float dist2_ee_f(f3 a0, f3 a1, f3 b0, f3 b1) {
+  const f3 d1 = f3sub(a1, a0), d2 = f3sub(b1, b0), q = f3sub(a0, b0);
+  const float a = f3dot(d1, d1), e = f3dot(d2, d2), b = f3dot(d1, d2), c = f3dot(d1, q), f = f3dot(d2, q);
+  const float den = a * e - b * b;
+  if (den > 1e-6f * a * e) {
+    const float iden = 1.f / den;
+    const float s = (b * f - c * e) * iden, t = (a * f - b * c) * iden;
+    if (s > 0.f && s < 1.f && t > 0.f && t < 1.f) {
+      const f3 v = f3axpy(-t, d2, f3axpy(s, d1, q));
+      return f3dot(v, v);
+    }
+  }
+  const float ia = 1.f / a, ie = 1.f / e;
+  return fminf(fminf(seg_d2f(a0, b0, d2, ie), seg_d2f(a1, b0, d2, ie)), fminf(seg_d2f(b0, a0, d1, ia), seg_d2f(b1, a0, d1, ia)));
+}
 // corners of a candidate / anchor: ids and sides (gel or indenter)
 struct Corners {
   int id[4];
@@ -1533,6 +1576,9 @@ __global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
   // near-ordered output slots: kinds 0, 1, 2 concatenated (the counts are final after classify)
   const int base = (KIND >= 1 ? d.nnear[3 * e] : 0) + (KIND >= 2 ? d.nnear[3 * e + 1] : 0);
   const uint2* list = d.nearl + ((size_t)e * 3 + KIND) * d.kmax;  // packed corners of the near pairs
+  constexpr float kNearScreen = 1e-6f;
+  const float far2 = ((float)d.dhat + kNearScreen) * ((float)d.dhat + kNearScreen);
+  bool far = false;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const uint2 cw = list[j];
     const unsigned id[4] = {cw.x & 0xffffu, cw.x >> 16, cw.y & 0xffffu, cw.y >> 16};
@@ -1551,11 +1597,28 @@ __global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
     const size_t slot = (size_t)e * d.kmax + base + j;
     d.ncorn[slot] = cw;
     float4* geo = d.cgeo + 2 * slot;
+    {  // fp32 screen: a pair at exact distance >= dhat carries no energy and is covered by
+       // the shared far-pair step bound (R15), like a pair the classification certified
+      f3 zf[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) zf[k] = f3{(float)(z[k].x - z[0].x), (float)(z[k].y - z[0].y), (float)(z[k].z - z[0].z)};
+      const float d2 = KIND == 2 ? dist2_ee_f(zf[0], zf[1], zf[2], zf[3]) : dist2_pt_f(zf[0], zf[1], zf[2], zf[3]);
+      if (d2 >= far2) {
+        far = true;
+        geo[0] = make_float4(0.f, 0.f, 0.f, 0.f);  // skipped by the curvature pass
+        continue;
+      }
+    }
     DR D = KIND == 2 ? dist_ee(z[0], z[1], z[2], z[3]) : dist_pt(z[0], z[1], z[2], z[3]);
     if (!(D.d > 0)) {
       Eb = INFINITY;
       geo[0] = make_float4(0.f, 0.f, 0.f, 0.f);
       geo[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+      continue;
+    }
+    if (D.d >= d.dhat) {  // exact distance >= dhat: far (R15), as the fp32 screen above
+      far = true;
+      geo[0] = make_float4(0.f, 0.f, 0.f, 0.f);
       continue;
     }
     d3 rr = mk(0, 0, 0);
@@ -1564,7 +1627,6 @@ __global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
     d3 nn = (1.0 / D.d) * rr;
     geo[0] = make_float4((float)D.d, (float)nn.x, (float)nn.y, (float)nn.z);
     geo[1] = make_float4((float)D.w[0], (float)D.w[1], (float)D.w[2], (float)D.w[3]);
-    if (D.d >= d.dhat) continue;
     double lg = log(D.d / d.dhat), dm = D.d - d.dhat, inv = 1.0 / D.d;
     Eb += kappa * (-dm * dm * lg);                                       // b
     double db = kappa * (-2 * dm * lg - dm * dm * inv);                  // b'
@@ -1588,6 +1650,8 @@ __global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
     add_sym(Dc, nn, ddb * sig * sig);
     add_sym(Dt, cross(rho, nn), ddb);
   }
+  if (__any_sync(0xffffffffu, far) && (threadIdx.x & 31) == 0)
+    atomic_min_pos(d.accu + (size_t)U_GFAR * d.Es + e, (float)d.dhat);
   double vals[20];
   vals[0] = Eb;
   vals[1] = 0;
@@ -1680,8 +1744,11 @@ __global__ void __launch_bounds__(128) k_contact_friction(Dev d, double eps_f) {
   // warp-uniform trip count (the aggregated scatter is a warp collective)
   for (int b0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); b0 < na; b0 += gridDim.x * blockDim.x) {
     const int i = b0 + lane;
-    float sc[3][9];
+    // per-corner terms are formed at their reduction from a few shared factors (force
+    // direction, T T^T entries, f1 and the corner weights), not held as 3 x 9 values
     unsigned key[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu};
+    float Ttf[3] = {0.f, 0.f, 0.f}, tt[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, wf[3] = {0.f, 0.f, 0.f};
+    float f1f = 0.f;
     if (i < na) {
     const Anchor& A = d.anc[(size_t)e * d.amax + i];
     const int gid[3] = {A.gid[0], A.gid[1], A.gid[2]};
@@ -1704,22 +1771,15 @@ __global__ void __launch_bounds__(128) k_contact_friction(Dev d, double eps_f) {
     double f1 = ml * moll_f1(sn, eps_f);
     d.anc_f1[(size_t)e * d.amax + i] = (float)f1;
     d3 Tt = ta * t1 + tb * t2;
+    f1f = (float)f1;
+    Ttf[0] = (float)Tt.x; Ttf[1] = (float)Tt.y; Ttf[2] = (float)Tt.z;
+    // GN: f1 w^2 T T^T (R8)
+    tt[0] = (float)(t1.x * t1.x + t2.x * t2.x); tt[1] = (float)(t1.y * t1.y + t2.y * t2.y);
+    tt[2] = (float)(t1.z * t1.z + t2.z * t2.z); tt[3] = (float)(t1.x * t1.y + t2.x * t2.y);
+    tt[4] = (float)(t1.x * t1.z + t2.x * t2.z); tt[5] = (float)(t1.y * t1.z + t2.y * t2.z);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const int v = gid[k];
-      if (v < 0) continue;
-      double wk = A.w[k];
-      d3 f = (f1 * wk) * Tt;
-      double sw = f1 * wk * wk;  // GN: f1 w^2 T T^T (R8)
-      key[k] = (unsigned)v;
-      sc[k][0] = (float)f.x; sc[k][1] = (float)f.y; sc[k][2] = (float)f.z;
-      sc[k][3] = (float)(sw * (t1.x * t1.x + t2.x * t2.x));
-      sc[k][4] = (float)(sw * (t1.y * t1.y + t2.y * t2.y));
-      sc[k][5] = (float)(sw * (t1.z * t1.z + t2.z * t2.z));
-      sc[k][6] = (float)(sw * (t1.x * t1.y + t2.x * t2.y));
-      sc[k][7] = (float)(sw * (t1.x * t1.z + t2.x * t2.z));
-      sc[k][8] = (float)(sw * (t1.y * t1.z + t2.y * t2.z));
-    }
+    for (int k = 0; k < 3; ++k)
+      if (gid[k] >= 0) { key[k] = (unsigned)gid[k]; wf[k] = A.w[k]; }
     // indenter side: force f1 sig T tau on c, torque rho x (f1 T tau)
     d3 F = (f1 * sig) * Tt, tq = cross(rho, f1 * Tt);
     gr[0] += F.x; gr[1] += F.y; gr[2] += F.z; gr[3] += tq.x; gr[4] += tq.y; gr[5] += tq.z;
@@ -1730,11 +1790,13 @@ __global__ void __launch_bounds__(128) k_contact_friction(Dev d, double eps_f) {
     }
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      if (key[k] == 0xffffffffu) {
+      float sc[9];
+      const float fw = f1f * wf[k], sw = fw * wf[k];  // 0 for an absent corner (wf = 0)
 #pragma unroll
-        for (int m = 0; m < 9; ++m) sc[k][m] = 0.f;
-      }
-      seg_red9(d, e, key[k], sc[k]);
+      for (int c = 0; c < 3; ++c) sc[c] = fw * Ttf[c];
+#pragma unroll
+      for (int m = 0; m < 6; ++m) sc[3 + m] = sw * tt[m];
+      seg_red9(d, e, key[k], sc);
     }
   }
   double vals[20];
@@ -2741,7 +2803,8 @@ static int eblocks(const Dev& d) { return (d.E + 127) / 128; }
 // the envs over E / 32 SMs instead of E / 128
 static int eblocks32(const Dev& d) { return (d.E + 31) / 32; }
 static dim3 sgrid(const Dev& d) {  // staged contact kernels: chunks per env
-  int nb = std::max(1, std::min(16, 2368 / std::max(1, d.E)));
+  static const int cap = getenv("TAC_SGRID_CAP") ? atoi(getenv("TAC_SGRID_CAP")) : 16;  // A/B experiments
+  int nb = std::max(1, std::min(cap, 2368 / std::max(1, d.E)));
   return dim3(nb, d.E);
 }
 // Every launch is a programmatic dependent launch: the next kernel's CTAs may be resident
