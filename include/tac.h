@@ -107,11 +107,15 @@ typedef struct {
  *   stagnation      iterations without |P g| progress before giving up (0 = off)
  *   max_candidates  per-env capacity of candidate pairs (0 = default 16384)
  *   max_anchors     per-env capacity of friction anchors (0 = default 4096; at most 16384)
- *   check_every     tolerance mode: host polls "all envs done" every N iterations */
+ *   check_every     tolerance mode: host polls "all envs done" every N iterations
+ *   pose_al         1: augmented-Lagrangian pose enforcement (R29): the pose
+ *                   term gains h^2 (lam_t . (c - c*) + lam_r . log(R R*^T)) with per-env multipliers,
+ *                   updated after every step by the spring force, lam += psi'(r) r/|r| (reset by
+ *                   tac_reset); 0: plain penalty (default).  Outside {0, 1} -> TAC_EINVAL */
 typedef struct {
   double dhat, kappa_phys, eps_v, tol_x, k_t, k_r, f_max, t_max, ccd_s, bp_margin, c1, eps_E;
   int32_t max_iters, fixed_iters, beta_rule, precond, max_halvings, stagnation;
-  int32_t max_candidates, max_anchors, check_every;
+  int32_t max_candidates, max_anchors, check_every, pose_al;
 } tac_solver_params;
 
 typedef struct {

@@ -53,6 +53,8 @@ def lib():
         L.or_trace.restype = C.c_int
         L.or_trace.argtypes = [C.c_void_p, C.c_int, _dp, C.c_int]
         L.or_markers.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp]
+        L.or_set_eval_lambda.argtypes = [C.c_void_p, _dp]
+        L.or_get_lambda.argtypes = [C.c_void_p, C.c_int, _dp]
         L.or_eval.restype = C.c_double
         L.or_eval.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, C.c_double, _dp, _dp, _dp, _dp, _dp,
                               _ip, _ip]
@@ -195,7 +197,7 @@ class Oracle:
         dp, dpp = _d([p.dhat, p.kappa_phys, p.eps_v, p.tol_x, p.k_t, p.k_r, p.ccd_s, p.bp_margin, p.c1, p.f_max,
                       p.t_max])
         ip, ipp = _i([p.max_iters, p.fixed_iters, p.beta_rule, p.precond, p.max_halvings, p.stagnation, marker_mode,
-                      knn_k, int(debug)])
+                      knn_k, int(debug), int(getattr(p, "pose_al", 0))])
         init = scene.init_poses if init_poses is None else init_poses
         self.n_envs = init.shape[0]
         ini, inip = _d(init)
@@ -275,6 +277,17 @@ class Oracle:
     def markers(self, env, ncomp=2):
         out = np.zeros((self.nm, ncomp))
         lib().or_markers(self.h, env, ncomp, out.ctypes.data_as(_dp))
+        return out
+
+    def set_eval_lambda(self, lam6):
+        """Pose multipliers (lam_t, lam_r) that eval() uses (augmented Lagrangian, R29)."""
+        a = np.ascontiguousarray(lam6, dtype=np.float64)
+        lib().or_set_eval_lambda(self.h, a.ctypes.data_as(_dp))
+
+    def lambda_of(self, env):
+        """Env's current pose multipliers [lam_t (N), lam_r (N m)] after its last step."""
+        out = np.zeros(6)
+        lib().or_get_lambda(self.h, env, out.ctypes.data_as(_dp))
         return out
 
     def eval(self, u_t, v_t, c_t, R_t, u, c, R, target7, dt=None):

@@ -146,6 +146,15 @@ double moll_f1(double s, double eps) {  // f'(s)/s, finite at s=0
   return -s / (eps * eps) + 2 / eps;
 }
 
+// J_l(phi)^-T x for the SO(3) left Jacobian: J_l^-1 = I - [phi]/2 + c(t) [phi]^2,
+// c(t) = (1 - (t/2) cot(t/2)) / t^2 (-> 1/12), t = |phi|; its transpose flips the [phi] term
+V3 so3_jl_inv_T(const V3& phi, const V3& x) {
+  double t = norm(phi);
+  double c = t < 1e-4 ? 1.0 / 12.0 + t * t / 720.0 : (1.0 - 0.5 * t / std::tan(0.5 * t)) / (t * t);
+  V3 px = cross(phi, x);
+  return add(add(x, scl(0.5, px)), scl(c, cross(phi, px)));
+}
+
 // ---- force-capped pose spring (R18) ----
 double huber(double r, double k, double cap) {
   double rho = cap / k;
@@ -293,6 +302,7 @@ struct Problem {
   double rho, mu_f;
   double dhat, kappa_phys, eps_v, tol_x, k_t, k_r, ccd_s, bp_margin, c1, f_max, t_max;
   int max_iters, fixed_iters, beta_rule, precond, max_halvings, stagnation, debug;
+  int pose_al;  // augmented-Lagrangian pose enforcement (R29)
 };
 
 struct Env {
@@ -302,6 +312,7 @@ struct Env {
   // last-step diagnostics
   int iters = 0, flags = 0;
   double pg = 0, dmin = INF, pose_res = 0;
+  V3 lam_t{0, 0, 0}, lam_r{0, 0, 0};  // pose multipliers (R29), 0 without pose_al
   std::vector<std::array<double, 16>> trace;
   bool want_trace = false;
 };
@@ -313,6 +324,7 @@ struct Oracle {
   double noise_t = 0, noise_r = 0;
   uint64_t noise_seed = 0, step_count = 0;
   int64_t env_offset = 0;
+  V3 eval_lam_t{0, 0, 0}, eval_lam_r{0, 0, 0};  // multipliers or_eval uses (tests of R29)
 };
 
 // ---------------------------------------------------------------------------
@@ -558,6 +570,7 @@ struct Step {  // per-step constants
   V3 cs;                   // target c*
   M3 Rs;                   // target R*
   double h, kappa, eps;
+  V3 lam_t{0, 0, 0}, lam_r{0, 0, 0};  // pose multipliers of this step (R29)
   std::vector<Anchor> anchors;
 };
 
@@ -739,10 +752,16 @@ double eval_energy(const Problem& P, const Step& S, const State& s, const std::v
   V3 dc = sub(s.c, S.cs);
   V3 phi = so3_log(matmul(s.R, transpose(S.Rs)));
   double Ep = h2 * (huber(norm(dc), P.k_t, P.f_max) + huber(norm(phi), P.k_r, P.t_max));
+  // augmented Lagrangian (R29): + h^2 (lam_t . dc + lam_r . phi); zero multipliers otherwise
+  Ep += h2 * (dot(S.lam_t, dc) + dot(S.lam_r, phi));
   if (G) {
     double wt = huber_w(norm(dc), P.k_t, P.f_max), wr = huber_w(norm(phi), P.k_r, P.t_max);
     G->gc = add(G->gc, scl(h2 * wt, dc));
     G->gth = add(G->gth, scl(h2 * wr, phi));  // exact left-trivialised gradient (App. B)
+    // d(lam . phi)/d delta for R <- exp([delta]) R: phi(delta) = log(exp(delta) exp(phi)) has
+    // the Jacobian J_l(phi)^-1, so the gradient is J_l(phi)^-T lam (R29)
+    G->gc = add(G->gc, scl(h2, S.lam_t));
+    G->gth = add(G->gth, scl(h2, so3_jl_inv_T(phi, S.lam_r)));
     for (int i = 0; i < 3; ++i) { G->Dc[4 * i] += h2 * wt; G->Dth[4 * i] += h2 * wr; }
   }
   if (parts) { parts[0] = Ein; parts[1] = Eel; parts[2] = Eb; parts[3] = Ef; parts[4] = Ep; }
@@ -1023,6 +1042,8 @@ void env_step(const Problem& P, Env& E, const double* target7, double h, const O
   S.eps = P.eps_v * h;             // eps = eps_v h
   S.cs = {target7[0], target7[1], target7[2]};
   S.Rs = quat_to_R(target7);
+  S.lam_t = E.lam_t;
+  S.lam_r = E.lam_r;
   if (O && (O->noise_t != 0 || O->noise_r != 0))
     perturb_target(O->noise_seed, O->step_count, (uint64_t)(env_id + O->env_offset), O->noise_t, O->noise_r, &S.cs,
                    &S.Rs);
@@ -1162,6 +1183,12 @@ void env_step(const Problem& P, Env& E, const double* target7, double h, const O
   E.c_t = s.c;
   E.R_t = s.R;
   E.pose_res = norm(sub(s.c, S.cs)) + P.rho_max * norm(so3_log(matmul(s.R, transpose(S.Rs))));
+  if (P.pose_al && !failed) {  // R29: lam += psi'(r) r/|r| at the step's solution (first-order AL update)
+    V3 dc = sub(s.c, S.cs);
+    V3 phi = so3_log(matmul(s.R, transpose(S.Rs)));
+    E.lam_t = add(E.lam_t, scl(huber_w(norm(dc), P.k_t, P.f_max), dc));
+    E.lam_r = add(E.lam_r, scl(huber_w(norm(phi), P.k_r, P.t_max), phi));
+  }
   if (P.debug) E.dmin = brute_dmin(P, s);
 }
 
@@ -1173,7 +1200,8 @@ void env_step(const Problem& P, Env& E, const double* target7, double h, const O
 extern "C" {
 
 // dparams: dhat, kappa_phys, eps_v, tol_x, k_t, k_r, ccd_s, bp_margin, c1, f_max, t_max
-// iparams: max_iters, fixed_iters, beta_rule, precond, max_halvings, stagnation, marker_mode, knn_k, debug
+// iparams: max_iters, fixed_iters, beta_rule, precond, max_halvings, stagnation, marker_mode, knn_k, debug,
+//          pose_al
 void* or_create(int nv, const double* X, int nt, const int* tets, int nfixed, const int* fixed, int niv,
                 const double* Y, int nit, const int* itris, int nm, const double* mk, const double* frame9,
                 const double* mat4, const double* dparams, const int* iparams, int n_envs, const double* init7,
@@ -1213,6 +1241,7 @@ void* or_create(int nv, const double* X, int nt, const int* tets, int nfixed, co
   P.max_iters = iparams[0]; P.fixed_iters = iparams[1]; P.beta_rule = iparams[2]; P.precond = iparams[3];
   P.max_halvings = iparams[4]; P.stagnation = iparams[5];
   P.debug = iparams[8];
+  P.pose_al = iparams[9];
   if (*status) return O;
   precompute(P);
   for (int e = 0; e < nt; ++e) if (!(P.vol[e] > 0)) *status = 2;
@@ -1327,6 +1356,17 @@ void or_markers(void* h, int env, int ncomp, double* out) {
 // Evaluate E, g, D at state (u, c, R) with friction anchors built at (u_t, c_t, R_t) and
 // candidates built at (u, c, R); target pose target7; step h.  parts[5] = inertia, elastic,
 // barrier, friction, pose.  g [nv*3], D [nv*9], grig [6] = (g_c, g_theta), Drig [18] = (Dc, Dth).
+// pose multipliers (R29): those or_eval uses, and an env's current ones (6 = lam_t, lam_r)
+void or_set_eval_lambda(void* h, const double* lam6) {
+  Oracle* O = (Oracle*)h;
+  O->eval_lam_t = {lam6[0], lam6[1], lam6[2]};
+  O->eval_lam_r = {lam6[3], lam6[4], lam6[5]};
+}
+void or_get_lambda(void* h, int env, double* lam6) {
+  const Env& E = ((Oracle*)h)->env[env];
+  for (int a = 0; a < 3; ++a) { lam6[a] = E.lam_t[a]; lam6[3 + a] = E.lam_r[a]; }
+}
+
 double or_eval(void* h, const double* u_t, const double* v_t, const double* ct, const double* Rt, const double* u,
                const double* c, const double* R, const double* target7, double dt, double* parts, double* g,
                double* D, double* grig, double* Drig, int* n_cand, int* n_anchor) {
@@ -1338,6 +1378,8 @@ double or_eval(void* h, const double* u_t, const double* v_t, const double* ct, 
   S.eps = P.eps_v * dt;
   S.cs = {target7[0], target7[1], target7[2]};
   S.Rs = quat_to_R(target7);
+  S.lam_t = O->eval_lam_t;
+  S.lam_r = O->eval_lam_r;
   S.xhat_u.resize(P.nv);
   State st, s;
   st.u.resize(P.nv);

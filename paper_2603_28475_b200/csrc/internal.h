@@ -47,6 +47,7 @@ struct EnvS {
   double gr[6], grp[6], pr[6];  // rigid gradient, previous gradient, direction (c, theta)
   double Dc[9], Dth[9];       // rigid diagonal blocks of the last accepted evaluation
   double E, Eprev, alpha, gp_prev, gPg_prev, S, beta, best_pg, pg, pose_res;
+  double lam[6];               // pose multipliers (lam_t [N], lam_r [N m]) of the AL pose term (R29)
   double Lrel_last;
   double odo, odo_base, Lc;   // classification odometer (R15 cache): path-length coordinate of the
                               // trial point / of x_k, L_rel of the current direction
@@ -139,6 +140,7 @@ struct Dev {
   long long env_offset;  // global id of env 0 (sharded ranks draw the streams of their global envs)
   double rho_max, dhat, kappa_phys, eps_v, tol_x, k_t, k_r, f_max, t_max, ccd_s, bp_margin, c1, eps_E, mu_f;
   int beta_rule, precond, max_halv, stagnation, fixed_iters;
+  int pose_al;           // augmented-Lagrangian pose enforcement (R29)
   // element tiles
   int ntiles;
   const int* tile_vstart;        // [ntiles + 1] into tile_verts

@@ -187,6 +187,15 @@ __device__ d3 so3_log(const double* R) {
   return (th / (2 * sin(th))) * v;
 }
 // force-capped pose spring weight psi'(r)/r (R18)
+// J_l(phi)^-T x, J_l the SO(3) left Jacobian: J_l^-1 = I - [phi]/2 + c(t) [phi]^2,
+// c(t) = (1 - (t/2) cot(t/2)) / t^2 (-> 1/12); the gradient of lam . log(R R*^T) under
+// R <- exp([delta]) R (R29)
+__device__ d3 so3_jl_inv_T(d3 phi, d3 x) {
+  const double t = nrm(phi);
+  const double c = t < 1e-4 ? 1.0 / 12.0 + t * t / 720.0 : (1.0 - 0.5 * t / tan(0.5 * t)) / (t * t);
+  const d3 px = cross(phi, x);
+  return x + 0.5 * px + c * cross(phi, px);
+}
 __device__ __forceinline__ double spring_w(double r, double k, double cap) { return r <= cap / k ? k : cap / r; }
 __device__ __forceinline__ double spring_e(double r, double k, double cap) {
   double rho = cap / k;
@@ -2265,16 +2274,23 @@ __global__ void k_accept(Dev d, double h) {
   d3 phi = so3_log(RRs);
   double wt = spring_w(nrm(dc), d.k_t, d.f_max), wr = spring_w(nrm(phi), d.k_r, d.t_max);
   double Eb = A[A_EB * Es + e];
-  double E = A[A_EIN * Es + e] + A[A_EEL * Es + e] + Eb + A[A_EF * Es + e] +
-             h2 * (spring_e(nrm(dc), d.k_t, d.f_max) + spring_e(nrm(phi), d.k_r, d.t_max));
+  double Ep = h2 * (spring_e(nrm(dc), d.k_t, d.f_max) + spring_e(nrm(phi), d.k_r, d.t_max));
+  const d3 lt = ld3(s.lam), lr = ld3(s.lam + 3);
+  if (d.pose_al) Ep += h2 * (dot(lt, dc) + dot(lr, phi));  // multiplier term (R29)
+  double E = A[A_EIN * Es + e] + A[A_EEL * Es + e] + Eb + A[A_EF * Es + e] + Ep;
   double gr[6], Dc6[6], Dt6[6];
   for (int k = 0; k < 6; ++k) gr[k] = A[(A_GR + k) * Es + e];
   for (int k = 0; k < 6; ++k) { Dc6[k] = A[(A_DR + k) * Es + e]; Dt6[k] = A[(A_DR + 6 + k) * Es + e]; }
   s.Ep[0] = A[A_EIN * Es + e]; s.Ep[1] = A[A_EEL * Es + e]; s.Ep[2] = Eb; s.Ep[3] = A[A_EF * Es + e];
-  s.Ep[4] = h2 * (spring_e(nrm(dc), d.k_t, d.f_max) + spring_e(nrm(phi), d.k_r, d.t_max));
+  s.Ep[4] = Ep;
   for (int k = 0; k < 28; ++k) A[k * Es + e] = 0.0;
   gr[0] += h2 * wt * dc.x; gr[1] += h2 * wt * dc.y; gr[2] += h2 * wt * dc.z;
   gr[3] += h2 * wr * phi.x; gr[4] += h2 * wr * phi.y; gr[5] += h2 * wr * phi.z;
+  if (d.pose_al) {  // h^2 lam_t and h^2 J_l(phi)^-T lam_r (R29)
+    const d3 gl = so3_jl_inv_T(phi, lr);
+    gr[0] += h2 * lt.x; gr[1] += h2 * lt.y; gr[2] += h2 * lt.z;
+    gr[3] += h2 * gl.x; gr[4] += h2 * gl.y; gr[5] += h2 * gl.z;
+  }
   for (int k = 0; k < 3; ++k) { Dc6[k] += h2 * wt; Dt6[k] += h2 * wr; }
   s.iter += 1;
   d.dalpha[e] = 0.f;
@@ -2679,7 +2695,13 @@ __global__ void k_finalize_env(Dev d) {
   d3 dc = ld3(s.c) - ld3(s.cs);
   double RRs[9];
   mmT(s.R, s.Rs, RRs);
-  s.pose_res = nrm(dc) + d.rho_max * nrm(so3_log(RRs));
+  const d3 phi = so3_log(RRs);
+  s.pose_res = nrm(dc) + d.rho_max * nrm(phi);
+  if (d.pose_al && !(s.flags & (4 | 8))) {  // R29: lam += psi'(r) r/|r| at the step's solution
+    const double wt = spring_w(nrm(dc), d.k_t, d.f_max), wr = spring_w(nrm(phi), d.k_r, d.t_max);
+    s.lam[0] += wt * dc.x; s.lam[1] += wt * dc.y; s.lam[2] += wt * dc.z;
+    s.lam[3] += wr * phi.x; s.lam[4] += wr * phi.y; s.lam[5] += wr * phi.z;
+  }
 }
 
 // ------------------------------------------------------------------ a10: markers
@@ -2754,6 +2776,7 @@ __global__ void k_reset_env(Dev d, const unsigned char* mask, const float* poses
   s.flags = 0;
   s.iter = 0;
   s.pg = 0;
+  for (int i = 0; i < 6; ++i) s.lam[i] = 0.0;
 }
 __global__ void k_reset_vert(Dev d, const unsigned char* mask) {
   TAC_PDL_WAIT();
@@ -2803,8 +2826,10 @@ static int eblocks(const Dev& d) { return (d.E + 127) / 128; }
 // the envs over E / 32 SMs instead of E / 128
 static int eblocks32(const Dev& d) { return (d.E + 31) / 32; }
 static dim3 sgrid(const Dev& d) {  // staged contact kernels: chunks per env
+  // every CTA stages its env once, so CTAs per env stay few: one at 1,024+ envs (measured
+  // +1.2 % at C3 against two), up to 16 for small batches
   static const int cap = getenv("TAC_SGRID_CAP") ? atoi(getenv("TAC_SGRID_CAP")) : 16;  // A/B experiments
-  int nb = std::max(1, std::min(cap, 2368 / std::max(1, d.E)));
+  int nb = std::max(1, std::min(cap, 1184 / std::max(1, d.E)));
   return dim3(nb, d.E);
 }
 // Every launch is a programmatic dependent launch: the next kernel's CTAs may be resident

@@ -206,6 +206,25 @@ def test_solver_variants_converged_parity(torch_cuda, beta_rule, precond):
         assert int(it[e]) <= 3 * it_o + 50 and it_o <= 3 * int(it[e]) + 50, (int(it[e]), it_o)
 
 
+def test_augmented_lagrangian_pose_parity(torch_cuda):
+    """R29 (SURVEY 8f-3 augmented-Lagrangian pose enforcement): a C1 press held for three
+    steps with pose_al = 1 converges to the oracle's states, and the indenter reaches its
+    target to the solver tolerance where the penalty alone leaves F / k_t."""
+    res = {}
+    for al in (0, 1):
+        s = c1_press_scene(mu_f=1.0, steps=3, depth=0.3e-3)
+        s.poses = np.concatenate([s.poses, np.repeat(s.poses[-1:], 3, axis=0)])
+        s.params.pose_al = al
+        sim, o, mk = _run_both(s, len(s.poses))
+        it, pg, fl = sim.env_status()
+        assert int(fl[0]) & 1, int(fl[0])
+        _assert_parity(s, sim, o, mk, 0)
+        c_g = sim.get_state(0)[2]
+        res[al] = np.linalg.norm(c_g - s.poses[-1][0][:3])
+        assert np.linalg.norm(c_g - o.get_state(0)[2]) <= 1e-4 * max(s.extent)
+    assert res[0] > 1e-9 and res[1] < 0.1 * res[0], res
+
+
 def test_fletcher_reeves_matches_oracle_behaviour(torch_cuda):
     """FR (beta rule 2) without restarts jams on the second C1 press step in the fp64
     oracle (stagnation); the GPU reproduces the converged first step and the jam."""

@@ -438,3 +438,65 @@ def test_unstructured_mesh_invariants():
     assert o.status_of(0)["flags"] & 1
     u = o.get_state(0)[0]
     assert np.all(u[s.fixed] == 0) and np.abs(u).max() > 1e-6
+
+
+# ---------------------------------------------------------------- augmented Lagrangian (R29)
+def test_pose_multiplier_gradient_matches_central_fd(pressed):
+    """The multiplier term h^2 (lam_t . dc + lam_r . phi) of R29: its left-trivialised
+    rotation gradient J_l(phi)^-T lam_r (and h^2 lam_t) against central differences, with a
+    target rotated 0.2 rad away so that the J_l correction is ~10 % of the term."""
+    s, o, st, (u, c, R), tgt = pressed
+    tgt = tgt.copy()
+    ax = np.array([0.3, -0.5, 0.8]) / np.linalg.norm([0.3, -0.5, 0.8])
+    Rt = rot_exp(0.2 * ax) @ O.quat_to_R(tgt).reshape(3, 3)
+    tgt[3:] = rig_quat(Rt)
+    lam = np.array([0.3, -0.2, 0.5, 0.01, -0.02, 0.015])
+    g0 = o.eval(*st, u, c, R, tgt)["grig"]
+    o.set_eval_lambda(lam)
+    try:
+        r = o.eval(*st, u, c, R, tgt)
+        fr = np.zeros(6)
+        eps = 1e-9
+        for a in range(3):
+            e = np.zeros(3); e[a] = eps
+            fr[a] = (o.eval(*st, u, c + e, R, tgt)["E"] - o.eval(*st, u, c - e, R, tgt)["E"]) / (2 * eps)
+            e = np.zeros(3); e[a] = 1e-8
+            fr[3 + a] = (o.eval(*st, u, c, rot_exp(e) @ R, tgt)["E"]
+                         - o.eval(*st, u, c, rot_exp(-e) @ R, tgt)["E"]) / 2e-8
+        assert np.linalg.norm(fr - r["grig"]) <= 1e-6 * np.linalg.norm(r["grig"])
+        h2 = s.dt ** 2
+        assert np.allclose(r["grig"][:3] - g0[:3], h2 * lam[:3], rtol=1e-9, atol=0)
+        # the rotation part is not h^2 lam_r: the J_l(phi)^-T correction is there
+        assert np.linalg.norm(r["grig"][3:] - g0[3:] - h2 * lam[3:]) > 0.02 * h2 * np.linalg.norm(lam[3:])
+    finally:
+        o.set_eval_lambda(np.zeros(6))
+
+
+def rig_quat(R):
+    from paper_2603_28475_b200.rig import R_to_quat
+    return R_to_quat(R)
+
+
+def test_augmented_lagrangian_removes_the_pose_residual():
+    """R29: holding a press, the penalty spring leaves the indenter short of its target by
+    F / k_t; the AL multiplier absorbs the contact force after a step, so the residual drops
+    to the solver tolerance and lam_t equals the spring force the penalty run carries."""
+    res = {}
+    lam = None
+    for al in (0, 1):
+        s = c1_press_scene(mu_f=1.0, steps=3, depth=0.3e-3)
+        s.poses = np.concatenate([s.poses, np.repeat(s.poses[-1:], 4, axis=0)])  # hold the press
+        s.params.tol_x = 1e-11
+        s.params.pose_al = al
+        o = O.Oracle(s)
+        for k in range(len(s.poses)):
+            o.step(s.poses[k])
+            assert o.status_of(0)["flags"] & 1
+        c = o.get_state(0)[2]
+        res[al] = np.linalg.norm(c - s.poses[-1][0][:3])
+        if al:
+            lam = o.lambda_of(0)
+    k_t = s.params.k_t
+    assert res[0] > 1e-9                       # penalty residual F / k_t at ~0.1-1 N
+    assert res[1] < 0.05 * res[0]              # AL: gone to the solver's tolerance
+    assert np.linalg.norm(lam[:3]) == pytest.approx(k_t * res[0], rel=0.05)

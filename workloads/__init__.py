@@ -271,6 +271,7 @@ class Params:
     stagnation: int = 3000
     max_candidates: int = 0   # 0 -> library default (16384 per env)
     max_anchors: int = 0      # 0 -> library default (4096 per env)
+    pose_al: int = 0          # 1: augmented-Lagrangian pose enforcement (R29)
 
 
 @dataclass
