@@ -1221,11 +1221,28 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
 #pragma unroll
       for (int c = 0; c < 6; ++c) aD[s][c] = 0.f;
     }
+    // coalesced red.add of corner s's 9 accumulated terms (skipped for a fixed corner)
+    auto flush = [&](int s) {
+      if (fix & (1u << s)) return;
+      float* pg = d.g + (vb[s] * 3u * 32u + lane);
+      float* pd = d.D + (vb[s] * 6u * 32u + lane);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) atomicAdd(pg + 32 * c, ag[s][c]);
+#pragma unroll
+      for (int c = 0; c < 6; ++c) atomicAdd(pd + 32 * c, aD[s][c]);
+    };
     if constexpr (ALL_AA) {  // packed tet pairs (0,1), (2,3), (4,5); every tet has volume caa.w
+      // each corner is flushed right after the last pair touching it (pair 0: corners 0 1 3 5 7,
+      // pair 1: 0 2 3 6 7, pair 2: 0 4 5 6 7), so at most 6 corners' accumulators are live
       const float w = h2 * caa.w, lc = w * l2;
       pair_grad_acc<0>(u, inv, mu, l2, w, lc, esum, ag, aD);
+      flush(1);
       pair_grad_acc<1>(u, inv, mu, l2, w, lc, esum, ag, aD);
+      flush(2);
+      flush(3);
       pair_grad_acc<2>(u, inv, mu, l2, w, lc, esum, ag, aD);
+#pragma unroll
+      for (int s : {0, 4, 5, 6, 7}) flush(s);
     } else {
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
@@ -1324,16 +1341,8 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
         aD[s0][3] += lc * c0[0] * c0[1]; aD[s0][4] += lc * c0[0] * c0[2]; aD[s0][5] += lc * c0[1] * c0[2];
       }
     }
-    }
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      if (fix & (1u << s)) continue;
-      float* pg = d.g + (vb[s] * 3u * 32u + lane);
-      float* pd = d.D + (vb[s] * 6u * 32u + lane);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) atomicAdd(pg + 32 * c, ag[s][c]);
-#pragma unroll
-      for (int c = 0; c < 6; ++c) atomicAdd(pd + 32 * c, aD[s][c]);
+    for (int s = 0; s < 8; ++s) flush(s);
     }
   }
   if (act) atomicAdd(d.acc + (size_t)A_EEL * d.Es + e, esum);
