@@ -63,6 +63,7 @@ struct tac_sim {
 };
 
 static thread_local std::string g_create_err;
+static int g_tl_iter = -1;  // TAC_TIMELINE: the iteration of each step whose timeline is printed
 
 namespace tac {
 // per-kernel CUDA-event timing of the launches issued by tac_step / tac_markers
@@ -101,6 +102,35 @@ struct Profiler {
     for (auto e : pool) cudaEventDestroy(e);
   }
 };
+thread_local bool g_tl_on = false;
+struct Timeline {
+  cudaEvent_t start = nullptr;
+  std::vector<std::pair<int, cudaEvent_t>> marks;
+  std::vector<cudaStream_t> streams;
+};
+static Timeline g_tl;
+void tl_mark(int kid, cudaStream_t s) {
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, s);
+  g_tl.marks.push_back({kid, e});
+  g_tl.streams.push_back(s);
+}
+static void tl_print() {  // end times (us from the iteration start) per launch and stream
+  cudaEventSynchronize(g_tl.marks.empty() ? g_tl.start : g_tl.marks.back().second);
+  cudaDeviceSynchronize();
+  std::vector<cudaStream_t> ids;
+  for (size_t i = 0; i < g_tl.marks.size(); ++i) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, g_tl.start, g_tl.marks[i].second);
+    int sid = (int)(std::find(ids.begin(), ids.end(), g_tl.streams[i]) - ids.begin());
+    if (sid == (int)ids.size()) ids.push_back(g_tl.streams[i]);
+    fprintf(stderr, "timeline stream %d %-22s end %8.1f us\n", sid, kernel_name(g_tl.marks[i].first), ms * 1e3);
+    cudaEventDestroy(g_tl.marks[i].second);
+  }
+  cudaEventDestroy(g_tl.start);
+  g_tl = Timeline{};
+}
 void prof_begin(int kid, cudaStream_t s) {
   cudaEvent_t e = g_prof->get();
   cudaEventRecord(e, s);
@@ -724,6 +754,10 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
   sim->fixed_iters = P.fixed_iters;
   sim->check_every = P.check_every > 0 ? P.check_every : 25;
   if (getenv("TAC_NO_GRAPH")) sim->use_graphs = false;
+  if (getenv("TAC_TIMELINE") && P.fixed_iters > 0) {  // measurement only: direct launches
+    sim->use_graphs = false;
+    g_tl_iter = P.fixed_iters / 2;
+  }
   // device upload
   std::vector<float4> Xf(nv), Yf(niv);
   for (int i = 0; i < nv; ++i) Xf[i] = make_float4((float)X[i][0], (float)X[i][1], (float)X[i][2], 0.f);
@@ -994,10 +1028,20 @@ static tac_status post_launch(tac_sim* sim) {
 
 static void launch_iterations(const Dev& d, double h, int n, cudaStream_t s) {
   for (int it = 0; it < n; ++it) {
+    const bool tl = it == g_tl_iter;
+    if (tl) {
+      cudaEventCreate(&g_tl.start);
+      cudaEventRecord(g_tl.start, s);
+      g_tl_on = true;
+    }
     launch_eval(d, h, s);       // a4 + a5 + Armijo (a8)
     launch_direction(d, s);     // a6
     launch_curvature(d, h, s);  // a7
     launch_alpha(d, h, s);      // a7/a8 (+ a2 rebuild)
+    if (tl) {
+      g_tl_on = false;
+      tl_print();
+    }
   }
 }
 

@@ -47,6 +47,7 @@ struct EnvS {
   double gr[6], grp[6], pr[6];  // rigid gradient, previous gradient, direction (c, theta)
   double Dc[9], Dth[9];       // rigid diagonal blocks of the last accepted evaluation
   double E, Eprev, alpha, gp_prev, gPg_prev, S, beta, best_pg, pg, pose_res;
+  double wt_acc, wr_acc;       // pose-spring weights psi'(r)/r at the last accepted point (k_alpha's curvature)
   double lam[6];               // pose multipliers (lam_t [N], lam_r [N m]) of the AL pose term (R29)
   double Lrel_last;
   double odo, odo_base, Lc;   // classification odometer (R15 cache): path-length coordinate of the
@@ -200,5 +201,9 @@ extern thread_local Profiler* g_prof;
 void prof_begin(int kid, cudaStream_t s);
 void prof_end(int kid, cudaStream_t s);
 const char* kernel_name(int kid);
+// optional per-stream timeline of one iteration (TAC_TIMELINE=1; measurement only): an event
+// recorded on the launching stream after every launch, streams kept concurrent
+extern thread_local bool g_tl_on;
+void tl_mark(int kid, cudaStream_t s);
 
 }  // namespace tac

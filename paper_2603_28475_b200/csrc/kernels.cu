@@ -2315,6 +2315,8 @@ __global__ void k_accept(Dev d, double h) {
   if (ok) {
     s.odo_base = s.odo;
     s.E = E;
+    s.wt_acc = wt;
+    s.wr_acc = wr;
     for (int k = 0; k < 6; ++k) s.gr[k] = gr[k];
     sym6_to_9(Dc6, s.Dc);
     sym6_to_9(Dt6, s.Dth);
@@ -2369,7 +2371,7 @@ __device__ __forceinline__ void precond(const float* D, int scalar, const float*
 __global__ void __launch_bounds__(256) k_dir_reduce(Dev d) {
   TAC_PDL_WAIT();
   int e = blockIdx.x * 32 + threadIdx.x;
-  bool act = e < d.E && (d.run[e] & 2);
+  bool act = e < d.E && (d.run[e] & 3);  // speculative: k_accept may run concurrently (see launch_eval)
   if (!__any_sync(0xffffffffu, act)) return;
   double gPy = 0, yp = 0, yPy = 0, pg = 0, gPg = 0, gg = 0, pp = 0;
   float pgmax = 0.f;
@@ -2453,9 +2455,14 @@ __device__ void rigid_P(const EnvS& s, int scalar, const double* x, double* y) {
 __global__ void k_dir_scalar(Dev d) {
   TAC_PDL_WAIT();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= d.E || !(d.run[e] & 2)) return;
-  EnvS& s = d.es[e];
+  if (e >= d.E) return;
   size_t Es = d.Es;
+  if (!(d.run[e] & 2)) {  // not accepted: drop the speculative sums of k_dir_reduce
+    for (int k = 0; k < 7; ++k) d.acc[(A_DOT + k) * Es + e] = 0.0;
+    d.accu[U_PGMAX * Es + e] = 0u;
+    return;
+  }
+  EnvS& s = d.es[e];
   double dt[7];
   for (int k = 0; k < 7; ++k) { dt[k] = d.acc[(A_DOT + k) * Es + e]; d.acc[(A_DOT + k) * Es + e] = 0.0; }
   float pgmax = __uint_as_float(d.accu[U_PGMAX * Es + e]);
@@ -2623,12 +2630,8 @@ __global__ void k_alpha(Dev d, double h) {
   double Lg = __uint_as_float(d.accu[U_LREL * Es + e]);
   double M = fmax(Mg, nrm(pc) + d.rho_max * nrm(pth));
   double L = fmax(Lg, nrm(pc)) + d.rho_max * nrm(pth);
-  d3 dc = ld3(s.c) - ld3(s.cs);
-  double RRs[9];
-  mmT(s.R, s.Rs, RRs);
-  d3 phi = so3_log(RRs);
-  double q = d.acc[A_PHP * Es + e] + h2 * (spring_w(nrm(dc), d.k_t, d.f_max) * dot(pc, pc) +
-                                           spring_w(nrm(phi), d.k_r, d.t_max) * dot(pth, pth));
+  // the pose spring's Gauss-Newton curvature at x_k, with its weights from k_accept
+  double q = d.acc[A_PHP * Es + e] + h2 * (s.wt_acc * dot(pc, pc) + s.wr_acc * dot(pth, pth));
   d.acc[A_PHP * Es + e] = 0.0;
   d.accu[U_M * Es + e] = 0u;
   d.accu[U_LREL * Es + e] = 0u;
@@ -2864,6 +2867,7 @@ static void pdl_launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
     if (g_prof) prof_begin(kid, s);                      \
     pdl_launch(kern, dim3(grid), dim3(block), (size_t)(smem), s, ##__VA_ARGS__); \
     if (g_prof) prof_end(kid, s);                        \
+    if (g_tl_on) tl_mark(kid, s);                        \
     ++g_launches;                                        \
   } while (0)
 
@@ -2941,11 +2945,20 @@ void launch_eval(const Dev& d, double h, cudaStream_t s) {
   if (fork) {
     cudaStreamWaitEvent(s, d.ev_join, 0);
     cudaStreamWaitEvent(s, d.ev_join2, 0);
+    // the Armijo decision (one thread per env, a latency-bound fp64 chain) runs on the side
+    // stream beside the direction reduction, which sums its dots speculatively for every env
+    // under evaluation; k_dir_scalar (after both) keeps the accepted envs' sums only
+    cudaEventRecord(d.ev_cls, s);
+    cudaStreamWaitEvent(cs, d.ev_cls, 0);
+    LAUNCHP(KID_ACCEPT, cs, k_accept, eblocks32(d), 32, 0, d, h);
+    cudaEventRecord(d.ev_join, cs);
+  } else {
+    LAUNCHP(KID_ACCEPT, s, k_accept, eblocks32(d), 32, 0, d, h);
   }
-  LAUNCHP(KID_ACCEPT, s, k_accept, eblocks32(d), 32, 0, d, h);
 }
 void launch_direction(const Dev& d, cudaStream_t s) {
   LAUNCHP(KID_DIR_REDUCE, s, k_dir_reduce, vgrid(d, d.nv), dim3(32, 8), 0, d);
+  if (g_prof == nullptr) cudaStreamWaitEvent(s, d.ev_join, 0);  // k_accept on the side stream
   LAUNCHP(KID_DIR_SCALAR, s, k_dir_scalar, eblocks32(d), 32, 0, d);
   LAUNCHP(KID_DIR_APPLY, s, k_dir_apply, vgrid(d, d.nv), dim3(32, 8), 0, d);
 }
