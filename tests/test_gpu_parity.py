@@ -373,6 +373,18 @@ def test_full_size_c3_converged_sampled(torch_cuda):
         assert np.abs(mk[e] - m_o).max() <= 1e-3 * np.abs(m_o).max()
 
 
+def test_c2_sphere_press_converged_parity(torch_cuda):
+    """BASELINE configs[1] (C2: GelSight-Mini-like 19,800-tet pad, R = 5 mm icosphere): the first
+    four steps of its press (to 0.3 mm) converge to the oracle's states on the north_star gates."""
+    s = w.scene_c2(steps=4)
+    sim, o, mk = _run_both(s, 4)
+    it, pg, fl = sim.env_status()
+    assert int(fl[0]) & 1, int(fl[0])
+    assert o.status_of(0)["flags"] & 1
+    _assert_parity(s, sim, o, mk, 0)
+    assert np.abs(o.markers(0)).max() > 1e-6  # the press reaches the markers
+
+
 # ---------------------------------------------------------------- §8f-1 unstructured mesh, C5 stress
 def _small_unstructured(n_envs=3, n_steps=3):
     s = w.scene_small_peg(n_envs=n_envs, n_steps=n_steps)
