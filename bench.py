@@ -39,7 +39,22 @@ WORKLOADS = {
           "8 mm diameter cylinder peg, 7x9 markers",
     "c3u": "C3 on the unstructured pad (jittered interior, random vertex/tet numbering; SURVEY 8f-1)",
     "c5": "C5 stress: 103,680-tet / 19,943-vertex pad, sharp 8x8 mm square peg (face / edge press, slide, twist)",
+    "c2": "C2: 1 env, GelSight-Mini-like 19,800-tet pad, R 5 mm icosphere: normal press + shear slide + retract, "
+          "50 steps (latency-bound; ms_per_step is the step latency)",
 }
+
+
+def make_scene(config, n_envs, n_steps, seed0):
+    """The workload of `config` (workloads/ generators; env ids from seed0)."""
+    import workloads as w
+    if config == "c5":
+        return w.scene_c5(n_envs=n_envs, n_steps=n_steps, seed0=20270000 + seed0)
+    if config == "c3u":
+        return w.scene_c3_unstructured(n_envs=n_envs, n_steps=n_steps, seed0=20260000 + seed0)
+    if config == "c2":
+        assert n_envs == 1, "C2 is a single-env config"
+        return w.scene_c2(steps=n_steps)
+    return w.scene_c3(n_envs=n_envs, n_steps=n_steps, seed0=20260000 + seed0)
 
 
 def _peaks():
@@ -125,12 +140,7 @@ def run_ours(args, rank, local, ws):
     else:  # weak: a fixed env count per GPU, distinct env ids per rank
         e0, e1 = rank * args.envs, (rank + 1) * args.envs
     E = e1 - e0
-    if args.config == "c5":
-        scene = w.scene_c5(n_envs=E, n_steps=nsteps, seed0=20270000 + e0)
-    elif args.config == "c3u":
-        scene = w.scene_c3_unstructured(n_envs=E, n_steps=nsteps, seed0=20260000 + e0)
-    else:
-        scene = w.scene_c3(n_envs=E, n_steps=nsteps, seed0=20260000 + e0)
+    scene = make_scene(args.config, E, nsteps, e0)
     if args.tol is not None:  # tolerance mode (SURVEY §8d.1 timing protocol iii)
         scene.params.fixed_iters = 0
         scene.params.tol_x = args.tol
@@ -319,15 +329,15 @@ def run_ours(args, rank, local, ws):
     return out, scene, sim
 
 
-def cpu_baseline(scene_envs=None, budget_s=12.0):
-    """The oracle (fp64, one env per thread on all host cores), fixed 50 iterations, on a
-    bounded sample of the C3 workload: 2 x nproc envs, steps until ~budget_s of CPU time."""
+def cpu_baseline(config="c3", iters=FIXED_ITERS, budget_s=12.0):
+    """The oracle (fp64, one env per thread on all host cores), the same fixed iteration count,
+    on a bounded sample of the bench's workload: 2 x nproc envs (1 for C2), steps until
+    ~budget_s of CPU time."""
     import oracle as O
-    import workloads as w
     nproc = os.cpu_count() or 1
-    n = 2 * nproc
-    s = w.scene_c3(n_envs=n, n_steps=64)
-    s.params.fixed_iters = FIXED_ITERS
+    n = 1 if config == "c2" else 2 * nproc
+    s = make_scene(config, n, 64, 0)
+    s.params.fixed_iters = iters
     o = O.Oracle(s)
     t0 = time.perf_counter()
     steps = 0
@@ -337,9 +347,9 @@ def cpu_baseline(scene_envs=None, budget_s=12.0):
         if time.perf_counter() - t0 > budget_s:
             break
     dt = time.perf_counter() - t0
-    return {"value": round(n * steps / dt, 3), "unit": "env-steps/s", "cores": nproc, "kind": "oracle",
-            "sample": f"C3 workload, {n} envs x {steps} steps (first steps of each trajectory), "
-                      f"{FIXED_ITERS} iterations/step, fp64 C++ oracle, one env per thread"}
+    return {"value": round(n * steps / dt, 3), "unit": "env-steps/s", "cores": min(nproc, n), "kind": "oracle",
+            "sample": f"{config.upper()} workload, {n} envs x {steps} steps (first steps of each trajectory), "
+                      f"{iters} iterations/step, fp64 C++ oracle, one env per thread"}
 
 
 def run_reference(args, rank, ws):
@@ -378,7 +388,7 @@ def main():
     ap.add_argument("--envs", type=int, default=None, help="envs per GPU (default 1024; 256 for c5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
-    ap.add_argument("--config", default="c3", choices=["c3", "c3u", "c5"])
+    ap.add_argument("--config", default="c3", choices=["c3", "c3u", "c5", "c2"])
     ap.add_argument("--iters", type=int, default=FIXED_ITERS, help="fixed PNCG iterations per step (headline 50)")
     ap.add_argument("--tol", type=float, default=None, help="tolerance mode: tol_x [m] (SURVEY §8d.1: 1e-7)")
     ap.add_argument("--max-iters", type=int, default=2000, help="tolerance mode iteration cap")
@@ -386,7 +396,7 @@ def main():
     args = ap.parse_args()
     assert args.warmup >= 1 and args.iters >= 1
     if args.envs is None:
-        args.envs = 256 if args.config == "c5" else ENVS_PER_GPU
+        args.envs = {"c5": 256, "c2": 1}.get(args.config, ENVS_PER_GPU)
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
         ws = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
@@ -398,7 +408,7 @@ def main():
     out, scene, sim = run_ours(args, rank, local, ws)
     if rank == 0:
         if ws == 1 and not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline()
+            out["cpu_baseline"] = cpu_baseline(args.config, args.iters)
         else:
             out["cpu_baseline"] = None
         print(json.dumps(out), flush=True)
