@@ -111,11 +111,15 @@ typedef struct {
  *   pose_al         1: augmented-Lagrangian pose enforcement (R29): the pose
  *                   term gains h^2 (lam_t . (c - c*) + lam_r . log(R R*^T)) with per-env multipliers,
  *                   updated after every step by the spring force, lam += psi'(r) r/|r| (reset by
- *                   tac_reset); 0: plain penalty (default).  Outside {0, 1} -> TAC_EINVAL */
+ *                   tac_reset); 0: plain penalty (default).  Outside {0, 1} -> TAC_EINVAL
+ *   ee_mollifier    1: IPC's edge-edge mollifier (R30): an edge-edge pair's
+ *                   barrier becomes m(c) kappa b(d), c = |e_a x e_b|^2, m = -c^2/eps^2 + 2c/eps below
+ *                   eps = 1e-3 |E_a|^2 |E_b|^2 (rest lengths), 1 above; its friction lambda too.
+ *                   0: off (default).  Outside {0, 1} -> TAC_EINVAL */
 typedef struct {
   double dhat, kappa_phys, eps_v, tol_x, k_t, k_r, f_max, t_max, ccd_s, bp_margin, c1, eps_E;
   int32_t max_iters, fixed_iters, beta_rule, precond, max_halvings, stagnation;
-  int32_t max_candidates, max_anchors, check_every, pose_al;
+  int32_t max_candidates, max_anchors, check_every, pose_al, ee_mollifier;
 } tac_solver_params;
 
 typedef struct {

@@ -155,6 +155,26 @@ V3 so3_jl_inv_T(const V3& phi, const V3& x) {
   return add(add(x, scl(0.5, px)), scl(c, cross(phi, px)));
 }
 
+// ---- edge-edge mollifier (R30; IPC's parallel-edge treatment) ----
+// c = |e_a x e_b|^2, eps_x = 1e-3 |E_a|^2 |E_b|^2 (rest edges); m(c) = -c^2/eps^2 + 2c/eps for
+// c < eps, else 1 (C^1 at eps); the EE barrier becomes m(c) kappa b(d)
+struct Moll {
+  double m = 1, dm = 0;  // m(c), m'(c)
+  V3 dc[4] = {};         // dc/dz_k for the corners (a0, a1, b0, b1)
+};
+Moll ee_mollifier(const V3 z[4], double La2, double Lb2) {
+  Moll M;
+  V3 ea = sub(z[1], z[0]), eb = sub(z[3], z[2]);
+  V3 w = cross(ea, eb);
+  double c = dot(w, w), eps = 1e-3 * La2 * Lb2;
+  V3 ga = scl(2.0, cross(eb, w)), gb = scl(2.0, cross(w, ea));  // dc/de_a, dc/de_b
+  M.dc[0] = scl(-1.0, ga); M.dc[1] = ga; M.dc[2] = scl(-1.0, gb); M.dc[3] = gb;
+  if (c < eps) {
+    M.m = (2.0 - c / eps) * c / eps;
+    M.dm = (2.0 - 2.0 * c / eps) / eps;
+  }
+  return M;
+}
 // ---- force-capped pose spring (R18) ----
 double huber(double r, double k, double cap) {
   double rho = cap / k;
@@ -303,6 +323,7 @@ struct Problem {
   double dhat, kappa_phys, eps_v, tol_x, k_t, k_r, ccd_s, bp_margin, c1, f_max, t_max;
   int max_iters, fixed_iters, beta_rule, precond, max_halvings, stagnation, debug;
   int pose_al;  // augmented-Lagrangian pose enforcement (R29)
+  int ee_moll;  // edge-edge parallel mollifier (R30)
 };
 
 struct Env {
@@ -472,6 +493,13 @@ V3 gel_pos(const Problem& P, const State& s, int v) { return add(P.X[v], s.u[v])
 V3 ind_pos(const Problem& P, const State& s, int j) { return add(matvec(s.R, P.Y[j]), s.c); }
 
 // corners of a pair: (is_indenter, vertex id) x 4 (PT uses 4 corners, EE 4 corners)
+// rest squared lengths of an EE pair's gel edge (corners 0, 1) and indenter edge (2, 3)
+void ee_rest(const Problem& P, const int ci[4], double* La2, double* Lb2) {
+  V3 a = sub(P.X[ci[1]], P.X[ci[0]]), b = sub(P.Y[ci[3]], P.Y[ci[2]]);
+  *La2 = dot(a, a);
+  *Lb2 = dot(b, b);
+}
+
 void pair_corners(const Problem& P, const Pair& pr, int ci[4], bool ind[4]) {
   if (pr.kind == PT_GI) {
     ci[0] = P.sv[pr.a]; ind[0] = false;
@@ -676,21 +704,29 @@ double eval_energy(const Problem& P, const Step& S, const State& s, const std::v
     Dist D = pair_dist(P, s, pr);
     if (!(D.d > 0)) return std::numeric_limits<double>::quiet_NaN();  // infeasible
     if (D.d >= P.dhat) continue;
-    Eb += S.kappa * barrier_b(D.d, P.dhat);
-    if (!G) continue;
     int ci[4];
     bool ind[4];
     pair_corners(P, pr, ci, ind);
     V3 z[4];
     for (int k = 0; k < 4; ++k) z[k] = corner_pos(P, s, ci[k], ind[k]);
+    Moll M;  // m = 1 unless the EE mollifier is on (R30)
+    if (P.ee_moll && pr.kind == EE) {
+      double La2, Lb2;
+      ee_rest(P, ci, &La2, &Lb2);
+      M = ee_mollifier(z, La2, Lb2);
+    }
+    const double bk = S.kappa * barrier_b(D.d, P.dhat);
+    Eb += M.m * bk;
+    if (!G) continue;
     V3 r{0, 0, 0};
     for (int k = 0; k < 4; ++k) r = add(r, scl(D.w[k], z[k]));
     V3 n = scl(1.0 / D.d, r);  // dd/dz_k = w_k n
-    double db = S.kappa * barrier_db(D.d, P.dhat), ddb = S.kappa * barrier_ddb(D.d, P.dhat);
+    double db = M.m * S.kappa * barrier_db(D.d, P.dhat), ddb = M.m * S.kappa * barrier_ddb(D.d, P.dhat);
     double sig = 0;  // sum of indenter weights
     V3 rho{0, 0, 0};
     for (int k = 0; k < 4; ++k) {
-      add_corner_force(P, s, G, ci[k], ind[k], scl(db * D.w[k], n));
+      // d(m kappa b)/dz_k = m kappa b' w_k n + kappa b m' dc/dz_k (GN blocks keep m kappa b'' only)
+      add_corner_force(P, s, G, ci[k], ind[k], add(scl(db * D.w[k], n), scl(bk * M.dm, M.dc[k])));
       if (!ind[k]) {
         if (P.fixed[ci[k]]) continue;
         for (int i = 0; i < 3; ++i)
@@ -806,7 +842,15 @@ double curvature(const Problem& P, const Step& S, const State& s, const std::vec
       dr = add(dr, scl(D.w[k], dz(ci[k], ind[k])));
     }
     double dn = dot(r, dr) / D.d;
-    q += S.kappa * barrier_ddb(D.d, P.dhat) * dn * dn;
+    double m = 1;
+    if (P.ee_moll && pr.kind == EE) {  // R30: the GN curvature scales with m
+      V3 z[4];
+      for (int k = 0; k < 4; ++k) z[k] = corner_pos(P, s, ci[k], ind[k]);
+      double La2, Lb2;
+      ee_rest(P, ci, &La2, &Lb2);
+      m = ee_mollifier(z, La2, Lb2).m;
+    }
+    q += m * S.kappa * barrier_ddb(D.d, P.dhat) * dn * dn;
   }
   for (const Anchor& A : S.anchors) {
     int ci[4];
@@ -1029,7 +1073,13 @@ void build_anchors(const Problem& P, Step& S, const State& s, const std::vector<
     V3 t1 = cross(n, e);
     A.t1 = scl(1.0 / norm(t1), t1);
     A.t2 = cross(n, A.t1);
-    A.lam = std::max(0.0, -S.kappa * barrier_db(D.d, P.dhat));  // lambda_k = -kappa b'(d_k)
+    double m = 1;
+    if (P.ee_moll && pr.kind == EE) {  // R30: lambda_k of the mollified barrier
+      double La2, Lb2;
+      ee_rest(P, ci, &La2, &Lb2);
+      m = ee_mollifier(A.z0, La2, Lb2).m;
+    }
+    A.lam = std::max(0.0, -m * S.kappa * barrier_db(D.d, P.dhat));  // lambda_k = -kappa b'(d_k)
     S.anchors.push_back(A);
   }
 }
@@ -1201,7 +1251,7 @@ extern "C" {
 
 // dparams: dhat, kappa_phys, eps_v, tol_x, k_t, k_r, ccd_s, bp_margin, c1, f_max, t_max
 // iparams: max_iters, fixed_iters, beta_rule, precond, max_halvings, stagnation, marker_mode, knn_k, debug,
-//          pose_al
+//          pose_al, ee_mollifier
 void* or_create(int nv, const double* X, int nt, const int* tets, int nfixed, const int* fixed, int niv,
                 const double* Y, int nit, const int* itris, int nm, const double* mk, const double* frame9,
                 const double* mat4, const double* dparams, const int* iparams, int n_envs, const double* init7,
@@ -1242,6 +1292,7 @@ void* or_create(int nv, const double* X, int nt, const int* tets, int nfixed, co
   P.max_halvings = iparams[4]; P.stagnation = iparams[5];
   P.debug = iparams[8];
   P.pose_al = iparams[9];
+  P.ee_moll = iparams[10];
   if (*status) return O;
   precompute(P);
   for (int e = 0; e < nt; ++e) if (!(P.vol[e] > 0)) *status = 2;

@@ -142,6 +142,7 @@ struct Dev {
   double rho_max, dhat, kappa_phys, eps_v, tol_x, k_t, k_r, f_max, t_max, ccd_s, bp_margin, c1, eps_E, mu_f;
   int beta_rule, precond, max_halv, stagnation, fixed_iters;
   int pose_al;           // augmented-Lagrangian pose enforcement (R29)
+  int ee_moll;           // edge-edge parallel mollifier (R30)
   // element tiles
   int ntiles;
   const int* tile_vstart;        // [ntiles + 1] into tile_verts

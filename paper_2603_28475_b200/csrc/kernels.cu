@@ -340,6 +340,30 @@ __device__ float dist2_ee_f(f3 a0, f3 a1, f3 b0, f3 b1) {
   const float ia = 1.f / a, ie = 1.f / e;
   return fminf(fminf(seg_d2f(a0, b0, d2, ie), seg_d2f(a1, b0, d2, ie)), fminf(seg_d2f(b0, a0, d1, ia), seg_d2f(b1, a0, d1, ia)));
 }
+// edge-edge mollifier (R30): c = |e_a x e_b|^2 over the corners (a0, a1, b0, b1), eps = 1e-3 La2 Lb2
+// (rest squared lengths); m = -c^2/eps^2 + 2c/eps below eps, else 1; dc[k] = dc/dz_k
+struct MollD {
+  double m, dm;
+  d3 dc[4];
+};
+__device__ MollD ee_moll(const d3* z, double La2, double Lb2) {
+  MollD M;
+  const d3 ea = z[1] - z[0], eb = z[3] - z[2], w = cross(ea, eb);
+  const double c = dot(w, w), eps = 1e-3 * La2 * Lb2;
+  const d3 ga = 2.0 * cross(eb, w), gb = 2.0 * cross(w, ea);
+  M.dc[0] = -1.0 * ga; M.dc[1] = ga; M.dc[2] = -1.0 * gb; M.dc[3] = gb;
+  M.m = 1.0;
+  M.dm = 0.0;
+  if (c < eps) {
+    M.m = (2.0 - c / eps) * c / eps;
+    M.dm = (2.0 - 2.0 * c / eps) / eps;
+  }
+  return M;
+}
+__device__ __forceinline__ double sqlen4(float4 a, float4 b) {
+  const double x = (double)a.x - (double)b.x, y = (double)a.y - (double)b.y, z = (double)a.z - (double)b.z;
+  return x * x + y * y + z * z;
+}
 // corners of a candidate / anchor: ids and sides (gel or indenter)
 struct Corners {
   int id[4];
@@ -823,7 +847,11 @@ __global__ void k_anchors(Dev d, double h2) {
     for (int k = 0; k < 3; ++k) { A.gid[k] = -1; A.w[k] = 0.f; }
     A.t1[0] = t1.x; A.t1[1] = t1.y; A.t1[2] = t1.z;
     A.t2[0] = t2.x; A.t2[1] = t2.y; A.t2[2] = t2.z;
-    A.lam = (float)fmax(0.0, -kappa * bar_db(D.d, d.dhat));
+    double mol = 1.0;
+    if (kind == 2 && d.ee_moll)  // R30: lambda of the mollified edge-edge barrier
+      mol = ee_moll(z, sqlen4(__ldg(d.X + C.id[1]), __ldg(d.X + C.id[0])),
+                    sqlen4(__ldg(d.Y + C.id[3]), __ldg(d.Y + C.id[2]))).m;
+    A.lam = (float)fmax(0.0, -mol * kappa * bar_db(D.d, d.dhat));
     A.pad2 = 0; A.pad3 = 0;
     // fold the rigid side: Y_w = sum_ind w Y, sig = sum_ind w; C0 = sum_gel w u^t + R^t Y_w + sig c^t.
     // Fixed gel corners are dropped: u = 0 there, so they add nothing to Delta and take no force
@@ -1576,7 +1604,7 @@ __device__ __forceinline__ void scatter_gel_free(const Dev& d, int v, int e, d3 
 }
 
 
-template <int KIND>
+template <int KIND, bool MOLL = false>  // MOLL: edge-edge mollifier (R30), KIND 2 only
 __global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
   TAC_PDL_WAIT();
   int e = blockIdx.y;
@@ -1643,17 +1671,26 @@ __global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) rr = rr + D.w[k] * z[k];
     d3 nn = (1.0 / D.d) * rr;
+    MollD Mo;
+    Mo.m = 1.0;
+    Mo.dm = 0.0;
+    if (MOLL)  // R30 (gel corners 0, 1 surface-local; indenter corners 2, 3)
+      Mo = ee_moll(z, sqlen4(__ldg(d.Xs + id[1]), __ldg(d.Xs + id[0])), sqlen4(__ldg(d.Y + id[3]), __ldg(d.Y + id[2])));
     geo[0] = make_float4((float)D.d, (float)nn.x, (float)nn.y, (float)nn.z);
-    geo[1] = make_float4((float)D.w[0], (float)D.w[1], (float)D.w[2], (float)D.w[3]);
+    const double sm = MOLL ? sqrt(Mo.m) : 1.0;  // curvature weights carry sqrt(m): m kappa b'' (n . dr)^2
+    geo[1] = make_float4((float)(sm * D.w[0]), (float)(sm * D.w[1]), (float)(sm * D.w[2]), (float)(sm * D.w[3]));
     double lg = log(D.d / d.dhat), dm = D.d - d.dhat, inv = 1.0 / D.d;
-    Eb += kappa * (-dm * dm * lg);                                       // b
-    double db = kappa * (-2 * dm * lg - dm * dm * inv);                  // b'
-    double ddb = kappa * (-2 * lg - 4 * dm * inv + dm * dm * inv * inv); // b''
+    const double bk = kappa * (-dm * dm * lg);                           // kappa b
+    Eb += Mo.m * bk;
+    double db = Mo.m * kappa * (-2 * dm * lg - dm * dm * inv);                  // m kappa b'
+    double ddb = Mo.m * kappa * (-2 * lg - 4 * dm * inv + dm * dm * inv * inv); // m kappa b'' (GN)
+    const double bdm = bk * Mo.dm;                                       // kappa b m' (R30)
     double sig = 0;
     d3 rho = mk(0, 0, 0);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       d3 f = (db * D.w[k]) * nn;
+      if (MOLL) f = f + bdm * Mo.dc[k];
       if (!ind[k]) {
         const int v = __ldg(d.svfree + id[k]);  // one load: id and fixed flag
         if (v >= 0) scatter_gel_free(d, v, e, f, ddb * D.w[k] * D.w[k], nn);
@@ -2924,7 +2961,8 @@ void launch_eval(const Dev& d, double h, cudaStream_t s) {
     cudaEventRecord(d.ev_cls, cs);
     cudaStreamWaitEvent(cs2, d.ev_cls, 0);
   }
-  LAUNCHP(KID_CONTACT_NEAR_EE, cs, k_contact_near<2>, cgrid(d), 128, 0, d, kap);
+  if (d.ee_moll) LAUNCHP(KID_CONTACT_NEAR_EE, cs, (k_contact_near<2, true>), cgrid(d), 128, 0, d, kap);
+  else LAUNCHP(KID_CONTACT_NEAR_EE, cs, k_contact_near<2>, cgrid(d), 128, 0, d, kap);
   LAUNCHP(KID_CONTACT_GRAD, cs2, k_contact_near<0>, cgrid(d), 128, 0, d, kap);
   LAUNCHP(KID_CONTACT_NEAR_IG, cs2, k_contact_near<1>, cgrid(d), 128, 0, d, kap);
   if (fork) {

@@ -31,3 +31,16 @@ def c1_press_scene(mu_f=1.0, steps=4, depth=0.2e-3, start_gap=0.05e-3, mirror=Fa
     z = np.linspace(R + start_gap, R - depth, steps + 1)[1:]
     s.poses = np.stack([np.stack([w.pose((0, 0, zz), q)]) for zz in z])
     return s
+
+
+def parallel_peg_scene(steps=2, depth=0.05e-3, start_gap=0.05e-3, offset_y=0.0):
+    """C1 pad and the small peg lying along the pad's x axis (yaw 0), its bottom axial edge
+    parallel to the pad's x edges: pressed to `depth` in `steps` steps.  Edge-edge pairs of
+    nearly parallel edges carry contact (the EE mollifier's case, R30)."""
+    s = w.scene_small_peg(n_envs=1, n_steps=steps)
+    r = 4e-3  # make_cylinder(4 mm, 14 mm, 24, 8): a vertex line at the bottom
+    q = [1.0, 0, 0, 0]
+    s.init_poses = np.stack([w.pose((0, offset_y, r + start_gap), q)])
+    z = np.linspace(r + start_gap, r - depth, steps + 1)[1:]
+    s.poses = np.stack([np.stack([w.pose((0, offset_y, zz), q)]) for zz in z])
+    return s

@@ -225,6 +225,44 @@ def test_augmented_lagrangian_pose_parity(torch_cuda):
     assert res[0] > 1e-9 and res[1] < 0.1 * res[0], res
 
 
+def test_ee_mollifier_kernel_and_converged_parity(torch_cuda):
+    """R30 (SURVEY 8f-3 edge-edge mollifier): a peg lying along the pad's x edges (nearly
+    parallel edge-edge contacts).  Kernel level: the GPU's gradient, blocks and energy parts at a
+    perturbed contact state match the oracle's with the mollifier on (<= 1e-5); converged
+    steps match the oracle's states."""
+    from helpers import parallel_peg_scene
+    s = parallel_peg_scene(steps=2, depth=0.05e-3)
+    s.params.ee_mollifier = 1
+    s.params.tol_x = 1e-10
+    o = O.Oracle(s)
+    o.step(s.poses[0])
+    u_t, v_t, c_t, R_t = o.get_state(0)
+    o.step(s.poses[1])
+    u, _, c, R = o.get_state(0)
+    rng = np.random.default_rng(11)
+    u = u + 2e-7 * rng.standard_normal(u.shape)
+    u[s.fixed] = 0
+    tgt = s.poses[1][0]
+    sim = _sim(s)
+    ut32 = u_t.astype(np.float32).astype(np.float64)
+    vt32 = v_t.astype(np.float32).astype(np.float64)
+    u32 = u.astype(np.float32).astype(np.float64)
+    ref = o.eval(ut32, vt32, c_t, R_t, u32, c, R, tgt)
+    gpu = sim.debug_eval(0, ut32, vt32, c_t, R_t, u32, c, R, tgt, s.dt)
+    free = np.setdiff1d(np.arange(len(u)), s.fixed)
+    g_ref, g_gpu = ref["g"][free], gpu["g"][free]
+    assert np.linalg.norm(g_gpu - g_ref) <= 1e-5 * np.linalg.norm(g_ref)
+    assert np.linalg.norm(gpu["grig"] - ref["grig"]) <= 1e-5 * np.linalg.norm(ref["grig"])
+    for k in range(5):
+        assert abs(gpu["parts"][k] - ref["parts"][k]) <= 1e-5 * abs(ref["E"]) + 1e-30, k
+    s2 = parallel_peg_scene(steps=3, depth=0.1e-3, offset_y=0.37e-3)
+    s2.params.ee_mollifier = 1
+    sim2, o2, mk = _run_both(s2, 3)
+    it, pg, fl = sim2.env_status()
+    assert int(fl[0]) & 1, int(fl[0])
+    _assert_parity(s2, sim2, o2, mk, 0)
+
+
 def test_fletcher_reeves_matches_oracle_behaviour(torch_cuda):
     """FR (beta rule 2) without restarts jams on the second C1 press step in the fp64
     oracle (stagnation); the GPU reproduces the converged first step and the jam."""

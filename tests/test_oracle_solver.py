@@ -500,3 +500,60 @@ def test_augmented_lagrangian_removes_the_pose_residual():
     assert res[0] > 1e-9                       # penalty residual F / k_t at ~0.1-1 N
     assert res[1] < 0.05 * res[0]              # AL: gone to the solver's tolerance
     assert np.linalg.norm(lam[:3]) == pytest.approx(k_t * res[0], rel=0.05)
+
+
+# ---------------------------------------------------------------- EE mollifier (R30)
+def test_ee_mollifier_gradient_matches_central_fd():
+    """R30: with the edge-edge mollifier on, the energy m(c) kappa b(d) of nearly parallel edge
+    pairs (a peg's axial edge over the pad's x edges) has the gradient m kappa b' w n +
+    kappa b m'(c) dc/dz: central differences agree, and the m' term is really present."""
+    from helpers import parallel_peg_scene
+    s = parallel_peg_scene(steps=2, depth=0.05e-3)
+    s.params.tol_x = 1e-10
+    s.params.ee_mollifier = 1
+    o = O.Oracle(s)
+    o.step(s.poses[0])
+    st = o.get_state(0)
+    o.step(s.poses[1])
+    u, _, c, R = o.get_state(0)
+    rng = np.random.default_rng(11)
+    u = u + 2e-7 * rng.standard_normal(u.shape)
+    u[s.fixed] = 0
+    tgt = s.poses[1][0]
+    r = o.eval(*st, u, c, R, tgt)
+    s0 = parallel_peg_scene(steps=2, depth=0.05e-3)
+    o0 = O.Oracle(s0)
+    r0 = o0.eval(*st, u, c, R, tgt)
+    assert r["parts"][2] > 0 and r["parts"][2] < r0["parts"][2]  # mollified EE barrier energy
+    free = np.setdiff1d(np.arange(len(u)), s.fixed)
+    eps = 1e-9
+    fd = np.zeros_like(u)
+    for v in free:
+        for a in range(3):
+            up = u.copy(); up[v, a] += eps
+            um = u.copy(); um[v, a] -= eps
+            fd[v, a] = (o.eval(*st, up, c, R, tgt)["E"] - o.eval(*st, um, c, R, tgt)["E"]) / (2 * eps)
+    g = r["g"][free]
+    assert np.linalg.norm(fd[free] - g) <= 1e-6 * np.linalg.norm(g)
+    fr = np.zeros(6)
+    for a in range(3):
+        e = np.zeros(3); e[a] = eps
+        fr[a] = (o.eval(*st, u, c + e, R, tgt)["E"] - o.eval(*st, u, c - e, R, tgt)["E"]) / (2 * eps)
+        e = np.zeros(3); e[a] = 1e-8
+        fr[3 + a] = (o.eval(*st, u, c, rot_exp(e) @ R, tgt)["E"] - o.eval(*st, u, c, rot_exp(-e) @ R, tgt)["E"]) / 2e-8
+    assert np.linalg.norm(fr - r["grig"]) <= 1e-6 * np.linalg.norm(r["grig"])
+    # gradient differs from the unmollified one beyond the FD tolerance
+    assert np.linalg.norm(r["g"][free] - r0["g"][free]) > 1e-4 * np.linalg.norm(g)
+
+
+def test_ee_mollifier_converges_and_stays_feasible():
+    """The mollified problem still converges with brute-force d_min > 0 (debug checks)."""
+    from helpers import parallel_peg_scene
+    s = parallel_peg_scene(steps=3, depth=0.1e-3)
+    s.params.tol_x = 1e-10
+    s.params.ee_mollifier = 1
+    o = O.Oracle(s, debug=True)
+    for k in range(3):
+        o.step(s.poses[k])
+        st = o.status_of(0)
+        assert st["flags"] & 1 and st["dmin"] > 0, st
