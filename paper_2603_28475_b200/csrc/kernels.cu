@@ -2249,8 +2249,11 @@ __global__ void __launch_bounds__(128) k_contact_curv_direct(Dev d, double h2) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) dr = dr + w[k] * dz[k];
       double dn = dot(nn, dr);
-      double lg = log(dist / d.dhat), dm = dist - d.dhat, inv = 1.0 / dist;
-      q += kappa * (-2 * lg - 4 * dm * inv + dm * dm * inv * inv) * dn * dn;
+      // b'' for the curvature estimate only (alpha_bar of P:461, then Armijo): fp32 log / rcp
+      const float rf = (float)(dist / d.dhat), lgf = __logf(rf), invf = __frcp_rn(rf);
+      const double dmr = (double)rf - 1.0;  // (d - dhat) / dhat
+      const double ddb = (-2.0 * lgf - 4.0 * dmr * invf + dmr * dmr * invf * invf);
+      q += kappa * ddb * dn * dn;
     }
     double la = -INFINITY, lb = -INFINITY;
 #pragma unroll

@@ -167,3 +167,60 @@ def test_native_marker_gather_world_of_one(torch):
         sim.gather_markers(g.comm, torch.empty((5, sim.nm, 4), device="cuda"), ncomp=4)
     g.close()
     g3.close()
+
+
+def test_graph_replay_matches_direct_launches(torch):
+    """The iteration loop replayed from CUDA graphs (default; chunks of check_every iterations
+    in the tolerance mode) and launched kernel by kernel (TAC_NO_GRAPH=1, read at create) run
+    the same kernels: converged steps agree far inside the oracle gates, and the per-step launch
+    counts are equal.  (Unconverged fixed-iteration trajectories are not compared: fp32
+    atomics' ordering noise changes Armijo / rebuild decisions along an NCG path.)"""
+    import os
+    s = w.scene_small_peg(n_envs=5, n_steps=3)
+    s.params.tol_x = 1e-9
+    s.params.stagnation = 3000
+    a = _sim(s)
+    os.environ["TAC_NO_GRAPH"] = "1"
+    try:
+        b = _sim(s)
+    finally:
+        del os.environ["TAC_NO_GRAPH"]
+    for k in range(3):
+        a.step(_poses(torch, s.poses[k]), s.dt)
+        b.step(_poses(torch, s.poses[k]), s.dt)
+    ia, _, fa = a.env_status()
+    ib, _, fb = b.env_status()
+    assert all(int(f) & 1 for f in fa) and all(int(f) & 1 for f in fb)
+    ma, mb = a.markers().cpu().numpy(), b.markers().cpu().numpy()
+    scale = np.abs(ma).max()
+    assert scale > 0 and np.abs(ma - mb).max() <= 1e-4 * scale
+    for e in range(5):
+        ua, ub = a.get_state(e)[0], b.get_state(e)[0]
+        assert np.abs(ua - ub).max() <= 1e-5 * 16e-3
+    # launch counts of a fixed-iteration step: graph replay counts its captured launches
+    s.params.fixed_iters = 20
+    a2 = _sim(s)
+    os.environ["TAC_NO_GRAPH"] = "1"
+    try:
+        b2 = _sim(s)
+    finally:
+        del os.environ["TAC_NO_GRAPH"]
+    a2.step(_poses(torch, s.poses[0]), s.dt)
+    b2.step(_poses(torch, s.poses[0]), s.dt)
+    assert a2.last_launch_count() == b2.last_launch_count() > 20
+
+
+def test_reset_clears_pose_multipliers(torch):
+    """R29: tac_reset zeroes an env's AL multipliers, so a reset env steps like a fresh one."""
+    s = c1_press_scene(mu_f=1.0, steps=3, depth=0.2e-3)
+    s.params.pose_al = 1
+    s.params.fixed_iters = 60
+    sim = _sim(s)
+    for k in range(3):
+        sim.step(_poses(torch, s.poses[k]), s.dt)
+    sim.reset(torch.ones(1, dtype=torch.uint8, device="cuda"), _poses(torch, s.init_poses))
+    sim.step(_poses(torch, s.poses[0]), s.dt)
+    fresh = _sim(s)
+    fresh.step(_poses(torch, s.poses[0]), s.dt)
+    u1, u2 = sim.get_state(0)[0], fresh.get_state(0)[0]
+    assert np.abs(u1 - u2).max() <= 1e-6 * 16e-3
