@@ -618,7 +618,7 @@ __device__ void bp_query(const Dev& d, int kind, int gid, const double* glo, con
         // exact prim box (min / max of its float Y corners), tested in double as before
         const double lo[3] = {blo.x, blo.y, blo.z}, hi[3] = {bhi.x, bhi.y, bhi.z};
         bool ok = true;
-  #pragma unroll
+#pragma unroll
         for (int a = 0; a < 3; ++a)
           if (glo[a] > __dadd_rn(hi[a], r) || lo[a] > __dadd_rn(ghi[a], r)) ok = false;
         if (!ok) continue;
@@ -1942,11 +1942,17 @@ __device__ __forceinline__ void push_local(bool mine, int lane, int* cnt, unsign
   if (slot < cap) list[slot] = (unsigned short)off;
   else glist[atomicAdd(gcnt, 1)] = cw;  // local list full: direct global append
 }
+template <bool BODY>
 __global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
   TAC_PDL_WAIT();
-  // fp32 positions (gel X + u, indenter c + R Y) carry absolute errors <= ~6e-9 m at the
-  // pad scale, so a pair is certified far only if its fp32 gap exceeds dhat + kClassMargin
-  // and the cached gap is lowered by the same margin: the certificate stays conservative
+  // BODY: the test runs in the indenter's body frame (separation along an axis of any
+  // orthonormal frame bounds the distance, R15): the env's gel surface is staged as
+  // R^T (X + u - c) and the indenter corners are its static body-frame vertices Y, shared by
+  // every env (L1/L2 resident) -- chosen when staging both sides would take more than 64 KB of
+  // shared memory per CTA (C5: 113 KB, one CTA per SM).  Otherwise both sides are staged in the
+  // gel frame (X + u, c + R Y; C3: 45 KB).  fp32 positions carry absolute errors
+  // <= ~6e-9 m at the pad scale, so a pair is certified far only if its fp32 gap exceeds
+  // dhat + kClassMargin and the cached gap is lowered by the same margin: conservative.
   constexpr float kClassMargin = 1e-7f;
   extern __shared__ __align__(16) char shc4[];
   __shared__ unsigned short q[kClassChunk];
@@ -1957,37 +1963,62 @@ __global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
   if (e >= d.E || !(d.run[e] & 1)) return;
   if ((int)blockIdx.x * kClassChunk >= min(d.ncand[e], d.kmax)) return;  // no chunk: skip the staging
   const EnvS& s = d.es[e];
-  float4* sx = reinterpret_cast<float4*>(shc4);                 // [nsv] gel X + u
-  float4* sy = reinterpret_cast<float4*>(shc4 + sizeof(float4) * d.nsv);  // [niv] c + R Y
-  if (threadIdx.x < 9) Rs[threadIdx.x] = s.R[threadIdx.x];
-  if (threadIdx.x < 3) cs[threadIdx.x] = s.c[threadIdx.x];
-  for (int i0 = threadIdx.x; i0 < d.nsv; i0 += kStageILP * blockDim.x) {
-    float4 X[kStageILP], u[kStageILP];
+  float4* sx = reinterpret_cast<float4*>(shc4);                           // [nsv] gel surface
+  float4* sy = reinterpret_cast<float4*>(shc4 + sizeof(float4) * d.nsv);  // [niv] c + R Y (gel frame only)
+  if constexpr (BODY) {
+    if (threadIdx.x < 9) Rs[threadIdx.x] = s.R[threadIdx.x];
+    if (threadIdx.x < 3) cs[threadIdx.x] = s.c[threadIdx.x];
+    __syncthreads();  // Rs, cs
+    for (int i0 = threadIdx.x; i0 < d.nsv; i0 += kStageILP * blockDim.x) {
+      float4 X[kStageILP], u[kStageILP];
 #pragma unroll
-    for (int k = 0; k < kStageILP; ++k) {
-      const int i = i0 + k * blockDim.x;
-      if (i < d.nsv) { X[k] = __ldg(d.Xs + i); u[k] = d.usurf[(size_t)i * d.Es + e]; }
+      for (int k = 0; k < kStageILP; ++k) {
+        const int i = i0 + k * blockDim.x;
+        if (i < d.nsv) { X[k] = __ldg(d.Xs + i); u[k] = d.usurf[(size_t)i * d.Es + e]; }
+      }
+#pragma unroll
+      for (int k = 0; k < kStageILP; ++k) {
+        const int i = i0 + k * blockDim.x;
+        if (i < d.nsv) {
+          const d3 x = mk((double)X[k].x + (double)u[k].x - cs[0], (double)X[k].y + (double)u[k].y - cs[1],
+                          (double)X[k].z + (double)u[k].z - cs[2]);
+          sx[i] = make_float4((float)(Rs[0] * x.x + Rs[3] * x.y + Rs[6] * x.z),
+                              (float)(Rs[1] * x.x + Rs[4] * x.y + Rs[7] * x.z),
+                              (float)(Rs[2] * x.x + Rs[5] * x.y + Rs[8] * x.z), 0.f);
+        }
+      }
     }
+  } else {
+    if (threadIdx.x < 9) Rs[threadIdx.x] = s.R[threadIdx.x];
+    if (threadIdx.x < 3) cs[threadIdx.x] = s.c[threadIdx.x];
+    for (int i0 = threadIdx.x; i0 < d.nsv; i0 += kStageILP * blockDim.x) {
+      float4 X[kStageILP], u[kStageILP];
 #pragma unroll
-    for (int k = 0; k < kStageILP; ++k) {
-      const int i = i0 + k * blockDim.x;
-      if (i < d.nsv) sx[i] = make_float4(X[k].x + u[k].x, X[k].y + u[k].y, X[k].z + u[k].z, 0.f);
+      for (int k = 0; k < kStageILP; ++k) {
+        const int i = i0 + k * blockDim.x;
+        if (i < d.nsv) { X[k] = __ldg(d.Xs + i); u[k] = d.usurf[(size_t)i * d.Es + e]; }
+      }
+#pragma unroll
+      for (int k = 0; k < kStageILP; ++k) {
+        const int i = i0 + k * blockDim.x;
+        if (i < d.nsv) sx[i] = make_float4(X[k].x + u[k].x, X[k].y + u[k].y, X[k].z + u[k].z, 0.f);
+      }
     }
-  }
-  __syncthreads();  // Rs, cs
-  for (int j0 = threadIdx.x; j0 < d.niv; j0 += kStageILP * blockDim.x) {
-    float4 yb[kStageILP];
+    __syncthreads();  // Rs, cs
+    for (int j0 = threadIdx.x; j0 < d.niv; j0 += kStageILP * blockDim.x) {
+      float4 yb[kStageILP];
 #pragma unroll
-    for (int k = 0; k < kStageILP; ++k) {
-      const int j = j0 + k * blockDim.x;
-      if (j < d.niv) yb[k] = __ldg(d.Y + j);
-    }
+      for (int k = 0; k < kStageILP; ++k) {
+        const int j = j0 + k * blockDim.x;
+        if (j < d.niv) yb[k] = __ldg(d.Y + j);
+      }
 #pragma unroll
-    for (int k = 0; k < kStageILP; ++k) {
-      const int j = j0 + k * blockDim.x;
-      if (j < d.niv) {
-        d3 y = mv(Rs, mk(yb[k].x, yb[k].y, yb[k].z)) + ld3(cs);
-        sy[j] = make_float4((float)y.x, (float)y.y, (float)y.z, 0.f);
+      for (int k = 0; k < kStageILP; ++k) {
+        const int j = j0 + k * blockDim.x;
+        if (j < d.niv) {
+          d3 y = mv(Rs, mk(yb[k].x, yb[k].y, yb[k].z)) + ld3(cs);
+          sy[j] = make_float4((float)y.x, (float)y.y, (float)y.z, 0.f);
+        }
       }
     }
   }
@@ -2052,7 +2083,7 @@ __global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const bool ind = kd == 0 ? k >= 1 : (kd == 1 ? k == 0 : k >= 2);
-            const float4 p = ind ? sy[id[k]] : sx[id[k]];
+            const float4 p = ind ? (BODY ? __ldg(d.Y + id[k]) : sy[id[k]]) : sx[id[k]];
             zx[k] = p.x; zy[k] = p.y; zz[k] = p.z;
           }
           float best = -INFINITY;
@@ -2957,8 +2988,11 @@ void launch_eval(const Dev& d, double h, cudaStream_t s) {
   LAUNCHP(KID_CONTACT_FRICTION, cs2, k_contact_friction, cgrid(d), 128, 0, d, d.eps_v * h);
   // R16: candidates of the envs k_alpha listed, rebuilt at the state k_vert_pre just reached
   launch_broadphase(d, true, cs);
-  const size_t cls_smem = sizeof(float4) * (size_t)(d.nsv + d.niv);  // [nsv] X + u, [niv] c + R Y
-  LAUNCHP(KID_CONTACT_CLASSIFY, cs, k_contact_classify_staged, sgrid(d), 256, cls_smem, d);
+  const size_t cls_both = sizeof(float4) * (size_t)(d.nsv + d.niv);  // [nsv] X + u, [niv] c + R Y
+  if (cls_both > 64 * 1024)  // body frame: stage the gel side only
+    LAUNCHP(KID_CONTACT_CLASSIFY, cs, k_contact_classify_staged<true>, sgrid(d), 256, sizeof(float4) * (size_t)d.nsv, d);
+  else
+    LAUNCHP(KID_CONTACT_CLASSIFY, cs, k_contact_classify_staged<false>, sgrid(d), 256, cls_both, d);
   const double kap = h * h;  // kernels scale by their env's kappa_phys
   if (fork) {
     cudaEventRecord(d.ev_cls, cs);
@@ -3071,7 +3105,8 @@ void kernels_init(int contact_smem) {
   // process (different meshes) share it, so it is set to the cap contact_smem_bytes
   // enforces rather than to this simulator's size (occupancy follows the launch size)
   (void)contact_smem;
-  cudaFuncSetAttribute(k_contact_classify_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, kContactSmemCap);
+  cudaFuncSetAttribute(k_contact_classify_staged<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kContactSmemCap);
+  cudaFuncSetAttribute(k_contact_classify_staged<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kContactSmemCap);
   cudaFuncSetAttribute(k_contact_curv_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, kContactSmemCap);
   cudaFuncSetAttribute(k_elem_curv_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, kTiledCurvSmem);
 }

@@ -62,12 +62,14 @@ def lib():
     global _lib
     if _lib is None:
         from . import build as _build
-        try:
-            _build.build()
-        except Exception as exc:  # no nvcc on this host: use the prebuilt library if present
-            if not os.path.exists(LIB_PATH):
-                raise RuntimeError(f"libtac.so missing and cannot be built: {exc}") from exc
-        L = C.CDLL(LIB_PATH)
+        alt = os.environ.get("TAC_LIB")  # A/B measurements: another in-tree build of libtac
+        if not alt:
+            try:
+                _build.build()
+            except Exception as exc:  # no nvcc on this host: use the prebuilt library if present
+                if not os.path.exists(LIB_PATH):
+                    raise RuntimeError(f"libtac.so missing and cannot be built: {exc}") from exc
+        L = C.CDLL(alt or LIB_PATH)
         vp = C.c_void_p
         L.tac_create.argtypes = [C.POINTER(CreateInfo), C.POINTER(vp)]
         L.tac_step.argtypes = [vp, vp, C.c_float, vp]
