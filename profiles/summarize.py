@@ -29,12 +29,14 @@ PROFILE_NAME = {"k_elem_grad_cells": "elem_grad", "k_elem_curv_cells": "elem_cur
 
 
 def short(name):
-    n = name.replace("void ", "")
-    n = n.split("(")[0]
+    n = name.replace("void ", "").replace("(int)", "").replace("(bool)", "")
+    n = n.split("(")[0].replace("tac::", "")
     for t in ("<1>", "<0>", "<true>", "<false>"):
-        if n.startswith("k_elem") and n.endswith(t):
+        if (n.startswith("k_elem") or n.startswith("k_contact_classify")) and n.endswith(t):
             n = n[: -len(t)]
-    return n.replace("tac::", "")
+    if n.startswith("k_contact_near<"):  # k_contact_near<KIND, MOLL> -> k_contact_near<KIND>
+        n = n.split(",")[0].rstrip(">") + ">"
+    return n
 
 
 def launches(path, tag):
