@@ -1643,8 +1643,10 @@ __global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
     const size_t slot = (size_t)e * d.kmax + base + j;
     d.ncorn[slot] = cw;
     float4* geo = d.cgeo + 2 * slot;
-    {  // fp32 screen: a pair at exact distance >= dhat carries no energy and is covered by
-       // the shared far-pair step bound (R15), like a pair the classification certified
+    if (KIND != 2) {  // fp32 screen (point-triangle kinds; edge-edge near pairs are nearly all
+       // within dhat, measured: the screen cost more than it saved there): a pair at exact
+       // distance >= dhat carries no energy and is covered by the shared far-pair step bound
+       // (R15), like a pair the classification certified
       f3 zf[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) zf[k] = f3{(float)(z[k].x - z[0].x), (float)(z[k].y - z[0].y), (float)(z[k].z - z[0].z)};
