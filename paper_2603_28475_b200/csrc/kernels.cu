@@ -1110,7 +1110,7 @@ __device__ __forceinline__ void aa_pair_cols(const float (*u)[3], const float* i
 // gradient of a packed tet pair: energy (per tet, without the factor w = h^2 V), and the
 // columns of P(F) and cof F scaled by 1/s_a (Pt[a][i] = w P_ia / s_a, Ct[a][i] = cof F_ia / s_a),
 // whose path differences are the corner forces and cofactor vectors (see aa branch below)
-__device__ __forceinline__ float2 grad_pair(const float2* Gm, float mu, float l2, float w, const float* inv,
+__device__ __forceinline__ float2 grad_pair(const float2* Gm, float mu, float l2, float w, const float* inv, const float* invc,
                                            float2 (*Pt)[3], float2 (*Ct)[3]) {
   const float2 trG = add2(add2(Gm[0], Gm[4]), Gm[8]);
   const float2 i2 = add2(add2(det2x2_2(Gm[0], Gm[4], Gm[1], Gm[3]), det2x2_2(Gm[0], Gm[8], Gm[2], Gm[6])),
@@ -1138,7 +1138,7 @@ __device__ __forceinline__ float2 grad_pair(const float2* Gm, float mu, float l2
       if (i == a) sym = sub2(sym, trG);
       const float2 PK = fma2(wlj, cF, mul2(f2(wmu), sub2(sym, cG[3 * i + a])));
       Pt[a][i] = mul2(PK, f2(inv[a]));
-      Ct[a][i] = mul2(cF, f2(inv[a]));
+      Ct[a][i] = mul2(cF, f2(invc[a]));  // invc = inv sqrt(lambda' h^2 V): the blocks need no further scale
     }
   return psi;
 }
@@ -1179,38 +1179,38 @@ __device__ __forceinline__ float2 curv_pair(const float2* Gm, const float2* dF, 
 // one packed pair of an axis-aligned cell: forces and lambda' c c^T blocks of both tets into the
 // cell's corner accumulators.  Tet A (.x) runs 0 -> s1 -> sA -> 7 over columns q0, qa, qb, tet B
 // (.y) 0 -> s1 -> sB -> 7 over q0, qb, qa; corner k of a path gets column(k-1) - column(k).
-__device__ __forceinline__ void corner_acc(float* ag, float* aD, float lc, float f0, float f1, float f2_,
+// (c arrives scaled by sqrt(lambda' h^2 V), so lambda' h^2 V c c^T is c c^T)
+__device__ __forceinline__ void corner_acc(float* ag, float* aD, float f0, float f1, float f2_,
                                            float c0, float c1, float c2) {
   ag[0] += f0; ag[1] += f1; ag[2] += f2_;
-  const float sx = lc * c0, sy = lc * c1, sz = lc * c2;
-  aD[0] = fmaf(sx, c0, aD[0]); aD[1] = fmaf(sy, c1, aD[1]); aD[2] = fmaf(sz, c2, aD[2]);
-  aD[3] = fmaf(sx, c1, aD[3]); aD[4] = fmaf(sx, c2, aD[4]); aD[5] = fmaf(sy, c2, aD[5]);
+  aD[0] = fmaf(c0, c0, aD[0]); aD[1] = fmaf(c1, c1, aD[1]); aD[2] = fmaf(c2, c2, aD[2]);
+  aD[3] = fmaf(c0, c1, aD[3]); aD[4] = fmaf(c0, c2, aD[4]); aD[5] = fmaf(c1, c2, aD[5]);
 }
 template <int m>
-__device__ __forceinline__ void pair_grad_acc(const float (*u)[3], const float* inv, float mu, float l2, float w,
-                                              float lc, double& esum, float (*ag)[3], float (*aD)[6]) {
+__device__ __forceinline__ void pair_grad_acc(const float (*u)[3], const float* inv, const float* invc, float mu,
+                                              float l2, float w, double& esum, float (*ag)[3], float (*aD)[6]) {
   constexpr int jA = 2 * m, jB = 2 * m + 1;
   constexpr int s1 = CELL_TET(jA, 1), sA = CELL_TET(jA, 2), sB = CELL_TET(jB, 2);
   constexpr int q0 = CELL_Q(jA, 0), qa = CELL_Q(jA, 1), qb = CELL_Q(jA, 2);
   float2 Gm[9], Pt[3][3], Ct[3][3];
   aa_pair_cols<m>(u, inv, Gm);
-  const float2 psi = grad_pair(Gm, mu, l2, w, inv, Pt, Ct);
+  const float2 psi = grad_pair(Gm, mu, l2, w, inv, invc, Pt, Ct);
   esum += (double)(w * psi.x);
   esum += (double)(w * psi.y);
   // tet A
-  corner_acc(ag[0], aD[0], lc, -Pt[q0][0].x, -Pt[q0][1].x, -Pt[q0][2].x, -Ct[q0][0].x, -Ct[q0][1].x, -Ct[q0][2].x);
-  corner_acc(ag[s1], aD[s1], lc, Pt[q0][0].x - Pt[qa][0].x, Pt[q0][1].x - Pt[qa][1].x, Pt[q0][2].x - Pt[qa][2].x,
+  corner_acc(ag[0], aD[0], -Pt[q0][0].x, -Pt[q0][1].x, -Pt[q0][2].x, -Ct[q0][0].x, -Ct[q0][1].x, -Ct[q0][2].x);
+  corner_acc(ag[s1], aD[s1], Pt[q0][0].x - Pt[qa][0].x, Pt[q0][1].x - Pt[qa][1].x, Pt[q0][2].x - Pt[qa][2].x,
              Ct[q0][0].x - Ct[qa][0].x, Ct[q0][1].x - Ct[qa][1].x, Ct[q0][2].x - Ct[qa][2].x);
-  corner_acc(ag[sA], aD[sA], lc, Pt[qa][0].x - Pt[qb][0].x, Pt[qa][1].x - Pt[qb][1].x, Pt[qa][2].x - Pt[qb][2].x,
+  corner_acc(ag[sA], aD[sA], Pt[qa][0].x - Pt[qb][0].x, Pt[qa][1].x - Pt[qb][1].x, Pt[qa][2].x - Pt[qb][2].x,
              Ct[qa][0].x - Ct[qb][0].x, Ct[qa][1].x - Ct[qb][1].x, Ct[qa][2].x - Ct[qb][2].x);
-  corner_acc(ag[7], aD[7], lc, Pt[qb][0].x, Pt[qb][1].x, Pt[qb][2].x, Ct[qb][0].x, Ct[qb][1].x, Ct[qb][2].x);
+  corner_acc(ag[7], aD[7], Pt[qb][0].x, Pt[qb][1].x, Pt[qb][2].x, Ct[qb][0].x, Ct[qb][1].x, Ct[qb][2].x);
   // tet B
-  corner_acc(ag[0], aD[0], lc, -Pt[q0][0].y, -Pt[q0][1].y, -Pt[q0][2].y, -Ct[q0][0].y, -Ct[q0][1].y, -Ct[q0][2].y);
-  corner_acc(ag[s1], aD[s1], lc, Pt[q0][0].y - Pt[qb][0].y, Pt[q0][1].y - Pt[qb][1].y, Pt[q0][2].y - Pt[qb][2].y,
+  corner_acc(ag[0], aD[0], -Pt[q0][0].y, -Pt[q0][1].y, -Pt[q0][2].y, -Ct[q0][0].y, -Ct[q0][1].y, -Ct[q0][2].y);
+  corner_acc(ag[s1], aD[s1], Pt[q0][0].y - Pt[qb][0].y, Pt[q0][1].y - Pt[qb][1].y, Pt[q0][2].y - Pt[qb][2].y,
              Ct[q0][0].y - Ct[qb][0].y, Ct[q0][1].y - Ct[qb][1].y, Ct[q0][2].y - Ct[qb][2].y);
-  corner_acc(ag[sB], aD[sB], lc, Pt[qb][0].y - Pt[qa][0].y, Pt[qb][1].y - Pt[qa][1].y, Pt[qb][2].y - Pt[qa][2].y,
+  corner_acc(ag[sB], aD[sB], Pt[qb][0].y - Pt[qa][0].y, Pt[qb][1].y - Pt[qa][1].y, Pt[qb][2].y - Pt[qa][2].y,
              Ct[qb][0].y - Ct[qa][0].y, Ct[qb][1].y - Ct[qa][1].y, Ct[qb][2].y - Ct[qa][2].y);
-  corner_acc(ag[7], aD[7], lc, Pt[qa][0].y, Pt[qa][1].y, Pt[qa][2].y, Ct[qa][0].y, Ct[qa][1].y, Ct[qa][2].y);
+  corner_acc(ag[7], aD[7], Pt[qa][0].y, Pt[qa][1].y, Pt[qa][2].y, Ct[qa][0].y, Ct[qa][1].y, Ct[qa][2].y);
 }
 
 // ALL_AA: every cell of the mesh is axis-aligned (structured pads) -- the stored-B branch is
@@ -1262,13 +1262,14 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
     if constexpr (ALL_AA) {  // packed tet pairs (0,1), (2,3), (4,5); every tet has volume caa.w
       // each corner is flushed right after the last pair touching it (pair 0: corners 0 1 3 5 7,
       // pair 1: 0 2 3 6 7, pair 2: 0 4 5 6 7), so at most 6 corners' accumulators are live
-      const float w = h2 * caa.w, lc = w * l2;
-      pair_grad_acc<0>(u, inv, mu, l2, w, lc, esum, ag, aD);
+      const float w = h2 * caa.w, sl = sqrtf(w * l2);
+      const float invc[3] = {inv[0] * sl, inv[1] * sl, inv[2] * sl};
+      pair_grad_acc<0>(u, inv, invc, mu, l2, w, esum, ag, aD);
       flush(1);
-      pair_grad_acc<1>(u, inv, mu, l2, w, lc, esum, ag, aD);
+      pair_grad_acc<1>(u, inv, invc, mu, l2, w, esum, ag, aD);
       flush(2);
       flush(3);
-      pair_grad_acc<2>(u, inv, mu, l2, w, lc, esum, ag, aD);
+      pair_grad_acc<2>(u, inv, invc, mu, l2, w, esum, ag, aD);
 #pragma unroll
       for (int s : {0, 4, 5, 6, 7}) flush(s);
     } else {
