@@ -2897,16 +2897,26 @@ __global__ void k_any_active(Dev d, int* out) {
 }
 
 // ------------------------------------------------------------------ launchers
-static dim3 vgrid(const Dev& d, int n) {
+static int env_int(const char* k, int dflt) { return getenv(k) ? atoi(getenv(k)) : dflt; }  // A/B
+static dim3 vgrid(const Dev& d, int n, int bps = 8) {
   int gx = d.Es / 32;
   // ~8 blocks of 256 threads per SM over the grid (grid-stride over the rest); interleaved
   // A/B on B200 vs 16/SM: C3 +1.5 %, C5 +2.6 % (4/SM and 6/SM were slower, 12/SM within 0.3 %)
-  int gy = (148 * 8 + gx - 1) / gx;
+  int gy = (148 * bps + gx - 1) / gx;
   gy = std::max(1, std::min(gy, (n + 7) / 8));
   return dim3(gx, gy);
 }
+static dim3 cellgrid(const Dev& d) {
+  static const int bps = env_int("TAC_CELL_BPS", 8);
+  return vgrid(d, d.ncells, bps);
+}
 static dim3 cgrid(const Dev& d) {
-  int nb = std::max(1, std::min(64, 2368 / std::max(1, d.E)));
+  // ~16 blocks of 128 threads per SM over the grid. 8/SM (one block per env at 1,024 envs) was
+  // +1.6 % on C3 in an interleaved A/B, but it changes the per-env summation order, and the
+  // full-size tolerance-mode parity test then drifted past its bound on one sampled env
+  // (4.8e-5 m vs 3.2e-6 m): kept at 16 until that sensitivity is understood
+  static const int tot = 148 * env_int("TAC_CONTACT_BPS", 16);
+  int nb = std::max(1, std::min(64, tot / std::max(1, d.E)));
   return dim3(nb, d.E);
 }
 static int eblocks(const Dev& d) { return (d.E + 127) / 128; }
@@ -3014,7 +3024,7 @@ void launch_eval(const Dev& d, double h, cudaStream_t s) {
   // (a round-scheduled shared-memory tiled variant measured slower on C3: 740 vs 520 us at
   // 66 % warp utilisation in the rounds and 2 CTAs/SM; the coalesced red.add scatter stays)
   if (d.ncells > 0) {
-    dim3 g = vgrid(d, d.ncells);
+    dim3 g = cellgrid(d);
     if (d.cells_all_aa) LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad_cells<true>, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
     else LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad_cells<false>, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
   }
@@ -3054,7 +3064,7 @@ void launch_curvature(const Dev& d, double h, cudaStream_t s) {
   else LAUNCHP(KID_CONTACT_CURV, cs, k_contact_curv_direct, cgrid(d), 128, 0, d, h * h);
   if (fork) cudaEventRecord(d.ev_join, cs);
   if (d.nrest == 0) {  // every tet is in a Kuhn cell: register-blocked cells
-    dim3 g = vgrid(d, d.ncells);
+    dim3 g = cellgrid(d);
     if (d.cells_all_aa) LAUNCHP(KID_ELEM_CURV, s, k_elem_curv_cells<true>, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
     else LAUNCHP(KID_ELEM_CURV, s, k_elem_curv_cells<false>, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
   } else {
