@@ -48,7 +48,8 @@ typedef int32_t tac_status;
 #define TAC_FLAG_NAN 4u         /* non-finite energy at the step start: env rolled back */
 #define TAC_FLAG_INFEASIBLE 8u  /* a candidate pair reached d <= 0 at the step start: rolled back */
 #define TAC_FLAG_LARGE_MOTION 16u /* target pose > 2 mm or > 5 deg from the current pose */
-#define TAC_FLAG_OVERFLOW 32u   /* candidate or anchor capacity exceeded (pairs dropped) */
+#define TAC_FLAG_OVERFLOW 32u   /* candidate or anchor capacity exceeded: pairs would be dropped, so the
+                                  step fails at its next evaluation and the env is rolled back */
 #define TAC_FLAG_STAGNATION 64u /* no decrease of |P g|_disp over `stagnation` iterations */
 
 /* Gel tetrahedral mesh (Supp. §A "We discretize the sensor gel using a tetrahedral
@@ -99,7 +100,10 @@ typedef struct {
  *   bp_margin [m]   candidate margin m_r; candidates within r = dhat + m_r (R16)
  *   c1, eps_E       Armijo constant and relative energy noise allowance (R14)
  *   max_iters       iteration budget per step (tolerance mode)
- *   fixed_iters     > 0: run exactly this many iterations per step (benchmark mode)
+ *   fixed_iters     > 0: run exactly this many iterations per step (benchmark mode).
+ *                   A step that ends without converging (fixed mode, or max_iters reached)
+ *                   commits its last ACCEPTED iterate, never an unevaluated or rejected trial
+ *                   (R31); the budget's last evaluation computes no new direction.
  *   beta_rule       0 Dai-Kou, 1 PR+, 2 FR, 3 DK+ (max(beta_DK, 0.5 g^T p/|p|^2), R28);
  *                   outside 0..3 -> TAC_EINVAL
  *   precond         0 3x3 block Jacobi, 1 scalar Jacobi P = diag(H)^-1; else TAC_EINVAL
@@ -191,6 +195,20 @@ tac_status tac_set_pose_noise(tac_sim* sim, double sigma_t, double sigma_r, uint
  * Asynchronous on `stream`. */
 tac_status tac_marker_sqerr(tac_sim* sim, const float* ref, double* acc, int32_t ncomp, void* stream);
 
+/* Checkpoint / resume: the state one step carries into the next -- u^t, v^t
+ * of every env, the per-env pose / multipliers / statistics record and the step counter that
+ * keys the pose-noise streams (R27).  Candidate lists and anchors are rebuilt at every step
+ * start, so they are not part of it.  `bytes` receives the size of a checkpoint; `dst` /
+ * `src` are caller-owned DEVICE buffers of at least that size on the handle's device.
+ * Save is asynchronous on `stream`; load validates the buffer's header (TAC_EINVAL if it was
+ * written by a simulator of another size) and therefore synchronises `stream` once before
+ * its asynchronous device-to-device copies.  Loading a checkpoint and stepping with the
+ * same targets reproduces the steps taken after the save (up to the order of fp32 atomic
+ * sums). */
+tac_status tac_checkpoint_size(const tac_sim* sim, uint64_t* bytes);
+tac_status tac_checkpoint_save(tac_sim* sim, void* dst, void* stream);
+tac_status tac_checkpoint_load(tac_sim* sim, const void* src, void* stream);
+
 /* Re-initialise the envs with env_mask[e] != 0 (device uint8 [n_envs]) to rest,
  * zero velocity and pose poses[e] (device fp32 [n_envs][7]). */
 tac_status tac_reset(tac_sim* sim, const uint8_t* env_mask, const float* poses, void* stream);
@@ -202,9 +220,11 @@ tac_status tac_reset(tac_sim* sim, const uint8_t* env_mask, const float* poses, 
  * nothing changes.  Takes effect at the next tac_step: Lame parameters (SNH),
  * lumped masses, the elastic diagonal blocks, the friction coefficient and,
  * with the default kappa rule (kappa_phys == 0 at create, R4), the barrier stiffness
- * 0.2 E lbar^2 / (12.25 dhat).  Synchronous (blocking host-to-device copy). */
+ * 0.2 E lbar^2 / (12.25 dhat).  The upload is ordered on `stream` after the work already
+ * queued there (a tac_step in flight on it finishes with the old tables) and the call returns
+ * once it has landed (it synchronises `stream`). */
 tac_status tac_set_env_material(tac_sim* sim, const double* E, const double* nu, const double* rho,
-                                const double* mu_f);
+                                const double* mu_f, void* stream);
 
 /* Per-env diagnostics of the last step (device outputs [n_envs], any may be NULL):
  * iterations used, |P g|_disp at exit, flags (TAC_FLAG_*). */

@@ -1124,7 +1124,7 @@ void env_step(const Problem& P, Env& E, const double* target7, double h, const O
   int halvings = 0, it = 0;
   double best_pg = INF;
   int best_it = 0;
-  bool converged = false, failed = false;
+  bool converged = false, failed = false, last_rejected = false;
   int K = P.fixed_iters > 0 ? P.fixed_iters : P.max_iters;
   for (it = 0; it < K; ++it) {
     // O4b: evaluate
@@ -1150,11 +1150,13 @@ void env_step(const Problem& P, Env& E, const double* target7, double h, const O
           halvings = 0;
         }
         if (E.want_trace) E.trace.push_back({(double)it, Ek, 0, alpha, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0});
+        last_rejected = true;
         continue;
       }
     }
     reeval = false;
     halvings = 0;
+    last_rejected = false;
     if (!std::isfinite(Ek)) { failed = true; break; }
     // O4d: convergence on |P g|_disp
     Vecs g = to_vecs(G);
@@ -1163,6 +1165,9 @@ void env_step(const Problem& P, Env& E, const double* target7, double h, const O
     if (P.fixed_iters == 0 && pgn <= P.tol_x) { converged = true; E.pg = pgn; break; }
     if (pgn < best_pg * (1 - 1e-3)) { best_pg = pgn; best_it = it; }
     if (P.fixed_iters == 0 && P.stagnation > 0 && it - best_it > P.stagnation) { E.flags |= F_STAG; E.pg = pgn; break; }
+    // the last evaluation of the budget: the step ends at this accepted iterate (no new
+    // direction, no unevaluated trial is committed)
+    if (it == K - 1) { E.pg = pgn; it = K; break; }
     // O4e: direction, Eq. (dk_direction)
     double gPg = vdot(P, g, Pg);
     bool rs = restart || it == 0;
@@ -1220,6 +1225,9 @@ void env_step(const Problem& P, Env& E, const double* target7, double h, const O
     E.pg = pgn;
   }
   E.iters = it;
+  // budget spent on a rejected trial: commit the last accepted iterate x_k, never a trial
+  // whose energy was not accepted
+  if (!converged && !failed && last_rejected) s = s_prev;
   if (failed) {  // roll back to x^t (SURVEY §5 failure detection)
     E.flags |= F_NAN;
     s = State{E.u_t, E.c_t, E.R_t};

@@ -56,8 +56,11 @@ struct tac_sim {
     const void* anc = nullptr;
     double h = 0;
     int n = 0;
+    bool fin = false;
     long long launches = 0;
-  } graphs[2];
+    unsigned long long used = 0;  // LRU stamp
+  } graphs[4];
+  unsigned long long graph_clock = 0;
   cudaStream_t cap = nullptr;  // capture stream (graphs are launched on the caller's stream)
   bool use_graphs = true;      // TAC_NO_GRAPH=1 at create disables (A/B measurements)
 };
@@ -244,7 +247,7 @@ int build_bvh(std::vector<BNode>& nodes, std::vector<int>& prims, const std::vec
 }
 
 // per-env material tables from the current theta (padding lanes take env 0's values)
-tac_status upload_env_material(tac_sim* sim) {
+tac_status upload_env_material(tac_sim* sim, cudaStream_t stream) {
   const Dev& d = sim->d;
   std::vector<float> em(4 * (size_t)d.Es);
   std::vector<double> ed(2 * (size_t)d.Es);
@@ -260,8 +263,11 @@ tac_status upload_env_material(tac_sim* sim) {
     ed[e] = sim->kappa_fixed ? d.kappa_phys : 0.2 * E * sim->lbar * sim->lbar / (12.25 * d.dhat);  // R4 per env
     ed[d.Es + e] = sim->thMu[s];
   }
-  if (cudaMemcpy(d.emat, em.data(), sizeof(float) * em.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
-      cudaMemcpy(d.edbl, ed.data(), sizeof(double) * ed.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+  // ordered on `stream` behind the caller's queued work; the host staging vectors are freed on
+  // return, so the copies must have landed first
+  if (cudaMemcpyAsync(d.emat, em.data(), sizeof(float) * em.size(), cudaMemcpyHostToDevice, stream) != cudaSuccess ||
+      cudaMemcpyAsync(d.edbl, ed.data(), sizeof(double) * ed.size(), cudaMemcpyHostToDevice, stream) != cudaSuccess ||
+      cudaStreamSynchronize(stream) != cudaSuccess)
     return TAC_ECUDA;
   return TAC_OK;
 }
@@ -924,7 +930,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
         (rc = zalloc(sim, 1, &sim->d_dbg_cnt)) || (rc = zalloc(sim, 3 * (size_t)nv, &sim->d_scratch)))
       goto fail;
     if (cudaMallocHost(&sim->h_flag, sizeof(int)) != cudaSuccess) { rc = TAC_ENOMEM; goto fail; }
-    if ((rc = upload_env_material(sim))) { sim->err = "upload per-env material"; goto fail; }
+    if ((rc = upload_env_material(sim, 0))) { sim->err = "upload per-env material"; goto fail; }
     int prio_lo = 0, prio_hi = 0;  // the rebuild's few long warps must start before the element pass fills the SMs
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
     if (cudaStreamCreateWithPriority(&d.side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
@@ -1028,7 +1034,9 @@ static tac_status post_launch(tac_sim* sim) {
   return TAC_OK;
 }
 
-static void launch_iterations(const Dev& d, double h, int n, cudaStream_t s) {
+// n PNCG iterations; with `fin` the last one is the step's final evaluation: Armijo and
+// the convergence test only (the step then commits the last accepted iterate, R31)
+static void launch_iterations(const Dev& d, double h, int n, bool fin, cudaStream_t s) {
   for (int it = 0; it < n; ++it) {
     const bool tl = it == g_tl_iter;
     if (tl) {
@@ -1037,6 +1045,10 @@ static void launch_iterations(const Dev& d, double h, int n, cudaStream_t s) {
       g_tl_on = true;
     }
     launch_eval(d, h, s);       // a4 + a5 + Armijo (a8)
+    if (fin && it == n - 1) {
+      launch_direction(d, s, false);  // a8 convergence test
+      break;
+    }
     launch_direction(d, s);     // a6
     launch_curvature(d, h, s);  // a7
     launch_alpha(d, h, s);      // a7/a8 (+ a2 rebuild)
@@ -1047,30 +1059,32 @@ static void launch_iterations(const Dev& d, double h, int n, cudaStream_t s) {
   }
 }
 
-// n PNCG iterations on stream s: replayed from a cached CUDA graph unless per-launch
-// profiling is on (its events sit between the launches) or graphs are disabled.
-static bool run_iterations(tac_sim* sim, double h, int n, cudaStream_t s) {
+// n PNCG iterations on stream s (the last one the step's final evaluation if `fin`):
+// replayed from a cached CUDA graph unless per-launch profiling is on (its events sit
+// between the launches) or graphs are disabled.  Graphs are keyed by (anchor buffer, h, n,
+// fin): the fixed mode uses one per anchor buffer, the tolerance mode a chunk graph and a
+// final-chunk graph per anchor buffer.
+static bool run_iterations(tac_sim* sim, double h, int n, bool fin, cudaStream_t s) {
   const Dev& d = sim->d;
   if (sim->prof || !sim->use_graphs) {
-    launch_iterations(d, h, n, s);
+    launch_iterations(d, h, n, fin, s);
     return true;
   }
   tac_sim::IterGraph* G = nullptr;
   for (auto& g : sim->graphs)
-    if (g.exec && g.anc == (const void*)d.anc && g.h == h && g.n == n) G = &g;
-  if (!G) {  // capture: reuse the slot of this anchor buffer, else an empty one, else slot 0
+    if (g.exec && g.anc == (const void*)d.anc && g.h == h && g.n == n && g.fin == fin) G = &g;
+  if (!G) {  // capture into an empty slot, else the least recently used one
     G = &sim->graphs[0];
-    for (auto& g : sim->graphs)
-      if (g.anc == (const void*)d.anc) { G = &g; break; }
-    if (G->anc != (const void*)d.anc)
-      for (auto& g : sim->graphs)
-        if (!g.exec) { G = &g; break; }
+    for (auto& g : sim->graphs) {
+      if (!g.exec) { G = &g; break; }
+      if (g.used < G->used) G = &g;
+    }
     if (G->exec) { cudaGraphExecDestroy(G->exec); G->exec = nullptr; }
     const long long l0 = g_launches;
     cudaGraph_t gr = nullptr;
     bool ok = cudaStreamBeginCapture(sim->cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
     if (ok) {
-      launch_iterations(d, h, n, sim->cap);
+      launch_iterations(d, h, n, fin, sim->cap);
       ok = cudaStreamEndCapture(sim->cap, &gr) == cudaSuccess && gr;
     }
     // kernel nodes keep their stream's priority (the contact chain's high priority)
@@ -1083,15 +1097,17 @@ static bool run_iterations(tac_sim* sim, double h, int n, cudaStream_t s) {
       sim->use_graphs = false;
       g_launches = l0;
       if (getenv("TAC_GRAPH_DEBUG")) fprintf(stderr, "tac: iteration graph capture failed, direct launches\n");
-      launch_iterations(d, h, n, s);
+      launch_iterations(d, h, n, fin, s);
       return true;
     }
     G->anc = d.anc;
     G->h = h;
     G->n = n;
+    G->fin = fin;
     G->launches = g_launches - l0;
     g_launches = l0;
   }
+  G->used = ++sim->graph_clock;
   g_launches += G->launches;
   return cudaGraphLaunch(G->exec, s) == cudaSuccess;
 }
@@ -1116,7 +1132,7 @@ tac_status tac_step(tac_sim* sim, const float* target_poses, float dt, void* str
   const int chunk = sim->fixed_iters > 0 ? K : std::min(K, sim->check_every);
   for (int it = 0; it < K;) {
     const int n = std::min(chunk, K - it);
-    if (!run_iterations(sim, h, n, s)) { g_prof = nullptr; return post_launch(sim); }
+    if (!run_iterations(sim, h, n, it + n == K, s)) { g_prof = nullptr; return post_launch(sim); }
     it += n;
     if (sim->fixed_iters == 0 && it % sim->check_every == 0 && it < K) {  // all envs done?
       cudaMemsetAsync(sim->d_flag, 0, sizeof(int), s);
@@ -1251,6 +1267,72 @@ tac_status tac_marker_sqerr(tac_sim* sim, const float* ref, double* acc, int32_t
   return post_launch(sim);
 }
 
+// ------------------------------------------------------------ checkpoint / resume
+// layout: 64-byte header {magic, version, nv, Es, E, sizeof(EnvS), step_count}, u^t, v^t
+// ([3][nv][Es] fp32 each, the AoSoA layout), EnvS [E]
+namespace {
+constexpr uint64_t kCkptMagic = 0x54414331434b5054ull;  // "TPKC1CAT"
+struct CkptHeader {
+  uint64_t magic, version, nv, Es, E, envs_bytes, step_count, pad;
+};
+static_assert(sizeof(CkptHeader) == 64, "checkpoint header");
+size_t ckpt_vec_bytes(const Dev& d) { return sizeof(float) * 3 * (size_t)d.nv * d.Es; }
+size_t ckpt_bytes(const Dev& d) { return sizeof(CkptHeader) + 2 * ckpt_vec_bytes(d) + sizeof(EnvS) * (size_t)d.E; }
+}  // namespace
+
+tac_status tac_checkpoint_size(const tac_sim* sim, uint64_t* bytes) {
+  if (!sim || !bytes) return TAC_EINVAL;
+  *bytes = ckpt_bytes(sim->d);
+  return TAC_OK;
+}
+
+tac_status tac_checkpoint_save(tac_sim* sim, void* dst, void* stream) {
+  tac_status st = check_sim(sim);
+  if (st) return st;
+  if (!dst) { sim->err = "tac_checkpoint_save: null buffer"; return TAC_EINVAL; }
+  cudaSetDevice(sim->device);
+  const Dev& d = sim->d;
+  cudaStream_t s = (cudaStream_t)stream;
+  CkptHeader h{kCkptMagic, 1, (uint64_t)d.nv, (uint64_t)d.Es, (uint64_t)d.E, sizeof(EnvS) * (uint64_t)d.E,
+               sim->step_count, 0};
+  char* p = (char*)dst;
+  // the header travels as a kernel argument (captured at launch: no host buffer to keep alive)
+  launch_write_words(d, (uint64_t*)p, (const uint64_t*)&h, sizeof(h) / 8, s);
+  p += sizeof(h);
+  CK(cudaMemcpyAsync(p, d.ut, ckpt_vec_bytes(d), cudaMemcpyDeviceToDevice, s));
+  p += ckpt_vec_bytes(d);
+  CK(cudaMemcpyAsync(p, d.vt, ckpt_vec_bytes(d), cudaMemcpyDeviceToDevice, s));
+  p += ckpt_vec_bytes(d);
+  CK(cudaMemcpyAsync(p, d.es, sizeof(EnvS) * (size_t)d.E, cudaMemcpyDeviceToDevice, s));
+  return post_launch(sim);
+}
+
+tac_status tac_checkpoint_load(tac_sim* sim, const void* src, void* stream) {
+  tac_status st = check_sim(sim);
+  if (st) return st;
+  if (!src) { sim->err = "tac_checkpoint_load: null buffer"; return TAC_EINVAL; }
+  cudaSetDevice(sim->device);
+  const Dev& d = sim->d;
+  cudaStream_t s = (cudaStream_t)stream;
+  CkptHeader h;
+  CK(cudaMemcpyAsync(&h, src, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (h.magic != kCkptMagic || h.version != 1 || h.nv != (uint64_t)d.nv || h.Es != (uint64_t)d.Es ||
+      h.E != (uint64_t)d.E || h.envs_bytes != sizeof(EnvS) * (uint64_t)d.E) {
+    sim->err = "tac_checkpoint_load: not a checkpoint of a simulator of this size";
+    return TAC_EINVAL;
+  }
+  const char* p = (const char*)src + sizeof(h);
+  CK(cudaMemcpyAsync(d.ut, p, ckpt_vec_bytes(d), cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(d.u, p, ckpt_vec_bytes(d), cudaMemcpyDeviceToDevice, s));
+  p += ckpt_vec_bytes(d);
+  CK(cudaMemcpyAsync(d.vt, p, ckpt_vec_bytes(d), cudaMemcpyDeviceToDevice, s));
+  p += ckpt_vec_bytes(d);
+  CK(cudaMemcpyAsync(d.es, p, sizeof(EnvS) * (size_t)d.E, cudaMemcpyDeviceToDevice, s));
+  sim->step_count = h.step_count;
+  return TAC_OK;
+}
+
 tac_status tac_reset(tac_sim* sim, const uint8_t* env_mask, const float* poses, void* stream) {
   tac_status st = check_sim(sim);
   if (st) return st;
@@ -1261,7 +1343,7 @@ tac_status tac_reset(tac_sim* sim, const uint8_t* env_mask, const float* poses, 
 }
 
 tac_status tac_set_env_material(tac_sim* sim, const double* E, const double* nu, const double* rho,
-                                const double* mu_f) {
+                                const double* mu_f, void* stream) {
   tac_status st = check_sim(sim);
   if (st) return st;
   const int n = sim->d.E;
@@ -1279,7 +1361,7 @@ tac_status tac_set_env_material(tac_sim* sim, const double* E, const double* nu,
     if (mu_f) sim->thMu[e] = mu_f[e];
   }
   cudaSetDevice(sim->device);
-  if ((st = upload_env_material(sim))) { sim->err = "tac_set_env_material: upload failed"; return st; }
+  if ((st = upload_env_material(sim, (cudaStream_t)stream))) { sim->err = "tac_set_env_material: upload failed"; return st; }
   return TAC_OK;
 }
 

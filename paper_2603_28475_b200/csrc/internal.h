@@ -49,6 +49,9 @@ struct EnvS {
   double E, Eprev, alpha, gp_prev, gPg_prev, S, beta, best_pg, pg, pose_res;
   double wt_acc, wr_acc;       // pose-spring weights psi'(r)/r at the last accepted point (k_alpha's curvature)
   double lam[6];               // pose multipliers (lam_t [N], lam_r [N m]) of the AL pose term (R29)
+  double back;                 // u moves by back * p from the last evaluated point to the last accepted
+                               // iterate x_k: 0 after an acceptance, -alpha of the rejected trial otherwise
+                               // (a step that ends without converging commits x_k, never a trial)
   double Lrel_last;
   double odo, odo_base, Lc;   // classification odometer (R15 cache): path-length coordinate of the
                               // trial point / of x_k, L_rel of the current direction
@@ -61,6 +64,10 @@ struct EnvS {
 
 // modes
 constexpr int kActive = 0, kDone = 1;
+// status flags (include/tac.h TAC_FLAG_*); a failed env is rolled back to x^t at finalize
+constexpr int kFlagConv = 1, kFlagMaxIt = 2, kFlagNaN = 4, kFlagInfeas = 8, kFlagLarge = 16, kFlagOverflow = 32,
+              kFlagStag = 64;
+constexpr int kFlagFailed = kFlagNaN | kFlagInfeas | kFlagOverflow;
 
 // double accumulators [kNAcc][Es]
 enum AccIdx {
@@ -171,7 +178,9 @@ void launch_vert_setup(const Dev& d, double h, cudaStream_t s);
 void launch_broadphase(const Dev& d, bool masked, cudaStream_t s);
 void launch_anchors(const Dev& d, double h, cudaStream_t s);
 void launch_eval(const Dev& d, double h, cudaStream_t s);  // vertex pre + element + contact + accept
-void launch_direction(const Dev& d, cudaStream_t s);
+// apply = false: the convergence test and scalars only (the step's last evaluation: no new
+// direction is needed, the step ends at the accepted iterate)
+void launch_direction(const Dev& d, cudaStream_t s, bool apply = true);
 void launch_curvature(const Dev& d, double h, cudaStream_t s);
 void launch_alpha(const Dev& d, double h, cudaStream_t s);
 void launch_finalize(const Dev& d, double h, cudaStream_t s);
@@ -182,6 +191,7 @@ void launch_marker_sqerr(const Dev& d, const float* ref, double* acc, int ncomp,
 void launch_reset(const Dev& d, const unsigned char* mask, const float* poses, cudaStream_t s);
 void launch_status(const Dev& d, int* iters, float* pg, unsigned* flags, cudaStream_t s);
 void launch_any_active(const Dev& d, int* out, cudaStream_t s);
+void launch_write_words(const Dev& d, uint64_t* dst, const uint64_t* words, int n, cudaStream_t s);  // n <= 8
 void launch_stats(const Dev& d, int4* out, cudaStream_t s);
 // debug
 void launch_debug_broadphase(const Dev& d, double r, unsigned long long* out, int* cnt, int cap, cudaStream_t s);

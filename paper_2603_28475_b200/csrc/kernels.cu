@@ -537,7 +537,7 @@ __global__ void k_step_setup(Dev d, const float* poses, unsigned long long step)
   s.iter = 0; s.halv = 0; s.restart = 1; s.reeval = 0; s.mode = kActive; s.best_it = 0; s.accepted = 0;
   s.rebuild = 0; s.ncand_over = 0; s.ncand_max = 0; s.nanc_last = 0;
   s.odo = 0; s.odo_base = 0; s.Lc = 0; s.cache_ok = 0;
-  s.alpha = 0; s.S = 0; s.best_pg = INFINITY; s.pg = 0; s.E = 0; s.Eprev = 0; s.gp_prev = 0; s.beta = 0;
+  s.alpha = 0; s.back = 0; s.S = 0; s.best_pg = INFINITY; s.pg = 0; s.E = 0; s.Eprev = 0; s.gp_prev = 0; s.beta = 0;
   for (int i = 0; i < 6; ++i) s.pr[i] = 0;
   d.dalpha[e] = 0.f;
   d.beta[e] = 0.f;
@@ -2367,6 +2367,15 @@ __global__ void k_accept(Dev d, double h) {
   s.Ep[0] = A[A_EIN * Es + e]; s.Ep[1] = A[A_EEL * Es + e]; s.Ep[2] = Eb; s.Ep[3] = A[A_EF * Es + e];
   s.Ep[4] = Ep;
   for (int k = 0; k < 28; ++k) A[k * Es + e] = 0.0;
+  if (s.ncand_over) {  // candidate or anchor capacity exceeded: pairs were dropped, the barrier
+    // and the step bound no longer see them -- the step fails and rolls back (flag 32)
+    s.flags |= kFlagOverflow;
+    s.mode = kDone;
+    s.back = 0;
+    d.run[e] = 0;
+    d.dalpha[e] = 0.f;
+    return;
+  }
   gr[0] += h2 * wt * dc.x; gr[1] += h2 * wt * dc.y; gr[2] += h2 * wt * dc.z;
   gr[3] += h2 * wr * phi.x; gr[4] += h2 * wr * phi.y; gr[5] += h2 * wr * phi.z;
   if (d.pose_al) {  // h^2 lam_t and h^2 J_l(phi)^-T lam_r (R29)
@@ -2379,7 +2388,7 @@ __global__ void k_accept(Dev d, double h) {
   d.dalpha[e] = 0.f;
   bool first = (s.iter == 1);
   if (first && !isfinite(E)) {  // infeasible / NaN at the step start: roll back
-    s.flags |= isfinite(Eb) ? 4 : 8;
+    s.flags |= isfinite(Eb) ? kFlagNaN : kFlagInfeas;
     s.mode = kDone;
     d.run[e] = 0;
     return;
@@ -2397,10 +2406,12 @@ __global__ void k_accept(Dev d, double h) {
     s.halv = 0;
     s.reeval = 0;
     s.accepted = 1;
+    s.back = 0;
     d.run[e] = 2;
     return;
   }
   s.accepted = 0;
+  s.back = -s.alpha;  // the rejected trial is x_k + alpha p
   d.accu[U_GFAR * Es + e] = 0x7f800000u;  // the next evaluation re-classifies
   s.halv += 1;
   s.odo_base = s.odo + s.alpha * s.Lc;  // the odometer path returns to x_k
@@ -2739,8 +2750,10 @@ __global__ void k_finalize_vert(Dev d, float inv_h) {
   TAC_PDL_WAIT();
   int e = blockIdx.x * 32 + threadIdx.x;
   if (e >= d.E) return;
-  bool failed = d.es[e].flags & (4 | 8);
-  float da = d.dalpha[e];
+  bool failed = d.es[e].flags & kFlagFailed;
+  // commit the last accepted iterate x_k: the last evaluated point moved back by a rejected
+  // trial's alpha (never the pending, unevaluated trial of the dalpha buffer)
+  float da = (float)d.es[e].back;
   for (int v = blockIdx.y * 8 + threadIdx.y; v < d.nv; v += gridDim.y * 8) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -2764,15 +2777,17 @@ __global__ void k_finalize_env(Dev d) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= d.E) return;
   EnvS& s = d.es[e];
-  if (s.flags & (4 | 8)) {
+  if (s.flags & kFlagFailed) {
     for (int i = 0; i < 3; ++i) s.c[i] = s.ct[i];
     for (int i = 0; i < 9; ++i) s.R[i] = s.Rt[i];
+  } else if (s.back != 0) {  // the last evaluation rejected its trial: x_k's pose
+    for (int i = 0; i < 3; ++i) s.ct[i] = s.c[i] = s.cp[i];
+    for (int i = 0; i < 9; ++i) s.Rt[i] = s.R[i] = s.Rp[i];
   } else {
     for (int i = 0; i < 3; ++i) s.ct[i] = s.c[i];
     for (int i = 0; i < 9; ++i) s.Rt[i] = s.R[i];
   }
-  if (s.mode == kActive) s.flags |= 2;
-  if (s.ncand_over) s.flags |= 32;
+  if (s.mode == kActive) s.flags |= kFlagMaxIt;
   s.ncand_max = max(s.ncand_max, d.ncand[e]);
   s.nanc_last = d.nanc[e];
   s.mode = kDone;
@@ -2783,7 +2798,7 @@ __global__ void k_finalize_env(Dev d) {
   mmT(s.R, s.Rs, RRs);
   const d3 phi = so3_log(RRs);
   s.pose_res = nrm(dc) + d.rho_max * nrm(phi);
-  if (d.pose_al && !(s.flags & (4 | 8))) {  // R29: lam += psi'(r) r/|r| at the step's solution
+  if (d.pose_al && !(s.flags & kFlagFailed)) {  // R29: lam += psi'(r) r/|r| at the step's solution
     const double wt = spring_w(nrm(dc), d.k_t, d.f_max), wr = spring_w(nrm(phi), d.k_r, d.t_max);
     s.lam[0] += wt * dc.x; s.lam[1] += wt * dc.y; s.lam[2] += wt * dc.z;
     s.lam[3] += wr * phi.x; s.lam[4] += wr * phi.y; s.lam[5] += wr * phi.z;
@@ -2894,6 +2909,12 @@ __global__ void k_any_active(Dev d, int* out) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   int a = (e < d.E && d.es[e].mode == kActive) ? 1 : 0;
   if (__any_sync(0xffffffffu, a) && (threadIdx.x & 31) == 0) atomicOr(out, 1);
+}
+
+struct Words8 { uint64_t w[8]; };
+__global__ void k_write_words(uint64_t* dst, Words8 v, int n) {
+  TAC_PDL_WAIT();
+  if (threadIdx.x < n) dst[threadIdx.x] = v.w[threadIdx.x];
 }
 
 // ------------------------------------------------------------------ launchers
@@ -3046,11 +3067,11 @@ void launch_eval(const Dev& d, double h, cudaStream_t s) {
     LAUNCHP(KID_ACCEPT, s, k_accept, eblocks32(d), 32, 0, d, h);
   }
 }
-void launch_direction(const Dev& d, cudaStream_t s) {
+void launch_direction(const Dev& d, cudaStream_t s, bool apply) {
   LAUNCHP(KID_DIR_REDUCE, s, k_dir_reduce, vgrid(d, d.nv), dim3(32, 8), 0, d);
   if (g_prof == nullptr) cudaStreamWaitEvent(s, d.ev_join, 0);  // k_accept on the side stream
   LAUNCHP(KID_DIR_SCALAR, s, k_dir_scalar, eblocks32(d), 32, 0, d);
-  LAUNCHP(KID_DIR_APPLY, s, k_dir_apply, vgrid(d, d.nv), dim3(32, 8), 0, d);
+  if (apply) LAUNCHP(KID_DIR_APPLY, s, k_dir_apply, vgrid(d, d.nv), dim3(32, 8), 0, d);
 }
 void launch_curvature(const Dev& d, double h, cudaStream_t s) {
   const bool fork = g_prof == nullptr;  // contact curvature concurrent with the element curvature
@@ -3103,6 +3124,12 @@ void launch_stats(const Dev& d, int4* out, cudaStream_t s) {
 }
 void launch_any_active(const Dev& d, int* out, cudaStream_t s) {
   LAUNCHP(KID_OTHER, s, k_any_active, eblocks(d), 128, 0, d, out);
+}
+void launch_write_words(const Dev& d, uint64_t* dst, const uint64_t* words, int n, cudaStream_t s) {
+  (void)d;
+  Words8 v{};
+  for (int i = 0; i < n && i < 8; ++i) v.w[i] = words[i];
+  LAUNCHP(KID_OTHER, s, k_write_words, 1, 32, 0, dst, v, n);
 }
 void launch_debug_broadphase(const Dev& d, double r, unsigned long long* out, int* cnt, int cap, cudaStream_t s) {
   int ntot = d.nsv + d.nse + d.nst;

@@ -76,10 +76,13 @@ def lib():
         L.tac_markers.argtypes = [vp, vp, C.c_int32, vp]
         L.tac_reset.argtypes = [vp, vp, vp, vp]
         L.tac_env_status.argtypes = [vp, vp, vp, vp, vp]
-        L.tac_set_env_material.argtypes = [vp, _dp, _dp, _dp, _dp]
+        L.tac_set_env_material.argtypes = [vp, _dp, _dp, _dp, _dp, vp]
         L.tac_marker_sqerr.argtypes = [vp, vp, vp, C.c_int32, vp]
         L.tac_set_pose_noise.argtypes = [vp, C.c_double, C.c_double, C.c_uint64, C.c_int64]
         L.tac_info.argtypes = [vp, _ip]
+        L.tac_checkpoint_size.argtypes = [vp, C.POINTER(C.c_uint64)]
+        L.tac_checkpoint_save.argtypes = [vp, vp, vp]
+        L.tac_checkpoint_load.argtypes = [vp, vp, vp]
         L.tac_nccl_unique_id.argtypes = [vp]
         L.tac_nccl_comm_create.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, C.POINTER(vp)]
         L.tac_nccl_comm_destroy.argtypes = [vp]
@@ -110,7 +113,8 @@ EXPORTED = ["tac_create", "tac_step", "tac_markers", "tac_reset", "tac_env_statu
             "tac_debug_broadphase", "tac_debug_surface", "tac_debug_marker_map", "tac_debug_eval",
             "tac_profile_enable", "tac_profile_read", "tac_profile_kernel_name", "tac_env_stats",
             "tac_set_env_material", "tac_marker_sqerr", "tac_set_pose_noise", "tac_nccl_unique_id",
-            "tac_nccl_comm_create", "tac_nccl_comm_destroy", "tac_gather_markers"]
+            "tac_nccl_comm_create", "tac_nccl_comm_destroy", "tac_gather_markers", "tac_checkpoint_size",
+            "tac_checkpoint_save", "tac_checkpoint_load"]
 N_KERNEL_IDS = 24
 
 
@@ -126,6 +130,22 @@ def _d(a):
 def _i(a):
     a = np.ascontiguousarray(a, dtype=np.int32)
     return a, a.ctypes.data_as(_ip)
+
+
+def _check_tensor(t, dtype, numel, device, name, at_least=False):
+    """Arguments of the C ABI are raw device pointers: refuse anything the kernels would read
+    as garbage (wrong dtype, host memory, another device, non-contiguous, wrong size)."""
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TacError(f"{name}: expected a torch.Tensor")
+    if t.dtype != dtype:
+        raise TacError(f"{name}: dtype {t.dtype}, expected {dtype}")
+    if not t.is_cuda or t.device.index != device:
+        raise TacError(f"{name}: must live on cuda:{device} (got {t.device})")
+    if not t.is_contiguous():
+        raise TacError(f"{name}: must be contiguous")
+    if (t.numel() < numel) if at_least else (t.numel() != numel):
+        raise TacError(f"{name}: {t.numel()} elements, expected {'>= ' if at_least else ''}{numel}")
 
 
 def _stream_ptr(stream):
@@ -206,7 +226,8 @@ class TacSim:
     # ---- hot path ----
     def step(self, target_poses, dt, stream=None):
         """target_poses: CUDA float32 tensor [n_envs, 7] (pose at t + dt)."""
-        assert target_poses.is_cuda and target_poses.dtype.is_floating_point and target_poses.is_contiguous()
+        import torch
+        _check_tensor(target_poses, torch.float32, 7 * self.n_envs, self.device, "target_poses")
         self._check(lib().tac_step(self.h, C.c_void_p(target_poses.data_ptr()), float(dt), _stream_ptr(stream)),
                     "tac_step")
 
@@ -214,15 +235,15 @@ class TacSim:
         import torch
         if out is None:
             out = torch.empty((self.n_envs, self.nm, ncomp), device=f"cuda:{self.device}", dtype=torch.float32)
-        assert out.is_cuda and out.is_contiguous() and out.numel() >= self.n_envs * self.nm * ncomp
+        _check_tensor(out, torch.float32, self.n_envs * self.nm * ncomp, self.device, "markers out", at_least=True)
         self._check(lib().tac_markers(self.h, C.c_void_p(out.data_ptr()), ncomp, _stream_ptr(stream)), "tac_markers")
         return out
 
     def gather_markers(self, comm, recvbuf, ncomp=2, stream=None):
         """tac_gather_markers: this rank's marker field into its slot of recvbuf (CUDA fp32
         [nranks * n_envs, n_markers, ncomp]) and an in-place NCCL all-gather of the slots."""
-        assert recvbuf.is_cuda and recvbuf.is_contiguous() and recvbuf.dtype.is_floating_point
-        assert recvbuf.numel() == comm.nranks * self.n_envs * self.nm * ncomp, "recvbuf size"
+        import torch
+        _check_tensor(recvbuf, torch.float32, comm.nranks * self.n_envs * self.nm * ncomp, self.device, "recvbuf")
         self._check(lib().tac_gather_markers(self.h, comm.handle, C.c_void_p(recvbuf.data_ptr()), ncomp,
                                              _stream_ptr(stream)), "tac_gather_markers")
         return recvbuf
@@ -235,17 +256,25 @@ class TacSim:
     def marker_sqerr(self, ref, acc, stream=None):
         """acc[e] += |markers(e) - ref[e]|^2 (calibration loss term, Eq. 6); ref [E, nm, ncomp] fp32,
         acc [E] fp64, both on this device."""
-        assert ref.is_cuda and ref.is_contiguous() and acc.is_cuda and acc.is_contiguous()
+        import torch
         ncomp = int(ref.shape[-1])
+        if ncomp not in (2, 3):
+            raise TacError("marker_sqerr: ref must be [n_envs, n_markers, 2 | 3]")
+        _check_tensor(ref, torch.float32, self.n_envs * self.nm * ncomp, self.device, "ref")
+        _check_tensor(acc, torch.float64, self.n_envs, self.device, "acc")
         self._check(lib().tac_marker_sqerr(self.h, C.c_void_p(ref.data_ptr()), C.c_void_p(acc.data_ptr()), ncomp,
                                            _stream_ptr(stream)), "tac_marker_sqerr")
         return acc
 
     def reset(self, mask, poses, stream=None):
+        """mask: CUDA uint8 [n_envs] (1 = reset), poses: CUDA float32 [n_envs, 7]."""
+        import torch
+        _check_tensor(mask, torch.uint8, self.n_envs, self.device, "mask")
+        _check_tensor(poses, torch.float32, 7 * self.n_envs, self.device, "poses")
         self._check(lib().tac_reset(self.h, C.c_void_p(mask.data_ptr()), C.c_void_p(poses.data_ptr()),
                                     _stream_ptr(stream)), "tac_reset")
 
-    def set_env_material(self, E=None, nu=None, rho=None, mu_f=None):
+    def set_env_material(self, E=None, nu=None, rho=None, mu_f=None, stream=None):
         """Per-env material theta_e: each argument None or n_envs values."""
         arrs = []
         for a in (E, nu, rho, mu_f):
@@ -254,7 +283,31 @@ class TacSim:
             else:
                 a = np.ascontiguousarray(np.broadcast_to(np.asarray(a, dtype=np.float64), (self.n_envs,)))
                 arrs.append((a, a.ctypes.data_as(_dp)))
-        self._check(lib().tac_set_env_material(self.h, *[p for _, p in arrs]), "tac_set_env_material")
+        self._check(lib().tac_set_env_material(self.h, *[p for _, p in arrs], _stream_ptr(stream)),
+                    "tac_set_env_material")
+
+    # ---- checkpoint / resume ----
+    def checkpoint_size(self):
+        n = C.c_uint64(0)
+        self._check(lib().tac_checkpoint_size(self.h, C.byref(n)), "tac_checkpoint_size")
+        return int(n.value)
+
+    def checkpoint_save(self, buf=None, stream=None):
+        """The carried state (u^t, v^t, per-env records, step counter) into a device uint8 buffer."""
+        import torch
+        n = self.checkpoint_size()
+        if buf is None:
+            buf = torch.empty(n, dtype=torch.uint8, device=f"cuda:{self.device}")
+        _check_tensor(buf, torch.uint8, n, self.device, "checkpoint buffer", at_least=True)
+        self._check(lib().tac_checkpoint_save(self.h, C.c_void_p(buf.data_ptr()), _stream_ptr(stream)),
+                    "tac_checkpoint_save")
+        return buf
+
+    def checkpoint_load(self, buf, stream=None):
+        import torch
+        _check_tensor(buf, torch.uint8, self.checkpoint_size(), self.device, "checkpoint buffer", at_least=True)
+        self._check(lib().tac_checkpoint_load(self.h, C.c_void_p(buf.data_ptr()), _stream_ptr(stream)),
+                    "tac_checkpoint_load")
 
     def env_status(self, stream=None):
         import torch

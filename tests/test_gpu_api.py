@@ -57,17 +57,22 @@ def test_reset_restores_rest_state_and_pose(torch):
     assert np.abs(m1[1] - m2[1]).max() <= 1e-4 * scale + 1e-12
 
 
-def test_candidate_overflow_is_flagged_not_fatal(torch):
-    """A candidate capacity far below the contact's needs sets flag 32 (overflow) and the
-    step still returns finite fields."""
+def test_candidate_overflow_fails_the_step_and_rolls_back(torch):
+    """A candidate capacity far below the contact's needs would drop pairs (the barrier and
+    the step bound would no longer see them): the step fails with flag 32 (overflow) and the
+    env is rolled back to its step-start state; the call itself succeeds and the fields stay
+    finite."""
     s = c1_press_scene(mu_f=1.0, steps=3, depth=0.3e-3)
     s.params.max_candidates = 16
     s.params.fixed_iters = 30
     sim = _sim(s)
     for k in range(3):
         sim.step(_poses(torch, s.poses[k]), s.dt)
-    it, pg, fl = sim.env_status()
-    assert int(fl[0]) & 32
+        it, pg, fl = sim.env_status()
+        assert int(fl[0]) & 32 and not int(fl[0]) & 1
+        u, v, c, R = sim.get_state(0)
+        assert np.all(u == 0) and np.all(v == 0)  # x^t = rest: every step rolled back
+        assert np.allclose(c, s.init_poses[0][:3], atol=1e-9)
     assert torch.isfinite(sim.markers()).all()
 
 
@@ -224,3 +229,38 @@ def test_reset_clears_pose_multipliers(torch):
     fresh.step(_poses(torch, s.poses[0]), s.dt)
     u1, u2 = sim.get_state(0)[0], fresh.get_state(0)[0]
     assert np.abs(u1 - u2).max() <= 1e-6 * 16e-3
+
+
+def test_checkpoint_resume_reproduces_the_steps(torch):
+    """tac_checkpoint_save / tac_checkpoint_load (SURVEY §5 checkpoint / resume): the marker
+    field right after a load equals the saved one bit for bit; stepping on from the loaded
+    state with the same targets reproduces the converged steps taken after the save (pose
+    noise included: the step counter keying the Philox streams, R27, is part of the
+    checkpoint); a checkpoint of a simulator of another size is refused."""
+    import paper_2603_28475_b200 as P
+    s = w.scene_small_peg(n_envs=5, n_steps=4)
+    s.params.tol_x = 1e-9
+    s.params.stagnation = 3000
+    sim = _sim(s)
+    sim.set_pose_noise(2e-5, 1e-3, 7)
+    sim.step(_poses(torch, s.poses[0]), s.dt)
+    ck = sim.checkpoint_save()
+    m_saved = sim.markers().clone()
+    for k in (1, 2):
+        sim.step(_poses(torch, s.poses[k]), s.dt)
+    a = [sim.get_state(e) for e in range(5)]
+    fa = sim.env_status()[2].cpu().numpy()
+    sim.checkpoint_load(ck)
+    assert torch.equal(sim.markers(), m_saved)
+    for k in (1, 2):
+        sim.step(_poses(torch, s.poses[k]), s.dt)
+    fb = sim.env_status()[2].cpu().numpy()
+    assert np.all(fa & 1) and np.all(fb & 1)
+    for e in range(5):
+        ub, _, cb, Rb = sim.get_state(e)
+        ua, _, ca, Ra = a[e]
+        assert np.abs(ua - ub).max() <= 1e-5 * 16e-3
+        assert np.abs(ca - cb).max() <= 1e-8 and np.abs(Ra - Rb).max() <= 1e-6
+    small = _sim(w.scene_small_peg(n_envs=3, n_steps=2))
+    with pytest.raises(P.TacError, match="size"):
+        small.checkpoint_load(ck)

@@ -348,8 +348,10 @@ def peg_trajectory(seed, n_steps=64, noise=True):
     """One env of the peg-insertion-shaped workload (C3): yaw ~ U[-35,35] deg
     (P:332), lateral offset ~ U[-3,3] mm, press depth ~ U[0.3,1.0] mm
     at <= 0.1 mm/step, then random-order shear / twist / partial-release phases,
-    per-step noise N(0,(0.01 mm)^2) and N(0,(0.05 deg)^2) (Table `random`,
-    P:693-694, scaled as stated in DESIGN.md)."""
+    repeated in cycles (a fresh press depth and phase order per cycle) until the last
+    n_steps // 10 steps, which lift the peg off (SURVEY §8d.1: ~10 % of the env-steps
+    out of contact, the rest in contact); per-step noise N(0,(0.01 mm)^2) and
+    N(0,(0.05 deg)^2) (Table `random`, scaled as stated in DESIGN.md)."""
     rng = np.random.Generator(np.random.PCG64(seed))
     rad = 4 * MM
     yaw = np.deg2rad(rng.uniform(-35, 35))
@@ -358,40 +360,51 @@ def peg_trajectory(seed, n_steps=64, noise=True):
     q0 = quat_axis_angle((0, 0, 1), yaw)
     lateral = np.array([-np.sin(yaw), np.cos(yaw), 0.0])
     c = lateral * off + np.array([0, 0, rad + 0.1 * MM])
+    c_start = c.copy()
     init = pose(c, q0)
     traj_c, traj_ang = [], []
     ang = 0.0
-    zt = rad - depth
-    while c[2] > zt + 1e-12:
-        c = c.copy()
-        c[2] = max(zt, c[2] - 0.1 * MM)
-        traj_c.append(c)
-        traj_ang.append(ang)
-    phases = ["shear", "twist", "release"]
-    rng.shuffle(phases)
-    for ph in phases:
-        if ph == "shear":
-            th = rng.uniform(0, 2 * np.pi)
-            d = np.array([np.cos(th), np.sin(th), 0.0])
-            step = rng.uniform(0.03, 0.1) * MM
-            for _ in range(rng.integers(5, 16)):
-                c = c + d * step
-                traj_c.append(c)
-                traj_ang.append(ang)
-        elif ph == "twist":
-            dang = np.deg2rad(rng.uniform(-0.5, 0.5))
-            for _ in range(rng.integers(4, 9)):
-                ang += dang
-                traj_c.append(c)
-                traj_ang.append(ang)
-        else:
-            up = rng.uniform(0.1, 0.6) * MM
-            n = int(np.ceil(up / (0.1 * MM)))
-            for _ in range(n):
-                c = c + (0, 0, up / n)
-                traj_c.append(c)
-                traj_ang.append(ang)
-    # lift-off: out of contact for the remaining steps (~10 % of env-steps)
+    n_tail = n_steps // 10
+    cycle = 0
+    while len(traj_c) < n_steps - n_tail:
+        if cycle > 0:
+            depth = rng.uniform(0.3, 1.0) * MM
+        zt = rad - depth
+        while abs(c[2] - zt) > 1e-12:  # press (or rise) to this cycle's depth at <= 0.1 mm/step
+            c = c.copy()
+            c[2] = max(zt, c[2] - 0.1 * MM) if c[2] > zt else min(zt, c[2] + 0.1 * MM)
+            traj_c.append(c)
+            traj_ang.append(ang)
+        phases = ["shear", "twist", "release"]
+        rng.shuffle(phases)
+        for ph in phases:
+            if ph == "shear":
+                th = rng.uniform(0, 2 * np.pi)
+                dxy = (c - c_start)[:2]
+                if cycle > 0 and np.linalg.norm(dxy) > 1.5 * MM:  # later cycles drift back toward the start
+                    th = np.arctan2(-dxy[1], -dxy[0]) + rng.uniform(-1.0, 1.0)
+                d = np.array([np.cos(th), np.sin(th), 0.0])
+                step = rng.uniform(0.03, 0.1) * MM
+                for _ in range(rng.integers(5, 16)):
+                    c = c + d * step
+                    traj_c.append(c)
+                    traj_ang.append(ang)
+            elif ph == "twist":
+                dang = np.deg2rad(rng.uniform(-0.5, 0.5))
+                for _ in range(rng.integers(4, 9)):
+                    ang += dang
+                    traj_c.append(c)
+                    traj_ang.append(ang)
+            else:  # partial release: 20-80 % of the current depth, the peg stays in contact
+                up = rng.uniform(0.2, 0.8) * (rad - c[2])
+                n = max(1, int(np.ceil(up / (0.1 * MM))))
+                for _ in range(n):
+                    c = c + (0, 0, up / n)
+                    traj_c.append(c)
+                    traj_ang.append(ang)
+        cycle += 1
+    del traj_c[n_steps - n_tail:], traj_ang[n_steps - n_tail:]
+    # lift-off tail: out of contact for the last n_tail steps once clear of the gel
     while len(traj_c) < n_steps:
         c = c.copy()
         c[2] = min(c[2] + 0.1 * MM, rad + 0.3 * MM)
