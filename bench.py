@@ -5,7 +5,9 @@
 
 One "step" = one pass of the whole hot path for every env
 of the rank: tac_step (fixed 50 PNCG iterations, the paper's "tens") +
-tac_markers.  Workload at N=1: BASELINE configs[2] (C3: 1,024 envs of peg-insertion
+tac_markers.  Timed window: steps [W, W+K) (default 16-63) from a
+checkpoint taken after the W warm-up steps; the per-kernel profile and e2e passes replay the
+same window from the same checkpoint.  Workload at N=1: BASELINE configs[2] (C3: 1,024 envs of peg-insertion
 trajectories on the 19,800-tet GelSight-Mini-like pad).  N>1 (torchrun): weak scaling,
 1,024 envs per GPU with distinct env ids, plus an NCCL all-gather of the marker fields
 every step (configs[3], C4).  Timing: CUDA events on the stream, barrier + synchronize
@@ -41,6 +43,8 @@ WORKLOADS = {
     "c5": "C5 stress: 103,680-tet / 19,943-vertex pad, sharp 8x8 mm square peg (face / edge press, slide, twist)",
     "c2": "C2: 1 env, GelSight-Mini-like 19,800-tet pad, R 5 mm icosphere: normal press + shear slide + retract, "
           "50 steps (latency-bound; ms_per_step is the step latency)",
+    "c1": "C1: 1 env, 288-tet pad, R 3 mm icosphere pressed 0.5 mm in one step from 0.2 mm above; every bench "
+          "step is that solve again from rest (tac_reset to the initial pose inside the timed region; latency)",
 }
 
 
@@ -54,6 +58,11 @@ def make_scene(config, n_envs, n_steps, seed0):
     if config == "c2":
         assert n_envs == 1, "C2 is a single-env config"
         return w.scene_c2(steps=n_steps)
+    if config == "c1":
+        assert n_envs == 1, "C1 is a single-env config"
+        s = w.scene_c1()
+        s.poses = np.repeat(s.poses[:1], n_steps, axis=0)  # the same press solved every step, from rest
+        return s
     return w.scene_c3(n_envs=n_envs, n_steps=n_steps, seed0=20260000 + seed0)
 
 
@@ -134,7 +143,7 @@ def run_ours(args, rank, local, ws):
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
     from paper_2603_28475_b200.dist import MarkerGather, NativeMarkerGather, env_range
-    nsteps = max(64, args.warmup + 3 * args.steps + 1)  # warm-up, timed, profiled pass, e2e
+    nsteps = max(64, args.warmup + args.steps)  # warm-up, then the timed window [W, W + K)
     if args.scaling == "strong":  # C4 strong: a fixed total split over the ranks
         e0, e1 = env_range(rank, ws, args.total_envs)
     else:  # weak: a fixed env count per GPU, distinct env ids per rank
@@ -161,6 +170,11 @@ def run_ours(args, rank, local, ws):
     mk = mg.slot  # this rank's slot of the gather buffer
     gather = mg if distributed else None
     stream = torch.cuda.current_stream()
+    # C1: every step solves the same press from rest (tac_reset of the env to its initial pose)
+    reset_all = args.config == "c1"
+    if reset_all:
+        rmask = torch.ones(E, dtype=torch.uint8, device=dev)
+        rposes = torch.tensor(scene.init_poses, dtype=torch.float32, device=dev).contiguous()
 
     def emit_markers():
         if native:
@@ -170,57 +184,69 @@ def run_ours(args, rank, local, ws):
         if gather is not None:
             gather.gather()
 
-    def one_step(k):
-        sim.step(poses[k], scene.dt)
+    def one_step(k, pose_k=None):
+        """One step of the hot path for every env of the rank; returns its kernel launches."""
+        if reset_all:
+            sim.reset(rmask, rposes)
+        sim.step(poses[k] if pose_k is None else pose_k, scene.dt)
+        n = sim.last_launch_count()
         emit_markers()
+        return n + sim.last_launch_count() + (2 if reset_all else 0)
 
-    launches = 0
+    import torch.distributed as dist
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist.is_initialized():
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if dist.is_initialized():
+            t = torch.tensor([x], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            x = float(t.item())
+        return x
+
     for k in range(args.warmup):
         one_step(k)
-    torch.cuda.synchronize()
-    import torch.distributed as dist
-    if dist.is_initialized():
-        dist.barrier()
+    # the state after warm-up: all three timed passes (headline, per-kernel profile, e2e)
+    # start from it and run the same window [W, W + K) of the trajectories
+    ckpt = sim.checkpoint_save()
+    window = range(args.warmup, args.warmup + args.steps)
+    barrier()
     clocks = Clocks(local)
-    torch.cuda.synchronize()
-    if dist.is_initialized():
-        dist.barrier()
+    barrier()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    # headline timed region: no per-launch events (they would add their own gaps)
+    # headline timed region: device-resident inputs, no per-launch events, no host syncs
+    launches = 0
     t0.record(stream)
-    iters_per_step = []
-    for k in range(args.warmup, args.warmup + args.steps):
-        sim.step(poses[k], scene.dt)
-        launches += sim.last_launch_count()
-        emit_markers()
-        launches += sim.last_launch_count()
-        if args.tol is not None:  # tolerance mode: per-env iteration counts of this step
-            iters_per_step.append(sim.env_status()[0])
-            launches += 1
+    for k in window:
+        launches += one_step(k)
     t1.record(stream)
-    torch.cuda.synchronize()
-    if dist.is_initialized():
-        dist.barrier()
+    barrier()
     cl = clocks.stop()
-    ms = t0.elapsed_time(t1)
-    if dist.is_initialized():  # max over ranks
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(t0.elapsed_time(t1))
     n_all = args.total_envs if args.scaling == "strong" else ws * E
     value = n_all * args.steps / (ms / 1e3)
 
-    # profiled timed pass over the next K steps: CUDA events around every launch on its
-    # stream give each kernel's live per-launch time (roofline, breakdown)
+    # profiled pass over the same window from the same state: CUDA events around every launch
+    # on its stream give each kernel's live per-launch time (roofline, breakdown); the per-step
+    # solver statistics of the window are read here (outside the headline timing)
+    sim.checkpoint_load(ckpt)
     sim.profile_enable(True)
     sim.profile_read()
-    torch.cuda.synchronize()
+    iters_per_step, stats_per_step, flags_per_step = [], [], []
+    barrier()
     t0.record(stream)
-    for k in range(args.warmup + args.steps, args.warmup + 2 * args.steps):
+    for k in window:
         one_step(k)
+        it_k, _, fl_k = sim.env_status()
+        iters_per_step.append(it_k)
+        flags_per_step.append(fl_k)
+        stats_per_step.append(sim.env_stats())
     t1.record(stream)
-    torch.cuda.synchronize()
+    barrier()
     pms = t0.elapsed_time(t1)
     prof = sim.profile_read()
     sim.profile_enable(False)
@@ -260,41 +286,29 @@ def run_ours(args, rank, local, ws):
         except Exception:
             pass
 
-    # e2e through the public API with host buffers (pinned), copies inside the timed region
+    # e2e through the public API with host buffers (pinned), copies inside the timed region,
+    # the same window from the same state again
     host_poses = torch.tensor(scene.poses, dtype=torch.float32).pin_memory()
     host_mk = torch.empty((E, nm, 2), dtype=torch.float32).pin_memory()
     dpose = torch.empty((E, 7), dtype=torch.float32, device=dev)
-    nsteps_e2e = min(args.steps, nsteps - args.warmup - 2 * args.steps) if nsteps - args.warmup - 2 * args.steps > 0 else args.steps
-    nsteps_e2e = max(1, nsteps_e2e)
-    # reset to the warm state cheaply: continue the trajectory (poses are continuous)
-    torch.cuda.synchronize()
-    if dist.is_initialized():
-        dist.barrier()
+    sim.checkpoint_load(ckpt)
+    barrier()
     w0 = time.perf_counter()
-    base = args.warmup + 2 * args.steps
-    for j in range(nsteps_e2e):
-        k = min(base + j, nsteps - 1)
+    for k in window:
         dpose.copy_(host_poses[k], non_blocking=True)
-        sim.step(dpose, scene.dt)
-        emit_markers()
+        one_step(k, dpose)
         host_mk.copy_(mk, non_blocking=True)
         torch.cuda.current_stream().synchronize()
     w1 = time.perf_counter()
-    e2e_s = w1 - w0
-    if dist.is_initialized():
-        t = torch.tensor([e2e_s], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e = {"value": round(n_all * nsteps_e2e / e2e_s, 2), "unit": "env-steps/s",
+    e2e_s = max_over_ranks(w1 - w0)
+    e2e = {"value": round(n_all * args.steps / e2e_s, 2), "unit": "env-steps/s",
            "h2d_bytes_per_step": E * 7 * 4, "d2h_bytes_per_step": E * nm * 2 * 4,
-           "timing": "wall clock, synchronize per step (result read on host)", "steps": nsteps_e2e}
+           "timing": "wall clock, steps [W, W+K) from the post-warm-up checkpoint, pinned poses H2D and marker "
+                     "field D2H every step, synchronize per step (result read on host)", "steps": args.steps}
 
-    it, pg, fl = sim.env_status()
-    stt = sim.env_stats().float()
-    if iters_per_step:
-        its = torch.stack(iters_per_step).float().flatten().cpu().numpy()
-    else:
-        its = np.full(E, float(args.iters))
+    its = torch.stack(iters_per_step).float().flatten().cpu().numpy()
+    stt = torch.stack(stats_per_step).float().reshape(-1, 4)
+    fls = torch.stack(flags_per_step).flatten()
     mean_it = float(its.mean())
     # whole-iteration HBM fraction (SURVEY §8d.2 "Reporting" 1): algorithmic bytes of one
     # PNCG iteration of one env (phases A + B + C per free vertex, static mesh amortised)
@@ -320,11 +334,17 @@ def run_ours(args, rank, local, ws):
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": cl,
-        "solver": {"mean_iters": mean_it, "p95_iters": float(np.percentile(its, 95)),
+        "solver": {"window": f"steps [{args.warmup}, {args.warmup + args.steps}) of every env (profiled pass from "
+                             "the same checkpoint)",
+                   "mean_iters": mean_it, "p95_iters": float(np.percentile(its, 95)),
                    "max_iters": float(its.max()), "mean_peak_candidates": float(stt[:, 1].mean()),
                    "max_peak_candidates": int(stt[:, 1].max()), "mean_anchors": float(stt[:, 2].mean()),
+                   "max_anchors": int(stt[:, 2].max()),
+                   "env_steps_with_anchors": round(float((stt[:, 2] > 0).float().mean()), 4),
                    "mean_rebuilds_per_step": float(stt[:, 3].mean()),
-                   "envs_flagged_overflow": int(((fl & 32) != 0).sum()), "envs_nan": int(((fl & 12) != 0).sum())},
+                   "converged_env_steps": int(((fls & 1) != 0).sum()),
+                   "overflow_env_steps": int(((fls & 32) != 0).sum()), "nan_env_steps": int(((fls & 12) != 0).sum()),
+                   "stagnated_env_steps": int(((fls & 64) != 0).sum())},
     }
     return out, scene, sim
 
@@ -382,13 +402,13 @@ def run_reference(args, rank, ws):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=48, help="timed steps (SURVEY §8d.1: steps 16-63)")
+    ap.add_argument("--warmup", type=int, default=16)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--envs", type=int, default=None, help="envs per GPU (default 1024; 256 for c5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
-    ap.add_argument("--config", default="c3", choices=["c3", "c3u", "c5", "c2"])
+    ap.add_argument("--config", default="c3", choices=["c3", "c3u", "c5", "c2", "c1"])
     ap.add_argument("--iters", type=int, default=FIXED_ITERS, help="fixed PNCG iterations per step (headline 50)")
     ap.add_argument("--tol", type=float, default=None, help="tolerance mode: tol_x [m] (SURVEY §8d.1: 1e-7)")
     ap.add_argument("--max-iters", type=int, default=2000, help="tolerance mode iteration cap")
@@ -396,7 +416,7 @@ def main():
     args = ap.parse_args()
     assert args.warmup >= 1 and args.iters >= 1
     if args.envs is None:
-        args.envs = {"c5": 256, "c2": 1}.get(args.config, ENVS_PER_GPU)
+        args.envs = {"c5": 256, "c2": 1, "c1": 1}.get(args.config, ENVS_PER_GPU)
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
         ws = int(os.environ.get("WORLD_SIZE", str(args.gpus)))

@@ -109,7 +109,8 @@ typedef struct {
  *   precond         0 3x3 block Jacobi, 1 scalar Jacobi P = diag(H)^-1; else TAC_EINVAL
  *   max_halvings    Armijo halvings before restarting along -P g
  *   stagnation      iterations without |P g| progress before giving up (0 = off)
- *   max_candidates  per-env capacity of candidate pairs (0 = default 16384)
+ *   max_candidates  per-env capacity of candidate pairs (0 = default 32768; an env that
+ *                   exceeds it fails its step, TAC_FLAG_OVERFLOW)
  *   max_anchors     per-env capacity of friction anchors (0 = default 4096; at most 16384)
  *   check_every     tolerance mode: host polls "all envs done" every N iterations
  *   pose_al         1: augmented-Lagrangian pose enforcement (R29): the pose

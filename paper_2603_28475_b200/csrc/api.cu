@@ -716,7 +716,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
   d.niv = niv; d.nie = (int)ies.size(); d.nit = nit; d.nm = nm;
   d.E = info->n_envs;
   d.Es = (d.E + 31) / 32 * 32;
-  d.kmax = P.max_candidates > 0 ? P.max_candidates : 16384;
+  d.kmax = P.max_candidates > 0 ? P.max_candidates : 32768;
   d.amax = P.max_anchors > 0 ? P.max_anchors : 4096;
   if (d.amax > 16384) {  // the per-step anchor sort holds next_pow2(max_anchors) keys in shared memory
     delete sim;

@@ -269,7 +269,7 @@ class Params:
     precond: int = 0        # 0 3x3 block Jacobi, 1 scalar Jacobi
     max_halvings: int = 10
     stagnation: int = 3000
-    max_candidates: int = 0   # 0 -> library default (16384 per env)
+    max_candidates: int = 0   # 0 -> library default (32768 per env)
     max_anchors: int = 0      # 0 -> library default (4096 per env)
     pose_al: int = 0          # 1: augmented-Lagrangian pose enforcement (R29)
     ee_mollifier: int = 0     # 1: IPC edge-edge parallel mollifier (R30)
