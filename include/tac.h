@@ -292,6 +292,20 @@ tac_status tac_debug_eval(tac_sim* sim, int32_t env, const double* u_t, const do
                           const double* target7, double dt, double* parts, double* g, double* D, double* grig,
                           double* Drig);
 
+/* One PNCG iteration's a6-a8 quantities (SURVEY §4 tier 2, kernel-level parity of the
+ * direction, curvature and step bounds): as tac_debug_eval at x_k = (u, c, R), then the
+ * direction from the previous iterate's gradient g_prev and direction p_prev ([n_verts*3 + 6]
+ * each: gel, then c, theta; fixed vertices ignored), gPg_prev = g_prev^T P_prev g_prev (used
+ * by the PR+ / FR rules) and restart != 0 (p = -P g), then the curvature and step-length
+ * kernels.  p_out [n_verts*3 + 6] = the new direction; out[12] = beta, g^T p, g^T P g,
+ * restarted (beta == 0), M = |p|_disp, alpha_upper, p^T H p, alpha_bar
+ * (P:461), alpha_ccd (R15), alpha (before the candidate-list cap of R16), L_rel,
+ * |P g|_disp.  Same kernels as tac_step; overwrites the env's state. */
+tac_status tac_debug_iteration(tac_sim* sim, int32_t env, const double* u_t, const double* v_t, const double* c_t,
+                               const double* R_t, const double* u, const double* c, const double* R,
+                               const double* target7, double dt, const double* g_prev, const double* p_prev,
+                               double gPg_prev, int32_t restart, double* p_out, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -60,6 +60,8 @@ def lib():
                               _ip, _ip]
         L.or_curvature.restype = C.c_double
         L.or_curvature.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, C.c_double]
+        L.or_iteration.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, C.c_double, _dp, _dp,
+                                   C.c_double, C.c_int, _dp, _dp]
         L.or_alpha_ccd.restype = C.c_double
         L.or_alpha_ccd.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _dp]
         L.or_broadphase_body.restype = C.c_int
@@ -308,6 +310,22 @@ class Oracle:
         dt = self.scene.dt if dt is None else dt
         ins = [_d(a) for a in (u_t, c_t, np.asarray(R_t).reshape(9), u, c, np.asarray(R).reshape(9), p, prig, target7)]
         return lib().or_curvature(self.h, *(a[1] for a in ins), dt)
+
+    ITERATION_FIELDS = ["beta", "gp", "gPg", "restarted", "M", "alpha_upper", "pHp", "alpha_bar", "alpha_ccd",
+                        "alpha", "L_rel", "pg_disp"]
+
+    def iteration(self, u_t, v_t, c_t, R_t, u, c, R, target7, g_prev, p_prev, gPg_prev, restart=False, dt=None):
+        """One PNCG iteration's a6-a8 quantities at x_k (O4b, O4d-O4f): the direction from the
+        previous gradient / direction ([nv*3 + 6] each, gel then c, theta) and the step length.
+        Returns (p [nv*3 + 6], dict of ITERATION_FIELDS)."""
+        dt = self.scene.dt if dt is None else dt
+        ins = [_d(a) for a in (u_t, v_t, c_t, np.asarray(R_t).reshape(9), u, c, np.asarray(R).reshape(9), target7,
+                                g_prev, p_prev)]
+        p = np.zeros(3 * self.nv + 6)
+        out = np.zeros(12)
+        lib().or_iteration(self.h, *(a[1] for a in ins[:8]), dt, ins[8][1], ins[9][1], float(gPg_prev), int(restart),
+                           p.ctypes.data_as(_dp), out.ctypes.data_as(_dp))
+        return p, dict(zip(self.ITERATION_FIELDS, out))
 
     def alpha_ccd(self, u, c, R, p, prig):
         ins = [_d(a) for a in (u, c, np.asarray(R).reshape(9), p, prig)]

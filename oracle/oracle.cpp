@@ -1038,6 +1038,60 @@ double rel_motion(const Problem& P, const Vecs& p) {
   return m + P.rho_max * norm(p.th);
 }
 
+// O4e: the search direction, Eq. (dk_direction), with the restarts of R12/R13:
+// p = -P g (restart) or -P g + beta p_prev; a non-descent direction restarts
+struct Direction {
+  Vecs p;
+  double beta, gp;  // beta used (0 on a restart), g^T p
+  bool restarted;
+};
+Direction direction(const Problem& P, const Grad& G, const Vecs& g, const Vecs& Pg, double gPg, const Vecs& gprev,
+                    const Vecs& pprev, double gPg_prev, bool restart) {
+  bool rs = restart;
+  double beta = 0;
+  if (!rs) {
+    Vecs y = vlin(P, 1.0, g, -1.0, gprev);
+    Vecs Py = apply_P(P, G, y);  // P_{k+1} y
+    double yp = vdot(P, y, pprev);
+    double ppn = vdot(P, pprev, pprev);
+    double scale = std::sqrt(vdot(P, g, g)) * std::sqrt(ppn);
+    if (std::fabs(yp) <= 1e-30 * scale) rs = true;
+    else beta = ncg_beta(P.beta_rule, vdot(P, g, Py), yp, vdot(P, y, Py), vdot(P, pprev, g), gPg, gPg_prev, ppn);
+    if (!std::isfinite(beta)) rs = true;
+  }
+  Direction D;
+  D.p = rs ? vlin(P, -1.0, Pg, 0.0, Pg) : vlin(P, -1.0, Pg, beta, pprev);
+  D.gp = vdot(P, g, D.p);
+  D.beta = rs ? 0.0 : beta;
+  if (D.gp >= 0) {  // non-descent -> restart
+    D.p = vlin(P, -1.0, Pg, 0.0, Pg);
+    D.gp = -gPg;
+    D.beta = 0;
+    rs = true;
+  }
+  D.restarted = rs;
+  return D;
+}
+
+// O4f: the step length, Eq. (step_size), alpha = min(alpha_upper, alpha_bar,
+// alpha_ccd (R15)); the candidate-list cap of R16 is applied by the caller
+struct StepLen {
+  double M, a_up, q, a_bar, a_ccd, alpha, Lrel;
+};
+StepLen step_length(const Problem& P, const Step& S, const State& s, const std::vector<Pair>& C, const Vecs& p,
+                    double gp) {
+  StepLen L;
+  L.M = disp_norm(P, p);
+  L.a_up = step_alpha_upper(P.dhat, L.M);
+  L.q = curvature(P, S, s, C, p.v, p.c, p.th);
+  L.a_bar = step_alpha_bar(gp, L.q);
+  L.a_ccd = alpha_ccd(P, s, C, p);
+  L.alpha = std::min(L.a_up, std::min(L.a_bar, L.a_ccd));
+  if (!std::isfinite(L.alpha)) L.alpha = 0;
+  L.Lrel = rel_motion(P, p);
+  return L;
+}
+
 double brute_dmin(const Problem& P, const State& s) {  // debug: all primitive pairs
   std::vector<Pair> all = broad_phase_state(P, s, INF);
   double m = INF;
@@ -1170,33 +1224,16 @@ void env_step(const Problem& P, Env& E, const double* target7, double h, const O
     if (it == K - 1) { E.pg = pgn; it = K; break; }
     // O4e: direction, Eq. (dk_direction)
     double gPg = vdot(P, g, Pg);
-    bool rs = restart || it == 0;
-    double beta = 0;
-    if (!rs) {
-      Vecs gpv = to_vecs(Gprev);
-      Vecs y = vlin(P, 1.0, g, -1.0, gpv);
-      Vecs Py = apply_P(P, G, y);  // P_{k+1} y
-      double yp = vdot(P, y, pprev);
-      double ppn = vdot(P, pprev, pprev);
-      double scale = std::sqrt(vdot(P, g, g)) * std::sqrt(ppn);
-      if (std::fabs(yp) <= 1e-30 * scale) rs = true;
-      else beta = ncg_beta(P.beta_rule, vdot(P, g, Py), yp, vdot(P, y, Py), vdot(P, pprev, g), gPg, gPg_prev, ppn);
-      if (!std::isfinite(beta)) rs = true;
-    }
-    p = rs ? vlin(P, -1.0, Pg, 0.0, Pg) : vlin(P, -1.0, Pg, beta, pprev);
-    double gp = vdot(P, g, p);
-    if (gp >= 0) { p = vlin(P, -1.0, Pg, 0.0, Pg); gp = -gPg; }  // non-descent -> restart
+    Direction Dn = direction(P, G, g, Pg, gPg, to_vecs(Gprev), pprev, gPg_prev, restart || it == 0);
+    p = Dn.p;
+    double gp = Dn.gp, beta = Dn.beta;
     restart = false;
     // O4f: step length, Eq. (step_size) P:459-461 + alpha_ccd (R15)
-    double M = disp_norm(P, p);
-    double a_up = step_alpha_upper(P.dhat, M);
-    double q = curvature(P, S, s, C, p.v, p.c, p.th);
-    double a_bar = step_alpha_bar(gp, q);
-    double a_ccd = alpha_ccd(P, s, C, p);
-    alpha = std::min(a_up, std::min(a_bar, a_ccd));
-    if (!std::isfinite(alpha)) alpha = 0;
+    StepLen SL = step_length(P, S, s, C, p, gp);
+    double M = SL.M, a_up = SL.a_up, q = SL.q, a_bar = SL.a_bar, a_ccd = SL.a_ccd;
+    alpha = SL.alpha;
     int rebuilt = 0;
-    Lrel = rel_motion(P, p);
+    Lrel = SL.Lrel;
     // R16: the list stays valid while the odometer <= m_r.  A step that would pass m_r is
     // capped at it; the list is rebuilt at the new state once the odometer passes
     // kRebuildAt * m_r (so a later cap never cuts a step below half of alpha_upper)
@@ -1496,6 +1533,65 @@ double or_curvature(void* h, const double* u_t, const double* ct, const double* 
   build_anchors(P, S, st, broad_phase_state(P, st, rad));
   std::vector<Pair> C = broad_phase_state(P, s, rad);
   return curvature(P, S, s, C, pv, V3{prig[0], prig[1], prig[2]}, V3{prig[3], prig[4], prig[5]});
+}
+// One PNCG iteration's a6-a8 quantities at x_k = (u, c, R) of a step that started at
+// (u_t, v_t, ct, Rt) with the given target: evaluation (O4b), |P g|_disp (O4d), the
+// direction from the previous iterate's gradient / direction (O4e) and the step length
+// (O4f, without the candidate-list cap of R16).  g_prev, p_prev: [nv*3 + 6] (gel, then c,
+// theta).  out_p: [nv*3 + 6].  out[12]: beta, g^T p, g^T P g, restarted, M, alpha_upper,
+// p^T H p, alpha_bar, alpha_ccd, alpha, L_rel, |P g|_disp.  (Test hook: kernel-level parity.)
+void or_iteration(void* h, const double* u_t, const double* v_t, const double* ct, const double* Rt, const double* u,
+                  const double* c, const double* R, const double* target7, double dt, const double* g_prev,
+                  const double* p_prev, double gPg_prev, int restart, double* out_p, double* out) {
+  Oracle* O = (Oracle*)h;
+  Problem& P = O->P;
+  Step S;
+  S.h = dt;
+  S.kappa = dt * dt * P.kappa_phys;
+  S.eps = P.eps_v * dt;
+  S.cs = {target7[0], target7[1], target7[2]};
+  S.Rs = quat_to_R(target7);
+  S.lam_t = O->eval_lam_t;
+  S.lam_r = O->eval_lam_r;
+  S.xhat_u.resize(P.nv);
+  State st, s;
+  st.u.resize(P.nv);
+  s.u.resize(P.nv);
+  Vecs gp, pp;
+  gp.v.resize(P.nv);
+  pp.v.resize(P.nv);
+  for (int v = 0; v < P.nv; ++v) {
+    V3 a{u_t[3 * v], u_t[3 * v + 1], u_t[3 * v + 2]}, b{v_t[3 * v], v_t[3 * v + 1], v_t[3 * v + 2]};
+    st.u[v] = a;
+    S.xhat_u[v] = P.fixed[v] ? V3{0, 0, 0} : add(a, scl(dt, b));
+    s.u[v] = {u[3 * v], u[3 * v + 1], u[3 * v + 2]};
+    gp.v[v] = P.fixed[v] ? V3{0, 0, 0} : V3{g_prev[3 * v], g_prev[3 * v + 1], g_prev[3 * v + 2]};
+    pp.v[v] = P.fixed[v] ? V3{0, 0, 0} : V3{p_prev[3 * v], p_prev[3 * v + 1], p_prev[3 * v + 2]};
+  }
+  const int o = 3 * P.nv;
+  gp.c = {g_prev[o], g_prev[o + 1], g_prev[o + 2]};
+  gp.th = {g_prev[o + 3], g_prev[o + 4], g_prev[o + 5]};
+  pp.c = {p_prev[o], p_prev[o + 1], p_prev[o + 2]};
+  pp.th = {p_prev[o + 3], p_prev[o + 4], p_prev[o + 5]};
+  st.c = {ct[0], ct[1], ct[2]};
+  s.c = {c[0], c[1], c[2]};
+  for (int i = 0; i < 9; ++i) { st.R[i] = Rt[i]; s.R[i] = R[i]; }
+  double rad = P.dhat + P.bp_margin;
+  build_anchors(P, S, st, broad_phase_state(P, st, rad));
+  std::vector<Pair> C = broad_phase_state(P, s, rad);
+  Grad G;
+  eval_energy(P, S, s, C, &G, nullptr);
+  Vecs g = to_vecs(G);
+  Vecs Pg = apply_P(P, G, g);
+  double gPg = vdot(P, g, Pg);
+  Direction Dn = direction(P, G, g, Pg, gPg, gp, pp, gPg_prev, restart != 0);
+  StepLen SL = step_length(P, S, s, C, Dn.p, Dn.gp);
+  for (int v = 0; v < P.nv; ++v)
+    for (int a = 0; a < 3; ++a) out_p[3 * v + a] = Dn.p.v[v][a];
+  for (int a = 0; a < 3; ++a) { out_p[o + a] = Dn.p.c[a]; out_p[o + 3 + a] = Dn.p.th[a]; }
+  const double r[12] = {Dn.beta, Dn.gp, gPg, Dn.restarted ? 1.0 : 0.0, SL.M, SL.a_up, SL.q, SL.a_bar, SL.a_ccd,
+                        SL.alpha, SL.Lrel, disp_norm(P, Pg)};
+  for (int k = 0; k < 12; ++k) out[k] = r[k];
 }
 // alpha_ccd over the candidates at (u, c, R) for direction p (R15)
 double or_alpha_ccd(void* h, const double* u, const double* c, const double* R, const double* p, const double* prig) {

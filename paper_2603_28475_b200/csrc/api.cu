@@ -746,6 +746,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     delete sim;
     return fail(TAC_EINVAL, "more than 65535 gel-surface or indenter vertices");
   }
+  d.contact_bps = getenv("TAC_CONTACT_BPS") ? std::max(1, atoi(getenv("TAC_CONTACT_BPS"))) : 16;
   d.contact_smem = contact_smem_bytes(d.nsv, niv);
   if (d.contact_smem == 0) {
     delete sim;
@@ -1619,6 +1620,44 @@ tac_status tac_debug_eval(tac_sim* sim, int32_t env, const double* u_t, const do
   if (Drig) for (int k = 0; k < 9; ++k) { Drig[k] = r.Dc[k]; Drig[9 + k] = r.Dth[k]; }
   if (parts) for (int k = 0; k < 5; ++k) parts[k] = r.Ep[k];
   return post_launch(sim);
+}
+
+tac_status tac_debug_iteration(tac_sim* sim, int32_t env, const double* u_t, const double* v_t, const double* c_t,
+                               const double* R_t, const double* u, const double* c, const double* R,
+                               const double* target7, double dt, const double* g_prev, const double* p_prev,
+                               double gPg_prev, int32_t restart, double* p_out, double* out) {
+  tac_status st = check_sim(sim);
+  if (st) return st;
+  if (env < 0 || env >= sim->d.E || !(dt > 0) || !g_prev || !p_prev || !p_out || !out) return TAC_EINVAL;
+  // evaluation at x_k (a4, a5, Armijo's first evaluation: accepted)
+  if ((st = tac_debug_eval(sim, env, u_t, v_t, c_t, R_t, u, c, R, target7, dt, nullptr, nullptr, nullptr, nullptr,
+                           nullptr)))
+    return st;
+  const Dev& d = sim->d;
+  const int nv = d.nv;
+  // the previous iterate's gradient and direction (fp32 vectors, fp64 rigid parts)
+  if ((st = scatter_vec(sim, d.gp, env, g_prev)) || (st = scatter_vec(sim, d.p, env, p_prev))) return st;
+  EnvS es;
+  CK(cudaMemcpy(&es, d.es + env, sizeof(EnvS), cudaMemcpyDeviceToHost));
+  for (int k = 0; k < 6; ++k) { es.grp[k] = g_prev[3 * nv + k]; es.pr[k] = p_prev[3 * nv + k]; }
+  es.gPg_prev = gPg_prev;
+  es.restart = restart ? 1 : 0;
+  es.iter = 2;  // not the step's first iteration
+  es.best_it = 2;
+  es.best_pg = INFINITY;
+  CK(cudaMemcpy(d.es + env, &es, sizeof(EnvS), cudaMemcpyHostToDevice));
+  launch_direction(d, 0);         // a6
+  launch_curvature(d, dt, 0);     // a7
+  launch_alpha(d, dt, 0);         // a7 / a8
+  CK(cudaDeviceSynchronize());
+  if ((st = post_launch(sim))) return st;
+  CK(cudaMemcpy(&es, d.es + env, sizeof(EnvS), cudaMemcpyDeviceToHost));
+  if ((st = gather_vec(sim, d.p, env, p_out))) return st;
+  for (int k = 0; k < 6; ++k) p_out[3 * nv + k] = es.pr[k];
+  const double r[12] = {es.beta, es.gp_prev, es.gPg_prev, es.beta == 0 ? 1.0 : 0.0, es.dbg[1], es.dbg[3], es.dbg[0],
+                        es.dbg[4], es.dbg[5], es.dbg[6], es.dbg[2], es.pg};
+  for (int k = 0; k < 12; ++k) out[k] = r[k];
+  return TAC_OK;
 }
 
 }  // extern "C"

@@ -58,6 +58,8 @@ struct EnvS {
   int cache_ok;               // candidate gap cache valid (same candidate list, classified once)
   int pad_cache;
   double Ep[5];                // energy parts of the last evaluation (diagnostics)
+  double dbg[7];               // k_alpha's last p^T H p, M, L_rel, alpha_upper, alpha_bar, alpha_ccd, alpha
+                               // before the candidate-list cap (diagnostics, tac_debug_iteration)
   int iter, halv, restart, reeval, mode, flags, best_it, accepted, rebuild, ncand_over;
   int ncand_max, nanc_last;   // per-step statistics (tac_env_stats)
 };
@@ -99,6 +101,7 @@ struct Dev {
   const int4* st;        // [nst]
   const int2* se_l;      // [nse] surface-local vertex indices
   const int4* st_l;      // [nst] surface-local vertex indices
+  int contact_bps;       // blocks per SM over the grid of the per-env contact passes (cgrid)
   int contact_smem;      // dynamic shared bytes of the staged contact kernels (0 = use the unstaged ones)
   cudaStream_t side, side2;  // per-simulator high-priority streams: the contact chain concurrent with the element pass
   cudaEvent_t ev_fork, ev_join, ev_cls, ev_join2;

@@ -2729,6 +2729,7 @@ __global__ void k_alpha(Dev d, double h) {
   double abar = q > 0 ? -s.gp_prev / q : INFINITY;
   double a = fmin(aup, fmin(abar, accd));
   if (!isfinite(a)) a = 0;
+  s.dbg[0] = q; s.dbg[1] = M; s.dbg[2] = L; s.dbg[3] = aup; s.dbg[4] = abar; s.dbg[5] = accd; s.dbg[6] = a;
   bool reb = false;
   if (L > 0 && s.S + a * L > kRebuildAt * d.bp_margin) {
     if (s.S + a * L > d.bp_margin) a = fmax(0.0, (d.bp_margin - s.S) / L);
@@ -2932,11 +2933,9 @@ static dim3 cellgrid(const Dev& d) {
   return vgrid(d, d.ncells, bps);
 }
 static dim3 cgrid(const Dev& d) {
-  // ~16 blocks of 128 threads per SM over the grid. 8/SM (one block per env at 1,024 envs) was
-  // +1.6 % on C3 in an interleaved A/B, but it changes the per-env summation order, and the
-  // full-size tolerance-mode parity test then drifted past its bound on one sampled env
-  // (4.8e-5 m vs 3.2e-6 m): kept at 16 until that sensitivity is understood
-  static const int tot = 148 * env_int("TAC_CONTACT_BPS", 16);
+  // ~contact_bps blocks of 128 threads per SM over the grid (per simulator: TAC_CONTACT_BPS at
+  // tac_create, default 16)
+  const int tot = 148 * d.contact_bps;
   int nb = std::max(1, std::min(64, tot / std::max(1, d.E)));
   return dim3(nb, d.E);
 }

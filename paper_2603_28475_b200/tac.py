@@ -104,6 +104,8 @@ def lib():
         L.tac_profile_kernel_name.restype = C.c_char_p
         L.tac_debug_eval.argtypes = [vp, C.c_int32, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, C.c_double, _dp, _dp,
                                      _dp, _dp, _dp]
+        L.tac_debug_iteration.argtypes = [vp, C.c_int32, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, C.c_double, _dp, _dp,
+                                          C.c_double, C.c_int32, _dp, _dp]
         _lib = L
     return _lib
 
@@ -114,7 +116,7 @@ EXPORTED = ["tac_create", "tac_step", "tac_markers", "tac_reset", "tac_env_statu
             "tac_profile_enable", "tac_profile_read", "tac_profile_kernel_name", "tac_env_stats",
             "tac_set_env_material", "tac_marker_sqerr", "tac_set_pose_noise", "tac_nccl_unique_id",
             "tac_nccl_comm_create", "tac_nccl_comm_destroy", "tac_gather_markers", "tac_checkpoint_size",
-            "tac_checkpoint_save", "tac_checkpoint_load"]
+            "tac_checkpoint_save", "tac_checkpoint_load", "tac_debug_iteration"]
 N_KERNEL_IDS = 24
 
 
@@ -382,6 +384,21 @@ class TacSim:
         self._check(lib().tac_debug_eval(self.h, env, *(a[1] for a in ins), float(dt),
                                          *(a.ctypes.data_as(_dp) for a in (parts, g, D, gr, Dr))), "tac_debug_eval")
         return dict(E=parts.sum(), parts=parts, g=g, D=D, grig=gr, Drig=Dr)
+
+    ITERATION_FIELDS = ["beta", "gp", "gPg", "restarted", "M", "alpha_upper", "pHp", "alpha_bar", "alpha_ccd",
+                        "alpha", "L_rel", "pg_disp"]
+
+    def debug_iteration(self, env, u_t, v_t, c_t, R_t, u, c, R, target7, dt, g_prev, p_prev, gPg_prev,
+                        restart=False):
+        """tac_debug_iteration: (p [nv*3 + 6], dict of ITERATION_FIELDS) of one PNCG iteration."""
+        ins = [_d(a) for a in (u_t, v_t, c_t, np.asarray(R_t).reshape(9), u, c, np.asarray(R).reshape(9), target7,
+                                g_prev, p_prev)]
+        p = np.zeros(3 * self.nv + 6)
+        out = np.zeros(12)
+        self._check(lib().tac_debug_iteration(self.h, env, *(a[1] for a in ins[:8]), float(dt), ins[8][1], ins[9][1],
+                                              float(gPg_prev), int(restart), p.ctypes.data_as(_dp),
+                                              out.ctypes.data_as(_dp)), "tac_debug_iteration")
+        return p, dict(zip(self.ITERATION_FIELDS, out))
 
 
 def nccl_unique_id() -> bytes:

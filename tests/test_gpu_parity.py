@@ -130,6 +130,34 @@ def test_broadphase_bitexact(torch_cuda, case):
             assert _canon(gpu, gsurf, s.tris) == _canon(ref, osurf, s.tris)
 
 
+EPS32 = 2.0 ** -24
+
+
+def _assert_eval_parity(s, o, ref, gpu, u_t, v_t, u):
+    """Kernel-level bars of SURVEY §8c (gradient and diagonal blocks <= 1e-5 relative, fp32),
+    applied element-wise: the gradient in norm, every free vertex's 3x3 block against its own
+    magnitude, the rigid gradient, and each energy part against its own value.  The inertia
+    part is a sum of m |u - u^|^2 with u^ = u^t + h v^t formed in fp32 on the device, so its bar
+    adds the propagated fp32 rounding of u^ and of u - u^ (a derived bound; at a state near
+    the prediction the part is a small difference of fp32 numbers)."""
+    free = np.setdiff1d(np.arange(len(u)), s.fixed)
+    g_ref, g_gpu = ref["g"][free], gpu["g"][free]
+    assert np.linalg.norm(g_gpu - g_ref) <= 1e-5 * np.linalg.norm(g_ref)
+    D_ref, D_gpu = ref["D"][free], gpu["D"][free]
+    blk = np.abs(D_gpu - D_ref).reshape(len(free), 9).max(axis=1)
+    scale = np.abs(D_ref).reshape(len(free), 9).max(axis=1)
+    assert np.all(blk <= 1e-5 * scale), (blk / scale).max()
+    assert np.linalg.norm(gpu["grig"] - ref["grig"]) <= 1e-5 * np.linalg.norm(ref["grig"])
+    m, _ = o.mass_vol()
+    uh = u_t + s.dt * v_t
+    du = (u - uh)[free]
+    in_bar = (m[free, None] * np.abs(du) * 4 * EPS32 * (np.abs(u_t) + s.dt * np.abs(v_t) + np.abs(u))[free]).sum()
+    assert abs(gpu["parts"][0] - ref["parts"][0]) <= 1e-5 * abs(ref["parts"][0]) + in_bar, (gpu["parts"][0], ref["parts"][0], in_bar)
+    for k in range(1, 5):
+        assert abs(gpu["parts"][k] - ref["parts"][k]) <= 1e-5 * abs(ref["parts"][k]) + 1e-30, \
+            (k, gpu["parts"][k], ref["parts"][k])
+
+
 def test_kernel_parity_gradient_diag(torch_cuda):
     s, o, (u_t, v_t, c_t, R_t), (u, c, R), tgt = _pressed_state()
     sim = _sim(s)
@@ -137,14 +165,78 @@ def test_kernel_parity_gradient_diag(torch_cuda):
     vt32 = v_t.astype(np.float32).astype(np.float64)
     ref = o.eval(ut32, vt32, c_t, R_t, u, c, R, tgt)
     gpu = sim.debug_eval(0, ut32, vt32, c_t, R_t, u, c, R, tgt, s.dt)
-    free = np.setdiff1d(np.arange(len(u)), s.fixed)
-    g_ref, g_gpu = ref["g"][free], gpu["g"][free]
-    assert np.linalg.norm(g_gpu - g_ref) <= 1e-5 * np.linalg.norm(g_ref)
-    D_ref, D_gpu = ref["D"][free], gpu["D"][free]
-    assert np.abs(D_gpu - D_ref).max() <= 1e-5 * np.abs(D_ref).max()
-    assert np.linalg.norm(gpu["grig"] - ref["grig"]) <= 1e-5 * np.linalg.norm(ref["grig"])
-    for k in range(5):
-        assert abs(gpu["parts"][k] - ref["parts"][k]) <= 1e-5 * abs(ref["E"]) + 1e-30, k
+    assert ref["parts"][2] > 0 and ref["parts"][3] > 0  # barrier and friction present
+    _assert_eval_parity(s, o, ref, gpu, ut32, vt32, u)
+
+
+def _iteration_inputs(s, o, st, x1, tgt):
+    """A realistic PNCG iteration for rows a6-a8: x_{k-1} = x1, the oracle's restart step from it
+    gives p_{k-1} and x_k = x_{k-1} + alpha p_{k-1} (O4g); everything the GPU stores in fp32 is
+    rounded to fp32 on both sides."""
+    u1, c1, R1 = x1
+    nv = len(u1)
+    r32 = lambda a: a.astype(np.float32).astype(np.float64)
+    zero = np.zeros(3 * nv + 6)
+    p1, it1 = o.iteration(*st, u1, c1, R1, tgt, zero, zero, 1.0, restart=True)
+    ev1 = o.eval(*st, u1, c1, R1, tgt)
+    g_prev = np.concatenate([r32(ev1["g"]).ravel(), ev1["grig"]])
+    p_prev = np.concatenate([r32(p1[:3 * nv]), p1[3 * nv:]])
+    a = it1["alpha"]
+    assert a > 0
+    u = r32(u1 + a * p_prev[:3 * nv].reshape(nv, 3))
+    u[s.fixed] = 0
+    c = c1 + a * p_prev[3 * nv:3 * nv + 3]
+    R = rot_exp(a * p_prev[3 * nv + 3:]) @ R1
+    return (u, c, R), g_prev, p_prev, it1["gPg"]
+
+
+def _rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+@pytest.mark.parametrize("beta_rule,precond", [(0, 0), (1, 0), (2, 0), (3, 0), (0, 1)])
+def test_kernel_parity_direction_curvature_step_bounds(torch_cuda, beta_rule, precond):
+    """Rows a6-a8 at kernel level on identical inputs (SURVEY §4 tier 2): the GPU's Dai-Kou beta
+    (and the PR+ / FR / DK+ variants, scalar Jacobi P:457), direction p, g^T p, |P g|_disp,
+    p^T H p, alpha_upper, alpha_bar, alpha_ccd (R15) and alpha vs the
+    oracle's at a C1 contact state with friction, for a restart (p = -P g) and a conjugate step.
+    Bars (derived from the kernel-level gradient bar): the gradient matches to 1e-5 of the force
+    level of the non-equilibrium state x_{k-1}; at x_k the error relative to g grows by
+    amp = sqrt(g_{k-1}^T P g_{k-1} / g_k^T P g_k), so e1 = 1e-5 amp on quantities linear in g
+    (p, |P g|, M, alpha_upper, L_rel), 2 e1 on quadratic ones (g^T P g, g^T p, p^T H p,
+    alpha_ccd), 3 e1 on beta and 4 e1 on alpha_bar = -g^T p / p^T H p and alpha."""
+    s, o, (u_t, v_t, c_t, R_t), x1, tgt = _pressed_state()
+    s.params.beta_rule = beta_rule
+    s.params.precond = precond
+    o = O.Oracle(s, params=s.params)
+    r32 = lambda a: a.astype(np.float32).astype(np.float64)
+    st = (r32(u_t), r32(v_t), c_t, R_t)
+    (u, c, R), g_prev, p_prev, gPg_prev = _iteration_inputs(s, o, st, x1, tgt)
+    sim = _sim(s)
+    nv = len(u)
+    free = np.setdiff1d(np.arange(nv), s.fixed)
+    for restart in (True, False):
+        p_o, r_o = o.iteration(*st, u, c, R, tgt, g_prev, p_prev, gPg_prev, restart=restart)
+        p_g, r_g = sim.debug_iteration(0, *st, u, c, R, tgt, s.dt, g_prev, p_prev, gPg_prev, restart=restart)
+        assert r_o["restarted"] == (1.0 if restart else 0.0) == r_g["restarted"], (restart, r_o, r_g)
+        # derived bar: the gradient at x_{k-1} matches to 1e-5 of its size (test above); at x_k,
+        # closer to equilibrium, the same absolute rounding is a larger share of the smaller g
+        amp = max(1.0, np.sqrt(gPg_prev / r_o["gPg"]))
+        e1 = 1e-5 * amp
+        if not restart:
+            assert r_o["beta"] != 0 and _rel(r_g["beta"], r_o["beta"]) <= 3 * e1, (r_g["beta"], r_o["beta"])
+        pv_o, pv_g = p_o[:3 * nv].reshape(nv, 3)[free], p_g[:3 * nv].reshape(nv, 3)[free]
+        assert np.abs(pv_g - pv_o).max() <= e1 * np.abs(pv_o).max()
+        # the rigid gradient is a sum of contact forces and the pose spring that nearly cancel
+        # near equilibrium: its rounding scales with the force level, i.e. with the previous
+        # (restart) direction's rigid part, not with the small remainder
+        rig_scale = max(np.abs(p_o[3 * nv:]).max(), np.abs(p_prev[3 * nv:]).max())
+        assert np.abs(p_g[3 * nv:] - p_o[3 * nv:]).max() <= e1 * rig_scale, (p_g[3 * nv:], p_o[3 * nv:], rig_scale)
+        for k, bar in (("pg_disp", e1), ("M", e1), ("alpha_upper", e1), ("L_rel", e1), ("gPg", 2 * e1),
+                       ("gp", 2 * e1), ("pHp", 2 * e1), ("alpha_ccd", 2 * e1), ("alpha_bar", 4 * e1),
+                       ("alpha", 4 * e1)):
+            assert np.isfinite(r_o[k]) and r_o[k] != 0 and _rel(r_g[k], r_o[k]) <= bar, (restart, k, r_g[k], r_o[k], bar)
+        assert r_o["pHp"] > 0 and r_o["alpha"] > 0
 
 
 def _run_both(scene, steps, tol_gpu=1e-9, tol_or=1e-11):
@@ -249,12 +341,7 @@ def test_ee_mollifier_kernel_and_converged_parity(torch_cuda):
     u32 = u.astype(np.float32).astype(np.float64)
     ref = o.eval(ut32, vt32, c_t, R_t, u32, c, R, tgt)
     gpu = sim.debug_eval(0, ut32, vt32, c_t, R_t, u32, c, R, tgt, s.dt)
-    free = np.setdiff1d(np.arange(len(u)), s.fixed)
-    g_ref, g_gpu = ref["g"][free], gpu["g"][free]
-    assert np.linalg.norm(g_gpu - g_ref) <= 1e-5 * np.linalg.norm(g_ref)
-    assert np.linalg.norm(gpu["grig"] - ref["grig"]) <= 1e-5 * np.linalg.norm(ref["grig"])
-    for k in range(5):
-        assert abs(gpu["parts"][k] - ref["parts"][k]) <= 1e-5 * abs(ref["E"]) + 1e-30, k
+    _assert_eval_parity(s, o, ref, gpu, ut32, vt32, u32)
     s2 = parallel_peg_scene(steps=3, depth=0.1e-3, offset_y=0.37e-3)
     s2.params.ee_mollifier = 1
     sim2, o2, mk = _run_both(s2, 3)
@@ -369,12 +456,8 @@ def test_full_size_c3_bench_config_sampled(torch_cuda):
         tgt = s.poses[5][e].astype(np.float64)
         ref = o.eval(u, v, c, R, u, c, R, tgt)
         gpu = sim.debug_eval(e, u, v, c, R, u, c, R, tgt, s.dt)
-        free = np.setdiff1d(np.arange(len(u)), s.fixed)
         assert ref["n_cand"] > 0
-        assert np.linalg.norm(gpu["g"][free] - ref["g"][free]) <= 1e-5 * np.linalg.norm(ref["g"][free])
-        assert np.abs(gpu["D"][free] - ref["D"][free]).max() <= 1e-5 * np.abs(ref["D"][free]).max()
-        assert np.linalg.norm(gpu["grig"] - ref["grig"]) <= 1e-5 * np.linalg.norm(ref["grig"])
-        assert abs(gpu["E"] - ref["E"]) <= 1e-5 * abs(ref["E"])
+        _assert_eval_parity(s, o, ref, gpu, u, v, u)
 
 
 def test_full_size_c3_converged_sampled(torch_cuda):
@@ -479,10 +562,7 @@ def test_c5_stress_bench_config_sampled(torch_cuda):
         tgt = s.poses[13][e].astype(np.float64)
         ref = o.eval(u, v, c, R, u, c, R, tgt)
         gpu = sim.debug_eval(e, u, v, c, R, u, c, R, tgt, s.dt)
-        free = np.setdiff1d(np.arange(len(u)), s.fixed)
-        assert np.linalg.norm(gpu["g"][free] - ref["g"][free]) <= 1e-5 * np.linalg.norm(ref["g"][free])
-        assert np.abs(gpu["D"][free] - ref["D"][free]).max() <= 1e-5 * np.abs(ref["D"][free]).max()
-        assert abs(gpu["E"] - ref["E"]) <= 1e-5 * abs(ref["E"])
+        _assert_eval_parity(s, o, ref, gpu, u, v, u)
 
 
 # ---------------------------------------------------------------- pose noise (R27)
