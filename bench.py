@@ -123,15 +123,16 @@ class Clocks:
                 "samples": len(rows)}
 
 
-# algorithmic work per launch (DESIGN.md §Kernels and roofline)
-def kernel_models(nv_free, nt, E):
+# algorithmic work per env-iteration (DESIGN.md §Kernels and roofline): a
+# kernel's work in the window = this x the env-iterations it processed (fixed mode: every env
+# every iteration; tolerance mode: the envs still iterating)
+def kernel_models(nv_free, nt):
     return {
-        "elem_grad": ("alu", 350.0 * nt * E, "flop", "350 flop per tet-env (SURVEY §8d.2 phase A)"),
-        "elem_curv": ("alu", 140.0 * nt * E, "flop", "140 flop per tet-env (phase C)"),
-        "vert_pre": ("hbm", 84.0 * nv_free * E, "B", "84 B per free vertex-env: read u,p,u^; write u,g,D"),
-        "dir_reduce": ("hbm", 60.0 * nv_free * E, "B", "60 B per free vertex-env: read g,g_prev,p,D"),
-        "dir_apply": ("hbm", 72.0 * nv_free * E, "B", "72 B per free vertex-env: read g,D,p; write p,g_prev"),
-        "finalize_vert": ("hbm", 48.0 * nv_free * E, "B", "48 B per vertex-env"),
+        "elem_grad": ("alu", 350.0 * nt, "flop", "350 flop per tet per env-iteration (SURVEY §8d.2 phase A)"),
+        "elem_curv": ("alu", 140.0 * nt, "flop", "140 flop per tet per env-iteration (phase C)"),
+        "vert_pre": ("hbm", 84.0 * nv_free, "B", "84 B per free vertex per env-iteration: read u,p,u^; write u,g,D"),
+        "dir_reduce": ("hbm", 60.0 * nv_free, "B", "60 B per free vertex per env-iteration: read g,g_prev,p,D"),
+        "dir_apply": ("hbm", 72.0 * nv_free, "B", "72 B per free vertex per env-iteration: read g,D,p; write p,g_prev"),
     }
 
 
@@ -184,14 +185,15 @@ def run_ours(args, rank, local, ws):
         if gather is not None:
             gather.gather()
 
-    def one_step(k, pose_k=None):
-        """One step of the hot path for every env of the rank; returns its kernel launches."""
+    def one_step(k, pose_k=None, count=False):
+        """One step of the hot path for every env of the rank; with `count`, returns its kernel
+        launches (tac_last_launch_count, which synchronises in tolerance mode)."""
         if reset_all:
             sim.reset(rmask, rposes)
         sim.step(poses[k] if pose_k is None else pose_k, scene.dt)
-        n = sim.last_launch_count()
+        n = sim.last_launch_count() if count else 0
         emit_markers()
-        return n + sim.last_launch_count() + (2 if reset_all else 0)
+        return n + sim.last_launch_count() + (2 if reset_all else 0) if count else 0
 
     import torch.distributed as dist
 
@@ -219,10 +221,9 @@ def run_ours(args, rank, local, ws):
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     # headline timed region: device-resident inputs, no per-launch events, no host syncs
-    launches = 0
     t0.record(stream)
     for k in window:
-        launches += one_step(k)
+        one_step(k)
     t1.record(stream)
     barrier()
     cl = clocks.stop()
@@ -237,10 +238,11 @@ def run_ours(args, rank, local, ws):
     sim.profile_enable(True)
     sim.profile_read()
     iters_per_step, stats_per_step, flags_per_step = [], [], []
+    launches = 0  # kernels of the window (the headline pass runs the same kernels)
     barrier()
     t0.record(stream)
     for k in window:
-        one_step(k)
+        launches += one_step(k, count=True)
         it_k, _, fl_k = sim.env_status()
         iters_per_step.append(it_k)
         flags_per_step.append(fl_k)
@@ -253,13 +255,20 @@ def run_ours(args, rank, local, ws):
 
     # roofline of the dominant kernel (live CUDA-event timing over the profiled pass)
     nfree = scene.X.shape[0] - len(scene.fixed)
-    models = kernel_models(nfree, scene.tets.shape[0], E)
+    models = kernel_models(nfree, scene.tets.shape[0])
+    # env-iterations of the profiled window (its per-step iteration counts): evaluations for the
+    # evaluation kernels; the step's last evaluation computes no direction or curvature (R31)
+    its_w = torch.stack(iters_per_step).float()
+    env_its = float(its_w.sum())
+    env_dirs = float((its_w - 1).clamp(min=0).sum())
     tot = {k: v for k, v in prof.items() if v[1] > 0}
     dom = max(tot, key=lambda k: tot[k][0])
     peaks, src = _peaks()
     share = {k: round(v[0] / pms, 4) for k, v in sorted(tot.items(), key=lambda kv: -kv[1][0])}
     dom_model = dom if dom in models else max((k for k in tot if k in models), key=lambda k: tot[k][0])
-    bound, work, wunit, note = models[dom_model]
+    bound, unit_work, wunit, note = models[dom_model]
+    n_units = env_its if dom_model in ("elem_grad", "vert_pre", "dir_reduce") else env_dirs
+    work = unit_work * n_units / tot[dom_model][1]  # per launch, averaged over the window
     avg_s = tot[dom_model][0] / tot[dom_model][1] / 1e3
     if bound == "hbm":
         achieved = work / avg_s / 1e9
@@ -272,7 +281,9 @@ def run_ours(args, rank, local, ws):
     roof = {"bound": bound, "kernel": dom_model, "achieved": round(achieved, 3), "peak": round(peak, 1),
             "unit": unit, "frac": round(achieved / peak, 4), "traffic": None,
             "peak_source": f"{src} ({'MEASURED_PEAKS.json hbm_gbs' if bound == 'hbm' else '148 SM x 128 FP32 lanes x 2 flop x sm_max_mhz'})",
-            "work_per_launch": work, "work_note": note, "avg_launch_us": round(avg_s * 1e6, 2),
+            "work_per_launch": work, "work_note": note + f"; {n_units:.0f} env-iterations over "
+                                                              f"{tot[dom_model][1]} launches in the window",
+            "avg_launch_us": round(avg_s * 1e6, 2),
             "dominant_by_time": dom, "share_of_step": share,
             "timing": f"per-launch CUDA events in a second timed pass of {args.steps} steps ({pms:.1f} ms, "
                       f"{pms / ms:.3f}x the unprofiled pass that gives value)",

@@ -240,7 +240,9 @@ tac_status tac_env_stats(tac_sim* sim, int32_t* out, void* stream);
  * n_other_tets (generic gradient). */
 tac_status tac_info(const tac_sim* sim, int32_t* out);
 
-/* Number of kernel launches issued by the last tac_step / tac_markers call. */
+/* Number of kernel launches issued by the last tac_step / tac_markers call.  In tolerance
+ * mode the iteration loop runs under device-side control (a CUDA-graph WHILE node); its trip
+ * count is then read back from the device, so this call synchronises the device. */
 int64_t tac_last_launch_count(const tac_sim* sim);
 
 /* Per-kernel timing (profiling hook used by bench.py for the roofline): when enabled,

@@ -78,6 +78,7 @@ def lib():
         L.or_dist_pt.argtypes = [_dp, _dp, _dp, _dp, _dp]
         L.or_dist_ee.restype = C.c_double
         L.or_dist_ee.argtypes = [_dp, _dp, _dp, _dp, _dp]
+        L.or_step_from.argtypes = [C.c_void_p, C.c_int, _dp, C.c_double, _dp, _dp, _dp]
         L.or_set_pose_noise.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_uint64, C.c_int64]
         L.or_philox.argtypes = [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
         L.or_certificate.restype = C.c_int
@@ -245,6 +246,14 @@ class Oracle:
     def step(self, targets, dt=None, threads=1, env0=0, n=0):
         targets, tp = _d(targets)
         lib().or_step(self.h, tp, float(self.scene.dt if dt is None else dt), threads, env0, n)
+
+    def step_from(self, env, target7, u0, c0, R0, dt=None):
+        """Env `env`'s step to target7 from its stored x^t, started at the feasible iterate
+        (u0, c0, R0) instead of x^t (anchors from x^t).  Test hook: polish another solver's
+        result -- a local minimiser of the step's potential stays where it is."""
+        ins = [_d(a) for a in (target7, u0, c0, np.asarray(R0).reshape(9))]
+        lib().or_step_from(self.h, int(env), ins[0][1], float(self.scene.dt if dt is None else dt), ins[1][1],
+                           ins[2][1], ins[3][1])
 
     def set_pose_noise(self, sigma_t, sigma_r, seed, env_offset=0):
         """Per-step target-pose noise (R27); one step() call = one step of the envs it covers."""

@@ -1138,8 +1138,10 @@ void build_anchors(const Problem& P, Step& S, const State& s, const std::vector<
   }
 }
 
+// x0: optional first iterate other than x^t (a feasible state of the same step, e.g. another
+// solver's result to be polished); the friction anchors stay those of x^t (R7)
 void env_step(const Problem& P, Env& E, const double* target7, double h, const Oracle* O = nullptr,
-              int64_t env_id = 0) {
+              int64_t env_id = 0, const State* x0 = nullptr) {
   Step S;
   S.h = h;
   S.kappa = h * h * P.kappa_phys;  // kappa = h^2 kappa_phys (R4)
@@ -1168,6 +1170,10 @@ void env_step(const Problem& P, Env& E, const double* target7, double h, const O
   const double mr = P.bp_margin, rad = P.dhat + P.bp_margin;
   std::vector<Pair> C = broad_phase_state(P, s, rad);
   build_anchors(P, S, s, C);
+  if (x0) {  // another first iterate: candidates at it, anchors from x^t
+    s = *x0;
+    C = broad_phase_state(P, s, rad);
+  }
   double Sacc = 0, Lrel = 0;
 
   Grad G, Gprev;
@@ -1404,6 +1410,19 @@ void or_step(void* h, const double* targets7, double dt, int n_threads, int env0
     });
   for (auto& x : th) x.join();
   O->step_count += 1;
+}
+// env `env`'s step from its stored x^t to `target7`, started at the feasible iterate
+// (u0, c0, R0) instead of x^t (test hook: polishing another solver's result to decide whether
+// it sits at a local minimiser of the same incremental potential)
+void or_step_from(void* h, int env, const double* target7, double dt, const double* u0, const double* c0,
+                  const double* R0) {
+  Oracle* O = (Oracle*)h;
+  State x0;
+  x0.u.resize(O->P.nv);
+  for (int v = 0; v < O->P.nv; ++v) x0.u[v] = {u0[3 * v], u0[3 * v + 1], u0[3 * v + 2]};
+  x0.c = {c0[0], c0[1], c0[2]};
+  for (int i = 0; i < 9; ++i) x0.R[i] = R0[i];
+  env_step(O->P, O->env[env], target7, dt, O, env, &x0);
 }
 void or_set_pose_noise(void* h, double sigma_t, double sigma_r, uint64_t seed, int64_t env_offset) {
   Oracle* O = (Oracle*)h;

@@ -61,6 +61,19 @@ struct tac_sim {
     unsigned long long used = 0;  // LRU stamp
   } graphs[4];
   unsigned long long graph_clock = 0;
+  // tolerance mode: one graph holding a WHILE node over (one PNCG iteration + k_loop_ctl), per
+  // (anchor buffer, h, budget); the loop runs on the device until no env iterates or the
+  // budget's last iteration is reached -- no host round trip inside a step
+  struct WhileGraph {
+    cudaGraphExec_t exec = nullptr;
+    const void* anc = nullptr;
+    double h = 0;
+    int K = 0;
+    long long launches_per_trip = 0;
+  } wgraphs[2];
+  bool use_while = true;     // TAC_NO_WHILE=1 at create: host-polled chunks instead (A/B)
+  int* d_loop = nullptr;     // [1] iterations run by the WHILE loop of the current step
+  long long while_per_trip = 0;  // launches per WHILE trip of the last step (0: no device loop)
   cudaStream_t cap = nullptr;  // capture stream (graphs are launched on the caller's stream)
   bool use_graphs = true;      // TAC_NO_GRAPH=1 at create disables (A/B measurements)
 };
@@ -763,6 +776,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
   sim->fixed_iters = P.fixed_iters;
   sim->check_every = P.check_every > 0 ? P.check_every : 25;
   if (getenv("TAC_NO_GRAPH")) sim->use_graphs = false;
+  if (getenv("TAC_NO_WHILE")) sim->use_while = false;
   if (getenv("TAC_TIMELINE") && P.fixed_iters > 0) {  // measurement only: direct launches
     sim->use_graphs = false;
     g_tl_iter = P.fixed_iters / 2;
@@ -917,17 +931,18 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     size_t nvec = 3 * (size_t)nv * d.Es;
     if ((rc = zalloc(sim, nvec, &d.u)) || (rc = zalloc(sim, nvec, &d.ut)) || (rc = zalloc(sim, nvec, &d.vt)) ||
         (rc = zalloc(sim, nvec, &d.uh)) || (rc = zalloc(sim, nvec, &d.g)) || (rc = zalloc(sim, nvec, &d.gp)) ||
-        (rc = zalloc(sim, nvec, &d.p)) || (rc = zalloc(sim, 2 * nvec, &d.D)) || (rc = zalloc(sim, (size_t)d.E, &d.es)) ||
+        (rc = zalloc(sim, nvec, &d.p)) || (rc = zalloc(sim, nvec, &d.Pg)) || (rc = zalloc(sim, 2 * nvec, &d.D)) || (rc = zalloc(sim, (size_t)d.E, &d.es)) ||
         (rc = zalloc(sim, 4 * (size_t)d.Es, &d.emat)) || (rc = zalloc(sim, 2 * (size_t)d.Es, &d.edbl)) ||
         (rc = zalloc(sim, (size_t)kNAcc * d.Es, &d.acc)) || (rc = zalloc(sim, (size_t)kNAccU * d.Es, &d.accu)) ||
         (rc = zalloc(sim, (size_t)d.Es, &d.dalpha)) || (rc = zalloc(sim, (size_t)d.Es, &d.beta)) ||
         (rc = zalloc(sim, (size_t)d.Es, &d.run)) || (rc = zalloc(sim, (size_t)d.Es, &d.pcf)) ||
         (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.cand)) || (rc = zalloc(sim, 2 * (size_t)d.E * d.kmax, &d.cgeo)) || (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.cgap)) || (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.ccorn)) || (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.ncorn)) || (rc = zalloc(sim, (size_t)d.E, &d.ncand)) || (rc = zalloc(sim, 3 * (size_t)d.E * d.kmax, &d.nearl)) ||
         (rc = zalloc(sim, 3 * (size_t)d.E, &d.nnear)) ||
+        (rc = zalloc(sim, 6 * (size_t)std::max(1, d.nsv) * d.Es, &d.Dcon)) ||
         (rc = zalloc(sim, (size_t)std::max(1, d.nsv) * d.Es, &d.usurf)) || (rc = zalloc(sim, (size_t)std::max(1, d.nsv) * d.Es, &d.psurf)) ||
         (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc)) || (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc2)) || (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc_f1)) || (rc = zalloc(sim, (size_t)d.E, &d.nanc)) || (rc = zalloc(sim, (size_t)d.E, &d.reb_list)) ||
         (rc = zalloc(sim, 1, &d.nreb)) ||
-        (rc = zalloc(sim, 1, &sim->d_flag)) || (rc = zalloc(sim, (size_t)d.kmax, &sim->d_dbg_cand)) ||
+        (rc = zalloc(sim, 1, &sim->d_flag)) || (rc = zalloc(sim, 1, &sim->d_loop)) || (rc = zalloc(sim, (size_t)d.kmax, &sim->d_dbg_cand)) ||
         (rc = zalloc(sim, 1, &sim->d_dbg_cnt)) || (rc = zalloc(sim, 3 * (size_t)nv, &sim->d_scratch)))
       goto fail;
     if (cudaMallocHost(&sim->h_flag, sizeof(int)) != cudaSuccess) { rc = TAC_ENOMEM; goto fail; }
@@ -1009,6 +1024,8 @@ tac_status tac_destroy(tac_sim* sim) {
   if (sim->d.side) { cudaStreamSynchronize(sim->d.side); cudaStreamDestroy(sim->d.side); }
   if (sim->d.side2) { cudaStreamSynchronize(sim->d.side2); cudaStreamDestroy(sim->d.side2); }
   for (auto& g : sim->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  for (auto& g : sim->wgraphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (sim->cap) cudaStreamDestroy(sim->cap);
   for (cudaEvent_t ev : {sim->d.ev_fork, sim->d.ev_join, sim->d.ev_cls, sim->d.ev_join2})
@@ -1113,6 +1130,63 @@ static bool run_iterations(tac_sim* sim, double h, int n, bool fin, cudaStream_t
   return cudaGraphLaunch(G->exec, s) == cudaSuccess;
 }
 
+// Tolerance mode's iteration loop on the device: a graph whose WHILE node runs (one PNCG
+// iteration + k_loop_ctl) until no env is active or K - 1 iterations have run.  Returns
+// false if conditional graphs are unavailable (the caller falls back to host-polled chunks).
+static bool run_while_loop(tac_sim* sim, double h, int K, cudaStream_t s) {
+  const Dev& d = sim->d;
+  tac_sim::WhileGraph* G = nullptr;
+  for (auto& g : sim->wgraphs)
+    if (g.exec && g.anc == (const void*)d.anc && g.h == h && g.K == K) G = &g;
+  if (!G) {
+    G = &sim->wgraphs[0];
+    for (auto& g : sim->wgraphs)
+      if (g.anc == (const void*)d.anc || !g.exec) { G = &g; break; }
+    if (G->exec) { cudaGraphExecDestroy(G->exec); G->exec = nullptr; }
+    cudaGraph_t gr = nullptr;
+    bool ok = cudaGraphCreate(&gr, 0) == cudaSuccess;
+    cudaGraphConditionalHandle hnd;
+    ok = ok && cudaGraphConditionalHandleCreate(&hnd, gr, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = hnd;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    ok = ok && cudaGraphAddNode(&node, gr, nullptr, 0, &cp) == cudaSuccess;
+    const long long l0 = g_launches;
+    if (ok) {
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      ok = cudaStreamBeginCaptureToGraph(sim->cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) ==
+           cudaSuccess;
+      if (ok) {
+        launch_iterations(d, h, 1, false, sim->cap);
+        launch_loop_ctl(d, hnd, sim->d_loop, K - 1, sim->cap);
+        cudaGraph_t out = nullptr;
+        ok = cudaStreamEndCapture(sim->cap, &out) == cudaSuccess;
+      }
+    }
+    ok = ok && cudaGraphInstantiateWithFlags(&G->exec, gr, cudaGraphInstantiateFlagUseNodePriority) == cudaSuccess;
+    if (gr) cudaGraphDestroy(gr);
+    G->launches_per_trip = g_launches - l0;
+    g_launches = l0;
+    if (!ok) {
+      cudaGetLastError();
+      if (G->exec) cudaGraphExecDestroy(G->exec);
+      *G = tac_sim::WhileGraph{};
+      sim->use_while = false;
+      if (getenv("TAC_GRAPH_DEBUG")) fprintf(stderr, "tac: WHILE-node graph unavailable, host-polled chunks\n");
+      return false;
+    }
+    G->anc = d.anc;
+    G->h = h;
+    G->K = K;
+  }
+  sim->while_per_trip = G->launches_per_trip;  // the trip count is only known on the device
+  if (cudaMemsetAsync(sim->d_loop, 0, sizeof(int), s) != cudaSuccess) return false;
+  return cudaGraphLaunch(G->exec, s) == cudaSuccess;
+}
+
 tac_status tac_step(tac_sim* sim, const float* target_poses, float dt, void* stream) {
   tac_status st = check_sim(sim);
   if (st) return st;
@@ -1122,6 +1196,7 @@ tac_status tac_step(tac_sim* sim, const float* target_poses, float dt, void* str
   const Dev& d = sim->d;
   double h = dt;
   g_launches = 0;
+  sim->while_per_trip = 0;
   g_prof = sim->prof;
   launch_step_setup(d, target_poses, h, sim->step_count++, s);  // a1
   cudaMemsetAsync(d.nreb, 0, sizeof(int), s);  // rebuilds flagged by the last step's final alpha are superseded
@@ -1130,6 +1205,16 @@ tac_status tac_step(tac_sim* sim, const float* target_poses, float dt, void* str
   launch_sort_anchors(d, sim->d.anc2, s);    // neighbouring anchors share gel corners (friction scatter)
   std::swap(sim->d.anc, sim->d.anc2);        // launches below read the sorted buffer
   int K = sim->fixed_iters > 0 ? sim->fixed_iters : sim->max_iters;
+  if (sim->fixed_iters == 0 && K > 1 && sim->use_while && sim->use_graphs && !sim->prof) {
+    // tolerance mode: K - 1 iterations under device-side control, then the final evaluation
+    if (run_while_loop(sim, h, K, s)) {
+      if (!run_iterations(sim, h, 1, true, s)) { g_prof = nullptr; return post_launch(sim); }
+      launch_finalize(d, h, s);  // a9
+      sim->launches = g_launches;
+      g_prof = nullptr;
+      return post_launch(sim);
+    }
+  }
   const int chunk = sim->fixed_iters > 0 ? K : std::min(K, sim->check_every);
   for (int it = 0; it < K;) {
     const int n = std::min(chunk, K - it);
@@ -1393,7 +1478,15 @@ tac_status tac_info(const tac_sim* sim, int32_t* out) {
   return TAC_OK;
 }
 
-int64_t tac_last_launch_count(const tac_sim* sim) { return sim ? sim->launches : 0; }
+int64_t tac_last_launch_count(const tac_sim* sim) {
+  if (!sim) return 0;
+  if (sim->while_per_trip == 0) return sim->launches;
+  // tolerance mode's device-side loop: its trip count is read back (synchronises the device)
+  int trips = 0;
+  cudaSetDevice(sim->device);
+  if (cudaMemcpy(&trips, sim->d_loop, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return sim->launches;
+  return sim->launches + (long long)trips * sim->while_per_trip;
+}
 
 tac_status tac_profile_enable(tac_sim* sim, int32_t on) {
   if (!sim) return TAC_EINVAL;
@@ -1605,14 +1698,25 @@ tac_status tac_debug_eval(tac_sim* sim, int32_t env, const double* u_t, const do
   EnvS r;
   CK(cudaMemcpy(&r, d.es + env, sizeof(EnvS), cudaMemcpyDeviceToHost));
   if (g && (st = gather_vec(sim, d.g, env, g))) return st;
-  if (D) {
-    std::vector<float> tmp(6 * (size_t)d.nv);
+  if (D) {  // elastic + inertia blocks, plus the surface vertices' contact blocks
+    std::vector<float> tmp(6 * (size_t)d.nv), tc(6 * (size_t)std::max(1, d.nsv));
     for (int c6 = 0; c6 < 6; ++c6)
       if ((st = copy_env_comp(sim, tmp.data() + (size_t)c6 * d.nv, d.D, env, c6, 6, true))) return st;
+    {
+      size_t pitch = sizeof(float) * (size_t)(d.Es / 32) * 6 * 32;
+      for (int c6 = 0; c6 < 6 && d.nsv > 0; ++c6) {
+        size_t off = ((size_t)(env / 32) * 6 + c6) * 32 + (env % 32);
+        CK(cudaMemcpy2D(tc.data() + (size_t)c6 * d.nsv, sizeof(float), d.Dcon + off, pitch, sizeof(float), d.nsv,
+                        cudaMemcpyDeviceToHost));
+      }
+    }
+    std::vector<int> sl(d.nv, -1);
+    for (size_t i = 0; i < sim->sv.size(); ++i) sl[sim->sv[i]] = (int)i;
     for (int v = 0; v < d.nv; ++v) {
-      float xx = tmp[v], yy = tmp[d.nv + v], zz = tmp[2 * d.nv + v], xy = tmp[3 * d.nv + v], xz = tmp[4 * d.nv + v],
-            yz = tmp[5 * d.nv + v];
-      double M[9] = {xx, xy, xz, xy, yy, yz, xz, yz, zz};
+      double q[6];
+      for (int c6 = 0; c6 < 6; ++c6)
+        q[c6] = (double)tmp[(size_t)c6 * d.nv + v] + (sl[v] >= 0 ? (double)tc[(size_t)c6 * d.nsv + sl[v]] : 0.0);
+      double M[9] = {q[0], q[3], q[4], q[3], q[1], q[5], q[4], q[5], q[2]};
       for (int k = 0; k < 9; ++k) D[9 * v + k] = M[k];
     }
   }

@@ -116,6 +116,11 @@ struct Dev {
   const float4* mk_w;    // [nm]
   // per-env vectors [c][nv][Es]
   float *u, *ut, *vt, *uh, *g, *gp, *p, *D;
+  float* Pg;             // [c][nv][Es] P g of the last direction reduction (k_dir_reduce -> k_dir_apply)
+  float* Dcon;           // [nsv][Es/32][6][32] contact Gauss-Newton blocks of the surface vertices (barrier +
+                         // friction), kept apart from D (elastic + inertia): a near-touching pair's block can
+                         // exceed the elastic one by ~1e8, beyond fp32's precision in a sum; the block-Jacobi
+                         // inverse forms D + Dcon in fp64 (R24)
   EnvS* es;              // [E]
   double* acc;           // [kNAcc][Es]
   unsigned* accu;        // [kNAccU][Es]
@@ -194,6 +199,7 @@ void launch_marker_sqerr(const Dev& d, const float* ref, double* acc, int ncomp,
 void launch_reset(const Dev& d, const unsigned char* mask, const float* poses, cudaStream_t s);
 void launch_status(const Dev& d, int* iters, float* pg, unsigned* flags, cudaStream_t s);
 void launch_any_active(const Dev& d, int* out, cudaStream_t s);
+void launch_loop_ctl(const Dev& d, cudaGraphConditionalHandle h, int* ctr, int limit, cudaStream_t s);
 void launch_write_words(const Dev& d, uint64_t* dst, const uint64_t* words, int n, cudaStream_t s);  // n <= 8
 void launch_stats(const Dev& d, int4* out, cudaStream_t s);
 // debug

@@ -39,6 +39,9 @@ __device__ __forceinline__ unsigned vidx(const Dev& d, int c, int v, int e) {  /
 __device__ __forceinline__ unsigned vidxD(const Dev& d, int c, int v, int e) {  // D: 6 components
   return (((unsigned)v * (unsigned)(d.Es >> 5) + ((unsigned)e >> 5)) * 6u + (unsigned)c) * 32u + ((unsigned)e & 31u);
 }
+__device__ __forceinline__ unsigned vidxS(const Dev& d, int c, int sl, int e) {  // Dcon: 6 per surface vertex
+  return (((unsigned)sl * (unsigned)(d.Es >> 5) + ((unsigned)e >> 5)) * 6u + (unsigned)c) * 32u + ((unsigned)e & 31u);
+}
 struct d3 {
   double x, y, z;
 };
@@ -930,7 +933,11 @@ __global__ void k_vert_pre(Dev d, float h2) {
         d.g[i] = m[t] * du;
         u[t][c] = uu;
       }
-      if (si[t] >= 0) d.usurf[(size_t)si[t] * d.Es + e] = make_float4(u[t][0], u[t][1], u[t][2], 0.f);
+      if (si[t] >= 0) {
+        d.usurf[(size_t)si[t] * d.Es + e] = make_float4(u[t][0], u[t][1], u[t][2], 0.f);
+#pragma unroll
+        for (int c = 0; c < 6; ++c) d.Dcon[vidxS(d, c, si[t], e)] = 0.f;
+      }
       const float dg = m[t] + h2 * sm[t];  // mass + state-independent elastic diagonal (App. B)
       d.D[vidxD(d, 0, v, e)] = dg;
       d.D[vidxD(d, 1, v, e)] = dg;
@@ -1590,17 +1597,18 @@ __device__ __forceinline__ void add_sym(double* A, d3 a, double s) {  // A(6) +=
   A[0] += s * a.x * a.x; A[1] += s * a.y * a.y; A[2] += s * a.z * a.z;
   A[3] += s * a.x * a.y; A[4] += s * a.x * a.z; A[5] += s * a.y * a.z;
 }
-__device__ __forceinline__ void scatter_gel_free(const Dev& d, int v, int e, d3 f, double s, d3 n) {
+// v: free gel vertex id (gradient), sl: its surface-local id (contact block, Dcon)
+__device__ __forceinline__ void scatter_gel_free(const Dev& d, int v, int sl, int e, d3 f, double s, d3 n) {
   atomicAdd(d.g + vidx(d, 0, v, e), (float)f.x);
   atomicAdd(d.g + vidx(d, 1, v, e), (float)f.y);
   atomicAdd(d.g + vidx(d, 2, v, e), (float)f.z);
   if (s != 0.0) {
-    atomicAdd(d.D + vidxD(d, 0, v, e), (float)(s * n.x * n.x));
-    atomicAdd(d.D + vidxD(d, 1, v, e), (float)(s * n.y * n.y));
-    atomicAdd(d.D + vidxD(d, 2, v, e), (float)(s * n.z * n.z));
-    atomicAdd(d.D + vidxD(d, 3, v, e), (float)(s * n.x * n.y));
-    atomicAdd(d.D + vidxD(d, 4, v, e), (float)(s * n.x * n.z));
-    atomicAdd(d.D + vidxD(d, 5, v, e), (float)(s * n.y * n.z));
+    atomicAdd(d.Dcon + vidxS(d, 0, sl, e), (float)(s * n.x * n.x));
+    atomicAdd(d.Dcon + vidxS(d, 1, sl, e), (float)(s * n.y * n.y));
+    atomicAdd(d.Dcon + vidxS(d, 2, sl, e), (float)(s * n.z * n.z));
+    atomicAdd(d.Dcon + vidxS(d, 3, sl, e), (float)(s * n.x * n.y));
+    atomicAdd(d.Dcon + vidxS(d, 4, sl, e), (float)(s * n.x * n.z));
+    atomicAdd(d.Dcon + vidxS(d, 5, sl, e), (float)(s * n.y * n.z));
   }
 }
 
@@ -1696,7 +1704,7 @@ __global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
       if (MOLL) f = f + bdm * Mo.dc[k];
       if (!ind[k]) {
         const int v = __ldg(d.svfree + id[k]);  // one load: id and fixed flag
-        if (v >= 0) scatter_gel_free(d, v, e, f, ddb * D.w[k] * D.w[k], nn);
+        if (v >= 0) scatter_gel_free(d, v, id[k], e, f, ddb * D.w[k] * D.w[k], nn);
       } else {
         d3 arm = z[k] - cc;
         d3 tq = cross(arm, f);
@@ -1743,8 +1751,9 @@ __device__ __forceinline__ void seg_red9(const Dev& d, int e, unsigned key, floa
   if (key == 0xffffffffu || (lane != 31 && next == key)) return;  // only the run's last lane
 #pragma unroll
   for (int c = 0; c < 3; ++c) atomicAdd(d.g + vidx(d, c, key, e), v[c]);
+  const int sl = __ldg(d.sidx + key);  // the contact block lives with the surface vertex
 #pragma unroll
-  for (int c = 0; c < 6; ++c) atomicAdd(d.D + vidxD(d, c, key, e), v[3 + c]);
+  for (int c = 0; c < 6; ++c) atomicAdd(d.Dcon + vidxS(d, c, sl, e), v[3 + c]);
 }
 
 // per-step anchor order: by (first, second) free gel corner, so anchors of one gel primitive
@@ -2387,7 +2396,7 @@ __global__ void k_accept(Dev d, double h) {
   s.iter += 1;
   d.dalpha[e] = 0.f;
   bool first = (s.iter == 1);
-  if (first && !isfinite(E)) {  // infeasible / NaN at the step start: roll back
+  if ((first || s.reeval) && !isfinite(E)) {  // infeasible / NaN at the step start or at x_k: roll back
     s.flags |= isfinite(Eb) ? kFlagNaN : kFlagInfeas;
     s.mode = kDone;
     d.run[e] = 0;
@@ -2438,22 +2447,35 @@ __global__ void k_accept(Dev d, double h) {
 
 // ------------------------------------------------------------------ a6: direction
 // P = 3x3 block inverse (default) or scalar Jacobi diag(H)^-1 (R9)
-__device__ __forceinline__ void precond(const float* D, int scalar, const float* x, float* y) {
+
+// P applied to two vectors (P g and P y share the block's inverse).  Surface vertices:
+// P = (D + Dcon)^-1 formed in fp64 (R24: the contact block may exceed the elastic one by
+// ~1e8); scalar Jacobi likewise from the fp64 diagonal.  Other vertices: fp32.
+__device__ __forceinline__ float rcp_(float x) { return 1.f / x; }
+__device__ __forceinline__ double rcp_(double x) { return __drcp_rn(x); }
+template <typename T>
+__device__ __forceinline__ void precond2(T a, T b, T c, T xy, T xz, T yz, int scalar, const float* x1, const float* x2,
+                                         float* y1, float* y2) {
   if (scalar) {
-    y[0] = x[0] / D[0]; y[1] = x[1] / D[1]; y[2] = x[2] / D[2];
+    const T ia = rcp_(a), ib = rcp_(b), ic = rcp_(c);
+    y1[0] = (float)(x1[0] * ia); y1[1] = (float)(x1[1] * ib); y1[2] = (float)(x1[2] * ic);
+    y2[0] = (float)(x2[0] * ia); y2[1] = (float)(x2[1] * ib); y2[2] = (float)(x2[2] * ic);
     return;
   }
-  // D = [xx xy xz; xy yy yz; xz yz zz] stored (xx, yy, zz, xy, xz, yz)
-  float a = D[0], b = D[1], c = D[2], xy = D[3], xz = D[4], yz = D[5];
-  float c00 = b * c - yz * yz, c01 = xz * yz - xy * c, c02 = xy * yz - b * xz;
-  float c11 = a * c - xz * xz, c12 = xy * xz - a * yz, c22 = a * b - xy * xy;
-  float inv = 1.f / (a * c00 + xy * c01 + xz * c02);
-  y[0] = inv * (c00 * x[0] + c01 * x[1] + c02 * x[2]);
-  y[1] = inv * (c01 * x[0] + c11 * x[1] + c12 * x[2]);
-  y[2] = inv * (c02 * x[0] + c12 * x[1] + c22 * x[2]);
+  const T c00 = b * c - yz * yz, c01 = xz * yz - xy * c, c02 = xy * yz - b * xz;
+  const T c11 = a * c - xz * xz, c12 = xy * xz - a * yz, c22 = a * b - xy * xy;
+  const T inv = rcp_(a * c00 + xy * c01 + xz * c02);
+  y1[0] = (float)(inv * (c00 * x1[0] + c01 * x1[1] + c02 * x1[2]));
+  y1[1] = (float)(inv * (c01 * x1[0] + c11 * x1[1] + c12 * x1[2]));
+  y1[2] = (float)(inv * (c02 * x1[0] + c12 * x1[1] + c22 * x1[2]));
+  y2[0] = (float)(inv * (c00 * x2[0] + c01 * x2[1] + c02 * x2[2]));
+  y2[1] = (float)(inv * (c01 * x2[0] + c11 * x2[1] + c12 * x2[2]));
+  y2[2] = (float)(inv * (c02 * x2[0] + c12 * x2[1] + c22 * x2[2]));
 }
 
-__global__ void __launch_bounds__(256) k_dir_reduce(Dev d) {
+constexpr int kDirNB = 1;  // vertices in flight per thread in k_dir_reduce: the fp64 surface block inverse
+                            // needs ~80 registers; 1 vertex x 3 blocks / SM measured 74 vs 82 us (2 x 2)
+__global__ void __launch_bounds__(256, 3) k_dir_reduce(Dev d) {
   TAC_PDL_WAIT();
   int e = blockIdx.x * 32 + threadIdx.x;
   bool act = e < d.E && (d.run[e] & 3);  // speculative: k_accept may run concurrently (see launch_eval)
@@ -2461,14 +2483,16 @@ __global__ void __launch_bounds__(256) k_dir_reduce(Dev d) {
   double gPy = 0, yp = 0, yPy = 0, pg = 0, gPg = 0, gg = 0, pp = 0;
   float pgmax = 0.f;
   const int stride = gridDim.y * 8;
-  for (int v0 = blockIdx.y * 8 + threadIdx.y; v0 < d.nv; v0 += 2 * stride) {  // two vertices in flight
-    float g[2][3], gq[2][3], p[2][3], D[2][6];
-    bool ok[2];
+  for (int v0 = blockIdx.y * 8 + threadIdx.y; v0 < d.nv; v0 += kDirNB * stride) {  // kDirNB vertices in flight
+    float g[kDirNB][3], gq[kDirNB][3], p[kDirNB][3], D[kDirNB][6];
+    int si[kDirNB];
+    bool ok[kDirNB];
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
+    for (int t = 0; t < kDirNB; ++t) {
       const int v = v0 + t * stride;
       ok[t] = act && v < d.nv && !(d.vflag[v] & 1);
       if (!ok[t]) continue;
+      si[t] = (d.vflag[v] & 2) ? d.sidx[v] : -1;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         g[t][c] = d.g[vidx(d, c, v, e)];
@@ -2479,13 +2503,26 @@ __global__ void __launch_bounds__(256) k_dir_reduce(Dev d) {
       for (int c = 0; c < 6; ++c) D[t][c] = d.D[vidxD(d, c, v, e)];
     }
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
+    for (int t = 0; t < kDirNB; ++t) {
       if (!ok[t]) continue;
       float y[3], Pg[3], Py[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) y[c] = g[t][c] - gq[t][c];
-      precond(D[t], d.precond, g[t], Pg);
-      precond(D[t], d.precond, y, Py);
+      if (si[t] >= 0) {  // contact block loaded here (fewer live registers than a prefetch)
+        const float* A = D[t];
+        float C[6];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) C[c] = d.Dcon[vidxS(d, c, si[t], e)];
+        precond2<double>((double)A[0] + C[0], (double)A[1] + C[1], (double)A[2] + C[2], (double)A[3] + C[3],
+                         (double)A[4] + C[4], (double)A[5] + C[5], d.precond, g[t], y, Pg, Py);
+      } else {
+        precond2<float>(D[t][0], D[t][1], D[t][2], D[t][3], D[t][4], D[t][5], d.precond, g[t], y, Pg, Py);
+      }
+      {  // P g for k_dir_apply (speculative like the dots: only accepted envs' values are used)
+        const int v = v0 + t * stride;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) d.Pg[vidx(d, c, v, e)] = Pg[c];
+      }
       const float* gv = g[t];
       const float* pv = p[t];
       gPy += gv[0] * Py[0] + gv[1] * Py[1] + gv[2] * Py[2];
@@ -2618,7 +2655,7 @@ __global__ void __launch_bounds__(256) k_dir_apply(Dev d) {
   double q = 0;
   const int stride = gridDim.y * 8;
   for (int v0 = blockIdx.y * 8 + threadIdx.y; v0 < d.nv; v0 += 2 * stride) {  // loads of two vertices first
-    float g[2][3], D[2][6], po[2][3], m[2];
+    float g[2][3], Pgv[2][3], po[2][3], m[2];
     int si[2];
     bool ok[2];
 #pragma unroll
@@ -2637,14 +2674,14 @@ __global__ void __launch_bounds__(256) k_dir_apply(Dev d) {
         po[t][c] = beta != 0.f ? d.p[vidx(d, c, v, e)] : 0.f;
       }
 #pragma unroll
-      for (int c = 0; c < 6; ++c) D[t][c] = d.D[vidxD(d, c, v, e)];
+      for (int c = 0; c < 3; ++c) Pgv[t][c] = d.Pg[vidx(d, c, v, e)];
     }
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
       if (!ok[t]) continue;
       const int v = v0 + t * stride;
-      float Pg[3], p[3];
-      precond(D[t], d.precond, g[t], Pg);
+      float p[3];
+      const float* Pg = Pgv[t];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const unsigned i = vidx(d, c, v, e);
@@ -2912,6 +2949,19 @@ __global__ void k_any_active(Dev d, int* out) {
   if (__any_sync(0xffffffffu, a) && (threadIdx.x & 31) == 0) atomicOr(out, 1);
 }
 
+// tolerance mode's device-side loop control (body of the CUDA-graph WHILE node, tac_step):
+// continue while any env is still iterating and fewer than `limit` iterations have run
+__global__ void __launch_bounds__(1024) k_loop_ctl(Dev d, cudaGraphConditionalHandle h, int* ctr, int limit) {
+  TAC_PDL_WAIT();
+  int a = 0;
+  for (int e = threadIdx.x; e < d.E; e += blockDim.x) a |= d.es[e].mode == kActive;
+  a = __syncthreads_or(a);
+  if (threadIdx.x == 0) {
+    const int c = ++(*ctr);
+    cudaGraphSetConditional(h, (a && c < limit) ? 1u : 0u);
+  }
+}
+
 struct Words8 { uint64_t w[8]; };
 __global__ void k_write_words(uint64_t* dst, Words8 v, int n) {
   TAC_PDL_WAIT();
@@ -3123,6 +3173,9 @@ void launch_stats(const Dev& d, int4* out, cudaStream_t s) {
 }
 void launch_any_active(const Dev& d, int* out, cudaStream_t s) {
   LAUNCHP(KID_OTHER, s, k_any_active, eblocks(d), 128, 0, d, out);
+}
+void launch_loop_ctl(const Dev& d, cudaGraphConditionalHandle h, int* ctr, int limit, cudaStream_t s) {
+  LAUNCHP(KID_OTHER, s, k_loop_ctl, 1, 1024, 0, d, h, ctr, limit);
 }
 void launch_write_words(const Dev& d, uint64_t* dst, const uint64_t* words, int n, cudaStream_t s) {
   (void)d;

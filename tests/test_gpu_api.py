@@ -264,3 +264,58 @@ def test_checkpoint_resume_reproduces_the_steps(torch):
     small = _sim(w.scene_small_peg(n_envs=3, n_steps=2))
     with pytest.raises(P.TacError, match="size"):
         small.checkpoint_load(ck)
+
+
+def test_tolerance_mode_device_loop_matches_host_polled(torch):
+    """Tolerance mode runs its iteration loop under device-side control (a CUDA-graph WHILE
+    node over one PNCG iteration + a loop-control kernel: no host round trip inside a step).
+    It converges every env to the same states as the host-polled chunked loop
+    (TAC_NO_WHILE=1, read at create), stops as soon as no env iterates, and the launch count
+    it reports covers the loop's device-side trips."""
+    import os
+    s = w.scene_small_peg(n_envs=5, n_steps=3)
+    s.params.tol_x = 1e-9
+    s.params.stagnation = 3000
+    a = _sim(s)
+    os.environ["TAC_NO_WHILE"] = "1"
+    try:
+        b = _sim(s)
+    finally:
+        del os.environ["TAC_NO_WHILE"]
+    for k in range(3):
+        a.step(_poses(torch, s.poses[k]), s.dt)
+        la = a.last_launch_count()
+        b.step(_poses(torch, s.poses[k]), s.dt)
+        lb = b.last_launch_count()
+        ia, _, fa = a.env_status()
+        ib, _, fb = b.env_status()
+        assert all(int(f) & 1 for f in fa) and all(int(f) & 1 for f in fb)
+        # the device loop runs exactly max(iterations) - 1 trips + the final evaluation; the
+        # host-polled loop rounds up to its 25-iteration chunks
+        assert la < lb + 50 and la > 15 * (int(ia.max()) - 2), (la, lb, int(ia.max()))
+    for e in range(5):
+        ua, ub = a.get_state(e)[0], b.get_state(e)[0]
+        assert np.abs(ua - ub).max() <= 1e-5 * 16e-3
+
+
+def test_tolerance_mode_c3_never_fails_or_overflows(torch):
+    """The bench's tolerance-mode configuration (C3, 1,024 envs, tol_x 1e-7 m, 2,000 iterations)
+    over 20 steps of press / shear / twist: no env step fails (NaN, infeasible, candidate
+    overflow) and no state goes non-finite.  (Round 1 saw NaN envs here: near-touching pairs
+    made the fp32 block-Jacobi inverse singular; the contact blocks now live apart from the
+    elastic ones and the inverse is formed in fp64 -- DESIGN.md R24.)"""
+    s = w.scene_c3(n_envs=1024, n_steps=20)
+    s.params.fixed_iters = 0
+    s.params.tol_x = 1e-7
+    s.params.max_iters = 2000
+    sim = _sim(s)
+    poses = _poses(torch, s.poses)
+    for k in range(20):
+        sim.step(poses[k], s.dt)
+        it, pg, fl = sim.env_status()
+        assert int(((fl & (4 | 8 | 32)) != 0).sum()) == 0, (k, np.nonzero((fl & 44).cpu().numpy())[0])
+        assert torch.isfinite(pg).all()
+    m = sim.markers()
+    assert torch.isfinite(m).all()
+    st = sim.env_stats().cpu().numpy()
+    assert st[:, 1].max() < 32768 and st[:, 2].mean() > 100
