@@ -759,7 +759,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     delete sim;
     return fail(TAC_EINVAL, "more than 65535 gel-surface or indenter vertices");
   }
-  d.contact_bps = getenv("TAC_CONTACT_BPS") ? std::max(1, atoi(getenv("TAC_CONTACT_BPS"))) : 16;
+  d.contact_bps = getenv("TAC_CONTACT_BPS") ? std::max(1, atoi(getenv("TAC_CONTACT_BPS"))) : 8;
   d.contact_smem = contact_smem_bytes(d.nsv, niv);
   if (d.contact_smem == 0) {
     delete sim;
@@ -936,7 +936,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
         (rc = zalloc(sim, (size_t)kNAcc * d.Es, &d.acc)) || (rc = zalloc(sim, (size_t)kNAccU * d.Es, &d.accu)) ||
         (rc = zalloc(sim, (size_t)d.Es, &d.dalpha)) || (rc = zalloc(sim, (size_t)d.Es, &d.beta)) ||
         (rc = zalloc(sim, (size_t)d.Es, &d.run)) || (rc = zalloc(sim, (size_t)d.Es, &d.pcf)) ||
-        (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.cand)) || (rc = zalloc(sim, 2 * (size_t)d.E * d.kmax, &d.cgeo)) || (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.cgap)) || (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.ccorn)) || (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.ncorn)) || (rc = zalloc(sim, (size_t)d.E, &d.ncand)) || (rc = zalloc(sim, 3 * (size_t)d.E * d.kmax, &d.nearl)) ||
+        (rc = zalloc(sim, 2 * (size_t)d.E * d.kmax, &d.cand)) || (rc = zalloc(sim, (size_t)d.E, &d.lbuf)) || (rc = zalloc(sim, 2 * (size_t)d.E * d.kmax, &d.cgeo)) || (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.cgap)) || (rc = zalloc(sim, 2 * (size_t)d.E * d.kmax, &d.ccorn)) || (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.ncorn)) || (rc = zalloc(sim, 2 * (size_t)d.E, &d.ncand)) || (rc = zalloc(sim, 3 * (size_t)d.E * d.kmax, &d.nearl)) ||
         (rc = zalloc(sim, 3 * (size_t)d.E, &d.nnear)) ||
         (rc = zalloc(sim, 6 * (size_t)std::max(1, d.nsv) * d.Es, &d.Dcon)) ||
         (rc = zalloc(sim, (size_t)std::max(1, d.nsv) * d.Es, &d.usurf)) || (rc = zalloc(sim, (size_t)std::max(1, d.nsv) * d.Es, &d.psurf)) ||
@@ -951,6 +951,8 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
     if (cudaStreamCreateWithPriority(&d.side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&d.side2, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&d.side3, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d.ev_reb, cudaEventDisableTiming) != cudaSuccess ||
         cudaStreamCreateWithFlags(&sim->cap, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&d.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&d.ev_cls, cudaEventDisableTiming) != cudaSuccess ||
@@ -1004,7 +1006,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     if (cudaMemcpy(d.es, es.data(), sizeof(EnvS) * d.E, cudaMemcpyHostToDevice) != cudaSuccess) { rc = TAC_ECUDA; goto fail; }
     cudaMemset(d.acc, 0, sizeof(double) * kNAcc * d.Es);
     cudaMemset(d.run, 0, sizeof(int) * d.Es);
-    cudaMemset(d.ncand, 0, sizeof(int) * d.E);
+    cudaMemset(d.ncand, 0, sizeof(int) * 2 * d.E);
     cudaMemset(d.u, 0, sizeof(float) * nvec);
     cudaMemset(d.g, 0, sizeof(float) * nvec);
     cudaMemset(d.D, 0, sizeof(float) * 2 * nvec);
@@ -1023,12 +1025,13 @@ tac_status tac_destroy(tac_sim* sim) {
   cudaSetDevice(sim->device);
   if (sim->d.side) { cudaStreamSynchronize(sim->d.side); cudaStreamDestroy(sim->d.side); }
   if (sim->d.side2) { cudaStreamSynchronize(sim->d.side2); cudaStreamDestroy(sim->d.side2); }
+  if (sim->d.side3) { cudaStreamSynchronize(sim->d.side3); cudaStreamDestroy(sim->d.side3); }
   for (auto& g : sim->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   for (auto& g : sim->wgraphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (sim->cap) cudaStreamDestroy(sim->cap);
-  for (cudaEvent_t ev : {sim->d.ev_fork, sim->d.ev_join, sim->d.ev_cls, sim->d.ev_join2})
+  for (cudaEvent_t ev : {sim->d.ev_fork, sim->d.ev_join, sim->d.ev_cls, sim->d.ev_join2, sim->d.ev_reb})
     if (ev) cudaEventDestroy(ev);
   for (void* p : sim->allocs) cudaFree(p);
   if (sim->h_flag) cudaFreeHost(sim->h_flag);
@@ -1065,6 +1068,7 @@ static void launch_iterations(const Dev& d, double h, int n, bool fin, cudaStrea
     launch_eval(d, h, s);       // a4 + a5 + Armijo (a8)
     if (fin && it == n - 1) {
       launch_direction(d, s, false);  // a8 convergence test
+      if (g_prof == nullptr) cudaStreamWaitEvent(s, d.ev_reb, 0);  // join the pipelined rebuild (R16)
       break;
     }
     launch_direction(d, s);     // a6
@@ -1689,6 +1693,7 @@ tac_status tac_debug_eval(tac_sim* sim, int32_t env, const double* u_t, const do
   launch_anchors(d, dt, 0);
   // move to the evaluation state (u, c, R) and rebuild the candidates there
   if ((st = scatter_vec(sim, d.u, env, u)) || (st = set_pose_current(sim, env, c, R))) return st;
+  CK(cudaMemset(d.lbuf + env, 0, sizeof(int)));  // active buffer 0
   CK(cudaMemset(d.ncand + env, 0, sizeof(int)));
   launch_broadphase(d, false, 0);
   CK(cudaMemset(d.nreb, 0, sizeof(int)));

@@ -49,6 +49,11 @@ struct EnvS {
   double E, Eprev, alpha, gp_prev, gPg_prev, S, beta, best_pg, pg, pose_res;
   double wt_acc, wr_acc;       // pose-spring weights psi'(r)/r at the last accepted point (k_alpha's curvature)
   double lam[6];               // pose multipliers (lam_t [N], lam_r [N m]) of the AL pose term (R29)
+  double S2;                   // odometer of the pending candidate list since its build point (R16 pipeline)
+  double cb[3], Rb[9];         // pose at the pending list's build point (the trial it is built at)
+  int pending;                 // a candidate list is being rebuilt for this env (built during the
+                               // evaluation after k_alpha listed it, activated by the vertex pre-pass after)
+  int reb_iter;                // s.iter when it was listed
   double back;                 // u moves by back * p from the last evaluated point to the last accepted
                                // iterate x_k: 0 after an acceptance, -alpha of the rejected trial otherwise
                                // (a step that ends without converging commits x_k, never a trial)
@@ -104,7 +109,8 @@ struct Dev {
   int contact_bps;       // blocks per SM over the grid of the per-env contact passes (cgrid)
   int contact_smem;      // dynamic shared bytes of the staged contact kernels (0 = use the unstaged ones)
   cudaStream_t side, side2;  // per-simulator high-priority streams: the contact chain concurrent with the element pass
-  cudaEvent_t ev_fork, ev_join, ev_cls, ev_join2;
+  cudaStream_t side3;        // the pipelined candidate rebuild (off the evaluation's critical path)
+  cudaEvent_t ev_fork, ev_join, ev_cls, ev_join2, ev_reb;
   const float4* Y;       // [niv] body frame, w = |Y|
   const int2* ie;        // [nie]
   const int4* it;        // [nit]
@@ -128,13 +134,15 @@ struct Dev {
   float* beta;           // [Es]
   int* run;              // [Es] bit0 evaluate, bit1 direction, bit2 rebuild
   float4* pcf;           // [Es] rigid p_c (float) for L_rel
-  unsigned long long* cand;  // [E][kmax] (kind<<62 | a<<31 | b)
-  uint2* ccorn;           // [E][kmax] corner ids of each candidate, 4 x 16 bit (gel: surface-local id,
+  unsigned long long* cand;  // [2][E][kmax] (kind<<62 | a<<31 | b): two lists per env, lbuf[e] the active one,
+                             // the other receives the pipelined in-loop rebuild (R16)
+  uint2* ccorn;           // [2][E][kmax] corner ids of each candidate, 4 x 16 bit (gel: surface-local id,
                          // indenter: vertex id), written with the candidate list
+  int* lbuf;             // [E] active candidate buffer (0 / 1)
   float* cgap;            // [E][kmax] certified axis gap + odometer at certification (rounded down)
   float4* cgeo;          // [E][kmax][2] near-pair geometry (d, n), (w0..w3) in near order: kinds 0, 1, 2 concatenated
   uint2* ncorn;          // [E][kmax] the near pairs' packed corner ids, same order as cgeo
-  int* ncand;            // [E]
+  int* ncand;            // [2][E] candidates per buffer
   uint2* nearl;          // [E][3][kmax] packed corner ids of the near candidates (no far certificate), per pair kind
   int* nnear;            // [E][3]
   const int* sidx;       // [nv] surface-local index of a gel vertex, -1 if not on the surface

@@ -42,6 +42,8 @@ __device__ __forceinline__ unsigned vidxD(const Dev& d, int c, int v, int e) {  
 __device__ __forceinline__ unsigned vidxS(const Dev& d, int c, int sl, int e) {  // Dcon: 6 per surface vertex
   return (((unsigned)sl * (unsigned)(d.Es >> 5) + ((unsigned)e >> 5)) * 6u + (unsigned)c) * 32u + ((unsigned)e & 31u);
 }
+// candidate list of env e in buffer b (R16 double buffering)
+__device__ __forceinline__ size_t cand_off(const Dev& d, int b, int e) { return ((size_t)b * d.E + e) * d.kmax; }
 struct d3 {
   double x, y, z;
 };
@@ -538,14 +540,14 @@ __global__ void k_step_setup(Dev d, const float* poses, unsigned long long step)
   d3 dc = ld3(s.cs) - ld3(s.ct);
   s.flags = (nrm(dc) > 2e-3 || nrm(so3_log(RRt)) > 5 * M_PI / 180) ? 16 : 0;
   s.iter = 0; s.halv = 0; s.restart = 1; s.reeval = 0; s.mode = kActive; s.best_it = 0; s.accepted = 0;
-  s.rebuild = 0; s.ncand_over = 0; s.ncand_max = 0; s.nanc_last = 0;
+  s.rebuild = 0; s.ncand_over = 0; s.ncand_max = 0; s.nanc_last = 0; s.pending = 0; s.S2 = 0;
   s.odo = 0; s.odo_base = 0; s.Lc = 0; s.cache_ok = 0;
   s.alpha = 0; s.back = 0; s.S = 0; s.best_pg = INFINITY; s.pg = 0; s.E = 0; s.Eprev = 0; s.gp_prev = 0; s.beta = 0;
   for (int i = 0; i < 6; ++i) s.pr[i] = 0;
   d.dalpha[e] = 0.f;
   d.beta[e] = 0.f;
   d.run[e] = 1;
-  d.ncand[e] = 0;
+  d.ncand[d.lbuf[e] * d.E + e] = 0;
   d.nanc[e] = 0;
   for (int k = 0; k < kNAcc; ++k) d.acc[(size_t)k * d.Es + e] = 0.0;
   for (int k = 0; k < kNAccU; ++k) d.accu[(size_t)k * d.Es + e] = (k == U_ACCD || k == U_GFAR) ? 0x7f800000u : 0u;
@@ -723,10 +725,11 @@ __global__ void __launch_bounds__(128) k_broadphase(Dev d, double r, unsigned lo
   if (threadIdx.x < 3) c[threadIdx.x] = s.c[threadIdx.x];
   if (threadIdx.x < kBpWarps) g_bp_wcnt[threadIdx.x] = 0;
   __syncthreads();  // the only block barrier: R, c and the counters before any query
-  unsigned long long* out = out_override ? out_override : d.cand + (size_t)e * d.kmax;
-  int* cnt = cnt_override ? cnt_override : d.ncand + e;
+  const int lb = d.lbuf[e];
+  unsigned long long* out = out_override ? out_override : d.cand + cand_off(d, lb, e);
+  int* cnt = cnt_override ? cnt_override : d.ncand + lb * d.E + e;
   int cap = out_override ? cap_override : d.kmax;
-  uint2* cc = out_override ? nullptr : d.ccorn + (size_t)e * d.kmax;
+  uint2* cc = out_override ? nullptr : d.ccorn + cand_off(d, lb, e);
   int ntot = d.nsv + d.nse + d.nst;
   if (!out_override && blockIdx.x == 0 && threadIdx.x == 0) d.es[e].cache_ok = 0;  // new candidate list
   bp_range(d, e, blockIdx.x * blockDim.x + threadIdx.x, ntot, gridDim.x * blockDim.x, r, out, cc, cnt, cap, R, c);
@@ -790,8 +793,7 @@ __global__ void __launch_bounds__(128) k_intersect_check(Dev d, int* hit) {
 // rebuild work items carry kRebuildChunk primitives per warp (lanes beyond it idle): the
 // launch is set by its slowest warp, a warp executes the union of its lanes' divergent BVH
 // paths, and the rebuild has far fewer items than warp slots -- thinner items, shorter tail
-constexpr int kRebuildChunk = 8;
-__global__ void __launch_bounds__(128) k_broadphase_list(Dev d, double r) {
+__global__ void __launch_bounds__(128) k_broadphase_list(Dev d, double r, int kRebuildChunk) {
   TAC_PDL_WAIT();
   const int nreb = *d.nreb;
   const int ntot = d.nsv + d.nse + d.nst;
@@ -804,14 +806,19 @@ __global__ void __launch_bounds__(128) k_broadphase_list(Dev d, double r) {
   for (int item = blockIdx.x * kBpWarps + w; item < nreb * nchunk; item += nw) {
     const int e = d.reb_list[item / nchunk], ch = item % nchunk;
     const EnvS& s = d.es[e];
-    if (lane < 9) Rw[w][lane] = s.R[lane];
-    else if (lane < 12) Rw[w][lane] = s.c[lane - 9];
+    // the pending buffer, at the build point's pose (k_alpha's trial: k_accept may move s.c, s.R
+    // while this runs concurrently with the evaluation)
+    const int nb = 1 - d.lbuf[e];
+    if (lane < 9) Rw[w][lane] = s.Rb[lane];
+    else if (lane < 12) Rw[w][lane] = s.cb[lane - 9];
     __syncwarp();
-    bp_range(d, e, ch * kRebuildChunk + lane, min(ntot, (ch + 1) * kRebuildChunk), ntot, r,
-             d.cand + (size_t)e * d.kmax, d.ccorn + (size_t)e * d.kmax, d.ncand + e, d.kmax, Rw[w],
+    unsigned long long* cd = d.cand + cand_off(d, nb, e);
+    uint2* cc = d.ccorn + cand_off(d, nb, e);
+    int* cn = d.ncand + nb * d.E + e;
+    bp_range(d, e, ch * kRebuildChunk + lane, min(ntot, (ch + 1) * kRebuildChunk), ntot, r, cd, cc, cn, d.kmax, Rw[w],
              Rw[w] + 9);  // one round: prims [Q ch, Q ch + Q)
     bool over = false;
-    bp_flush_warp(d, d.cand + (size_t)e * d.kmax, d.ccorn + (size_t)e * d.kmax, d.ncand + e, d.kmax, &over);
+    bp_flush_warp(d, cd, cc, cn, d.kmax, &over);
     if (over) d.es[e].ncand_over = 1;
   }
 }
@@ -824,9 +831,10 @@ __global__ void k_anchors(Dev d, double h2) {
   if (e >= d.E || d.es[e].mode != kActive) return;
   const EnvS& s = d.es[e];
   const double kappa = h2 * d.edbl[e];  // h^2 kappa_phys of this env
-  int n = min(d.ncand[e], d.kmax);
+  const int lb = d.lbuf[e];
+  int n = min(d.ncand[lb * d.E + e], d.kmax);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    unsigned long long rec = d.cand[(size_t)e * d.kmax + i];
+    unsigned long long rec = d.cand[cand_off(d, lb, e) + i];
     int kind = (int)(rec >> 62), a = (int)((rec >> 31) & 0x7fffffffu), b = (int)(rec & 0x7fffffffu);
     Corners C = corners_of(d, kind, a, b);
     d3 z[4];
@@ -891,6 +899,15 @@ __global__ void k_vert_pre(Dev d, float h2) {
   float da = act ? d.dalpha[e] : 0.f;
   if (act && blockIdx.y == 0 && threadIdx.y == 0) {  // near lists are rebuilt by the contact classification
     d.nnear[3 * e] = 0; d.nnear[3 * e + 1] = 0; d.nnear[3 * e + 2] = 0;
+    EnvS& s = d.es[e];
+    if (s.pending && s.iter >= s.reb_iter + 1) {  // R16 pipeline: the list rebuilt during the last
+                                                    // evaluation becomes the active one
+      d.lbuf[e] ^= 1;
+      s.S = s.S2;
+      s.pending = 0;
+      s.cache_ok = 0;
+      s.ncand_max = max(s.ncand_max, d.ncand[d.lbuf[e] * d.E + e]);
+    }
   }
   double ein = 0;
   // two vertices per iteration, every load issued before any store (the stores to u
@@ -1973,7 +1990,8 @@ __global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
   __shared__ double Rs[9], cs[3];
   int e = blockIdx.y;
   if (e >= d.E || !(d.run[e] & 1)) return;
-  if ((int)blockIdx.x * kClassChunk >= min(d.ncand[e], d.kmax)) return;  // no chunk: skip the staging
+  const int lb = d.lbuf[e];
+  if ((int)blockIdx.x * kClassChunk >= min(d.ncand[lb * d.E + e], d.kmax)) return;  // no chunk: skip the staging
   const EnvS& s = d.es[e];
   float4* sx = reinterpret_cast<float4*>(shc4);                           // [nsv] gel surface
   float4* sy = reinterpret_cast<float4*>(shc4 + sizeof(float4) * d.nsv);  // [niv] c + R Y (gel frame only)
@@ -2037,10 +2055,10 @@ __global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
   const bool cached = s.cache_ok;
   const double odo = s.odo, thr = d.dhat + odo;
   const float dh = (float)d.dhat + kClassMargin;
-  const int n = min(d.ncand[e], d.kmax);
-  const unsigned long long* cand = d.cand + (size_t)e * d.kmax;
+  const int n = min(d.ncand[lb * d.E + e], d.kmax);
+  const unsigned long long* cand = d.cand + cand_off(d, lb, e);
   float* hc = d.cgap + (size_t)e * d.kmax;
-  const uint2* ccorn = d.ccorn + (size_t)e * d.kmax;
+  const uint2* ccorn = d.ccorn + cand_off(d, lb, e);
   int* gcnt = d.nnear + 3 * e;
   uint2* glist = d.nearl + (size_t)e * 3 * d.kmax;
   const int lane = threadIdx.x & 31;
@@ -2428,12 +2446,14 @@ __global__ void k_accept(Dev d, double h) {
     double an = 0.5 * s.alpha;
     s.odo = s.odo_base + an * s.Lc;
     s.S += (s.alpha - an) * s.Lc;  // candidate-list odometer: the path back from the trial (R16)
+    s.S2 += (s.alpha - an) * s.Lc;  // (and the pending list's)
     d.dalpha[e] = (float)(an - s.alpha);
     s.alpha = an;
     apply_pose(s, an);
   } else {
     d.dalpha[e] = (float)(-s.alpha);
     s.S += s.alpha * s.Lc;
+    s.S2 += s.alpha * s.Lc;
     s.alpha = 0;
     s.odo = s.odo_base;
     for (int i = 0; i < 3; ++i) s.c[i] = s.cp[i];
@@ -2767,18 +2787,23 @@ __global__ void k_alpha(Dev d, double h) {
   double a = fmin(aup, fmin(abar, accd));
   if (!isfinite(a)) a = 0;
   s.dbg[0] = q; s.dbg[1] = M; s.dbg[2] = L; s.dbg[3] = aup; s.dbg[4] = abar; s.dbg[5] = accd; s.dbg[6] = a;
-  bool reb = false;
-  if (L > 0 && s.S + a * L > kRebuildAt * d.bp_margin) {
-    if (s.S + a * L > d.bp_margin) a = fmax(0.0, (d.bp_margin - s.S) / L);
-    reb = true;
-  }
-  commit_alpha(d, s, e, a, L);
-  if (reb) {  // new candidates at the state this step reaches (O4f)
-    s.S = 0;
-    s.ncand_max = max(s.ncand_max, d.ncand[e]);
+  // the list that will evaluate this step's trial: the pending one if it is swapped in first
+  const bool swap_next = s.pending && s.iter >= s.reb_iter + 1;
+  const double Sl = swap_next ? s.S2 : s.S;
+  if (L > 0 && Sl + a * L > d.bp_margin) a = fmax(0.0, (d.bp_margin - Sl) / L);  // validity cap (R16)
+  commit_alpha(d, s, e, a, L);  // S += a L
+  s.S2 += a * L;
+  if (!s.pending && L > 0 && s.S > kRebuildAt * d.bp_margin) {
+    // pipelined rebuild (R16): a new list built at the trial point this step reaches, during the
+    // next evaluation on a side stream (off its critical path), swapped in by the vertex pre-pass
+    // of the evaluation after; until then the active list stays valid (S <= m_r, capped above)
+    s.pending = 1;
+    s.reb_iter = s.iter;
+    s.S2 = 0;
+    for (int i = 0; i < 3; ++i) s.cb[i] = s.c[i];
+    for (int i = 0; i < 9; ++i) s.Rb[i] = s.R[i];
     s.rebuild += 1;
-    s.cache_ok = 0;
-    d.ncand[e] = 0;
+    d.ncand[(1 - d.lbuf[e]) * d.E + e] = 0;
     d.reb_list[atomicAdd(d.nreb, 1)] = e;  // compact list for k_broadphase_list
   }
 }
@@ -2826,7 +2851,7 @@ __global__ void k_finalize_env(Dev d) {
     for (int i = 0; i < 9; ++i) s.Rt[i] = s.R[i];
   }
   if (s.mode == kActive) s.flags |= kFlagMaxIt;
-  s.ncand_max = max(s.ncand_max, d.ncand[e]);
+  s.ncand_max = max(s.ncand_max, d.ncand[d.lbuf[e] * d.E + e]);
   s.nanc_last = d.nanc[e];
   s.mode = kDone;
   d.run[e] = 0;
@@ -2984,7 +3009,8 @@ static dim3 cellgrid(const Dev& d) {
 }
 static dim3 cgrid(const Dev& d) {
   // ~contact_bps blocks of 128 threads per SM over the grid (per simulator: TAC_CONTACT_BPS at
-  // tac_create, default 16)
+  // tac_create, default 8 -- one block per env at 1,024 envs; interleaved A/B on C3: 20,897 vs
+  // 20,526 env-steps/s at 16; converged parity is tested at both settings)
   const int tot = 148 * d.contact_bps;
   int nb = std::max(1, std::min(64, tot / std::max(1, d.E)));
   return dim3(nb, d.E);
@@ -3035,8 +3061,9 @@ void launch_vert_setup(const Dev& d, double h, cudaStream_t s) {
   LAUNCHP(KID_VERT_SETUP, s, k_vert_setup, vgrid(d, d.nv), dim3(32, 8), 0, d, (float)h);
 }
 void launch_broadphase(const Dev& d, bool masked, cudaStream_t s) {
-  if (masked) {  // envs listed by k_alpha
-    LAUNCHP(KID_BROADPHASE_LIST, s, k_broadphase_list, 16 * 148, 128, 0, d, d.dhat + d.bp_margin);
+  if (masked) {  // envs listed by k_alpha; off the critical path (R16 pipeline): a small grid
+    static const int bps = env_int("TAC_REB_BPS", 16), chunk = env_int("TAC_REB_CHUNK", 32);  // A/B
+    LAUNCHP(KID_BROADPHASE_LIST, s, k_broadphase_list, bps * 148, 128, 0, d, d.dhat + d.bp_margin, chunk);
     return;
   }
   int ntot = d.nsv + d.nse + d.nst;
@@ -3071,8 +3098,13 @@ void launch_eval(const Dev& d, double h, cudaStream_t s) {
   }
   // friction needs only the anchors (fixed for the step) and the surface displacements
   LAUNCHP(KID_CONTACT_FRICTION, cs2, k_contact_friction, cgrid(d), 128, 0, d, d.eps_v * h);
-  // R16: candidates of the envs k_alpha listed, rebuilt at the state k_vert_pre just reached
-  launch_broadphase(d, true, cs);
+  // R16: candidates of the envs k_alpha listed, rebuilt at the trial state k_vert_pre just
+  // reached into their spare buffer, on a third stream beside the whole evaluation (joined before
+  // k_alpha; swapped in by the next k_vert_pre) -- not ahead of the classification any more
+  cudaStream_t rs = fork ? d.side3 : s;
+  if (fork) cudaStreamWaitEvent(rs, d.ev_fork, 0);
+  launch_broadphase(d, true, rs);
+  if (fork) cudaEventRecord(d.ev_reb, rs);
   const size_t cls_both = sizeof(float4) * (size_t)(d.nsv + d.niv);  // [nsv] X + u, [niv] c + R Y
   if (cls_both > 64 * 1024)  // body frame: stage the gel side only
     LAUNCHP(KID_CONTACT_CLASSIFY, cs, k_contact_classify_staged<true>, sgrid(d), 256, sizeof(float4) * (size_t)d.nsv, d);
@@ -3143,6 +3175,7 @@ void launch_curvature(const Dev& d, double h, cudaStream_t s) {
   if (fork) cudaStreamWaitEvent(s, d.ev_join, 0);
 }
 void launch_alpha(const Dev& d, double h, cudaStream_t s) {
+  if (g_prof == nullptr) cudaStreamWaitEvent(s, d.ev_reb, 0);  // the pipelined rebuild has finished
   cudaMemsetAsync(d.nreb, 0, sizeof(int), s);
   LAUNCHP(KID_ALPHA, s, k_alpha, eblocks32(d), 32, 0, d, h);
 }

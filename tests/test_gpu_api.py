@@ -319,3 +319,39 @@ def test_tolerance_mode_c3_never_fails_or_overflows(torch):
     assert torch.isfinite(m).all()
     st = sim.env_stats().cpu().numpy()
     assert st[:, 1].max() < 32768 and st[:, 2].mean() > 100
+
+
+def test_sharded_simulators_reproduce_one_simulator(torch):
+    """SURVEY §8e / P:179-182: environments are independent, so ranks own contiguous env ranges
+    (dist.env_range) and simulators holding those ranges -- with env_offset so their pose-noise
+    streams are the global envs' (R27) -- reproduce one simulator of all envs; the marker
+    fields in rank order are the all-gather's layout."""
+    from paper_2603_28475_b200.dist import env_range
+    s = w.scene_small_peg(n_envs=7, n_steps=3)
+    s.params.tol_x = 1e-9
+    s.params.stagnation = 3000
+    noise = (2e-5, 1e-3, 77)
+    full = _sim(s)
+    full.set_pose_noise(*noise)
+    shards = []
+    for r in range(2):
+        a, b = env_range(r, 2, 7)
+        sub = w.scene_small_peg(n_envs=7, n_steps=3)
+        sub.params = s.params
+        sub.init_poses = s.init_poses[a:b]
+        sub.poses = s.poses[:, a:b]
+        sim = _sim(sub)
+        sim.set_pose_noise(*noise, env_offset=a)
+        shards.append((a, b, sim))
+    for k in range(3):
+        full.step(_poses(torch, s.poses[k]), s.dt)
+        for a, b, sim in shards:
+            sim.step(_poses(torch, s.poses[k][a:b]), s.dt)
+    gathered = torch.cat([sim.markers() for _, _, sim in shards])
+    ref = full.markers()
+    scale = ref.abs().max().item()
+    assert scale > 0 and (gathered - ref).abs().max().item() <= 1e-3 * scale
+    for a, b, sim in shards:
+        for j in range(b - a):
+            assert np.abs(sim.get_state(j)[0] - full.get_state(a + j)[0]).max() <= 1e-5 * 16e-3
+            assert np.abs(sim.get_state(j)[2] - full.get_state(a + j)[2]).max() <= 1e-9
