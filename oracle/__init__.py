@@ -200,7 +200,8 @@ class Oracle:
         dp, dpp = _d([p.dhat, p.kappa_phys, p.eps_v, p.tol_x, p.k_t, p.k_r, p.ccd_s, p.bp_margin, p.c1, p.f_max,
                       p.t_max])
         ip, ipp = _i([p.max_iters, p.fixed_iters, p.beta_rule, p.precond, p.max_halvings, p.stagnation, marker_mode,
-                      knn_k, int(debug), int(getattr(p, "pose_al", 0)), int(getattr(p, "ee_mollifier", 0))])
+                      knn_k, int(debug), int(getattr(p, "pose_al", 0)), int(getattr(p, "ee_mollifier", 0)),
+                      int(getattr(p, "dedup", 0))])
         init = scene.init_poses if init_poses is None else init_poses
         self.n_envs = init.shape[0]
         ini, inip = _d(init)

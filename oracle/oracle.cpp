@@ -324,6 +324,7 @@ struct Problem {
   int max_iters, fixed_iters, beta_rule, precond, max_halvings, stagnation, debug;
   int pose_al;  // augmented-Lagrangian pose enforcement (R29)
   int ee_moll;  // edge-edge parallel mollifier (R30)
+  int dedup;    // IPC-toolkit constraint deduplication (R33)
 };
 
 struct Env {
@@ -525,6 +526,37 @@ Dist pair_dist(const Problem& P, const State& s, const Pair& pr) {
 }
 
 // ---------------------------------------------------------------------------
+// IPC-toolkit constraint deduplication (R33): a pair's constraint is
+// identified by its closest features -- the corners with a non-zero closest-point weight on
+// each side (gel vertex / edge / face, indenter vertex / edge / face).  A point-edge or
+// point-point constraint (one side a single vertex, the other at most an edge) is realised by
+// several primitive pairs (the triangles and edges around the feature); it is counted once.
+// Point-face and edge-edge-interior constraints belong to one pair only.
+// ---------------------------------------------------------------------------
+typedef std::array<int, 5> CKey;  // (gel ids sorted, -1 padded) x 2, (indenter ids sorted) x 2, 0
+bool dedup_key(const Problem& P, const Pair& pr, const Dist& D, CKey* key) {
+  int ci[4];
+  bool ind[4];
+  pair_corners(P, pr, ci, ind);
+  std::vector<int> g, y;
+  for (int k = 0; k < 4; ++k)
+    if (D.w[k] != 0.0) (ind[k] ? y : g).push_back(ci[k]);
+  if (g.size() > 2 || y.size() > 2 || (g.size() == 2 && y.size() == 2)) return false;  // face / edge-edge
+  std::sort(g.begin(), g.end());
+  std::sort(y.begin(), y.end());
+  *key = {g.size() > 0 ? g[0] : -1, g.size() > 1 ? g[1] : -1, y.size() > 0 ? y[0] : -1, y.size() > 1 ? y[1] : -1, 0};
+  return true;
+}
+// true if the pair's constraint was already counted (and records it otherwise)
+bool dedup_seen(const Problem& P, const Pair& pr, const Dist& D, std::set<CKey>* seen, bool* interior_ee) {
+  CKey key;
+  const bool shared = dedup_key(P, pr, D, &key);
+  if (interior_ee) *interior_ee = !shared && pr.kind == EE;
+  if (!P.dedup || !shared) return false;
+  return !seen->insert(key).second;
+}
+
+// ---------------------------------------------------------------------------
 // broad phase (R16): all (gel vert, ind tri), (ind vert,
 // gel tri), (gel edge, ind edge) pairs whose axis-aligned boxes IN THE INDENTER BODY
 // FRAME are within r on every axis (complete: a pair at distance <= r has every axis
@@ -698,19 +730,22 @@ double eval_energy(const Problem& P, const Step& S, const State& s, const std::v
         for (int j = 0; j < 3; ++j) G->D[v][3 * i + j] += w * ((i == j ? P.mu * bb : 0.0) + P.lam2 * cv[i] * cv[j]);
     }
   }
-  // barrier kappa sum_{k in C} b(d_k)
+  // barrier kappa sum_{k in C} b(d_k); with dedup (R33) each constraint once
   double Eb = 0;
+  std::set<CKey> seen;
   for (const Pair& pr : C) {
     Dist D = pair_dist(P, s, pr);
     if (!(D.d > 0)) return std::numeric_limits<double>::quiet_NaN();  // infeasible
     if (D.d >= P.dhat) continue;
+    bool ee_int = false;
+    if (dedup_seen(P, pr, D, &seen, &ee_int)) continue;
     int ci[4];
     bool ind[4];
     pair_corners(P, pr, ci, ind);
     V3 z[4];
     for (int k = 0; k < 4; ++k) z[k] = corner_pos(P, s, ci[k], ind[k]);
-    Moll M;  // m = 1 unless the EE mollifier is on (R30)
-    if (P.ee_moll && pr.kind == EE) {
+    Moll M;  // m = 1 unless the EE mollifier is on (R30; with dedup, edge-edge constraints only)
+    if (P.ee_moll && pr.kind == EE && (!P.dedup || ee_int)) {
       double La2, Lb2;
       ee_rest(P, ci, &La2, &Lb2);
       M = ee_mollifier(z, La2, Lb2);
@@ -830,9 +865,12 @@ double curvature(const Problem& P, const Step& S, const State& s, const std::vec
     if (!ind) return p[c];
     return add(pc, cross(pth, sub(ind_pos(P, s, c), s.c)));
   };
+  std::set<CKey> seen;
   for (const Pair& pr : C) {
     Dist D = pair_dist(P, s, pr);
     if (D.d >= P.dhat) continue;
+    bool ee_int = false;
+    if (dedup_seen(P, pr, D, &seen, &ee_int)) continue;  // R33
     int ci[4];
     bool ind[4];
     pair_corners(P, pr, ci, ind);
@@ -843,7 +881,7 @@ double curvature(const Problem& P, const Step& S, const State& s, const std::vec
     }
     double dn = dot(r, dr) / D.d;
     double m = 1;
-    if (P.ee_moll && pr.kind == EE) {  // R30: the GN curvature scales with m
+    if (P.ee_moll && pr.kind == EE && (!P.dedup || ee_int)) {  // R30: the GN curvature scales with m
       V3 z[4];
       for (int k = 0; k < 4; ++k) z[k] = corner_pos(P, s, ci[k], ind[k]);
       double La2, Lb2;
@@ -1105,9 +1143,12 @@ enum Flags { F_CONV = 1, F_MAXIT = 2, F_NAN = 4, F_INFEAS = 8, F_LARGE = 16, F_O
 void build_anchors(const Problem& P, Step& S, const State& s, const std::vector<Pair>& C) {
   S.anchors.clear();
   if (P.mu_f <= 0) return;
+  std::set<CKey> seen;
   for (const Pair& pr : C) {
     Dist D = pair_dist(P, s, pr);
     if (!(D.d < P.dhat)) continue;
+    bool ee_int = false;
+    if (dedup_seen(P, pr, D, &seen, &ee_int)) continue;  // R33: one anchor per constraint
     Anchor A;
     A.pr = pr;
     int ci[4];
@@ -1128,7 +1169,7 @@ void build_anchors(const Problem& P, Step& S, const State& s, const std::vector<
     A.t1 = scl(1.0 / norm(t1), t1);
     A.t2 = cross(n, A.t1);
     double m = 1;
-    if (P.ee_moll && pr.kind == EE) {  // R30: lambda_k of the mollified barrier
+    if (P.ee_moll && pr.kind == EE && (!P.dedup || ee_int)) {  // R30: lambda_k of the mollified barrier
       double La2, Lb2;
       ee_rest(P, ci, &La2, &Lb2);
       m = ee_mollifier(A.z0, La2, Lb2).m;
@@ -1302,7 +1343,7 @@ extern "C" {
 
 // dparams: dhat, kappa_phys, eps_v, tol_x, k_t, k_r, ccd_s, bp_margin, c1, f_max, t_max
 // iparams: max_iters, fixed_iters, beta_rule, precond, max_halvings, stagnation, marker_mode, knn_k, debug,
-//          pose_al, ee_mollifier
+//          pose_al, ee_mollifier, dedup
 void* or_create(int nv, const double* X, int nt, const int* tets, int nfixed, const int* fixed, int niv,
                 const double* Y, int nit, const int* itris, int nm, const double* mk, const double* frame9,
                 const double* mat4, const double* dparams, const int* iparams, int n_envs, const double* init7,
@@ -1344,6 +1385,7 @@ void* or_create(int nv, const double* X, int nt, const int* tets, int nfixed, co
   P.debug = iparams[8];
   P.pose_al = iparams[9];
   P.ee_moll = iparams[10];
+  P.dedup = iparams[11];
   if (*status) return O;
   precompute(P);
   for (int e = 0; e < nt; ++e) if (!(P.vol[e] > 0)) *status = 2;

@@ -273,6 +273,7 @@ class Params:
     max_anchors: int = 0      # 0 -> library default (4096 per env)
     pose_al: int = 0          # 1: augmented-Lagrangian pose enforcement (R29)
     ee_mollifier: int = 0     # 1: IPC edge-edge parallel mollifier (R30)
+    dedup: int = 0            # 1: IPC-toolkit constraint deduplication (R33)
 
 
 @dataclass
