@@ -120,11 +120,17 @@ typedef struct {
  *   ee_mollifier    1: IPC's edge-edge mollifier (R30): an edge-edge pair's
  *                   barrier becomes m(c) kappa b(d), c = |e_a x e_b|^2, m = -c^2/eps^2 + 2c/eps below
  *                   eps = 1e-3 |E_a|^2 |E_b|^2 (rest lengths), 1 above; its friction lambda too.
- *                   0: off (default).  Outside {0, 1} -> TAC_EINVAL */
+ *                   0: off (default).  Outside {0, 1} -> TAC_EINVAL
+ *   dedup           1: IPC-toolkit constraint deduplication (R33): a pair's
+ *                   constraint is its closest features (corners with a non-zero closest-point
+ *                   weight); point-edge and point-point constraints, realised by several
+ *                   point-triangle / edge-edge pairs, carry their barrier and friction anchor once
+ *                   (the mollifier then applies to edge-edge constraints only).  0: the literal sum
+ *                   over pairs of P:432 (default).  Outside {0, 1} -> TAC_EINVAL */
 typedef struct {
   double dhat, kappa_phys, eps_v, tol_x, k_t, k_r, f_max, t_max, ccd_s, bp_margin, c1, eps_E;
   int32_t max_iters, fixed_iters, beta_rule, precond, max_halvings, stagnation;
-  int32_t max_candidates, max_anchors, check_every, pose_al, ee_mollifier;
+  int32_t max_candidates, max_anchors, check_every, pose_al, ee_mollifier, dedup;
 } tac_solver_params;
 
 typedef struct {

@@ -315,7 +315,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
   if (!(P.dhat > 0) || !(P.bp_margin >= 0.5 * P.dhat) || !(P.ccd_s > 0 && P.ccd_s < 1) || !(P.k_t > 0) ||
       !(P.k_r > 0) || !(P.f_max > 0) || !(P.t_max > 0) || !(P.eps_v > 0) || P.max_iters < 1 || P.fixed_iters < 0 ||
       P.beta_rule < 0 || P.beta_rule > 3 || P.precond < 0 || P.precond > 1 || P.pose_al < 0 || P.pose_al > 1 ||
-      P.ee_mollifier < 0 || P.ee_mollifier > 1)
+      P.ee_mollifier < 0 || P.ee_mollifier > 1 || P.dedup < 0 || P.dedup > 1)
     return fail(TAC_EINVAL, "invalid solver parameters");
   if (MS.rows * MS.cols < 1 || !MS.rest_xyz || (MS.mode != 0 && MS.mode != 1))
     return fail(TAC_EINVAL, "invalid marker set");
@@ -768,6 +768,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
   kernels_init(d.contact_smem);
   d.pose_al = P.pose_al;
   d.ee_moll = P.ee_mollifier;
+  d.dedup = P.dedup;
   d.beta_rule = P.beta_rule; d.precond = P.precond; d.max_halv = P.max_halvings; d.stagnation = P.stagnation;
   d.fixed_iters = P.fixed_iters;
   for (int a = 0; a < 3; ++a) { d.t1[a] = MS.t1[a]; d.t2[a] = MS.t2[a]; d.nrm[a] = MS.n[a]; }
@@ -939,6 +940,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
         (rc = zalloc(sim, 2 * (size_t)d.E * d.kmax, &d.cand)) || (rc = zalloc(sim, (size_t)d.E, &d.lbuf)) || (rc = zalloc(sim, 2 * (size_t)d.E * d.kmax, &d.cgeo)) || (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.cgap)) || (rc = zalloc(sim, 2 * (size_t)d.E * d.kmax, &d.ccorn)) || (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.ncorn)) || (rc = zalloc(sim, 2 * (size_t)d.E, &d.ncand)) || (rc = zalloc(sim, 3 * (size_t)d.E * d.kmax, &d.nearl)) ||
         (rc = zalloc(sim, 3 * (size_t)d.E, &d.nnear)) ||
         (rc = zalloc(sim, 6 * (size_t)std::max(1, d.nsv) * d.Es, &d.Dcon)) ||
+        (rc = zalloc(sim, d.dedup ? (size_t)kDedupSlots * d.Es : 1, &d.dtab)) ||
         (rc = zalloc(sim, (size_t)std::max(1, d.nsv) * d.Es, &d.usurf)) || (rc = zalloc(sim, (size_t)std::max(1, d.nsv) * d.Es, &d.psurf)) ||
         (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc)) || (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc2)) || (rc = zalloc(sim, (size_t)d.E * d.amax, &d.anc_f1)) || (rc = zalloc(sim, (size_t)d.E, &d.nanc)) || (rc = zalloc(sim, (size_t)d.E, &d.reb_list)) ||
         (rc = zalloc(sim, 1, &d.nreb)) ||

@@ -12,6 +12,7 @@
 namespace tac {
 
 constexpr int kNodeLeaf = 4;
+constexpr int kDedupSlots = 4096;  // per-env open-addressing table of shared constraints (R33)
 // element tiles (k_elem_*_tiled): Morton-ordered tets grouped into tiles of <= kTileT tets
 // touching <= kTileV vertices; each tile is scheduled into rounds of <= kTileW
 // vertex-disjoint tets (one per warp) so shared-memory accumulation needs no atomics
@@ -166,6 +167,8 @@ struct Dev {
   int beta_rule, precond, max_halv, stagnation, fixed_iters;
   int pose_al;           // augmented-Lagrangian pose enforcement (R29)
   int ee_moll;           // edge-edge parallel mollifier (R30)
+  int dedup;             // IPC-toolkit constraint deduplication (R33)
+  unsigned long long* dtab;  // [kDedupSlots][Es] claimed constraint keys of the current evaluation (R33)
   // element tiles
   int ntiles;
   const int* tile_vstart;        // [ntiles + 1] into tile_verts

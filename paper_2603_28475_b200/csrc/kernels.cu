@@ -303,6 +303,41 @@ __device__ DR dist_ee(d3 a0, d3 a1, d3 b0, d3 b1) {
   return r;
 }
 
+// ---- R33: IPC-toolkit constraint deduplication.  A pair's constraint is its closest features:
+// the corners with a non-zero closest-point weight (gel ids surface-local, indenter ids vertex
+// ids).  Point-edge and point-point constraints (one side a single vertex, neither side a face,
+// not edge-edge) are realised by several pairs; the first pair to claim the constraint's key in
+// the env's table carries it (all realisations have the same distance and closest points).
+// Returns true for a duplicate.  *interior_ee: an edge-edge constraint (the mollifier's case).
+__device__ bool dedup_duplicate(const Dev& d, int e, const unsigned* id, const bool* ind, const double* w,
+                                bool* interior_ee) {
+  unsigned g[4], y[4];
+  int ng = 0, ny = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (w[k] != 0.0) {
+      if (ind[k]) y[ny++] = id[k];
+      else g[ng++] = id[k];
+    }
+  const bool shared = ng <= 2 && ny <= 2 && !(ng == 2 && ny == 2);
+  *interior_ee = ng == 2 && ny == 2;
+  if (!shared) return false;
+  const unsigned g0 = ng > 1 ? min(g[0], g[1]) : (ng ? g[0] : 0xffffu), g1 = ng > 1 ? max(g[0], g[1]) : 0xffffu;
+  const unsigned y0 = ny > 1 ? min(y[0], y[1]) : (ny ? y[0] : 0xffffu), y1 = ny > 1 ? max(y[0], y[1]) : 0xffffu;
+  const unsigned long long key = (unsigned long long)g0 | ((unsigned long long)g1 << 16) |
+                                 ((unsigned long long)y0 << 32) | ((unsigned long long)y1 << 48);  // never 0
+  unsigned slot = (unsigned)((key * 0x9E3779B97F4A7C15ull) >> 52) & (kDedupSlots - 1);
+  for (int probe = 0; probe < kDedupSlots; ++probe) {
+    unsigned long long* t = d.dtab + (size_t)slot * d.Es + e;
+    const unsigned long long prev = atomicCAS(t, 0ull, key);
+    if (prev == 0ull) return false;   // claimed: this pair carries the constraint
+    if (prev == key) return true;     // another pair carries it
+    slot = (slot + 1) & (kDedupSlots - 1);
+  }
+  d.es[e].ncand_over = 1;  // table full: the step fails (R32)
+  return true;
+}
+
 // ---- fp32 squared distances on coordinates relative to the pair's first corner: only a
 // far/near screen (the same case logic as dist_pt / dist_ee, no weights).  Rounding of the
 // relative coordinates and of the case solves stays below ~1e-9 m at pad scale, so a pair
@@ -568,6 +603,8 @@ __global__ void k_vert_setup(Dev d, float h) {
       d.uh[i] = fixed ? 0.f : ut + h * d.vt[i];
     }
   }
+  if (d.dedup)  // R33: the step-start anchors' constraint table starts empty
+    for (int sl = blockIdx.y * 8 + threadIdx.y; sl < kDedupSlots; sl += gridDim.y * 8) d.dtab[(size_t)sl * d.Es + e] = 0ull;
 }
 
 // ------------------------------------------------------------------ a2: broad phase
@@ -841,6 +878,13 @@ __global__ void k_anchors(Dev d, double h2) {
     for (int k = 0; k < 4; ++k) z[k] = C.ind[k] ? mv(s.R, ind_body(d, C.id[k])) + ld3(s.c) : gel_pos(d, d.u, C.id[k], e);
     DR D = pair_dist(kind, z);
     if (!(D.d < d.dhat) || !(D.d > 0)) continue;
+    CornersL L = corners_l(d, kind, a, b);
+    bool ee_int = true;
+    if (d.dedup) {  // R33: one anchor per constraint (ids: gel surface-local, indenter vertex)
+      unsigned kid[4];
+      for (int k = 0; k < 4; ++k) kid[k] = C.ind[k] ? (unsigned)C.id[k] : (unsigned)L.sid[k];
+      if (dedup_duplicate(d, e, kid, C.ind, D.w, &ee_int)) continue;
+    }
     d3 rr = mk(0, 0, 0);
     for (int k = 0; k < 4; ++k) rr = rr + D.w[k] * z[k];
     d3 nn = (1.0 / D.d) * rr;
@@ -852,14 +896,13 @@ __global__ void k_anchors(Dev d, double h2) {
     int slot = atomicAdd(d.nanc + e, 1);
     if (slot >= d.amax) { d.es[e].ncand_over = 1; continue; }
     Anchor A;
-    CornersL L = corners_l(d, kind, a, b);
     int ng = 0;
     unsigned sid[3] = {0, 0, 0};
     for (int k = 0; k < 3; ++k) { A.gid[k] = -1; A.w[k] = 0.f; }
     A.t1[0] = t1.x; A.t1[1] = t1.y; A.t1[2] = t1.z;
     A.t2[0] = t2.x; A.t2[1] = t2.y; A.t2[2] = t2.z;
     double mol = 1.0;
-    if (kind == 2 && d.ee_moll)  // R30: lambda of the mollified edge-edge barrier
+    if (kind == 2 && d.ee_moll && ee_int)  // R30: lambda of the mollified edge-edge barrier
       mol = ee_moll(z, sqlen4(__ldg(d.X + C.id[1]), __ldg(d.X + C.id[0])),
                     sqlen4(__ldg(d.Y + C.id[3]), __ldg(d.Y + C.id[2]))).m;
     A.lam = (float)fmax(0.0, -mol * kappa * bar_db(D.d, d.dhat));
@@ -965,6 +1008,8 @@ __global__ void k_vert_pre(Dev d, float h2) {
     }
   }
   if (act && ein != 0.0) atomicAdd(d.acc + (size_t)A_EIN * d.Es + e, ein);
+  if (d.dedup && act)  // R33: this evaluation's constraint table starts empty
+    for (int sl = blockIdx.y * 8 + threadIdx.y; sl < kDedupSlots; sl += gridDim.y * 8) d.dtab[(size_t)sl * d.Es + e] = 0ull;
 }
 
 // ------------------------------------------------------------------ a4: element gradient
@@ -1695,6 +1740,11 @@ __global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
       geo[0] = make_float4(0.f, 0.f, 0.f, 0.f);
       continue;
     }
+    bool ee_int = true;
+    if (d.dedup && dedup_duplicate(d, e, id, ind, D.w, &ee_int)) {  // R33: counted by another pair
+      geo[0] = make_float4(0.f, 0.f, 0.f, 0.f);                     // (same geometry: nothing to add)
+      continue;
+    }
     d3 rr = mk(0, 0, 0);
 #pragma unroll
     for (int k = 0; k < 4; ++k) rr = rr + D.w[k] * z[k];
@@ -1702,10 +1752,10 @@ __global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
     MollD Mo;
     Mo.m = 1.0;
     Mo.dm = 0.0;
-    if (MOLL)  // R30 (gel corners 0, 1 surface-local; indenter corners 2, 3)
+    if (MOLL && ee_int)  // R30 (gel corners 0, 1 surface-local; indenter corners 2, 3); with R33 edge-edge only
       Mo = ee_moll(z, sqlen4(__ldg(d.Xs + id[1]), __ldg(d.Xs + id[0])), sqlen4(__ldg(d.Y + id[3]), __ldg(d.Y + id[2])));
     geo[0] = make_float4((float)D.d, (float)nn.x, (float)nn.y, (float)nn.z);
-    const double sm = MOLL ? sqrt(Mo.m) : 1.0;  // curvature weights carry sqrt(m): m kappa b'' (n . dr)^2
+    const double sm = (MOLL && ee_int) ? sqrt(Mo.m) : 1.0;  // curvature weights carry sqrt(m): m kappa b'' (n . dr)^2
     geo[1] = make_float4((float)(sm * D.w[0]), (float)(sm * D.w[1]), (float)(sm * D.w[2]), (float)(sm * D.w[3]));
     double lg = log(D.d / d.dhat), dm = D.d - d.dhat, inv = 1.0 / D.d;
     const double bk = kappa * (-dm * dm * lg);                           // kappa b
@@ -1718,7 +1768,7 @@ __global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       d3 f = (db * D.w[k]) * nn;
-      if (MOLL) f = f + bdm * Mo.dc[k];
+      if (MOLL && ee_int) f = f + bdm * Mo.dc[k];
       if (!ind[k]) {
         const int v = __ldg(d.svfree + id[k]);  // one load: id and fixed flag
         if (v >= 0) scatter_gel_free(d, v, id[k], e, f, ddb * D.w[k] * D.w[k], nn);

@@ -45,7 +45,7 @@ class SolverParams(C.Structure):
                                            "ccd_s", "bp_margin", "c1", "eps_E")] + \
                [(n, C.c_int32) for n in ("max_iters", "fixed_iters", "beta_rule", "precond", "max_halvings",
                                           "stagnation", "max_candidates", "max_anchors", "check_every", "pose_al",
-                                          "ee_mollifier")]
+                                          "ee_mollifier", "dedup")]
 
 
 class CreateInfo(C.Structure):
@@ -184,7 +184,8 @@ class TacSim:
                           params.max_iters, params.fixed_iters, params.beta_rule, params.precond,
                           params.max_halvings, params.stagnation, getattr(params, "max_candidates", 0),
                           getattr(params, "max_anchors", 0), getattr(params, "check_every", 0),
-                          getattr(params, "pose_al", 0), getattr(params, "ee_mollifier", 0))
+                          getattr(params, "pose_al", 0), getattr(params, "ee_mollifier", 0),
+                          getattr(params, "dedup", 0))
         ip = np.ascontiguousarray(init_poses, dtype=np.float32).reshape(n_envs, 7)
         self._keep.append(ip)
         info = CreateInfo(C.pointer(gel), C.pointer(mat), C.pointer(ms), C.pointer(ind), C.pointer(sp), n_envs,

@@ -623,3 +623,54 @@ def test_pose_noise_contact_parity_and_env_offset(torch_cuda):
         _assert_parity(s, sim, o, mk, e)
     scale = np.abs(mk[1:]).max()
     assert np.abs(mk2 - mk[1:]).max() <= 1e-3 * scale
+
+
+# ---------------------------------------------------------------- R33 constraint deduplication
+def test_dedup_kernel_parity_and_closed_form(torch_cuda):
+    """IPC-toolkit constraint deduplication on the GPU (dedup = 1): at a pressed C1 contact state
+    the energy parts, gradient, blocks (element-wise bars) and the a6-a8 quantities match the
+    oracle's deduplicated ones, and differ from the literal sum's.  (The closed form under an
+    inverted pyramid's tip is pinned on the oracle only: there the tip projects exactly onto a
+    mesh vertex, on a boundary between closest-feature regions, where the classification -- and
+    R33's energy -- depends on the last bit of the barycentric solve, which two implementations
+    with different operation orders need not share; the literal sum does not depend on it.)"""
+    from test_oracle_dedup import _pyramid_scene
+    h = 0.5e-4
+    s = _pyramid_scene(h)
+    sim = _sim(s)
+    o = O.Oracle(s)
+    z = np.zeros_like(s.X)
+    c = s.init_poses[0, :3].astype(np.float64)
+    gpu = sim.debug_eval(0, z, z, c, np.eye(3), z, c, np.eye(3), s.init_poses[0], s.dt)
+    ref = o.eval(z, z, c, np.eye(3), z, c, np.eye(3), s.init_poses[0])
+    assert abs(gpu["parts"][2] - ref["parts"][2]) <= 1e-9 * ref["parts"][2]  # literal: m kappa b(h)
+    s, o0, (u_t, v_t, c_t, R_t), (u, c, R), tgt = _pressed_state()
+    s.params.dedup = 1
+    o = O.Oracle(s, params=s.params)
+    sim = _sim(s)
+    ut32 = u_t.astype(np.float32).astype(np.float64)
+    vt32 = v_t.astype(np.float32).astype(np.float64)
+    ref = o.eval(ut32, vt32, c_t, R_t, u, c, R, tgt)
+    gpu = sim.debug_eval(0, ut32, vt32, c_t, R_t, u, c, R, tgt, s.dt)
+    lit = o0.eval(ut32, vt32, c_t, R_t, u, c, R, tgt)
+    assert lit["parts"][2] > ref["parts"][2] * (1 + 1e-3)  # duplicates exist here
+    _assert_eval_parity(s, o, ref, gpu, ut32, vt32, u)
+    st = (ut32, vt32, c_t, R_t)
+    (u2, c2, R2), g_prev, p_prev, gPg_prev = _iteration_inputs(s, o, st, (u, c, R), tgt)
+    p_o, r_o = o.iteration(*st, u2, c2, R2, tgt, g_prev, p_prev, gPg_prev, restart=True)
+    p_g, r_g = sim.debug_iteration(0, *st, u2, c2, R2, tgt, s.dt, g_prev, p_prev, gPg_prev, restart=True)
+    amp = max(1.0, np.sqrt(gPg_prev / r_o["gPg"]))
+    for k in ("pHp", "alpha_bar", "alpha_ccd", "alpha"):
+        assert _rel(r_g[k], r_o[k]) <= 4e-5 * amp, (k, r_g[k], r_o[k])
+
+
+def test_dedup_converged_parity(torch_cuda):
+    """Converged steps with deduplicated constraints (small peg, 3 ragged envs x 3 steps) match
+    the oracle's on the north_star gates."""
+    s = w.scene_small_peg(n_envs=3, n_steps=3)
+    s.params.dedup = 1
+    sim, o, mk = _run_both(s, 3)
+    it, pg, fl = sim.env_status()
+    for e in range(3):
+        assert int(fl[e]) & 1 and o.status_of(e)["flags"] & 1, (e, int(fl[e]), o.status_of(e))
+        _assert_parity(s, sim, o, mk, e)
