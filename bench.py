@@ -338,7 +338,9 @@ def run_ours(args, rank, local, ws):
                    "envs_per_gpu": E, "total_envs": n_all, "iters_per_step": args.iters if args.tol is None else None,
                    "iteration_mode": "fixed" if args.tol is None else f"tolerance (tol_x {args.tol:g} m, max {args.max_iters})",
                    "parallelism": f"env-sharded dp{ws}" + ((" + NCCL all-gather of markers ("
-                                  + ("tac_gather_markers, C ABI" if native else "torch.distributed") + ")") if distributed else ""),
+                                  + (("tac_gather_markers, C ABI, " + ("torch's NCCL communicator"
+                                      if type(mg.comm).__name__ == "_BorrowedComm" else "own communicator"))
+                                     if native else "torch.distributed") + ")") if distributed else ""),
                    "l2": "per-env state ~470 MB/GPU > 126 MB L2 (no flush needed)"},
         "roofline": roof,
         "hbm_iteration": hbm_it,
