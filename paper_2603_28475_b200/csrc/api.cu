@@ -782,6 +782,10 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     sim->use_graphs = false;
     g_tl_iter = P.fixed_iters / 2;
   }
+  if (getenv("TAC_TIMELINE_ITER")) {  // measurement only: that iteration of every launched chunk
+    sim->use_graphs = false;
+    g_tl_iter = atoi(getenv("TAC_TIMELINE_ITER"));
+  }
   // device upload
   std::vector<float4> Xf(nv), Yf(niv);
   for (int i = 0; i < nv; ++i) Xf[i] = make_float4((float)X[i][0], (float)X[i][1], (float)X[i][2], 0.f);
