@@ -5,8 +5,8 @@ gpurun brought back into gpurun_out/):
     python profiles/summarize.py TAG [--launches gpurun_out/prof_launches.csv]
                                      [--full gpurun_out/prof_full.ncu-rep]
 
-writes profiles/r01_TAG_ncu_launch_list_summary.txt (per-kernel shares of the launch list),
-profiles/r01_TAG_ncu_full_summary.txt (time, DRAM, registers, occupancy, issue, FMA pipe and
+writes profiles/rNN_TAG_ncu_launch_list_summary.txt (per-kernel shares of the launch list),
+profiles/rNN_TAG_ncu_full_summary.txt (time, DRAM, registers, occupancy, issue, FMA pipe and
 the top stall reasons per kernel of the --set full capture) and refreshes
 profiles/ncu_traffic.json (DRAM bytes per launch, read by bench.py's roofline)."""
 import argparse
@@ -19,6 +19,7 @@ import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
+ROUND = os.environ.get("PROFILE_ROUND", "r02")  # file prefix of the summaries
 ROOT = os.path.dirname(HERE)
 # bench.py profile names of the kernels (tac_profile_kernel_name)
 PROFILE_NAME = {"k_elem_grad_cells": "elem_grad", "k_elem_curv_cells": "elem_curv", "k_vert_pre": "vert_pre",
@@ -59,7 +60,7 @@ def launches(path, tag):
            f"{'kernel':32s} {'launches':>8s} {'total':>12s} {'mean':>10s} {'share':>7s}"]
     for k in sorted(tot, key=lambda k: -tot[k]):
         out.append(f"{k:32s} {cnt[k]:8d} {tot[k]:12.1f} {tot[k] / cnt[k]:10.2f} {100 * tot[k] / s:6.1f}%")
-    p = os.path.join(HERE, f"r01_{tag}_ncu_launch_list_summary.txt")
+    p = os.path.join(HERE, f"{ROUND}_{tag}_ncu_launch_list_summary.txt")
     open(p, "w").write("\n".join(out) + "\n")
     print(p)
 
@@ -90,12 +91,12 @@ def full(path, tag):
             mb = float(row[idx[1]]) + float(row[idx[2]])
             scale = {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1.0}.get(units[idx[1]], 1e6)
             traffic[PROFILE_NAME[k]] = int(round(mb * scale))
-    p = os.path.join(HERE, f"r01_{tag}_ncu_full_summary.txt")
+    p = os.path.join(HERE, f"{ROUND}_{tag}_ncu_full_summary.txt")
     open(p, "w").write("\n".join(out) + "\n")
     print(p)
     if traffic:
         traffic = {"_source": f"ncu --set full --clock-control none (profiles/profile_round.sh), dram__bytes_read.sum + "
-                              f"dram__bytes_write.sum per launch, C3 1,024 envs; see profiles/r01_{tag}_ncu_full_summary.txt",
+                              f"dram__bytes_write.sum per launch, C3 1,024 envs; see profiles/{ROUND}_{tag}_ncu_full_summary.txt",
                    **dict(sorted(traffic.items()))}
         json.dump(traffic, open(os.path.join(HERE, "ncu_traffic.json"), "w"), indent=1)
 
