@@ -1254,6 +1254,7 @@ tac_status tac_markers(tac_sim* sim, float* out, int32_t ncomp, void* stream) {
   launch_markers(sim->d, out, ncomp, (cudaStream_t)stream);
   g_prof = nullptr;
   sim->launches = g_launches;
+  sim->while_per_trip = 0;  // this call's launches only
   return post_launch(sim);
 }
 
@@ -1341,6 +1342,7 @@ tac_status tac_gather_markers(tac_sim* sim, void* comm, float* recvbuf, int32_t 
   launch_markers(sim->d, slot, ncomp, (cudaStream_t)stream);  // this rank's slot, then in place
   g_prof = nullptr;
   sim->launches = g_launches;
+  sim->while_per_trip = 0;
   if ((st = post_launch(sim))) return st;
   const int rc = nccl().allgather(slot, recvbuf, count, kNcclFloat32, comm, (cudaStream_t)stream);
   if (rc != 0) {
@@ -1360,6 +1362,7 @@ tac_status tac_marker_sqerr(tac_sim* sim, const float* ref, double* acc, int32_t
   launch_marker_sqerr(sim->d, ref, acc, ncomp, (cudaStream_t)stream);
   g_prof = nullptr;
   sim->launches = g_launches;
+  sim->while_per_trip = 0;  // this call's launches only
   return post_launch(sim);
 }
 
