@@ -82,13 +82,14 @@ def _gates(scene, u_g, u_o, m_g, m_o, what, check=True):
     return du
 
 
-def _compare(scene, p_or, e, start, target, u_g, c_g, R_g, m_g, u_o, m_o, what, alt):
+def _compare(scene, p_or, e, start, target, u_g, c_g, R_g, m_g, u_o, m_o, what, alt, oracle_ok=True):
     """Gates against the oracle's minimiser; where they fail, the GPU has reached ANOTHER local
     minimiser of the same step's incremental potential (the IPC potential is not convex: a gel
     vertex against a faceted indenter, R25) -- certified by the oracle itself: its
     PNCG started at the GPU's result (same anchors, same target) converges without leaving it
-    (north_star gates between the GPU's state and the polished one).  `alt` collects these."""
-    if _gates(scene, u_g, u_o, m_g, m_o, what, check=False):
+    (north_star gates between the GPU's state and the polished one).  `alt` collects these, and
+    the steps whose own oracle solve stagnated (oracle_ok False) are certified the same way."""
+    if oracle_ok and _gates(scene, u_g, u_o, m_g, m_o, what, check=False):
         return _gates(scene, u_g, u_o, m_g, m_o, what)
     o1 = O.Oracle(scene, params=p_or, init_poses=scene.init_poses[[0]])
     o1.set_state(0, *start)
@@ -219,10 +220,13 @@ def test_c3_full_size_windows_shear_twist_release(torch_cuda, bps):
             seen[phases[e]] += 1
             u_o, m_o, st = res[j]
             (u_g, _, c_g, R_g), m_g, fg = finals[e]
-            assert _oracle_converged(st), (k, e, st)
             assert fg & (1 | 64), (k, e, fg)  # converged (or stagnated at |Pg| ~ 1e-7)
+            # an oracle solve that stagnates from this start (seen once in ~600 env-steps, |Pg|
+            # 2e-5 m after 5,600 iterations) is replaced by certifying the GPU's result
             worst = max(worst, _compare(s, p_or, e, starts[e], s.poses[k][e], u_g, c_g, R_g, m_g, u_o, m_o,
-                                        f"C3 step {k} env {e} ({phases[e]})", alt))
+                                        f"C3 step {k} env {e} ({phases[e]})" + ("" if _oracle_converged(st)
+                                                                                 else " [oracle stagnated]"),
+                                        alt, oracle_ok=_oracle_converged(st)))
     n = sum(seen.values())
     print(f"bps {bps}: worst |u_gpu - u_oracle| = {worst:.3e} m over {n} env-steps {seen}; "
           f"other local minimisers: {alt}")
