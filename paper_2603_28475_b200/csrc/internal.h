@@ -225,7 +225,8 @@ enum KernelId {
   KID_STEP_SETUP = 0, KID_VERT_SETUP, KID_BROADPHASE, KID_ANCHORS, KID_VERT_PRE, KID_ELEM_GRAD, KID_CONTACT_GRAD,
   KID_ACCEPT, KID_DIR_REDUCE, KID_DIR_SCALAR, KID_DIR_APPLY, KID_ELEM_CURV, KID_CONTACT_CURV, KID_ALPHA,
   KID_CCD, KID_FIN_VERT, KID_FIN_ENV, KID_MARKERS, KID_OTHER, KID_CONTACT_CLASSIFY,
-  KID_CONTACT_NEAR_IG, KID_CONTACT_NEAR_EE, KID_CONTACT_FRICTION, KID_BROADPHASE_LIST, KID_COUNT
+  KID_CONTACT_NEAR_IG, KID_CONTACT_NEAR_EE, KID_CONTACT_FRICTION, KID_BROADPHASE_LIST, KID_DIR_REDUCE_SURF,
+  KID_COUNT
 };
 struct Profiler;
 extern thread_local Profiler* g_prof;

@@ -26,7 +26,7 @@ static const char* kNames[KID_COUNT] = {
     "step_setup", "vert_setup", "broadphase", "anchors", "vert_pre", "elem_grad", "contact_near_gi", "accept",
     "dir_reduce", "dir_scalar", "dir_apply", "elem_curv", "contact_curv", "alpha", "ccd", "finalize_vert",
     "finalize_env", "markers", "other", "contact_classify", "contact_near_ig", "contact_near_ee",
-    "contact_friction", "broadphase_rebuild"};
+    "contact_friction", "broadphase_rebuild", "dir_reduce_surf"};
 const char* kernel_name(int kid) { return (kid >= 0 && kid < KID_COUNT) ? kNames[kid] : "?"; }
 
 // ------------------------------------------------------------------ small helpers
@@ -2543,26 +2543,37 @@ __device__ __forceinline__ void precond2(T a, T b, T c, T xy, T xz, T yz, int sc
   y2[2] = (float)(inv * (c02 * x2[0] + c12 * x2[1] + c22 * x2[2]));
 }
 
-constexpr int kDirNB = 1;  // vertices in flight per thread in k_dir_reduce: the fp64 surface block inverse
-                            // needs ~80 registers; 1 vertex x 3 blocks / SM measured 74 vs 82 us (2 x 2)
-__global__ void __launch_bounds__(256, 3) k_dir_reduce(Dev d) {
+// Direction reduction: the dots g^T P y, y^T p, y^T P y, p^T g, g^T P g, g^T g, p^T p and
+// max |P g| per env, and P g stored for k_dir_apply.  SURF = false: the vertices off the gel
+// surface (and fixed-free surface vertices are skipped), fp32 block inverse, two vertices in
+// flight; SURF = true: the free surface vertices (the list sv), whose P = (D + Dcon)^-1 is formed
+// in fp64 (R24) -- on a side stream beside the first, so the fp64 inverse's registers no longer
+// throttle the bulk of the vertices (one kernel with both: 80 registers, one vertex in flight)
+template <bool SURF>
+__global__ void __launch_bounds__(256) k_dir_reduce(Dev d) {
   TAC_PDL_WAIT();
+  constexpr int NB = SURF ? 1 : 2;
   int e = blockIdx.x * 32 + threadIdx.x;
   bool act = e < d.E && (d.run[e] & 3);  // speculative: k_accept may run concurrently (see launch_eval)
   if (!__any_sync(0xffffffffu, act)) return;
   double gPy = 0, yp = 0, yPy = 0, pg = 0, gPg = 0, gg = 0, pp = 0;
   float pgmax = 0.f;
   const int stride = gridDim.y * 8;
-  for (int v0 = blockIdx.y * 8 + threadIdx.y; v0 < d.nv; v0 += kDirNB * stride) {  // kDirNB vertices in flight
-    float g[kDirNB][3], gq[kDirNB][3], p[kDirNB][3], D[kDirNB][6];
-    int si[kDirNB];
-    bool ok[kDirNB];
+  const int n = SURF ? d.nsv : d.nv;
+  for (int i0 = blockIdx.y * 8 + threadIdx.y; i0 < n; i0 += NB * stride) {  // NB vertices in flight
+    float g[NB][3], gq[NB][3], p[NB][3], D[NB][6];
+    int vv[NB];
+    bool ok[NB];
 #pragma unroll
-    for (int t = 0; t < kDirNB; ++t) {
-      const int v = v0 + t * stride;
-      ok[t] = act && v < d.nv && !(d.vflag[v] & 1);
+    for (int t = 0; t < NB; ++t) {
+      const int i = i0 + t * stride;
+      ok[t] = false;
+      if (!act || i >= n) continue;
+      const int v = SURF ? d.sv[i] : i;
+      const unsigned char fl = d.vflag[v];
+      ok[t] = !(fl & 1) && (SURF || !(fl & 2));
+      vv[t] = v;
       if (!ok[t]) continue;
-      si[t] = (d.vflag[v] & 2) ? d.sidx[v] : -1;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         g[t][c] = d.g[vidx(d, c, v, e)];
@@ -2573,26 +2584,25 @@ __global__ void __launch_bounds__(256, 3) k_dir_reduce(Dev d) {
       for (int c = 0; c < 6; ++c) D[t][c] = d.D[vidxD(d, c, v, e)];
     }
 #pragma unroll
-    for (int t = 0; t < kDirNB; ++t) {
+    for (int t = 0; t < NB; ++t) {
       if (!ok[t]) continue;
+      const int v = vv[t];
       float y[3], Pg[3], Py[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) y[c] = g[t][c] - gq[t][c];
-      if (si[t] >= 0) {  // contact block loaded here (fewer live registers than a prefetch)
+      if constexpr (SURF) {
+        const int sl = i0 + t * stride;  // surface-local id
         const float* A = D[t];
         float C[6];
 #pragma unroll
-        for (int c = 0; c < 6; ++c) C[c] = d.Dcon[vidxS(d, c, si[t], e)];
+        for (int c = 0; c < 6; ++c) C[c] = d.Dcon[vidxS(d, c, sl, e)];
         precond2<double>((double)A[0] + C[0], (double)A[1] + C[1], (double)A[2] + C[2], (double)A[3] + C[3],
                          (double)A[4] + C[4], (double)A[5] + C[5], d.precond, g[t], y, Pg, Py);
       } else {
         precond2<float>(D[t][0], D[t][1], D[t][2], D[t][3], D[t][4], D[t][5], d.precond, g[t], y, Pg, Py);
       }
-      {  // P g for k_dir_apply (speculative like the dots: only accepted envs' values are used)
-        const int v = v0 + t * stride;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) d.Pg[vidx(d, c, v, e)] = Pg[c];
-      }
+      for (int c = 0; c < 3; ++c) d.Pg[vidx(d, c, v, e)] = Pg[c];  // for k_dir_apply (speculative, like the dots)
       const float* gv = g[t];
       const float* pv = p[t];
       gPy += gv[0] * Py[0] + gv[1] * Py[1] + gv[2] * Py[2];
@@ -3199,8 +3209,21 @@ void launch_eval(const Dev& d, double h, cudaStream_t s) {
   }
 }
 void launch_direction(const Dev& d, cudaStream_t s, bool apply) {
-  LAUNCHP(KID_DIR_REDUCE, s, k_dir_reduce, vgrid(d, d.nv), dim3(32, 8), 0, d);
-  if (g_prof == nullptr) cudaStreamWaitEvent(s, d.ev_join, 0);  // k_accept on the side stream
+  // the surface vertices' fp64-preconditioned part beside the bulk (joined before k_dir_scalar)
+  const bool fork = g_prof == nullptr;
+  cudaStream_t ss = fork ? d.side2 : s;
+  if (fork) {
+    cudaEventRecord(d.ev_fork, s);
+    cudaStreamWaitEvent(ss, d.ev_fork, 0);
+  }
+  static const int sbps = env_int("TAC_DIRS_BPS", 2);  // A/B
+  LAUNCHP(KID_DIR_REDUCE_SURF, ss, k_dir_reduce<true>, vgrid(d, std::max(1, d.nsv), sbps), dim3(32, 8), 0, d);
+  if (fork) cudaEventRecord(d.ev_join2, ss);
+  LAUNCHP(KID_DIR_REDUCE, s, k_dir_reduce<false>, vgrid(d, d.nv), dim3(32, 8), 0, d);
+  if (fork) {
+    cudaStreamWaitEvent(s, d.ev_join, 0);   // k_accept on the side stream
+    cudaStreamWaitEvent(s, d.ev_join2, 0);  // the surface part
+  }
   LAUNCHP(KID_DIR_SCALAR, s, k_dir_scalar, eblocks32(d), 32, 0, d);
   if (apply) LAUNCHP(KID_DIR_APPLY, s, k_dir_apply, vgrid(d, d.nv), dim3(32, 8), 0, d);
 }

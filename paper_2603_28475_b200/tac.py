@@ -117,7 +117,7 @@ EXPORTED = ["tac_create", "tac_step", "tac_markers", "tac_reset", "tac_env_statu
             "tac_set_env_material", "tac_marker_sqerr", "tac_set_pose_noise", "tac_nccl_unique_id",
             "tac_nccl_comm_create", "tac_nccl_comm_destroy", "tac_gather_markers", "tac_checkpoint_size",
             "tac_checkpoint_save", "tac_checkpoint_load", "tac_debug_iteration"]
-N_KERNEL_IDS = 24
+N_KERNEL_IDS = 25
 
 
 class TacError(RuntimeError):
