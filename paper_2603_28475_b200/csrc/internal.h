@@ -215,7 +215,6 @@ void launch_write_words(const Dev& d, uint64_t* dst, const uint64_t* words, int 
 void launch_stats(const Dev& d, int4* out, cudaStream_t s);
 // debug
 void launch_debug_broadphase(const Dev& d, double r, unsigned long long* out, int* cnt, int cap, cudaStream_t s);
-int launches_per_iteration();
 void kernels_init(int contact_smem);  // per-device kernel attributes (call after cudaSetDevice)
 int contact_smem_bytes(int nsv, int niv);  // 0 if the staged contact kernels do not fit
 extern thread_local long long g_launches;

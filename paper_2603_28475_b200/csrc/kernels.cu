@@ -3310,6 +3310,5 @@ void kernels_init(int contact_smem) {
   cudaFuncSetAttribute(k_contact_curv_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, kContactSmemCap);
   cudaFuncSetAttribute(k_elem_curv_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, kTiledCurvSmem);
 }
-int launches_per_iteration() { return 8 + 3 + 2 + 4; }
 
 }  // namespace tac
