@@ -77,7 +77,8 @@ def main():
             ug, vg, cg, Rg = finals[e]
             d = float(np.abs(ug - uo).max())
             du.append(d)
-            if d > a.dump_above:
+            stuck = not (st["flags"] & 1) and not (st["flags"] & 64 and st["pg"] <= 1e-10)
+            if d > a.dump_above or stuck:
                 n_bad += 1
                 ut, vt, ct, Rt = starts[e]
                 fn = f"gpurun_out/mismatch{a.tag}_bps{a.bps}_k{k}_e{e}.npz"
@@ -85,7 +86,7 @@ def main():
                                     u_gpu=ug, c_gpu=cg, R_gpu=Rg, u_or=uo, c_or=co, R_or=Ro, gpu_iters=it[e],
                                     gpu_flags=fl[e], gpu_pg=pg[e], or_iters=st["iters"], or_flags=st["flags"],
                                     env=e, k=k)
-                print(json.dumps(dict(k=k, env=e, du=d, gpu_iters=int(it[e]), gpu_flags=int(fl[e]),
+                print(json.dumps(dict(k=k, env=e, du=d, oracle_stuck=stuck, gpu_iters=int(it[e]), gpu_flags=int(fl[e]),
                                       gpu_pg=float(pg[e]), oracle=st)), flush=True)
         summary.append(dict(k=k, worst=max(du), n_over_1e7=int(sum(x > 1e-7 for x in du)), n=len(du)))
         print(json.dumps(summary[-1]), flush=True)
