@@ -624,6 +624,59 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     for (int e = 0; e < nt; ++e)
       if (!used[e]) rest_tets.push_back(e);
   }
+  // cell rows: chains of cells along corner bit 0 (cell k+1's corners 0, 2, 4, 6 are cell k's
+  // 1, 3, 5, 7), cells reordered chain by chain and cut into segments of <= seg_len cells; the
+  // row-marching gradient pass carries the shared face's u and accumulators from one cell to
+  // the next (half the corner loads and red.adds of one cell at a time)
+  std::vector<int2> cell_seg;
+  {
+    const int ncell = (int)cell_fix.size();
+    auto corner = [&](int c, int k) {
+      const int4 q = cell_v[2 * c + (k >> 2)];
+      const int r = k & 3;
+      return r == 0 ? q.x : r == 1 ? q.y : r == 2 ? q.z : q.w;
+    };
+    std::map<int, int> by0;
+    for (int c = 0; c < ncell; ++c) by0[corner(c, 0)] = c;
+    std::vector<int> nxt(ncell, -1), has_prev(ncell, 0);
+    for (int c = 0; c < ncell; ++c) {
+      auto it = by0.find(corner(c, 1));
+      if (it == by0.end()) continue;
+      const int c2 = it->second;
+      bool ok = c2 != c;
+      for (int k = 0; k < 8 && ok; k += 2) ok = corner(c2, k) == corner(c, k + 1);
+      if (ok && !has_prev[c2]) { nxt[c] = c2; has_prev[c2] = 1; }
+    }
+    std::vector<int> order;
+    std::vector<char> seen(ncell, 0);
+    const int seg_len = getenv("TAC_ROW_SEG") ? std::max(1, atoi(getenv("TAC_ROW_SEG"))) : 10;
+    auto chain = [&](int h) {
+      int len = 0;
+      for (int c = h; c >= 0 && !seen[c]; c = nxt[c]) { seen[c] = 1; order.push_back(c); ++len; }
+      // split into near-equal segments of <= seg_len cells
+      const int base = (int)order.size() - len, nsg = (len + seg_len - 1) / seg_len;
+      for (int k = 0, at = 0; k < nsg; ++k) {
+        const int n = (len - at) / (nsg - k);
+        cell_seg.push_back(make_int2(base + at, n));
+        at += n;
+      }
+    };
+    for (int c = 0; c < ncell; ++c)
+      if (!has_prev[c]) chain(c);
+    for (int c = 0; c < ncell; ++c)
+      if (!seen[c]) chain(c);  // (cycles cannot occur on a pad; kept total)
+    std::vector<int4> v2(cell_v.size());
+    std::vector<unsigned> f2(cell_fix.size());
+    std::vector<float4> a2(cell_aa.size()), t2(cell_tb.size());
+    for (int k = 0; k < ncell; ++k) {
+      const int c = order[k];
+      v2[2 * k] = cell_v[2 * c]; v2[2 * k + 1] = cell_v[2 * c + 1];
+      f2[k] = cell_fix[c];
+      a2[k] = cell_aa[c];
+      for (int j = 0; j < 18; ++j) t2[18 * k + j] = cell_tb[18 * c + j];
+    }
+    cell_v.swap(v2); cell_fix.swap(f2); cell_aa.swap(a2); cell_tb.swap(t2);
+  }
   // element tiles: Morton order of tet centroids, greedy cut at kTileT tets / kTileV
   // vertices, then greedy rounds of <= kTileW vertex-disjoint tets
   std::vector<int> tile_vstart{0}, tile_verts, tile_tstart{0}, tile_rstart{0};
@@ -929,6 +982,9 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
       fprintf(stderr, "cells: %zu, axis-aligned (bit b along axis b): %zu\n", cell_aa.size(), naa);
     }
     UP(cell_tb, d.cell_tb);
+    UP(cell_seg, d.cell_seg);
+    d.nseg = (int)cell_seg.size();
+    d.rows = d.cells_all_aa && !getenv("TAC_NO_ROWS");
     UP(rest_tets, d.rest_tets);
     d.ncells = (int)cell_fix.size();
     d.nrest = (int)rest_tets.size();

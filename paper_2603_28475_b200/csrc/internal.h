@@ -187,6 +187,8 @@ struct Dev {
   const float4* cell_tb;         // [ncells][6][3] (b1, vol), (b2, 0), (b3, 0) in canonical corner order
   const float4* cell_aa;         // [ncells] axis-aligned box (corner bit b along axis b): (1/s0, 1/s1, 1/s2, tet volume), else 0
   int cells_all_aa;              // every cell axis-aligned: the cell kernels compile the stored-B branch out
+  const int2* cell_seg;          // [nseg] (first cell, count): runs of cells along corner bit 0 (cell order is chain order)
+  int nseg, rows;                // rows: the gradient pass marches along the segments (all cells axis-aligned)
   const int* rest_tets;          // [nrest] tets not in any cell
   double t1[3], t2[3], nrm[3];
 };

@@ -1446,6 +1446,85 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
   if (act) atomicAdd(d.acc + (size_t)A_EEL * d.Es + e, esum);
 }
 
+// ---- row-marching Kuhn-cell gradient (all cells axis-aligned): one warp = one segment of
+// consecutive cells along corner bit 0 x 32 envs.  Cell k+1's corners 0, 2, 4, 6 are cell k's
+// 1, 3, 5, 7, so their u and their force / block accumulators stay in registers from one cell
+// to the next: per cell 12 corner row loads and 36 red.adds instead of 24 and 72.  Pair order
+// 1, 2, 0 finishes the carried-in corners early (2 after pair 1; 4, 6 after pair 2; 0 after
+// pair 0), so at most 6 corners' accumulators are live, as in the one-cell pass.
+__global__ void __launch_bounds__(256, 2) k_elem_grad_rows(Dev d, float h2) {
+  TAC_PDL_WAIT();
+  const int e = blockIdx.y * 32 + threadIdx.x;
+  const bool act = e < d.E && (d.run[e] & 1);
+  if (!__any_sync(0xffffffffu, act)) return;
+  const float mu = d.emat[e], l2 = d.emat[d.Es + e];  // per-env material
+  const unsigned G = (unsigned)(d.Es >> 5), eg = (unsigned)blockIdx.y, lane = threadIdx.x;
+  double esum = 0;
+  for (int sg = blockIdx.x * 8 + threadIdx.y; sg < d.nseg; sg += gridDim.x * 8) {
+    if (!act) continue;
+    const int2 seg = __ldg(d.cell_seg + sg);
+    float u[8][3], ag[8][3], aD[8][6];
+    {  // the first cell's -x face into the slots of the +x face (shifted in below)
+      const int4 va = __ldg(d.cell_v + 2 * seg.x), vb4 = __ldg(d.cell_v + 2 * seg.x + 1);
+      const unsigned f[4] = {(unsigned)va.x, (unsigned)va.z, (unsigned)vb4.x, (unsigned)vb4.z};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float* p = d.u + ((f[k] * G + eg) * 3u * 32u + lane);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) { u[2 * k + 1][c] = p[32 * c]; ag[2 * k + 1][c] = 0.f; }
+#pragma unroll
+        for (int c = 0; c < 6; ++c) aD[2 * k + 1][c] = 0.f;
+      }
+    }
+    for (int cidx = seg.x; cidx < seg.x + seg.y; ++cidx) {
+      const int4 va = __ldg(d.cell_v + 2 * cidx), vb4 = __ldg(d.cell_v + 2 * cidx + 1);
+      const unsigned fix = __ldg(d.cell_fix + cidx);
+      const float4 caa = __ldg(d.cell_aa + cidx);
+      const float inv[3] = {caa.x, caa.y, caa.z};
+      const unsigned vb[8] = {(unsigned)va.x * G + eg, (unsigned)va.y * G + eg, (unsigned)va.z * G + eg,
+                              (unsigned)va.w * G + eg, (unsigned)vb4.x * G + eg, (unsigned)vb4.y * G + eg,
+                              (unsigned)vb4.z * G + eg, (unsigned)vb4.w * G + eg};
+      // shift the previous cell's +x face into this cell's -x face, load the new +x face
+      // (loading rows 1 and 5 just before their first pair measured 187.8 vs 184.6 us)
+#pragma unroll
+      for (int k = 0; k < 8; k += 2) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) { u[k][c] = u[k + 1][c]; ag[k][c] = ag[k + 1][c]; ag[k + 1][c] = 0.f; }
+#pragma unroll
+        for (int c = 0; c < 6; ++c) { aD[k][c] = aD[k + 1][c]; aD[k + 1][c] = 0.f; }
+        const float* p = d.u + (vb[k + 1] * 3u * 32u + lane);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) u[k + 1][c] = p[32 * c];
+      }
+      auto flush = [&](int s) {
+        if (fix & (1u << s)) return;
+        float* pg = d.g + (vb[s] * 3u * 32u + lane);
+        float* pd = d.D + (vb[s] * 6u * 32u + lane);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) atomicAdd(pg + 32 * c, ag[s][c]);
+#pragma unroll
+        for (int c = 0; c < 6; ++c) atomicAdd(pd + 32 * c, aD[s][c]);
+      };
+      const float w = h2 * caa.w, sl = sqrtf(w * l2);
+      const float invc[3] = {inv[0] * sl, inv[1] * sl, inv[2] * sl};
+      pair_grad_acc<1>(u, inv, invc, mu, l2, w, esum, ag, aD);  // corners 0 2 3 6 7
+      flush(2);
+      pair_grad_acc<2>(u, inv, invc, mu, l2, w, esum, ag, aD);  // corners 0 4 5 6 7
+      flush(4);
+      flush(6);
+      pair_grad_acc<0>(u, inv, invc, mu, l2, w, esum, ag, aD);  // corners 0 1 3 5 7
+      flush(0);
+      if (cidx == seg.x + seg.y - 1) {
+        flush(1);
+        flush(3);
+        flush(5);
+        flush(7);
+      }
+    }
+  }
+  if (act) atomicAdd(d.acc + (size_t)A_EEL * d.Es + e, esum);
+}
+
 // ------------------------------------------------------------------ a7: curvature
 // p^T H_e p = h^2 V [mu |dF|^2 + lambda' (cof F : dF)^2 + 2 (lambda'(J-1) - mu) F : cof(dF)]  (App. B)
 
@@ -3187,7 +3266,10 @@ void launch_eval(const Dev& d, double h, cudaStream_t s) {
   // 66 % warp utilisation in the rounds and 2 CTAs/SM; the coalesced red.add scatter stays)
   if (d.ncells > 0) {
     dim3 g = cellgrid(d);
-    if (d.cells_all_aa) LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad_cells<true>, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
+    if (d.rows) {
+      const int gy = (d.nseg + 7) / 8;  // one segment per warp
+      LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad_rows, dim3(gy, g.x), dim3(32, 8), 0, d, (float)(h * h));
+    } else if (d.cells_all_aa) LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad_cells<true>, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
     else LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad_cells<false>, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
   }
   if (d.nrest > 0) {
@@ -3240,6 +3322,8 @@ void launch_curvature(const Dev& d, double h, cudaStream_t s) {
   if (fork) cudaEventRecord(d.ev_join, cs);
   if (d.nrest == 0) {  // every tet is in a Kuhn cell: register-blocked cells
     dim3 g = cellgrid(d);
+    // (a row-marching curvature pass -- u and p of the shared face carried -- measured 125 vs
+    // 114 us: this pass is FMA-bound and the carried rows cost spills)
     if (d.cells_all_aa) LAUNCHP(KID_ELEM_CURV, s, k_elem_curv_cells<true>, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
     else LAUNCHP(KID_ELEM_CURV, s, k_elem_curv_cells<false>, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
   } else {

@@ -22,7 +22,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROUND = os.environ.get("PROFILE_ROUND", "r02")  # file prefix of the summaries
 ROOT = os.path.dirname(HERE)
 # bench.py profile names of the kernels (tac_profile_kernel_name)
-PROFILE_NAME = {"k_elem_grad_cells": "elem_grad", "k_elem_curv_cells": "elem_curv", "k_vert_pre": "vert_pre",
+PROFILE_NAME = {"k_elem_grad_cells": "elem_grad", "k_elem_grad_rows": "elem_grad", "k_elem_curv_cells": "elem_curv", "k_vert_pre": "vert_pre",
                 "k_dir_reduce": "dir_reduce", "k_dir_apply": "dir_apply", "k_contact_classify_staged": "contact_classify",
                 "k_contact_curv_staged": "contact_curv", "k_contact_curv_direct": "contact_curv", "k_contact_friction": "contact_friction",
                 "k_contact_near<2>": "contact_near_ee", "k_contact_near<0>": "contact_near_gi",

@@ -1,0 +1,6 @@
+# interleaved A/B of in-tree builds (libtac_a.so vs libtac_b.so) on C3; extra env per variant
+run() { tag=$1; shift; env "$@" timeout 300 python bench.py --no-cpu-baseline > gpurun_out/ab_$tag.json 2>gpurun_out/ab_$tag.err; }
+for r in 1 2; do
+  run a$r TAC_LIB=paper_2603_28475_b200/libtac_a.so
+  run b$r TAC_LIB=paper_2603_28475_b200/libtac_b.so
+done
