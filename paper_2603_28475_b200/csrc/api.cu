@@ -812,6 +812,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     delete sim;
     return fail(TAC_EINVAL, "more than 65535 gel-surface or indenter vertices");
   }
+  d.remap_blocks = getenv("TAC_REMAP_BLOCKS") ? std::max(0, atoi(getenv("TAC_REMAP_BLOCKS"))) : 128;
   d.contact_bps = getenv("TAC_CONTACT_BPS") ? std::max(1, atoi(getenv("TAC_CONTACT_BPS"))) : 8;
   d.contact_smem = contact_smem_bytes(d.nsv, niv);
   if (d.contact_smem == 0) {
@@ -996,7 +997,9 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
         (rc = zalloc(sim, 4 * (size_t)d.Es, &d.emat)) || (rc = zalloc(sim, 2 * (size_t)d.Es, &d.edbl)) ||
         (rc = zalloc(sim, (size_t)kNAcc * d.Es, &d.acc)) || (rc = zalloc(sim, (size_t)kNAccU * d.Es, &d.accu)) ||
         (rc = zalloc(sim, (size_t)d.Es, &d.dalpha)) || (rc = zalloc(sim, (size_t)d.Es, &d.beta)) ||
-        (rc = zalloc(sim, (size_t)d.Es, &d.run)) || (rc = zalloc(sim, (size_t)d.Es, &d.pcf)) ||
+        (rc = zalloc(sim, (size_t)d.Es, &d.run)) || (rc = zalloc(sim, (size_t)d.Es, &d.alist)) ||
+        (rc = zalloc(sim, (size_t)d.Es / 32 + 1, &d.glist)) || (rc = zalloc(sim, (size_t)2, &d.anum)) ||
+        (rc = zalloc(sim, (size_t)1, &d.adone)) || (rc = zalloc(sim, (size_t)d.Es, &d.pcf)) ||
         (rc = zalloc(sim, 2 * (size_t)d.E * d.kmax, &d.cand)) || (rc = zalloc(sim, (size_t)d.E, &d.lbuf)) || (rc = zalloc(sim, 2 * (size_t)d.E * d.kmax, &d.cgeo)) || (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.cgap)) || (rc = zalloc(sim, 2 * (size_t)d.E * d.kmax, &d.ccorn)) || (rc = zalloc(sim, (size_t)d.E * d.kmax, &d.ncorn)) || (rc = zalloc(sim, 2 * (size_t)d.E, &d.ncand)) || (rc = zalloc(sim, 3 * (size_t)d.E * d.kmax, &d.nearl)) ||
         (rc = zalloc(sim, 3 * (size_t)d.E, &d.nnear)) ||
         (rc = zalloc(sim, 6 * (size_t)std::max(1, d.nsv) * d.Es, &d.Dcon)) ||

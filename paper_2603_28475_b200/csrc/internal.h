@@ -188,6 +188,11 @@ struct Dev {
   const float4* cell_aa;         // [ncells] axis-aligned box (corner bit b along axis b): (1/s0, 1/s1, 1/s2, tet volume), else 0
   int cells_all_aa;              // every cell axis-aligned: the cell kernels compile the stored-B branch out
   const int2* cell_seg;          // [nseg] (first cell, count): runs of cells along corner bit 0 (cell order is chain order)
+  int* alist;                    // [E] tolerance mode: envs evaluating next (run bit 0), built by k_alpha's last block
+  int* glist;                    // [Es / 32] env groups holding one of them
+  int* anum;                     // [2] sizes of alist / glist; -1: not built (identity mappings)
+  unsigned* adone;               // k_alpha's block counter (last block builds the lists, resets it)
+  int remap_blocks;              // tolerance mode: CTAs dealt over the active envs' contact passes when few iterate
   int nseg, rows;                // rows: the gradient pass marches along the segments (all cells axis-aligned)
   const int* rest_tets;          // [nrest] tets not in any cell
   double t1[3], t2[3], nrm[3];

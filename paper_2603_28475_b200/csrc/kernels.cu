@@ -582,6 +582,7 @@ __global__ void k_step_setup(Dev d, const float* poses, unsigned long long step)
   d.dalpha[e] = 0.f;
   d.beta[e] = 0.f;
   d.run[e] = 1;
+  if (e == 0) { d.anum[0] = -1; d.anum[1] = -1; }  // no active lists yet: identity block mappings
   d.ncand[d.lbuf[e] * d.E + e] = 0;
   d.nanc[e] = 0;
   for (int k = 0; k < kNAcc; ++k) d.acc[(size_t)k * d.Es + e] = 0.0;
@@ -934,13 +935,40 @@ __global__ void k_anchors(Dev d, double h2) {
 // ------------------------------------------------------------------ a4: vertex pre-pass
 // applies the pending update u += dalpha p (a8), then the inertia term
 // 1/2 m |u - u^|^2, g = m (u - u^), D = m I (lumped M)
+// ---- env-group grids of the vertex and element passes (one block dimension = the Es / 32
+// groups of 32 envs, the other = chunks of the vertex / cell loop).  In the tolerance mode, once
+// at most half the groups hold an env of k_alpha's list, the blocks of the idle groups are dealt
+// to the listed groups (each gets up to cap chunks instead of its own row of the grid); otherwise
+// (and in the fixed mode) the mapping is the identity.  ng_grid: the group index of this block
+// in the launch grid, nc / c: chunks per group and this block's chunk.
+__device__ __forceinline__ bool group_block(const Dev& d, int cap, int ng_grid, int c, int nc, int& grp, int& bc,
+                                            int& nbc) {
+  grp = ng_grid;
+  bc = c;
+  nbc = nc;
+  const int G = d.Es >> 5;
+  if (d.fixed_iters > 0 || G < 2 || nc >= cap) return true;
+  const int n_g = d.anum[1];
+  if (n_g <= 0 || 2 * n_g > G) return true;
+  const int per = min(cap, (G * nc) / n_g);
+  if (per <= nc) return true;
+  const int lin = ng_grid * nc + c, idx = lin / per;
+  if (idx >= n_g) return false;
+  bc = lin - idx * per;
+  nbc = per;
+  grp = d.glist[idx];
+  return true;
+}
+
 __global__ void k_vert_pre(Dev d, float h2) {
   TAC_PDL_WAIT();
-  int e = blockIdx.x * 32 + threadIdx.x;
+  int grp, by, nby;
+  if (!group_block(d, (d.nv + 7) / 8, blockIdx.x, blockIdx.y, gridDim.y, grp, by, nby)) return;
+  int e = grp * 32 + threadIdx.x;
   bool act = e < d.E && (d.run[e] & 1);
   if (!__any_sync(0xffffffffu, act)) return;
   float da = act ? d.dalpha[e] : 0.f;
-  if (act && blockIdx.y == 0 && threadIdx.y == 0) {  // near lists are rebuilt by the contact classification
+  if (act && by == 0 && threadIdx.y == 0) {  // near lists are rebuilt by the contact classification
     d.nnear[3 * e] = 0; d.nnear[3 * e + 1] = 0; d.nnear[3 * e + 2] = 0;
     EnvS& s = d.es[e];
     if (s.pending && s.iter >= s.reb_iter + 1) {  // R16 pipeline: the list rebuilt during the last
@@ -955,8 +983,8 @@ __global__ void k_vert_pre(Dev d, float h2) {
   double ein = 0;
   // two vertices per iteration, every load issued before any store (the stores to u
   // could otherwise alias the next loads and serialise them): twice the bytes in flight
-  const int stride = gridDim.y * 8;
-  for (int v0 = blockIdx.y * 8 + threadIdx.y; v0 < d.nv; v0 += 2 * stride) {
+  const int stride = nby * 8;
+  for (int v0 = by * 8 + threadIdx.y; v0 < d.nv; v0 += 2 * stride) {
     float u[2][3], pv[2][3], uh[2][3], m[2], sm[2];
     int si[2];
     bool ok[2];
@@ -1009,7 +1037,7 @@ __global__ void k_vert_pre(Dev d, float h2) {
   }
   if (act && ein != 0.0) atomicAdd(d.acc + (size_t)A_EIN * d.Es + e, ein);
   if (d.dedup && act)  // R33: this evaluation's constraint table starts empty
-    for (int sl = blockIdx.y * 8 + threadIdx.y; sl < kDedupSlots; sl += gridDim.y * 8) d.dtab[(size_t)sl * d.Es + e] = 0ull;
+    for (int sl = by * 8 + threadIdx.y; sl < kDedupSlots; sl += nby * 8) d.dtab[(size_t)sl * d.Es + e] = 0ull;
 }
 
 // ------------------------------------------------------------------ a4: element gradient
@@ -1287,13 +1315,15 @@ __device__ __forceinline__ void pair_grad_acc(const float (*u)[3], const float* 
 template <bool ALL_AA>
 __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
   TAC_PDL_WAIT();
-  const int e = blockIdx.y * 32 + threadIdx.x;
+  int grp, bx, nbx;
+  if (!group_block(d, (d.ncells + 7) / 8, blockIdx.y, blockIdx.x, gridDim.x, grp, bx, nbx)) return;
+  const int e = grp * 32 + threadIdx.x;
   const bool act = e < d.E && (d.run[e] & 1);
   if (!__any_sync(0xffffffffu, act)) return;
   const float mu = d.emat[e], l2 = d.emat[d.Es + e];  // per-env material
-  const unsigned G = (unsigned)(d.Es >> 5), eg = (unsigned)blockIdx.y, lane = threadIdx.x;
+  const unsigned G = (unsigned)(d.Es >> 5), eg = (unsigned)grp, lane = threadIdx.x;
   double esum = 0;
-  for (int cidx = blockIdx.x * 8 + threadIdx.y; cidx < d.ncells; cidx += gridDim.x * 8) {
+  for (int cidx = bx * 8 + threadIdx.y; cidx < d.ncells; cidx += nbx * 8) {
     const int4 va = __ldg(d.cell_v + 2 * cidx), vb4 = __ldg(d.cell_v + 2 * cidx + 1);
     const unsigned fix = __ldg(d.cell_fix + cidx);
     const float4 caa = __ldg(d.cell_aa + cidx);
@@ -1454,13 +1484,15 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
 // pair 0), so at most 6 corners' accumulators are live, as in the one-cell pass.
 __global__ void __launch_bounds__(256, 2) k_elem_grad_rows(Dev d, float h2) {
   TAC_PDL_WAIT();
-  const int e = blockIdx.y * 32 + threadIdx.x;
+  int grp, bx, nbx;
+  if (!group_block(d, (d.nseg + 7) / 8, blockIdx.y, blockIdx.x, gridDim.x, grp, bx, nbx)) return;
+  const int e = grp * 32 + threadIdx.x;
   const bool act = e < d.E && (d.run[e] & 1);
   if (!__any_sync(0xffffffffu, act)) return;
   const float mu = d.emat[e], l2 = d.emat[d.Es + e];  // per-env material
-  const unsigned G = (unsigned)(d.Es >> 5), eg = (unsigned)blockIdx.y, lane = threadIdx.x;
+  const unsigned G = (unsigned)(d.Es >> 5), eg = (unsigned)grp, lane = threadIdx.x;
   double esum = 0;
-  for (int sg = blockIdx.x * 8 + threadIdx.y; sg < d.nseg; sg += gridDim.x * 8) {
+  for (int sg = bx * 8 + threadIdx.y; sg < d.nseg; sg += nbx * 8) {
     if (!act) continue;
     const int2 seg = __ldg(d.cell_seg + sg);
     float u[8][3], ag[8][3], aD[8][6];
@@ -1533,13 +1565,15 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_rows(Dev d, float h2) {
 template <bool ALL_AA>
 __global__ void __launch_bounds__(256, 2) k_elem_curv_cells(Dev d, float h2) {
   TAC_PDL_WAIT();
-  const int e = blockIdx.y * 32 + threadIdx.x;
+  int grp, bx, nbx;
+  if (!group_block(d, (d.ncells + 7) / 8, blockIdx.y, blockIdx.x, gridDim.x, grp, bx, nbx)) return;
+  const int e = grp * 32 + threadIdx.x;
   const bool act = e < d.E && (d.run[e] & 2);
   if (!__any_sync(0xffffffffu, act)) return;
   const float mu = d.emat[e], l2 = d.emat[d.Es + e];  // per-env material
-  const unsigned G = (unsigned)(d.Es >> 5), eg = (unsigned)blockIdx.y, lane = threadIdx.x;
+  const unsigned G = (unsigned)(d.Es >> 5), eg = (unsigned)grp, lane = threadIdx.x;
   double qsum = 0;
-  for (int cidx = blockIdx.x * 8 + threadIdx.y; cidx < d.ncells; cidx += gridDim.x * 8) {
+  for (int cidx = bx * 8 + threadIdx.y; cidx < d.ncells; cidx += nbx * 8) {
     const int4 va = __ldg(d.cell_v + 2 * cidx), vb4 = __ldg(d.cell_v + 2 * cidx + 1);
     const float4 caa = __ldg(d.cell_aa + cidx);
     const bool aa = ALL_AA || caa.w > 0.f;  // warp-uniform (one cell per warp)
@@ -1754,11 +1788,39 @@ __device__ __forceinline__ void scatter_gel_free(const Dev& d, int v, int sl, in
 }
 
 
+// ---- per-env contact grids: gridDim.x blocks per env x E.  In the tolerance mode, once few
+// envs are still iterating (the tail of a step: n < remap_blocks / gridDim.x), the blocks are
+// dealt over the envs of k_alpha's list (alist, the envs evaluating next) -- each gets up to
+// min(kMaxEnvBlocks, remap_blocks / n) blocks, so a straggler's contact passes are not run by
+// one CTA while the GPU idles.  With more envs active, without a list (fixed mode, the first
+// evaluation of a step) the mapping is the identity (e = blockIdx.y, bx = blockIdx.x): splitting
+// many envs over more CTAs only repeats per-CTA setup (measured, tools/diag_tail.py).  The
+// curvature passes (bit 2) use the same list: their envs are a subset of the evaluated ones.
+constexpr int kMaxEnvBlocks = 64;
+__device__ __forceinline__ bool env_block(const Dev& d, int bit, int& e, int& bx, int& nbx) {
+  bx = blockIdx.x;
+  nbx = gridDim.x;
+  if (d.fixed_iters <= 0 && (int)gridDim.x < kMaxEnvBlocks) {
+    const int n = d.anum[0], T = gridDim.x * gridDim.y;  // (n * per <= T: every listed env gets all per blocks)
+    const int per = n > 0 ? min(kMaxEnvBlocks, min(d.remap_blocks, T) / n) : 0;
+    if (per > (int)gridDim.x) {
+      const int lin = blockIdx.y * gridDim.x + blockIdx.x, idx = lin / per;
+      if (idx >= n) return false;
+      nbx = per;
+      bx = lin - idx * per;
+      e = d.alist[idx];
+      return (d.run[e] & bit) != 0;
+    }
+  }
+  e = blockIdx.y;
+  return e < d.E && (d.run[e] & bit);
+}
+
 template <int KIND, bool MOLL = false>  // MOLL: edge-edge mollifier (R30), KIND 2 only
 __global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
   TAC_PDL_WAIT();
-  int e = blockIdx.y;
-  if (e >= d.E || !(d.run[e] & 1)) return;
+  int e, bx, nbx;
+  if (!env_block(d, 1, e, bx, nbx)) return;
   const double kappa = h2 * d.edbl[e];  // h^2 kappa_phys of this env
   const EnvS& s = d.es[e];
   __shared__ double R[9], c[3];
@@ -1775,7 +1837,7 @@ __global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
   constexpr float kNearScreen = 1e-6f;
   const float far2 = ((float)d.dhat + kNearScreen) * ((float)d.dhat + kNearScreen);
   bool far = false;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+  for (int j = bx * blockDim.x + threadIdx.x; j < n; j += nbx * blockDim.x) {
     const uint2 cw = list[j];
     const unsigned id[4] = {cw.x & 0xffffu, cw.x >> 16, cw.y & 0xffffu, cw.y >> 16};
     bool ind[4];
@@ -1942,8 +2004,8 @@ __global__ void __launch_bounds__(1024) k_sort_anchors(Dev d, Anchor* out) {
 // mu lambda f1(s) per anchor for the curvature pass
 __global__ void __launch_bounds__(128) k_contact_friction(Dev d, double eps_f) {
   TAC_PDL_WAIT();
-  int e = blockIdx.y;
-  if (e >= d.E || !(d.run[e] & 1)) return;
+  int e, bx, nbx;
+  if (!env_block(d, 1, e, bx, nbx)) return;
   const EnvS& s = d.es[e];
   __shared__ double R[9], c[3];
   __shared__ double smr[4 * 20];
@@ -1955,7 +2017,7 @@ __global__ void __launch_bounds__(128) k_contact_friction(Dev d, double eps_f) {
   const int na = min(d.nanc[e], d.amax);
   const int lane = threadIdx.x & 31;
   // warp-uniform trip count (the aggregated scatter is a warp collective)
-  for (int b0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); b0 < na; b0 += gridDim.x * blockDim.x) {
+  for (int b0 = bx * blockDim.x + (threadIdx.x & ~31); b0 < na; b0 += nbx * blockDim.x) {
     const int i = b0 + lane;
     // per-corner terms are formed at their reduction from a few shared factors (force
     // direction, T T^T entries, f1 and the corner weights), not held as 3 x 9 values
@@ -2100,7 +2162,10 @@ __device__ __forceinline__ void push_local(bool mine, int lane, int* cnt, unsign
   if (slot < cap) list[slot] = (unsigned short)off;
   else glist[atomicAdd(gcnt, 1)] = cw;  // local list full: direct global append
 }
-template <bool BODY>
+// REMAP (tolerance mode): env_block's mapping and shorter chunks for a straggler's extra CTAs;
+// the fixed mode's instantiation keeps the identity mapping and compile-time chunks (the
+// runtime chunk length measured 171 -> 191 us per launch at C3)
+template <bool BODY, bool REMAP>
 __global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
   TAC_PDL_WAIT();
   // BODY: the test runs in the indenter's body frame (separation along an axis of any
@@ -2117,10 +2182,21 @@ __global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
   __shared__ unsigned short nl[3][kClassNL];
   __shared__ int qn, nn[3], nbase[3];
   __shared__ double Rs[9], cs[3];
-  int e = blockIdx.y;
-  if (e >= d.E || !(d.run[e] & 1)) return;
+  int e, bx, nbx;
+  if constexpr (REMAP) {
+    if (!env_block(d, 1, e, bx, nbx)) return;
+  } else {
+    e = blockIdx.y;
+    bx = blockIdx.x;
+    nbx = gridDim.x;
+    if (e >= d.E || !(d.run[e] & 1)) return;
+  }
   const int lb = d.lbuf[e];
-  if ((int)blockIdx.x * kClassChunk >= min(d.ncand[lb * d.E + e], d.kmax)) return;  // no chunk: skip the staging
+  const int n = min(d.ncand[lb * d.E + e], d.kmax);
+  // chunk length: kClassChunk, or less (>= 1024: every CTA stages the whole env) when the env
+  // has more blocks than kClassChunk-chunks
+  const int cl = REMAP ? min(kClassChunk, max(1024, ((n + nbx - 1) / nbx + 255) & ~255)) : kClassChunk;
+  if (bx * cl >= n) return;  // no chunk: skip the staging
   const EnvS& s = d.es[e];
   float4* sx = reinterpret_cast<float4*>(shc4);                           // [nsv] gel surface
   float4* sy = reinterpret_cast<float4*>(shc4 + sizeof(float4) * d.nsv);  // [niv] c + R Y (gel frame only)
@@ -2184,7 +2260,6 @@ __global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
   const bool cached = s.cache_ok;
   const double odo = s.odo, thr = d.dhat + odo;
   const float dh = (float)d.dhat + kClassMargin;
-  const int n = min(d.ncand[lb * d.E + e], d.kmax);
   const unsigned long long* cand = d.cand + cand_off(d, lb, e);
   float* hc = d.cgap + (size_t)e * d.kmax;
   const uint2* ccorn = d.ccorn + cand_off(d, lb, e);
@@ -2192,7 +2267,7 @@ __global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
   uint2* glist = d.nearl + (size_t)e * 3 * d.kmax;
   const int lane = threadIdx.x & 31;
   bool any_far = false;
-  for (int c0 = blockIdx.x * kClassChunk; c0 < n; c0 += gridDim.x * kClassChunk) {
+  for (int c0 = bx * cl; c0 < n; c0 += nbx * cl) {
     if (threadIdx.x < 3) nn[threadIdx.x] = 0;
     if (threadIdx.x == 0) qn = 0;
     __syncthreads();  // (also orders the staging above before phase B)
@@ -2201,12 +2276,12 @@ __global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
 #pragma unroll
     for (int k = 0; k < kClassA; ++k) {
       const int i = c0 + k * 256 + threadIdx.x;
-      h[k] = (cached && i < n) ? hc[i] : -INFINITY;
+      h[k] = (cached && i < n && k * 256 + (int)threadIdx.x < cl) ? hc[i] : -INFINITY;
     }
 #pragma unroll
     for (int k = 0; k < kClassA; ++k) {
       const int off = k * 256 + threadIdx.x;
-      const bool in = c0 + off < n;
+      const bool in = off < cl && c0 + off < n;
       const bool hit = in && (double)h[k] >= thr;
       any_far |= hit;
       const bool need = in && !hit;
@@ -2300,8 +2375,8 @@ __global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
 __global__ void __launch_bounds__(256) k_contact_curv_staged(Dev d, double h2) {
   TAC_PDL_WAIT();
   extern __shared__ __align__(16) char shc3[];
-  int e = blockIdx.y;
-  if (e >= d.E || !(d.run[e] & 2)) return;
+  int e, bx, nbx;
+  if (!env_block(d, 2, e, bx, nbx)) return;
   const double kappa = h2 * d.edbl[e];  // h^2 kappa_phys of this env
   const EnvS& s = d.es[e];
   __shared__ double R[9], pr[6];
@@ -2325,7 +2400,7 @@ __global__ void __launch_bounds__(256) k_contact_curv_staged(Dev d, double h2) {
   };
   double q = 0, amin = INFINITY;
   const int n0 = d.nnear[3 * e], n1 = d.nnear[3 * e + 1], n = n0 + n1 + d.nnear[3 * e + 2];
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+  for (int j = bx * blockDim.x + threadIdx.x; j < n; j += nbx * blockDim.x) {
     const int kk = j < n0 ? 0 : (j < n0 + n1 ? 1 : 2);
     // near-ordered geometry and corners (written by k_contact_near at this position)
     const size_t slot = (size_t)e * d.kmax + j;
@@ -2359,7 +2434,7 @@ __global__ void __launch_bounds__(256) k_contact_curv_staged(Dev d, double h2) {
     if (l > 0) amin = fmin(amin, (1 - d.ccd_s) * dist / l);
   }
   const int na = min(d.nanc[e], d.amax);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
+  for (int i = bx * blockDim.x + threadIdx.x; i < na; i += nbx * blockDim.x) {
     const Anchor& A = d.anc[(size_t)e * d.amax + i];
     const unsigned sid[3] = {A.sid01 & 0xffffu, A.sid01 >> 16, A.sid2};
     // indenter side folded: sig p_c + p_theta x (R Y_w)
@@ -2395,8 +2470,8 @@ __global__ void __launch_bounds__(256) k_contact_curv_staged(Dev d, double h2) {
 // indenter per CTA
 __global__ void __launch_bounds__(128) k_contact_curv_direct(Dev d, double h2) {
   TAC_PDL_WAIT();
-  int e = blockIdx.y;
-  if (e >= d.E || !(d.run[e] & 2)) return;
+  int e, bx, nbx;
+  if (!env_block(d, 2, e, bx, nbx)) return;
   const double kappa = h2 * d.edbl[e];  // h^2 kappa_phys of this env
   const EnvS& s = d.es[e];
   __shared__ double R[9], pr[6];
@@ -2418,7 +2493,7 @@ __global__ void __launch_bounds__(128) k_contact_curv_direct(Dev d, double h2) {
   };
   double q = 0, amin = INFINITY;
   const int n0 = d.nnear[3 * e], n1 = d.nnear[3 * e + 1], n = n0 + n1 + d.nnear[3 * e + 2];
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+  for (int j = bx * blockDim.x + threadIdx.x; j < n; j += nbx * blockDim.x) {
     const int kk = j < n0 ? 0 : (j < n0 + n1 ? 1 : 2);
     // near-ordered geometry and corners (written by k_contact_near at this position)
     const size_t slot = (size_t)e * d.kmax + j;
@@ -2455,7 +2530,7 @@ __global__ void __launch_bounds__(128) k_contact_curv_direct(Dev d, double h2) {
     if (l > 0) amin = fmin(amin, (1 - d.ccd_s) * dist / l);
   }
   const int na = min(d.nanc[e], d.amax);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
+  for (int i = bx * blockDim.x + threadIdx.x; i < na; i += nbx * blockDim.x) {
     const Anchor& A = d.anc[(size_t)e * d.amax + i];
     const unsigned sid[3] = {A.sid01 & 0xffffu, A.sid01 >> 16, A.sid2};
     // indenter side folded: sig p_c + p_theta x (R Y_w)
@@ -2632,14 +2707,16 @@ template <bool SURF>
 __global__ void __launch_bounds__(256) k_dir_reduce(Dev d) {
   TAC_PDL_WAIT();
   constexpr int NB = SURF ? 1 : 2;
-  int e = blockIdx.x * 32 + threadIdx.x;
+  int grp, by, nby;
+  if (!group_block(d, ((SURF ? d.nsv : d.nv) + 7) / 8, blockIdx.x, blockIdx.y, gridDim.y, grp, by, nby)) return;
+  int e = grp * 32 + threadIdx.x;
   bool act = e < d.E && (d.run[e] & 3);  // speculative: k_accept may run concurrently (see launch_eval)
   if (!__any_sync(0xffffffffu, act)) return;
   double gPy = 0, yp = 0, yPy = 0, pg = 0, gPg = 0, gg = 0, pp = 0;
   float pgmax = 0.f;
-  const int stride = gridDim.y * 8;
+  const int stride = nby * 8;
   const int n = SURF ? d.nsv : d.nv;
-  for (int i0 = blockIdx.y * 8 + threadIdx.y; i0 < n; i0 += NB * stride) {  // NB vertices in flight
+  for (int i0 = by * 8 + threadIdx.y; i0 < n; i0 += NB * stride) {  // NB vertices in flight
     float g[NB][3], gq[NB][3], p[NB][3], D[NB][6];
     int vv[NB];
     bool ok[NB];
@@ -2805,15 +2882,17 @@ __global__ void k_dir_scalar(Dev d) {
 // p = -P g + beta p_prev; g_prev = g; M = max |p_v|, L_rel = max_surface |p_v - p_c|, inertia p^T M p
 __global__ void __launch_bounds__(256) k_dir_apply(Dev d) {
   TAC_PDL_WAIT();
-  int e = blockIdx.x * 32 + threadIdx.x;
+  int grp, by, nby;
+  if (!group_block(d, (d.nv + 7) / 8, blockIdx.x, blockIdx.y, gridDim.y, grp, by, nby)) return;
+  int e = grp * 32 + threadIdx.x;
   bool act = e < d.E && (d.run[e] & 2);
   if (!__any_sync(0xffffffffu, act)) return;
   float beta = act ? d.beta[e] : 0.f;
   float4 pc = act ? d.pcf[e] : make_float4(0, 0, 0, 0);
   float M = 0.f, L = 0.f;
   double q = 0;
-  const int stride = gridDim.y * 8;
-  for (int v0 = blockIdx.y * 8 + threadIdx.y; v0 < d.nv; v0 += 2 * stride) {  // loads of two vertices first
+  const int stride = nby * 8;
+  for (int v0 = by * 8 + threadIdx.y; v0 < d.nv; v0 += 2 * stride) {  // loads of two vertices first
     float g[2][3], Pgv[2][3], po[2][3], m[2];
     int si[2];
     bool ok[2];
@@ -2897,10 +2976,48 @@ __device__ void commit_alpha(const Dev& d, EnvS& s, int e, double a, double L) {
 // next k_vert_pre, on a side stream concurrent with the element pass.  kRebuildAt keeps a
 // later cap from cutting a step below half of alpha_upper.
 constexpr double kRebuildAt = 0.75;
+__device__ void alpha_env(const Dev& d, double h, int e);
+// tolerance mode: the block that finishes last lists the envs that evaluate next (run bit 0)
+// and their groups for the next evaluation's block mappings (env_block / group_block)
+__device__ void build_active_lists(const Dev& d) {
+  __shared__ int last;
+  __syncthreads();
+  __threadfence();
+  if (threadIdx.x == 0) last = atomicAdd(d.adone, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last || threadIdx.x >= 32) return;
+  __threadfence();
+  const int lane = threadIdx.x;
+  int n = 0, ng = 0;
+  for (int base = 0; base < d.E; base += 1024) {
+    int f[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int en = base + 32 * j + lane;
+      f[j] = en < d.E ? __ldcg(d.run + en) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const unsigned m = __ballot_sync(0xffffffffu, f[j] & 1);
+      if (f[j] & 1) d.alist[n + __popc(m & ((1u << lane) - 1))] = base + 32 * j + lane;
+      n += __popc(m);
+      if (m && lane == 0) d.glist[ng] = (base >> 5) + j;
+      ng += m != 0u;
+    }
+  }
+  if (lane == 0) {
+    d.anum[0] = n;
+    d.anum[1] = ng;
+    *d.adone = 0u;
+  }
+}
 __global__ void k_alpha(Dev d, double h) {
   TAC_PDL_WAIT();
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= d.E) return;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < d.E) alpha_env(d, h, e);
+  if (d.fixed_iters <= 0) build_active_lists(d);
+}
+__device__ void alpha_env(const Dev& d, double h, int e) {
   int rb = d.run[e];
   size_t Es = d.Es;
   EnvS& s = d.es[e];
@@ -3245,10 +3362,14 @@ void launch_eval(const Dev& d, double h, cudaStream_t s) {
   launch_broadphase(d, true, rs);
   if (fork) cudaEventRecord(d.ev_reb, rs);
   const size_t cls_both = sizeof(float4) * (size_t)(d.nsv + d.niv);  // [nsv] X + u, [niv] c + R Y
-  if (cls_both > 64 * 1024)  // body frame: stage the gel side only
-    LAUNCHP(KID_CONTACT_CLASSIFY, cs, k_contact_classify_staged<true>, sgrid(d), 256, sizeof(float4) * (size_t)d.nsv, d);
-  else
-    LAUNCHP(KID_CONTACT_CLASSIFY, cs, k_contact_classify_staged<false>, sgrid(d), 256, cls_both, d);
+  const bool remap = d.fixed_iters <= 0;
+  if (cls_both > 64 * 1024) {  // body frame: stage the gel side only
+    if (remap) LAUNCHP(KID_CONTACT_CLASSIFY, cs, (k_contact_classify_staged<true, true>), sgrid(d), 256, sizeof(float4) * (size_t)d.nsv, d);
+    else LAUNCHP(KID_CONTACT_CLASSIFY, cs, (k_contact_classify_staged<true, false>), sgrid(d), 256, sizeof(float4) * (size_t)d.nsv, d);
+  } else {
+    if (remap) LAUNCHP(KID_CONTACT_CLASSIFY, cs, (k_contact_classify_staged<false, true>), sgrid(d), 256, cls_both, d);
+    else LAUNCHP(KID_CONTACT_CLASSIFY, cs, (k_contact_classify_staged<false, false>), sgrid(d), 256, cls_both, d);
+  }
   const double kap = h * h;  // kernels scale by their env's kappa_phys
   if (fork) {
     cudaEventRecord(d.ev_cls, cs);
@@ -3389,8 +3510,10 @@ void kernels_init(int contact_smem) {
   // process (different meshes) share it, so it is set to the cap contact_smem_bytes
   // enforces rather than to this simulator's size (occupancy follows the launch size)
   (void)contact_smem;
-  cudaFuncSetAttribute(k_contact_classify_staged<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kContactSmemCap);
-  cudaFuncSetAttribute(k_contact_classify_staged<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kContactSmemCap);
+  cudaFuncSetAttribute(k_contact_classify_staged<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kContactSmemCap);
+  cudaFuncSetAttribute(k_contact_classify_staged<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kContactSmemCap);
+  cudaFuncSetAttribute(k_contact_classify_staged<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kContactSmemCap);
+  cudaFuncSetAttribute(k_contact_classify_staged<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kContactSmemCap);
   cudaFuncSetAttribute(k_contact_curv_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, kContactSmemCap);
   cudaFuncSetAttribute(k_elem_curv_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, kTiledCurvSmem);
 }

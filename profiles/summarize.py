@@ -35,6 +35,8 @@ def short(name):
     for t in ("<1>", "<0>", "<true>", "<false>"):
         if (n.startswith("k_elem") or n.startswith("k_contact_classify")) and n.endswith(t):
             n = n[: -len(t)]
+    if n.startswith("k_contact_classify"):  # k_contact_classify_staged<BODY, REMAP>
+        n = n.split("<")[0]
     if n.startswith("k_contact_near<"):  # k_contact_near<KIND, MOLL> -> k_contact_near<KIND>
         n = n.split(",")[0].rstrip(">") + ">"
     return n

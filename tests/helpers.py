@@ -44,3 +44,17 @@ def parallel_peg_scene(steps=2, depth=0.05e-3, start_gap=0.05e-3, offset_y=0.0):
     z = np.linspace(r + start_gap, r - depth, steps + 1)[1:]
     s.poses = np.stack([np.stack([w.pose((0, offset_y, zz), q)]) for zz in z])
     return s
+
+
+def pg_disp(o, scene, ev, rho_max):
+    """fp64 |P g|_disp of an oracle evaluation (block-Jacobi P: the 3x3 D^-1 per free vertex and
+    the rigid blocks; the convergence measure of P:465 / R12): the stationarity certificate of a
+    state, independent of the solver that produced it."""
+    free = np.setdiff1d(np.arange(len(scene.X)), scene.fixed)
+    g, D = ev["g"], ev["D"]
+    m = 0.0
+    for v in free:
+        m = max(m, np.linalg.norm(np.linalg.solve(D[v], g[v])))
+    pc = np.linalg.solve(ev["Drig"][0], ev["grig"][:3])
+    pt = np.linalg.solve(ev["Drig"][1], ev["grig"][3:])
+    return max(m, np.linalg.norm(pc) + rho_max * np.linalg.norm(pt))
