@@ -808,9 +808,9 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
   }
   sim->E0 = MT.E; sim->nu0 = MT.nu; sim->rho0 = MT.rho;
   sim->thE.assign(d.E, MT.E); sim->thNu.assign(d.E, MT.nu); sim->thRho.assign(d.E, MT.rho); sim->thMu.assign(d.E, MT.mu_f);
-  if (d.nsv >= 65536 || niv >= 65536) {  // candidate corner ids are packed 16 bit (Dev::ccorn)
+  if (d.nsv >= 16384 || niv >= 16384) {  // candidate corner ids are packed 14 bit + the kind (Dev::ccorn)
     delete sim;
-    return fail(TAC_EINVAL, "more than 65535 gel-surface or indenter vertices");
+    return fail(TAC_EINVAL, "more than 16383 gel-surface or indenter vertices");
   }
   d.remap_blocks = getenv("TAC_REMAP_BLOCKS") ? std::max(0, atoi(getenv("TAC_REMAP_BLOCKS"))) : 128;
   d.contact_bps = getenv("TAC_CONTACT_BPS") ? std::max(1, atoi(getenv("TAC_CONTACT_BPS"))) : 8;

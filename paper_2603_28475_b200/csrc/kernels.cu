@@ -465,14 +465,15 @@ __device__ __forceinline__ CornersL corners_l(const Dev& d, int kind, int a, int
   return c;
 }
 // corner ids of a candidate record packed 4 x 16 bit: gel corners by surface-local id,
-// indenter corners by vertex id (kind decides which); nsv, niv < 65536 (checked at create)
+// indenter corners by vertex id (kind decides which), 16 bits each, the pair's kind in the top
+// two bits of the last (nsv, niv < 16384, checked at create): the classification needs no other word
 __device__ __forceinline__ uint2 pack_corners(const Dev& d, unsigned long long rec) {
   int kind = (int)(rec >> 62), a = (int)((rec >> 31) & 0x7fffffffu), b = (int)(rec & 0x7fffffffu);
   CornersL C = corners_l(d, kind, a, b);
   unsigned id[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) id[k] = (unsigned)(C.ind[k] ? C.gid[k] : C.sid[k]);
-  return make_uint2(id[0] | (id[1] << 16), id[2] | (id[3] << 16));
+  return make_uint2(id[0] | (id[1] << 16), id[2] | (id[3] << 16) | ((unsigned)kind << 30));
 }
 __device__ __forceinline__ d3 gel_pos(const Dev& d, const float* u, int v, int e) {
   float4 X = d.X[v];
@@ -1839,7 +1840,7 @@ __global__ void __launch_bounds__(128) k_contact_near(Dev d, double h2) {
   bool far = false;
   for (int j = bx * blockDim.x + threadIdx.x; j < n; j += nbx * blockDim.x) {
     const uint2 cw = list[j];
-    const unsigned id[4] = {cw.x & 0xffffu, cw.x >> 16, cw.y & 0xffffu, cw.y >> 16};
+    const unsigned id[4] = {cw.x & 0xffffu, cw.x >> 16, cw.y & 0xffffu, (cw.y >> 16) & 0x3fffu};
     bool ind[4];
     d3 z[4];
 #pragma unroll
@@ -2260,7 +2261,6 @@ __global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
   const bool cached = s.cache_ok;
   const double odo = s.odo, thr = d.dhat + odo;
   const float dh = (float)d.dhat + kClassMargin;
-  const unsigned long long* cand = d.cand + cand_off(d, lb, e);
   float* hc = d.cgap + (size_t)e * d.kmax;
   const uint2* ccorn = d.ccorn + cand_off(d, lb, e);
   int* gcnt = d.nnear + 3 * e;
@@ -2302,14 +2302,14 @@ __global__ void __launch_bounds__(256) k_contact_classify_staged(Dev d) {
         const int jq = jb + t * blockDim.x + lane;
         off[t] = jq < nq ? q[jq] : -1;
         kind[t] = 0;
-        if (off[t] >= 0) { kind[t] = (int)(cand[c0 + off[t]] >> 62); cc[t] = ccorn[c0 + off[t]]; }
+        if (off[t] >= 0) { cc[t] = ccorn[c0 + off[t]]; kind[t] = (int)(cc[t].y >> 30); }
       }
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         bool near = false;
         if (off[t] >= 0) {
           const int i = c0 + off[t];
-          const unsigned id[4] = {cc[t].x & 0xffffu, cc[t].x >> 16, cc[t].y & 0xffffu, cc[t].y >> 16};
+          const unsigned id[4] = {cc[t].x & 0xffffu, cc[t].x >> 16, cc[t].y & 0xffffu, (cc[t].y >> 16) & 0x3fffu};
           // corner k is on the indenter: kind 0 (gel point, indenter triangle) k >= 1,
           // kind 1 (indenter point, gel triangle) k == 0, kind 2 (gel edge, indenter edge) k >= 2
           const int kd = kind[t], na = kd == 2 ? 2 : 1;
@@ -2405,7 +2405,7 @@ __global__ void __launch_bounds__(256) k_contact_curv_staged(Dev d, double h2) {
     // near-ordered geometry and corners (written by k_contact_near at this position)
     const size_t slot = (size_t)e * d.kmax + j;
     const uint2 cc = d.ncorn[slot];
-    const unsigned id[4] = {cc.x & 0xffffu, cc.x >> 16, cc.y & 0xffffu, cc.y >> 16};
+    const unsigned id[4] = {cc.x & 0xffffu, cc.x >> 16, cc.y & 0xffffu, (cc.y >> 16) & 0x3fffu};
     const int na = kk == 2 ? 2 : 1;
     const float4* geo = d.cgeo + 2 * slot;
     float4 g0 = geo[0], g1 = geo[1];
@@ -2498,7 +2498,7 @@ __global__ void __launch_bounds__(128) k_contact_curv_direct(Dev d, double h2) {
     // near-ordered geometry and corners (written by k_contact_near at this position)
     const size_t slot = (size_t)e * d.kmax + j;
     const uint2 cc = d.ncorn[slot];
-    const unsigned id[4] = {cc.x & 0xffffu, cc.x >> 16, cc.y & 0xffffu, cc.y >> 16};
+    const unsigned id[4] = {cc.x & 0xffffu, cc.x >> 16, cc.y & 0xffffu, (cc.y >> 16) & 0x3fffu};
     const int na = kk == 2 ? 2 : 1;
     const float4* geo = d.cgeo + 2 * slot;
     float4 g0 = geo[0], g1 = geo[1];
