@@ -1229,8 +1229,13 @@ static bool run_while_loop(tac_sim* sim, double h, int K, cudaStream_t s) {
       ok = cudaStreamBeginCaptureToGraph(sim->cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) ==
            cudaSuccess;
       if (ok) {
-        launch_iterations(d, h, 1, false, sim->cap);
-        launch_loop_ctl(d, hnd, sim->d_loop, K - 1, sim->cap);
+        // loop control in k_alpha's last block (one launch per trip less than a k_loop_ctl;
+        // TAC_LOOP_CTL_KERNEL=1 keeps the separate kernel for A/B)
+        Dev dl = d;
+        const bool sep = getenv("TAC_LOOP_CTL_KERNEL") != nullptr;
+        if (!sep) { dl.loop_on = 1; dl.loop_h = hnd; dl.loop_ctr = sim->d_loop; dl.loop_limit = K - 1; }
+        launch_iterations(dl, h, 1, false, sim->cap);
+        if (sep) launch_loop_ctl(d, hnd, sim->d_loop, K - 1, sim->cap);
         cudaGraph_t out = nullptr;
         ok = cudaStreamEndCapture(sim->cap, &out) == cudaSuccess;
       }

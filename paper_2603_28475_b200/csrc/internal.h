@@ -192,6 +192,11 @@ struct Dev {
   int* glist;                    // [Es / 32] env groups holding one of them
   int* anum;                     // [2] sizes of alist / glist; -1: not built (identity mappings)
   unsigned* adone;               // k_alpha's block counter (last block builds the lists, resets it)
+  // tolerance mode's WHILE graph body only: k_alpha's last block also runs the loop control
+  // (continue while an env iterates and fewer than loop_limit trips ran): one launch less per trip
+  int loop_on, loop_limit;
+  int* loop_ctr;
+  cudaGraphConditionalHandle loop_h;
   int remap_blocks;              // tolerance mode: CTAs dealt over the active envs' contact passes when few iterate
   int nseg, rows;                // rows: the gradient pass marches along the segments (all cells axis-aligned)
   const int* rest_tets;          // [nrest] tets not in any cell

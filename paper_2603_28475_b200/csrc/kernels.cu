@@ -3009,6 +3009,10 @@ __device__ void build_active_lists(const Dev& d) {
     d.anum[0] = n;
     d.anum[1] = ng;
     *d.adone = 0u;
+    if (d.loop_on) {  // WHILE body: continue while an env evaluates next (= is active) and trips remain
+      const int c = ++(*d.loop_ctr);
+      cudaGraphSetConditional(d.loop_h, (n > 0 && c < d.loop_limit) ? 1u : 0u);
+    }
   }
 }
 __global__ void k_alpha(Dev d, double h) {
