@@ -2577,28 +2577,39 @@ __device__ void apply_pose(EnvS& s, double a) {  // (c, R) = (c_p + a p_c, exp([
 __global__ void k_accept(Dev d, double h) {
   TAC_PDL_WAIT();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= d.E || !(d.run[e] & 1)) return;
+  if (e >= d.E) return;
   EnvS& s = d.es[e];
   double* A = d.acc;
-  size_t Es = d.Es;
+  const size_t Es = d.Es;
+  // every load of the common path before the first store (see k_dir_scalar)
+  const int rb = d.run[e];
+  double acc[28];
+  for (int k = 0; k < 28; ++k) acc[k] = A[k * Es + e];
+  double c[3], cs[3], R[9], Rs[9], lam[6];
+  for (int k = 0; k < 3; ++k) { c[k] = s.c[k]; cs[k] = s.cs[k]; }
+  for (int k = 0; k < 9; ++k) { R[k] = s.R[k]; Rs[k] = s.Rs[k]; }
+  for (int k = 0; k < 6; ++k) lam[k] = s.lam[k];
+  const int ncand_over = s.ncand_over, iter = s.iter, reeval = s.reeval;
+  const double sE = s.E, salpha = s.alpha, sgp = s.gp_prev, sodo = s.odo;
+  if (!(rb & 1)) return;
   double h2 = h * h;
-  d3 dc = ld3(s.c) - ld3(s.cs);
+  d3 dc = ld3(c) - ld3(cs);
   double RRs[9];
-  mmT(s.R, s.Rs, RRs);
+  mmT(R, Rs, RRs);
   d3 phi = so3_log(RRs);
   double wt = spring_w(nrm(dc), d.k_t, d.f_max), wr = spring_w(nrm(phi), d.k_r, d.t_max);
-  double Eb = A[A_EB * Es + e];
+  double Eb = acc[A_EB];
   double Ep = h2 * (spring_e(nrm(dc), d.k_t, d.f_max) + spring_e(nrm(phi), d.k_r, d.t_max));
-  const d3 lt = ld3(s.lam), lr = ld3(s.lam + 3);
+  const d3 lt = ld3(lam), lr = ld3(lam + 3);
   if (d.pose_al) Ep += h2 * (dot(lt, dc) + dot(lr, phi));  // multiplier term (R29)
-  double E = A[A_EIN * Es + e] + A[A_EEL * Es + e] + Eb + A[A_EF * Es + e] + Ep;
+  double E = acc[A_EIN] + acc[A_EEL] + Eb + acc[A_EF] + Ep;
   double gr[6], Dc6[6], Dt6[6];
-  for (int k = 0; k < 6; ++k) gr[k] = A[(A_GR + k) * Es + e];
-  for (int k = 0; k < 6; ++k) { Dc6[k] = A[(A_DR + k) * Es + e]; Dt6[k] = A[(A_DR + 6 + k) * Es + e]; }
-  s.Ep[0] = A[A_EIN * Es + e]; s.Ep[1] = A[A_EEL * Es + e]; s.Ep[2] = Eb; s.Ep[3] = A[A_EF * Es + e];
+  for (int k = 0; k < 6; ++k) gr[k] = acc[A_GR + k];
+  for (int k = 0; k < 6; ++k) { Dc6[k] = acc[A_DR + k]; Dt6[k] = acc[A_DR + 6 + k]; }
+  s.Ep[0] = acc[A_EIN]; s.Ep[1] = acc[A_EEL]; s.Ep[2] = Eb; s.Ep[3] = acc[A_EF];
   s.Ep[4] = Ep;
   for (int k = 0; k < 28; ++k) A[k * Es + e] = 0.0;
-  if (s.ncand_over) {  // candidate or anchor capacity exceeded: pairs were dropped, the barrier
+  if (ncand_over) {  // candidate or anchor capacity exceeded: pairs were dropped, the barrier
     // and the step bound no longer see them -- the step fails and rolls back (flag 32)
     s.flags |= kFlagOverflow;
     s.mode = kDone;
@@ -2615,19 +2626,19 @@ __global__ void k_accept(Dev d, double h) {
     gr[3] += h2 * gl.x; gr[4] += h2 * gl.y; gr[5] += h2 * gl.z;
   }
   for (int k = 0; k < 3; ++k) { Dc6[k] += h2 * wt; Dt6[k] += h2 * wr; }
-  s.iter += 1;
+  s.iter = iter + 1;
   d.dalpha[e] = 0.f;
-  bool first = (s.iter == 1);
-  if ((first || s.reeval) && !isfinite(E)) {  // infeasible / NaN at the step start or at x_k: roll back
+  bool first = (iter + 1 == 1);
+  if ((first || reeval) && !isfinite(E)) {  // infeasible / NaN at the step start or at x_k: roll back
     s.flags |= isfinite(Eb) ? kFlagNaN : kFlagInfeas;
     s.mode = kDone;
     d.run[e] = 0;
     return;
   }
-  bool ok = first || s.reeval || (isfinite(E) && E <= s.E + d.c1 * s.alpha * s.gp_prev + d.eps_E * fabs(s.E));
+  bool ok = first || reeval || (isfinite(E) && E <= sE + d.c1 * salpha * sgp + d.eps_E * fabs(sE));
   s.cache_ok = 1;  // this evaluation classified every candidate of the current list
   if (ok) {
-    s.odo_base = s.odo;
+    s.odo_base = sodo;
     s.E = E;
     s.wt_acc = wt;
     s.wr_acc = wr;
@@ -2810,33 +2821,56 @@ __device__ void rigid_P(const EnvS& s, int scalar, const double* x, double* y) {
 
 // per env: convergence on |P g|_disp (R17), Dai-Kou beta with restarts (R13),
 // rigid part of the direction
+__device__ __forceinline__ void rigid_P_m(const double* Dc, const double* Dth, int scalar, const double* x, double* y) {
+  for (int b = 0; b < 2; ++b) {  // blockdiag(Dc, Dth)^-1 x (rigid_P on register copies)
+    const double* M = b == 0 ? Dc : Dth;
+    const double* xx = x + 3 * b;
+    double* yy = y + 3 * b;
+    if (scalar) {
+      for (int i = 0; i < 3; ++i) yy[i] = xx[i] / M[4 * i];
+      continue;
+    }
+    double c00 = M[4] * M[8] - M[5] * M[7], c01 = M[5] * M[6] - M[3] * M[8], c02 = M[3] * M[7] - M[4] * M[6];
+    double c11 = M[0] * M[8] - M[2] * M[6], c12 = M[2] * M[3] - M[0] * M[5], c22 = M[0] * M[4] - M[1] * M[3];
+    double inv = 1.0 / (M[0] * c00 + M[1] * c01 + M[2] * c02);
+    yy[0] = inv * (c00 * xx[0] + c01 * xx[1] + c02 * xx[2]);
+    yy[1] = inv * (c01 * xx[0] + c11 * xx[1] + c12 * xx[2]);
+    yy[2] = inv * (c02 * xx[0] + c12 * xx[1] + c22 * xx[2]);
+  }
+}
+// One thread per env: every load is issued before the first store (a store through d.acc /
+// d.es could alias a later load, so the compiler would otherwise keep each load behind the
+// stores before it -- a chain of dependent memory round trips in a latency-bound kernel).
 __global__ void k_dir_scalar(Dev d) {
   TAC_PDL_WAIT();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= d.E) return;
-  size_t Es = d.Es;
-  if (!(d.run[e] & 2)) {  // not accepted: drop the speculative sums of k_dir_reduce
-    for (int k = 0; k < 7; ++k) d.acc[(A_DOT + k) * Es + e] = 0.0;
-    d.accu[U_PGMAX * Es + e] = 0u;
-    return;
-  }
+  const size_t Es = d.Es;
   EnvS& s = d.es[e];
+  const int rb = d.run[e];
   double dt[7];
-  for (int k = 0; k < 7; ++k) { dt[k] = d.acc[(A_DOT + k) * Es + e]; d.acc[(A_DOT + k) * Es + e] = 0.0; }
-  float pgmax = __uint_as_float(d.accu[U_PGMAX * Es + e]);
+  for (int k = 0; k < 7; ++k) dt[k] = d.acc[(A_DOT + k) * Es + e];
+  const float pgmax = __uint_as_float(d.accu[U_PGMAX * Es + e]);
+  double gr[6], grp[6], pr[6], Dc[9], Dth[9];
+  for (int k = 0; k < 6; ++k) { gr[k] = s.gr[k]; grp[k] = s.grp[k]; pr[k] = s.pr[k]; }
+  for (int k = 0; k < 9; ++k) { Dc[k] = s.Dc[k]; Dth[k] = s.Dth[k]; }
+  const int restart = s.restart, iter = s.iter, best_it = s.best_it;
+  const double best_pg = s.best_pg, gPg_prev = s.gPg_prev;
+  for (int k = 0; k < 7; ++k) d.acc[(A_DOT + k) * Es + e] = 0.0;
   d.accu[U_PGMAX * Es + e] = 0u;
+  if (!(rb & 2)) return;  // not accepted: the speculative sums of k_dir_reduce are dropped
   double Pg[6], y[6], Py[6];
-  rigid_P(s, d.precond, s.gr, Pg);
-  for (int k = 0; k < 6; ++k) y[k] = s.gr[k] - s.grp[k];
-  rigid_P(s, d.precond, y, Py);
+  rigid_P_m(Dc, Dth, d.precond, gr, Pg);
+  for (int k = 0; k < 6; ++k) y[k] = gr[k] - grp[k];
+  rigid_P_m(Dc, Dth, d.precond, y, Py);
   for (int k = 0; k < 6; ++k) {
-    dt[0] += s.gr[k] * Py[k];
-    dt[1] += y[k] * s.pr[k];
+    dt[0] += gr[k] * Py[k];
+    dt[1] += y[k] * pr[k];
     dt[2] += y[k] * Py[k];
-    dt[3] += s.pr[k] * s.gr[k];
-    dt[4] += s.gr[k] * Pg[k];
-    dt[5] += s.gr[k] * s.gr[k];
-    dt[6] += s.pr[k] * s.pr[k];
+    dt[3] += pr[k] * gr[k];
+    dt[4] += gr[k] * Pg[k];
+    dt[5] += gr[k] * gr[k];
+    dt[6] += pr[k] * pr[k];
   }
   double pgd = fmax((double)pgmax, nrm(mk(Pg[0], Pg[1], Pg[2])) + d.rho_max * nrm(mk(Pg[3], Pg[4], Pg[5])));
   s.pg = pgd;
@@ -2845,19 +2879,19 @@ __global__ void k_dir_scalar(Dev d) {
       s.mode = kDone; s.flags |= 1; d.run[e] = 0;
       return;
     }
-    if (pgd < s.best_pg * (1 - 1e-3)) { s.best_pg = pgd; s.best_it = s.iter; }
-    if (d.stagnation > 0 && s.iter - s.best_it > d.stagnation) {
+    if (pgd < best_pg * (1 - 1e-3)) { s.best_pg = pgd; s.best_it = iter; }
+    else if (d.stagnation > 0 && iter - best_it > d.stagnation) {
       s.mode = kDone; s.flags |= 64; d.run[e] = 0;
       return;
     }
   }
   double gPy = dt[0], yp = dt[1], yPy = dt[2], pg = dt[3], gPg = dt[4], gg = dt[5], pp = dt[6];
-  bool rs = s.restart || s.iter == 1;
+  bool rs = restart || iter == 1;
   double beta = 0;
   if (!rs) {
     if (fabs(yp) <= 1e-30 * sqrt(gg) * sqrt(pp)) rs = true;
-    else if (d.beta_rule == 1) beta = fmax(0.0, gPy / s.gPg_prev);
-    else if (d.beta_rule == 2) beta = gPg / s.gPg_prev;
+    else if (d.beta_rule == 1) beta = fmax(0.0, gPy / gPg_prev);
+    else if (d.beta_rule == 2) beta = gPg / gPg_prev;
     else {
       beta = gPy / yp - (yPy / yp) * (pg / yp);
       if (d.beta_rule == 3) beta = fmax(beta, 0.5 * pg / pp);  // DK+ truncation (R28)
@@ -2873,10 +2907,11 @@ __global__ void k_dir_scalar(Dev d) {
   s.gp_prev = gp;
   s.gPg_prev = gPg;
   for (int k = 0; k < 6; ++k) {
-    s.pr[k] = -Pg[k] + (beta != 0 ? beta * s.pr[k] : 0.0);
-    s.grp[k] = s.gr[k];
+    pr[k] = -Pg[k] + (beta != 0 ? beta * pr[k] : 0.0);
+    s.pr[k] = pr[k];
+    s.grp[k] = gr[k];
   }
-  d.pcf[e] = make_float4((float)s.pr[0], (float)s.pr[1], (float)s.pr[2], 0.f);
+  d.pcf[e] = make_float4((float)pr[0], (float)pr[1], (float)pr[2], 0.f);
 }
 
 // p = -P g + beta p_prev; g_prev = g; M = max |p_v|, L_rel = max_surface |p_v - p_c|, inertia p^T M p
@@ -2957,18 +2992,6 @@ __global__ void __launch_bounds__(256) k_dir_apply(Dev d) {
 // ------------------------------------------------------------------ a7/a8: step length (per env)
 // alpha = min(alpha_upper = dhat / (2 |p|_disp), alpha_bar = -g^T p / p^T H p,
 // alpha_ccd (R15)); rebuild the candidates first if S + alpha L_rel > m_r (R16)
-__device__ void commit_alpha(const Dev& d, EnvS& s, int e, double a, double L) {
-  if (!isfinite(a)) a = 0;
-  for (int i = 0; i < 3; ++i) s.cp[i] = s.c[i];
-  for (int i = 0; i < 9; ++i) s.Rp[i] = s.R[i];
-  s.alpha = a;
-  apply_pose(s, a);
-  d.dalpha[e] = (float)a;
-  s.S += a * L;
-  s.odo = s.odo_base + a * L;  // trial point x_k + a p on the odometer path
-  s.Lc = L;
-  d.run[e] = 1;
-}
 
 // R16: the candidate list stays valid while the odometer S <= m_r.  A step that would pass
 // m_r is capped at it; once S + alpha L_rel passes kRebuildAt m_r the env is listed and its
@@ -3022,49 +3045,71 @@ __global__ void k_alpha(Dev d, double h) {
   if (d.fixed_iters <= 0) build_active_lists(d);
 }
 __device__ void alpha_env(const Dev& d, double h, int e) {
-  int rb = d.run[e];
-  size_t Es = d.Es;
+  const size_t Es = d.Es;
   EnvS& s = d.es[e];
+  // every load before the first store (see k_dir_scalar)
+  const int rb = d.run[e];
+  double pr[6], c[3], R[9];
+  for (int k = 0; k < 6; ++k) pr[k] = s.pr[k];
+  for (int k = 0; k < 3; ++k) c[k] = s.c[k];
+  for (int k = 0; k < 9; ++k) R[k] = s.R[k];
+  const double wt_acc = s.wt_acc, wr_acc = s.wr_acc, gp_prev = s.gp_prev, S = s.S, S2 = s.S2, odo_base = s.odo_base;
+  const int pending = s.pending, iter = s.iter, reb_iter = s.reb_iter;
+  const double Mg = __uint_as_float(d.accu[U_M * Es + e]);
+  const double Lg = __uint_as_float(d.accu[U_LREL * Es + e]);
+  const double php = d.acc[A_PHP * Es + e];
+  double accd = (double)__uint_as_float(d.accu[U_ACCD * Es + e]);
+  const double gfar = (double)__uint_as_float(d.accu[U_GFAR * Es + e]);
   if (!(rb & 2)) return;
   double h2 = h * h;
-  d3 pc = mk(s.pr[0], s.pr[1], s.pr[2]), pth = mk(s.pr[3], s.pr[4], s.pr[5]);
-  double Mg = __uint_as_float(d.accu[U_M * Es + e]);
-  double Lg = __uint_as_float(d.accu[U_LREL * Es + e]);
+  d3 pc = mk(pr[0], pr[1], pr[2]), pth = mk(pr[3], pr[4], pr[5]);
   double M = fmax(Mg, nrm(pc) + d.rho_max * nrm(pth));
   double L = fmax(Lg, nrm(pc)) + d.rho_max * nrm(pth);
   // the pose spring's Gauss-Newton curvature at x_k, with its weights from k_accept
-  double q = d.acc[A_PHP * Es + e] + h2 * (s.wt_acc * dot(pc, pc) + s.wr_acc * dot(pth, pth));
+  double q = php + h2 * (wt_acc * dot(pc, pc) + wr_acc * dot(pth, pth));
   d.acc[A_PHP * Es + e] = 0.0;
   d.accu[U_M * Es + e] = 0u;
   d.accu[U_LREL * Es + e] = 0u;
-  double accd = (double)__uint_as_float(d.accu[U_ACCD * Es + e]);
-  double gfar = (double)__uint_as_float(d.accu[U_GFAR * Es + e]);
   if (gfar < INFINITY && L > 0) accd = fmin(accd, (1 - d.ccd_s) * d.dhat / L);  // far pairs (R15)
   d.accu[U_ACCD * Es + e] = 0x7f800000u;
   d.accu[U_GFAR * Es + e] = 0x7f800000u;
   double aup = M > 0 ? d.dhat / (2 * M) : INFINITY;
-  double abar = q > 0 ? -s.gp_prev / q : INFINITY;
+  double abar = q > 0 ? -gp_prev / q : INFINITY;
   double a = fmin(aup, fmin(abar, accd));
   if (!isfinite(a)) a = 0;
   s.dbg[0] = q; s.dbg[1] = M; s.dbg[2] = L; s.dbg[3] = aup; s.dbg[4] = abar; s.dbg[5] = accd; s.dbg[6] = a;
   // the list that will evaluate this step's trial: the pending one if it is swapped in first
-  const bool swap_next = s.pending && s.iter >= s.reb_iter + 1;
-  const double Sl = swap_next ? s.S2 : s.S;
+  const bool swap_next = pending && iter >= reb_iter + 1;
+  const double Sl = swap_next ? S2 : S;
   if (L > 0 && Sl + a * L > d.bp_margin) a = fmax(0.0, (d.bp_margin - Sl) / L);  // validity cap (R16)
-  commit_alpha(d, s, e, a, L);  // S += a L
-  s.S2 += a * L;
-  if (!s.pending && L > 0 && s.S > kRebuildAt * d.bp_margin) {
+  // commit: x_k -> (c_p, R_p); trial pose (c, R) = (c_p + a p_c, exp([a p_theta]) R_p)
+  if (!isfinite(a)) a = 0;
+  double cn[3], Rn[9], Q[9];
+  for (int i = 0; i < 3; ++i) { s.cp[i] = c[i]; cn[i] = c[i] + a * pr[i]; s.c[i] = cn[i]; }
+  rodrigues(a * pth, Q);
+  mm3(Q, R, Rn);
+  for (int i = 0; i < 9; ++i) { s.Rp[i] = R[i]; s.R[i] = Rn[i]; }
+  s.alpha = a;
+  d.dalpha[e] = (float)a;
+  const double Sn = S + a * L;
+  s.S = Sn;
+  s.odo = odo_base + a * L;  // trial point x_k + a p on the odometer path
+  s.Lc = L;
+  d.run[e] = 1;
+  if (!pending && L > 0 && Sn > kRebuildAt * d.bp_margin) {
     // pipelined rebuild (R16): a new list built at the trial point this step reaches, during the
     // next evaluation on a side stream (off its critical path), swapped in by the vertex pre-pass
     // of the evaluation after; until then the active list stays valid (S <= m_r, capped above)
     s.pending = 1;
-    s.reb_iter = s.iter;
+    s.reb_iter = iter;
     s.S2 = 0;
-    for (int i = 0; i < 3; ++i) s.cb[i] = s.c[i];
-    for (int i = 0; i < 9; ++i) s.Rb[i] = s.R[i];
+    for (int i = 0; i < 3; ++i) s.cb[i] = cn[i];
+    for (int i = 0; i < 9; ++i) s.Rb[i] = Rn[i];
     s.rebuild += 1;
     d.ncand[(1 - d.lbuf[e]) * d.E + e] = 0;
     d.reb_list[atomicAdd(d.nreb, 1)] = e;  // compact list for k_broadphase_list
+  } else {
+    s.S2 = S2 + a * L;
   }
 }
 
