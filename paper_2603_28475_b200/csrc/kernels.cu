@@ -961,11 +961,48 @@ __device__ __forceinline__ bool group_block(const Dev& d, int cap, int ng_grid, 
   return true;
 }
 
+// Lane -> env of the vertex / element passes.  As group_block, and in addition: in the tolerance
+// mode, once the listed envs are sparse in their groups (on average <= 8 of 32 lanes), the
+// passes run over compacted groups -- lane l of compacted group j is env alist[32 j + l] (lanes
+// past the list get e = E: inactive) -- so a warp serves 32 envs that still iterate instead of a
+// few: the element passes are instruction-bound, and the scattered per-lane rows cost L2
+// requests, not bytes.  Otherwise e = 32 grp + lane.
+template <bool TOL>  // TOL: the tolerance mode's instantiation (the fixed mode's is the identity)
+__device__ __forceinline__ bool env_lanes(const Dev& d, int cap, int ng_grid, int c, int nc, int& e, int& bc,
+                                          int& nbc) {
+  const int lane = threadIdx.x & 31;
+  if constexpr (!TOL) {
+    bc = c;
+    nbc = nc;
+    e = ng_grid * 32 + lane;
+    return true;
+  }
+  const int G = d.Es >> 5;
+  if (G >= 2 && d.compact) {
+    const int n = d.anum[0], n_g = d.anum[1];
+    if (n > 0 && n * 4 <= n_g * 32) {
+      const int Gc = (n + 31) >> 5;
+      const int per = max(nc, min(cap, (G * nc) / Gc));
+      const int lin = ng_grid * nc + c, idx = lin / per;
+      if (idx >= Gc) return false;
+      bc = lin - idx * per;
+      nbc = per;
+      const int j = 32 * idx + lane;
+      e = j < n ? d.alist[j] : d.E;
+      return true;
+    }
+  }
+  int grp;
+  if (!group_block(d, cap, ng_grid, c, nc, grp, bc, nbc)) return false;
+  e = grp * 32 + lane;
+  return true;
+}
+
+template <bool TOL>
 __global__ void k_vert_pre(Dev d, float h2) {
   TAC_PDL_WAIT();
-  int grp, by, nby;
-  if (!group_block(d, (d.nv + 7) / 8, blockIdx.x, blockIdx.y, gridDim.y, grp, by, nby)) return;
-  int e = grp * 32 + threadIdx.x;
+  int e, by, nby;
+  if (!env_lanes<TOL>(d, (d.nv + 7) / 8, blockIdx.x, blockIdx.y, gridDim.y, e, by, nby)) return;
   bool act = e < d.E && (d.run[e] & 1);
   if (!__any_sync(0xffffffffu, act)) return;
   float da = act ? d.dalpha[e] : 0.f;
@@ -1483,15 +1520,16 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
 // to the next: per cell 12 corner row loads and 36 red.adds instead of 24 and 72.  Pair order
 // 1, 2, 0 finishes the carried-in corners early (2 after pair 1; 4, 6 after pair 2; 0 after
 // pair 0), so at most 6 corners' accumulators are live, as in the one-cell pass.
+template <bool TOL>
 __global__ void __launch_bounds__(256, 2) k_elem_grad_rows(Dev d, float h2) {
   TAC_PDL_WAIT();
-  int grp, bx, nbx;
-  if (!group_block(d, (d.nseg + 7) / 8, blockIdx.y, blockIdx.x, gridDim.x, grp, bx, nbx)) return;
-  const int e = grp * 32 + threadIdx.x;
+  int e, bx, nbx;
+  if (!env_lanes<TOL>(d, (d.nseg + 7) / 8, blockIdx.y, blockIdx.x, gridDim.x, e, bx, nbx)) return;
   const bool act = e < d.E && (d.run[e] & 1);
   if (!__any_sync(0xffffffffu, act)) return;
   const float mu = d.emat[e], l2 = d.emat[d.Es + e];  // per-env material
-  const unsigned G = (unsigned)(d.Es >> 5), eg = (unsigned)grp, lane = threadIdx.x;
+  const unsigned G = (unsigned)(d.Es >> 5), eg = TOL ? (unsigned)e >> 5 : (unsigned)blockIdx.y,
+                 lane = TOL ? (unsigned)e & 31u : (unsigned)threadIdx.x;  // (compacted: per lane)
   double esum = 0;
   for (int sg = bx * 8 + threadIdx.y; sg < d.nseg; sg += nbx * 8) {
     if (!act) continue;
@@ -1563,16 +1601,16 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_rows(Dev d, float h2) {
 
 // ---- Kuhn-cell element curvature: one warp = one cell x 32 envs, u and p of the 8 corners
 // in registers; p^T H_e p summed over the 6 tets (App. B quadratic form)
-template <bool ALL_AA>
+template <bool ALL_AA, bool TOL>
 __global__ void __launch_bounds__(256, 2) k_elem_curv_cells(Dev d, float h2) {
   TAC_PDL_WAIT();
-  int grp, bx, nbx;
-  if (!group_block(d, (d.ncells + 7) / 8, blockIdx.y, blockIdx.x, gridDim.x, grp, bx, nbx)) return;
-  const int e = grp * 32 + threadIdx.x;
+  int e, bx, nbx;
+  if (!env_lanes<TOL>(d, (d.ncells + 7) / 8, blockIdx.y, blockIdx.x, gridDim.x, e, bx, nbx)) return;
   const bool act = e < d.E && (d.run[e] & 2);
   if (!__any_sync(0xffffffffu, act)) return;
   const float mu = d.emat[e], l2 = d.emat[d.Es + e];  // per-env material
-  const unsigned G = (unsigned)(d.Es >> 5), eg = (unsigned)grp, lane = threadIdx.x;
+  const unsigned G = (unsigned)(d.Es >> 5), eg = TOL ? (unsigned)e >> 5 : (unsigned)blockIdx.y,
+                 lane = TOL ? (unsigned)e & 31u : (unsigned)threadIdx.x;  // (compacted: per lane)
   double qsum = 0;
   for (int cidx = bx * 8 + threadIdx.y; cidx < d.ncells; cidx += nbx * 8) {
     const int4 va = __ldg(d.cell_v + 2 * cidx), vb4 = __ldg(d.cell_v + 2 * cidx + 1);
@@ -2729,13 +2767,12 @@ __device__ __forceinline__ void precond2(T a, T b, T c, T xy, T xz, T yz, int sc
 // flight; SURF = true: the free surface vertices (the list sv), whose P = (D + Dcon)^-1 is formed
 // in fp64 (R24) -- on a side stream beside the first, so the fp64 inverse's registers no longer
 // throttle the bulk of the vertices (one kernel with both: 80 registers, one vertex in flight)
-template <bool SURF>
+template <bool SURF, bool TOL>
 __global__ void __launch_bounds__(256) k_dir_reduce(Dev d) {
   TAC_PDL_WAIT();
   constexpr int NB = SURF ? 1 : 2;
-  int grp, by, nby;
-  if (!group_block(d, ((SURF ? d.nsv : d.nv) + 7) / 8, blockIdx.x, blockIdx.y, gridDim.y, grp, by, nby)) return;
-  int e = grp * 32 + threadIdx.x;
+  int e, by, nby;
+  if (!env_lanes<TOL>(d, ((SURF ? d.nsv : d.nv) + 7) / 8, blockIdx.x, blockIdx.y, gridDim.y, e, by, nby)) return;
   bool act = e < d.E && (d.run[e] & 3);  // speculative: k_accept may run concurrently (see launch_eval)
   if (!__any_sync(0xffffffffu, act)) return;
   double gPy = 0, yp = 0, yPy = 0, pg = 0, gPg = 0, gg = 0, pp = 0;
@@ -2930,11 +2967,11 @@ __global__ void k_dir_scalar(Dev d) {
 }
 
 // p = -P g + beta p_prev; g_prev = g; M = max |p_v|, L_rel = max_surface |p_v - p_c|, inertia p^T M p
+template <bool TOL>
 __global__ void __launch_bounds__(256) k_dir_apply(Dev d) {
   TAC_PDL_WAIT();
-  int grp, by, nby;
-  if (!group_block(d, (d.nv + 7) / 8, blockIdx.x, blockIdx.y, gridDim.y, grp, by, nby)) return;
-  int e = grp * 32 + threadIdx.x;
+  int e, by, nby;
+  if (!env_lanes<TOL>(d, (d.nv + 7) / 8, blockIdx.x, blockIdx.y, gridDim.y, e, by, nby)) return;
   bool act = e < d.E && (d.run[e] & 2);
   if (!__any_sync(0xffffffffu, act)) return;
   float beta = act ? d.beta[e] : 0.f;
@@ -3408,7 +3445,8 @@ void launch_sort_anchors(const Dev& d, Anchor* out, cudaStream_t s) {
 // joined before k_accept / k_alpha.  With per-launch profiling on, everything stays on the
 // caller's stream so each kernel's time is its own.
 void launch_eval(const Dev& d, double h, cudaStream_t s) {
-  LAUNCHP(KID_VERT_PRE, s, k_vert_pre, vgrid(d, d.nv), dim3(32, 8), 0, d, (float)(h * h));
+  if (d.fixed_iters > 0) LAUNCHP(KID_VERT_PRE, s, k_vert_pre<false>, vgrid(d, d.nv), dim3(32, 8), 0, d, (float)(h * h));
+  else LAUNCHP(KID_VERT_PRE, s, k_vert_pre<true>, vgrid(d, d.nv), dim3(32, 8), 0, d, (float)(h * h));
   const bool fork = g_prof == nullptr;
   cudaStream_t cs = fork ? d.side : s, cs2 = fork ? d.side2 : s;
   if (fork) {
@@ -3453,7 +3491,8 @@ void launch_eval(const Dev& d, double h, cudaStream_t s) {
     dim3 g = cellgrid(d);
     if (d.rows) {
       const int gy = (d.nseg + 7) / 8;  // one segment per warp
-      LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad_rows, dim3(gy, g.x), dim3(32, 8), 0, d, (float)(h * h));
+      if (d.fixed_iters > 0) LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad_rows<false>, dim3(gy, g.x), dim3(32, 8), 0, d, (float)(h * h));
+      else LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad_rows<true>, dim3(gy, g.x), dim3(32, 8), 0, d, (float)(h * h));
     } else if (d.cells_all_aa) LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad_cells<true>, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
     else LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad_cells<false>, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
   }
@@ -3484,15 +3523,20 @@ void launch_direction(const Dev& d, cudaStream_t s, bool apply) {
     cudaStreamWaitEvent(ss, d.ev_fork, 0);
   }
   static const int sbps = env_int("TAC_DIRS_BPS", 2);  // A/B
-  LAUNCHP(KID_DIR_REDUCE_SURF, ss, k_dir_reduce<true>, vgrid(d, std::max(1, d.nsv), sbps), dim3(32, 8), 0, d);
+  if (d.fixed_iters > 0) LAUNCHP(KID_DIR_REDUCE_SURF, ss, (k_dir_reduce<true, false>), vgrid(d, std::max(1, d.nsv), sbps), dim3(32, 8), 0, d);
+  else LAUNCHP(KID_DIR_REDUCE_SURF, ss, (k_dir_reduce<true, true>), vgrid(d, std::max(1, d.nsv), sbps), dim3(32, 8), 0, d);
   if (fork) cudaEventRecord(d.ev_join2, ss);
-  LAUNCHP(KID_DIR_REDUCE, s, k_dir_reduce<false>, vgrid(d, d.nv), dim3(32, 8), 0, d);
+  if (d.fixed_iters > 0) LAUNCHP(KID_DIR_REDUCE, s, (k_dir_reduce<false, false>), vgrid(d, d.nv), dim3(32, 8), 0, d);
+  else LAUNCHP(KID_DIR_REDUCE, s, (k_dir_reduce<false, true>), vgrid(d, d.nv), dim3(32, 8), 0, d);
   if (fork) {
     cudaStreamWaitEvent(s, d.ev_join, 0);   // k_accept on the side stream
     cudaStreamWaitEvent(s, d.ev_join2, 0);  // the surface part
   }
   LAUNCHP(KID_DIR_SCALAR, s, k_dir_scalar, eblocks32(d), 32, 0, d);
-  if (apply) LAUNCHP(KID_DIR_APPLY, s, k_dir_apply, vgrid(d, d.nv), dim3(32, 8), 0, d);
+  if (apply) {
+    if (d.fixed_iters > 0) LAUNCHP(KID_DIR_APPLY, s, k_dir_apply<false>, vgrid(d, d.nv), dim3(32, 8), 0, d);
+    else LAUNCHP(KID_DIR_APPLY, s, k_dir_apply<true>, vgrid(d, d.nv), dim3(32, 8), 0, d);
+  }
 }
 void launch_curvature(const Dev& d, double h, cudaStream_t s) {
   const bool fork = g_prof == nullptr;  // contact curvature concurrent with the element curvature
@@ -3509,8 +3553,11 @@ void launch_curvature(const Dev& d, double h, cudaStream_t s) {
     dim3 g = cellgrid(d);
     // (a row-marching curvature pass -- u and p of the shared face carried -- measured 125 vs
     // 114 us: this pass is FMA-bound and the carried rows cost spills)
-    if (d.cells_all_aa) LAUNCHP(KID_ELEM_CURV, s, k_elem_curv_cells<true>, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
-    else LAUNCHP(KID_ELEM_CURV, s, k_elem_curv_cells<false>, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
+    const bool tol = d.fixed_iters <= 0;
+    if (d.cells_all_aa && tol) LAUNCHP(KID_ELEM_CURV, s, (k_elem_curv_cells<true, true>), dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
+    else if (d.cells_all_aa) LAUNCHP(KID_ELEM_CURV, s, (k_elem_curv_cells<true, false>), dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
+    else if (tol) LAUNCHP(KID_ELEM_CURV, s, (k_elem_curv_cells<false, true>), dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
+    else LAUNCHP(KID_ELEM_CURV, s, (k_elem_curv_cells<false, false>), dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
   } else {
     LAUNCHP(KID_ELEM_CURV, s, k_elem_curv_tiled, dim3(d.Es / 32, d.ntiles), 256, kTiledCurvSmem, d, (float)(h * h));
   }

@@ -32,11 +32,12 @@ PROFILE_NAME = {"k_elem_grad_cells": "elem_grad", "k_elem_grad_rows": "elem_grad
 def short(name):
     n = name.replace("void ", "").replace("(int)", "").replace("(bool)", "")
     n = n.split("(")[0].replace("tac::", "")
-    for t in ("<1>", "<0>", "<true>", "<false>"):
-        if (n.startswith("k_elem") or n.startswith("k_contact_classify")) and n.endswith(t):
-            n = n[: -len(t)]
-    if n.startswith("k_contact_classify"):  # k_contact_classify_staged<BODY, REMAP>
+    # template arguments that only select an instantiation (axis-aligned cells, body frame,
+    # tolerance-mode remapping) are dropped; k_dir_reduce keeps SURF, k_contact_near its KIND
+    if n.startswith(("k_elem", "k_contact_classify", "k_vert_pre", "k_dir_apply")):
         n = n.split("<")[0]
+    if n.startswith("k_dir_reduce<"):  # k_dir_reduce<SURF, TOL> -> k_dir_reduce<SURF>
+        n = n.split(",")[0].rstrip(">") + ">"
     if n.startswith("k_contact_near<"):  # k_contact_near<KIND, MOLL> -> k_contact_near<KIND>
         n = n.split(",")[0].rstrip(">") + ">"
     return n
