@@ -1018,6 +1018,8 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     if (cudaStreamCreateWithPriority(&d.side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&d.side2, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&d.side3, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&d.side4, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d.ev_join4, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&d.ev_reb, cudaEventDisableTiming) != cudaSuccess ||
         cudaStreamCreateWithFlags(&sim->cap, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&d.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
@@ -1092,12 +1094,13 @@ tac_status tac_destroy(tac_sim* sim) {
   if (sim->d.side) { cudaStreamSynchronize(sim->d.side); cudaStreamDestroy(sim->d.side); }
   if (sim->d.side2) { cudaStreamSynchronize(sim->d.side2); cudaStreamDestroy(sim->d.side2); }
   if (sim->d.side3) { cudaStreamSynchronize(sim->d.side3); cudaStreamDestroy(sim->d.side3); }
+  if (sim->d.side4) { cudaStreamSynchronize(sim->d.side4); cudaStreamDestroy(sim->d.side4); }
   for (auto& g : sim->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   for (auto& g : sim->wgraphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (sim->cap) cudaStreamDestroy(sim->cap);
-  for (cudaEvent_t ev : {sim->d.ev_fork, sim->d.ev_join, sim->d.ev_cls, sim->d.ev_join2, sim->d.ev_reb})
+  for (cudaEvent_t ev : {sim->d.ev_fork, sim->d.ev_join, sim->d.ev_cls, sim->d.ev_join2, sim->d.ev_reb, sim->d.ev_join4})
     if (ev) cudaEventDestroy(ev);
   for (void* p : sim->allocs) cudaFree(p);
   if (sim->h_flag) cudaFreeHost(sim->h_flag);

@@ -111,7 +111,8 @@ struct Dev {
   int contact_smem;      // dynamic shared bytes of the staged contact kernels (0 = use the unstaged ones)
   cudaStream_t side, side2;  // per-simulator high-priority streams: the contact chain concurrent with the element pass
   cudaStream_t side3;        // the pipelined candidate rebuild (off the evaluation's critical path)
-  cudaEvent_t ev_fork, ev_join, ev_cls, ev_join2, ev_reb;
+  cudaStream_t side4;        // the ind-gel point-triangle near pairs beside the gel-ind ones
+  cudaEvent_t ev_fork, ev_join, ev_cls, ev_join2, ev_reb, ev_join4;
   const float4* Y;       // [niv] body frame, w = |Y|
   const int2* ie;        // [nie]
   const int4* it;        // [nit]

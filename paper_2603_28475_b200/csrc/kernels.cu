@@ -3473,17 +3473,24 @@ void launch_eval(const Dev& d, double h, cudaStream_t s) {
     else LAUNCHP(KID_CONTACT_CLASSIFY, cs, (k_contact_classify_staged<false, false>), sgrid(d), 256, cls_both, d);
   }
   const double kap = h * h;  // kernels scale by their env's kappa_phys
+  // the three near-pair passes are independent (atomics into g / Dcon): edge-edge after the
+  // classification on its stream, gel-ind point-triangle after the friction pass, ind-gel on a
+  // fourth stream (one dependent launch less in a tolerance-mode tail iteration)
+  static const bool four = getenv("TAC_NO_SIDE4") == nullptr;
+  cudaStream_t cs4 = fork && four ? d.side4 : cs2;
   if (fork) {
     cudaEventRecord(d.ev_cls, cs);
     cudaStreamWaitEvent(cs2, d.ev_cls, 0);
+    if (four) cudaStreamWaitEvent(cs4, d.ev_cls, 0);
   }
   if (d.ee_moll) LAUNCHP(KID_CONTACT_NEAR_EE, cs, (k_contact_near<2, true>), cgrid(d), 128, 0, d, kap);
   else LAUNCHP(KID_CONTACT_NEAR_EE, cs, k_contact_near<2>, cgrid(d), 128, 0, d, kap);
   LAUNCHP(KID_CONTACT_GRAD, cs2, k_contact_near<0>, cgrid(d), 128, 0, d, kap);
-  LAUNCHP(KID_CONTACT_NEAR_IG, cs2, k_contact_near<1>, cgrid(d), 128, 0, d, kap);
+  LAUNCHP(KID_CONTACT_NEAR_IG, cs4, k_contact_near<1>, cgrid(d), 128, 0, d, kap);
   if (fork) {
     cudaEventRecord(d.ev_join, cs);
     cudaEventRecord(d.ev_join2, cs2);
+    if (four) cudaEventRecord(d.ev_join4, cs4);
   }
   // (a round-scheduled shared-memory tiled variant measured slower on C3: 740 vs 520 us at
   // 66 % warp utilisation in the rounds and 2 CTAs/SM; the coalesced red.add scatter stays)
@@ -3503,6 +3510,7 @@ void launch_eval(const Dev& d, double h, cudaStream_t s) {
   if (fork) {
     cudaStreamWaitEvent(s, d.ev_join, 0);
     cudaStreamWaitEvent(s, d.ev_join2, 0);
+    if (four) cudaStreamWaitEvent(s, d.ev_join4, 0);
     // the Armijo decision (one thread per env, a latency-bound fp64 chain) runs on the side
     // stream beside the direction reduction, which sums its dots speculatively for every env
     // under evaluation; k_dir_scalar (after both) keeps the accepted envs' sums only
