@@ -17,6 +17,7 @@
 #include <numeric>
 #include <set>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "../../include/tac.h"
@@ -906,35 +907,60 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     UP(ie2, d.ie);
     UP(it4, d.it);
     {
-      // wide (child-box) form of the three BVHs: one 64-byte node per internal node holding
-      // both children's boxes and refs (>= 0 internal, < 0 leaf: -1 - (first prim << 3 | count)),
-      // plus one virtual root per tree whose child 0 is the tree root and child 1 never hits
-      std::vector<int> widx(nodes.size(), -1);
-      int nw = 3;
-      for (size_t k = 0; k < nodes.size(); ++k)
-        if (nodes[k].left >= 0) widx[k] = nw++;
-      auto ref = [&](int k) {
-        const BNode& n = nodes[k];
-        return n.left >= 0 ? widx[k] : -1 - (((-n.left - 1) << 3) | n.right);
-      };
-      std::vector<float4> wide(4 * (size_t)nw);
-      auto put = [&](int w, const BNode& a, int ra, const BNode* b, int rb) {
-        const float inf = INFINITY;
-        float lo1[3] = {inf, inf, inf}, hi1[3] = {-inf, -inf, -inf};
-        if (b) for (int t = 0; t < 3; ++t) { lo1[t] = b->lo[t]; hi1[t] = b->hi[t]; }
-        float r0, r1;
-        memcpy(&r0, &ra, 4);
-        memcpy(&r1, &rb, 4);
-        wide[4 * w] = make_float4(a.lo[0], a.lo[1], a.lo[2], a.hi[0]);
-        wide[4 * w + 1] = make_float4(a.hi[1], a.hi[2], lo1[0], lo1[1]);
-        wide[4 * w + 2] = make_float4(lo1[2], hi1[0], hi1[1], hi1[2]);
-        wide[4 * w + 3] = make_float4(r0, r1, 0.f, 0.f);
+      // 4-wide (child-box) form of the three BVHs: two binary levels collapsed into one 128-byte
+      // node holding up to four children's boxes and refs (>= 0 internal, < 0 leaf: -1 - (first
+      // prim << 3 | count)); empty slots never hit.  Wide nodes 0, 1, 2 are virtual roots (tri,
+      // edge, vert) whose child 0 is the tree root.  Half the depth of the binary tree: a query
+      // pays half the dependent node loads.
+      std::vector<float4> wide(8 * 3);
+      auto leaf_ref = [&](int k) { return -1 - (((-nodes[k].left - 1) << 3) | nodes[k].right); };
+      std::function<int(int)> make_wide = [&](int k) -> int {  // binary internal node k -> wide index
+        std::vector<int> ch;
+        for (int c : {nodes[k].left, nodes[k].right}) {
+          if (nodes[c].left >= 0) { ch.push_back(nodes[c].left); ch.push_back(nodes[c].right); }
+          else ch.push_back(c);
+        }
+        const int w = (int)wide.size() / 8;
+        wide.resize(wide.size() + 8);
+        float lo[4][3], hi[4][3];
+        int ref[4];
+        for (int j = 0; j < 4; ++j) {
+          for (int t = 0; t < 3; ++t) { lo[j][t] = INFINITY; hi[j][t] = -INFINITY; }
+          ref[j] = -1;  // empty leaf (never reached: its box never overlaps)
+        }
+        for (size_t j = 0; j < ch.size(); ++j) {
+          const BNode& n = nodes[ch[j]];
+          for (int t = 0; t < 3; ++t) { lo[j][t] = n.lo[t]; hi[j][t] = n.hi[t]; }
+          ref[j] = n.left >= 0 ? make_wide(ch[j]) : leaf_ref(ch[j]);
+        }
+        float rf[4];
+        memcpy(rf, ref, sizeof(rf));
+        for (int j = 0; j < 4; j += 2) {  // children j, j+1: 12 floats in 3 float4
+          wide[8 * w + 3 * (j / 2)] = make_float4(lo[j][0], lo[j][1], lo[j][2], hi[j][0]);
+          wide[8 * w + 3 * (j / 2) + 1] = make_float4(hi[j][1], hi[j][2], lo[j + 1][0], lo[j + 1][1]);
+          wide[8 * w + 3 * (j / 2) + 2] = make_float4(lo[j + 1][2], hi[j + 1][0], hi[j + 1][1], hi[j + 1][2]);
+        }
+        wide[8 * w + 6] = make_float4(rf[0], rf[1], rf[2], rf[3]);
+        wide[8 * w + 7] = make_float4(0.f, 0.f, 0.f, 0.f);
+        return w;
       };
       const int roots[3] = {d.root_tri, d.root_edge, d.root_vert};
-      for (int t = 0; t < 3; ++t) put(t, nodes[roots[t]], ref(roots[t]), nullptr, -1);  // child 1 empty leaf
-      for (size_t k = 0; k < nodes.size(); ++k)
-        if (nodes[k].left >= 0)
-          put(widx[k], nodes[nodes[k].left], ref(nodes[k].left), &nodes[nodes[k].right], ref(nodes[k].right));
+      for (int t = 0; t < 3; ++t) {  // virtual root t: child 0 = the tree's root, the rest empty
+        const BNode& n = nodes[roots[t]];
+        const int r = n.left >= 0 ? make_wide(roots[t]) : leaf_ref(roots[t]);
+        const float inf = INFINITY;
+        int ref[4] = {r, -1, -1, -1};
+        float rf[4];
+        memcpy(rf, ref, sizeof(rf));
+        wide[8 * t] = make_float4(n.lo[0], n.lo[1], n.lo[2], n.hi[0]);
+        wide[8 * t + 1] = make_float4(n.hi[1], n.hi[2], inf, inf);
+        wide[8 * t + 2] = make_float4(inf, -inf, -inf, -inf);
+        wide[8 * t + 3] = make_float4(inf, inf, inf, -inf);
+        wide[8 * t + 4] = make_float4(-inf, -inf, inf, inf);
+        wide[8 * t + 5] = make_float4(inf, -inf, -inf, -inf);
+        wide[8 * t + 6] = make_float4(rf[0], rf[1], rf[2], rf[3]);
+        wide[8 * t + 7] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
       UP(wide, d.bvhw);
     }
     UP(prims, d.bvh_prims);

@@ -119,7 +119,7 @@ struct Dev {
   const int* bvh_prims;  // prim lists
   const float4* bvh_pbox;  // [2 n_prims] per-prim box in leaf order: (lo, prim id bits), (hi, 0)
   int root_tri, root_edge, root_vert;  // binary-tree roots (host build; kernels start at the wide virtual roots)
-  const float4* bvhw;    // [4 n_wide] child-box nodes; wide nodes 0, 1, 2 = virtual roots (tri, edge, vert)
+  const float4* bvhw;    // [8 n_wide] 4-wide child-box nodes; wide nodes 0, 1, 2 = virtual roots (tri, edge, vert)
   const int4* mk_idx;    // [nm]
   const float4* mk_w;    // [nm]
   // per-env vectors [c][nv][Es]
