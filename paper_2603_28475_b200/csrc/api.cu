@@ -912,19 +912,38 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
       // prim << 3 | count)); empty slots never hit.  Wide nodes 0, 1, 2 are virtual roots (tri,
       // edge, vert) whose child 0 is the tree root.  Half the depth of the binary tree: a query
       // pays half the dependent node loads.
-      std::vector<float4> wide(8 * 3);
+      std::vector<float4> wide(kBvhF4 * 3);
+      auto put_wide = [&](int w, const float (*lo)[3], const float (*hi)[3], const int* ref) {
+        for (int j = 0; j < kBvhW; j += 2) {  // children j, j+1: 12 floats in 3 float4
+          wide[kBvhF4 * w + 3 * (j / 2)] = make_float4(lo[j][0], lo[j][1], lo[j][2], hi[j][0]);
+          wide[kBvhF4 * w + 3 * (j / 2) + 1] = make_float4(hi[j][1], hi[j][2], lo[j + 1][0], lo[j + 1][1]);
+          wide[kBvhF4 * w + 3 * (j / 2) + 2] = make_float4(lo[j + 1][2], hi[j + 1][0], hi[j + 1][1], hi[j + 1][2]);
+        }
+        for (int j = 0; j < kBvhW; j += 4) {  // refs, four per float4
+          float rf[4];
+          memcpy(rf, ref + j, sizeof(rf));
+          wide[kBvhF4 * w + 3 * kBvhW / 2 + j / 4] = make_float4(rf[0], rf[1], rf[2], rf[3]);
+        }
+      };
       auto leaf_ref = [&](int k) { return -1 - (((-nodes[k].left - 1) << 3) | nodes[k].right); };
       std::function<int(int)> make_wide = [&](int k) -> int {  // binary internal node k -> wide index
-        std::vector<int> ch;
-        for (int c : {nodes[k].left, nodes[k].right}) {
-          if (nodes[c].left >= 0) { ch.push_back(nodes[c].left); ch.push_back(nodes[c].right); }
-          else ch.push_back(c);
+        // children: expand internal descendants breadth-first while they fit in kBvhW slots
+        std::vector<int> ch = {nodes[k].left, nodes[k].right};
+        for (size_t j = 0; j < ch.size() && (int)ch.size() < kBvhW;) {
+          if (nodes[ch[j]].left >= 0) {
+            const int c = ch[j];
+            ch.erase(ch.begin() + j);
+            ch.push_back(nodes[c].left);
+            ch.push_back(nodes[c].right);
+          } else {
+            ++j;
+          }
         }
-        const int w = (int)wide.size() / 8;
-        wide.resize(wide.size() + 8);
-        float lo[4][3], hi[4][3];
-        int ref[4];
-        for (int j = 0; j < 4; ++j) {
+        const int w = (int)wide.size() / kBvhF4;
+        wide.resize(wide.size() + kBvhF4);
+        float lo[kBvhW][3], hi[kBvhW][3];
+        int ref[kBvhW];
+        for (int j = 0; j < kBvhW; ++j) {
           for (int t = 0; t < 3; ++t) { lo[j][t] = INFINITY; hi[j][t] = -INFINITY; }
           ref[j] = -1;  // empty leaf (never reached: its box never overlaps)
         }
@@ -933,33 +952,21 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
           for (int t = 0; t < 3; ++t) { lo[j][t] = n.lo[t]; hi[j][t] = n.hi[t]; }
           ref[j] = n.left >= 0 ? make_wide(ch[j]) : leaf_ref(ch[j]);
         }
-        float rf[4];
-        memcpy(rf, ref, sizeof(rf));
-        for (int j = 0; j < 4; j += 2) {  // children j, j+1: 12 floats in 3 float4
-          wide[8 * w + 3 * (j / 2)] = make_float4(lo[j][0], lo[j][1], lo[j][2], hi[j][0]);
-          wide[8 * w + 3 * (j / 2) + 1] = make_float4(hi[j][1], hi[j][2], lo[j + 1][0], lo[j + 1][1]);
-          wide[8 * w + 3 * (j / 2) + 2] = make_float4(lo[j + 1][2], hi[j + 1][0], hi[j + 1][1], hi[j + 1][2]);
-        }
-        wide[8 * w + 6] = make_float4(rf[0], rf[1], rf[2], rf[3]);
-        wide[8 * w + 7] = make_float4(0.f, 0.f, 0.f, 0.f);
+        put_wide(w, lo, hi, ref);
         return w;
       };
       const int roots[3] = {d.root_tri, d.root_edge, d.root_vert};
       for (int t = 0; t < 3; ++t) {  // virtual root t: child 0 = the tree's root, the rest empty
         const BNode& n = nodes[roots[t]];
-        const int r = n.left >= 0 ? make_wide(roots[t]) : leaf_ref(roots[t]);
-        const float inf = INFINITY;
-        int ref[4] = {r, -1, -1, -1};
-        float rf[4];
-        memcpy(rf, ref, sizeof(rf));
-        wide[8 * t] = make_float4(n.lo[0], n.lo[1], n.lo[2], n.hi[0]);
-        wide[8 * t + 1] = make_float4(n.hi[1], n.hi[2], inf, inf);
-        wide[8 * t + 2] = make_float4(inf, -inf, -inf, -inf);
-        wide[8 * t + 3] = make_float4(inf, inf, inf, -inf);
-        wide[8 * t + 4] = make_float4(-inf, -inf, inf, inf);
-        wide[8 * t + 5] = make_float4(inf, -inf, -inf, -inf);
-        wide[8 * t + 6] = make_float4(rf[0], rf[1], rf[2], rf[3]);
-        wide[8 * t + 7] = make_float4(0.f, 0.f, 0.f, 0.f);
+        float lo[kBvhW][3], hi[kBvhW][3];
+        int ref[kBvhW];
+        for (int j = 0; j < kBvhW; ++j) {
+          for (int q = 0; q < 3; ++q) { lo[j][q] = INFINITY; hi[j][q] = -INFINITY; }
+          ref[j] = -1;
+        }
+        for (int q = 0; q < 3; ++q) { lo[0][q] = n.lo[q]; hi[0][q] = n.hi[q]; }
+        ref[0] = n.left >= 0 ? make_wide(roots[t]) : leaf_ref(roots[t]);
+        put_wide(t, lo, hi, ref);
       }
       UP(wide, d.bvhw);
     }

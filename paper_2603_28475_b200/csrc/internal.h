@@ -12,6 +12,8 @@
 namespace tac {
 
 constexpr int kNodeLeaf = 4;
+constexpr int kBvhW = 4;  // children per wide BVH node (8 measured slower: 1,430 vs 851 us per step-start broad phase, 120 registers)
+constexpr int kBvhF4 = 3 * kBvhW / 2 + kBvhW / 4;  // float4 per wide node: boxes in pairs, refs four per float4
 constexpr int kDedupSlots = 4096;  // per-env open-addressing table of shared constraints (R33)
 // element tiles (k_elem_*_tiled): Morton-ordered tets grouped into tiles of <= kTileT tets
 // touching <= kTileV vertices; each tile is scheduled into rounds of <= kTileW
@@ -119,7 +121,7 @@ struct Dev {
   const int* bvh_prims;  // prim lists
   const float4* bvh_pbox;  // [2 n_prims] per-prim box in leaf order: (lo, prim id bits), (hi, 0)
   int root_tri, root_edge, root_vert;  // binary-tree roots (host build; kernels start at the wide virtual roots)
-  const float4* bvhw;    // [8 n_wide] 4-wide child-box nodes; wide nodes 0, 1, 2 = virtual roots (tri, edge, vert)
+  const float4* bvhw;    // [kBvhF4 n_wide] kBvhW-wide child-box nodes; wide nodes 0, 1, 2 = virtual roots (tri, edge, vert)
   const int4* mk_idx;    // [nm]
   const float4* mk_w;    // [nm]
   // per-env vectors [c][nv][Es]

@@ -640,24 +640,25 @@ __device__ void bp_query(const Dev& d, int kind, int gid, const double* glo, con
     qlo[a] = (float)(glo[a] - r) - eps;
     qhi[a] = (float)(ghi[a] + r) + eps;
   }
-  // 4-wide BVH (child boxes in the parent): a popped node is loaded once (112 bytes) and its
-  // four children are tested from it, so rejected children and leaves cost no node load
+  // kBvhW-wide BVH (child boxes in the parent): a popped node is loaded once and all its
+  // children are tested from it, so rejected children and leaves cost no node load
   int stack[48];
   int sp = 0;
   stack[sp++] = root;  // virtual root of the tree
   while (sp > 0) {
-    const float4* wn = d.bvhw + 8 * stack[--sp];
-    float4 nd[7];
+    const float4* wn = d.bvhw + kBvhF4 * stack[--sp];
+    float4 nd[kBvhF4];
 #pragma unroll
-    for (int k = 0; k < 7; ++k) nd[k] = __ldg(wn + k);
+    for (int k = 0; k < kBvhF4; ++k) nd[k] = __ldg(wn + k);
 #pragma unroll
-    for (int chd = 0; chd < 4; ++chd) {
+    for (int chd = 0; chd < kBvhW; ++chd) {
       const float4 n0 = nd[3 * (chd >> 1)], n1 = nd[3 * (chd >> 1) + 1], n2 = nd[3 * (chd >> 1) + 2];
       const bool odd = chd & 1;
       const float lx = odd ? n1.z : n0.x, ly = odd ? n1.w : n0.y, lz = odd ? n2.x : n0.z;
       const float hx = odd ? n2.y : n0.w, hy = odd ? n2.z : n1.x, hz = odd ? n2.w : n1.y;
       if (lx > qhi[0] || hx < qlo[0] || ly > qhi[1] || hy < qlo[1] || lz > qhi[2] || hz < qlo[2]) continue;
-      const float rw = chd == 0 ? nd[6].x : (chd == 1 ? nd[6].y : (chd == 2 ? nd[6].z : nd[6].w));
+      const float4 rq = nd[3 * kBvhW / 2 + (chd >> 2)];
+      const float rw = (chd & 3) == 0 ? rq.x : ((chd & 3) == 1 ? rq.y : ((chd & 3) == 2 ? rq.z : rq.w));
       const int rf = __float_as_int(rw);
       if (rf >= 0) { stack[sp++] = rf; continue; }
       const int code = -1 - rf, p0 = code >> 3, np = code & 7;
@@ -806,18 +807,19 @@ __global__ void __launch_bounds__(128) k_intersect_check(Dev d, int* hit) {
   int sp = 0;
   stack[sp++] = 0;  // virtual root of the triangle BVH
   while (sp > 0) {
-    const float4* wn = d.bvhw + 8 * stack[--sp];
-    float4 nd[7];
+    const float4* wn = d.bvhw + kBvhF4 * stack[--sp];
+    float4 nd[kBvhF4];
 #pragma unroll
-    for (int k = 0; k < 7; ++k) nd[k] = __ldg(wn + k);
+    for (int k = 0; k < kBvhF4; ++k) nd[k] = __ldg(wn + k);
 #pragma unroll
-    for (int chd = 0; chd < 4; ++chd) {
+    for (int chd = 0; chd < kBvhW; ++chd) {
       const float4 n0 = nd[3 * (chd >> 1)], n1 = nd[3 * (chd >> 1) + 1], n2 = nd[3 * (chd >> 1) + 2];
       const bool odd = chd & 1;
       const float lx = odd ? n1.z : n0.x, ly = odd ? n1.w : n0.y, lz = odd ? n2.x : n0.z;
       const float hx = odd ? n2.y : n0.w, hy = odd ? n2.z : n1.x, hz = odd ? n2.w : n1.y;
       if (lx > qhi[0] || hx < qlo[0] || ly > qhi[1] || hy < qlo[1] || lz > qhi[2] || hz < qlo[2]) continue;
-      const float rw = chd == 0 ? nd[6].x : (chd == 1 ? nd[6].y : (chd == 2 ? nd[6].z : nd[6].w));
+      const float4 rq = nd[3 * kBvhW / 2 + (chd >> 2)];
+      const float rw = (chd & 3) == 0 ? rq.x : ((chd & 3) == 1 ? rq.y : ((chd & 3) == 2 ? rq.z : rq.w));
       const int rf = __float_as_int(rw);
       if (rf >= 0) { stack[sp++] = rf; continue; }
       const int code = -1 - rf, q0 = code >> 3, nq = code & 7;
