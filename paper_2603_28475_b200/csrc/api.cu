@@ -650,7 +650,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     }
     std::vector<int> order;
     std::vector<char> seen(ncell, 0);
-    const int seg_len = getenv("TAC_ROW_SEG") ? std::max(1, atoi(getenv("TAC_ROW_SEG"))) : 10;
+    const int seg_len = std::min(kRowSegMax, getenv("TAC_ROW_SEG") ? std::max(1, atoi(getenv("TAC_ROW_SEG"))) : 10);
     auto chain = [&](int h) {
       int len = 0;
       for (int c = h; c >= 0 && !seen[c]; c = nxt[c]) { seen[c] = 1; order.push_back(c); ++len; }

@@ -12,6 +12,7 @@
 namespace tac {
 
 constexpr int kNodeLeaf = 4;
+constexpr int kRowSegMax = 16;  // cells per row segment at most (k_elem_grad_rows stages a segment's records per warp)
 constexpr int kBvhW = 4;  // children per wide BVH node (8 measured slower: 1,430 vs 851 us per step-start broad phase, 120 registers)
 constexpr int kBvhF4 = 3 * kBvhW / 2 + kBvhW / 4;  // float4 per wide node: boxes in pairs, refs four per float4
 constexpr int kDedupSlots = 4096;  // per-env open-addressing table of shared constraints (R33)

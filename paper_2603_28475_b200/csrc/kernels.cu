@@ -1544,12 +1544,22 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_rows(Dev d, float h2) {
   const unsigned G = (unsigned)(d.Es >> 5), eg = TOL ? (unsigned)e >> 5 : (unsigned)blockIdx.y,
                  lane = TOL ? (unsigned)e & 31u : (unsigned)threadIdx.x;  // (compacted: per lane)
   double esum = 0;
+  // the segment's cell records (corner ids, fixed mask, axis-aligned box) staged per warp in
+  // shared memory at the segment start: one load round trip per segment instead of one per cell
+  // (the corner-row address arithmetic waited on each cell's record)
+  __shared__ int4 smv[8][2 * kRowSegMax];
+  __shared__ float4 sma[8][kRowSegMax];
+  __shared__ unsigned smf[8][kRowSegMax];
+  const int ty = threadIdx.y, tl = threadIdx.x;
   for (int sg = bx * 8 + threadIdx.y; sg < d.nseg; sg += nbx * 8) {
-    if (!act) continue;
     const int2 seg = __ldg(d.cell_seg + sg);
+    if (tl < 2 * seg.y) smv[ty][tl] = __ldg(d.cell_v + 2 * seg.x + tl);
+    if (tl < seg.y) { smf[ty][tl] = __ldg(d.cell_fix + seg.x + tl); sma[ty][tl] = __ldg(d.cell_aa + seg.x + tl); }
+    __syncwarp();
+    if (act) {
     float u[8][3], ag[8][3], aD[8][6];
     {  // the first cell's -x face into the slots of the +x face (shifted in below)
-      const int4 va = __ldg(d.cell_v + 2 * seg.x), vb4 = __ldg(d.cell_v + 2 * seg.x + 1);
+      const int4 va = smv[ty][0], vb4 = smv[ty][1];
       const unsigned f[4] = {(unsigned)va.x, (unsigned)va.z, (unsigned)vb4.x, (unsigned)vb4.z};
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -1560,10 +1570,10 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_rows(Dev d, float h2) {
         for (int c = 0; c < 6; ++c) aD[2 * k + 1][c] = 0.f;
       }
     }
-    for (int cidx = seg.x; cidx < seg.x + seg.y; ++cidx) {
-      const int4 va = __ldg(d.cell_v + 2 * cidx), vb4 = __ldg(d.cell_v + 2 * cidx + 1);
-      const unsigned fix = __ldg(d.cell_fix + cidx);
-      const float4 caa = __ldg(d.cell_aa + cidx);
+    for (int ci = 0; ci < seg.y; ++ci) {
+      const int4 va = smv[ty][2 * ci], vb4 = smv[ty][2 * ci + 1];
+      const unsigned fix = smf[ty][ci];
+      const float4 caa = sma[ty][ci];
       const float inv[3] = {caa.x, caa.y, caa.z};
       const unsigned vb[8] = {(unsigned)va.x * G + eg, (unsigned)va.y * G + eg, (unsigned)va.z * G + eg,
                               (unsigned)va.w * G + eg, (unsigned)vb4.x * G + eg, (unsigned)vb4.y * G + eg,
@@ -1598,13 +1608,15 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_rows(Dev d, float h2) {
       flush(6);
       pair_grad_acc<0>(u, inv, invc, mu, l2, w, esum, ag, aD);  // corners 0 1 3 5 7
       flush(0);
-      if (cidx == seg.x + seg.y - 1) {
+      if (ci == seg.y - 1) {
         flush(1);
         flush(3);
         flush(5);
         flush(7);
       }
     }
+    }  // act
+    __syncwarp();  // the records are read before the next segment's staging overwrites them
   }
   if (act) atomicAdd(d.acc + (size_t)A_EEL * d.Es + e, esum);
 }
