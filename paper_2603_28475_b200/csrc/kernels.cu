@@ -1637,9 +1637,21 @@ __global__ void __launch_bounds__(256, 2) k_elem_curv_cells(Dev d, float h2) {
   const unsigned G = (unsigned)(d.Es >> 5), eg = TOL ? (unsigned)e >> 5 : (unsigned)blockIdx.y,
                  lane = TOL ? (unsigned)e & 31u : (unsigned)threadIdx.x;  // (compacted: per lane)
   double qsum = 0;
-  for (int cidx = bx * 8 + threadIdx.y; cidx < d.ncells; cidx += nbx * 8) {
-    const int4 va = __ldg(d.cell_v + 2 * cidx), vb4 = __ldg(d.cell_v + 2 * cidx + 1);
-    const float4 caa = __ldg(d.cell_aa + cidx);
+  // the next cell's record is loaded ahead (the corner-row addresses wait on it)
+  const int cstep = nbx * 8;
+  int4 nva = make_int4(0, 0, 0, 0), nvb = make_int4(0, 0, 0, 0);
+  float4 ncaa = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (bx * 8 + (int)threadIdx.y < d.ncells) {
+    const int c0 = bx * 8 + threadIdx.y;
+    nva = __ldg(d.cell_v + 2 * c0); nvb = __ldg(d.cell_v + 2 * c0 + 1); ncaa = __ldg(d.cell_aa + c0);
+  }
+  for (int cidx = bx * 8 + threadIdx.y; cidx < d.ncells; cidx += cstep) {
+    const int4 va = nva, vb4 = nvb;
+    const float4 caa = ncaa;
+    if (cidx + cstep < d.ncells) {
+      nva = __ldg(d.cell_v + 2 * (cidx + cstep)); nvb = __ldg(d.cell_v + 2 * (cidx + cstep) + 1);
+      ncaa = __ldg(d.cell_aa + cidx + cstep);
+    }
     const bool aa = ALL_AA || caa.w > 0.f;  // warp-uniform (one cell per warp)
     const float inv[3] = {caa.x, caa.y, caa.z};
     if (!act) continue;
