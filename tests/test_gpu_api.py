@@ -391,7 +391,7 @@ def test_tolerance_tail_block_remap_matches_identity(torch):
         tgt[e] = poses[k][e]
     rho = float(np.linalg.norm(s.Y, axis=1).max())
     energies = {}
-    for remap in ("128", "0"):
+    for remap in ("512", "0"):
         os.environ["TAC_REMAP_BLOCKS"] = remap
         try:
             sim = _sim(s, params=pt)
@@ -415,5 +415,5 @@ def test_tolerance_tail_block_remap_matches_identity(torch):
             energies[(remap, e)] = ev["E"]
         sim.close()
     for e in acts:
-        ea, eb = energies[("128", e)], energies[("0", e)]
+        ea, eb = energies[("512", e)], energies[("0", e)]
         assert abs(ea - eb) <= 0.05 * abs(eb), (e, ea, eb)

@@ -2,7 +2,7 @@
 
 The setup of tests/test_gpu_api.py::test_tolerance_tail_block_remap_matches_identity: a
 1,024-env C3 simulator with a few envs in contact (the rest at rest) solved in tolerance mode,
-twice with the remapped tail (TAC_REMAP_BLOCKS=128) and twice with the identity mapping
+twice with the remapped tail (TAC_REMAP_BLOCKS=512) and twice with the identity mapping
 (TAC_REMAP_BLOCKS=0).  Prints per env the iterations of each run, the pairwise max |du| and the
 oracle's energy and fp64 |P g|_disp at each final state (two different converged states with
 equal standing are two minima; a remap bug would show as a non-converged state).
@@ -50,7 +50,7 @@ def main():
     for e in acts:
         tgt[e] = poses[a.k][e]
     runs = []
-    for remap in ("128", "0", "128", "0"):
+    for remap in ("512", "0", "512", "0"):
         os.environ["TAC_REMAP_BLOCKS"] = remap
         sim = P.TacSim.from_scene(s, params=pt)
         del os.environ["TAC_REMAP_BLOCKS"]
