@@ -813,7 +813,7 @@ tac_status tac_create(const tac_create_info* info, tac_sim** out) {
     delete sim;
     return fail(TAC_EINVAL, "more than 16383 gel-surface or indenter vertices");
   }
-  d.compact = getenv("TAC_NO_COMPACT") ? 0 : 1;
+  d.compact = getenv("TAC_NO_COMPACT") ? 0 : (getenv("TAC_COMPACT_LANES") ? atoi(getenv("TAC_COMPACT_LANES")) : 16);
   d.remap_blocks = getenv("TAC_REMAP_BLOCKS") ? std::max(0, atoi(getenv("TAC_REMAP_BLOCKS"))) : 512;
   d.contact_bps = getenv("TAC_CONTACT_BPS") ? std::max(1, atoi(getenv("TAC_CONTACT_BPS"))) : 8;
   d.contact_smem = contact_smem_bytes(d.nsv, niv);

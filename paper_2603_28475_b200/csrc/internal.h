@@ -202,7 +202,7 @@ struct Dev {
   int* loop_ctr;
   cudaGraphConditionalHandle loop_h;
   int remap_blocks;
-  int compact;                   // tolerance mode: vertex / element passes over compacted env groups when sparse              // tolerance mode: CTAs dealt over the active envs' contact passes when few iterate
+  int compact;                   // tolerance mode: vertex / element passes over compacted env groups once the listed envs fill <= compact lanes per listed group on average (0: never)              // tolerance mode: CTAs dealt over the active envs' contact passes when few iterate
   int nseg, rows;                // rows: the gradient pass marches along the segments (all cells axis-aligned)
   const int* rest_tets;          // [nrest] tets not in any cell
   double t1[3], t2[3], nrm[3];

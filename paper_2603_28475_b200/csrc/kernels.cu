@@ -975,7 +975,7 @@ __device__ __forceinline__ bool group_block(const Dev& d, int cap, int ng_grid, 
 }
 
 // Lane -> env of the vertex / element passes.  As group_block, and in addition: in the tolerance
-// mode, once the listed envs are sparse in their groups (on average <= 8 of 32 lanes), the
+// mode, once the listed envs are sparse in their groups (on average <= d.compact of 32 lanes), the
 // passes run over compacted groups -- lane l of compacted group j is env alist[32 j + l] (lanes
 // past the list get e = E: inactive) -- so a warp serves 32 envs that still iterate instead of a
 // few: the element passes are instruction-bound, and the scattered per-lane rows cost L2
@@ -993,7 +993,7 @@ __device__ __forceinline__ bool env_lanes(const Dev& d, int cap, int ng_grid, in
   const int G = d.Es >> 5;
   if (G >= 2 && d.compact) {
     const int n = d.anum[0], n_g = d.anum[1];
-    if (n > 0 && n * 4 <= n_g * 32) {
+    if (n > 0 && n <= n_g * d.compact) {  // on average <= d.compact listed lanes per listed group
       const int Gc = (n + 31) >> 5;
       const int per = max(nc, min(cap, (G * nc) / Gc));
       const int lin = ng_grid * nc + c, idx = lin / per;
