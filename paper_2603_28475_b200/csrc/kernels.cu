@@ -1533,11 +1533,12 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_cells(Dev d, float h2) {
 // to the next: per cell 12 corner row loads and 36 red.adds instead of 24 and 72.  Pair order
 // 1, 2, 0 finishes the carried-in corners early (2 after pair 1; 4, 6 after pair 2; 0 after
 // pair 0), so at most 6 corners' accumulators are live, as in the one-cell pass.
+constexpr int kRowWarps = 6;  // warps per CTA of the row-marching gradient
 template <bool TOL>
-__global__ void __launch_bounds__(256, 2) k_elem_grad_rows(Dev d, float h2) {
+__global__ void __launch_bounds__(32 * kRowWarps, 2) k_elem_grad_rows(Dev d, float h2) {
   TAC_PDL_WAIT();
   int e, bx, nbx;
-  if (!env_lanes<TOL>(d, (d.nseg + 7) / 8, blockIdx.y, blockIdx.x, gridDim.x, e, bx, nbx)) return;
+  if (!env_lanes<TOL>(d, (d.nseg + kRowWarps - 1) / kRowWarps, blockIdx.y, blockIdx.x, gridDim.x, e, bx, nbx)) return;
   const bool act = e < d.E && (d.run[e] & 1);
   if (!__any_sync(0xffffffffu, act)) return;
   const float mu = d.emat[e], l2 = d.emat[d.Es + e];  // per-env material
@@ -1547,11 +1548,11 @@ __global__ void __launch_bounds__(256, 2) k_elem_grad_rows(Dev d, float h2) {
   // the segment's cell records (corner ids, fixed mask, axis-aligned box) staged per warp in
   // shared memory at the segment start: one load round trip per segment instead of one per cell
   // (the corner-row address arithmetic waited on each cell's record)
-  __shared__ int4 smv[8][2 * kRowSegMax];
-  __shared__ float4 sma[8][kRowSegMax];
-  __shared__ unsigned smf[8][kRowSegMax];
+  __shared__ int4 smv[kRowWarps][2 * kRowSegMax];
+  __shared__ float4 sma[kRowWarps][kRowSegMax];
+  __shared__ unsigned smf[kRowWarps][kRowSegMax];
   const int ty = threadIdx.y, tl = threadIdx.x;
-  for (int sg = bx * 8 + threadIdx.y; sg < d.nseg; sg += nbx * 8) {
+  for (int sg = bx * kRowWarps + threadIdx.y; sg < d.nseg; sg += nbx * kRowWarps) {
     const int2 seg = __ldg(d.cell_seg + sg);
     if (tl < 2 * seg.y) smv[ty][tl] = __ldg(d.cell_v + 2 * seg.x + tl);
     if (tl < seg.y) { smf[ty][tl] = __ldg(d.cell_fix + seg.x + tl); sma[ty][tl] = __ldg(d.cell_aa + seg.x + tl); }
@@ -3539,9 +3540,9 @@ void launch_eval(const Dev& d, double h, cudaStream_t s) {
   if (d.ncells > 0) {
     dim3 g = cellgrid(d);
     if (d.rows) {
-      const int gy = (d.nseg + 7) / 8;  // one segment per warp
-      if (d.fixed_iters > 0) LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad_rows<false>, dim3(gy, g.x), dim3(32, 8), 0, d, (float)(h * h));
-      else LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad_rows<true>, dim3(gy, g.x), dim3(32, 8), 0, d, (float)(h * h));
+      const int gy = (d.nseg + kRowWarps - 1) / kRowWarps;  // one segment per warp
+      if (d.fixed_iters > 0) LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad_rows<false>, dim3(gy, g.x), dim3(32, kRowWarps), 0, d, (float)(h * h));
+      else LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad_rows<true>, dim3(gy, g.x), dim3(32, kRowWarps), 0, d, (float)(h * h));
     } else if (d.cells_all_aa) LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad_cells<true>, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
     else LAUNCHP(KID_ELEM_GRAD, s, k_elem_grad_cells<false>, dim3(g.y, g.x), dim3(32, 8), 0, d, (float)(h * h));
   }
