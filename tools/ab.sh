@@ -2,7 +2,6 @@
 # paper_2603_28475_b200/libtac_{a,b,c}.so selected with TAC_LIB, extra environment per variant.
 run() { tag=$1; shift; env "$@" timeout 300 python bench.py --no-cpu-baseline > gpurun_out/ab_$tag.json 2>gpurun_out/ab_$tag.err; }
 for r in 1 2; do
-  run w4_$r TAC_LIB=paper_2603_28475_b200/libtac_a.so
-  run w6_$r TAC_LIB=paper_2603_28475_b200/libtac_b.so
-  run w5_$r TAC_LIB=paper_2603_28475_b200/libtac_c.so
+  run base$r
+  run body$r TAC_CLS_BODY=1
 done
